@@ -1,0 +1,502 @@
+/*
+ * hdp_oracle.c -- CPU restatement of the reference HDP stereo hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library,
+ * and only as the checker (or the timed CPU baseline).  The product path
+ * (paper_1509_08197_b200/) never links or calls it.
+ *
+ * Every routine restates, in plain float64 C, the arithmetic of the reference
+ * Python package `treestereo` (cited file:line below, paths relative to
+ * /root/reference/pkg/src/treestereo/).  Evaluation orders follow numpy's:
+ *   - 3-channel means are sequential ((a0+a1)+a2)/3      (cost_volume.py:84,98)
+ *   - the 7x7 window mean is numpy's 8-accumulator pairwise sum then /49
+ *     (hdp_model.py:394)
+ *   - gray = fma(B,.114, fma(R,.299, G*.587)), the OpenBLAS dgemv order the
+ *     reference's `unit @ GRAY_WEIGHTS` (cost_volume.py:65) produces on this
+ *     host (checked against golden vectors in tests/test_oracle_golden.py)
+ *   - no other contraction: compile with -ffp-contract=off.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+static double np_pairwise(const double *a, int64_t n);
+double or_np_sum(const double *a, int64_t n);
+
+/* numpy add.reduce / reduceat order over a strided run of n values. */
+static double np_sum_strided(const double *a, int64_t n, int64_t stride) {
+    double buf[4096];
+    double *b = n <= 4096 ? buf : (double *)malloc(sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; i++) b[i] = a[i * stride];
+    double r = or_np_sum(b, n);
+    if (b != buf) free(b);
+    return r;
+}
+
+/* ------------------------------------------------------------------ pyramid */
+
+/* pyramid.py:62-75  block_mean: reduceat over rows, then over columns. */
+void or_block_mean(int h, int w, int c, int s, const double *src, double *dst) {
+    int oh = (h + s - 1) / s, ow = (w + s - 1) / s;
+    double *rows = (double *)malloc(sizeof(double) * (size_t)oh * w * c);
+    for (int i = 0; i < oh; i++)
+        for (int x = 0; x < w; x++)
+            for (int k = 0; k < c; k++) {
+                int r0 = i * s, r1 = r0 + s < h ? r0 + s : h;
+                rows[((size_t)i * w + x) * c + k] =
+                    np_sum_strided(src + ((size_t)r0 * w + x) * c + k, r1 - r0, (int64_t)w * c);
+            }
+    for (int i = 0; i < oh; i++) {
+        int rc = (i * s + s < h ? s : h - i * s);
+        for (int j = 0; j < ow; j++) {
+            int c0 = j * s, c1 = c0 + s < w ? c0 + s : w;
+            double cnt = (double)((int64_t)rc * (c1 - c0));
+            for (int k = 0; k < c; k++) {
+                double acc = np_sum_strided(rows + ((size_t)i * w + c0) * c + k, c1 - c0, c);
+                dst[((size_t)i * ow + j) * c + k] = acc / cnt;
+            }
+        }
+    }
+    free(rows);
+}
+
+/* ------------------------------------------------------------------ prepare */
+
+/* cost_volume.py:62-69 prepare_layer */
+void or_prepare(int h, int w, int c, const double *I, double *unit, double *gray, double *grad) {
+    size_t n = (size_t)h * w;
+    for (size_t p = 0; p < n * c; p++) unit[p] = I[p] / 255.0;
+    for (size_t p = 0; p < n; p++) {
+        if (c == 3) {
+            const double *u = unit + p * 3;
+            gray[p] = fma(u[2], 0.114, fma(u[0], 0.299, u[1] * 0.587));
+        } else {
+            gray[p] = unit[p * c];
+        }
+    }
+    for (int r = 0; r < h; r++) {
+        const double *g = gray + (size_t)r * w;
+        double *o = grad + (size_t)r * w;
+        if (w == 1) { o[0] = 0.0; continue; }
+        /* numpy.gradient, edge_order=1, unit spacing */
+        o[0] = (g[1] - g[0]) / 1.0;
+        o[w - 1] = (g[w - 1] - g[w - 2]) / 1.0;
+        for (int x = 1; x < w - 1; x++) o[x] = (g[x + 1] - g[x - 1]) / 2.0;
+    }
+}
+
+static inline double color_mean(const double *a, const double *b, int c) {
+    double acc = fabs(a[0] - b[0]);
+    for (int k = 1; k < c; k++) acc += fabs(a[k] - b[k]);
+    return acc / (double)c;
+}
+
+static inline double trunc_cost(double color, double gdiff, double alpha, double tc, double tg) {
+    double v = (1.0 - alpha) * (color < tc ? color : tc);
+    double t = alpha * (gdiff < tg ? gdiff : tg);
+    return v + t;
+}
+
+/* cost_volume.py:91-102 cost_grid (one disparity x over the whole grid) */
+void or_cost_grid(int h, int w, int c, const double *lu, const double *lg, const double *ru,
+                  const double *rg, int x, double alpha, double tc, double tg, double *out) {
+    double border = (1.0 - alpha) * tc + alpha * tg; /* cost_volume.py:48-50 */
+    for (int r = 0; r < h; r++)
+        for (int col = 0; col < w; col++) {
+            size_t p = (size_t)r * w + col;
+            if (col - x < 0) { out[p] = border; continue; }
+            size_t q = (size_t)r * w + (col - x);
+            double color = color_mean(lu + p * c, ru + q * c, c);
+            out[p] = trunc_cost(color, fabs(lg[p] - rg[q]), alpha, tc, tg);
+        }
+}
+
+/* ------------------------------------------------------------------- edges */
+
+/* spanning_forest.py:61-93 build_edge_list: row-major scan, right before down. */
+int64_t or_edge_list(int h, int w, int c, const double *I, int64_t *u, int64_t *v, double *wt) {
+    int64_t e = 0;
+    for (int r = 0; r < h; r++)
+        for (int col = 0; col < w; col++) {
+            int64_t p = (int64_t)r * w + col;
+            if (col + 1 < w) {
+                double m = 0.0;
+                for (int k = 0; k < c; k++) {
+                    double d = fabs(I[p * c + k] - I[(p + 1) * c + k]);
+                    if (d > m) m = d;
+                }
+                u[e] = p; v[e] = p + 1; wt[e] = m; e++;
+            }
+            if (r + 1 < h) {
+                double m = 0.0;
+                for (int k = 0; k < c; k++) {
+                    double d = fabs(I[p * c + k] - I[(p + w) * c + k]);
+                    if (d > m) m = d;
+                }
+                u[e] = p; v[e] = p + w; wt[e] = m; e++;
+            }
+        }
+    return e;
+}
+
+/* spanning_forest.py:96-107 mst_edge_order: stable argsort by weight.  A
+ * bottom-up merge sort on (weight, index) is stable by construction. */
+void or_mst_order(int64_t n_edges, const double *wt, int64_t *order) {
+    int64_t *tmp = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_edges > 0 ? n_edges : 1));
+    for (int64_t i = 0; i < n_edges; i++) order[i] = i;
+    for (int64_t width = 1; width < n_edges; width *= 2) {
+        for (int64_t lo = 0; lo < n_edges; lo += 2 * width) {
+            int64_t mid = lo + width < n_edges ? lo + width : n_edges;
+            int64_t hi = lo + 2 * width < n_edges ? lo + 2 * width : n_edges;
+            int64_t i = lo, j = mid, k = lo;
+            while (i < mid && j < hi) {
+                if (wt[order[j]] < wt[order[i]]) tmp[k++] = order[j++];
+                else tmp[k++] = order[i++];
+            }
+            while (i < mid) tmp[k++] = order[i++];
+            while (j < hi) tmp[k++] = order[j++];
+        }
+        memcpy(order, tmp, sizeof(int64_t) * (size_t)n_edges);
+    }
+    free(tmp);
+}
+
+/* ------------------------------------------------------------- union-find */
+
+/* spanning_forest.py:123-143: path halving, union by size. */
+static int64_t uf_find(int64_t *par, int64_t x) {
+    while (par[x] != x) {
+        par[x] = par[par[x]];
+        x = par[x];
+    }
+    return x;
+}
+
+static int popcount_words(const uint64_t *a, int nw) {
+    int c = 0;
+    for (int i = 0; i < nw; i++) c += __builtin_popcountll(a[i]);
+    return c;
+}
+
+/* hdp_forest.py:151-216 build_hdpf (and spanning_forest.py:286-322
+ * build_forest when every mask is full and beta == 0).  Masks are bitsets of
+ * nw 64-bit words per pixel.  Returns the number of accepted edges; writes the
+ * accepted edges in acceptance order and, per pixel, its final union-find root
+ * and that root's tree mask. */
+int64_t or_hdpf(int64_t n, int64_t n_edges, const int64_t *u, const int64_t *v, const double *wt,
+                const int64_t *order, int nw, const uint64_t *pix_mask, double beta,
+                int64_t *acc_u, int64_t *acc_v, double *acc_w, int64_t *root_out,
+                uint64_t *root_mask_out) {
+    int64_t *par = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *sz = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    uint64_t *tm = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n * nw);
+    memcpy(tm, pix_mask, sizeof(uint64_t) * (size_t)n * nw);
+    for (int64_t i = 0; i < n; i++) { par[i] = i; sz[i] = 1; }
+    int64_t nacc = 0;
+    for (int64_t k = 0; k < n_edges; k++) {
+        int64_t e = order[k];
+        int64_t a = u[e], b = v[e];
+        /* rule 1: hdp_forest.py:187-188 */
+        int meet = 0;
+        for (int i = 0; i < nw; i++)
+            if (pix_mask[a * nw + i] & pix_mask[b * nw + i]) { meet = 1; break; }
+        if (!meet) continue;
+        int64_t ra = uf_find(par, a), rb = uf_find(par, b);
+        if (ra == rb) continue;
+        /* rule 2: hdp_forest.py:192-196, IEEE double division */
+        int inter = 0, uni = 0;
+        for (int i = 0; i < nw; i++) {
+            inter += __builtin_popcountll(tm[ra * nw + i] & tm[rb * nw + i]);
+            uni += __builtin_popcountll(tm[ra * nw + i] | tm[rb * nw + i]);
+        }
+        if ((double)inter / (double)uni < beta) continue;
+        /* UnionFind.union: larger size survives (ties keep `ra`) */
+        int64_t keep = ra, gone = rb;
+        if (sz[ra] < sz[rb]) { keep = rb; gone = ra; }
+        par[gone] = keep;
+        sz[keep] += sz[gone];
+        for (int i = 0; i < nw; i++) tm[keep * nw + i] |= tm[gone * nw + i];
+        acc_u[nacc] = a; acc_v[nacc] = b; acc_w[nacc] = wt[e]; nacc++;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        int64_t r = uf_find(par, i);
+        root_out[i] = r;
+        memcpy(root_mask_out + i * nw, tm + r * nw, sizeof(uint64_t) * nw);
+    }
+    free(par); free(sz); free(tm);
+    (void)popcount_words;
+    return nacc;
+}
+
+/* ------------------------------------------------------------------- BFS */
+
+/* spanning_forest.py:191-283 _bfs_forest: symmetric adjacency with neighbour
+ * lists ascending (lexsort by (of, to)), roots = lowest unvisited id, trees
+ * numbered in root order.  Returns the tree count; tree_slices has n+1 room. */
+int64_t or_bfs_forest(int64_t n, int64_t m, const int64_t *acc_u, const int64_t *acc_v,
+                      const double *acc_w, int64_t *parent, double *pw, int64_t *depth,
+                      int64_t *tree_id, int64_t *order, int64_t *tree_slices) {
+    int64_t *deg = (int64_t *)calloc((size_t)n + 1, sizeof(int64_t));
+    for (int64_t i = 0; i < m; i++) { deg[acc_u[i] + 1]++; deg[acc_v[i] + 1]++; }
+    for (int64_t i = 0; i < n; i++) deg[i + 1] += deg[i];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; i++) fill[i] = deg[i];
+    int64_t *nb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(2 * m + 1));
+    double *nw = (double *)malloc(sizeof(double) * (size_t)(2 * m + 1));
+    for (int64_t i = 0; i < m; i++) {
+        nb[fill[acc_u[i]]] = acc_v[i]; nw[fill[acc_u[i]]++] = acc_w[i];
+        nb[fill[acc_v[i]]] = acc_u[i]; nw[fill[acc_v[i]]++] = acc_w[i];
+    }
+    /* ascending neighbour id per node (insertion sort: degree <= a handful on
+     * grids, arbitrary for general forests -> fall back to a simple sort) */
+    for (int64_t x = 0; x < n; x++) {
+        for (int64_t i = deg[x] + 1; i < deg[x + 1]; i++) {
+            int64_t kb = nb[i]; double kw = nw[i]; int64_t j = i - 1;
+            while (j >= deg[x] && nb[j] > kb) { nb[j + 1] = nb[j]; nw[j + 1] = nw[j]; j--; }
+            nb[j + 1] = kb; nw[j + 1] = kw;
+        }
+    }
+    for (int64_t i = 0; i < n; i++) { parent[i] = i; pw[i] = 0.0; depth[i] = 0; tree_id[i] = -1; }
+    int64_t filled = 0, cur = 0;
+    tree_slices[0] = 0;
+    for (int64_t start = 0; start < n; start++) {
+        if (tree_id[start] >= 0) continue;
+        tree_id[start] = cur;
+        int64_t head = filled;
+        order[filled++] = start;
+        while (head < filled) {
+            int64_t node = order[head++];
+            int64_t d = depth[node] + 1;
+            for (int64_t k = deg[node]; k < deg[node + 1]; k++) {
+                int64_t nx = nb[k];
+                if (tree_id[nx] >= 0) continue;
+                tree_id[nx] = cur; parent[nx] = node; pw[nx] = nw[k]; depth[nx] = d;
+                order[filled++] = nx;
+            }
+        }
+        cur++;
+        tree_slices[cur] = filled;
+    }
+    free(deg); free(fill); free(nb); free(nw);
+    return cur;
+}
+
+/* ------------------------------------------------------------- aggregation */
+
+/* aggregation.py:158-179 _two_pass, applied tree by tree (aggregation.py:
+ * 216-236).  `costs` and `out` are (n, m) row-major by pixel id; `order` is
+ * the BFS order; `pos` its inverse; `sim` per node.  Sibling sums follow
+ * np.add.reduceat (sequential), then up[parent] += sum. */
+void or_aggregate_forest(int64_t n, int64_t m, const int64_t *parent, const int64_t *order,
+                         const int64_t *depth, const int64_t *tree_slices, int64_t n_trees,
+                         const double *sim, const double *costs, double *out) {
+    double *up = (double *)malloc(sizeof(double) * (size_t)n * m);
+    double *sum = (double *)malloc(sizeof(double) * (size_t)(n > m ? n : m));
+    memcpy(up, costs, sizeof(double) * (size_t)n * m);
+    for (int64_t t = 0; t < n_trees; t++) {
+        int64_t s = tree_slices[t], e = tree_slices[t + 1];
+        if (e - s == 1) { memcpy(out + order[s] * m, costs + order[s] * m, sizeof(double) * m); continue; }
+        /* level bounds: BFS depth is nondecreasing along order[s:e] */
+        int64_t top = depth[order[e - 1]];
+        int64_t *lb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(top + 2));
+        int64_t k = s;
+        for (int64_t lev = 0; lev <= top + 1; lev++) {
+            while (k < e && depth[order[k]] < lev) k++;
+            lb[lev] = k;
+        }
+        for (int64_t lev = top; lev >= 1; lev--) {
+            int64_t i = lb[lev];
+            while (i < lb[lev + 1]) {
+                int64_t p = parent[order[i]];
+                int64_t j = i + 1;
+                while (j < lb[lev + 1] && parent[order[j]] == p) j++;
+                /* vals = sim * up, then np.add.reduceat over the sibling run */
+                for (int64_t c = 0; c < m; c++) {
+                    for (int64_t q = i; q < j; q++) sum[q - i] = sim[order[q]] * up[order[q] * m + c];
+                    up[p * m + c] += or_np_sum(sum, j - i);
+                }
+                i = j;
+            }
+        }
+        memcpy(out + order[s] * m, up + order[s] * m, sizeof(double) * m);
+        for (int64_t i = lb[1]; i < e; i++) {
+            int64_t v = order[i], p = parent[v];
+            double sl = sim[v];
+            double a = 1.0 - sl * sl;
+            for (int64_t c = 0; c < m; c++) {
+                double t1 = sl * out[p * m + c];
+                double t2 = a * up[v * m + c];
+                out[v * m + c] = t1 + t2;
+            }
+        }
+        free(lb);
+    }
+    free(up); free(sum);
+}
+
+/* --------------------------------------------------------------- the prior */
+
+/* numpy's pairwise summation (add.reduce over a contiguous axis): the first
+ * element seeds the accumulator, the rest go through pairwise_sum with eight
+ * accumulators for blocks <= 128 (numpy loops_utils.h).  hdp_model.py:394. */
+static double np_pairwise(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; i++) r += a[i];
+        return r;
+    } else if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += a[i];
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+    }
+}
+
+double or_np_sum(const double *a, int64_t n) {
+    if (n == 0) return 0.0;
+    return a[0] + np_pairwise(a + 1, n - 1);
+}
+
+/* hdp_model.py:377-422 _matched_window_cost + _windowed_wta.  sign=-1 matches
+ * src (col) against dst (col - x); sign=+1 against (col + x). */
+void or_windowed_wta(int h, int w, int c, const double *su, const double *sg, const double *du,
+                     const double *dg, int64_t ncent, const int64_t *cr, const int64_t *cc,
+                     int d_max, int sign, int window, double alpha, double tc, double tg,
+                     int64_t *winner) {
+    double border = (1.0 - alpha) * tc + alpha * tg;
+    int half = window / 2;
+    int nwin = window * window;
+    double *vals = (double *)malloc(sizeof(double) * (size_t)nwin);
+    for (int64_t k = 0; k < ncent; k++) {
+        double best = INFINITY;
+        int64_t win = 0;
+        for (int x = 0; x <= d_max; x++) {
+            int idx = 0;
+            for (int dr = -half; dr <= half; dr++) {
+                int64_t r = cr[k] + dr;
+                if (r < 0) r = 0;
+                if (r > h - 1) r = h - 1;
+                for (int dc = -half; dc <= half; dc++) {
+                    int64_t col = cc[k] + dc;
+                    if (col < 0) col = 0;
+                    if (col > w - 1) col = w - 1;
+                    int64_t dcol = col + (int64_t)sign * x;
+                    int inside = dcol >= 0 && dcol < w;
+                    int64_t safe = dcol < 0 ? 0 : (dcol > w - 1 ? w - 1 : dcol);
+                    size_t p = (size_t)r * w + col, q = (size_t)r * w + safe;
+                    double color = color_mean(su + p * c, du + q * c, c);
+                    double v = trunc_cost(color, fabs(sg[p] - dg[q]), alpha, tc, tg);
+                    vals[idx++] = inside ? v : border;
+                }
+            }
+            double cost = or_np_sum(vals, nwin) / (double)nwin;
+            if (cost < best) { best = cost; win = x; }
+        }
+        winner[k] = win;
+    }
+    free(vals);
+}
+
+/* --------------------------------------------------- one HDP / dense layer */
+
+/* cost_volume.py:72-88 cost_at_pixels for one (pixel, x). */
+static inline double cost_px(int w, int c, const double *lu, const double *lg, const double *ru,
+                             const double *rg, int64_t p, int x, double alpha, double tc,
+                             double tg, double border) {
+    int64_t col = p % w;
+    if (col - x < 0) return border;
+    int64_t q = p - x;
+    double color = color_mean(lu + p * c, ru + q * c, c);
+    return trunc_cost(color, fabs(lg[p] - rg[q]), alpha, tc, tg);
+}
+
+/* masked_cost_volume (cost_volume.py:183-236) + aggregate_tree
+ * (aggregation.py:182-213, _two_pass :158-179) + winner_takes_all_with_cost
+ * (aggregation.py:239-256), tree by tree on each tree's interval.
+ * iv_off/iv_vals: per tree sorted disparity list (CSR).  Outputs per pixel:
+ * disparity (first argmin), best and second-best aggregated cost; optionally
+ * the aggregated entries at agg_out[ent_off[p] + j]. */
+void or_layer_wta(int h, int w, int c, const double *lu, const double *lg, const double *ru,
+                  const double *rg, double alpha, double tc, double tg, int64_t n_trees,
+                  const int64_t *tree_slices, const int64_t *order, const int64_t *pos,
+                  const int64_t *parent, const int64_t *depth, const double *sim, const int64_t *iv_off,
+                  const int64_t *iv_vals, int32_t *disp, double *best, double *second,
+                  const int64_t *ent_off, double *agg_out) {
+    double border = (1.0 - alpha) * tc + alpha * tg;
+    (void)h;
+    for (int64_t t = 0; t < n_trees; t++) {
+        int64_t s = tree_slices[t], e = tree_slices[t + 1], n_t = e - s;
+        int64_t m = iv_off[t + 1] - iv_off[t];
+        const int64_t *xs = iv_vals + iv_off[t];
+        double *up = (double *)malloc(sizeof(double) * (size_t)(n_t * m));
+        double *dn = (double *)malloc(sizeof(double) * (size_t)(n_t * m));
+        double *sum = (double *)malloc(sizeof(double) * (size_t)(n_t > m ? n_t : m));
+        for (int64_t i = 0; i < n_t; i++)
+            for (int64_t j = 0; j < m; j++)
+                up[i * m + j] = cost_px(w, c, lu, lg, ru, rg, order[s + i], (int)xs[j], alpha, tc, tg, border);
+        if (n_t > 1) {
+            /* local position of every node's parent; BFS => parent earlier */
+            int64_t top = depth[order[e - 1]];
+            int64_t *lb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(top + 2));
+            int64_t k = 0;
+            for (int64_t lev = 0; lev <= top + 1; lev++) {
+                while (k < n_t && depth[order[s + k]] < lev) k++;
+                lb[lev] = k;
+            }
+            int64_t *pl = (int64_t *)malloc(sizeof(int64_t) * (size_t)n_t);
+            for (int64_t i = 0; i < n_t; i++) pl[i] = pos[parent[order[s + i]]] - s;
+            for (int64_t lev = top; lev >= 1; lev--) {
+                int64_t i = lb[lev];
+                while (i < lb[lev + 1]) {
+                    int64_t p = pl[i];
+                    int64_t jn = i + 1;
+                    while (jn < lb[lev + 1] && pl[jn] == p) jn++;
+                    for (int64_t j = 0; j < m; j++) {
+                        for (int64_t q = i; q < jn; q++) sum[q - i] = sim[order[s + q]] * up[q * m + j];
+                        up[p * m + j] += or_np_sum(sum, jn - i);
+                    }
+                    i = jn;
+                }
+            }
+            for (int64_t j = 0; j < m; j++) dn[j] = up[j];
+            for (int64_t i = lb[1]; i < n_t; i++) {
+                double sl = sim[order[s + i]];
+                double a = 1.0 - sl * sl;
+                for (int64_t j = 0; j < m; j++) {
+                    double t1 = sl * dn[pl[i] * m + j];
+                    double t2 = a * up[i * m + j];
+                    dn[i * m + j] = t1 + t2;
+                }
+            }
+            free(lb); free(pl);
+        } else {
+            for (int64_t j = 0; j < m; j++) dn[j] = up[j];
+        }
+        for (int64_t i = 0; i < n_t; i++) {
+            int64_t p = order[s + i];
+            double b1 = dn[i * m], b2 = INFINITY;
+            int64_t bj = 0;
+            for (int64_t j = 1; j < m; j++) {
+                double vj = dn[i * m + j];
+                if (vj < b1) { b2 = b1; b1 = vj; bj = j; }
+                else if (vj < b2) b2 = vj;
+            }
+            disp[p] = (int32_t)xs[bj];
+            best[p] = b1;
+            second[p] = b2;
+            if (agg_out)
+                for (int64_t j = 0; j < m; j++) agg_out[ent_off[p] + j] = dn[i * m + j];
+        }
+        free(up); free(dn); free(sum);
+    }
+}
