@@ -1,0 +1,186 @@
+/*
+ * hdp_stereo.h -- C ABI of the B200-native (sm_100a) HDP tree-stereo hot path.
+ *
+ * Plain pointers and sizes only.  Every device pointer is caller-owned CUDA
+ * device memory; every entry point is stream-ordered on `stream` (a
+ * cudaStream_t passed as void*, NULL = legacy default stream) and reentrant
+ * per stream: scratch comes from the stream-ordered pool, there is no hidden
+ * global mutable state (except the thread-local message behind
+ * hdp_last_error).  Functions return an HDP_* status code, never abort.
+ *
+ * The reference (Python package `treestereo`, /root/reference/pkg/src/
+ * treestereo/) has no FFI for this path; its public functions ARE the
+ * interface.  Each entry point below names the reference function(s) it
+ * replaces; the Python binding that maps them back onto those signatures is
+ * paper_1509_08197_b200/ (see INTEGRATION.md).
+ *
+ * Layouts: a batch of B stereo pairs of identical geometry H x W x C
+ * (C in {1,3}); node (pixel) ids are global: g = b*H*W + r*W + c.  Grid edge
+ * ids are per pair, in the reference's scan order (right edge before down
+ * edge, spanning_forest.py:61-93).
+ */
+#ifndef HDP_STEREO_H
+#define HDP_STEREO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* Status codes: same numbering as the reference exit codes (errors.py:8-29). */
+#define HDP_OK 0
+#define HDP_ERR_CONFIG 2   /* -> ConfigError   */
+#define HDP_ERR_DATA 3     /* -> DataError     */
+#define HDP_ERR_INTERNAL 4 /* -> InternalError */
+#define HDP_ERR_CUDA 5     /* CUDA runtime failure (-> InternalError)       */
+
+#define HDP_ABI_VERSION 1
+
+int hdp_abi_version(void);
+/* Message for the last non-OK status on the calling thread. */
+const char *hdp_last_error(void);
+
+/* ---------------------------------------------------------- images, pyramid */
+
+/* uint8 -> float64 copy (RasterImage.data.astype(float64), aggregation.py:269). */
+int hdp_u8_to_f64(const uint8_t *src, double *dst, int64_t n, void *stream);
+
+/* S x S block mean over covered pixels, per pair (pyramid.py:62-75
+ * block_mean; pyramid.py:78-113 build_pyramid calls it once per level).
+ * src (B,H,W,C) f64 -> dst (B,ceil(H/S),ceil(W/S),C) f64, numpy's reduceat
+ * summation order, so exact for the reference's inputs. */
+int hdp_block_mean(const double *src, double *dst, int batch, int h, int w, int c, int s,
+                   void *stream);
+
+/* prepare_layer (cost_volume.py:62-69): unit = I/255, gray, row gradient.
+ * Outputs (each nullable): unit (B,H,W,C) f64, gray (B,H,W) f64, grad
+ * (B,H,W) f64 (all bit-identical to the reference) and packed (B,H,W,4) f32
+ * = (u0,u1,u2,grad) for the fp32 matching cost. */
+int hdp_prepare(const double *img, int batch, int h, int w, int c, double *unit, double *gray,
+                double *grad, float *packed, void *stream);
+
+/* Stable ascending argsort of 64-bit keys (radix): perm[i] = index of the
+ * i-th smallest key, ties in index order -- numpy argsort(kind="stable") on
+ * the keys (mst_edge_order, spanning_forest.py:96-107, on weight-bit keys). */
+int hdp_argsort_u64(const uint64_t *keys, int64_t n, int32_t *perm, void *stream);
+
+/* cost_grid / cost_at_pixels (cost_volume.py:72-102) for the disparities
+ * xs[0..nx): out (B*H*W, nx) f32, disparity innermost. */
+int hdp_cost_volume(const float *packed_l, const float *packed_r, int batch, int h, int w, int c,
+                    const int32_t *xs, int nx, float alpha, float tau_c, float tau_g, float *out,
+                    void *stream);
+
+/* ------------------------------------------------------------ edges + MST */
+
+/* build_edge_list (spanning_forest.py:61-93) for a batch: per pair
+ * E = 2HW-H-W edges in scan order.  eu/ev global node ids, ew = max channel
+ * |difference| (f32; exact for uint8 inputs and S=2 pyramid levels), key =
+ * (f32 bits of ew) << 32 | per-pair edge index  -- the (weight, index) order
+ * of mst_edge_order's stable sort (spanning_forest.py:96-107). */
+int hdp_grid_edges(const double *img, int batch, int h, int w, int c, int32_t *eu, int32_t *ev,
+                   float *ew, uint64_t *key, void *stream);
+
+/* build_forest(edges, "mst") edge selection (spanning_forest.py:286-322) as
+ * Boruvka on unique 64-bit keys (the MST under a total order is unique, so it
+ * equals stable-sort Kruskal's).  Works on any edge list (not only grids).
+ * Outputs: in_tree[e] in {0,1}; comp[v] = a component representative. */
+int hdp_mst(int64_t n_nodes, int64_t n_edges, const int32_t *eu, const int32_t *ev,
+            const uint64_t *key, uint8_t *in_tree, int32_t *comp, int *rounds_out, void *stream);
+
+/* --------------------------------------------------------------- HDP parts */
+
+/* estimate_prior up to the histogram (hdp_model.py:425-470): sampled
+ * windowed WTA in both directions, float64 bit-exact with the reference,
+ * cross-check |dL - dR| <= max_offset.  counts (B, d_max+1) int64;
+ * kept (B) int64 = number of surviving samples. */
+int hdp_prior_counts(const double *unit_l, const double *grad_l, const double *unit_r,
+                     const double *grad_r, int batch, int h, int w, int c, int d_max,
+                     int stride, int window, int max_offset, double alpha, double tau_c,
+                     double tau_g, int64_t *counts, int64_t *kept, void *stream);
+
+/* assign_pixel_intervals (hdp_forest.py:91-123): pixel_row[g] =
+ * parent_disp[b, r/S, c/S]; DATA error if a parent disparity is outside
+ * [0, n_rows). */
+int hdp_assign_rows(const int32_t *parent_disp, int batch, int ph, int pw, int h, int w, int s,
+                    int n_rows, int32_t *pixel_row, void *stream);
+
+/* build_hdpf (hdp_forest.py:151-216): rule 1 (disjoint pixel sets drop the
+ * edge), then Kruskal order (key) with rule 2 (Jaccard of the LIVE tree sets
+ * >= beta, IEEE double division) decided exactly by deterministic
+ * reservations.  row_masks: (B, n_rows, nw) u32 bitsets; pixel_row per node.
+ * Outputs in_tree[e], comp[v] (representative), tree_masks (n_nodes, nw):
+ * the final tree set, valid at every node. */
+int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, const int32_t *eu,
+             const int32_t *ev, const uint64_t *key, const int32_t *pixel_row,
+             const uint32_t *row_masks, int n_rows, int nw, double beta, uint8_t *in_tree,
+             int32_t *comp, uint32_t *tree_masks, int *rounds_out, void *stream);
+
+/* ------------------------------------------- rooted forest + aggregation */
+
+typedef struct hdp_forest hdp_forest;
+
+/* Root the forest given by the edges with in_tree set (all if NULL):
+ * root = lowest node id per component, trees numbered by root id
+ * (_bfs_forest, spanning_forest.py:191-283), parent / depth / subtree size
+ * by Euler tour + list ranking, similarities exp(-w/(gamma*255))
+ * (spanning_forest.py:184-188), and the heavy-path layout the aggregation
+ * kernels scan.  comp (nullable) = any component labelling of the edges. */
+int hdp_forest_create(int64_t n_nodes, int64_t n_edges, const int32_t *eu, const int32_t *ev,
+                      const float *ew, const uint8_t *in_tree, const int32_t *comp, float gamma,
+                      hdp_forest **out, void *stream);
+
+/* Host-visible sizes (synchronises the creating stream once). */
+int hdp_forest_stats(const hdp_forest *f, int64_t *n_trees, int64_t *n_paths, int64_t *n_phases,
+                     int64_t *max_depth);
+
+/* RootedForest fields (spanning_forest.py:146-188), nullable outputs:
+ * parent (root: itself), depth, tree_id, subtree size, parent_weight (f32),
+ * root id per node. */
+int hdp_forest_export(const hdp_forest *f, int32_t *parent, int32_t *depth, int32_t *tree_id,
+                      int32_t *size, float *parent_weight, int32_t *root, void *stream);
+
+/* Per-tree disparity lanes.  set_lanes: tree_masks (n_trees, nw) u32
+ * bitsets (DisparityForest.intervals, hdp_forest.py:126-148); set_lanes_range:
+ * every tree gets x0 .. x0+nx-1 (dense baseline / a disparity slab). */
+int hdp_forest_set_lanes(hdp_forest *f, const uint32_t *tree_masks, int nw, void *stream);
+int hdp_forest_set_lanes_range(hdp_forest *f, int x0, int nx, void *stream);
+
+/* Stored entries sum_p |interval(tree(p))| (hdp_forest.py:144-148) and,
+ * optionally, the per-node offsets of the pixel-major volume layout. */
+int hdp_forest_entries(hdp_forest *f, int64_t *total, int64_t *node_offsets, void *stream);
+
+/* masked_cost_volume + aggregate_tree + winner_takes_all_with_cost
+ * (cost_volume.py:183-236, aggregation.py:158-256, baseline fold
+ * aggregation.py:311-326), fused: the raw cost is computed on the fly from
+ * the packed planes of pair b = node / (h*w) (or read from cost_rows
+ * (n_nodes, m) f32 when non-NULL: aggregate_forest, aggregation.py:216-236),
+ * aggregated leaf->root and root->leaf along heavy paths, and reduced to the
+ * first argmin per node.  Outputs (nullable): disp (int32), min_cost (f32),
+ * keys (u64 = order-preserving f32 encoding << 32 | d: the u64 minimum is
+ * the first argmin, so keys combine across disparity slabs with a min),
+ * volume (f32, pixel-major at node_offsets). */
+int hdp_aggregate_wta(hdp_forest *f, const float *packed_l, const float *packed_r, int h, int w,
+                      int c, float alpha, float tau_c, float tau_g, const float *cost_rows,
+                      int32_t *disp, float *min_cost, uint64_t *keys, float *volume,
+                      void *stream);
+
+void hdp_forest_destroy(hdp_forest *f);
+
+/* keys -> (disp, min_cost) for keys combined across slabs (NCCL min). */
+int hdp_keys_unpack(const uint64_t *keys, int64_t n, int32_t *disp, float *min_cost,
+                    void *stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HDP_STEREO_H */

@@ -1,0 +1,824 @@
+// Rooting a spanning forest and building its heavy-path layout, all on the
+// device in O(log n) parallel rounds.
+//
+// Replaces _bfs_forest (spanning_forest.py:191-283).  The reference roots
+// every tree at its lowest pixel id and walks BFS levels one by one; tree
+// depth on these grids reaches thousands of levels, so a level-synchronous
+// GPU walk would be latency bound.  Instead:
+//   1. components -> root = min id per component, trees numbered by root id
+//      (the reference's numbering);
+//   2. Euler tour over the CSR adjacency, list-ranked by pointer jumping;
+//      a tree edge is a parent link in the direction its tour arc comes
+//      first; subtree size = half the tour span; depth and light depth come
+//      from prefix sums over the tour;
+//   3. heavy child = largest subtree (ties -> lower id), heavy paths by
+//      pointer jumping, layout sorted by (light depth, path head, depth):
+//      every heavy path is contiguous and every phase (light depth) a block.
+// parent / depth / tree_id / subtree sizes are tree properties, identical to
+// the reference's.  Only the node ORDER differs from BFS, which the
+// reference uses as a layout (not a parity artifact).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "forest.cuh"
+#include "prims.cuh"
+
+namespace hdp {
+
+int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, const uint64_t* key,
+                uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st);
+
+__global__ void k_flag_edges(int64_t m, const uint8_t* __restrict__ in_tree, int32_t* flags) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < m) flags[e] = in_tree ? (in_tree[e] ? 1 : 0) : 1;
+}
+
+__global__ void k_compact_edges(int64_t m, const int32_t* __restrict__ flags,
+                                const int32_t* __restrict__ pos, const int32_t* __restrict__ eu,
+                                const int32_t* __restrict__ ev, const float* __restrict__ ew,
+                                int32_t* tu, int32_t* tv, float* tw, uint64_t* tkey) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m || !flags[e]) return;
+    int32_t i = pos[e];
+    tu[i] = eu[e];
+    tv[i] = ev[e];
+    tw[i] = ew ? ew[e] : 0.0f;
+    tkey[i] = (uint64_t)i;
+}
+
+__global__ void k_fill_int(int64_t n, int32_t* a, int32_t v) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = v;
+}
+
+__global__ void k_min_root(int64_t n, const int32_t* __restrict__ comp, int32_t* minid) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) atomicMin(&minid[comp[v]], (int32_t)v);
+}
+
+__global__ void k_root_flags(int64_t n, const int32_t* __restrict__ comp,
+                             const int32_t* __restrict__ minid, int32_t* root, int32_t* is_root) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t r = minid[comp[v]];
+    root[v] = r;
+    is_root[v] = (r == v) ? 1 : 0;
+}
+
+__global__ void k_tree_ids(int64_t n, const int32_t* __restrict__ root,
+                           const int32_t* __restrict__ tindex, int32_t* tree_id) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) tree_id[v] = tindex[root[v]];
+}
+
+__global__ void k_make_arcs(int64_t m, const int32_t* __restrict__ tu, const int32_t* __restrict__ tv,
+                            const float* __restrict__ tw, uint64_t* akey, float* aw,
+                            int32_t* deg) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    int32_t u = tu[e], v = tv[e];
+    akey[2 * e] = ((uint64_t)(uint32_t)u << 32) | (uint32_t)v;
+    akey[2 * e + 1] = ((uint64_t)(uint32_t)v << 32) | (uint32_t)u;
+    aw[2 * e] = tw[e];
+    aw[2 * e + 1] = tw[e];
+    atomicAdd(&deg[u], 1);
+    atomicAdd(&deg[v], 1);
+}
+
+__global__ void k_arc_unpack(int64_t na, const uint64_t* __restrict__ akey, int32_t* asrc,
+                             int32_t* adst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    asrc[i] = (int32_t)(akey[i] >> 32);
+    adst[i] = (int32_t)(akey[i] & 0xffffffffu);
+}
+
+// twin arc (y -> x) of arc i = (x -> y): binary search in y's sorted list.
+__device__ __forceinline__ int32_t find_arc(const int32_t* __restrict__ adj_start,
+                                            const int32_t* __restrict__ adst, int32_t y,
+                                            int32_t x) {
+    int32_t lo = adj_start[y], hi = adj_start[y + 1] - 1;
+    while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (adst[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Euler-tour successor; the arc entering a root just before the tour would
+// wrap around to the root's first arc ends the list (next = -1).
+__global__ void k_tour_next(int64_t na, const int32_t* __restrict__ asrc,
+                            const int32_t* __restrict__ adst, const int32_t* __restrict__ adj_start,
+                            const int32_t* __restrict__ root, int32_t* twin, int32_t* next) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    int32_t x = asrc[i], y = adst[i];
+    int32_t j = find_arc(adj_start, adst, y, x);
+    twin[i] = j;
+    int32_t s = adj_start[y], d = adj_start[y + 1] - s;
+    int32_t nx = s + ((j - s + 1) % d);
+    // wrapping past the last arc of the root back to its first arc ends the tour
+    if (root[y] == y && nx == s) nx = -1;
+    next[i] = nx;
+}
+
+__global__ void k_rank_init(int64_t na, int32_t* rank) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) rank[i] = 1;
+}
+
+// Wyllie pointer jumping: rank = number of arcs from i to the end of its list.
+__global__ void k_rank_jump(int64_t na, const int32_t* __restrict__ next_in,
+                            const int32_t* __restrict__ rank_in, int32_t* next_out,
+                            int32_t* rank_out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    int32_t nx = next_in[i];
+    if (nx >= 0) {
+        rank_out[i] = rank_in[i] + rank_in[nx];
+        next_out[i] = next_in[nx];
+    } else {
+        rank_out[i] = rank_in[i];
+        next_out[i] = -1;
+    }
+}
+
+// Per tree: tour length L = rank of the root's first arc (0 for singletons).
+__global__ void k_tour_len(int64_t n, const int32_t* __restrict__ adj_start,
+                           const int32_t* __restrict__ root, const int32_t* __restrict__ tree_id,
+                           const int32_t* __restrict__ rank, int32_t* tlen) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n || root[v] != v) return;
+    int32_t s = adj_start[v], e = adj_start[v + 1];
+    tlen[tree_id[v]] = (e > s) ? rank[s] : 0;
+}
+
+__global__ void k_tour_pos(int64_t na, const int32_t* __restrict__ asrc,
+                           const int32_t* __restrict__ tree_id, const int32_t* __restrict__ tlen,
+                           const int32_t* __restrict__ rank, int32_t* tpos) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) tpos[i] = tlen[tree_id[asrc[i]]] - rank[i];
+}
+
+// Parent links, subtree sizes and the +1/-1 tour steps for the depth scan.
+__global__ void k_orient(int64_t na, const int32_t* __restrict__ asrc, const int32_t* __restrict__ adst,
+                         const float* __restrict__ aw, const int32_t* __restrict__ twin,
+                         const int32_t* __restrict__ tpos, const int32_t* __restrict__ tree_id,
+                         const int32_t* __restrict__ toff, int32_t* parent, float* pweight,
+                         int32_t* size, int32_t* down_arc, int32_t* steps) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    int32_t x = asrc[i], y = adst[i];
+    int32_t j = twin[i];
+    bool down = tpos[i] < tpos[j];
+    int32_t t = tree_id[x];
+    steps[toff[t] + tpos[i]] = down ? 1 : -1;
+    if (down) {
+        parent[y] = x;
+        pweight[y] = aw[i];
+        size[y] = (tpos[j] - tpos[i] + 1) / 2;
+        down_arc[y] = toff[t] + tpos[i];
+    }
+}
+
+__global__ void k_root_init(int64_t n, const int32_t* __restrict__ root,
+                            const int32_t* __restrict__ tree_id, const int32_t* __restrict__ tlen,
+                            int32_t* parent, float* pweight, int32_t* size, int32_t* depth,
+                            int32_t* down_arc) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n || root[v] != v) return;
+    parent[v] = (int32_t)v;
+    pweight[v] = 0.0f;
+    size[v] = tlen[tree_id[v]] / 2 + 1;
+    depth[v] = 0;
+    down_arc[v] = -1;
+}
+
+__global__ void k_depth_gather(int64_t n, const int32_t* __restrict__ down_arc,
+                               const int32_t* __restrict__ scanned, int32_t* depth) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t a = down_arc[v];
+    if (a >= 0) depth[v] = scanned[a];
+}
+
+// heavy child: largest subtree among children, ties -> lower id (adjacency
+// lists are ascending by id, so keep the first maximum).
+__global__ void k_heavy(int64_t n, const int32_t* __restrict__ adj_start,
+                        const int32_t* __restrict__ adst, const int32_t* __restrict__ parent,
+                        const int32_t* __restrict__ size, int32_t* heavy) {
+    int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
+    int32_t best = -1, bs = -1;
+    for (int32_t k = adj_start[x]; k < adj_start[x + 1]; k++) {
+        int32_t y = adst[k];
+        if (parent[y] == x && y != x) {
+            if (size[y] > bs) {
+                bs = size[y];
+                best = y;
+            }
+        }
+    }
+    heavy[x] = best;
+}
+
+__global__ void k_hp_init(int64_t n, const int32_t* __restrict__ parent,
+                          const int32_t* __restrict__ heavy, int32_t* hp, int32_t* dist) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t p = parent[v];
+    bool on = (p != v) && heavy[p] == v;
+    hp[v] = on ? p : (int32_t)v;
+    dist[v] = on ? 1 : 0;
+}
+
+__global__ void k_hp_jump(int64_t n, const int32_t* __restrict__ hp_in,
+                          const int32_t* __restrict__ d_in, int32_t* hp_out, int32_t* d_out) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t h = hp_in[v];
+    int32_t hh = hp_in[h];
+    if (hh != h) {
+        hp_out[v] = hh;
+        d_out[v] = d_in[v] + d_in[h];
+    } else {
+        hp_out[v] = h;
+        d_out[v] = d_in[v];
+    }
+}
+
+// light-edge steps for the light-depth scan: entering / leaving a path head.
+__global__ void k_light_steps(int64_t na, const int32_t* __restrict__ asrc,
+                              const int32_t* __restrict__ adst, const int32_t* __restrict__ parent,
+                              const int32_t* __restrict__ head, const int32_t* __restrict__ tpos,
+                              const int32_t* __restrict__ tree_id, const int32_t* __restrict__ toff,
+                              int32_t* steps) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    int32_t x = asrc[i], y = adst[i];
+    int32_t pos = toff[tree_id[x]] + tpos[i];
+    if (parent[y] == x) {
+        steps[pos] = (head[y] == y) ? 1 : 0;  // down into y
+    } else {
+        steps[pos] = (head[x] == x) ? -1 : 0;  // up out of x
+    }
+}
+
+__global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
+                              const int32_t* __restrict__ lscan, const int32_t* __restrict__ head,
+                              const int32_t* __restrict__ dist, uint64_t* key, int32_t* idx,
+                              int32_t* ld_out) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t a = down_arc[v];
+    int32_t ld = a >= 0 ? lscan[a] : 0;
+    ld_out[v] = ld;
+    key[v] = ((uint64_t)ld << 56) | ((uint64_t)(uint32_t)head[v] << 24) | (uint64_t)dist[v];
+    idx[v] = (int32_t)v;
+}
+
+__global__ void k_layout_pos(int64_t n, const int32_t* __restrict__ lnode,
+                             const float* __restrict__ pweight, float gamma, int32_t* lpos,
+                             float* lsim) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int32_t v = lnode[k];
+    lpos[v] = (int32_t)k;
+    // RootedForest.similarities (spanning_forest.py:184-188) in float64,
+    // rounded once to the f32 the aggregation runs in.
+    lsim[k] = (float)exp(-(double)pweight[v] / ((double)gamma * 255.0));
+}
+
+__global__ void k_path_flags(int64_t n, const int32_t* __restrict__ lnode,
+                             const int32_t* __restrict__ head, int32_t* flag) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int32_t v = lnode[k];
+    flag[k] = head[v] == v ? 1 : 0;
+}
+
+__global__ void k_path_fill(int64_t n, const int32_t* __restrict__ flag,
+                            const int32_t* __restrict__ pidx, int32_t* p_start) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n && flag[k]) p_start[pidx[k]] = (int32_t)k;
+}
+
+__global__ void k_path_info(int64_t np, int64_t n, const int32_t* __restrict__ p_start,
+                            const int32_t* __restrict__ lnode, const int32_t* __restrict__ parent,
+                            const int32_t* __restrict__ lpos, const int32_t* __restrict__ tree_id,
+                            const int32_t* __restrict__ ld, int32_t* p_len, int32_t* p_par,
+                            int32_t* p_tree, int32_t* phase_cnt) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    int32_t s = p_start[i];
+    int32_t e = (i + 1 < np) ? p_start[i + 1] : (int32_t)n;
+    int32_t h = lnode[s];
+    p_len[i] = e - s;
+    p_par[i] = parent[h] == h ? -1 : lpos[parent[h]];
+    p_tree[i] = tree_id[h];
+    atomicAdd(&phase_cnt[ld[h]], 1);
+}
+
+// light children of the node at layout position k, ascending id
+__global__ void k_lc_count(int64_t n, const int32_t* __restrict__ lnode,
+                           const int32_t* __restrict__ adj_start, const int32_t* __restrict__ adst,
+                           const int32_t* __restrict__ parent, const int32_t* __restrict__ head,
+                           int32_t* cnt) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int32_t x = lnode[k];
+    int32_t c = 0;
+    for (int32_t a = adj_start[x]; a < adj_start[x + 1]; a++) {
+        int32_t y = adst[a];
+        if (parent[y] == x && y != x && head[y] == y) c++;
+    }
+    cnt[k] = c;
+}
+
+__global__ void k_lc_fill(int64_t n, const int32_t* __restrict__ lnode,
+                          const int32_t* __restrict__ adj_start, const int32_t* __restrict__ adst,
+                          const int32_t* __restrict__ parent, const int32_t* __restrict__ head,
+                          const int32_t* __restrict__ lpos, const int32_t* __restrict__ lc_start,
+                          int32_t* lc_list) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int32_t x = lnode[k];
+    int32_t o = lc_start[k];
+    for (int32_t a = adj_start[x]; a < adj_start[x + 1]; a++) {
+        int32_t y = adst[a];
+        if (parent[y] == x && y != x && head[y] == y) lc_list[o++] = lpos[y];
+    }
+}
+
+// ---- lanes
+__global__ void k_lanes_range(int64_t nt, int nx, int32_t* t_m, int32_t* t_doff) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    t_m[t] = nx;
+    t_doff[t] = 0;
+}
+
+__global__ void k_iota(int64_t n, int32_t* a, int32_t x0) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = x0 + (int32_t)i;
+}
+
+__global__ void k_lanes_count(int64_t nt, const uint32_t* __restrict__ masks, int nw, int32_t* t_m) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    int c = 0;
+    for (int i = 0; i < nw; i++) c += __popc(masks[t * nw + i]);
+    t_m[t] = c;
+}
+
+__global__ void k_lanes_fill(int64_t nt, const uint32_t* __restrict__ masks, int nw,
+                             const int32_t* __restrict__ t_doff, int32_t* dlist) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    int32_t o = t_doff[t];
+    for (int i = 0; i < nw; i++) {
+        uint32_t word = masks[t * nw + i];
+        while (word) {
+            int b = __ffs(word) - 1;
+            dlist[o++] = i * 32 + b;
+            word &= word - 1;
+        }
+    }
+}
+
+__global__ void k_row_m(int64_t n, const int32_t* __restrict__ lnode,
+                        const int32_t* __restrict__ tree_id, const int32_t* __restrict__ t_m,
+                        int64_t* rm) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) rm[k] = t_m[tree_id[lnode[k]]];
+    if (k == n) rm[k] = 0;
+}
+
+__global__ void k_node_m(int64_t n, const int32_t* __restrict__ tree_id,
+                         const int32_t* __restrict__ t_m, int64_t* nm) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) nm[v] = t_m[tree_id[v]];
+}
+
+}  // namespace hdp
+
+using namespace hdp;
+
+static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const int32_t* ev,
+                        const float* ew, const uint8_t* in_tree, const int32_t* comp_in) {
+    cudaStream_t st = f->st;
+    const int64_t n = f->n;
+    const int B = 256;
+
+    // ---- 1. tree edges
+    DevBuf<int32_t> flags, fpos;
+    HDP_TRY(flags.alloc(m_in + 1, st));
+    HDP_TRY(fpos.alloc(m_in + 1, st));
+    int64_t m = 0;
+    if (m_in > 0) {
+        k_flag_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, in_tree, flags.get());
+        HDP_TRY(exclusive_sum(flags.get(), fpos.get(), m_in, st));
+        int32_t last_pos = 0, last_flag = 0;
+        HDP_TRY(to_host(&last_pos, fpos.get() + m_in - 1, 1, st));
+        HDP_TRY(to_host(&last_flag, flags.get() + m_in - 1, 1, st));
+        m = (int64_t)last_pos + last_flag;
+    }
+    HDP_REQUIRE(m <= n - 1 || n == 0, HDP_ERR_DATA, "forest has %lld edges for %lld nodes (cycle)",
+                (long long)m, (long long)n);
+    DevBuf<int32_t> tu, tv;
+    DevBuf<float> tw;
+    DevBuf<uint64_t> tkey;
+    HDP_TRY(tu.alloc(m + 1, st));
+    HDP_TRY(tv.alloc(m + 1, st));
+    HDP_TRY(tw.alloc(m + 1, st));
+    HDP_TRY(tkey.alloc(m + 1, st));
+    if (m_in > 0)
+        k_compact_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, flags.get(), fpos.get(), eu, ev, ew,
+                                                        tu.get(), tv.get(), tw.get(), tkey.get());
+    flags.release();
+    fpos.release();
+
+    // ---- 2. components, roots, tree numbering
+    DevBuf<int32_t> comp;
+    HDP_TRY(comp.alloc(n, st));
+    if (comp_in) {
+        HDP_CHECK_CUDA(cudaMemcpyAsync(comp.get(), comp_in, n * sizeof(int32_t),
+                                       cudaMemcpyDeviceToDevice, st));
+    } else {
+        DevBuf<uint8_t> sel;
+        HDP_TRY(sel.alloc(m + 1, st));
+        HDP_TRY(run_boruvka(n, m, tu.get(), tv.get(), tkey.get(), sel.get(), comp.get(), nullptr, st));
+    }
+    tkey.release();
+    DevBuf<int32_t> minid, is_root, tindex;
+    HDP_TRY(minid.alloc(n, st));
+    HDP_TRY(is_root.alloc(n, st));
+    HDP_TRY(tindex.alloc(n, st));
+    HDP_TRY(f->root.alloc(n, st));
+    HDP_TRY(f->tree_id.alloc(n, st));
+    k_fill_int<<<grid_for(n, B), B, 0, st>>>(n, minid.get(), INT_MAX);
+    k_min_root<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get());
+    k_root_flags<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get(), f->root.get(),
+                                              is_root.get());
+    HDP_TRY(exclusive_sum(is_root.get(), tindex.get(), n, st));
+    {
+        int32_t a = 0, b = 0;
+        HDP_TRY(to_host(&a, tindex.get() + n - 1, 1, st));
+        HDP_TRY(to_host(&b, is_root.get() + n - 1, 1, st));
+        f->n_trees = (int64_t)a + b;
+    }
+    k_tree_ids<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), tindex.get(), f->tree_id.get());
+    HDP_CHECK_LAUNCH();
+    comp.release();
+    minid.release();
+    tindex.release();
+
+    // ---- 3. CSR adjacency (arcs sorted by (src, dst))
+    const int64_t na = 2 * m;
+    DevBuf<uint64_t> akey, akey2;
+    DevBuf<float> aw, aw2;
+    DevBuf<int32_t> deg, adj_start, asrc, adst;
+    HDP_TRY(akey.alloc(na + 1, st));
+    HDP_TRY(akey2.alloc(na + 1, st));
+    HDP_TRY(aw.alloc(na + 1, st));
+    HDP_TRY(aw2.alloc(na + 1, st));
+    HDP_TRY(deg.alloc(n + 1, st));
+    HDP_TRY(adj_start.alloc(n + 1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(deg.get(), 0, (n + 1) * sizeof(int32_t), st));
+    if (m > 0) {
+        k_make_arcs<<<grid_for(m, B), B, 0, st>>>(m, tu.get(), tv.get(), tw.get(), akey.get(),
+                                                 aw.get(), deg.get());
+        HDP_TRY(sort_pairs(akey.get(), akey2.get(), aw.get(), aw2.get(), na, 0,
+                           32 + bits_for(n), st));
+    }
+    HDP_TRY(exclusive_sum(deg.get(), adj_start.get(), n + 1, st));
+    tu.release();
+    tv.release();
+    tw.release();
+    akey.release();
+    aw.release();
+    HDP_TRY(asrc.alloc(na + 1, st));
+    HDP_TRY(adst.alloc(na + 1, st));
+    if (na > 0) k_arc_unpack<<<grid_for(na, B), B, 0, st>>>(na, akey2.get(), asrc.get(), adst.get());
+    akey2.release();
+
+    // ---- 4. Euler tour + list ranking
+    DevBuf<int32_t> twin, nxt, nxt2, rank, rank2, tlen, toff, tpos;
+    HDP_TRY(twin.alloc(na + 1, st));
+    HDP_TRY(nxt.alloc(na + 1, st));
+    HDP_TRY(nxt2.alloc(na + 1, st));
+    HDP_TRY(rank.alloc(na + 1, st));
+    HDP_TRY(rank2.alloc(na + 1, st));
+    HDP_TRY(tlen.alloc(f->n_trees + 1, st));
+    HDP_TRY(toff.alloc(f->n_trees + 1, st));
+    HDP_TRY(tpos.alloc(na + 1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(tlen.get(), 0, (f->n_trees + 1) * sizeof(int32_t), st));
+    if (na > 0) {
+        k_tour_next<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), adj_start.get(),
+                                                  f->root.get(), twin.get(), nxt.get());
+        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, rank.get());
+        int rounds = ceil_log2(na + 1);
+        for (int r = 0; r < rounds; r++) {
+            k_rank_jump<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), rank.get(), nxt2.get(),
+                                                      rank2.get());
+            std::swap(nxt.p, nxt2.p);
+            std::swap(rank.p, rank2.p);
+        }
+        HDP_CHECK_LAUNCH();
+    }
+    k_tour_len<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), f->root.get(), f->tree_id.get(),
+                                             rank.get(), tlen.get());
+    HDP_TRY(exclusive_sum(tlen.get(), toff.get(), f->n_trees + 1, st));
+    if (na > 0)
+        k_tour_pos<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), f->tree_id.get(), tlen.get(),
+                                                 rank.get(), tpos.get());
+    nxt.release();
+    nxt2.release();
+    rank.release();
+    rank2.release();
+
+    // ---- 5. orientation, sizes, depth
+    HDP_TRY(f->parent.alloc(n, st));
+    HDP_TRY(f->pweight.alloc(n, st));
+    HDP_TRY(f->size.alloc(n, st));
+    HDP_TRY(f->depth.alloc(n, st));
+    DevBuf<int32_t> down_arc, steps, scanned;
+    HDP_TRY(down_arc.alloc(n, st));
+    HDP_TRY(steps.alloc(na + 1, st));
+    HDP_TRY(scanned.alloc(na + 1, st));
+    k_root_init<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), f->tree_id.get(), tlen.get(),
+                                              f->parent.get(), f->pweight.get(), f->size.get(),
+                                              f->depth.get(), down_arc.get());
+    if (na > 0) {
+        k_orient<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), aw2.get(), twin.get(),
+                                               tpos.get(), f->tree_id.get(), toff.get(),
+                                               f->parent.get(), f->pweight.get(), f->size.get(),
+                                               down_arc.get(), steps.get());
+        HDP_TRY(inclusive_sum(steps.get(), scanned.get(), na, st));
+        k_depth_gather<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), f->depth.get());
+    }
+    HDP_CHECK_LAUNCH();
+    {
+        DevBuf<int32_t> mx;
+        HDP_TRY(mx.alloc(1, st));
+        HDP_TRY(reduce_max(f->depth.get(), mx.get(), n, st));
+        int32_t h = 0;
+        HDP_TRY(to_host(&h, mx.get(), 1, st));
+        f->max_depth = h;
+    }
+    aw2.release();
+    twin.release();
+
+    // ---- 6. heavy paths
+    DevBuf<int32_t> heavy, hp, hp2, dist, dist2;
+    HDP_TRY(heavy.alloc(n, st));
+    HDP_TRY(hp.alloc(n, st));
+    HDP_TRY(hp2.alloc(n, st));
+    HDP_TRY(dist.alloc(n, st));
+    HDP_TRY(dist2.alloc(n, st));
+    k_heavy<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), adst.get(), f->parent.get(),
+                                          f->size.get(), heavy.get());
+    k_hp_init<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), hp.get(), dist.get());
+    {
+        int rounds = ceil_log2(f->max_depth + 2);
+        for (int r = 0; r < rounds; r++) {
+            k_hp_jump<<<grid_for(n, B), B, 0, st>>>(n, hp.get(), dist.get(), hp2.get(), dist2.get());
+            std::swap(hp.p, hp2.p);
+            std::swap(dist.p, dist2.p);
+        }
+    }
+    HDP_CHECK_LAUNCH();
+    heavy.release();
+    hp2.release();
+    dist2.release();
+    int32_t* head = hp.get();
+
+    // ---- 7. light depth (tour scan) and layout order
+    DevBuf<int32_t> ld;
+    HDP_TRY(ld.alloc(n, st));
+    if (na > 0) {
+        k_light_steps<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), f->parent.get(),
+                                                    head, tpos.get(), f->tree_id.get(), toff.get(),
+                                                    steps.get());
+        HDP_TRY(inclusive_sum(steps.get(), scanned.get(), na, st));
+    }
+    DevBuf<uint64_t> lkey, lkey2;
+    DevBuf<int32_t> lidx;
+    HDP_TRY(lkey.alloc(n, st));
+    HDP_TRY(lkey2.alloc(n, st));
+    HDP_TRY(lidx.alloc(n, st));
+    HDP_TRY(f->lnode.alloc(n, st));
+    k_layout_keys<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), head, dist.get(),
+                                                lkey.get(), lidx.get(), ld.get());
+    HDP_CHECK_LAUNCH();
+    HDP_TRY(sort_pairs(lkey.get(), lkey2.get(), lidx.get(), f->lnode.get(), n, 0, 64, st));
+    lkey.release();
+    lkey2.release();
+    lidx.release();
+    steps.release();
+    scanned.release();
+    tpos.release();
+    toff.release();
+    tlen.release();
+    down_arc.release();
+    asrc.release();
+    HDP_TRY(f->lpos.alloc(n, st));
+    HDP_TRY(f->lsim.alloc(n, st));
+    k_layout_pos<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), f->pweight.get(), f->gamma,
+                                               f->lpos.get(), f->lsim.get());
+
+    // ---- 8. paths and phases
+    DevBuf<int32_t> pflag, pidx;
+    HDP_TRY(pflag.alloc(n, st));
+    HDP_TRY(pidx.alloc(n, st));
+    k_path_flags<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), head, pflag.get());
+    HDP_TRY(exclusive_sum(pflag.get(), pidx.get(), n, st));
+    {
+        int32_t a = 0, b = 0;
+        HDP_TRY(to_host(&a, pidx.get() + n - 1, 1, st));
+        HDP_TRY(to_host(&b, pflag.get() + n - 1, 1, st));
+        f->n_paths = (int64_t)a + b;
+    }
+    HDP_TRY(f->p_start.alloc(f->n_paths, st));
+    HDP_TRY(f->p_len.alloc(f->n_paths, st));
+    HDP_TRY(f->p_par.alloc(f->n_paths, st));
+    HDP_TRY(f->p_tree.alloc(f->n_paths, st));
+    k_path_fill<<<grid_for(n, B), B, 0, st>>>(n, pflag.get(), pidx.get(), f->p_start.get());
+    const int MAXPH = 256;
+    DevBuf<int32_t> phase_cnt;
+    HDP_TRY(phase_cnt.alloc(MAXPH, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(phase_cnt.get(), 0, MAXPH * sizeof(int32_t), st));
+    k_path_info<<<grid_for(f->n_paths, B), B, 0, st>>>(
+        f->n_paths, n, f->p_start.get(), f->lnode.get(), f->parent.get(), f->lpos.get(),
+        f->tree_id.get(), ld.get(), f->p_len.get(), f->p_par.get(), f->p_tree.get(),
+        phase_cnt.get());
+    HDP_CHECK_LAUNCH();
+    {
+        std::vector<int32_t> cnt(MAXPH);
+        HDP_TRY(to_host(cnt.data(), phase_cnt.get(), MAXPH, st));
+        int last = 0;
+        for (int r = 0; r < MAXPH; r++)
+            if (cnt[r]) last = r;
+        f->n_phases = last + 1;
+        f->phase_off.assign(f->n_phases + 1, 0);
+        for (int r = 0; r < f->n_phases; r++) f->phase_off[r + 1] = f->phase_off[r] + cnt[r];
+    }
+
+    // ---- 9. light-children CSR in layout order
+    DevBuf<int32_t> lcc;
+    HDP_TRY(lcc.alloc(n + 1, st));
+    HDP_TRY(f->lc_start.alloc(n + 1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(lcc.get(), 0, (n + 1) * sizeof(int32_t), st));
+    k_lc_count<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
+                                             f->parent.get(), head, lcc.get());
+    HDP_TRY(exclusive_sum(lcc.get(), f->lc_start.get(), n + 1, st));
+    int32_t n_lc = 0;
+    HDP_TRY(to_host(&n_lc, f->lc_start.get() + n, 1, st));
+    HDP_TRY(f->lc_list.alloc(n_lc + 1, st));
+    k_lc_fill<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
+                                            f->parent.get(), head, f->lpos.get(),
+                                            f->lc_start.get(), f->lc_list.get());
+    HDP_CHECK_LAUNCH();
+    HDP_CHECK_CUDA(cudaStreamSynchronize(st));
+    return HDP_OK;
+}
+
+static int lanes_finish(hdp_forest* f) {
+    cudaStream_t st = f->st;
+    const int B = 256;
+    const int64_t n = f->n;
+    DevBuf<int64_t> rm, nm;
+    HDP_TRY(rm.alloc(n + 1, st));
+    HDP_TRY(nm.alloc(n + 1, st));
+    HDP_TRY(f->rowoff.alloc(n + 1, st));
+    HDP_TRY(f->nodeoff.alloc(n + 1, st));
+    k_row_m<<<grid_for(n + 1, B), B, 0, st>>>(n, f->lnode.get(), f->tree_id.get(), f->t_m.get(),
+                                              rm.get());
+    HDP_TRY(exclusive_sum(rm.get(), f->rowoff.get(), n + 1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(nm.get() + n, 0, sizeof(int64_t), st));
+    k_node_m<<<grid_for(n, B), B, 0, st>>>(n, f->tree_id.get(), f->t_m.get(), nm.get());
+    HDP_TRY(exclusive_sum(nm.get(), f->nodeoff.get(), n + 1, st));
+    HDP_CHECK_LAUNCH();
+    HDP_TRY(to_host(&f->total_entries, f->rowoff.get() + n, 1, st));
+    DevBuf<int32_t> mx;
+    HDP_TRY(mx.alloc(1, st));
+    HDP_TRY(reduce_max(f->t_m.get(), mx.get(), f->n_trees, st));
+    int32_t hm = 0;
+    HDP_TRY(to_host(&hm, mx.get(), 1, st));
+    f->max_m = hm;
+    f->lanes_set = 1;
+    return HDP_OK;
+}
+
+extern "C" {
+
+int hdp_forest_create(int64_t n_nodes, int64_t n_edges, const int32_t* eu, const int32_t* ev,
+                      const float* ew, const uint8_t* in_tree, const int32_t* comp, float gamma,
+                      hdp_forest** out, void* stream) {
+    HDP_REQUIRE(out != nullptr, HDP_ERR_CONFIG, "null output handle");
+    HDP_REQUIRE(n_nodes >= 1 && n_nodes < ((int64_t)1 << 31) - 2, HDP_ERR_CONFIG,
+                "node count %lld out of range", (long long)n_nodes);
+    HDP_REQUIRE(n_edges >= 0 && 2 * n_edges < ((int64_t)1 << 31) - 2, HDP_ERR_CONFIG,
+                "edge count %lld out of range", (long long)n_edges);
+    HDP_REQUIRE(gamma > 0.0f, HDP_ERR_CONFIG, "gamma must be positive, got %g", (double)gamma);
+    hdp_forest* f = new hdp_forest();
+    f->st = (cudaStream_t)stream;
+    f->n = n_nodes;
+    f->gamma = gamma;
+    int s = forest_build(f, n_edges, eu, ev, ew, in_tree, comp);
+    if (s != HDP_OK) {
+        delete f;
+        return s;
+    }
+    *out = f;
+    return HDP_OK;
+}
+
+int hdp_forest_stats(const hdp_forest* f, int64_t* n_trees, int64_t* n_paths, int64_t* n_phases,
+                     int64_t* max_depth) {
+    HDP_REQUIRE(f != nullptr, HDP_ERR_CONFIG, "null forest");
+    if (n_trees) *n_trees = f->n_trees;
+    if (n_paths) *n_paths = f->n_paths;
+    if (n_phases) *n_phases = f->n_phases;
+    if (max_depth) *max_depth = f->max_depth;
+    return HDP_OK;
+}
+
+int hdp_forest_export(const hdp_forest* f, int32_t* parent, int32_t* depth, int32_t* tree_id,
+                      int32_t* size, float* parent_weight, int32_t* root, void* stream) {
+    HDP_REQUIRE(f != nullptr, HDP_ERR_CONFIG, "null forest");
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t b = f->n * sizeof(int32_t);
+    if (parent) HDP_CHECK_CUDA(cudaMemcpyAsync(parent, f->parent.get(), b, cudaMemcpyDeviceToDevice, st));
+    if (depth) HDP_CHECK_CUDA(cudaMemcpyAsync(depth, f->depth.get(), b, cudaMemcpyDeviceToDevice, st));
+    if (tree_id) HDP_CHECK_CUDA(cudaMemcpyAsync(tree_id, f->tree_id.get(), b, cudaMemcpyDeviceToDevice, st));
+    if (size) HDP_CHECK_CUDA(cudaMemcpyAsync(size, f->size.get(), b, cudaMemcpyDeviceToDevice, st));
+    if (root) HDP_CHECK_CUDA(cudaMemcpyAsync(root, f->root.get(), b, cudaMemcpyDeviceToDevice, st));
+    if (parent_weight)
+        HDP_CHECK_CUDA(cudaMemcpyAsync(parent_weight, f->pweight.get(), f->n * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, st));
+    return HDP_OK;
+}
+
+int hdp_forest_set_lanes_range(hdp_forest* f, int x0, int nx, void* stream) {
+    HDP_REQUIRE(f != nullptr, HDP_ERR_CONFIG, "null forest");
+    HDP_REQUIRE(nx >= 1 && x0 >= 0, HDP_ERR_CONFIG, "empty disparity range");
+    f->st = (cudaStream_t)stream;
+    cudaStream_t st = f->st;
+    HDP_TRY(f->t_m.alloc(f->n_trees, st));
+    HDP_TRY(f->t_doff.alloc(f->n_trees, st));
+    HDP_TRY(f->dlist.alloc(nx, st));
+    k_lanes_range<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, nx, f->t_m.get(),
+                                                             f->t_doff.get());
+    k_iota<<<grid_for(nx, 256), 256, 0, st>>>(nx, f->dlist.get(), x0);
+    HDP_CHECK_LAUNCH();
+    return lanes_finish(f);
+}
+
+int hdp_forest_set_lanes(hdp_forest* f, const uint32_t* tree_masks, int nw, void* stream) {
+    HDP_REQUIRE(f != nullptr, HDP_ERR_CONFIG, "null forest");
+    HDP_REQUIRE(nw >= 1, HDP_ERR_CONFIG, "mask width must be >= 1 word");
+    f->st = (cudaStream_t)stream;
+    cudaStream_t st = f->st;
+    HDP_TRY(f->t_m.alloc(f->n_trees, st));
+    HDP_TRY(f->t_doff.alloc(f->n_trees + 1, st));
+    k_lanes_count<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw, f->t_m.get());
+    HDP_TRY(exclusive_sum(f->t_m.get(), f->t_doff.get(), f->n_trees, st));
+    int32_t a = 0, b = 0;
+    HDP_TRY(to_host(&a, f->t_doff.get() + f->n_trees - 1, 1, st));
+    HDP_TRY(to_host(&b, f->t_m.get() + f->n_trees - 1, 1, st));
+    HDP_TRY(f->dlist.alloc((size_t)a + b + 1, st));
+    k_lanes_fill<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw,
+                                                            f->t_doff.get(), f->dlist.get());
+    HDP_CHECK_LAUNCH();
+    {
+        DevBuf<int32_t> mn;
+        // every tree needs a non-empty interval (cost_volume.py:212-213)
+        HDP_TRY(mn.alloc(1, st));
+        size_t bytes = 0;
+        HDP_CHECK_CUDA(cub::DeviceReduce::Min(nullptr, bytes, f->t_m.get(), mn.get(), (int)f->n_trees, st));
+        DevBuf<char> tmp;
+        HDP_TRY(tmp.alloc(bytes, st));
+        HDP_CHECK_CUDA(cub::DeviceReduce::Min(tmp.get(), bytes, f->t_m.get(), mn.get(), (int)f->n_trees, st));
+        int32_t h = 0;
+        HDP_TRY(to_host(&h, mn.get(), 1, st));
+        HDP_REQUIRE(h >= 1, HDP_ERR_INTERNAL, "a tree has an empty disparity interval");
+    }
+    return lanes_finish(f);
+}
+
+int hdp_forest_entries(hdp_forest* f, int64_t* total, int64_t* node_offsets, void* stream) {
+    HDP_REQUIRE(f != nullptr && f->lanes_set, HDP_ERR_CONFIG, "forest lanes not set");
+    if (total) *total = f->total_entries;
+    if (node_offsets)
+        HDP_CHECK_CUDA(cudaMemcpyAsync(node_offsets, f->nodeoff.get(), f->n * sizeof(int64_t),
+                                       cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    return HDP_OK;
+}
+
+void hdp_forest_destroy(hdp_forest* f) { delete f; }
+
+}  // extern "C"

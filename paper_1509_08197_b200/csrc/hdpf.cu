@@ -1,0 +1,250 @@
+// Disparity-tree forest (HDPF) build, exact with the reference's sequential
+// Kruskal-with-rules (hdp_forest.py:151-216).
+//
+// Rule 1 (pixel sets disjoint -> drop) is a static per-edge filter; the
+// survivors are sorted per pair by the Kruskal key (weight, scan index).
+// Rule 2 compares the LIVE tree sets of the two components at the moment the
+// edge is reached, so the result depends on the order of merges; a plain
+// connected-components / Boruvka formulation is not equivalent.  We decide
+// the edges with deterministic reservations: one CTA per stereo pair walks
+// the sorted edge list in windows; every undecided window edge finds its two
+// roots and reserves both with an atomicMax of a (round, -position) stamp;
+// an edge that holds both reservations has no earlier pending edge touching
+// either tree, so its sequential outcome is already determined and it is
+// decided now (rule 2 + union).  Self-loops are dropped at once.  Undecided
+// edges are compacted (order preserved) in front of the next window.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "prims.cuh"
+
+namespace hdp {
+
+__device__ __forceinline__ const uint32_t* pix_mask(const uint32_t* row_masks,
+                                                   const int32_t* pixel_row, int32_t node,
+                                                   int64_t npp, int n_rows, int nw) {
+    int64_t b = node / npp;
+    return row_masks + ((int64_t)b * n_rows + pixel_row[node]) * nw;
+}
+
+__global__ void k_rule1(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                        const uint64_t* __restrict__ key, const int32_t* __restrict__ pixel_row,
+                        const uint32_t* __restrict__ row_masks, int64_t npp, int64_t epp,
+                        int n_rows, int nw, int32_t* flag, uint64_t* skey) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    int32_t a = eu[e], b = ev[e];
+    const uint32_t* ma = pix_mask(row_masks, pixel_row, a, npp, n_rows, nw);
+    const uint32_t* mb = pix_mask(row_masks, pixel_row, b, npp, n_rows, nw);
+    bool meet = false;
+    for (int i = 0; i < nw; i++) meet |= (ma[i] & mb[i]) != 0;
+    flag[e] = meet ? 1 : 0;
+    uint64_t k = key[e];
+    uint64_t pair = (uint64_t)(e / epp);
+    // (pair, weight bits, scan index): weights are non-negative floats < 2^31
+    skey[e] = (pair << 55) | ((k >> 32) << 24) | (k & 0xffffffull);
+}
+
+__global__ void k_select(int64_t m, const int32_t* __restrict__ flag,
+                         const int32_t* __restrict__ pos, const uint64_t* __restrict__ skey,
+                         uint64_t* okey, int32_t* oidx) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m || !flag[e]) return;
+    okey[pos[e]] = skey[e];
+    oidx[pos[e]] = (int32_t)e;
+}
+
+__global__ void k_seg_bounds(int64_t ms, const uint64_t* __restrict__ skey, int batch,
+                             int32_t* seg) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > ms) return;
+    int pb = (i == 0) ? -1 : (int)(skey[i - 1] >> 55);
+    int pc = (i == ms) ? batch : (int)(skey[i] >> 55);
+    for (int b = pb + 1; b <= pc; b++) seg[b] = (int32_t)i;
+}
+
+__global__ void k_uf_init(int64_t n, const int32_t* __restrict__ pixel_row,
+                          const uint32_t* __restrict__ row_masks, int64_t npp, int n_rows, int nw,
+                          int32_t* uf, int32_t* usz, uint32_t* tm, unsigned long long* res) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    uf[v] = (int32_t)v;
+    usz[v] = 1;
+    res[v] = 0ull;
+    const uint32_t* pm = pix_mask(row_masks, pixel_row, (int32_t)v, npp, n_rows, nw);
+    for (int i = 0; i < nw; i++) tm[v * nw + i] = pm[i];
+}
+
+__device__ __forceinline__ int32_t uf_find(int32_t* uf, int32_t x) {
+    while (true) {
+        int32_t p = uf[x];
+        if (p == x) return x;
+        int32_t gp = uf[p];
+        if (gp != p) uf[x] = gp;  // path halving (stores an ancestor: race-safe)
+        x = gp;
+    }
+}
+
+constexpr int DR_THREADS = 1024;
+
+__global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ seg,
+                                                   int32_t* __restrict__ order,
+                                                   const int32_t* __restrict__ eu,
+                                                   const int32_t* __restrict__ ev, int32_t* uf,
+                                                   int32_t* usz, uint32_t* tm,
+                                                   unsigned long long* res, int nw, double beta,
+                                                   uint8_t* in_tree, int* rounds_out) {
+    __shared__ int s_warp[DR_THREADS / 32];
+    __shared__ int s_total;
+    int b = blockIdx.x;
+    int tid = threadIdx.x;
+    int lane = tid & 31, wid = tid >> 5;
+    int32_t head = seg[b], end = seg[b + 1];
+    unsigned int round = 0;
+    while (head < end) {
+        int32_t win = min((int32_t)DR_THREADS, end - head);
+        bool pend = tid < win;
+        bool decided = false;
+        int32_t e = 0, ra = 0, rb = 0;
+        unsigned long long stamp = ((unsigned long long)(round + 1) << 32) |
+                                   (unsigned long long)(0xffffffffu - (unsigned)tid);
+        if (pend) {
+            e = order[head + tid];
+            ra = uf_find(uf, eu[e]);
+            rb = uf_find(uf, ev[e]);
+            if (ra == rb) {
+                decided = true;  // would close a cycle: skipped (hdp_forest.py:190-191)
+            } else {
+                atomicMax(&res[ra], stamp);
+                atomicMax(&res[rb], stamp);
+            }
+        }
+        __syncthreads();
+        if (pend && !decided) {
+            unsigned long long xa = *((volatile unsigned long long*)&res[ra]);
+            unsigned long long xb = *((volatile unsigned long long*)&res[rb]);
+            if (xa == stamp && xb == stamp) {
+                decided = true;
+                int inter = 0, uni = 0;
+                for (int i = 0; i < nw; i++) {
+                    uint32_t p = tm[(int64_t)ra * nw + i], q = tm[(int64_t)rb * nw + i];
+                    inter += __popc(p & q);
+                    uni += __popc(p | q);
+                }
+                // rule 2: IEEE double division, as hdp_forest.py:195
+                if (!(__ddiv_rn((double)inter, (double)uni) < beta)) {
+                    int32_t keep = ra, gone = rb;
+                    if (usz[ra] < usz[rb]) { keep = rb; gone = ra; }
+                    uf[gone] = keep;
+                    usz[keep] += usz[gone];
+                    for (int i = 0; i < nw; i++) tm[(int64_t)keep * nw + i] |= tm[(int64_t)gone * nw + i];
+                    in_tree[e] = 1;
+                }
+            }
+        }
+        __syncthreads();
+        // stable compaction of the undecided window edges
+        bool keepme = pend && !decided;
+        unsigned bal = __ballot_sync(0xffffffffu, keepme);
+        if (lane == 0) s_warp[wid] = __popc(bal);
+        __syncthreads();
+        if (wid == 0) {
+            int v = s_warp[lane];
+            int incl = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            s_warp[lane] = incl - v;
+            if (lane == 31) s_total = incl;
+        }
+        __syncthreads();
+        int kept = s_total;
+        int32_t new_head = head + win - kept;
+        if (keepme) {
+            int rank = s_warp[wid] + __popc(bal & ((1u << lane) - 1));
+            order[new_head + rank] = e;
+        }
+        head = new_head;
+        round++;
+        __syncthreads();
+    }
+    if (tid == 0) atomicMax(rounds_out, (int)round);
+}
+
+__global__ void k_uf_final(int64_t n, int32_t* uf, int nw, const uint32_t* __restrict__ tm,
+                           int32_t* comp, uint32_t* tree_masks) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t r = (int32_t)v;
+    while (uf[r] != r) r = uf[r];
+    comp[v] = r;
+    for (int i = 0; i < nw; i++) tree_masks[v * nw + i] = tm[(int64_t)r * nw + i];
+}
+
+}  // namespace hdp
+
+using namespace hdp;
+
+extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pair,
+                        const int32_t* eu, const int32_t* ev, const uint64_t* key,
+                        const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
+                        double beta, uint8_t* in_tree, int32_t* comp, uint32_t* tree_masks,
+                        int* rounds_out, void* stream) {
+    HDP_REQUIRE(beta >= 0.0 && beta <= 1.0, HDP_ERR_CONFIG, "beta must be in [0, 1], got %g", beta);
+    HDP_REQUIRE(batch >= 1 && batch <= 255, HDP_ERR_CONFIG, "batch must be in [1, 255]");
+    HDP_REQUIRE(edges_per_pair < (1 << 24), HDP_ERR_CONFIG, "too many edges per pair for HDPF keys");
+    HDP_REQUIRE(nw >= 1 && n_rows >= 1, HDP_ERR_CONFIG, "empty interval table");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = (int64_t)batch * nodes_per_pair;
+    const int64_t m = (int64_t)batch * edges_per_pair;
+    const int B = 256;
+    DevBuf<int32_t> flag, pos, oidx, oidx2, seg, uf, usz;
+    DevBuf<uint64_t> skey, okey, okey2;
+    DevBuf<uint32_t> tm;
+    DevBuf<unsigned long long> res;
+    DevBuf<int> rounds;
+    HDP_TRY(flag.alloc(m + 1, st));
+    HDP_TRY(pos.alloc(m + 1, st));
+    HDP_TRY(skey.alloc(m + 1, st));
+    if (m > 0) HDP_CHECK_CUDA(cudaMemsetAsync(in_tree, 0, m, st));
+    int64_t ms = 0;
+    if (m > 0) {
+        k_rule1<<<grid_for(m, B), B, 0, st>>>(m, eu, ev, key, pixel_row, row_masks, nodes_per_pair,
+                                              edges_per_pair, n_rows, nw, flag.get(), skey.get());
+        HDP_TRY(exclusive_sum(flag.get(), pos.get(), m, st));
+        int32_t a = 0, b2 = 0;
+        HDP_TRY(to_host(&a, pos.get() + m - 1, 1, st));
+        HDP_TRY(to_host(&b2, flag.get() + m - 1, 1, st));
+        ms = (int64_t)a + b2;
+    }
+    HDP_TRY(okey.alloc(ms + 1, st));
+    HDP_TRY(okey2.alloc(ms + 1, st));
+    HDP_TRY(oidx.alloc(ms + 1, st));
+    HDP_TRY(oidx2.alloc(ms + 1, st));
+    HDP_TRY(seg.alloc(batch + 1, st));
+    if (m > 0)
+        k_select<<<grid_for(m, B), B, 0, st>>>(m, flag.get(), pos.get(), skey.get(), okey.get(),
+                                               oidx.get());
+    flag.release();
+    pos.release();
+    skey.release();
+    HDP_TRY(sort_pairs(okey.get(), okey2.get(), oidx.get(), oidx2.get(), ms, 0, 63, st));
+    k_seg_bounds<<<grid_for(ms + 1, B), B, 0, st>>>(ms, okey2.get(), batch, seg.get());
+    HDP_TRY(uf.alloc(n, st));
+    HDP_TRY(usz.alloc(n, st));
+    HDP_TRY(tm.alloc(n * nw, st));
+    HDP_TRY(res.alloc(n, st));
+    HDP_TRY(rounds.alloc(1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(rounds.get(), 0, sizeof(int), st));
+    k_uf_init<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
+                                            uf.get(), usz.get(), tm.get(), res.get());
+    HDP_CHECK_LAUNCH();
+    k_dr<<<batch, DR_THREADS, 0, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(),
+                                       res.get(), nw, beta, in_tree, rounds.get());
+    HDP_CHECK_LAUNCH();
+    k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks);
+    HDP_CHECK_LAUNCH();
+    if (rounds_out) HDP_TRY(to_host(rounds_out, rounds.get(), 1, st));
+    return HDP_OK;
+}

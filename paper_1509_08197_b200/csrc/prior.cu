@@ -1,0 +1,211 @@
+// Sampled disparity prior, float64 bit-exact with the reference.
+//
+// Replaces estimate_prior's matching part (hdp_model.py:425-470 with
+// _window_indices :366-374, _matched_window_cost :377-394, _windowed_wta
+// :397-422).  One warp per sample centre: lanes take disparities x, x+32, ...,
+// each lane evaluates the window-mean cost in exactly numpy's order
+// (sequential 3-channel mean, separate multiply/add, numpy pairwise sum of
+// the window, strict '<' over ascending x), and a lexicographic (cost, x)
+// shuffle reduction reproduces the reference's first-minimum scan.  The
+// cross-checked winners are histogrammed with integer atomics.  FP64 compute
+// bound; inputs are L1/L2 resident.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace hdp {
+
+struct PriorArgs {
+    const double* ul;
+    const double* gl;
+    const double* ur;
+    const double* gr;
+    int h, w, c, d_max, stride, window, max_offset;
+    int nrc, ncc;  // centre grid
+    double one_minus_alpha, alpha, tc, tg, border;
+    unsigned long long* counts;
+    unsigned long long* kept;
+};
+
+__device__ __forceinline__ double px_cost(const PriorArgs& a, const double* su, const double* sg,
+                                          const double* du, const double* dg, int64_t p,
+                                          int64_t q) {
+    double acc = fabs(__dsub_rn(su[p * a.c], du[q * a.c]));
+    for (int k = 1; k < a.c; k++) acc = __dadd_rn(acc, fabs(__dsub_rn(su[p * a.c + k], du[q * a.c + k])));
+    double color = __ddiv_rn(acc, (double)a.c);
+    double gd = fabs(__dsub_rn(sg[p], dg[q]));
+    double v = __dmul_rn(a.one_minus_alpha, color < a.tc ? color : a.tc);
+    double t = __dmul_rn(a.alpha, gd < a.tg ? gd : a.tg);
+    return __dadd_rn(v, t);
+}
+
+// window-mean cost of matching centre (cr, cc) of `src` against `dst` at
+// column offset sign*x (hdp_model.py:377-394), numpy summation order.
+__device__ double window_cost(const PriorArgs& a, const double* su, const double* sg,
+                              const double* du, const double* dg, int64_t base, int cr, int cc,
+                              int sign, int x) {
+    int half = a.window / 2;
+    int nwin = a.window * a.window;
+    int rest_n = nwin - 1;
+    int main_n = rest_n < 8 ? 0 : rest_n - (rest_n % 8);
+    double first = 0.0, res = 0.0;
+    double acc[8];
+    int q = 0;
+    for (int dr = -half; dr <= half; dr++) {
+        int r = min(max(cr + dr, 0), a.h - 1);
+        for (int dc = -half; dc <= half; dc++) {
+            int col = min(max(cc + dc, 0), a.w - 1);
+            int dcol = col + sign * x;
+            double v;
+            if (dcol >= 0 && dcol < a.w) {
+                int64_t p = base + (int64_t)r * a.w + col;
+                int64_t qq = base + (int64_t)r * a.w + dcol;
+                v = px_cost(a, su, sg, du, dg, p, qq);
+            } else {
+                v = a.border;
+            }
+            if (q == 0) {
+                first = v;
+            } else if (rest_n < 8) {
+                res = __dadd_rn(res, v);  // pairwise_sum below 8: 0 + a1 + a2 ...
+            } else {
+                int i = q - 1;
+                if (i < 8) {
+                    acc[i] = v;
+                } else if (i < main_n) {
+                    acc[i & 7] = __dadd_rn(acc[i & 7], v);
+                } else {
+                    if (i == main_n) {
+                        res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
+                                        __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
+                    }
+                    res = __dadd_rn(res, v);
+                }
+            }
+            q++;
+        }
+    }
+    if (rest_n >= 8 && main_n == rest_n) {
+        res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
+                        __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
+    }
+    return __ddiv_rn(__dadd_rn(first, res), (double)nwin);
+}
+
+// warp-wide windowed WTA: first minimum over x = 0..d_max
+__device__ int warp_wta(const PriorArgs& a, const double* su, const double* sg, const double* du,
+                        const double* dg, int64_t base, int cr, int cc, int sign) {
+    int lane = threadIdx.x & 31;
+    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    int bx = 0x7fffffff;
+    for (int x = lane; x <= a.d_max; x += 32) {
+        double v = window_cost(a, su, sg, du, dg, base, cr, cc, sign, x);
+        if (v < best) {
+            best = v;
+            bx = x;
+        }
+    }
+    for (int o = 16; o >= 1; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+        if (ob < best || (ob == best && ox < bx)) {
+            best = ob;
+            bx = ox;
+        }
+    }
+    return bx;
+}
+
+__global__ void __launch_bounds__(256) k_prior(PriorArgs a, int batch) {
+    int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t per = (int64_t)a.nrc * a.ncc;
+    if (wid >= per * batch) return;
+    int b = (int)(wid / per);
+    int k = (int)(wid % per);
+    int i = k / a.ncc, j = k % a.ncc;
+    int rs = i * a.stride, cs = j * a.stride;
+    int cr = (rs + min(rs + a.stride, a.h) - 1) / 2;
+    int cc = (cs + min(cs + a.stride, a.w) - 1) / 2;
+    int64_t base = (int64_t)b * a.h * a.w;
+    int dl = warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
+    int mc = cc - dl;
+    if (mc < 0) return;  // infeasible (hdp_model.py:458-459)
+    int dr = warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
+    int diff = dl - dr;
+    if (diff < 0) diff = -diff;
+    if ((threadIdx.x & 31) == 0 && diff <= a.max_offset) {
+        atomicAdd(&a.counts[(int64_t)b * (a.d_max + 1) + dl], 1ull);
+        atomicAdd(&a.kept[b], 1ull);
+    }
+}
+
+__global__ void k_assign_rows(const int32_t* __restrict__ pd, int batch, int ph, int pw, int h,
+                              int w, int s, int n_rows, int32_t* __restrict__ rows, int* bad) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t n = (int64_t)h * w;
+    if (t >= (int64_t)batch * n) return;
+    int b = t / n;
+    int64_t p = t % n;
+    int r = p / w, col = p % w;
+    int32_t v = pd[((int64_t)b * ph + r / s) * pw + col / s];
+    if (v < 0 || v >= n_rows) {
+        atomicAdd(bad, 1);
+        v = 0;
+    }
+    rows[t] = v;
+}
+
+}  // namespace hdp
+
+using namespace hdp;
+
+extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, const double* unit_r,
+                                const double* grad_r, int batch, int h, int w, int c, int d_max,
+                                int stride, int window, int max_offset, double alpha, double tau_c,
+                                double tau_g, int64_t* counts, int64_t* kept, void* stream) {
+    HDP_REQUIRE(stride >= 1 && window >= 1 && window % 2 == 1, HDP_ERR_CONFIG,
+                "sample_stride must be >= 1 and window odd and positive");
+    HDP_REQUIRE(window * window <= 129, HDP_ERR_CONFIG, "window larger than 11 not supported");
+    HDP_REQUIRE(c == 1 || c == 3, HDP_ERR_DATA, "channels must be 1 or 3");
+    HDP_REQUIRE(d_max >= 0, HDP_ERR_CONFIG, "d_max must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    HDP_CHECK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * batch * (d_max + 1), st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(kept, 0, sizeof(int64_t) * batch, st));
+    PriorArgs a;
+    a.ul = unit_l; a.gl = grad_l; a.ur = unit_r; a.gr = grad_r;
+    a.h = h; a.w = w; a.c = c; a.d_max = d_max; a.stride = stride; a.window = window;
+    a.max_offset = max_offset;
+    a.nrc = (h + stride - 1) / stride;
+    a.ncc = (w + stride - 1) / stride;
+    a.one_minus_alpha = 1.0 - alpha;
+    a.alpha = alpha; a.tc = tau_c; a.tg = tau_g;
+    a.border = (1.0 - alpha) * tau_c + alpha * tau_g;  // cost_volume.py:48-50, host IEEE
+    a.counts = (unsigned long long*)counts;
+    a.kept = (unsigned long long*)kept;
+    int64_t warps = (int64_t)a.nrc * a.ncc * batch;
+    if (warps == 0) return HDP_OK;
+    k_prior<<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch);
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+extern "C" int hdp_assign_rows(const int32_t* parent_disp, int batch, int ph, int pw, int h, int w,
+                               int s, int n_rows, int32_t* pixel_row, void* stream) {
+    HDP_REQUIRE(s >= 2, HDP_ERR_CONFIG, "block_size must be >= 2");
+    HDP_REQUIRE(ph == (h + s - 1) / s && pw == (w + s - 1) / s, HDP_ERR_INTERNAL,
+                "parent map %dx%d does not cover child %dx%d at block %d", ph, pw, h, w, s);
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf<int> bad;
+    HDP_TRY(bad.alloc(1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), st));
+    int64_t n = (int64_t)batch * h * w;
+    k_assign_rows<<<grid_for(n, 256), 256, 0, st>>>(parent_disp, batch, ph, pw, h, w, s, n_rows,
+                                                    pixel_row, bad.get());
+    HDP_CHECK_LAUNCH();
+    int hb = 0;
+    HDP_CHECK_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    HDP_CHECK_CUDA(cudaStreamSynchronize(st));
+    HDP_REQUIRE(hb == 0, HDP_ERR_INTERNAL, "%d parent disparities outside the %d-row table", hb,
+                n_rows);
+    return HDP_OK;
+}

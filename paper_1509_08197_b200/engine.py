@@ -1,0 +1,511 @@
+"""Device-resident, batched HDP stereo pipeline.
+
+Torch tensors carry device memory and the current stream; all arithmetic is
+in libhdpstereo.so (sm_100a) behind the C ABI (include/hdp_stereo.h).  Host
+code here only sequences stages and builds the small probability tables
+(A13-A15 of SURVEY.md §8a, <= 121x241 entries) with the reference's own numpy
+formulas -- control plane, not a fallback.
+
+Entry points:
+  run_baseline_batch -- run_baseline_pipeline (aggregation.py:274-358) for B pairs
+  run_hdp_batch      -- run_hdp_pipeline (aggregation.py:367-488) for B pairs
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .errors import ConfigError, DataError
+
+ALPHA, TAU_C, TAU_G = 0.9, 0.0275, 0.0078  # cost_volume.py:38-40
+
+
+def _t():
+    return L.torch_mod()
+
+
+@dataclass(frozen=True)
+class CostConsts:
+    alpha: float = ALPHA
+    tau_color: float = TAU_C
+    tau_grad: float = TAU_G
+
+
+# ------------------------------------------------------------------ levels
+@dataclass
+class Level:
+    level: int
+    h: int
+    w: int
+    c: int
+    d_max: int
+    img_l: object  # (B, h, w, c) f64
+    img_r: object
+    packed_l: object = None  # (B, h, w, 4) f32
+    packed_r: object = None
+    unit_l: object = None  # f64 planes for the exact prior
+    grad_l: object = None
+    unit_r: object = None
+    grad_r: object = None
+
+
+def to_f64(u8):
+    torch = _t()
+    out = torch.empty(u8.shape, dtype=torch.float64, device=u8.device)
+    L.call("hdp_u8_to_f64", L.ptr(u8), L.ptr(out), u8.numel(), L.stream())
+    return out
+
+
+def block_mean(img, s: int):
+    torch = _t()
+    b, h, w, c = img.shape
+    out = torch.empty((b, -(-h // s), -(-w // s), c), dtype=torch.float64, device=img.device)
+    L.call("hdp_block_mean", L.ptr(img), L.ptr(out), b, h, w, c, s, L.stream())
+    return out
+
+
+def prepare(img, want_f64: bool, want_packed: bool = True, want_gray: bool = False):
+    torch = _t()
+    b, h, w, c = img.shape
+    dev = img.device
+    unit = torch.empty((b, h, w, c), dtype=torch.float64, device=dev) if want_f64 else None
+    grad = torch.empty((b, h, w), dtype=torch.float64, device=dev) if want_f64 else None
+    gray = torch.empty((b, h, w), dtype=torch.float64, device=dev) if want_gray else None
+    packed = torch.empty((b, h, w, 4), dtype=torch.float32, device=dev) if want_packed else None
+    L.call("hdp_prepare", L.ptr(img), b, h, w, c, L.ptr(unit), L.ptr(gray), L.ptr(grad),
+           L.ptr(packed), L.stream())
+    return unit, gray, grad, packed
+
+
+def build_levels(left_u8, right_u8, d_max: int, levels: int, s: int, need_prior: bool):
+    """pyramid.py:78-122 + prepare_layer per level (device)."""
+    out = []
+    il, ir = to_f64(left_u8), to_f64(right_u8)
+    d = d_max
+    for lvl in range(levels + 1):
+        if lvl > 0:
+            il, ir = block_mean(il, s), block_mean(ir, s)
+            d = d // s
+        b, h, w, c = il.shape
+        prior = need_prior and lvl < levels
+        ul, _, gl, pl = prepare(il, prior)
+        ur, _, gr, pr = prepare(ir, prior)
+        out.append(Level(lvl, h, w, c, d, il, ir, pl, pr, ul, gl, ur, gr))
+    return out
+
+
+# ------------------------------------------------------------------- edges
+def grid_edges(img):
+    torch = _t()
+    b, h, w, c = img.shape
+    E = 2 * h * w - h - w
+    dev = img.device
+    eu = torch.empty(b * E, dtype=torch.int32, device=dev)
+    ev = torch.empty(b * E, dtype=torch.int32, device=dev)
+    ew = torch.empty(b * E, dtype=torch.float32, device=dev)
+    key = torch.empty(b * E, dtype=torch.int64, device=dev)
+    if b * E > 0:
+        L.call("hdp_grid_edges", L.ptr(img), b, h, w, c, L.ptr(eu), L.ptr(ev), L.ptr(ew),
+               L.ptr(key), L.stream())
+    return eu, ev, ew, key, E
+
+
+def rt_keys(n_edges: int, batch: int, seed: int, device):
+    """rt_edge_order (spanning_forest.py:110-112): the seeded numpy PCG64
+    permutation defines the order; key = (rank << 32) | index."""
+    torch = _t()
+    perm = np.random.default_rng(seed).permutation(n_edges)
+    rank = np.empty(n_edges, np.int64)
+    rank[perm] = np.arange(n_edges, dtype=np.int64)
+    key = (rank << 32) | np.arange(n_edges, dtype=np.int64)
+    return torch.from_numpy(np.tile(key, batch)).to(device)
+
+
+def mst(n_nodes: int, eu, ev, key):
+    torch = _t()
+    m = eu.numel()
+    in_tree = torch.empty(max(m, 1), dtype=torch.uint8, device=eu.device)
+    comp = torch.empty(n_nodes, dtype=torch.int32, device=eu.device)
+    rounds = C.c_int(0)
+    L.call("hdp_mst", n_nodes, m, L.ptr(eu), L.ptr(ev), L.ptr(key), L.ptr(in_tree), L.ptr(comp),
+           C.byref(rounds), L.stream())
+    return in_tree[:m], comp, rounds.value
+
+
+# ------------------------------------------------------------------ forest
+class DeviceForest:
+    """Rooted forest + heavy-path layout owned by libhdpstereo (hdp_forest*)."""
+
+    def __init__(self, n_nodes, eu, ev, ew, in_tree=None, comp=None, gamma: float = 0.1):
+        self._h = C.c_void_p()
+        self.n = int(n_nodes)
+        L.call("hdp_forest_create", self.n, eu.numel(), L.ptr(eu), L.ptr(ev), L.ptr(ew),
+               L.ptr(in_tree), L.ptr(comp), float(gamma), C.byref(self._h), L.stream())
+        a, b, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        L.call("hdp_forest_stats", self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
+        self.n_trees, self.n_paths, self.n_phases, self.max_depth = a.value, b.value, c.value, d.value
+        self.total_entries = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                L.load().hdp_forest_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
+
+    def export(self):
+        torch = _t()
+        dev = L.device()
+        o = {k: torch.empty(self.n, dtype=torch.int32, device=dev)
+             for k in ("parent", "depth", "tree_id", "size", "root")}
+        o["parent_weight"] = torch.empty(self.n, dtype=torch.float32, device=dev)
+        L.call("hdp_forest_export", self._h, L.ptr(o["parent"]), L.ptr(o["depth"]),
+               L.ptr(o["tree_id"]), L.ptr(o["size"]), L.ptr(o["parent_weight"]),
+               L.ptr(o["root"]), L.stream())
+        return o
+
+    def set_lanes_range(self, x0: int, nx: int):
+        L.call("hdp_forest_set_lanes_range", self._h, int(x0), int(nx), L.stream())
+        self._entries()
+
+    def set_lanes(self, tree_masks):
+        """tree_masks: (n_trees, nw) int32/uint32 bitsets on the device."""
+        L.call("hdp_forest_set_lanes", self._h, L.ptr(tree_masks), tree_masks.shape[1], L.stream())
+        self._entries()
+
+    def _entries(self):
+        t = C.c_int64()
+        L.call("hdp_forest_entries", self._h, C.byref(t), None, L.stream())
+        self.total_entries = t.value
+
+    def node_offsets(self):
+        torch = _t()
+        off = torch.empty(self.n + 1, dtype=torch.int64, device=L.device())
+        L.call("hdp_forest_entries", self._h, None, L.ptr(off), L.stream())
+        off[self.n] = self.total_entries
+        return off
+
+    def aggregate(self, lev: Level | None = None, cost: CostConsts = CostConsts(),
+                  cost_rows=None, want_volume=False, want_keys=False):
+        """Fused cost + two-pass aggregation + WTA.  Returns
+        (disp int32 (n), min_cost f32 (n), keys u64-as-int64 (n) | None,
+        volume f32 (total_entries) | None)."""
+        torch = _t()
+        dev = L.device()
+        disp = torch.empty(self.n, dtype=torch.int32, device=dev)
+        mc = torch.empty(self.n, dtype=torch.float32, device=dev)
+        keys = torch.empty(self.n, dtype=torch.int64, device=dev) if want_keys else None
+        vol = (torch.empty(max(self.total_entries, 1), dtype=torch.float32, device=dev)
+               if want_volume else None)
+        if lev is not None:
+            args = (L.ptr(lev.packed_l), L.ptr(lev.packed_r), lev.h, lev.w, lev.c)
+        else:
+            args = (None, None, 0, 0, 3)
+        L.call("hdp_aggregate_wta", self._h, *args, cost.alpha, cost.tau_color, cost.tau_grad,
+               L.ptr(cost_rows), L.ptr(disp), L.ptr(mc), L.ptr(keys), L.ptr(vol), L.stream())
+        return disp, mc, keys, vol
+
+
+def keys_unpack(keys):
+    torch = _t()
+    n = keys.numel()
+    disp = torch.empty(n, dtype=torch.int32, device=keys.device)
+    mc = torch.empty(n, dtype=torch.float32, device=keys.device)
+    L.call("hdp_keys_unpack", L.ptr(keys), n, L.ptr(disp), L.ptr(mc), L.stream())
+    return disp, mc
+
+
+# ------------------------------------------------------------------ tables
+def nwords32(d_max: int) -> int:
+    return (d_max + 1 + 31) // 32
+
+
+def mixture_density(weights, means, sigmas, x):
+    """Mixture1D.density (hdp_model.py:67-72), same numpy expression."""
+    x = np.asarray(x, dtype=np.float64)
+    z = (x[..., None] - means) / sigmas
+    comp = np.exp(-0.5 * z * z) / (sigmas * np.sqrt(2.0 * np.pi))
+    return comp @ weights
+
+
+def conditional_matrix(mix, d_child, d_parent, s):
+    """conditional_parent_given_child (hdp_model.py:320-331)."""
+    from .errors import InternalError
+
+    i = np.arange(d_parent + 1)
+    j = np.arange(d_child + 1)
+    dens = mixture_density(mix.weights, mix.means, mix.sigmas, i[:, None] - (j // s)[None, :])
+    col_sum = dens.sum(axis=0)
+    if np.any(col_sum <= 0):
+        raise InternalError("conditional column vanished; mixture degenerated")
+    return dens / col_sum
+
+
+def bayes_batched(cond, priors):
+    """bayes_child_given_parent (hdp_model.py:334-363) for B priors at once.
+    Returns (matrix (B, rows, cols), number of dead rows per pair)."""
+    joint = cond[None, :, :] * priors[:, None, :]
+    row_sum = joint.sum(axis=2, keepdims=True)
+    dead = row_sum[:, :, 0] <= 0.0
+    n_dead = dead.sum(axis=1)
+    if np.any(dead):
+        joint[dead] = 1.0
+        row_sum = joint.sum(axis=2, keepdims=True)
+    return joint / row_sum, n_dead
+
+
+def predict_masks(bayes, delta: float):
+    """predict_intervals (hdp_model.py:498-525), vectorised but in the same
+    arithmetic: descending stable order, running mass c accumulated left to
+    right (np.cumsum is sequential), stop at the first P/(c+P) < delta.
+    Returns chosen (B, rows, cols) bool over disparities."""
+    order = np.argsort(-bayes, axis=-1, kind="stable")
+    p = np.take_along_axis(bayes, order, axis=-1)
+    csum = np.cumsum(p, axis=-1)
+    ratio = p[..., 1:] / (csum[..., :-1] + p[..., 1:])
+    fail = ratio < delta
+    first_fail = np.where(fail.any(axis=-1), fail.argmax(axis=-1), fail.shape[-1])
+    k = first_fail + 1  # number of chosen candidates
+    ranks = np.arange(bayes.shape[-1])
+    chosen_sorted = ranks[None, None, :] < k[..., None]
+    chosen = np.zeros_like(chosen_sorted)
+    np.put_along_axis(chosen, order, chosen_sorted, axis=-1)
+    return chosen
+
+
+def pack_masks(chosen) -> np.ndarray:
+    """(…, d+1) bool -> (…, nw) uint32 bitsets."""
+    d1 = chosen.shape[-1]
+    nw = (d1 + 31) // 32
+    pad = np.zeros(chosen.shape[:-1] + (nw * 32,), bool)
+    pad[..., :d1] = chosen
+    bits = pad.reshape(chosen.shape[:-1] + (nw, 32)).astype(np.uint64)
+    weights = (np.uint64(1) << np.arange(32, dtype=np.uint64))
+    return (bits * weights).sum(axis=-1).astype(np.uint32)
+
+
+def prior_counts(lev: Level, stride=5, window=7, max_offset=1, cost: CostConsts = CostConsts()):
+    torch = _t()
+    b = lev.img_l.shape[0]
+    dev = lev.img_l.device
+    counts = torch.empty((b, lev.d_max + 1), dtype=torch.int64, device=dev)
+    kept = torch.empty(b, dtype=torch.int64, device=dev)
+    L.call("hdp_prior_counts", L.ptr(lev.unit_l), L.ptr(lev.grad_l), L.ptr(lev.unit_r),
+           L.ptr(lev.grad_r), b, lev.h, lev.w, lev.c, lev.d_max, stride, window, max_offset,
+           cost.alpha, cost.tau_color, cost.tau_grad, L.ptr(counts), L.ptr(kept), L.stream())
+    return counts, kept
+
+
+def priors_from_counts(counts: np.ndarray, kept: np.ndarray) -> np.ndarray:
+    """hdp_model.py:465-470 per pair."""
+    b, d1 = counts.shape
+    out = np.empty((b, d1))
+    for i in range(b):
+        if kept[i] == 0:
+            out[i] = np.full(d1, 1.0 / d1)
+        else:
+            hist = counts[i].astype(np.float64) + 1.0
+            out[i] = hist / hist.sum()
+    return out
+
+
+def assign_rows(parent_disp, h: int, w: int, s: int, n_rows: int):
+    torch = _t()
+    b, ph, pw = parent_disp.shape
+    rows = torch.empty(b * h * w, dtype=torch.int32, device=parent_disp.device)
+    L.call("hdp_assign_rows", L.ptr(parent_disp), b, ph, pw, h, w, s, n_rows, L.ptr(rows),
+           L.stream())
+    return rows
+
+
+def hdpf(batch, npp, epp, eu, ev, key, pixel_row, row_masks, beta: float):
+    torch = _t()
+    dev = eu.device
+    n = batch * npp
+    nw = row_masks.shape[-1]
+    n_rows = row_masks.shape[1]
+    in_tree = torch.empty(max(eu.numel(), 1), dtype=torch.uint8, device=dev)
+    comp = torch.empty(n, dtype=torch.int32, device=dev)
+    tmasks = torch.empty((n, nw), dtype=torch.int32, device=dev)
+    rounds = C.c_int(0)
+    L.call("hdp_hdpf", batch, npp, epp, L.ptr(eu), L.ptr(ev), L.ptr(key), L.ptr(pixel_row),
+           L.ptr(row_masks), n_rows, nw, float(beta), L.ptr(in_tree), L.ptr(comp), L.ptr(tmasks),
+           C.byref(rounds), L.stream())
+    return in_tree[: eu.numel()], comp, tmasks, rounds.value
+
+
+# --------------------------------------------------------------- pipelines
+@dataclass
+class LevelOut:
+    level: int
+    h: int
+    w: int
+    d_max: int
+    disparity: object  # (B, h, w) int32 device
+    min_cost: object  # (B, h, w) f32 device
+    n_trees: np.ndarray  # (B,)
+    stored_entries: np.ndarray  # (B,)
+    search_ratio: np.ndarray  # (B,) float
+    timings: dict = field(default_factory=dict)
+    forest: object = None
+    extra: dict = field(default_factory=dict)
+
+
+def _per_pair_stats(f: DeviceForest, batch: int, npp: int, d_max: int):
+    torch = _t()
+    off = f.node_offsets()
+    o = f.export()
+    idx = torch.arange(batch + 1, device=off.device, dtype=torch.int64) * npp
+    stored = (off[idx[1:]] - off[idx[:-1]]).cpu().numpy()
+    tid = torch.cat([o["tree_id"].to(torch.int64), torch.tensor([f.n_trees], device=off.device)])
+    ntrees = (tid[idx[1:]] - tid[idx[:-1]]).cpu().numpy()
+    # DisparityForest.search_ratio: mean interval size over pixels / (d+1)
+    ratio = np.array([float(s) / npp / (d_max + 1) for s in stored])
+    return ntrees, stored, ratio
+
+
+class _Clock:
+    def __init__(self, on: bool):
+        self.on = on
+        self.acc: dict = {}
+
+    def lap(self, key, t0):
+        if not self.on:
+            return time.perf_counter()
+        L.torch_mod().cuda.synchronize()
+        t1 = time.perf_counter()
+        self.acc[key] = self.acc.get(key, 0.0) + (t1 - t0)
+        return t1
+
+
+def _forest_layer(lev: Level, eu, ev, ew, in_tree, comp, gamma, cost, masks=None,
+                  x0=0, nx=None, want_volume=False, want_keys=False, clock=None, t0=None):
+    f = DeviceForest(lev.img_l.shape[0] * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
+    if masks is None:
+        f.set_lanes_range(x0, lev.d_max + 1 if nx is None else nx)
+    else:
+        f.set_lanes(masks)
+    if clock is not None:
+        t0 = clock.lap("forest", t0)
+    disp, mc, keys, vol = f.aggregate(lev, cost, want_volume=want_volume, want_keys=want_keys)
+    if clock is not None:
+        clock.lap("cost_aggregate", t0)
+    return f, disp, mc, keys, vol
+
+
+def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
+                       cost: CostConsts = CostConsts(), tree_kind: str = "mst", seed: int = 0,
+                       x0: int = 0, nx: int | None = None, want_volume=False, want_keys=False,
+                       keep_forest=False, timing=False) -> LevelOut:
+    """Full-range aggregation over one MST per pair (aggregation.py:274-358).
+    left/right: (B, H, W, C) uint8 device tensors.  [x0, x0+nx) restricts the
+    disparity lanes (a slab of the multi-GPU split); default full range."""
+    if tree_kind not in ("mst", "rt"):
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    if d_max < 1:
+        raise ConfigError(f"d_max must be >= 1, got {d_max}")
+    clock = _Clock(timing)
+    t0 = time.perf_counter()
+    b, h, w, c = left_u8.shape
+    il, ir = to_f64(left_u8), to_f64(right_u8)
+    _, _, _, pl = prepare(il, False)
+    _, _, _, pr = prepare(ir, False)
+    lev = Level(0, h, w, c, d_max, il, ir, pl, pr)
+    eu, ev, ew, key, E = grid_edges(il)
+    if tree_kind == "rt":
+        key = rt_keys(E, b, seed, il.device)
+    in_tree, comp, _ = mst(b * h * w, eu, ev, key)
+    f, disp, mc, keys, vol = _forest_layer(lev, eu, ev, ew, in_tree, comp, gamma, cost, None, x0,
+                                           nx, want_volume, want_keys, clock, t0)
+    ntrees, stored, ratio = _per_pair_stats(f, b, h * w, d_max)
+    out = LevelOut(0, h, w, d_max, disp.view(b, h, w), mc.view(b, h, w), ntrees, stored, ratio,
+                   dict(clock.acc), f if keep_forest else None)
+    out.extra["keys"] = keys
+    out.extra["volume"] = vol
+    return out
+
+
+def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_size: int = 2,
+                  gamma: float = 0.1, delta0: float = 0.064, beta: float = 0.6,
+                  cost: CostConsts = CostConsts(), tree_kind: str = "mst", seed: int = 0,
+                  teacher: dict | None = None, keep=False, want_volume=False, timing=False,
+                  on_level=None) -> list[LevelOut]:
+    """Coarse-to-fine HDP matching for B pairs (aggregation.py:367-488).
+
+    `model` exposes .layers[l] with .weights/.means/.sigmas (GmmModel).
+    `teacher`: optional {level: (B, h_l, w_l) int32 device map} handed to the
+    next finer level instead of this level's own result (teacher forcing)."""
+    torch = _t()
+    if tree_kind not in ("mst", "rt"):
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    if len(model.layers) < levels:
+        raise DataError(f"model covers {len(model.layers)} level transitions, run needs {levels}")
+    if d_max // block_size**levels < 1:
+        raise ConfigError(f"d_max={d_max} collapses to {d_max // block_size**levels} after "
+                          f"{levels} levels of /{block_size}; reduce levels or block_size")
+    clock = _Clock(timing)
+    t0 = time.perf_counter()
+    b = left_u8.shape[0]
+    lv = build_levels(left_u8, right_u8, d_max, levels, block_size, True)
+    t0 = clock.lap("pyramid", t0)
+    outs: list[LevelOut] = []
+
+    def finish(lev, f, disp, mc, vol, stage):
+        ntrees, stored, ratio = _per_pair_stats(f, b, lev.h * lev.w, lev.d_max)
+        o = LevelOut(lev.level, lev.h, lev.w, lev.d_max, disp.view(b, lev.h, lev.w),
+                     mc.view(b, lev.h, lev.w), ntrees, stored, ratio, stage,
+                     f if keep else None)
+        o.extra["volume"] = vol
+        outs.append(o)
+        if on_level is not None:
+            on_level(o)
+        return o
+
+    top = lv[levels]
+    eu, ev, ew, key, E = grid_edges(top.img_l)
+    if tree_kind == "rt":
+        key = rt_keys(E, b, seed, top.img_l.device)
+    in_tree, comp, _ = mst(b * top.h * top.w, eu, ev, key)
+    lclock = _Clock(timing)
+    f, disp, mc, _, vol = _forest_layer(top, eu, ev, ew, in_tree, comp, gamma, cost, None,
+                                        want_volume=want_volume, clock=lclock, t0=t0)
+    o = finish(top, f, disp, mc, vol, dict(lclock.acc))
+    parent = o.disparity if teacher is None or levels not in teacher else teacher[levels]
+    for level in range(levels - 1, -1, -1):
+        lev = lv[level]
+        t0 = time.perf_counter()
+        lclock = _Clock(timing)
+        counts, kept = prior_counts(lev, cost=cost)
+        counts_h, kept_h = counts.cpu().numpy(), kept.cpu().numpy()
+        priors = priors_from_counts(counts_h, kept_h)
+        cond = conditional_matrix(model.layers[level], lev.d_max, lv[level + 1].d_max, block_size)
+        bm, _ = bayes_batched(cond, priors)
+        chosen = predict_masks(bm, delta0 * block_size**level)
+        row_masks = torch.from_numpy(pack_masks(chosen).view(np.int32)).to(lev.img_l.device)
+        rows = assign_rows(parent.contiguous(), lev.h, lev.w, block_size, chosen.shape[1])
+        t0 = lclock.lap("predict", t0)
+        eu, ev, ew, key, E = grid_edges(lev.img_l)
+        if tree_kind == "rt":
+            key = rt_keys(E, b, seed, lev.img_l.device)
+        in_tree, comp, tmasks, rounds = hdpf(b, lev.h * lev.w, E, eu, ev, key, rows,
+                                             row_masks.contiguous(), beta)
+        fo = DeviceForest(b * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
+        roots = fo.export()["root"]
+        ar = torch.arange(fo.n, device=roots.device, dtype=torch.int32)
+        root_ids = torch.nonzero(roots == ar).flatten()
+        fo.set_lanes(tmasks[root_ids].contiguous())
+        t0 = lclock.lap("forest", t0)
+        disp, mc, _, vol = fo.aggregate(lev, cost, want_volume=want_volume)
+        lclock.lap("cost_aggregate", t0)
+        o = finish(lev, fo, disp, mc, vol, dict(lclock.acc))
+        o.extra.update(counts=counts_h, kept=kept_h, chosen=chosen if keep else None,
+                       dr_rounds=rounds)
+        parent = o.disparity if teacher is None or level not in teacher else teacher[level]
+    return outs
