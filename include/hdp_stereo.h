@@ -42,6 +42,8 @@ extern "C" {
 #define HDP_ABI_VERSION 1
 
 int hdp_abi_version(void);
+/* Number of kernels this library has launched in the process (diagnostic). */
+int64_t hdp_launch_count(void);
 /* Message for the last non-OK status on the calling thread. */
 const char *hdp_last_error(void);
 

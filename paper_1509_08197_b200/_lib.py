@@ -26,6 +26,7 @@ _D = C.c_double
 SIGNATURES = {
     "hdp_abi_version": (_I, []),
     "hdp_last_error": (C.c_char_p, []),
+    "hdp_launch_count": (_I64, []),
     "hdp_u8_to_f64": (_I, [_P, _P, _I64, _P]),
     "hdp_block_mean": (_I, [_P, _P, _I, _I, _I, _I, _I, _P]),
     "hdp_prepare": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),

@@ -45,6 +45,15 @@ struct Status {
         if (_s != HDP_OK) return _s;                                                 \
     } while (0)
 
+// Keep freed pool blocks cached across stream synchronisations (the default
+// release threshold of 0 would hand every block back to the driver at each
+// sync and re-map it on the next allocation).
+void keep_pool_memory();
+
+// Process-wide count of this library's kernel launches (diagnostics for the
+// bench's gpu_launches claim; CUB launches are not counted).
+void note_launch();
+
 // Stream-ordered device scratch (cudaMallocAsync from the device's default
 // pool, which caches freed blocks, so steady-state calls do not hit the
 // driver allocator).
@@ -64,6 +73,7 @@ struct DevBuf {
     }
     int alloc(size_t count, cudaStream_t stream) {
         release();
+        keep_pool_memory();
         s = stream;
         n = count;
         if (count == 0) return HDP_OK;

@@ -55,7 +55,13 @@ __global__ void k_fill_int(int64_t n, int32_t* a, int32_t v) {
 
 __global__ void k_min_root(int64_t n, const int32_t* __restrict__ comp, int32_t* minid) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < n) atomicMin(&minid[comp[v]], (int32_t)v);
+    bool ok = v < n;
+    int32_t c = ok ? comp[v] : -1;
+    // lanes of a warp mostly share a component: one atomic per distinct label
+    unsigned peers = __match_any_sync(0xffffffffu, c);
+    int32_t mn = __reduce_min_sync(peers, ok ? (int32_t)v : INT_MAX);
+    int leader = __ffs(peers) - 1;
+    if (ok && (int)(threadIdx.x & 31) == leader) atomicMin(&minid[c], mn);
 }
 
 __global__ void k_root_flags(int64_t n, const int32_t* __restrict__ comp,
@@ -270,13 +276,14 @@ __global__ void k_light_steps(int64_t na, const int32_t* __restrict__ asrc,
 __global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
                               const int32_t* __restrict__ lscan, const int32_t* __restrict__ head,
                               const int32_t* __restrict__ dist, uint64_t* key, int32_t* idx,
-                              int32_t* ld_out) {
+                              int32_t* ld_out, int hbits, int dbits) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     int32_t a = down_arc[v];
     int32_t ld = a >= 0 ? lscan[a] : 0;
     ld_out[v] = ld;
-    key[v] = ((uint64_t)ld << 56) | ((uint64_t)(uint32_t)head[v] << 24) | (uint64_t)dist[v];
+    key[v] = ((uint64_t)ld << (hbits + dbits)) | ((uint64_t)(uint32_t)head[v] << dbits) |
+             (uint64_t)dist[v];
     idx[v] = (int32_t)v;
 }
 
@@ -310,7 +317,7 @@ __global__ void k_path_info(int64_t np, int64_t n, const int32_t* __restrict__ p
                             const int32_t* __restrict__ lnode, const int32_t* __restrict__ parent,
                             const int32_t* __restrict__ lpos, const int32_t* __restrict__ tree_id,
                             const int32_t* __restrict__ ld, int32_t* p_len, int32_t* p_par,
-                            int32_t* p_tree, int32_t* phase_cnt) {
+                            int32_t* p_tree, int32_t* p_ld, int32_t* is_long) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
     int32_t s = p_start[i];
@@ -319,7 +326,28 @@ __global__ void k_path_info(int64_t np, int64_t n, const int32_t* __restrict__ p
     p_len[i] = e - s;
     p_par[i] = parent[h] == h ? -1 : lpos[parent[h]];
     p_tree[i] = tree_id[h];
-    atomicAdd(&phase_cnt[ld[h]], 1);
+    p_ld[i] = ld[h];
+    is_long[i] = (e - s) >= 2 ? 1 : 0;
+}
+
+// first path index of every phase (paths are phase-major)
+__global__ void k_phase_bounds(int64_t np, const int32_t* __restrict__ p_ld, int nph,
+                               int32_t* first) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > np) return;
+    int a = (i == 0) ? -1 : p_ld[i - 1];
+    int b = (i == np) ? nph : p_ld[i];
+    for (int r = a + 1; r <= b; r++) first[r] = (int32_t)i;
+}
+
+__global__ void k_split_paths(int64_t np, const int32_t* __restrict__ is_long,
+                              const int32_t* __restrict__ lpos_excl, int32_t* long_paths,
+                              int32_t* short_paths) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    int32_t l = lpos_excl[i];
+    if (is_long[i]) long_paths[l] = (int32_t)i;
+    else short_paths[i - l] = (int32_t)i;
 }
 
 // light children of the node at layout position k, ascending id
@@ -419,7 +447,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(fpos.alloc(m_in + 1, st));
     int64_t m = 0;
     if (m_in > 0) {
-        k_flag_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, in_tree, flags.get());
+        k_flag_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, in_tree, flags.get()); note_launch();
         HDP_TRY(exclusive_sum(flags.get(), fpos.get(), m_in, st));
         int32_t last_pos = 0, last_flag = 0;
         HDP_TRY(to_host(&last_pos, fpos.get() + m_in - 1, 1, st));
@@ -437,7 +465,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(tkey.alloc(m + 1, st));
     if (m_in > 0)
         k_compact_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, flags.get(), fpos.get(), eu, ev, ew,
-                                                        tu.get(), tv.get(), tw.get(), tkey.get());
+                                                        tu.get(), tv.get(), tw.get(), tkey.get()); note_launch();
     flags.release();
     fpos.release();
 
@@ -459,10 +487,10 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(tindex.alloc(n, st));
     HDP_TRY(f->root.alloc(n, st));
     HDP_TRY(f->tree_id.alloc(n, st));
-    k_fill_int<<<grid_for(n, B), B, 0, st>>>(n, minid.get(), INT_MAX);
-    k_min_root<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get());
+    k_fill_int<<<grid_for(n, B), B, 0, st>>>(n, minid.get(), INT_MAX); note_launch();
+    k_min_root<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get()); note_launch();
     k_root_flags<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get(), f->root.get(),
-                                              is_root.get());
+                                              is_root.get()); note_launch();
     HDP_TRY(exclusive_sum(is_root.get(), tindex.get(), n, st));
     {
         int32_t a = 0, b = 0;
@@ -470,7 +498,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         HDP_TRY(to_host(&b, is_root.get() + n - 1, 1, st));
         f->n_trees = (int64_t)a + b;
     }
-    k_tree_ids<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), tindex.get(), f->tree_id.get());
+    k_tree_ids<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), tindex.get(), f->tree_id.get()); note_launch();
     HDP_CHECK_LAUNCH();
     comp.release();
     minid.release();
@@ -490,7 +518,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_CHECK_CUDA(cudaMemsetAsync(deg.get(), 0, (n + 1) * sizeof(int32_t), st));
     if (m > 0) {
         k_make_arcs<<<grid_for(m, B), B, 0, st>>>(m, tu.get(), tv.get(), tw.get(), akey.get(),
-                                                 aw.get(), deg.get());
+                                                 aw.get(), deg.get()); note_launch();
         HDP_TRY(sort_pairs(akey.get(), akey2.get(), aw.get(), aw2.get(), na, 0,
                            32 + bits_for(n), st));
     }
@@ -502,7 +530,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     aw.release();
     HDP_TRY(asrc.alloc(na + 1, st));
     HDP_TRY(adst.alloc(na + 1, st));
-    if (na > 0) k_arc_unpack<<<grid_for(na, B), B, 0, st>>>(na, akey2.get(), asrc.get(), adst.get());
+    if (na > 0) k_arc_unpack<<<grid_for(na, B), B, 0, st>>>(na, akey2.get(), asrc.get(), adst.get()); note_launch();
     akey2.release();
 
     // ---- 4. Euler tour + list ranking
@@ -518,23 +546,23 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_CHECK_CUDA(cudaMemsetAsync(tlen.get(), 0, (f->n_trees + 1) * sizeof(int32_t), st));
     if (na > 0) {
         k_tour_next<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), adj_start.get(),
-                                                  f->root.get(), twin.get(), nxt.get());
-        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, rank.get());
+                                                  f->root.get(), twin.get(), nxt.get()); note_launch();
+        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, rank.get()); note_launch();
         int rounds = ceil_log2(na + 1);
         for (int r = 0; r < rounds; r++) {
             k_rank_jump<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), rank.get(), nxt2.get(),
-                                                      rank2.get());
+                                                      rank2.get()); note_launch();
             std::swap(nxt.p, nxt2.p);
             std::swap(rank.p, rank2.p);
         }
         HDP_CHECK_LAUNCH();
     }
     k_tour_len<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), f->root.get(), f->tree_id.get(),
-                                             rank.get(), tlen.get());
+                                             rank.get(), tlen.get()); note_launch();
     HDP_TRY(exclusive_sum(tlen.get(), toff.get(), f->n_trees + 1, st));
     if (na > 0)
         k_tour_pos<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), f->tree_id.get(), tlen.get(),
-                                                 rank.get(), tpos.get());
+                                                 rank.get(), tpos.get()); note_launch();
     nxt.release();
     nxt2.release();
     rank.release();
@@ -551,14 +579,14 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(scanned.alloc(na + 1, st));
     k_root_init<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), f->tree_id.get(), tlen.get(),
                                               f->parent.get(), f->pweight.get(), f->size.get(),
-                                              f->depth.get(), down_arc.get());
+                                              f->depth.get(), down_arc.get()); note_launch();
     if (na > 0) {
         k_orient<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), aw2.get(), twin.get(),
                                                tpos.get(), f->tree_id.get(), toff.get(),
                                                f->parent.get(), f->pweight.get(), f->size.get(),
-                                               down_arc.get(), steps.get());
+                                               down_arc.get(), steps.get()); note_launch();
         HDP_TRY(inclusive_sum(steps.get(), scanned.get(), na, st));
-        k_depth_gather<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), f->depth.get());
+        k_depth_gather<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), f->depth.get()); note_launch();
     }
     HDP_CHECK_LAUNCH();
     {
@@ -580,12 +608,12 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(dist.alloc(n, st));
     HDP_TRY(dist2.alloc(n, st));
     k_heavy<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), adst.get(), f->parent.get(),
-                                          f->size.get(), heavy.get());
-    k_hp_init<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), hp.get(), dist.get());
+                                          f->size.get(), heavy.get()); note_launch();
+    k_hp_init<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), hp.get(), dist.get()); note_launch();
     {
         int rounds = ceil_log2(f->max_depth + 2);
         for (int r = 0; r < rounds; r++) {
-            k_hp_jump<<<grid_for(n, B), B, 0, st>>>(n, hp.get(), dist.get(), hp2.get(), dist2.get());
+            k_hp_jump<<<grid_for(n, B), B, 0, st>>>(n, hp.get(), dist.get(), hp2.get(), dist2.get()); note_launch();
             std::swap(hp.p, hp2.p);
             std::swap(dist.p, dist2.p);
         }
@@ -602,7 +630,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     if (na > 0) {
         k_light_steps<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), f->parent.get(),
                                                     head, tpos.get(), f->tree_id.get(), toff.get(),
-                                                    steps.get());
+                                                    steps.get()); note_launch();
         HDP_TRY(inclusive_sum(steps.get(), scanned.get(), na, st));
     }
     DevBuf<uint64_t> lkey, lkey2;
@@ -611,10 +639,12 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(lkey2.alloc(n, st));
     HDP_TRY(lidx.alloc(n, st));
     HDP_TRY(f->lnode.alloc(n, st));
+    int dbits = bits_for(f->max_depth + 1), hbits = bits_for(n);
     k_layout_keys<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), head, dist.get(),
-                                                lkey.get(), lidx.get(), ld.get());
+                                                lkey.get(), lidx.get(), ld.get(), hbits, dbits); note_launch();
     HDP_CHECK_LAUNCH();
-    HDP_TRY(sort_pairs(lkey.get(), lkey2.get(), lidx.get(), f->lnode.get(), n, 0, 64, st));
+    HDP_TRY(sort_pairs(lkey.get(), lkey2.get(), lidx.get(), f->lnode.get(), n, 0,
+                       std::min(64, dbits + hbits + 8), st));
     lkey.release();
     lkey2.release();
     lidx.release();
@@ -628,13 +658,13 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(f->lpos.alloc(n, st));
     HDP_TRY(f->lsim.alloc(n, st));
     k_layout_pos<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), f->pweight.get(), f->gamma,
-                                               f->lpos.get(), f->lsim.get());
+                                               f->lpos.get(), f->lsim.get()); note_launch();
 
     // ---- 8. paths and phases
     DevBuf<int32_t> pflag, pidx;
     HDP_TRY(pflag.alloc(n, st));
     HDP_TRY(pidx.alloc(n, st));
-    k_path_flags<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), head, pflag.get());
+    k_path_flags<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), head, pflag.get()); note_launch();
     HDP_TRY(exclusive_sum(pflag.get(), pidx.get(), n, st));
     {
         int32_t a = 0, b = 0;
@@ -646,25 +676,49 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(f->p_len.alloc(f->n_paths, st));
     HDP_TRY(f->p_par.alloc(f->n_paths, st));
     HDP_TRY(f->p_tree.alloc(f->n_paths, st));
-    k_path_fill<<<grid_for(n, B), B, 0, st>>>(n, pflag.get(), pidx.get(), f->p_start.get());
-    const int MAXPH = 256;
-    DevBuf<int32_t> phase_cnt;
-    HDP_TRY(phase_cnt.alloc(MAXPH, st));
-    HDP_CHECK_CUDA(cudaMemsetAsync(phase_cnt.get(), 0, MAXPH * sizeof(int32_t), st));
+    k_path_fill<<<grid_for(n, B), B, 0, st>>>(n, pflag.get(), pidx.get(), f->p_start.get()); note_launch();
+    DevBuf<int32_t> p_ld, is_long, lexcl, first;
+    HDP_TRY(p_ld.alloc(f->n_paths + 1, st));
+    HDP_TRY(is_long.alloc(f->n_paths + 1, st));
+    HDP_TRY(lexcl.alloc(f->n_paths + 1, st));
     k_path_info<<<grid_for(f->n_paths, B), B, 0, st>>>(
         f->n_paths, n, f->p_start.get(), f->lnode.get(), f->parent.get(), f->lpos.get(),
-        f->tree_id.get(), ld.get(), f->p_len.get(), f->p_par.get(), f->p_tree.get(),
-        phase_cnt.get());
+        f->tree_id.get(), ld.get(), f->p_len.get(), f->p_par.get(), f->p_tree.get(), p_ld.get(),
+        is_long.get()); note_launch();
     HDP_CHECK_LAUNCH();
     {
-        std::vector<int32_t> cnt(MAXPH);
-        HDP_TRY(to_host(cnt.data(), phase_cnt.get(), MAXPH, st));
-        int last = 0;
-        for (int r = 0; r < MAXPH; r++)
-            if (cnt[r]) last = r;
-        f->n_phases = last + 1;
-        f->phase_off.assign(f->n_phases + 1, 0);
-        for (int r = 0; r < f->n_phases; r++) f->phase_off[r + 1] = f->phase_off[r] + cnt[r];
+        int32_t last_ld = 0;
+        HDP_TRY(to_host(&last_ld, p_ld.get() + f->n_paths - 1, 1, st));
+        f->n_phases = last_ld + 1;
+        HDP_TRY(first.alloc(f->n_phases + 1, st));
+        k_phase_bounds<<<grid_for(f->n_paths + 1, B), B, 0, st>>>(f->n_paths, p_ld.get(),
+                                                                  (int)f->n_phases, first.get()); note_launch();
+        HDP_CHECK_CUDA(cudaMemsetAsync(is_long.get() + f->n_paths, 0, sizeof(int32_t), st));
+        HDP_TRY(exclusive_sum(is_long.get(), lexcl.get(), f->n_paths + 1, st));
+        std::vector<int32_t> fh(f->n_phases + 1);
+        HDP_TRY(to_host(fh.data(), first.get(), f->n_phases + 1, st));
+        f->phase_off.assign(fh.begin(), fh.end());
+        // layout node ranges and long/short split offsets per phase
+        f->phase_node.assign(f->n_phases + 1, n);
+        f->long_off.assign(f->n_phases + 1, 0);
+        f->short_off.assign(f->n_phases + 1, 0);
+        for (int64_t r = 0; r <= f->n_phases; r++) {
+            int64_t pi = f->phase_off[r];
+            int32_t v = 0;
+            if (pi < f->n_paths) {
+                HDP_TRY(to_host(&v, f->p_start.get() + pi, 1, st));
+                f->phase_node[r] = v;
+            }
+            HDP_TRY(to_host(&v, lexcl.get() + pi, 1, st));
+            f->long_off[r] = v;
+            f->short_off[r] = pi - v;
+        }
+        HDP_TRY(f->long_paths.alloc(f->long_off[f->n_phases] + 1, st));
+        HDP_TRY(f->short_paths.alloc(f->short_off[f->n_phases] + 1, st));
+        k_split_paths<<<grid_for(f->n_paths, B), B, 0, st>>>(f->n_paths, is_long.get(), lexcl.get(),
+                                                             f->long_paths.get(),
+                                                             f->short_paths.get()); note_launch();
+        HDP_CHECK_LAUNCH();
     }
 
     // ---- 9. light-children CSR in layout order
@@ -673,14 +727,14 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(f->lc_start.alloc(n + 1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(lcc.get(), 0, (n + 1) * sizeof(int32_t), st));
     k_lc_count<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
-                                             f->parent.get(), head, lcc.get());
+                                             f->parent.get(), head, lcc.get()); note_launch();
     HDP_TRY(exclusive_sum(lcc.get(), f->lc_start.get(), n + 1, st));
     int32_t n_lc = 0;
     HDP_TRY(to_host(&n_lc, f->lc_start.get() + n, 1, st));
     HDP_TRY(f->lc_list.alloc(n_lc + 1, st));
     k_lc_fill<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
                                             f->parent.get(), head, f->lpos.get(),
-                                            f->lc_start.get(), f->lc_list.get());
+                                            f->lc_start.get(), f->lc_list.get()); note_launch();
     HDP_CHECK_LAUNCH();
     HDP_CHECK_CUDA(cudaStreamSynchronize(st));
     return HDP_OK;
@@ -696,10 +750,10 @@ static int lanes_finish(hdp_forest* f) {
     HDP_TRY(f->rowoff.alloc(n + 1, st));
     HDP_TRY(f->nodeoff.alloc(n + 1, st));
     k_row_m<<<grid_for(n + 1, B), B, 0, st>>>(n, f->lnode.get(), f->tree_id.get(), f->t_m.get(),
-                                              rm.get());
+                                              rm.get()); note_launch();
     HDP_TRY(exclusive_sum(rm.get(), f->rowoff.get(), n + 1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(nm.get() + n, 0, sizeof(int64_t), st));
-    k_node_m<<<grid_for(n, B), B, 0, st>>>(n, f->tree_id.get(), f->t_m.get(), nm.get());
+    k_node_m<<<grid_for(n, B), B, 0, st>>>(n, f->tree_id.get(), f->t_m.get(), nm.get()); note_launch();
     HDP_TRY(exclusive_sum(nm.get(), f->nodeoff.get(), n + 1, st));
     HDP_CHECK_LAUNCH();
     HDP_TRY(to_host(&f->total_entries, f->rowoff.get() + n, 1, st));
@@ -772,8 +826,8 @@ int hdp_forest_set_lanes_range(hdp_forest* f, int x0, int nx, void* stream) {
     HDP_TRY(f->t_doff.alloc(f->n_trees, st));
     HDP_TRY(f->dlist.alloc(nx, st));
     k_lanes_range<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, nx, f->t_m.get(),
-                                                             f->t_doff.get());
-    k_iota<<<grid_for(nx, 256), 256, 0, st>>>(nx, f->dlist.get(), x0);
+                                                             f->t_doff.get()); note_launch();
+    k_iota<<<grid_for(nx, 256), 256, 0, st>>>(nx, f->dlist.get(), x0); note_launch();
     HDP_CHECK_LAUNCH();
     return lanes_finish(f);
 }
@@ -785,14 +839,14 @@ int hdp_forest_set_lanes(hdp_forest* f, const uint32_t* tree_masks, int nw, void
     cudaStream_t st = f->st;
     HDP_TRY(f->t_m.alloc(f->n_trees, st));
     HDP_TRY(f->t_doff.alloc(f->n_trees + 1, st));
-    k_lanes_count<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw, f->t_m.get());
+    k_lanes_count<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw, f->t_m.get()); note_launch();
     HDP_TRY(exclusive_sum(f->t_m.get(), f->t_doff.get(), f->n_trees, st));
     int32_t a = 0, b = 0;
     HDP_TRY(to_host(&a, f->t_doff.get() + f->n_trees - 1, 1, st));
     HDP_TRY(to_host(&b, f->t_m.get() + f->n_trees - 1, 1, st));
     HDP_TRY(f->dlist.alloc((size_t)a + b + 1, st));
     k_lanes_fill<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw,
-                                                            f->t_doff.get(), f->dlist.get());
+                                                            f->t_doff.get(), f->dlist.get()); note_launch();
     HDP_CHECK_LAUNCH();
     {
         DevBuf<int32_t> mn;

@@ -28,6 +28,11 @@ struct hdp_forest {
     // per heavy path (ordered by layout)
     hdp::DevBuf<int32_t> p_start, p_len, p_par, p_tree;
     std::vector<int64_t> phase_off;  // host: paths of phase r = [phase_off[r], phase_off[r+1])
+    std::vector<int64_t> phase_node;  // host: layout positions of phase r = [phase_node[r], phase_node[r+1])
+    // paths of length >= 2 (need a sequential scan) and single-node paths,
+    // each list phase-major; host offsets per phase
+    hdp::DevBuf<int32_t> long_paths, short_paths;
+    std::vector<int64_t> long_off, short_off;
 
     // disparity lanes per tree
     int lanes_set = 0;

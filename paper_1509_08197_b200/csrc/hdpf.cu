@@ -211,7 +211,7 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
     int64_t ms = 0;
     if (m > 0) {
         k_rule1<<<grid_for(m, B), B, 0, st>>>(m, eu, ev, key, pixel_row, row_masks, nodes_per_pair,
-                                              edges_per_pair, n_rows, nw, flag.get(), skey.get());
+                                              edges_per_pair, n_rows, nw, flag.get(), skey.get()); note_launch();
         HDP_TRY(exclusive_sum(flag.get(), pos.get(), m, st));
         int32_t a = 0, b2 = 0;
         HDP_TRY(to_host(&a, pos.get() + m - 1, 1, st));
@@ -225,12 +225,12 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
     HDP_TRY(seg.alloc(batch + 1, st));
     if (m > 0)
         k_select<<<grid_for(m, B), B, 0, st>>>(m, flag.get(), pos.get(), skey.get(), okey.get(),
-                                               oidx.get());
+                                               oidx.get()); note_launch();
     flag.release();
     pos.release();
     skey.release();
     HDP_TRY(sort_pairs(okey.get(), okey2.get(), oidx.get(), oidx2.get(), ms, 0, 63, st));
-    k_seg_bounds<<<grid_for(ms + 1, B), B, 0, st>>>(ms, okey2.get(), batch, seg.get());
+    k_seg_bounds<<<grid_for(ms + 1, B), B, 0, st>>>(ms, okey2.get(), batch, seg.get()); note_launch();
     HDP_TRY(uf.alloc(n, st));
     HDP_TRY(usz.alloc(n, st));
     HDP_TRY(tm.alloc(n * nw, st));
@@ -238,12 +238,12 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
     HDP_TRY(rounds.alloc(1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(rounds.get(), 0, sizeof(int), st));
     k_uf_init<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
-                                            uf.get(), usz.get(), tm.get(), res.get());
+                                            uf.get(), usz.get(), tm.get(), res.get()); note_launch();
     HDP_CHECK_LAUNCH();
     k_dr<<<batch, DR_THREADS, 0, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(),
-                                       res.get(), nw, beta, in_tree, rounds.get());
+                                       res.get(), nw, beta, in_tree, rounds.get()); note_launch();
     HDP_CHECK_LAUNCH();
-    k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks);
+    k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks); note_launch();
     HDP_CHECK_LAUNCH();
     if (rounds_out) HDP_TRY(to_host(rounds_out, rounds.get(), 1, st));
     return HDP_OK;

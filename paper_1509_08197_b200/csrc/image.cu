@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 
 #include "common.cuh"
 #include "prims.cuh"
@@ -13,6 +14,22 @@
 namespace hdp {
 
 static thread_local char g_err[1024] = "";
+
+void keep_pool_memory() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
     va_list ap;
@@ -215,11 +232,13 @@ extern "C" {
 
 int hdp_abi_version(void) { return HDP_ABI_VERSION; }
 
+int64_t hdp_launch_count(void) { return (int64_t)launch_count(); }
+
 const char* hdp_last_error(void) { return g_err; }
 
 int hdp_u8_to_f64(const uint8_t* src, double* dst, int64_t n, void* stream) {
     if (n <= 0) return HDP_OK;
-    k_u8_to_f64<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(src, dst, n);
+    k_u8_to_f64<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(src, dst, n); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }
@@ -233,10 +252,10 @@ int hdp_block_mean(const double* src, double* dst, int batch, int h, int w, int 
     DevBuf<double> rows;
     HDP_TRY(rows.alloc((size_t)batch * oh * w * c, st));
     int64_t n1 = (int64_t)batch * oh * w * c;
-    k_block_rows<<<grid_for(n1, 256), 256, 0, st>>>(src, rows.get(), batch, h, w, c, s, oh);
+    k_block_rows<<<grid_for(n1, 256), 256, 0, st>>>(src, rows.get(), batch, h, w, c, s, oh); note_launch();
     HDP_CHECK_LAUNCH();
     int64_t n2 = (int64_t)batch * oh * ow * c;
-    k_block_cols<<<grid_for(n2, 256), 256, 0, st>>>(rows.get(), dst, batch, h, w, c, s, oh, ow);
+    k_block_cols<<<grid_for(n2, 256), 256, 0, st>>>(rows.get(), dst, batch, h, w, c, s, oh, ow); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }
@@ -247,7 +266,7 @@ int hdp_prepare(const double* img, int batch, int h, int w, int c, double* unit,
     int64_t n = (int64_t)batch * h * w;
     if (n <= 0) return HDP_OK;
     k_prepare<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(img, batch, h, w, c, unit,
-                                                                   gray, grad, (float4*)packed);
+                                                                   gray, grad, (float4*)packed); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }
@@ -260,7 +279,7 @@ int hdp_cost_volume(const float* packed_l, const float* packed_r, int batch, int
     if (total <= 0) return HDP_OK;
     k_cost_volume<<<grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
         (const float4*)packed_l, (const float4*)packed_r, batch, h, w, c, xs, nx, alpha, tau_c,
-        tau_g, out);
+        tau_g, out); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }
@@ -272,7 +291,7 @@ int hdp_grid_edges(const double* img, int batch, int h, int w, int c, int32_t* e
     HDP_REQUIRE((int64_t)batch * n < ((int64_t)1 << 31), HDP_ERR_CONFIG, "too many nodes");
     if (batch * n <= 0) return HDP_OK;
     k_grid_edges<<<grid_for(batch * n, 256), 256, 0, (cudaStream_t)stream>>>(img, batch, h, w, c,
-                                                                             eu, ev, ew, key);
+                                                                             eu, ev, ew, key); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }
@@ -285,7 +304,7 @@ int hdp_argsort_u64(const uint64_t* keys, int64_t n, int32_t* perm, void* stream
     DevBuf<int32_t> idx;
     HDP_TRY(kout.alloc(n, st));
     HDP_TRY(idx.alloc(n, st));
-    k_iota32<<<grid_for(n, 256), 256, 0, st>>>(n, idx.get());
+    k_iota32<<<grid_for(n, 256), 256, 0, st>>>(n, idx.get()); note_launch();
     HDP_CHECK_LAUNCH();
     return sort_pairs(keys, kout.get(), idx.get(), perm, n, 0, 64, st);
 }
@@ -293,7 +312,7 @@ int hdp_argsort_u64(const uint64_t* keys, int64_t n, int32_t* perm, void* stream
 int hdp_keys_unpack(const uint64_t* keys, int64_t n, int32_t* disp, float* min_cost,
                     void* stream) {
     if (n <= 0) return HDP_OK;
-    k_keys_unpack<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(keys, n, disp, min_cost);
+    k_keys_unpack<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(keys, n, disp, min_cost); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

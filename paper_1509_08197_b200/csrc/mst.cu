@@ -102,7 +102,7 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
     HDP_TRY(hooks.alloc(1, st));
     int* h_hooks = nullptr;
     HDP_CHECK_CUDA(cudaMallocHost((void**)&h_hooks, sizeof(int)));
-    k_mst_init<<<grid_for(n, 256), 256, 0, st>>>(n, comp);
+    k_mst_init<<<grid_for(n, 256), 256, 0, st>>>(n, comp); note_launch();
     if (m > 0) {
         HDP_CHECK_CUDA(cudaMemsetAsync(alive.get(), 1, m, st));
         HDP_CHECK_CUDA(cudaMemsetAsync(in_tree, 0, m, st));
@@ -110,13 +110,13 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
     int rounds = 0;
     while (m > 0) {
         HDP_CHECK_CUDA(cudaMemsetAsync(hooks.get(), 0, sizeof(int), st));
-        k_mst_reset<<<grid_for(n, 256), 256, 0, st>>>(n, best.get(), win.get());
-        k_mst_offer<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get());
+        k_mst_reset<<<grid_for(n, 256), 256, 0, st>>>(n, best.get(), win.get()); note_launch();
+        k_mst_offer<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get()); note_launch();
         k_mst_win<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get(),
-                                                   win.get());
+                                                   win.get()); note_launch();
         k_mst_hook<<<grid_for(n, 256), 256, 0, st>>>(n, eu, ev, comp, win.get(), link.get(),
-                                                    in_tree, hooks.get());
-        k_mst_relabel<<<grid_for(n, 256), 256, 0, st>>>(n, comp, link.get());
+                                                    in_tree, hooks.get()); note_launch();
+        k_mst_relabel<<<grid_for(n, 256), 256, 0, st>>>(n, comp, link.get()); note_launch();
         HDP_CHECK_LAUNCH();
         HDP_CHECK_CUDA(cudaMemcpyAsync(h_hooks, hooks.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
         HDP_CHECK_CUDA(cudaStreamSynchronize(st));

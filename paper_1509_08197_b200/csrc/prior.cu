@@ -184,7 +184,7 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
     a.kept = (unsigned long long*)kept;
     int64_t warps = (int64_t)a.nrc * a.ncc * batch;
     if (warps == 0) return HDP_OK;
-    k_prior<<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch);
+    k_prior<<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }
@@ -200,7 +200,7 @@ extern "C" int hdp_assign_rows(const int32_t* parent_disp, int batch, int ph, in
     HDP_CHECK_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), st));
     int64_t n = (int64_t)batch * h * w;
     k_assign_rows<<<grid_for(n, 256), 256, 0, st>>>(parent_disp, batch, ph, pw, h, w, s, n_rows,
-                                                    pixel_row, bad.get());
+                                                    pixel_row, bad.get()); note_launch();
     HDP_CHECK_LAUNCH();
     int hb = 0;
     HDP_CHECK_CUDA(cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -386,7 +386,8 @@ class _Clock:
 
 
 def _forest_layer(lev: Level, eu, ev, ew, in_tree, comp, gamma, cost, masks=None,
-                  x0=0, nx=None, want_volume=False, want_keys=False, clock=None, t0=None):
+                  x0=0, nx=None, want_volume=False, want_keys=False, clock=None, t0=None,
+                  probe=None):
     f = DeviceForest(lev.img_l.shape[0] * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
     if masks is None:
         f.set_lanes_range(x0, lev.d_max + 1 if nx is None else nx)
@@ -394,7 +395,14 @@ def _forest_layer(lev: Level, eu, ev, ew, in_tree, comp, gamma, cost, masks=None
         f.set_lanes(masks)
     if clock is not None:
         t0 = clock.lap("forest", t0)
+    if probe is not None:  # CUDA events around the fused aggregation (bench roofline)
+        ev0 = _t().cuda.Event(enable_timing=True)
+        ev1 = _t().cuda.Event(enable_timing=True)
+        ev0.record()
     disp, mc, keys, vol = f.aggregate(lev, cost, want_volume=want_volume, want_keys=want_keys)
+    if probe is not None:
+        ev1.record()
+        probe.append((ev0, ev1, f.total_entries, f.n))
     if clock is not None:
         clock.lap("cost_aggregate", t0)
     return f, disp, mc, keys, vol
@@ -403,7 +411,7 @@ def _forest_layer(lev: Level, eu, ev, ew, in_tree, comp, gamma, cost, masks=None
 def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
                        cost: CostConsts = CostConsts(), tree_kind: str = "mst", seed: int = 0,
                        x0: int = 0, nx: int | None = None, want_volume=False, want_keys=False,
-                       keep_forest=False, timing=False) -> LevelOut:
+                       keep_forest=False, timing=False, probe=None) -> LevelOut:
     """Full-range aggregation over one MST per pair (aggregation.py:274-358).
     left/right: (B, H, W, C) uint8 device tensors.  [x0, x0+nx) restricts the
     disparity lanes (a slab of the multi-GPU split); default full range."""
@@ -423,7 +431,7 @@ def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
         key = rt_keys(E, b, seed, il.device)
     in_tree, comp, _ = mst(b * h * w, eu, ev, key)
     f, disp, mc, keys, vol = _forest_layer(lev, eu, ev, ew, in_tree, comp, gamma, cost, None, x0,
-                                           nx, want_volume, want_keys, clock, t0)
+                                           nx, want_volume, want_keys, clock, t0, probe)
     ntrees, stored, ratio = _per_pair_stats(f, b, h * w, d_max)
     out = LevelOut(0, h, w, d_max, disp.view(b, h, w), mc.view(b, h, w), ntrees, stored, ratio,
                    dict(clock.acc), f if keep_forest else None)
@@ -509,3 +517,28 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
                        dr_rounds=rounds)
         parent = o.disparity if teacher is None or level not in teacher else teacher[level]
     return outs
+
+
+def run_baseline_host(left_u8: np.ndarray, right_u8: np.ndarray, d_max: int, **kw):
+    """Host-buffer entry point: (B, H, W, C) uint8 numpy (pinned if the caller
+    wants async copies) -> (disparity (B, H, W) int32, min_cost (B, H, W)
+    float32) numpy.  The copies in both directions are part of the call."""
+    torch = _t()
+    dev = L.device()
+    lt = torch.from_numpy(left_u8) if isinstance(left_u8, np.ndarray) else left_u8
+    rt = torch.from_numpy(right_u8) if isinstance(right_u8, np.ndarray) else right_u8
+    ld = lt.to(dev, non_blocking=True)
+    rd = rt.to(dev, non_blocking=True)
+    out = run_baseline_batch(ld, rd, d_max, **kw)
+    return out.disparity.cpu().numpy(), out.min_cost.cpu().numpy()
+
+
+def run_hdp_host(left_u8, right_u8, d_max: int, model, **kw):
+    """Host-buffer HDP entry point -> finest-level disparity (B, H, W) int32."""
+    torch = _t()
+    dev = L.device()
+    lt = torch.from_numpy(left_u8) if isinstance(left_u8, np.ndarray) else left_u8
+    rt = torch.from_numpy(right_u8) if isinstance(right_u8, np.ndarray) else right_u8
+    outs = run_hdp_batch(lt.to(dev, non_blocking=True), rt.to(dev, non_blocking=True), d_max,
+                         model, **kw)
+    return outs[-1].disparity.cpu().numpy()
