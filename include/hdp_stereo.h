@@ -87,6 +87,15 @@ int hdp_cost_volume(const float *packed_l, const float *packed_r, int batch, int
 int hdp_grid_edges(const double *img, int batch, int h, int w, int c, int32_t *eu, int32_t *ev,
                    float *ew, uint64_t *key, void *stream);
 
+/* The same edges' weights in float64 (EdgeList.weight, spanning_forest.py:
+ * 33-49), for the host-facing API. */
+int hdp_grid_edge_weights64(const double *img, int batch, int h, int w, int c, double *ew,
+                            void *stream);
+
+/* apply_median_prefilter (spanning_forest.py:342-347): 3x3 per-channel
+ * median with reflected borders (scipy.ndimage mode "reflect"), uint8. */
+int hdp_median3x3(const uint8_t *src, uint8_t *dst, int batch, int h, int w, int c, void *stream);
+
 /* build_forest(edges, "mst") edge selection (spanning_forest.py:286-322) as
  * Boruvka on unique 64-bit keys (the MST under a total order is unique, so it
  * equals stable-sort Kruskal's).  Works on any edge list (not only grids).
@@ -160,7 +169,8 @@ int hdp_forest_entries(hdp_forest *f, int64_t *total, int64_t *node_offsets, voi
  * (cost_volume.py:183-236, aggregation.py:158-256, baseline fold
  * aggregation.py:311-326), fused: the raw cost is computed on the fly from
  * the packed planes of pair b = node / (h*w) (or read from cost_rows
- * (n_nodes, m) f32 when non-NULL: aggregate_forest, aggregation.py:216-236),
+ * pixel-major ragged rows f32 at the node offsets of hdp_forest_entries when
+ * non-NULL: aggregate_forest / aggregate_tree, aggregation.py:182-236),
  * aggregated leaf->root and root->leaf along heavy paths, and reduced to the
  * first argmin per node.  Outputs (nullable): disp (int32), min_cost (f32),
  * keys (u64 = order-preserving f32 encoding << 32 | d: the u64 minimum is

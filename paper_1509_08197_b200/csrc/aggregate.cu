@@ -59,7 +59,7 @@ struct AggArgs {
 };
 
 __device__ __forceinline__ float raw_cost(const AggArgs& a, int32_t node, int d, int j, int m) {
-    if (a.cost_rows) return a.cost_rows[(int64_t)node * m + j];
+    if (a.cost_rows) return a.cost_rows[a.nodeoff[node] + j];  // pixel-major ragged rows
     int32_t p = node % a.npix;
     int32_t col = p % a.w;
     if (col - d < 0) return a.border;

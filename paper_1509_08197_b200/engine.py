@@ -472,8 +472,6 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
                      f if keep else None)
         o.extra["volume"] = vol
         outs.append(o)
-        if on_level is not None:
-            on_level(o)
         return o
 
     top = lv[levels]
@@ -485,6 +483,8 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     f, disp, mc, _, vol = _forest_layer(top, eu, ev, ew, in_tree, comp, gamma, cost, None,
                                         want_volume=want_volume, clock=lclock, t0=t0)
     o = finish(top, f, disp, mc, vol, dict(lclock.acc))
+    if on_level is not None:
+        on_level(o)
     parent = o.disparity if teacher is None or levels not in teacher else teacher[levels]
     for level in range(levels - 1, -1, -1):
         lev = lv[level]
@@ -514,7 +514,11 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
         lclock.lap("cost_aggregate", t0)
         o = finish(lev, fo, disp, mc, vol, dict(lclock.acc))
         o.extra.update(counts=counts_h, kept=kept_h, chosen=chosen if keep else None,
-                       dr_rounds=rounds)
+                       dr_rounds=rounds,
+                       tree_masks=(tmasks[root_ids].cpu().numpy().view(np.uint32)
+                                   if keep else None))
+        if on_level is not None:
+            on_level(o)
         parent = o.disparity if teacher is None or level not in teacher else teacher[level]
     return outs
 
