@@ -19,7 +19,9 @@
 //   down : k_down_long  the same walk head -> tail, plus the per-node argmin
 //                       (transpose butterfly, 31 shuffles per 32 nodes)
 //          k_down_short single-node paths, fully parallel
-// A is written back in place only where a light child will read it.
+// A is written back in place only where a light child will read it.  All
+// per-position / per-path metadata is pre-packed (forest.cu lanes_finish) so
+// every thread starts from one or two independent loads.
 #include <cuda_runtime.h>
 
 #include "forest.cuh"
@@ -28,43 +30,43 @@
 namespace hdp {
 
 struct AggArgs {
-    const int32_t* lnode;
-    const float* lsim;
+    const int4* lmeta;      // (node, lane offset, image column, m) per layout position
+    const float* lsimf;     // similarity, sign = has light children
     const int32_t* lc_start;
-    const int32_t* lc_list;
-    const int32_t* p_start;
-    const int32_t* p_len;
-    const int32_t* p_par;
-    const int32_t* p_tree;
-    const int32_t* tree_id;
-    const int32_t* t_m;
-    const int32_t* t_doff;
+    const int64_t* lc_row;
+    const float* lc_sim;
+    const int4* pinfo;      // per path of the launch list
+    const longlong2* prows;
     const int32_t* dlist;
     const int64_t* rowoff;
+    const int32_t* lp_list;
     const int64_t* nodeoff;
-    const int32_t* paths;  // long or short path list of the launch
     const float4* pl;
     const float4* pr;
     const float* cost_rows;
     int32_t npix;  // pixels per pair
     int32_t w;
     int c;
+    int range_x0;  // >= 0: lane j is disparity range_x0 + j
     float alpha, tc, tg, border;
     float* aup;
     float* volume;
     unsigned long long* keys;
     int groups;  // 32-lane groups per node when sub == 32
     int sub;     // lanes per item for the packed mappings (power of 2 <= 32)
+    int sub_shift;
     int atomic_keys;
 };
 
-__device__ __forceinline__ float raw_cost(const AggArgs& a, int32_t node, int d, int j, int m) {
+__device__ __forceinline__ int lane_disp(const AggArgs& a, int doff, int j) {
+    return a.range_x0 >= 0 ? a.range_x0 + j : a.dlist[doff + j];
+}
+
+__device__ __forceinline__ float raw_cost(const AggArgs& a, int32_t node, int col, int d, int j) {
     if (a.cost_rows) return a.cost_rows[a.nodeoff[node] + j];  // pixel-major ragged rows
-    int32_t p = node % a.npix;
-    int32_t col = p % a.w;
     if (col - d < 0) return a.border;
-    float4 L = a.pl[node];
-    float4 R = a.pr[node - d];
+    float4 L = __ldg(a.pl + node);
+    float4 R = __ldg(a.pr + node - d);
     float color;
     if (a.c == 3)
         color = (fabsf(L.x - R.x) + fabsf(L.y - R.y) + fabsf(L.z - R.z)) * (1.0f / 3.0f);
@@ -96,43 +98,99 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Thread -> (item, lane j): with sub < 32 several items share a warp (sub
-// lanes each, aligned); otherwise one item spans `groups` warps.
+// Thread -> (item, lane j).  With sub < 32 (a power of two) several items
+// share a warp, `sub` lanes each; otherwise one warp covers 32 lanes of one
+// item and the lane group is blockIdx.y (no integer division anywhere).
 struct Slot {
     int64_t item;
     int j;
 };
-__device__ __forceinline__ Slot slot_of(const AggArgs& a) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ Slot slot_at(const AggArgs& a, int64_t t) {
     Slot s;
     if (a.sub < 32) {
-        s.item = t / a.sub;
-        s.j = (int)(t % a.sub);
+        s.item = t >> a.sub_shift;
+        s.j = (int)(t & (a.sub - 1));
     } else {
-        int64_t w = t >> 5;
-        s.item = w / a.groups;
-        s.j = (int)(w % a.groups) * 32 + (int)(t & 31);
+        s.item = t >> 5;
+        s.j = (int)blockIdx.y * 32 + (int)(t & 31);
     }
     return s;
 }
+__device__ __forceinline__ Slot slot_of(const AggArgs& a) {
+    return slot_at(a, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+}
 
-// b(v) = E(v) + sum_{light children c} s_c A_up(c), every node of a phase.
-__global__ void __launch_bounds__(256) k_bcompute(AggArgs a, int64_t k0, int64_t nk) {
-    Slot s = slot_of(a);
-    if (s.item >= nk) return;
-    int64_t k = k0 + s.item;
-    int64_t row = a.rowoff[k];
-    int m = (int)(a.rowoff[k + 1] - row);
-    if (s.j >= m) return;
-    int32_t node = a.lnode[k];
-    int d = a.dlist[a.t_doff[a.tree_id[node]] + s.j];
-    float v = raw_cost(a, node, d, s.j, m);
-    int32_t c0 = a.lc_start[k], c1 = a.lc_start[k + 1];
-    for (int32_t q = c0; q < c1; q++) {
-        int32_t ck = a.lc_list[q];
-        v += a.lsim[ck] * a.aup[a.rowoff[ck] + s.j];
+constexpr int BU = 4;  // independent work items per thread (memory-level parallelism)
+
+// b(v) = E(v) for every node of a phase, BU independent (node, lane) items
+// per thread; two load levels (metadata -> image planes).
+__global__ void __launch_bounds__(256) k_ecompute(AggArgs a, int64_t k0, int64_t nk) {
+    int64_t T = (int64_t)gridDim.x * blockDim.x;
+    int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t row[BU];
+    int4 mt[BU];
+    int j[BU];
+    bool ok[BU];
+#pragma unroll
+    for (int u = 0; u < BU; u++) {
+        Slot s = slot_at(a, t0 + u * T);
+        ok[u] = s.item < nk;
+        j[u] = s.j;
+        int64_t k = k0 + (ok[u] ? s.item : 0);
+        mt[u] = a.lmeta[k];
+        row[u] = a.rowoff[k];
+        ok[u] = ok[u] && s.j < mt[u].w;
     }
-    a.aup[row + s.j] = v;
+    float v[BU];
+#pragma unroll
+    for (int u = 0; u < BU; u++) {
+        int d = ok[u] ? lane_disp(a, mt[u].y, j[u]) : 0;
+        v[u] = ok[u] ? raw_cost(a, mt[u].x, mt[u].z, d, j[u]) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < BU; u++)
+        if (ok[u]) a.aup[row[u] + j[u]] = v[u];
+}
+
+// b(v) += sum_{light children c} s_c A_up(c) for the phase's light parents
+// (children in ascending id order, their A_up final since the deeper phase).
+__global__ void __launch_bounds__(256) k_light(AggArgs a, int64_t p0, int64_t np) {
+    Slot s = slot_of(a);
+    if (s.item >= np) return;
+    int32_t k = a.lp_list[p0 + s.item];
+    int4 mt = a.lmeta[k];
+    if (s.j >= mt.w) return;
+    int64_t row = a.rowoff[k];
+    int32_t c0 = a.lc_start[k], c1 = a.lc_start[k + 1];
+    float x = 0.0f;
+    for (int32_t q = c0; q < c1; q++) x += a.lc_sim[q] * a.aup[a.lc_row[q] + s.j];
+    a.aup[row + s.j] += x;
+}
+
+// A_up along short paths (2..kShortPath nodes), one thread per (path, lane),
+// values in registers.
+__global__ void __launch_bounds__(256) k_scan_up_short(AggArgs a, int64_t s0, int64_t ns) {
+    Slot s = slot_of(a);
+    if (s.item >= ns) return;
+    int4 info = a.pinfo[s0 + s.item];
+    int len = info.y, m = info.z;
+    if (len < 2 || s.j >= m) return;
+    int64_t row0 = a.prows[s0 + s.item].x;
+    float b[kShortPath], sim[kShortPath];
+#pragma unroll
+    for (int u = 0; u < kShortPath; u++) {
+        b[u] = u < len ? a.aup[row0 + (int64_t)u * m + s.j] : 0.0f;
+        sim[u] = u < len ? fabsf(a.lsimf[info.x + u]) : 0.0f;
+    }
+    float x = 0.0f;
+#pragma unroll
+    for (int u = kShortPath - 1; u >= 0; u--) {
+        if (u < len) {
+            float sn = (u + 1 < len) ? sim[u + 1] : 0.0f;
+            x = b[u] + sn * x;
+            a.aup[row0 + (int64_t)u * m + s.j] = x;
+        }
+    }
 }
 
 constexpr int CH = 32;  // nodes per staged chunk
@@ -141,14 +199,13 @@ constexpr int CH = 32;  // nodes per staged chunk
 __global__ void __launch_bounds__(128) k_scan_up(AggArgs a, int64_t l0, int64_t nl) {
     __shared__ float buf[4][2][CH][32];
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t li = wid / a.groups;
-    int g = (int)(wid % a.groups);
+    int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int g = (int)blockIdx.y;
     if (li >= nl) return;
-    int32_t pi = a.paths[l0 + li];
-    int32_t start = a.p_start[pi], len = a.p_len[pi];
-    int64_t row0 = a.rowoff[start];
-    int m = (int)(a.rowoff[start + 1] - row0);
+    int4 info = a.pinfo[l0 + li];
+    int64_t row0 = a.prows[l0 + li].x;
+    int32_t start = info.x, len = info.y;
+    int m = info.z;
     if (g * 32 >= m) return;
     int j = g * 32 + lane;
     bool act = j < m;
@@ -163,7 +220,7 @@ __global__ void __launch_bounds__(128) k_scan_up(AggArgs a, int64_t l0, int64_t 
     int32_t lo = max(start, hi - CH);
     int bi = 0;
     stage(0, lo, hi - lo);
-    float sim_l = (lane < hi - lo) ? a.lsim[lo + lane] : 0.0f;
+    float sim_l = (lane < hi - lo) ? fabsf(a.lsimf[lo + lane]) : 0.0f;
     float x_prev = 0.0f, s_next = 0.0f;
     while (true) {
         int cnt = hi - lo;
@@ -172,7 +229,7 @@ __global__ void __launch_bounds__(128) k_scan_up(AggArgs a, int64_t l0, int64_t 
         float sim_n = 0.0f;
         if (more) {
             stage(bi ^ 1, nlo, nhi - nlo);
-            sim_n = (lane < nhi - nlo) ? a.lsim[nlo + lane] : 0.0f;
+            sim_n = (lane < nhi - nlo) ? fabsf(a.lsimf[nlo + lane]) : 0.0f;
             cp_wait<1>();
         } else {
             cp_wait<0>();
@@ -210,100 +267,190 @@ __device__ __forceinline__ unsigned long long warp_min_per_node(unsigned long lo
     return key[0];
 }
 
+__device__ __forceinline__ unsigned long long warp_min(unsigned long long k) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        unsigned long long other = __shfl_xor_sync(0xffffffffu, k, o);
+        k = other < k ? other : k;
+    }
+    return k;
+}
+
+// First argmin of (cost, d) over the lanes of one item: `width` lanes
+// (power of two, aligned) or the full warp.  32-bit redux/shuffle min on the
+// order-preserving cost, then the lowest lane holding it (lanes are in
+// ascending disparity order) supplies d.  Every lane gets the packed key.
+__device__ __forceinline__ unsigned long long group_argmin(bool act, float y, int d, int width,
+                                                           int lane) {
+    uint32_t o = act ? ord_f32(y) : 0xffffffffu;
+    uint32_t mn = o;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        uint32_t t = __shfl_xor_sync(0xffffffffu, mn, off);
+        if (off < width) mn = min(mn, t);
+    }
+    unsigned gmask = width == 32 ? 0xffffffffu : ((1u << width) - 1u) << (lane & ~(width - 1));
+    unsigned eq = __ballot_sync(0xffffffffu, o == mn) & gmask;
+    int dmin = __shfl_sync(0xffffffffu, d, __ffs(eq) - 1);
+    return ((unsigned long long)mn << 32) | (uint32_t)dmin;
+}
+
+__device__ __forceinline__ void store_key(const AggArgs& a, int32_t node, unsigned long long k) {
+    if (!a.keys) return;
+    if (a.atomic_keys)
+        atomicMin(&a.keys[node], k);
+    else
+        a.keys[node] = k;
+}
+
 // A along paths of length >= 2, head -> tail, fused with the argmin.
 __global__ void __launch_bounds__(128) k_down_long(AggArgs a, int64_t l0, int64_t nl) {
     __shared__ float buf[4][2][CH][32];
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t li = wid / a.groups;
-    int g = (int)(wid % a.groups);
+    int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int g = (int)blockIdx.y;
     if (li >= nl) return;
-    int32_t pi = a.paths[l0 + li];
-    int32_t start = a.p_start[pi], len = a.p_len[pi];
-    int64_t row0 = a.rowoff[start];
-    int m = (int)(a.rowoff[start + 1] - row0);
+    int4 info = a.pinfo[l0 + li];
+    longlong2 rows = a.prows[l0 + li];
+    int32_t start = info.x, len = info.y;
+    int m = info.z;
     if (g * 32 >= m) return;
     int j = g * 32 + lane;
     bool act = j < m;
-    int32_t node0 = a.lnode[start];
-    int d = act ? a.dlist[a.t_doff[a.tree_id[node0]] + j] : 0;
-    int32_t par = a.p_par[pi];
+    int d = act ? lane_disp(a, info.w, j) : 0;
+    int64_t row0 = rows.x;
+    bool root_path = rows.y < 0;
     float* aup = a.aup;
     float y = 0.0f;
-    if (par >= 0 && act) y = aup[a.rowoff[par] + j];  // A(parent), stored in place
+    if (!root_path && act) y = aup[rows.y + j];  // A(parent), stored in place
     auto stage = [&](int bi, int32_t lo, int cnt) {
         for (int i = 0; i < cnt; i++)
             cp_async4(&buf[warp][bi][i][lane], aup + row0 + (int64_t)(lo + i - start) * m + j, act);
         cp_commit();
     };
-    auto meta = [&](int32_t lo, int cnt, float& sim, int32_t& node, unsigned& light) {
+    auto meta = [&](int32_t lo, int cnt, float& simf, int32_t& node) {
         bool in = lane < cnt;
-        sim = in ? a.lsim[lo + lane] : 0.0f;
-        node = in ? a.lnode[lo + lane] : 0;
-        bool lt = in && a.lc_start[lo + lane + 1] > a.lc_start[lo + lane];
-        light = __ballot_sync(0xffffffffu, lt);
+        simf = in ? a.lsimf[lo + lane] : 0.0f;
+        node = in ? a.lmeta[lo + lane].x : 0;
     };
     int32_t end = start + len;
     int32_t lo = start, hi = min(end, start + CH);
     int bi = 0;
     stage(0, lo, hi - lo);
-    float sim_l;
+    float simf_l;
     int32_t node_l;
-    unsigned light;
-    meta(lo, hi - lo, sim_l, node_l, light);
+    meta(lo, hi - lo, simf_l, node_l);
     while (true) {
         int cnt = hi - lo;
         int32_t nlo = hi, nhi = min(end, hi + CH);
         bool more = nlo < end;
-        float sim_n = 0.0f;
+        float simf_n = 0.0f;
         int32_t node_n = 0;
-        unsigned light_n = 0;
         if (more) {
             stage(bi ^ 1, nlo, nhi - nlo);
-            meta(nlo, nhi - nlo, sim_n, node_n, light_n);
+            meta(nlo, nhi - nlo, simf_n, node_n);
             cp_wait<1>();
         } else {
             cp_wait<0>();
         }
         __syncwarp();
-        unsigned long long key[CH];
-#pragma unroll
-        for (int i = 0; i < CH; i++) {
-            float s = __shfl_sync(0xffffffffu, sim_l, i);
-            if (i < cnt) {
+        unsigned light = __ballot_sync(0xffffffffu, signbit(simf_l));
+        if (cnt <= 4) {
+            // short chunk: one warp reduction per node
+            for (int i = 0; i < cnt; i++) {
+                float sf = __shfl_sync(0xffffffffu, simf_l, i);
+                float s = fabsf(sf);
                 float u = buf[warp][bi][i][lane];
-                if (par < 0 && lo + i == start)
+                if (root_path && lo + i == start)
                     y = u;
                 else
                     y = s * y + (1.0f - s * s) * u;
                 int64_t row = row0 + (int64_t)(lo + i - start) * m;
                 if (act && (((light >> i) & 1u) || a.volume)) aup[row + j] = y;
-                key[i] = act ? pack_key(y, d) : ~0ull;
-            } else {
-                key[i] = ~0ull;
+                unsigned long long k = group_argmin(act, y, d, 32, lane);
+                int32_t nd = __shfl_sync(0xffffffffu, node_l, i);
+                if (lane == 0) store_key(a, nd, k);
             }
-        }
-        unsigned long long best = warp_min_per_node(key, lane);
-        if (lane < cnt && a.keys) {
-            if (a.atomic_keys)
-                atomicMin(&a.keys[node_l], best);
-            else
-                a.keys[node_l] = best;
+        } else {
+            unsigned long long key[CH];
+#pragma unroll
+            for (int i = 0; i < CH; i++) {
+                float s = fabsf(__shfl_sync(0xffffffffu, simf_l, i));
+                if (i < cnt) {
+                    float u = buf[warp][bi][i][lane];
+                    if (root_path && lo + i == start)
+                        y = u;
+                    else
+                        y = s * y + (1.0f - s * s) * u;
+                    int64_t row = row0 + (int64_t)(lo + i - start) * m;
+                    if (act && (((light >> i) & 1u) || a.volume)) aup[row + j] = y;
+                    key[i] = act ? pack_key(y, d) : ~0ull;
+                } else {
+                    key[i] = ~0ull;
+                }
+            }
+            unsigned long long best = warp_min_per_node(key, lane);
+            if (lane < cnt) store_key(a, node_l, best);
         }
         __syncwarp();
         if (!more) break;
         lo = nlo;
         hi = nhi;
         bi ^= 1;
-        sim_l = sim_n;
+        simf_l = simf_n;
         node_l = node_n;
-        light = light_n;
     }
 }
 
-// Pixel-major copy of the final aggregated volume (parity / API use only):
-// after the down pass every node's row holds A only where it was stored, so
-// this is produced by a dedicated pass in volume mode (see hdp_aggregate_wta).
+// Short paths (1..kShortPath nodes): A = s A(parent) + (1 - s^2) A_up head ->
+// tail in registers, then the per-node argmin across the item's lanes.
+__global__ void __launch_bounds__(256) k_down_short(AggArgs a, int64_t s0, int64_t ns) {
+    Slot s = slot_of(a);
+    int lane = threadIdx.x & 31;
+    bool valid = s.item < ns;
+    int len = 0, m = 0, start = 0, d = 0;
+    int64_t row0 = 0, prow = -1;
+    if (valid) {
+        int4 info = a.pinfo[s0 + s.item];
+        longlong2 rows = a.prows[s0 + s.item];
+        start = info.x;
+        len = info.y;
+        m = info.z;
+        row0 = rows.x;
+        prow = rows.y;
+        if (s.j < m) d = lane_disp(a, info.w, s.j);
+    }
+    bool act = valid && s.j < m;
+    float u[kShortPath], sf[kShortPath];
+    int32_t nd[kShortPath];
+#pragma unroll
+    for (int q = 0; q < kShortPath; q++) {
+        bool in = valid && q < len;
+        u[q] = (in && act) ? a.aup[row0 + (int64_t)q * m + s.j] : 0.0f;
+        sf[q] = in ? a.lsimf[start + q] : 0.0f;
+        nd[q] = in ? a.lmeta[start + q].x : 0;
+    }
+    float y = (act && prow >= 0) ? a.aup[prow + s.j] : 0.0f;
+    int width = a.sub < 32 ? a.sub : 32;
+    // the longest path among the lanes of this warp bounds the loop
+    int wlen = len;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) wlen = max(wlen, __shfl_xor_sync(0xffffffffu, wlen, o));
+#pragma unroll
+    for (int q = 0; q < kShortPath; q++) {
+        if (q >= wlen) break;
+        bool on = act && q < len;
+        if (on) {
+            float sv = fabsf(sf[q]);
+            y = (q == 0 && prow < 0) ? u[q] : sv * y + (1.0f - sv * sv) * u[q];
+            if (signbit(sf[q]) || a.volume) a.aup[row0 + (int64_t)q * m + s.j] = y;
+        }
+        unsigned long long key = group_argmin(on, y, d, width, lane);
+        if (valid && q < len && (lane & (width - 1)) == 0) store_key(a, nd[q], key);
+    }
+}
+
+// Pixel-major copy of the final aggregated volume (parity / API use only).
 __global__ void __launch_bounds__(256) k_volume_copy(AggArgs a, int64_t n) {
     Slot s = slot_of(a);
     if (s.item >= n) return;
@@ -311,46 +458,13 @@ __global__ void __launch_bounds__(256) k_volume_copy(AggArgs a, int64_t n) {
     int64_t row = a.rowoff[k];
     int m = (int)(a.rowoff[k + 1] - row);
     if (s.j >= m) return;
-    a.volume[a.nodeoff[a.lnode[k]] + s.j] = a.aup[row + s.j];
+    a.volume[a.nodeoff[a.lmeta[k].x] + s.j] = a.aup[row + s.j];
 }
 
-// Single-node paths: A(v) = s A(parent) + (1 - s^2) A_up(v), then argmin.
-__global__ void __launch_bounds__(256) k_down_short(AggArgs a, int64_t s0, int64_t ns) {
-    Slot s = slot_of(a);
-    int lane = threadIdx.x & 31;
-    bool valid = s.item < ns;
-    unsigned long long key = ~0ull;
-    int32_t node = 0;
-    if (valid) {
-        int32_t pi = a.paths[s0 + s.item];
-        int32_t k = a.p_start[pi];
-        int64_t row = a.rowoff[k];
-        int m = (int)(a.rowoff[k + 1] - row);
-        node = a.lnode[k];
-        if (s.j < m) {
-            int d = a.dlist[a.t_doff[a.tree_id[node]] + s.j];
-            float u = a.aup[row + s.j];
-            int32_t par = a.p_par[pi];
-            float y = u;
-            if (par >= 0) {
-                float sv = a.lsim[k];
-                y = sv * a.aup[a.rowoff[par] + s.j] + (1.0f - sv * sv) * u;
-            }
-            if (a.lc_start[k + 1] > a.lc_start[k] || a.volume) a.aup[row + s.j] = y;
-            key = pack_key(y, d);
-        }
-    }
-    int width = a.sub < 32 ? a.sub : 32;
-    for (int o = width >> 1; o >= 1; o >>= 1) {
-        unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-        key = other < key ? other : key;
-    }
-    if (valid && (lane & (width - 1)) == 0 && a.keys) {
-        if (a.atomic_keys)
-            atomicMin(&a.keys[node], key);
-        else
-            a.keys[node] = key;
-    }
+// image column of every layout position for this call's geometry
+__global__ void k_fill_cols(int64_t n, int4* lmeta, int32_t npix, int32_t w) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) lmeta[k].z = (lmeta[k].x % npix) % w;
 }
 
 __global__ void k_keys_init(int64_t n, unsigned long long* keys) {
@@ -378,8 +492,12 @@ static int pow2_at_least(int x) {
     return p;
 }
 
-static int64_t packed_threads(const AggArgs& a, int64_t items) {
-    return a.sub < 32 ? items * a.sub : items * a.groups * 32;
+// grid for the packed mappings: x covers items (sub lanes or one warp each,
+// bu items per thread), y covers the 32-lane groups when sub == 32
+static dim3 packed_grid(const AggArgs& a, int64_t items, int bu, int block) {
+    int64_t th = a.sub < 32 ? items * a.sub : items * 32;
+    th = (th + bu - 1) / bu;
+    return dim3((unsigned)grid_for(th, block), a.sub < 32 ? 1u : (unsigned)a.groups, 1u);
 }
 
 }  // namespace hdp
@@ -396,27 +514,24 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_REQUIRE(cost_rows || (int64_t)h * w < ((int64_t)1 << 31), HDP_ERR_CONFIG, "image too large");
     cudaStream_t st = (cudaStream_t)stream;
     AggArgs a;
-    a.lnode = f->lnode.get();
-    a.lsim = f->lsim.get();
+    a.lmeta = f->lmeta.get();
+    a.lsimf = f->lsimf.get();
     a.lc_start = f->lc_start.get();
-    a.lc_list = f->lc_list.get();
-    a.p_start = f->p_start.get();
-    a.p_len = f->p_len.get();
-    a.p_par = f->p_par.get();
-    a.p_tree = f->p_tree.get();
-    a.tree_id = f->tree_id.get();
-    a.t_m = f->t_m.get();
-    a.t_doff = f->t_doff.get();
+    a.lc_row = f->lc_row.get();
+    a.lc_sim = f->lc_sim.get();
+    a.pinfo = nullptr;
+    a.prows = nullptr;
     a.dlist = f->dlist.get();
     a.rowoff = f->rowoff.get();
+    a.lp_list = f->lp_list.get();
     a.nodeoff = f->nodeoff.get();
-    a.paths = nullptr;
     a.pl = (const float4*)packed_l;
     a.pr = (const float4*)packed_r;
     a.cost_rows = cost_rows;
     a.npix = (h > 0 && w > 0) ? h * w : 1;
     a.w = w > 0 ? w : 1;
     a.c = c;
+    a.range_x0 = f->range_x0;
     a.alpha = alpha;
     a.tc = tau_c;
     a.tg = tau_g;
@@ -424,6 +539,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.volume = volume;
     a.groups = (f->max_m + 31) / 32;
     a.sub = f->max_m <= 16 ? pow2_at_least(f->max_m) : 32;
+    a.sub_shift = 0;
+    while ((1 << a.sub_shift) < a.sub) a.sub_shift++;
     DevBuf<float> aup;
     HDP_TRY(aup.alloc(f->total_entries + 32, st));
     a.aup = aup.get();
@@ -435,35 +552,58 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     }
     a.keys = kp;
     a.atomic_keys = a.groups > 1 ? 1 : 0;
-    if (a.atomic_keys) k_keys_init<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp); note_launch();
+    if (!cost_rows && (f->geom_w != a.w || f->geom_np != a.npix)) {
+        k_fill_cols<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, f->lmeta.get(), a.npix, a.w); note_launch();
+        f->geom_w = a.w;
+        f->geom_np = a.npix;
+    }
+    if (a.atomic_keys) {
+        k_keys_init<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp); note_launch();
+    }
 
     AggArgs lg = a;  // long-path kernels: one warp per (path, 32 lanes)
     lg.sub = 32;
-    lg.paths = f->long_paths.get();
+    lg.pinfo = f->long_info.get();
+    lg.prows = f->long_rows.get();
     AggArgs sh = a;
-    sh.paths = f->short_paths.get();
+    sh.pinfo = f->short_info.get();
+    sh.prows = f->short_rows.get();
     for (int64_t r = f->n_phases - 1; r >= 0; r--) {
         int64_t k0 = f->phase_node[r], nk = f->phase_node[r + 1] - k0;
-        if (nk > 0) k_bcompute<<<grid_for(packed_threads(a, nk), 256), 256, 0, st>>>(a, k0, nk); note_launch();
+        if (nk > 0) {
+            k_ecompute<<<packed_grid(a, nk, BU, 256), 256, 0, st>>>(a, k0, nk); note_launch();
+        }
+        int64_t p0 = f->lp_off[r], np = f->lp_off[r + 1] - p0;
+        if (np > 0) {
+            k_light<<<packed_grid(a, np, 1, 256), 256, 0, st>>>(a, p0, np); note_launch();
+        }
         int64_t l0 = f->long_off[r], nl = f->long_off[r + 1] - l0;
-        if (nl > 0)
-            k_scan_up<<<grid_for(nl * lg.groups * 32, 128), 128, 0, st>>>(lg, l0, nl); note_launch();
+        if (nl > 0) {
+            k_scan_up<<<dim3(grid_for(nl * 32, 128), lg.groups), 128, 0, st>>>(lg, l0, nl); note_launch();
+        }
+        int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
+        if (ns > 0) {
+            k_scan_up_short<<<packed_grid(sh, ns, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
+        }
     }
     HDP_CHECK_LAUNCH();
     for (int64_t r = 0; r < f->n_phases; r++) {
         int64_t l0 = f->long_off[r], nl = f->long_off[r + 1] - l0;
-        if (nl > 0)
-            k_down_long<<<grid_for(nl * lg.groups * 32, 128), 128, 0, st>>>(lg, l0, nl); note_launch();
+        if (nl > 0) {
+            k_down_long<<<dim3(grid_for(nl * 32, 128), lg.groups), 128, 0, st>>>(lg, l0, nl); note_launch();
+        }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
-        if (ns > 0) k_down_short<<<grid_for(packed_threads(sh, ns), 256), 256, 0, st>>>(sh, s0, ns); note_launch();
+        if (ns > 0) {
+            k_down_short<<<packed_grid(sh, ns, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
+        }
     }
     HDP_CHECK_LAUNCH();
     if (volume) {
-        AggArgs va = a;
-        k_volume_copy<<<grid_for(packed_threads(va, f->n), 256), 256, 0, st>>>(va, f->n); note_launch();
+        k_volume_copy<<<packed_grid(a, f->n, 1, 256), 256, 0, st>>>(a, f->n); note_launch();
     }
-    if (disp || min_cost)
+    if (disp || min_cost) {
         k_keys_finish<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp, disp, min_cost); note_launch();
+    }
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

@@ -287,6 +287,24 @@ __global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
     idx[v] = (int32_t)v;
 }
 
+__global__ void k_lp_flags(int64_t n, const int32_t* __restrict__ lc_start, int32_t* fl) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) fl[k] = lc_start[k + 1] > lc_start[k] ? 1 : 0;
+    else if (k == n) fl[k] = 0;
+}
+
+__global__ void k_lp_fill(int64_t n, const int32_t* __restrict__ fl, const int32_t* __restrict__ ex,
+                          int32_t* list) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n && fl[k]) list[ex[k]] = (int32_t)k;
+}
+
+__global__ void k_gather_i32(int64_t m, const int32_t* __restrict__ src,
+                             const int32_t* __restrict__ idx, int32_t* out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) out[i] = src[idx[i]];
+}
+
 __global__ void k_layout_pos(int64_t n, const int32_t* __restrict__ lnode,
                              const float* __restrict__ pweight, float gamma, int32_t* lpos,
                              float* lsim) {
@@ -327,7 +345,7 @@ __global__ void k_path_info(int64_t np, int64_t n, const int32_t* __restrict__ p
     p_par[i] = parent[h] == h ? -1 : lpos[parent[h]];
     p_tree[i] = tree_id[h];
     p_ld[i] = ld[h];
-    is_long[i] = (e - s) >= 2 ? 1 : 0;
+    is_long[i] = (e - s) > kShortPath ? 1 : 0;
 }
 
 // first path index of every phase (paths are phase-major)
@@ -338,6 +356,18 @@ __global__ void k_phase_bounds(int64_t np, const int32_t* __restrict__ p_ld, int
     int a = (i == 0) ? -1 : p_ld[i - 1];
     int b = (i == np) ? nph : p_ld[i];
     for (int r = a + 1; r <= b; r++) first[r] = (int32_t)i;
+}
+
+// per phase: first layout position and the long-path prefix count at its start
+__global__ void k_phase_gather(int64_t nb, const int32_t* __restrict__ first,
+                               const int32_t* __restrict__ p_start,
+                               const int32_t* __restrict__ lexcl, int64_t np, int64_t n,
+                               int32_t* out) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nb) return;
+    int32_t pi = first[r];
+    out[2 * r] = pi < np ? p_start[pi] : (int32_t)n;
+    out[2 * r + 1] = lexcl[pi];
 }
 
 __global__ void k_split_paths(int64_t np, const int32_t* __restrict__ is_long,
@@ -702,16 +732,19 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         f->phase_node.assign(f->n_phases + 1, n);
         f->long_off.assign(f->n_phases + 1, 0);
         f->short_off.assign(f->n_phases + 1, 0);
-        for (int64_t r = 0; r <= f->n_phases; r++) {
-            int64_t pi = f->phase_off[r];
-            int32_t v = 0;
-            if (pi < f->n_paths) {
-                HDP_TRY(to_host(&v, f->p_start.get() + pi, 1, st));
-                f->phase_node[r] = v;
+        {
+            DevBuf<int32_t> bnd;
+            HDP_TRY(bnd.alloc(2 * (f->n_phases + 1), st));
+            k_phase_gather<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(
+                f->n_phases + 1, first.get(), f->p_start.get(), lexcl.get(), f->n_paths, n,
+                bnd.get()); note_launch();
+            std::vector<int32_t> hb(2 * (f->n_phases + 1));
+            HDP_TRY(to_host(hb.data(), bnd.get(), 2 * (f->n_phases + 1), st));
+            for (int64_t r = 0; r <= f->n_phases; r++) {
+                f->phase_node[r] = hb[2 * r];
+                f->long_off[r] = hb[2 * r + 1];
+                f->short_off[r] = f->phase_off[r] - hb[2 * r + 1];
             }
-            HDP_TRY(to_host(&v, lexcl.get() + pi, 1, st));
-            f->long_off[r] = v;
-            f->short_off[r] = pi - v;
         }
         HDP_TRY(f->long_paths.alloc(f->long_off[f->n_phases] + 1, st));
         HDP_TRY(f->short_paths.alloc(f->short_off[f->n_phases] + 1, st));
@@ -736,9 +769,75 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                             f->parent.get(), head, f->lpos.get(),
                                             f->lc_start.get(), f->lc_list.get()); note_launch();
     HDP_CHECK_LAUNCH();
+
+    // ---- 10. light parents (positions with light children), phase-major
+    {
+        DevBuf<int32_t> fl, ex, bnd, pn;
+        HDP_TRY(fl.alloc(n + 1, st));
+        HDP_TRY(ex.alloc(n + 1, st));
+        k_lp_flags<<<grid_for(n + 1, B), B, 0, st>>>(n, f->lc_start.get(), fl.get()); note_launch();
+        HDP_TRY(exclusive_sum(fl.get(), ex.get(), n + 1, st));
+        int32_t n_lp = 0;
+        HDP_TRY(to_host(&n_lp, ex.get() + n, 1, st));
+        HDP_TRY(f->lp_list.alloc(n_lp + 1, st));
+        k_lp_fill<<<grid_for(n, B), B, 0, st>>>(n, fl.get(), ex.get(), f->lp_list.get()); note_launch();
+        std::vector<int32_t> hp(f->n_phases + 1), hl(f->n_phases + 1);
+        for (int64_t r = 0; r <= f->n_phases; r++) hp[r] = (int32_t)f->phase_node[r];
+        HDP_TRY(pn.alloc(f->n_phases + 1, st));
+        HDP_TRY(bnd.alloc(f->n_phases + 1, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(pn.get(), hp.data(), sizeof(int32_t) * (f->n_phases + 1),
+                                       cudaMemcpyHostToDevice, st));
+        k_gather_i32<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(f->n_phases + 1, ex.get(), pn.get(),
+                                                                   bnd.get()); note_launch();
+        HDP_TRY(to_host(hl.data(), bnd.get(), f->n_phases + 1, st));
+        f->lp_off.assign(hl.begin(), hl.end());
+    }
     HDP_CHECK_CUDA(cudaStreamSynchronize(st));
     return HDP_OK;
 }
+
+namespace hdp {
+
+__global__ void k_pos_meta(int64_t n, const int32_t* __restrict__ lnode,
+                           const int32_t* __restrict__ tree_id, const int32_t* __restrict__ t_doff,
+                           const float* __restrict__ lsim, const int32_t* __restrict__ lc_start,
+                           const int64_t* __restrict__ rowoff, int4* lmeta, float* lsimf) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int32_t v = lnode[k];
+    // (node, lane-table offset, image column (set per call), lane count m)
+    lmeta[k] = make_int4(v, t_doff[tree_id[v]], -1, (int)(rowoff[k + 1] - rowoff[k]));
+    float s = lsim[k];
+    lsimf[k] = (lc_start[k + 1] > lc_start[k]) ? -s : s;  // sign bit: has light children
+}
+
+__global__ void k_lc_meta(int64_t nl, const int32_t* __restrict__ lc_list,
+                          const int64_t* __restrict__ rowoff, const float* __restrict__ lsim,
+                          int64_t* lc_row, float* lc_sim) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nl) return;
+    int32_t ck = lc_list[q];
+    lc_row[q] = rowoff[ck];
+    lc_sim[q] = lsim[ck];
+}
+
+__global__ void k_path_meta(int64_t np, const int32_t* __restrict__ list,
+                            const int32_t* __restrict__ p_start, const int32_t* __restrict__ p_len,
+                            const int32_t* __restrict__ p_par, const int32_t* __restrict__ p_tree,
+                            const int32_t* __restrict__ t_doff, const int64_t* __restrict__ rowoff,
+                            int4* info, longlong2* rows) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    int32_t pi = list[i];
+    int32_t s = p_start[pi];
+    int64_t r0 = rowoff[s];
+    int32_t m = (int32_t)(rowoff[s + 1] - r0);
+    int32_t par = p_par[pi];
+    info[i] = make_int4(s, p_len[pi], m, t_doff[p_tree[pi]]);
+    rows[i] = make_longlong2(r0, par >= 0 ? rowoff[par] : -1);
+}
+
+}  // namespace hdp
 
 static int lanes_finish(hdp_forest* f) {
     cudaStream_t st = f->st;
@@ -763,7 +862,38 @@ static int lanes_finish(hdp_forest* f) {
     int32_t hm = 0;
     HDP_TRY(to_host(&hm, mx.get(), 1, st));
     f->max_m = hm;
+    // packed metadata for the aggregation kernels
+    int32_t n_lc = 0;
+    HDP_TRY(to_host(&n_lc, f->lc_start.get() + n, 1, st));
+    HDP_TRY(f->lmeta.alloc(n, st));
+    HDP_TRY(f->lsimf.alloc(n, st));
+    HDP_TRY(f->lc_row.alloc(n_lc + 1, st));
+    HDP_TRY(f->lc_sim.alloc(n_lc + 1, st));
+    k_pos_meta<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), f->tree_id.get(), f->t_doff.get(),
+                                            f->lsim.get(), f->lc_start.get(), f->rowoff.get(),
+                                            f->lmeta.get(),
+                                            f->lsimf.get()); note_launch();
+    if (n_lc > 0)
+        k_lc_meta<<<grid_for(n_lc, B), B, 0, st>>>(n_lc, f->lc_list.get(), f->rowoff.get(),
+                                                  f->lsim.get(), f->lc_row.get(), f->lc_sim.get()); note_launch();
+    int64_t nl = f->long_off[f->n_phases], ns = f->short_off[f->n_phases];
+    HDP_TRY(f->long_info.alloc(nl + 1, st));
+    HDP_TRY(f->long_rows.alloc(nl + 1, st));
+    HDP_TRY(f->short_info.alloc(ns + 1, st));
+    HDP_TRY(f->short_rows.alloc(ns + 1, st));
+    if (nl > 0)
+        k_path_meta<<<grid_for(nl, B), B, 0, st>>>(nl, f->long_paths.get(), f->p_start.get(),
+                                                  f->p_len.get(), f->p_par.get(), f->p_tree.get(),
+                                                  f->t_doff.get(), f->rowoff.get(),
+                                                  f->long_info.get(), f->long_rows.get()); note_launch();
+    if (ns > 0)
+        k_path_meta<<<grid_for(ns, B), B, 0, st>>>(ns, f->short_paths.get(), f->p_start.get(),
+                                                  f->p_len.get(), f->p_par.get(), f->p_tree.get(),
+                                                  f->t_doff.get(), f->rowoff.get(),
+                                                  f->short_info.get(), f->short_rows.get()); note_launch();
+    HDP_CHECK_LAUNCH();
     f->lanes_set = 1;
+    f->geom_w = -1;
     return HDP_OK;
 }
 
@@ -829,6 +959,7 @@ int hdp_forest_set_lanes_range(hdp_forest* f, int x0, int nx, void* stream) {
                                                              f->t_doff.get()); note_launch();
     k_iota<<<grid_for(nx, 256), 256, 0, st>>>(nx, f->dlist.get(), x0); note_launch();
     HDP_CHECK_LAUNCH();
+    f->range_x0 = x0;
     return lanes_finish(f);
 }
 
@@ -837,6 +968,7 @@ int hdp_forest_set_lanes(hdp_forest* f, const uint32_t* tree_masks, int nw, void
     HDP_REQUIRE(nw >= 1, HDP_ERR_CONFIG, "mask width must be >= 1 word");
     f->st = (cudaStream_t)stream;
     cudaStream_t st = f->st;
+    f->range_x0 = -1;
     HDP_TRY(f->t_m.alloc(f->n_trees, st));
     HDP_TRY(f->t_doff.alloc(f->n_trees + 1, st));
     k_lanes_count<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw, f->t_m.get()); note_launch();

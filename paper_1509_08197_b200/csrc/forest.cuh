@@ -6,6 +6,10 @@
 
 #include "common.cuh"
 
+// Heavy paths of at most this many nodes are aggregated register-resident
+// (one thread per (path, lane)); longer ones by a warp walking staged chunks.
+constexpr int kShortPath = 8;
+
 struct hdp_forest {
     cudaStream_t st = nullptr;
     int64_t n = 0;         // nodes
@@ -21,6 +25,8 @@ struct hdp_forest {
 
     // per layout position k (phase-major, path-contiguous, head first)
     hdp::DevBuf<int32_t> lnode;     // node id at k
+    hdp::DevBuf<int32_t> lp_list;   // positions with light children, phase-major
+    std::vector<int64_t> lp_off;    // host: light parents of phase r = [lp_off[r], lp_off[r+1])
     hdp::DevBuf<float> lsim;        // exp(-w(parent)/(gamma*255)) of that node
     hdp::DevBuf<int32_t> lc_start;  // n+1, CSR over light children
     hdp::DevBuf<int32_t> lc_list;   // layout positions of light children
@@ -41,4 +47,16 @@ struct hdp_forest {
     hdp::DevBuf<int64_t> rowoff;   // layout order, n+1: hypothesis row offsets
     hdp::DevBuf<int64_t> nodeoff;  // node-id order, n: pixel-major volume offsets
     int64_t total_entries = 0;
+    int range_x0 = -1;             // >= 0: every tree's lanes are x0 + j
+
+    // packed metadata for the aggregation kernels (built with the lanes):
+    hdp::DevBuf<int4> lmeta;       // per layout position: (node, lane offset, column, m)
+    int geom_w = -1, geom_np = -1; // image geometry the lmeta columns were filled for
+    hdp::DevBuf<float> lsimf;      // per position: similarity, sign bit = has light children
+    hdp::DevBuf<int64_t> lc_row;   // per light-child entry: row offset of the child
+    hdp::DevBuf<float> lc_sim;     // per light-child entry: similarity of the child
+    hdp::DevBuf<int4> long_info;   // long paths: (start, len, m, lane offset)
+    hdp::DevBuf<longlong2> long_rows;   // (first row, parent's row or -1)
+    hdp::DevBuf<int4> short_info;  // single-node paths: (position, m, lane offset, 0)
+    hdp::DevBuf<longlong2> short_rows;
 };
