@@ -181,6 +181,12 @@ int hdp_aggregate_wta(hdp_forest *f, const float *packed_l, const float *packed_
                       int32_t *disp, float *min_cost, uint64_t *keys, float *volume,
                       void *stream);
 
+/* Per pair of a batch (nodes_per_pair consecutive node ids each): tree count
+ * (LayerResult.n_trees) and stored entries (LayerResult.stored_entries,
+ * aggregation.py:418-426); host output arrays of length batch. */
+int hdp_forest_pair_stats(const hdp_forest *f, int batch, int64_t nodes_per_pair,
+                          int64_t *n_trees, int64_t *stored, void *stream);
+
 void hdp_forest_destroy(hdp_forest *f);
 
 /* keys -> (disp, min_cost) for keys combined across slabs (NCCL min). */

@@ -88,6 +88,17 @@ struct DevBuf {
     T* get() const { return p; }
 };
 
+// HDP_TRACE=1: host-side timestamps (ms since the previous mark) on stderr,
+// synchronising the stream at each mark so the interval is GPU-complete.
+struct Tracer {
+    bool on = false;
+    double last = 0.0;
+    cudaStream_t st = nullptr;
+    static double now_ms();
+    explicit Tracer(cudaStream_t s);
+    void mark(const char* what);
+};
+
 inline int grid_for(int64_t n, int block) {
     int64_t g = (n + block - 1) / block;
     if (g < 1) g = 1;

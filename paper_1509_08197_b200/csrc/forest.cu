@@ -471,6 +471,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     const int64_t n = f->n;
     const int B = 256;
 
+    Tracer tr(st);
     // ---- 1. tree edges
     DevBuf<int32_t> flags, fpos;
     HDP_TRY(flags.alloc(m_in + 1, st));
@@ -499,6 +500,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     flags.release();
     fpos.release();
 
+    tr.mark("1 tree edges");
     // ---- 2. components, roots, tree numbering
     DevBuf<int32_t> comp;
     HDP_TRY(comp.alloc(n, st));
@@ -534,6 +536,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     minid.release();
     tindex.release();
 
+    tr.mark("2 components/roots");
     // ---- 3. CSR adjacency (arcs sorted by (src, dst))
     const int64_t na = 2 * m;
     DevBuf<uint64_t> akey, akey2;
@@ -563,6 +566,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     if (na > 0) k_arc_unpack<<<grid_for(na, B), B, 0, st>>>(na, akey2.get(), asrc.get(), adst.get()); note_launch();
     akey2.release();
 
+    tr.mark("3 csr adjacency");
     // ---- 4. Euler tour + list ranking
     DevBuf<int32_t> twin, nxt, nxt2, rank, rank2, tlen, toff, tpos;
     HDP_TRY(twin.alloc(na + 1, st));
@@ -598,6 +602,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     rank.release();
     rank2.release();
 
+    tr.mark("4 euler tour+ranking");
     // ---- 5. orientation, sizes, depth
     HDP_TRY(f->parent.alloc(n, st));
     HDP_TRY(f->pweight.alloc(n, st));
@@ -630,6 +635,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     aw2.release();
     twin.release();
 
+    tr.mark("5 orient/depth");
     // ---- 6. heavy paths
     DevBuf<int32_t> heavy, hp, hp2, dist, dist2;
     HDP_TRY(heavy.alloc(n, st));
@@ -654,6 +660,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     dist2.release();
     int32_t* head = hp.get();
 
+    tr.mark("6 heavy paths");
     // ---- 7. light depth (tour scan) and layout order
     DevBuf<int32_t> ld;
     HDP_TRY(ld.alloc(n, st));
@@ -690,6 +697,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     k_layout_pos<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), f->pweight.get(), f->gamma,
                                                f->lpos.get(), f->lsim.get()); note_launch();
 
+    tr.mark("7 layout sort");
     // ---- 8. paths and phases
     DevBuf<int32_t> pflag, pidx;
     HDP_TRY(pflag.alloc(n, st));
@@ -754,6 +762,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         HDP_CHECK_LAUNCH();
     }
 
+    tr.mark("8 paths/phases");
     // ---- 9. light-children CSR in layout order
     DevBuf<int32_t> lcc;
     HDP_TRY(lcc.alloc(n + 1, st));
@@ -770,6 +779,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                             f->lc_start.get(), f->lc_list.get()); note_launch();
     HDP_CHECK_LAUNCH();
 
+    tr.mark("9 light children");
     // ---- 10. light parents (positions with light children), phase-major
     {
         DevBuf<int32_t> fl, ex, bnd, pn;
@@ -792,6 +802,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         HDP_TRY(to_host(hl.data(), bnd.get(), f->n_phases + 1, st));
         f->lp_off.assign(hl.begin(), hl.end());
     }
+    tr.mark("10 light parents");
     HDP_CHECK_CUDA(cudaStreamSynchronize(st));
     return HDP_OK;
 }
@@ -841,6 +852,7 @@ __global__ void k_path_meta(int64_t np, const int32_t* __restrict__ list,
 
 static int lanes_finish(hdp_forest* f) {
     cudaStream_t st = f->st;
+    Tracer tr(st);
     const int B = 256;
     const int64_t n = f->n;
     DevBuf<int64_t> rm, nm;
@@ -892,6 +904,7 @@ static int lanes_finish(hdp_forest* f) {
                                                   f->t_doff.get(), f->rowoff.get(),
                                                   f->short_info.get(), f->short_rows.get()); note_launch();
     HDP_CHECK_LAUNCH();
+    tr.mark("lanes finish");
     f->lanes_set = 1;
     f->geom_w = -1;
     return HDP_OK;
@@ -1008,3 +1021,40 @@ int hdp_forest_entries(hdp_forest* f, int64_t* total, int64_t* node_offsets, voi
 void hdp_forest_destroy(hdp_forest* f) { delete f; }
 
 }  // extern "C"
+
+namespace hdp {
+// per pair b: trees = tree_id of its first node .. next pair's first node;
+// stored entries = node offsets over the pair's node range
+__global__ void k_pair_stats(int batch, int64_t npp, int64_t n, int64_t n_trees, int64_t total,
+                             const int32_t* __restrict__ tree_id,
+                             const int64_t* __restrict__ nodeoff, int64_t* out) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    int64_t v0 = (int64_t)b * npp, v1 = v0 + npp;
+    int64_t t0 = tree_id[v0], t1 = v1 < n ? tree_id[v1] : n_trees;
+    int64_t e0 = nodeoff[v0], e1 = v1 < n ? nodeoff[v1] : total;
+    out[b] = t1 - t0;
+    out[batch + b] = e1 - e0;
+}
+}  // namespace hdp
+
+extern "C" int hdp_forest_pair_stats(const hdp_forest* f, int batch, int64_t nodes_per_pair,
+                                     int64_t* n_trees, int64_t* stored, void* stream) {
+    HDP_REQUIRE(f != nullptr && f->lanes_set, HDP_ERR_CONFIG, "forest lanes not set");
+    HDP_REQUIRE(batch >= 1 && (int64_t)batch * nodes_per_pair == f->n, HDP_ERR_CONFIG,
+                "batch x nodes_per_pair must equal the node count");
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf<int64_t> out;
+    HDP_TRY(out.alloc(2 * batch, st));
+    k_pair_stats<<<grid_for(batch, 128), 128, 0, st>>>(batch, nodes_per_pair, f->n, f->n_trees,
+                                                       f->total_entries, f->tree_id.get(),
+                                                       f->nodeoff.get(), out.get()); note_launch();
+    HDP_CHECK_LAUNCH();
+    std::vector<int64_t> h(2 * batch);
+    HDP_TRY(to_host(h.data(), out.get(), 2 * batch, st));
+    for (int b = 0; b < batch; b++) {
+        if (n_trees) n_trees[b] = h[b];
+        if (stored) stored[b] = h[batch + b];
+    }
+    return HDP_OK;
+}

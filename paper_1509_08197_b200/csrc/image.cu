@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "prims.cuh"
@@ -30,6 +32,26 @@ void keep_pool_memory() {
 static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+double Tracer::now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+Tracer::Tracer(cudaStream_t s) : st(s) {
+    const char* e = getenv("HDP_TRACE");
+    on = e && e[0] == '1';
+    if (on) {
+        cudaStreamSynchronize(st);
+        last = now_ms();
+    }
+}
+void Tracer::mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    double t = now_ms();
+    fprintf(stderr, "[hdp] %-28s %8.3f ms\n", what, t - last);
+    last = t;
+}
 
 void set_error(const char* fmt, ...) {
     va_list ap;

@@ -359,13 +359,10 @@ class LevelOut:
 
 
 def _per_pair_stats(f: DeviceForest, batch: int, npp: int, d_max: int):
-    torch = _t()
-    off = f.node_offsets()
-    o = f.export()
-    idx = torch.arange(batch + 1, device=off.device, dtype=torch.int64) * npp
-    stored = (off[idx[1:]] - off[idx[:-1]]).cpu().numpy()
-    tid = torch.cat([o["tree_id"].to(torch.int64), torch.tensor([f.n_trees], device=off.device)])
-    ntrees = (tid[idx[1:]] - tid[idx[:-1]]).cpu().numpy()
+    ntrees = np.zeros(batch, np.int64)
+    stored = np.zeros(batch, np.int64)
+    L.call("hdp_forest_pair_stats", f._h, batch, npp, ntrees.ctypes.data, stored.ctypes.data,
+           L.stream())
     # DisparityForest.search_ratio: mean interval size over pixels / (d+1)
     ratio = np.array([float(s) / npp / (d_max + 1) for s in stored])
     return ntrees, stored, ratio
