@@ -86,7 +86,63 @@ __device__ __forceinline__ int32_t uf_find(int32_t* uf, int32_t x) {
 }
 
 constexpr int DR_THREADS = 1024;
+constexpr int DR_MAXS = 64;      // roots the multi-commit leader can absorb per round
+constexpr int DR_SCAN = 1024;    // window edges the leader may inspect per round
+constexpr int DR_HASH = 256;     // shared-memory hash set of the leader's roots
 
+__device__ __forceinline__ unsigned dr_hash(int32_t x) {
+    return ((unsigned)x * 2654435761u) >> 24;  // top 8 bits
+}
+__device__ __forceinline__ void dr_hash_put(int32_t* h, int32_t x) {
+    unsigned i = dr_hash(x);
+    while (h[i] != -1 && h[i] != x) i = (i + 1) & (DR_HASH - 1);
+    h[i] = x;
+}
+__device__ __forceinline__ bool dr_hash_has(const int32_t* h, int32_t x) {
+    unsigned i = dr_hash(x);
+    while (true) {
+        int32_t v = h[i];
+        if (v == x) return true;
+        if (v == -1) return false;
+        i = (i + 1) & (DR_HASH - 1);
+    }
+}
+
+__device__ __forceinline__ unsigned long long dr_stamp(unsigned round, int pos) {
+    return ((unsigned long long)(round + 1) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos);
+}
+
+__device__ __forceinline__ bool dr_jaccard_ok(const uint32_t* tm, int32_t a, int32_t b, int nw,
+                                              double beta) {
+    int inter = 0, uni = 0;
+    for (int i = 0; i < nw; i++) {
+        uint32_t p = tm[(int64_t)a * nw + i], q = tm[(int64_t)b * nw + i];
+        inter += __popc(p & q);
+        uni += __popc(p | q);
+    }
+    // rule 2: IEEE double division, as hdp_forest.py:195
+    return !(__ddiv_rn((double)inter, (double)uni) < beta);
+}
+
+// merge roots a, b (union by size); returns the surviving root
+__device__ __forceinline__ int32_t dr_union(int32_t* uf, int32_t* usz, uint32_t* tm, int nw,
+                                            int32_t a, int32_t b) {
+    int32_t keep = a, gone = b;
+    if (usz[a] < usz[b]) { keep = b; gone = a; }
+    uf[gone] = keep;
+    usz[keep] += usz[gone];
+    for (int i = 0; i < nw; i++) tm[(int64_t)keep * nw + i] |= tm[(int64_t)gone * nw + i];
+    return keep;
+}
+
+// One CTA per stereo pair.  Per round: (A) every window edge finds its roots
+// and reserves both (atomicMax of a (round, -position) stamp); self-loops are
+// dropped.  (B) an edge holding both reservations has no earlier pending edge
+// touching either tree -> decided now.  (C) multi-commit: the leader of every
+// merge keeps scanning the window in order; the next edge touching its grown
+// component is decided too when its other root is reserved by that very edge
+// (no earlier pending edge touches it), otherwise the leader stops.
+// Compaction keeps the undecided edges, in order, for the next window.
 __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ seg,
                                                    int32_t* __restrict__ order,
                                                    const int32_t* __restrict__ eu,
@@ -96,6 +152,10 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
                                                    uint8_t* in_tree, int* rounds_out) {
     __shared__ int s_warp[DR_THREADS / 32];
     __shared__ int s_total;
+    __shared__ int32_t s_ra[DR_THREADS], s_rb[DR_THREADS], s_e[DR_THREADS];
+    __shared__ uint8_t s_dec[DR_THREADS];
+    __shared__ int32_t s_hash[DR_HASH];
+    __shared__ unsigned long long s_best;
     int b = blockIdx.x;
     int tid = threadIdx.x;
     int lane = tid & 31, wid = tid >> 5;
@@ -104,10 +164,10 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
     while (head < end) {
         int32_t win = min((int32_t)DR_THREADS, end - head);
         bool pend = tid < win;
-        bool decided = false;
-        int32_t e = 0, ra = 0, rb = 0;
-        unsigned long long stamp = ((unsigned long long)(round + 1) << 32) |
-                                   (unsigned long long)(0xffffffffu - (unsigned)tid);
+        bool decided = false, leader = false;
+        int32_t e = 0, ra = 0, rb = 0, keep = 0;
+        unsigned long long stamp = dr_stamp(round, tid);
+        if (tid == 0) s_best = 0ull;
         if (pend) {
             e = order[head + tid];
             ra = uf_find(uf, eu[e]);
@@ -118,6 +178,9 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
                 atomicMax(&res[ra], stamp);
                 atomicMax(&res[rb], stamp);
             }
+            s_ra[tid] = ra;
+            s_rb[tid] = rb;
+            s_e[tid] = e;
         }
         __syncthreads();
         if (pend && !decided) {
@@ -125,26 +188,87 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
             unsigned long long xb = *((volatile unsigned long long*)&res[rb]);
             if (xa == stamp && xb == stamp) {
                 decided = true;
-                int inter = 0, uni = 0;
-                for (int i = 0; i < nw; i++) {
-                    uint32_t p = tm[(int64_t)ra * nw + i], q = tm[(int64_t)rb * nw + i];
-                    inter += __popc(p & q);
-                    uni += __popc(p | q);
-                }
-                // rule 2: IEEE double division, as hdp_forest.py:195
-                if (!(__ddiv_rn((double)inter, (double)uni) < beta)) {
-                    int32_t keep = ra, gone = rb;
-                    if (usz[ra] < usz[rb]) { keep = rb; gone = ra; }
-                    uf[gone] = keep;
-                    usz[keep] += usz[gone];
-                    for (int i = 0; i < nw; i++) tm[(int64_t)keep * nw + i] |= tm[(int64_t)gone * nw + i];
+                if (dr_jaccard_ok(tm, ra, rb, nw, beta)) {
+                    keep = dr_union(uf, usz, tm, nw, ra, rb);
                     in_tree[e] = 1;
+                    leader = true;
                 }
             }
         }
+        if (pend) s_dec[tid] = decided ? 1 : 0;
+        __syncthreads();
+        if (leader) atomicMax(&s_best, ((unsigned long long)usz[keep] << 32) | (unsigned)tid);
+        __syncthreads();
+        // multi-commit for the largest merged tree of the round (the giant
+        // whose edges would otherwise be decided one per round), by warp 0
+        if (wid == 0 && s_best != 0ull) {
+            int lt = (int)(s_best & 0xffffffffu);
+            int32_t root = uf_find(uf, s_ra[lt]);  // the leader's surviving root
+            for (int i = lane; i < DR_HASH; i += 32) s_hash[i] = -1;
+            __syncwarp();
+            if (lane == 0) {
+                dr_hash_put(s_hash, s_ra[lt]);
+                dr_hash_put(s_hash, s_rb[lt]);
+            }
+            int nS = 2;
+            __syncwarp();
+            uint32_t tmk = lane < nw ? tm[(int64_t)root * nw + lane] : 0u;
+            bool grew = false, stop = false;
+            for (int base = lt + 1; base < win && !stop && base < lt + 1 + DR_SCAN; base += 32) {
+                int g = base + lane;
+                bool live = g < win && !s_dec[g];
+                int32_t ga = live ? s_ra[g] : -1, gb = live ? s_rb[g] : -1;
+                bool ia = live && dr_hash_has(s_hash, ga);
+                bool ib = live && dr_hash_has(s_hash, gb);
+                unsigned done = 0u;  // lanes already handled in this chunk
+                while (true) {
+                    unsigned touch = __ballot_sync(0xffffffffu, live && (ia || ib)) & ~done;
+                    if (!touch) break;
+                    int q = __ffs(touch) - 1;
+                    done |= (2u << q) - 1u;  // everything up to q is now in order
+                    int gq = base + q;
+                    bool both = __shfl_sync(0xffffffffu, ia && ib, q);
+                    bool qa = __shfl_sync(0xffffffffu, ia, q);
+                    if (both) {
+                        if (lane == 0) s_dec[gq] = 1;  // now inside one tree
+                        continue;
+                    }
+                    int32_t y = qa ? __shfl_sync(0xffffffffu, gb, q) : __shfl_sync(0xffffffffu, ga, q);
+                    unsigned long long xy = *((volatile unsigned long long*)&res[y]);
+                    uint32_t ty = lane < nw ? tm[(int64_t)y * nw + lane] : 0u;
+                    if (xy != dr_stamp(round, gq)) {  // y has an earlier pending edge
+                        stop = true;
+                        break;
+                    }
+                    int inter = __reduce_add_sync(0xffffffffu, __popc(tmk & ty));
+                    int uni = __reduce_add_sync(0xffffffffu, __popc(tmk | ty));
+                    if (lane == 0) s_dec[gq] = 1;
+                    if (!(__ddiv_rn((double)inter, (double)uni) < beta)) {
+                        tmk |= ty;
+                        grew = true;
+                        if (lane == 0) {
+                            uf[y] = root;  // the giant's root stays the root
+                            usz[root] += usz[y];
+                            in_tree[s_e[gq]] = 1;
+                            dr_hash_put(s_hash, y);
+                        }
+                        nS++;
+                        // later edges of this chunk that touch y now touch the tree
+                        ia |= ga == y;
+                        ib |= gb == y;
+                        __syncwarp();
+                        if (nS == DR_MAXS) {
+                            stop = true;
+                            break;
+                        }
+                    }
+                }
+            }
+            if (grew && lane < nw) tm[(int64_t)root * nw + lane] = tmk;
+        }
         __syncthreads();
         // stable compaction of the undecided window edges
-        bool keepme = pend && !decided;
+        bool keepme = pend && !s_dec[tid];
         unsigned bal = __ballot_sync(0xffffffffu, keepme);
         if (lane == 0) s_warp[wid] = __popc(bal);
         __syncthreads();
@@ -195,6 +319,7 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
     HDP_REQUIRE(batch >= 1 && batch <= 255, HDP_ERR_CONFIG, "batch must be in [1, 255]");
     HDP_REQUIRE(edges_per_pair < (1 << 24), HDP_ERR_CONFIG, "too many edges per pair for HDPF keys");
     HDP_REQUIRE(nw >= 1 && n_rows >= 1, HDP_ERR_CONFIG, "empty interval table");
+    HDP_REQUIRE(nw <= 8, HDP_ERR_CONFIG, "disparity range above 255 not supported by the HDPF kernel");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = (int64_t)batch * nodes_per_pair;
     const int64_t m = (int64_t)batch * edges_per_pair;
