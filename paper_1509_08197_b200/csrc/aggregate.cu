@@ -8,21 +8,28 @@
 //   down: A(root) = A_up(root);  A(v) = s_v A(parent) + (1 - s_v^2) A_up(v)
 //
 // Work follows the heavy-path layout of forest.cu (phases = light depth,
-// every heavy path contiguous, rows of one path contiguous because all its
-// nodes share the tree's lane count m).  Per phase:
-//   up   : k_bcompute   b(v) = E(v) + sum_{light c} s_c A_up(c) for all nodes of
-//                       the phase in parallel (E recomputed from the images)
-//          k_scan_up    A_up(v) = b(v) + s_h A_up(h) along every path of length
-//                       >= 2: one warp per (path, 32 lanes), chunks of 32 nodes
-//                       staged with cp.async (double buffered) so the
-//                       recurrence runs from shared memory at FMA latency
-//   down : k_down_long  the same walk head -> tail, plus the per-node argmin
-//                       (transpose butterfly, 31 shuffles per 32 nodes)
-//          k_down_short single-node paths, fully parallel
-// A is written back in place only where a light child will read it.  All
-// per-position / per-path metadata is pre-packed (forest.cu lanes_finish) so
-// every thread starts from one or two independent loads.
+// every heavy path contiguous, the rows of one path contiguous because all
+// its nodes share the tree's lane count m).  Per phase:
+//   up   : k_ecompute   b(v) = E(v), all nodes of the phase in parallel (E
+//                       recomputed from the packed image planes)
+//          k_light      b(v) += sum_{light c} s_c A_up(c) for light parents
+//          k_seg_up     A_up(v) = b(v) + s_h A_up(h) along paths > kShortPath
+//                       nodes, cut into kSeg-node segments, one warp per
+//                       (segment, 32 lanes): the segment is staged into shared
+//                       memory with cp.async, a local pass yields its carry
+//                       map (scalar product P, local value), carries are
+//                       chained tail -> head by decoupled look-back (warps take
+//                       segments by ticket, so a warp only waits on earlier
+//                       tickets), and a second pass from shared memory writes
+//                       the results
+//          k_scan_up_short  register-resident walk of paths <= kShortPath
+//   down : k_seg_down   the same for A (head -> tail), fused with the per-node
+//                       first argmin (transpose butterfly, 31 shuffles / 32 nodes)
+//          k_down_short short paths
+// A is written back in place only where a light child will read it.
 #include <cuda_runtime.h>
+
+#include <atomic>
 
 #include "forest.cuh"
 #include "prims.cuh"
@@ -35,8 +42,9 @@ struct AggArgs {
     const int32_t* lc_start;
     const int64_t* lc_row;
     const float* lc_sim;
-    const int4* pinfo;      // per path of the launch list
-    const longlong2* prows;
+    const int4* pinfo;      // per path of the launch list: (start, len, m, lane offset)
+    const longlong2* prows; // (first row, parent's row or -1)
+    const int2* seg_tab;    // (long-path index, segment index from the head)
     const int32_t* dlist;
     const int64_t* rowoff;
     const int32_t* lp_list;
@@ -52,10 +60,15 @@ struct AggArgs {
     float* aup;
     float* volume;
     unsigned long long* keys;
+    unsigned long long* carry;  // per (segment, lane): (epoch << 32 | f32 bits), the
+                                // epoch tag doubles as the readiness flag
+    unsigned epoch_up, epoch_down;
+    int* tickets;        // per (phase, pass, group)
     int groups;  // 32-lane groups per node when sub == 32
     int sub;     // lanes per item for the packed mappings (power of 2 <= 32)
     int sub_shift;
     int atomic_keys;
+    int max_m;
 };
 
 __device__ __forceinline__ int lane_disp(const AggArgs& a, int doff, int j) {
@@ -93,10 +106,7 @@ __device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool p
                  : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // Thread -> (item, lane j).  With sub < 32 (a power of two) several items
 // share a warp, `sub` lanes each; otherwise one warp covers 32 lanes of one
@@ -193,65 +203,105 @@ __global__ void __launch_bounds__(256) k_scan_up_short(AggArgs a, int64_t s0, in
     }
 }
 
-constexpr int CH = 32;  // nodes per staged chunk
+// ---------------------------------------------------------------- segments
 
-// A_up along paths of length >= 2, tail -> head, in place over b.
-__global__ void __launch_bounds__(128) k_scan_up(AggArgs a, int64_t l0, int64_t nl) {
-    __shared__ float buf[4][2][CH][32];
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int g = (int)blockIdx.y;
-    if (li >= nl) return;
-    int4 info = a.pinfo[l0 + li];
-    int64_t row0 = a.prows[l0 + li].x;
-    int32_t start = info.x, len = info.y;
-    int m = info.z;
-    if (g * 32 >= m) return;
-    int j = g * 32 + lane;
-    bool act = j < m;
-    float* aup = a.aup;
-    auto stage = [&](int bi, int32_t lo, int cnt) {
-        for (int i = 0; i < cnt; i++)
-            cp_async4(&buf[warp][bi][i][lane], aup + row0 + (int64_t)(lo + i - start) * m + j, act);
-        cp_commit();
-    };
-    int32_t end = start + len;
-    int32_t hi = end;
-    int32_t lo = max(start, hi - CH);
-    int bi = 0;
-    stage(0, lo, hi - lo);
-    float sim_l = (lane < hi - lo) ? fabsf(a.lsimf[lo + lane]) : 0.0f;
-    float x_prev = 0.0f, s_next = 0.0f;
+struct SegCtx {
+    int32_t start, len, m, doff;
+    int64_t row0, prow;
+    int32_t a, b;    // segment node range [a, b) (layout positions)
+    int s, nseg;
+    int64_t gseg;    // global segment index
+};
+
+__device__ __forceinline__ SegCtx seg_ctx(const AggArgs& a, int64_t gseg) {
+    int2 st = a.seg_tab[gseg];
+    int4 info = a.pinfo[st.x];
+    longlong2 rows = a.prows[st.x];
+    SegCtx c;
+    c.start = info.x;
+    c.len = info.y;
+    c.m = info.z;
+    c.doff = info.w;
+    c.row0 = rows.x;
+    c.prow = rows.y;
+    c.s = st.y;
+    c.nseg = (c.len + kSeg - 1) / kSeg;
+    c.a = c.start + c.s * kSeg;
+    c.b = min(c.start + c.len, c.a + kSeg);
+    c.gseg = gseg;
+    return c;
+}
+
+__device__ __forceinline__ int warp_ticket(int* ctr) {
+    int t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(ctr, 1);
+    return __shfl_sync(0xffffffffu, t, 0);
+}
+
+// Carry words hold (epoch << 32 | value bits): a 64-bit store is a single
+// transaction, so a reader that sees the epoch also sees the value -- no
+// separate flag and no fences on the chain (decoupled look-back, flag in data).
+__device__ __forceinline__ void put_carry(unsigned long long* p, unsigned epoch, float v) {
+    unsigned long long w = ((unsigned long long)epoch << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+
+__device__ __forceinline__ float get_carry(const unsigned long long* p, unsigned epoch) {
+    unsigned long long w;
     while (true) {
-        int cnt = hi - lo;
-        int32_t nhi = lo, nlo = max(start, lo - CH);
-        bool more = nhi > start;
-        float sim_n = 0.0f;
-        if (more) {
-            stage(bi ^ 1, nlo, nhi - nlo);
-            sim_n = (lane < nhi - nlo) ? fabsf(a.lsimf[nlo + lane]) : 0.0f;
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
-        }
-        __syncwarp();
-        for (int i = cnt - 1; i >= 0; i--) {
-            float x = buf[warp][bi][i][lane] + s_next * x_prev;
-            if (act) aup[row0 + (int64_t)(lo + i - start) * m + j] = x;
-            x_prev = x;
-            s_next = __shfl_sync(0xffffffffu, sim_l, i);
-        }
-        __syncwarp();
-        if (!more) break;
-        hi = nhi;
-        lo = nlo;
-        bi ^= 1;
-        sim_l = sim_n;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+        if ((unsigned)(w >> 32) == epoch) break;
+        __nanosleep(20);
+    }
+    return __uint_as_float((unsigned)(w & 0xffffffffu));
+}
+
+// Up pass over one segment (tail -> head).  Segments are taken by ticket in
+// reverse table order, so a path's tail segment comes first; the carry is
+// X_a = x_loc(a) + P * X_b with P = prod s_{a+1..b}.
+__global__ void __launch_bounds__(128) k_seg_up(AggArgs a, int64_t g0, int64_t ng, int* ctr) {
+    __shared__ float buf[4][kSeg][32];
+    __shared__ float ssim[4][kSeg + 1];
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int g = (int)blockIdx.y;
+    int t = warp_ticket(ctr + g);
+    if (t >= ng) return;
+    SegCtx c = seg_ctx(a, g0 + ng - 1 - t);
+    if (g * 32 >= c.m) return;
+    int j = g * 32 + lane;
+    bool act = j < c.m;
+    int cnt = c.b - c.a;
+    const float* base = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.m + j;
+    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], base + (int64_t)i * c.m, act);
+    cp_commit();
+    bool has_next = c.b < c.start + c.len;  // a segment toward the tail exists
+    for (int i = lane; i <= cnt; i += 32) {
+        int p = c.a + i;
+        ssim[warp][i] = (i < cnt || has_next) ? fabsf(a.lsimf[p]) : 0.0f;
+    }
+    cp_wait_all();
+    __syncwarp();
+    // local pass with X_b = 0: x_loc(a) and P = prod_{t=a+1..b} s_t
+    float x = 0.0f, P = 1.0f;
+    for (int i = cnt - 1; i >= 0; i--) {
+        float sn = ssim[warp][i + 1];  // s of the node after i (0 past the tail)
+        x = buf[warp][i][lane] + sn * x;
+        P *= sn;
+    }
+    float Xb = 0.0f;
+    if (has_next && act) Xb = get_carry(a.carry + (c.gseg + 1) * a.max_m + j, a.epoch_up);
+    if (act && c.s > 0) put_carry(a.carry + c.gseg * a.max_m + j, a.epoch_up, x + P * Xb);
+    // final pass: exact recurrence from the true X_b
+    x = Xb;
+    float* out = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.m + j;
+    for (int i = cnt - 1; i >= 0; i--) {
+        x = buf[warp][i][lane] + ssim[warp][i + 1] * x;
+        if (act) out[(int64_t)i * c.m] = x;
     }
 }
 
 // warp transpose butterfly: lane l ends with the minimum key of node l
-__device__ __forceinline__ unsigned long long warp_min_per_node(unsigned long long (&key)[CH],
+__device__ __forceinline__ unsigned long long warp_min_per_node(unsigned long long (&key)[32],
                                                                 int lane) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -267,17 +317,8 @@ __device__ __forceinline__ unsigned long long warp_min_per_node(unsigned long lo
     return key[0];
 }
 
-__device__ __forceinline__ unsigned long long warp_min(unsigned long long k) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        unsigned long long other = __shfl_xor_sync(0xffffffffu, k, o);
-        k = other < k ? other : k;
-    }
-    return k;
-}
-
 // First argmin of (cost, d) over the lanes of one item: `width` lanes
-// (power of two, aligned) or the full warp.  32-bit redux/shuffle min on the
+// (power of two, aligned) or the full warp.  32-bit shuffle min on the
 // order-preserving cost, then the lowest lane holding it (lanes are in
 // ascending disparity order) supplies d.  Every lane gets the packed key.
 __device__ __forceinline__ unsigned long long group_argmin(bool act, float y, int d, int width,
@@ -303,102 +344,70 @@ __device__ __forceinline__ void store_key(const AggArgs& a, int32_t node, unsign
         a.keys[node] = k;
 }
 
-// A along paths of length >= 2, head -> tail, fused with the argmin.
-__global__ void __launch_bounds__(128) k_down_long(AggArgs a, int64_t l0, int64_t nl) {
-    __shared__ float buf[4][2][CH][32];
+// Down pass over one segment (head -> tail) fused with the argmin.  The
+// carry is Y_end = y_loc(b-1) + Q * Y_in with Q = prod_{t=a..b-1} s_t; the
+// head of a root path uses s = 0 so that A(root) = A_up(root).
+__global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t ng, int* ctr) {
+    __shared__ float buf[4][kSeg][32];
+    __shared__ float ssim[4][kSeg];
+    __shared__ int32_t snode[4][kSeg];
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t li = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int g = (int)blockIdx.y;
-    if (li >= nl) return;
-    int4 info = a.pinfo[l0 + li];
-    longlong2 rows = a.prows[l0 + li];
-    int32_t start = info.x, len = info.y;
-    int m = info.z;
-    if (g * 32 >= m) return;
+    int t = warp_ticket(ctr + g);
+    if (t >= ng) return;
+    SegCtx c = seg_ctx(a, g0 + t);
+    if (g * 32 >= c.m) return;
     int j = g * 32 + lane;
-    bool act = j < m;
-    int d = act ? lane_disp(a, info.w, j) : 0;
-    int64_t row0 = rows.x;
-    bool root_path = rows.y < 0;
-    float* aup = a.aup;
-    float y = 0.0f;
-    if (!root_path && act) y = aup[rows.y + j];  // A(parent), stored in place
-    auto stage = [&](int bi, int32_t lo, int cnt) {
-        for (int i = 0; i < cnt; i++)
-            cp_async4(&buf[warp][bi][i][lane], aup + row0 + (int64_t)(lo + i - start) * m + j, act);
-        cp_commit();
-    };
-    auto meta = [&](int32_t lo, int cnt, float& simf, int32_t& node) {
-        bool in = lane < cnt;
-        simf = in ? a.lsimf[lo + lane] : 0.0f;
-        node = in ? a.lmeta[lo + lane].x : 0;
-    };
-    int32_t end = start + len;
-    int32_t lo = start, hi = min(end, start + CH);
-    int bi = 0;
-    stage(0, lo, hi - lo);
-    float simf_l;
-    int32_t node_l;
-    meta(lo, hi - lo, simf_l, node_l);
-    while (true) {
-        int cnt = hi - lo;
-        int32_t nlo = hi, nhi = min(end, hi + CH);
-        bool more = nlo < end;
-        float simf_n = 0.0f;
-        int32_t node_n = 0;
-        if (more) {
-            stage(bi ^ 1, nlo, nhi - nlo);
-            meta(nlo, nhi - nlo, simf_n, node_n);
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
-        }
-        __syncwarp();
-        unsigned light = __ballot_sync(0xffffffffu, signbit(simf_l));
-        if (cnt <= 4) {
-            // short chunk: one warp reduction per node
-            for (int i = 0; i < cnt; i++) {
-                float sf = __shfl_sync(0xffffffffu, simf_l, i);
-                float s = fabsf(sf);
-                float u = buf[warp][bi][i][lane];
-                if (root_path && lo + i == start)
-                    y = u;
-                else
-                    y = s * y + (1.0f - s * s) * u;
-                int64_t row = row0 + (int64_t)(lo + i - start) * m;
-                if (act && (((light >> i) & 1u) || a.volume)) aup[row + j] = y;
-                unsigned long long k = group_argmin(act, y, d, 32, lane);
-                int32_t nd = __shfl_sync(0xffffffffu, node_l, i);
-                if (lane == 0) store_key(a, nd, k);
-            }
-        } else {
-            unsigned long long key[CH];
+    bool act = j < c.m;
+    int d = act ? lane_disp(a, c.doff, j) : 0;
+    int cnt = c.b - c.a;
+    float* rows = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.m + j;
+    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], rows + (int64_t)i * c.m, act);
+    cp_commit();
+    unsigned light[2] = {0u, 0u};
+    for (int i = lane, h = 0; i < kSeg; i += 32, h++) {
+        float sf = i < cnt ? a.lsimf[c.a + i] : 0.0f;
+        float sv = fabsf(sf);
+        if (c.a + i == c.start && c.prow < 0) sv = 0.0f;  // root: A = A_up
+        ssim[warp][i] = sv;
+        snode[warp][i] = i < cnt ? a.lmeta[c.a + i].x : 0;
+        light[h] = __ballot_sync(0xffffffffu, i < cnt && signbit(sf));
+    }
+    cp_wait_all();
+    __syncwarp();
+    // local pass with Y_in = 0: y_loc(b-1) and Q = prod_{t=a..b-1} s_t
+    float yl = 0.0f, Q = 1.0f;
+    for (int i = 0; i < cnt; i++) {
+        float sv = ssim[warp][i];
+        yl = sv * yl + (1.0f - sv * sv) * buf[warp][i][lane];
+        Q *= sv;
+    }
+    float Yin = 0.0f;
+    if (c.s == 0) {
+        if (c.prow >= 0 && act) Yin = a.aup[c.prow + j];  // A(parent), stored in place
+    } else if (act) {
+        Yin = get_carry(a.carry + (c.gseg - 1) * a.max_m + j, a.epoch_down);
+    }
+    // publish the tail-end carry before the final pass
+    if (act && c.s + 1 < c.nseg) put_carry(a.carry + c.gseg * a.max_m + j, a.epoch_down, yl + Q * Yin);
+    // final pass from the true Y_in
+    float y = Yin;
+    for (int h = 0; h * 32 < cnt; h++) {
+        unsigned long long key[32];
 #pragma unroll
-            for (int i = 0; i < CH; i++) {
-                float s = fabsf(__shfl_sync(0xffffffffu, simf_l, i));
-                if (i < cnt) {
-                    float u = buf[warp][bi][i][lane];
-                    if (root_path && lo + i == start)
-                        y = u;
-                    else
-                        y = s * y + (1.0f - s * s) * u;
-                    int64_t row = row0 + (int64_t)(lo + i - start) * m;
-                    if (act && (((light >> i) & 1u) || a.volume)) aup[row + j] = y;
-                    key[i] = act ? pack_key(y, d) : ~0ull;
-                } else {
-                    key[i] = ~0ull;
-                }
+        for (int q = 0; q < 32; q++) {
+            int i = h * 32 + q;
+            if (i < cnt) {
+                float sv = ssim[warp][i];
+                y = sv * y + (1.0f - sv * sv) * buf[warp][i][lane];
+                if (act && (((light[h] >> q) & 1u) || a.volume)) rows[(int64_t)i * c.m] = y;
+                key[q] = act ? pack_key(y, d) : ~0ull;
+            } else {
+                key[q] = ~0ull;
             }
-            unsigned long long best = warp_min_per_node(key, lane);
-            if (lane < cnt) store_key(a, node_l, best);
         }
-        __syncwarp();
-        if (!more) break;
-        lo = nlo;
-        hi = nhi;
-        bi ^= 1;
-        simf_l = simf_n;
-        node_l = node_n;
+        unsigned long long best = warp_min_per_node(key, lane);
+        if (h * 32 + lane < cnt) store_key(a, snode[warp][h * 32 + lane], best);
     }
 }
 
@@ -521,6 +530,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.lc_sim = f->lc_sim.get();
     a.pinfo = nullptr;
     a.prows = nullptr;
+    a.seg_tab = f->seg_tab.get();
     a.dlist = f->dlist.get();
     a.rowoff = f->rowoff.get();
     a.lp_list = f->lp_list.get();
@@ -538,12 +548,28 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.border = (1.0f - alpha) * tau_c + alpha * tau_g;
     a.volume = volume;
     a.groups = (f->max_m + 31) / 32;
+    a.max_m = f->max_m;
     a.sub = f->max_m <= 16 ? pow2_at_least(f->max_m) : 32;
     a.sub_shift = 0;
     while ((1 << a.sub_shift) < a.sub) a.sub_shift++;
     DevBuf<float> aup;
+    DevBuf<unsigned long long> carry;
+    DevBuf<int> tickets;
     HDP_TRY(aup.alloc(f->total_entries + 32, st));
     a.aup = aup.get();
+    const int64_t nseg = f->n_segs;
+    HDP_TRY(carry.alloc(nseg * a.max_m + 1, st));
+    HDP_TRY(tickets.alloc(2 * f->n_phases * a.groups + 1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(tickets.get(), 0,
+                                   sizeof(int) * (2 * f->n_phases * a.groups + 1), st));
+    // fresh epochs per call: stale words in recycled pool memory never match
+    static std::atomic<unsigned> g_epoch{1};
+    unsigned ep = g_epoch.fetch_add(2);
+    if (ep == 0u || ep + 1 == 0u) ep = g_epoch.fetch_add(2);
+    a.carry = carry.get();
+    a.epoch_up = ep;
+    a.epoch_down = ep + 1;
+    a.tickets = tickets.get();
     DevBuf<unsigned long long> kbuf;
     unsigned long long* kp = (unsigned long long*)keys;
     if (!kp) {
@@ -561,7 +587,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         k_keys_init<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp); note_launch();
     }
 
-    AggArgs lg = a;  // long-path kernels: one warp per (path, 32 lanes)
+    AggArgs lg = a;  // segment kernels: one warp per (segment, 32 lanes)
     lg.sub = 32;
     lg.pinfo = f->long_info.get();
     lg.prows = f->long_rows.get();
@@ -577,9 +603,10 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         if (np > 0) {
             k_light<<<packed_grid(a, np, 1, 256), 256, 0, st>>>(a, p0, np); note_launch();
         }
-        int64_t l0 = f->long_off[r], nl = f->long_off[r + 1] - l0;
-        if (nl > 0) {
-            k_scan_up<<<dim3(grid_for(nl * 32, 128), lg.groups), 128, 0, st>>>(lg, l0, nl); note_launch();
+        int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
+        if (ng > 0) {
+            k_seg_up<<<dim3(grid_for(ng * 32, 128), lg.groups), 128, 0, st>>>(
+                lg, g0, ng, a.tickets + (2 * r) * a.groups); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (ns > 0) {
@@ -588,9 +615,10 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     }
     HDP_CHECK_LAUNCH();
     for (int64_t r = 0; r < f->n_phases; r++) {
-        int64_t l0 = f->long_off[r], nl = f->long_off[r + 1] - l0;
-        if (nl > 0) {
-            k_down_long<<<dim3(grid_for(nl * 32, 128), lg.groups), 128, 0, st>>>(lg, l0, nl); note_launch();
+        int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
+        if (ng > 0) {
+            k_seg_down<<<dim3(grid_for(ng * 32, 128), lg.groups), 128, 0, st>>>(
+                lg, g0, ng, a.tickets + (2 * r + 1) * a.groups); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (ns > 0) {

@@ -287,6 +287,21 @@ __global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
     idx[v] = (int32_t)v;
 }
 
+__global__ void k_seg_count(int64_t nl, const int32_t* __restrict__ long_paths,
+                            const int32_t* __restrict__ p_len, int32_t* nseg) {
+    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < nl) nseg[l] = (p_len[long_paths[l]] + kSeg - 1) / kSeg;
+    else if (l == nl) nseg[l] = 0;
+}
+
+__global__ void k_seg_fill(int64_t nl, const int32_t* __restrict__ nseg,
+                           const int32_t* __restrict__ soff, int2* seg_tab) {
+    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= nl) return;
+    int32_t o = soff[l];
+    for (int s = 0; s < nseg[l]; s++) seg_tab[o + s] = make_int2((int)l, s);
+}
+
 __global__ void k_lp_flags(int64_t n, const int32_t* __restrict__ lc_start, int32_t* fl) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) fl[k] = lc_start[k + 1] > lc_start[k] ? 1 : 0;
@@ -760,6 +775,30 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                              f->long_paths.get(),
                                                              f->short_paths.get()); note_launch();
         HDP_CHECK_LAUNCH();
+        // segments of kSeg nodes over the long paths (head first), phase-major
+        int64_t nl = f->long_off[f->n_phases];
+        DevBuf<int32_t> nseg, soff, sb, sbh;
+        HDP_TRY(nseg.alloc(nl + 1, st));
+        HDP_TRY(soff.alloc(nl + 1, st));
+        k_seg_count<<<grid_for(nl + 1, B), B, 0, st>>>(nl, f->long_paths.get(), f->p_len.get(),
+                                                       nseg.get()); note_launch();
+        HDP_TRY(exclusive_sum(nseg.get(), soff.get(), nl + 1, st));
+        int32_t ns_total = 0;
+        HDP_TRY(to_host(&ns_total, soff.get() + nl, 1, st));
+        f->n_segs = ns_total;
+        HDP_TRY(f->seg_tab.alloc(ns_total + 1, st));
+        if (nl > 0)
+            k_seg_fill<<<grid_for(nl, B), B, 0, st>>>(nl, nseg.get(), soff.get(), f->seg_tab.get()); note_launch();
+        std::vector<int32_t> lo(f->n_phases + 1), so(f->n_phases + 1);
+        for (int64_t r = 0; r <= f->n_phases; r++) lo[r] = (int32_t)f->long_off[r];
+        HDP_TRY(sb.alloc(f->n_phases + 1, st));
+        HDP_TRY(sbh.alloc(f->n_phases + 1, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(sb.get(), lo.data(), sizeof(int32_t) * (f->n_phases + 1),
+                                       cudaMemcpyHostToDevice, st));
+        k_gather_i32<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(f->n_phases + 1, soff.get(),
+                                                                   sb.get(), sbh.get()); note_launch();
+        HDP_TRY(to_host(so.data(), sbh.get(), f->n_phases + 1, st));
+        f->seg_off.assign(so.begin(), so.end());
     }
 
     tr.mark("8 paths/phases");

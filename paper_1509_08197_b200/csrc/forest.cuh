@@ -9,6 +9,9 @@
 // Heavy paths of at most this many nodes are aggregated register-resident
 // (one thread per (path, lane)); longer ones by a warp walking staged chunks.
 constexpr int kShortPath = 8;
+// Long paths are cut into segments of kSeg nodes, one warp each, chained by
+// decoupled look-back in the aggregation kernels.
+constexpr int kSeg = 64;
 
 struct hdp_forest {
     cudaStream_t st = nullptr;
@@ -39,6 +42,9 @@ struct hdp_forest {
     // each list phase-major; host offsets per phase
     hdp::DevBuf<int32_t> long_paths, short_paths;
     std::vector<int64_t> long_off, short_off;
+    hdp::DevBuf<int2> seg_tab;      // (long-path index, segment index from the head)
+    std::vector<int64_t> seg_off;   // host: segments of phase r = [seg_off[r], seg_off[r+1])
+    int64_t n_segs = 0;
 
     // disparity lanes per tree
     int lanes_set = 0;
