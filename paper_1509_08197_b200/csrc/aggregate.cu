@@ -164,41 +164,62 @@ __global__ void __launch_bounds__(256) k_ecompute(AggArgs a, int64_t k0, int64_t
 
 // b(v) += sum_{light children c} s_c A_up(c) for the phase's light parents
 // (children in ascending id order, their A_up final since the deeper phase).
+// PU parents per thread; the first child of each is gathered up front.
 __global__ void __launch_bounds__(256) k_light(AggArgs a, int64_t p0, int64_t np) {
     Slot s = slot_of(a);
-    if (s.item >= np) return;
-    int32_t k = a.lp_list[p0 + s.item];
-    int4 mt = a.lmeta[k];
-    if (s.j >= mt.w) return;
-    int64_t row = a.rowoff[k];
-    int32_t c0 = a.lc_start[k], c1 = a.lc_start[k + 1];
-    float x = 0.0f;
-    for (int32_t q = c0; q < c1; q++) x += a.lc_sim[q] * a.aup[a.lc_row[q] + s.j];
-    a.aup[row + s.j] += x;
+    int32_t k[4], c0[4], c1[4];
+    int m[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        int64_t it = s.item * 4 + u;
+        ok[u] = it < np;
+        k[u] = ok[u] ? a.lp_list[p0 + it] : 0;
+        m[u] = a.lmeta[k[u]].w;
+        c0[u] = a.lc_start[k[u]];
+        c1[u] = a.lc_start[k[u] + 1];
+        ok[u] = ok[u] && s.j < m[u];
+    }
+    float first[4], bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        first[u] = ok[u] ? a.lc_sim[c0[u]] * a.aup[a.lc_row[c0[u]] + s.j] : 0.0f;
+        bv[u] = ok[u] ? a.aup[a.rowoff[k[u]] + s.j] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        if (!ok[u]) continue;
+        float x = first[u];
+        for (int32_t q = c0[u] + 1; q < c1[u]; q++) x += a.lc_sim[q] * a.aup[a.lc_row[q] + s.j];
+        a.aup[a.rowoff[k[u]] + s.j] = bv[u] + x;
+    }
 }
 
-// A_up along short paths (2..kShortPath nodes), one thread per (path, lane),
-// values in registers.
+// A_up along short paths (2..kShortPath nodes), one thread per (PU paths,
+// lane), values in registers.
 __global__ void __launch_bounds__(256) k_scan_up_short(AggArgs a, int64_t s0, int64_t ns) {
     Slot s = slot_of(a);
-    if (s.item >= ns) return;
-    int4 info = a.pinfo[s0 + s.item];
-    int len = info.y, m = info.z;
-    if (len < 2 || s.j >= m) return;
-    int64_t row0 = a.prows[s0 + s.item].x;
-    float b[kShortPath], sim[kShortPath];
+    for (int u = 0; u < 4; u++) {
+        int64_t it = s.item * 4 + u;
+        if (it >= ns) return;
+        int4 info = a.pinfo[s0 + it];
+        int len = info.y, m = info.z;
+        if (len < 2 || s.j >= m) continue;
+        int64_t row0 = a.prows[s0 + it].x;
+        float b[kShortPath], sim[kShortPath];
 #pragma unroll
-    for (int u = 0; u < kShortPath; u++) {
-        b[u] = u < len ? a.aup[row0 + (int64_t)u * m + s.j] : 0.0f;
-        sim[u] = u < len ? fabsf(a.lsimf[info.x + u]) : 0.0f;
-    }
-    float x = 0.0f;
+        for (int q = 0; q < kShortPath; q++) {
+            b[q] = q < len ? a.aup[row0 + (int64_t)q * m + s.j] : 0.0f;
+            sim[q] = q < len ? fabsf(a.lsimf[info.x + q]) : 0.0f;
+        }
+        float x = 0.0f;
 #pragma unroll
-    for (int u = kShortPath - 1; u >= 0; u--) {
-        if (u < len) {
-            float sn = (u + 1 < len) ? sim[u + 1] : 0.0f;
-            x = b[u] + sn * x;
-            a.aup[row0 + (int64_t)u * m + s.j] = x;
+        for (int q = kShortPath - 1; q >= 0; q--) {
+            if (q < len) {
+                float sn = (q + 1 < len) ? sim[q + 1] : 0.0f;
+                x = b[q] + sn * x;
+                a.aup[row0 + (int64_t)q * m + s.j] = x;
+            }
         }
     }
 }
@@ -344,13 +365,13 @@ __device__ __forceinline__ void store_key(const AggArgs& a, int32_t node, unsign
         a.keys[node] = k;
 }
 
-// Down pass over one segment (head -> tail) fused with the argmin.  The
-// carry is Y_end = y_loc(b-1) + Q * Y_in with Q = prod_{t=a..b-1} s_t; the
-// head of a root path uses s = 0 so that A(root) = A_up(root).
+// Down pass over one segment (head -> tail).  The carry is
+// Y_end = y_loc(b-1) + Q * Y_in with Q = prod_{t=a..b-1} s_t; the head of a
+// root path uses s = 0 so that A(root) = A_up(root).  A is stored in place
+// for every node; the argmin runs afterwards in k_wta.
 __global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t ng, int* ctr) {
     __shared__ float buf[4][kSeg][32];
     __shared__ float ssim[4][kSeg];
-    __shared__ int32_t snode[4][kSeg];
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int g = (int)blockIdx.y;
     int t = warp_ticket(ctr + g);
@@ -359,19 +380,14 @@ __global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t
     if (g * 32 >= c.m) return;
     int j = g * 32 + lane;
     bool act = j < c.m;
-    int d = act ? lane_disp(a, c.doff, j) : 0;
     int cnt = c.b - c.a;
     float* rows = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.m + j;
     for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], rows + (int64_t)i * c.m, act);
     cp_commit();
-    unsigned light[2] = {0u, 0u};
-    for (int i = lane, h = 0; i < kSeg; i += 32, h++) {
-        float sf = i < cnt ? a.lsimf[c.a + i] : 0.0f;
-        float sv = fabsf(sf);
+    for (int i = lane; i < cnt; i += 32) {
+        float sv = fabsf(a.lsimf[c.a + i]);
         if (c.a + i == c.start && c.prow < 0) sv = 0.0f;  // root: A = A_up
         ssim[warp][i] = sv;
-        snode[warp][i] = i < cnt ? a.lmeta[c.a + i].x : 0;
-        light[h] = __ballot_sync(0xffffffffu, i < cnt && signbit(sf));
     }
     cp_wait_all();
     __syncwarp();
@@ -390,73 +406,88 @@ __global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t
     }
     // publish the tail-end carry before the final pass
     if (act && c.s + 1 < c.nseg) put_carry(a.carry + c.gseg * a.max_m + j, a.epoch_down, yl + Q * Yin);
-    // final pass from the true Y_in
     float y = Yin;
-    for (int h = 0; h * 32 < cnt; h++) {
-        unsigned long long key[32];
-#pragma unroll
-        for (int q = 0; q < 32; q++) {
-            int i = h * 32 + q;
-            if (i < cnt) {
-                float sv = ssim[warp][i];
-                y = sv * y + (1.0f - sv * sv) * buf[warp][i][lane];
-                if (act && (((light[h] >> q) & 1u) || a.volume)) rows[(int64_t)i * c.m] = y;
-                key[q] = act ? pack_key(y, d) : ~0ull;
-            } else {
-                key[q] = ~0ull;
-            }
-        }
-        unsigned long long best = warp_min_per_node(key, lane);
-        if (h * 32 + lane < cnt) store_key(a, snode[warp][h * 32 + lane], best);
+    for (int i = 0; i < cnt; i++) {
+        float sv = ssim[warp][i];
+        y = sv * y + (1.0f - sv * sv) * buf[warp][i][lane];
+        if (act) rows[(int64_t)i * c.m] = y;
     }
 }
 
 // Short paths (1..kShortPath nodes): A = s A(parent) + (1 - s^2) A_up head ->
-// tail in registers, then the per-node argmin across the item's lanes.
+// tail, stored in place.  Each thread takes 4 consecutive paths and issues
+// the first-node loads of all of them up front (most have a single node).
 __global__ void __launch_bounds__(256) k_down_short(AggArgs a, int64_t s0, int64_t ns) {
     Slot s = slot_of(a);
-    int lane = threadIdx.x & 31;
-    bool valid = s.item < ns;
-    int len = 0, m = 0, start = 0, d = 0;
-    int64_t row0 = 0, prow = -1;
-    if (valid) {
-        int4 info = a.pinfo[s0 + s.item];
-        longlong2 rows = a.prows[s0 + s.item];
-        start = info.x;
-        len = info.y;
-        m = info.z;
-        row0 = rows.x;
-        prow = rows.y;
-        if (s.j < m) d = lane_disp(a, info.w, s.j);
+    int4 info[4];
+    longlong2 rows[4];
+    bool act[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        int64_t it = s.item * 4 + u;
+        bool valid = it < ns;
+        info[u] = valid ? a.pinfo[s0 + it] : make_int4(0, 0, 0, 0);
+        rows[u] = valid ? a.prows[s0 + it] : make_longlong2(0, -1);
+        act[u] = valid && s.j < info[u].z;
     }
-    bool act = valid && s.j < m;
-    float u[kShortPath], sf[kShortPath];
-    int32_t nd[kShortPath];
+    float u0[4], y0[4], s0v[4];
 #pragma unroll
-    for (int q = 0; q < kShortPath; q++) {
-        bool in = valid && q < len;
-        u[q] = (in && act) ? a.aup[row0 + (int64_t)q * m + s.j] : 0.0f;
-        sf[q] = in ? a.lsimf[start + q] : 0.0f;
-        nd[q] = in ? a.lmeta[start + q].x : 0;
+    for (int u = 0; u < 4; u++) {
+        s0v[u] = act[u] ? fabsf(a.lsimf[info[u].x]) : 0.0f;
+        u0[u] = act[u] ? a.aup[rows[u].x + s.j] : 0.0f;
+        y0[u] = (act[u] && rows[u].y >= 0) ? a.aup[rows[u].y + s.j] : 0.0f;
     }
-    float y = (act && prow >= 0) ? a.aup[prow + s.j] : 0.0f;
-    int width = a.sub < 32 ? a.sub : 32;
-    // the longest path among the lanes of this warp bounds the loop
-    int wlen = len;
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) wlen = max(wlen, __shfl_xor_sync(0xffffffffu, wlen, o));
-#pragma unroll
-    for (int q = 0; q < kShortPath; q++) {
-        if (q >= wlen) break;
-        bool on = act && q < len;
-        if (on) {
-            float sv = fabsf(sf[q]);
-            y = (q == 0 && prow < 0) ? u[q] : sv * y + (1.0f - sv * sv) * u[q];
-            if (signbit(sf[q]) || a.volume) a.aup[row0 + (int64_t)q * m + s.j] = y;
+    for (int u = 0; u < 4; u++) {
+        if (!act[u]) continue;
+        int m = info[u].z;
+        float* row = a.aup + rows[u].x + s.j;
+        float y = rows[u].y < 0 ? u0[u] : s0v[u] * y0[u] + (1.0f - s0v[u] * s0v[u]) * u0[u];
+        row[0] = y;
+        for (int q = 1; q < info[u].y; q++) {
+            float sv = fabsf(a.lsimf[info[u].x + q]);
+            float* rq = row + (int64_t)q * m;
+            y = sv * y + (1.0f - sv * sv) * rq[0];
+            rq[0] = y;
         }
-        unsigned long long key = group_argmin(on, y, d, width, lane);
-        if (valid && q < len && (lane & (width - 1)) == 0) store_key(a, nd[q], key);
     }
+}
+
+// First argmin per layout position (aggregation.py:249: np.argmin, smallest
+// disparity on ties).  Rows are read in layout order (streaming); with sub
+// < 32 several short rows share a warp, otherwise one warp scans a row.
+__global__ void __launch_bounds__(256) k_wta(AggArgs a, int64_t n) {
+    Slot s = slot_of(a);
+    int lane = threadIdx.x & 31;
+    bool valid = s.item < n;
+    int4 mt = valid ? a.lmeta[s.item] : make_int4(0, 0, 0, 0);
+    int64_t row = valid ? a.rowoff[s.item] : 0;
+    uint32_t best = 0xffffffffu;
+    int bj = 0x7fffffff;
+    int width = a.sub < 32 ? a.sub : 32;
+    int step = width;
+    // sub == 32: lane j0 scans j0, j0+32, ... ; keep the first minimum
+    for (int jj = (a.sub < 32 ? s.j : lane); valid && jj < mt.w; jj += step) {
+        uint32_t o = ord_f32(a.aup[row + jj]);
+        if (o < best) {
+            best = o;
+            bj = jj;
+        }
+    }
+    uint32_t mn = best;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        uint32_t t = __shfl_xor_sync(0xffffffffu, mn, off);
+        if (off < width) mn = min(mn, t);
+    }
+    int jm = (best == mn) ? bj : 0x7fffffff;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        int t = __shfl_xor_sync(0xffffffffu, jm, off);
+        if (off < width) jm = min(jm, t);
+    }
+    if (valid && (lane & (width - 1)) == 0 && a.keys && jm != 0x7fffffff)
+        a.keys[mt.x] = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, mt.y, jm);
 }
 
 // Pixel-major copy of the final aggregated volume (parity / API use only).
@@ -577,14 +608,11 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         kp = kbuf.get();
     }
     a.keys = kp;
-    a.atomic_keys = a.groups > 1 ? 1 : 0;
+    a.atomic_keys = 0;  // k_wta writes each key once
     if (!cost_rows && (f->geom_w != a.w || f->geom_np != a.npix)) {
         k_fill_cols<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, f->lmeta.get(), a.npix, a.w); note_launch();
         f->geom_w = a.w;
         f->geom_np = a.npix;
-    }
-    if (a.atomic_keys) {
-        k_keys_init<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp); note_launch();
     }
 
     AggArgs lg = a;  // segment kernels: one warp per (segment, 32 lanes)
@@ -601,7 +629,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         }
         int64_t p0 = f->lp_off[r], np = f->lp_off[r + 1] - p0;
         if (np > 0) {
-            k_light<<<packed_grid(a, np, 1, 256), 256, 0, st>>>(a, p0, np); note_launch();
+            k_light<<<packed_grid(a, (np + 3) / 4, 1, 256), 256, 0, st>>>(a, p0, np); note_launch();
         }
         int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
         if (ng > 0) {
@@ -610,7 +638,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (ns > 0) {
-            k_scan_up_short<<<packed_grid(sh, ns, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
+            k_scan_up_short<<<packed_grid(sh, (ns + 3) / 4, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
     }
     HDP_CHECK_LAUNCH();
@@ -622,10 +650,15 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (ns > 0) {
-            k_down_short<<<packed_grid(sh, ns, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
+            k_down_short<<<packed_grid(sh, (ns + 3) / 4, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
     }
     HDP_CHECK_LAUNCH();
+    {
+        AggArgs wa = a;  // one warp (sub == 32) or one sub-group per row
+        wa.groups = 1;
+        k_wta<<<packed_grid(wa, f->n, 1, 256), 256, 0, st>>>(wa, f->n); note_launch();
+    }
     if (volume) {
         k_volume_copy<<<packed_grid(a, f->n, 1, 256), 256, 0, st>>>(a, f->n); note_launch();
     }
