@@ -29,6 +29,7 @@
 // A is written back in place only where a light child will read it.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "forest.cuh"
@@ -49,6 +50,8 @@ struct AggArgs {
     const int64_t* rowoff;
     const int32_t* lp_list;
     const int64_t* nodeoff;
+    const int64_t* lc_rowoff;
+    const int64_t* auxd;
     const float4* pl;
     const float4* pr;
     const float* cost_rows;
@@ -68,6 +71,7 @@ struct AggArgs {
     int sub;     // lanes per item for the packed mappings (power of 2 <= 32)
     int sub_shift;
     int atomic_keys;
+    int store_all;  // store A for every node (volume requested), not only light parents
     int max_m;
 };
 
@@ -149,17 +153,68 @@ __global__ void __launch_bounds__(256) k_ecompute(AggArgs a, int64_t k0, int64_t
         int64_t k = k0 + (ok[u] ? s.item : 0);
         mt[u] = a.lmeta[k];
         row[u] = a.rowoff[k];
-        ok[u] = ok[u] && s.j < mt[u].w;
+        ok[u] = ok[u] && s.j < ((mt[u].w + 3) & ~3);  // pad lanes get 0
     }
     float v[BU];
 #pragma unroll
     for (int u = 0; u < BU; u++) {
-        int d = ok[u] ? lane_disp(a, mt[u].y, j[u]) : 0;
-        v[u] = ok[u] ? raw_cost(a, mt[u].x, mt[u].z, d, j[u]) : 0.0f;
+        bool lv = ok[u] && j[u] < mt[u].w;
+        int d = lv ? lane_disp(a, mt[u].y, j[u]) : 0;
+        v[u] = lv ? raw_cost(a, mt[u].x, mt[u].z, d, j[u]) : 0.0f;
     }
 #pragma unroll
     for (int u = 0; u < BU; u++)
         if (ok[u]) a.aup[row[u] + j[u]] = v[u];
+}
+
+// b(v) = E(v) for every node at once, in pixel order: one CTA per (image
+// row, kETile columns).  The right-image window the tile's lanes can reach
+// (columns c0 - max_d .. c0 + kETile) is staged in shared memory once, so
+// each hypothesis costs one shared load and one 4-byte global store into the
+// node's layout row (the rows of one node are contiguous; m lanes -> m/32
+// coalesced stores per warp).
+constexpr int kETile = 64;
+__global__ void __launch_bounds__(256) k_ecost_pix(AggArgs a, const int32_t* __restrict__ lpos,
+                                                   int d_hi, int use_smem) {
+    extern __shared__ float4 win[];
+    const int64_t base = (int64_t)blockIdx.x * a.w;  // node id of column 0 of this image row
+    const int c0 = (int)blockIdx.y * kETile;
+    const int lo = max(0, c0 - d_hi), hi = min(a.w, c0 + kETile);
+    if (use_smem)
+        for (int i = threadIdx.x; i < hi - lo; i += blockDim.x) win[i] = __ldg(a.pr + base + lo + i);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int per = 32 >> a.sub_shift;  // nodes per warp pass
+    const int sl = lane & (a.sub - 1);
+    for (int q = (threadIdx.x >> 5) * per + (lane >> a.sub_shift); q < kETile;
+         q += (blockDim.x >> 5) * per) {
+        const int col = c0 + q;
+        if (col >= a.w) break;
+        const int64_t node = base + col;
+        const int kk = __ldg(lpos + node);
+        const int4 mt = __ldg(a.lmeta + kk);
+        float* out = a.aup + __ldg(a.rowoff + kk);
+        const float4 L = __ldg(a.pl + node);
+        const int mp = (mt.w + 3) & ~3;
+        for (int j = sl; j < mp; j += a.sub) {
+            if (j >= mt.w) {  // row padding
+                out[j] = 0.0f;
+                continue;
+            }
+            const int d = lane_disp(a, mt.y, j);
+            float e = a.border;
+            if (col - d >= 0) {
+                const float4 R = use_smem ? win[col - d - lo] : __ldg(a.pr + node - d);
+                float color;
+                if (a.c == 3)
+                    color = (fabsf(L.x - R.x) + fabsf(L.y - R.y) + fabsf(L.z - R.z)) * (1.0f / 3.0f);
+                else
+                    color = fabsf(L.x - R.x);
+                e = (1.0f - a.alpha) * fminf(a.tc, color) + a.alpha * fminf(a.tg, fabsf(L.w - R.w));
+            }
+            out[j] = e;
+        }
+    }
 }
 
 // b(v) += sum_{light children c} s_c A_up(c) for the phase's light parents
@@ -195,30 +250,47 @@ __global__ void __launch_bounds__(256) k_light(AggArgs a, int64_t p0, int64_t np
     }
 }
 
-// A_up along short paths (2..kShortPath nodes), one thread per (PU paths,
-// lane), values in registers.
+// Short-path kernels: one `sub`-lane group per path (sub == 32: one warp per
+// path, the 32-lane groups looped inside the kernel).  Two lane groups are in
+// flight per iteration and every row of the path is loaded before the chain
+// runs, so a warp keeps 2 * (len + 1) independent loads outstanding.
+struct ShortSlot {
+    int64_t item;
+    int sl;
+};
+__device__ __forceinline__ ShortSlot short_slot(const AggArgs& a) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    return ShortSlot{t >> a.sub_shift, (int)(t & (a.sub - 1))};
+}
+
+// A_up along short paths (2..kShortPath nodes), tail -> head.
 __global__ void __launch_bounds__(256) k_scan_up_short(AggArgs a, int64_t s0, int64_t ns) {
-    Slot s = slot_of(a);
-    for (int u = 0; u < 4; u++) {
-        int64_t it = s.item * 4 + u;
-        if (it >= ns) return;
-        int4 info = a.pinfo[s0 + it];
-        int len = info.y, m = info.z;
-        if (len < 2 || s.j >= m) continue;
-        int64_t row0 = a.prows[s0 + it].x;
-        float b[kShortPath], sim[kShortPath];
+    const ShortSlot s = short_slot(a);
+    if (s.item >= ns) return;
+    const int4 info = a.pinfo[s0 + s.item];
+    const int len = info.y, m = info.z, mp = (m + 3) & ~3;
+    if (len < 2) return;
+    float* row0 = a.aup + a.prows[s0 + s.item].x;
+    float sn[kShortPath];  // similarity of the node after q (0 past the tail)
+#pragma unroll
+    for (int q = 0; q < kShortPath; q++) sn[q] = q + 1 < len ? fabsf(a.lsimf[info.x + q + 1]) : 0.0f;
+    for (int j = s.sl; j < m; j += 2 * a.sub) {
+        const int j2 = j + a.sub;
+        const bool h2 = j2 < m;
+        float b0[kShortPath], b1[kShortPath];
 #pragma unroll
         for (int q = 0; q < kShortPath; q++) {
-            b[q] = q < len ? a.aup[row0 + (int64_t)q * m + s.j] : 0.0f;
-            sim[q] = q < len ? fabsf(a.lsimf[info.x + q]) : 0.0f;
+            b0[q] = q < len ? row0[(int64_t)q * mp + j] : 0.0f;
+            b1[q] = (q < len && h2) ? row0[(int64_t)q * mp + j2] : 0.0f;
         }
-        float x = 0.0f;
+        float x0 = 0.0f, x1 = 0.0f;
 #pragma unroll
         for (int q = kShortPath - 1; q >= 0; q--) {
             if (q < len) {
-                float sn = (q + 1 < len) ? sim[q + 1] : 0.0f;
-                x = b[q] + sn * x;
-                a.aup[row0 + (int64_t)q * m + s.j] = x;
+                x0 = b0[q] + sn[q] * x0;
+                x1 = b1[q] + sn[q] * x1;
+                row0[(int64_t)q * mp + j] = x0;
+                if (h2) row0[(int64_t)q * mp + j2] = x1;
             }
         }
     }
@@ -227,7 +299,7 @@ __global__ void __launch_bounds__(256) k_scan_up_short(AggArgs a, int64_t s0, in
 // ---------------------------------------------------------------- segments
 
 struct SegCtx {
-    int32_t start, len, m, doff;
+    int32_t start, len, m, doff, mp;
     int64_t row0, prow;
     int32_t a, b;    // segment node range [a, b) (layout positions)
     int s, nseg;
@@ -242,6 +314,7 @@ __device__ __forceinline__ SegCtx seg_ctx(const AggArgs& a, int64_t gseg) {
     c.start = info.x;
     c.len = info.y;
     c.m = info.z;
+    c.mp = (info.z + 3) & ~3;
     c.doff = info.w;
     c.row0 = rows.x;
     c.prow = rows.y;
@@ -292,8 +365,8 @@ __global__ void __launch_bounds__(128) k_seg_up(AggArgs a, int64_t g0, int64_t n
     int j = g * 32 + lane;
     bool act = j < c.m;
     int cnt = c.b - c.a;
-    const float* base = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.m + j;
-    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], base + (int64_t)i * c.m, act);
+    const float* base = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp + j;
+    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], base + (int64_t)i * c.mp, act);
     cp_commit();
     bool has_next = c.b < c.start + c.len;  // a segment toward the tail exists
     for (int i = lane; i <= cnt; i += 32) {
@@ -314,10 +387,10 @@ __global__ void __launch_bounds__(128) k_seg_up(AggArgs a, int64_t g0, int64_t n
     if (act && c.s > 0) put_carry(a.carry + c.gseg * a.max_m + j, a.epoch_up, x + P * Xb);
     // final pass: exact recurrence from the true X_b
     x = Xb;
-    float* out = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.m + j;
+    float* out = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp + j;
     for (int i = cnt - 1; i >= 0; i--) {
         x = buf[warp][i][lane] + ssim[warp][i + 1] * x;
-        if (act) out[(int64_t)i * c.m] = x;
+        if (act) out[(int64_t)i * c.mp] = x;
     }
 }
 
@@ -367,11 +440,14 @@ __device__ __forceinline__ void store_key(const AggArgs& a, int32_t node, unsign
 
 // Down pass over one segment (head -> tail).  The carry is
 // Y_end = y_loc(b-1) + Q * Y_in with Q = prod_{t=a..b-1} s_t; the head of a
-// root path uses s = 0 so that A(root) = A_up(root).  A is stored in place
-// for every node; the argmin runs afterwards in k_wta.
+// root path uses s = 0 so that A(root) = A_up(root).  The first argmin of
+// each node over this warp's 32 lanes is folded into the node's key with a
+// 64-bit min (several lane groups per node) or stored (one group); A is
+// written back only where a light child will read it.
 __global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t ng, int* ctr) {
     __shared__ float buf[4][kSeg][32];
     __shared__ float ssim[4][kSeg];
+    __shared__ int32_t snode[4][kSeg];
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int g = (int)blockIdx.y;
     int t = warp_ticket(ctr + g);
@@ -381,14 +457,22 @@ __global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t
     int j = g * 32 + lane;
     bool act = j < c.m;
     int cnt = c.b - c.a;
-    float* rows = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.m + j;
-    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], rows + (int64_t)i * c.m, act);
+    float* rows = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp + j;
+    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], rows + (int64_t)i * c.mp, act);
     cp_commit();
-    for (int i = lane; i < cnt; i += 32) {
-        float sv = fabsf(a.lsimf[c.a + i]);
+    unsigned long long lmask = 0;  // bit i: node a+i has light children
+    for (int i0 = 0; i0 < kSeg; i0 += 32) {
+        int i = i0 + lane;
+        float f = i < cnt ? a.lsimf[c.a + i] : 0.0f;
+        if (i < cnt) snode[warp][i] = a.lmeta[c.a + i].x;
+        float sv = fabsf(f);
         if (c.a + i == c.start && c.prow < 0) sv = 0.0f;  // root: A = A_up
-        ssim[warp][i] = sv;
+        if (i < cnt) ssim[warp][i] = sv;
+        unsigned b = __ballot_sync(0xffffffffu, i < cnt && (__float_as_uint(f) >> 31));
+        lmask |= (unsigned long long)b << i0;
     }
+    if (a.store_all) lmask = ~0ull;
+    const int d = act ? lane_disp(a, c.doff, j) : 0;
     cp_wait_all();
     __syncwarp();
     // local pass with Y_in = 0: y_loc(b-1) and Q = prod_{t=a..b-1} s_t
@@ -410,45 +494,326 @@ __global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t
     for (int i = 0; i < cnt; i++) {
         float sv = ssim[warp][i];
         y = sv * y + (1.0f - sv * sv) * buf[warp][i][lane];
-        if (act) rows[(int64_t)i * c.m] = y;
+        if (act && ((lmask >> i) & 1ull)) rows[(int64_t)i * c.mp] = y;
+        unsigned long long key = group_argmin(act, y, d, 32, lane);
+        if (lane == 0 && a.keys) {
+            if (a.atomic_keys)
+                atomicMin(&a.keys[snode[warp][i]], key);
+            else
+                a.keys[snode[warp][i]] = key;
+        }
     }
 }
 
 // Short paths (1..kShortPath nodes): A = s A(parent) + (1 - s^2) A_up head ->
-// tail, stored in place.  Each thread takes 4 consecutive paths and issues
-// the first-node loads of all of them up front (most have a single node).
+// tail fused with the first argmin of every node (aggregation.py:249,
+// smallest disparity on ties: lanes ascend in disparity and each lane keeps
+// its first minimum).  A is stored only for nodes with light children.
 __global__ void __launch_bounds__(256) k_down_short(AggArgs a, int64_t s0, int64_t ns) {
-    Slot s = slot_of(a);
-    int4 info[4];
-    longlong2 rows[4];
-    bool act[4];
+    const ShortSlot s = short_slot(a);
+    const bool valid = s.item < ns;
+    const int4 info = valid ? a.pinfo[s0 + s.item] : make_int4(0, 0, 0, 0);
+    const longlong2 rows = valid ? a.prows[s0 + s.item] : make_longlong2(0, -1);
+    const int len = info.y, m = info.z, mp = (m + 3) & ~3;
+    float sv[kShortPath];
+    bool st[kShortPath];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-        int64_t it = s.item * 4 + u;
-        bool valid = it < ns;
-        info[u] = valid ? a.pinfo[s0 + it] : make_int4(0, 0, 0, 0);
-        rows[u] = valid ? a.prows[s0 + it] : make_longlong2(0, -1);
-        act[u] = valid && s.j < info[u].z;
+    for (int q = 0; q < kShortPath; q++) {
+        float f = q < len ? a.lsimf[info.x + q] : 0.0f;
+        sv[q] = fabsf(f);
+        st[q] = a.store_all || (__float_as_uint(f) >> 31);
     }
-    float u0[4], y0[4], s0v[4];
+    if (rows.y < 0) sv[0] = 0.0f;  // root: A = A_up
+    float* row0 = a.aup + rows.x;
+    const float* prow = a.aup + (rows.y >= 0 ? rows.y : 0);
+    uint32_t best[kShortPath];
+    int bj[kShortPath];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-        s0v[u] = act[u] ? fabsf(a.lsimf[info[u].x]) : 0.0f;
-        u0[u] = act[u] ? a.aup[rows[u].x + s.j] : 0.0f;
-        y0[u] = (act[u] && rows[u].y >= 0) ? a.aup[rows[u].y + s.j] : 0.0f;
+    for (int q = 0; q < kShortPath; q++) {
+        best[q] = 0xffffffffu;
+        bj[q] = 0x7fffffff;
     }
+    for (int j = s.sl; j < m; j += 2 * a.sub) {
+        const int j2 = j + a.sub;
+        const bool h2 = j2 < m;
+        float u0[kShortPath], u1[kShortPath];
+        float y0 = rows.y >= 0 ? prow[j] : 0.0f;
+        float y1 = (rows.y >= 0 && h2) ? prow[j2] : 0.0f;
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-        if (!act[u]) continue;
-        int m = info[u].z;
-        float* row = a.aup + rows[u].x + s.j;
-        float y = rows[u].y < 0 ? u0[u] : s0v[u] * y0[u] + (1.0f - s0v[u] * s0v[u]) * u0[u];
-        row[0] = y;
-        for (int q = 1; q < info[u].y; q++) {
-            float sv = fabsf(a.lsimf[info[u].x + q]);
-            float* rq = row + (int64_t)q * m;
-            y = sv * y + (1.0f - sv * sv) * rq[0];
-            rq[0] = y;
+        for (int q = 0; q < kShortPath; q++) {
+            u0[q] = q < len ? row0[(int64_t)q * mp + j] : 0.0f;
+            u1[q] = (q < len && h2) ? row0[(int64_t)q * mp + j2] : 0.0f;
+        }
+#pragma unroll
+        for (int q = 0; q < kShortPath; q++) {
+            if (q < len) {
+                y0 = sv[q] * y0 + (1.0f - sv[q] * sv[q]) * u0[q];
+                y1 = sv[q] * y1 + (1.0f - sv[q] * sv[q]) * u1[q];
+                if (st[q]) {
+                    row0[(int64_t)q * mp + j] = y0;
+                    if (h2) row0[(int64_t)q * mp + j2] = y1;
+                }
+                uint32_t o0 = ord_f32(y0);
+                if (o0 < best[q]) {
+                    best[q] = o0;
+                    bj[q] = j;
+                }
+                uint32_t o1 = ord_f32(y1);
+                if (h2 && o1 < best[q]) {
+                    best[q] = o1;
+                    bj[q] = j2;
+                }
+            }
+        }
+    }
+    const int width = a.sub;
+#pragma unroll
+    for (int q = 0; q < kShortPath; q++) {
+        if (!__any_sync(0xffffffffu, q < len)) break;
+        uint32_t mn = best[q];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            uint32_t t = __shfl_xor_sync(0xffffffffu, mn, off);
+            if (off < width) mn = min(mn, t);
+        }
+        int jm = best[q] == mn ? bj[q] : 0x7fffffff;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            int t = __shfl_xor_sync(0xffffffffu, jm, off);
+            if (off < width) jm = min(jm, t);
+        }
+        if (s.sl == 0 && q < len && a.keys && jm != 0x7fffffff)
+            a.keys[a.lmeta[info.x + q].x] =
+                ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, info.w, jm);
+    }
+}
+
+// ------------------------------------------------------------ short chunks
+//
+// The short paths of a phase sit first in the phase's layout block, so their
+// rows are one contiguous range; a chunk (forest.cuh) is a run of them whose
+// rows, auxiliary rows (light children's A_up on the way up, the parent's A
+// on the way down) and metadata fit in shared memory.  The CTA stages all of
+// it first -- 16-byte loads for the row block, cp.async row gathers for the
+// auxiliary rows, every load independent -- so the per-path walks that
+// follow touch only shared memory, and global traffic is the chunk's rows in,
+// the changed rows and the keys out.  One `sub`-lane group walks one path.
+
+struct ChunkSm {
+    int4* info;     // per path: (start, len, m, lane offset)
+    int* rowo;      // per path: offset of its first row in `own`
+    int* paro;      // down: offset of its parent row in `aux` (-1 at a root)
+    float* own;     // the chunk's rows
+    float* aux;
+    float* sim;     // per node: lsimf
+    int* nodei;     // up: lc_start - L0 (nk + 1); down: node id (nk)
+    float* lsim;    // up: per light-child entry, its similarity
+    int* loff;      // up: per entry, offset of its row in `aux`
+};
+
+template <bool UP>
+__device__ __forceinline__ ChunkSm carve(const ChunkDesc& d, float4* sm4) {
+    ChunkSm s;
+    s.info = reinterpret_cast<int4*>(sm4);
+    float4* p = sm4 + d.np;
+    s.own = reinterpret_cast<float*>(p);
+    p += d.n4;
+    float* q = reinterpret_cast<float*>(p);
+    s.aux = q;
+    q += ((UP ? d.naux_up : d.naux_dn) + 3) & ~3;
+    s.sim = q;
+    q += (d.nk + 3) & ~3;
+    s.nodei = reinterpret_cast<int*>(q);
+    q += (d.nk + 4) & ~3;
+    s.rowo = reinterpret_cast<int*>(q);
+    q += (d.np + 3) & ~3;
+    s.paro = reinterpret_cast<int*>(q);
+    q += (d.np + 3) & ~3;
+    s.lsim = q;
+    q += (d.nl + 3) & ~3;
+    s.loff = reinterpret_cast<int*>(q);
+    return s;
+}
+
+// 4-byte cp.async of `cnt` floats, lanes of one warp striding the row
+__device__ __forceinline__ void row_async(float* dst, const float* src, int cnt, int lane) {
+    for (int j = lane; j < cnt; j += 32) cp_async4(dst + j, src + j, true);
+}
+
+template <bool UP>
+__device__ __forceinline__ ChunkSm stage_chunk(const AggArgs& a, const ChunkDesc& d, float4* sm4) {
+    ChunkSm s = carve<UP>(d, sm4);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const float4* src = reinterpret_cast<const float4*>(a.aup + d.a0);
+    for (int i = tid; i < d.n4; i += nt) reinterpret_cast<float4*>(s.own)[i] = src[i];
+    for (int i = tid; i < d.nk; i += nt) s.sim[i] = a.lsimf[d.K0 + i];
+    if (UP) {
+        for (int i = tid; i <= d.nk; i += nt) s.nodei[i] = a.lc_start[d.K0 + i] - d.L0;
+        for (int i = tid; i < d.nl; i += nt) {
+            s.lsim[i] = a.lc_sim[d.L0 + i];
+            s.loff[i] = (int)(a.lc_rowoff[d.L0 + i] - d.lcr0);
+        }
+    } else {
+        for (int i = tid; i < d.nk; i += nt) s.nodei[i] = a.lmeta[d.K0 + i].x;
+    }
+    // path metadata, 32 paths per warp step; the auxiliary rows are issued as
+    // soon as their source offsets are known
+    for (int i0 = warp * 32; i0 < d.np; i0 += nw * 32) {
+        const int i = i0 + lane;
+        int4 in = make_int4(0, 0, 0, 0);
+        longlong2 rw = make_longlong2(0, -1);
+        int po = -1;
+        if (i < d.np) {
+            in = a.pinfo[d.p0 + i];
+            rw = a.prows[d.p0 + i];
+            s.info[i] = in;
+            s.rowo[i] = (int)(rw.x - d.a0);
+            if (!UP && rw.y >= 0) po = (int)(a.auxd[d.p0 + i] - d.auxd0);
+            s.paro[i] = po;
+        }
+        if (!UP) {
+            const int cnt = min(32, d.np - i0);
+            for (int t = 0; t < cnt; t++) {
+                const int pot = __shfl_sync(0xffffffffu, po, t);
+                const long long src_row = __shfl_sync(0xffffffffu, rw.y, t);
+                const int mt = __shfl_sync(0xffffffffu, in.z, t);
+                if (pot >= 0) row_async(s.aux + pot, a.aup + src_row, mt, lane);
+            }
+        }
+    }
+    if (UP) {
+        for (int e0 = warp * 32; e0 < d.nl; e0 += nw * 32) {
+            const int e = e0 + lane;
+            long long row = 0;
+            int off = 0, me = 0;
+            if (e < d.nl) {
+                row = a.lc_row[d.L0 + e];
+                const long long r0 = a.lc_rowoff[d.L0 + e];
+                off = (int)(r0 - d.lcr0);
+                me = (int)(a.lc_rowoff[d.L0 + e + 1] - r0);
+            }
+            const int cnt = min(32, d.nl - e0);
+            for (int t = 0; t < cnt; t++) {
+                const long long rt = __shfl_sync(0xffffffffu, row, t);
+                const int ot = __shfl_sync(0xffffffffu, off, t);
+                const int mt = __shfl_sync(0xffffffffu, me, t);
+                row_async(s.aux + ot, a.aup + rt, mt, lane);
+            }
+        }
+    }
+    cp_commit();
+    cp_wait_all();
+    __syncthreads();
+    return s;
+}
+
+// Up pass: tail -> head, A_up(q) = (E(q) + sum_light s_c A_up(c)) + s_{q+1} A_up(q+1)
+// (the operation order of k_light + k_scan_up_short).  Changed rows are
+// stored; a lone leaf row (A_up = E) is left alone.
+__global__ void __launch_bounds__(256) k_up_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
+                                                  int64_t cbase) {
+    extern __shared__ float4 sm4[];
+    const ChunkDesc d = descs[cbase + blockIdx.x];
+    if (d.np == 0) return;
+    const ChunkSm s = stage_chunk<true>(a, d, sm4);
+    const int lane = threadIdx.x & 31;
+    const int per = 32 >> a.sub_shift;
+    const int sl = lane & (a.sub - 1);
+    for (int pb = (int)(threadIdx.x >> 5) * per; pb < d.np; pb += (int)(blockDim.x >> 5) * per) {
+        const int pi = pb + (lane >> a.sub_shift);
+        if (pi >= d.np) break;  // no warp-collective operations below
+        const int4 info = s.info[pi];
+        const int len = info.y, m = info.z, mp = (m + 3) & ~3;
+        float* srow = s.own + s.rowo[pi];
+        float* grow = a.aup + d.a0 + s.rowo[pi];
+        float sn = 0.0f;  // similarity of node q + 1
+        for (int q = len - 1; q >= 0; q--) {
+            const int kk = info.x - d.K0 + q;
+            const float f = s.sim[kk];
+            const bool has_l = __float_as_uint(f) >> 31;
+            const bool changed = has_l || q + 1 < len;
+            const int e0 = s.nodei[kk], e1 = s.nodei[kk + 1];
+            float* sq = srow + q * mp;
+            for (int j = sl; j < m; j += a.sub) {
+                float b = sq[j];
+                if (has_l) {
+                    float x = s.lsim[e0] * s.aux[s.loff[e0] + j];
+                    for (int e = e0 + 1; e < e1; e++) x += s.lsim[e] * s.aux[s.loff[e] + j];
+                    b = b + x;
+                }
+                const float x = (q + 1 < len) ? b + sn * sq[mp + j] : b;
+                sq[j] = x;
+                if (changed) grow[q * mp + j] = x;
+            }
+            sn = fabsf(f);
+        }
+    }
+}
+
+// Down pass fused with the first argmin: head -> tail,
+// A(q) = s_q A(q - 1) + (1 - s_q^2) A_up(q) with A(-1) = A(parent) (s = 0 at a
+// root); A is stored only where a light child will read it.
+__global__ void __launch_bounds__(256) k_down_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
+                                                    int64_t cbase) {
+    extern __shared__ float4 sm4[];
+    const ChunkDesc d = descs[cbase + blockIdx.x];
+    if (d.np == 0) return;
+    const ChunkSm s = stage_chunk<false>(a, d, sm4);
+    const int lane = threadIdx.x & 31;
+    const int per = 32 >> a.sub_shift;
+    const int sl = lane & (a.sub - 1);
+    const int width = a.sub;
+    for (int pb = (int)(threadIdx.x >> 5) * per; pb < d.np; pb += (int)(blockDim.x >> 5) * per) {
+        const int pi = pb + (lane >> a.sub_shift);
+        const bool valid = pi < d.np;
+        const int4 info = valid ? s.info[pi] : make_int4(0, 0, 0, 0);
+        const int len = info.y, m = info.z, mp = (m + 3) & ~3;
+        int lmax = len;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
+        const int ro = valid ? s.rowo[pi] : 0;
+        const int po = valid ? s.paro[pi] : -1;
+        float* srow = s.own + ro;
+        float* grow = a.aup + d.a0 + ro;
+        for (int q = 0; q < lmax; q++) {
+            const bool on = q < len;
+            const int kk = info.x - d.K0 + q;
+            const float f = on ? s.sim[kk] : 0.0f;
+            float sv = fabsf(f);
+            if (q == 0 && po < 0) sv = 0.0f;  // root: A = A_up
+            const bool st = on && (a.store_all || (__float_as_uint(f) >> 31));
+            const float w = 1.0f - sv * sv;
+            float* sq = srow + q * mp;
+            const float* prev = q == 0 ? s.aux + (po >= 0 ? po : 0) : sq - mp;
+            const bool has_prev = q > 0 || po >= 0;
+            uint32_t best = 0xffffffffu;
+            int bj = 0x7fffffff;
+            for (int j = sl; on && j < m; j += a.sub) {
+                const float yp = has_prev ? prev[j] : 0.0f;
+                const float y = sv * yp + w * sq[j];
+                sq[j] = y;
+                if (st) grow[q * mp + j] = y;
+                const uint32_t o = ord_f32(y);
+                if (o < best) {
+                    best = o;
+                    bj = j;
+                }
+            }
+            uint32_t mn = best;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                uint32_t t = __shfl_xor_sync(0xffffffffu, mn, off);
+                if (off < width) mn = min(mn, t);
+            }
+            int jm = best == mn ? bj : 0x7fffffff;
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                int t = __shfl_xor_sync(0xffffffffu, jm, off);
+                if (off < width) jm = min(jm, t);
+            }
+            if (on && sl == 0 && a.keys && jm != 0x7fffffff)
+                a.keys[s.nodei[kk]] = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, info.w, jm);
         }
     }
 }
@@ -496,7 +861,7 @@ __global__ void __launch_bounds__(256) k_volume_copy(AggArgs a, int64_t n) {
     if (s.item >= n) return;
     int64_t k = s.item;
     int64_t row = a.rowoff[k];
-    int m = (int)(a.rowoff[k + 1] - row);
+    int m = a.lmeta[k].w;
     if (s.j >= m) return;
     a.volume[a.nodeoff[a.lmeta[k].x] + s.j] = a.aup[row + s.j];
 }
@@ -566,6 +931,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.rowoff = f->rowoff.get();
     a.lp_list = f->lp_list.get();
     a.nodeoff = f->nodeoff.get();
+    a.lc_rowoff = nullptr;
+    a.auxd = nullptr;
     a.pl = (const float4*)packed_l;
     a.pr = (const float4*)packed_r;
     a.cost_rows = cost_rows;
@@ -580,13 +947,13 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.volume = volume;
     a.groups = (f->max_m + 31) / 32;
     a.max_m = f->max_m;
-    a.sub = f->max_m <= 16 ? pow2_at_least(f->max_m) : 32;
+    a.sub = f->max_m <= 16 ? std::max(4, pow2_at_least(f->max_m)) : 32;  // >= one padded row
     a.sub_shift = 0;
     while ((1 << a.sub_shift) < a.sub) a.sub_shift++;
     DevBuf<float> aup;
     DevBuf<unsigned long long> carry;
     DevBuf<int> tickets;
-    HDP_TRY(aup.alloc(f->total_entries + 32, st));
+    HDP_TRY(aup.alloc(f->total_rows + 32, st));
     a.aup = aup.get();
     const int64_t nseg = f->n_segs;
     HDP_TRY(carry.alloc(nseg * a.max_m + 1, st));
@@ -608,7 +975,10 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         kp = kbuf.get();
     }
     a.keys = kp;
-    a.atomic_keys = 0;  // k_wta writes each key once
+    // long-path nodes get one key contribution per 32-lane group
+    a.atomic_keys = (f->n_segs > 0 && a.groups > 1) ? 1 : 0;
+    if (a.atomic_keys) HDP_CHECK_CUDA(cudaMemsetAsync(kp, 0xff, sizeof(unsigned long long) * f->n, st));
+    a.store_all = volume != nullptr;
     if (!cost_rows && (f->geom_w != a.w || f->geom_np != a.npix)) {
         k_fill_cols<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, f->lmeta.get(), a.npix, a.w); note_launch();
         f->geom_w = a.w;
@@ -622,12 +992,28 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     AggArgs sh = a;
     sh.pinfo = f->short_info.get();
     sh.prows = f->short_rows.get();
+    if (cost_rows) {
+        k_ecompute<<<packed_grid(a, f->n, BU, 256), 256, 0, st>>>(a, 0, f->n); note_launch();
+    } else {
+        HDP_REQUIRE(f->n % a.w == 0, HDP_ERR_CONFIG, "node count is not a whole number of image rows");
+        int64_t rows = f->n / a.w;
+        HDP_REQUIRE(rows < ((int64_t)1 << 31), HDP_ERR_CONFIG, "too many image rows");
+        size_t smem = (size_t)(kETile + f->max_d) * sizeof(float4);
+        int use = smem <= 48 * 1024;
+        dim3 g((unsigned)rows, (unsigned)((a.w + kETile - 1) / kETile));
+        k_ecost_pix<<<g, 256, use ? smem : 0, st>>>(a, f->lpos.get(), f->max_d, use); note_launch();
+    }
+    const bool chunks = f->chunks_ok != 0;
+    const size_t csmem = (size_t)f->chunk_words * sizeof(float);
+    sh.lc_rowoff = f->lc_rowoff.get();
+    sh.auxd = f->auxd.get();
+    if (chunks && csmem > 48 * 1024) {
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_up_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_down_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+    }
     for (int64_t r = f->n_phases - 1; r >= 0; r--) {
-        int64_t k0 = f->phase_node[r], nk = f->phase_node[r + 1] - k0;
-        if (nk > 0) {
-            k_ecompute<<<packed_grid(a, nk, BU, 256), 256, 0, st>>>(a, k0, nk); note_launch();
-        }
-        int64_t p0 = f->lp_off[r], np = f->lp_off[r + 1] - p0;
+        // light parents on short paths are handled inside k_up_chunk
+        int64_t p0 = chunks ? f->lp_mid[r] : f->lp_off[r], np = f->lp_off[r + 1] - p0;
         if (np > 0) {
             k_light<<<packed_grid(a, (np + 3) / 4, 1, 256), 256, 0, st>>>(a, p0, np); note_launch();
         }
@@ -637,8 +1023,11 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
                 lg, g0, ng, a.tickets + (2 * r) * a.groups); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
-        if (ns > 0) {
-            k_scan_up_short<<<packed_grid(sh, (ns + 3) / 4, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
+        int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
+        if (chunks && nc > 0) {
+            k_up_chunk<<<(unsigned)nc, 256, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
+        } else if (!chunks && ns > 0) {
+            k_scan_up_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
     }
     HDP_CHECK_LAUNCH();
@@ -649,16 +1038,14 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
                 lg, g0, ng, a.tickets + (2 * r + 1) * a.groups); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
-        if (ns > 0) {
-            k_down_short<<<packed_grid(sh, (ns + 3) / 4, 1, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
+        int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
+        if (chunks && nc > 0) {
+            k_down_chunk<<<(unsigned)nc, 256, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
+        } else if (!chunks && ns > 0) {
+            k_down_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
     }
     HDP_CHECK_LAUNCH();
-    {
-        AggArgs wa = a;  // one warp (sub == 32) or one sub-group per row
-        wa.groups = 1;
-        k_wta<<<packed_grid(wa, f->n, 1, 256), 256, 0, st>>>(wa, f->n); note_launch();
-    }
     if (volume) {
         k_volume_copy<<<packed_grid(a, f->n, 1, 256), 256, 0, st>>>(a, f->n); note_launch();
     }

@@ -273,17 +273,28 @@ __global__ void k_light_steps(int64_t na, const int32_t* __restrict__ asrc,
     }
 }
 
+// nodes per heavy path, stored at the head
+__global__ void k_path_len(int64_t n, const int32_t* __restrict__ head,
+                           const int32_t* __restrict__ dist, int32_t* plen) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) atomicMax(&plen[head[v]], dist[v] + 1);
+}
+
+// layout key (light depth, long path, head, distance from head): within a
+// phase the short paths come first, so their rows form one contiguous block
 __global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
                               const int32_t* __restrict__ lscan, const int32_t* __restrict__ head,
-                              const int32_t* __restrict__ dist, uint64_t* key, int32_t* idx,
-                              int32_t* ld_out, int hbits, int dbits) {
+                              const int32_t* __restrict__ dist, const int32_t* __restrict__ plen,
+                              uint64_t* key, int32_t* idx, int32_t* ld_out, int hbits, int dbits) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     int32_t a = down_arc[v];
     int32_t ld = a >= 0 ? lscan[a] : 0;
     ld_out[v] = ld;
-    key[v] = ((uint64_t)ld << (hbits + dbits)) | ((uint64_t)(uint32_t)head[v] << dbits) |
-             (uint64_t)dist[v];
+    int32_t h = head[v];
+    uint64_t lg = plen[h] > kShortPath ? 1ull : 0ull;
+    key[v] = ((uint64_t)ld << (1 + hbits + dbits)) | (lg << (hbits + dbits)) |
+             ((uint64_t)(uint32_t)h << dbits) | (uint64_t)dist[v];
     idx[v] = (int32_t)v;
 }
 
@@ -385,6 +396,20 @@ __global__ void k_phase_gather(int64_t nb, const int32_t* __restrict__ first,
     out[2 * r + 1] = lexcl[pi];
 }
 
+// end position of the short-path block of each phase (short paths first)
+__global__ void k_short_end(int nph, const int64_t* __restrict__ soff, const int64_t* __restrict__ pnode,
+                            const int32_t* __restrict__ short_paths, const int32_t* __restrict__ p_start,
+                            const int32_t* __restrict__ p_len, int64_t* out) {
+    int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nph) return;
+    if (soff[r + 1] > soff[r]) {
+        int32_t p = short_paths[soff[r + 1] - 1];
+        out[r] = (int64_t)p_start[p] + p_len[p];
+    } else {
+        out[r] = pnode[r];
+    }
+}
+
 __global__ void k_split_paths(int64_t np, const int32_t* __restrict__ is_long,
                               const int32_t* __restrict__ lpos_excl, int32_t* long_paths,
                               int32_t* short_paths) {
@@ -466,7 +491,7 @@ __global__ void k_row_m(int64_t n, const int32_t* __restrict__ lnode,
                         const int32_t* __restrict__ tree_id, const int32_t* __restrict__ t_m,
                         int64_t* rm) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n) rm[k] = t_m[tree_id[lnode[k]]];
+    if (k < n) rm[k] = (t_m[tree_id[lnode[k]]] + 3) & ~3;  // rows padded to 16 bytes
     if (k == n) rm[k] = 0;
 }
 
@@ -692,11 +717,20 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(lidx.alloc(n, st));
     HDP_TRY(f->lnode.alloc(n, st));
     int dbits = bits_for(f->max_depth + 1), hbits = bits_for(n);
-    k_layout_keys<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), head, dist.get(),
-                                                lkey.get(), lidx.get(), ld.get(), hbits, dbits); note_launch();
-    HDP_CHECK_LAUNCH();
+    // light depth <= log2(n) + 1 < 64 needs 6 bits, the long flag one more
+    HDP_REQUIRE(hbits + dbits <= 57, HDP_ERR_CONFIG, "forest too large for the layout key");
+    {
+        DevBuf<int32_t> plen;
+        HDP_TRY(plen.alloc(n, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(plen.get(), 0, n * sizeof(int32_t), st));
+        k_path_len<<<grid_for(n, B), B, 0, st>>>(n, head, dist.get(), plen.get()); note_launch();
+        k_layout_keys<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), head, dist.get(),
+                                                    plen.get(), lkey.get(), lidx.get(), ld.get(),
+                                                    hbits, dbits); note_launch();
+        HDP_CHECK_LAUNCH();
+    }
     HDP_TRY(sort_pairs(lkey.get(), lkey2.get(), lidx.get(), f->lnode.get(), n, 0,
-                       std::min(64, dbits + hbits + 8), st));
+                       std::min(64, dbits + hbits + 7), st));
     lkey.release();
     lkey2.release();
     lidx.release();
@@ -775,6 +809,21 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                              f->long_paths.get(),
                                                              f->short_paths.get()); note_launch();
         HDP_CHECK_LAUNCH();
+        {
+            const int nph = (int)f->n_phases;
+            DevBuf<int64_t> dso, dpn, dse;
+            HDP_TRY(dso.alloc(nph + 1, st));
+            HDP_TRY(dpn.alloc(nph + 1, st));
+            HDP_TRY(dse.alloc(nph + 1, st));
+            HDP_CHECK_CUDA(cudaMemcpyAsync(dso.get(), f->short_off.data(), sizeof(int64_t) * (nph + 1),
+                                           cudaMemcpyHostToDevice, st));
+            HDP_CHECK_CUDA(cudaMemcpyAsync(dpn.get(), f->phase_node.data(), sizeof(int64_t) * (nph + 1),
+                                           cudaMemcpyHostToDevice, st));
+            k_short_end<<<grid_for(nph, 64), 64, 0, st>>>(nph, dso.get(), dpn.get(), f->short_paths.get(),
+                                                          f->p_start.get(), f->p_len.get(), dse.get()); note_launch();
+            f->short_end.assign(nph + 1, n);
+            HDP_TRY(to_host(f->short_end.data(), dse.get(), nph, st));
+        }
         // segments of kSeg nodes over the long paths (head first), phase-major
         int64_t nl = f->long_off[f->n_phases];
         DevBuf<int32_t> nseg, soff, sb, sbh;
@@ -840,6 +889,13 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                                    bnd.get()); note_launch();
         HDP_TRY(to_host(hl.data(), bnd.get(), f->n_phases + 1, st));
         f->lp_off.assign(hl.begin(), hl.end());
+        for (int64_t r = 0; r <= f->n_phases; r++) hp[r] = (int32_t)f->short_end[r];
+        HDP_CHECK_CUDA(cudaMemcpyAsync(pn.get(), hp.data(), sizeof(int32_t) * (f->n_phases + 1),
+                                       cudaMemcpyHostToDevice, st));
+        k_gather_i32<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(f->n_phases + 1, ex.get(), pn.get(),
+                                                                   bnd.get()); note_launch();
+        HDP_TRY(to_host(hl.data(), bnd.get(), f->n_phases + 1, st));
+        f->lp_mid.assign(hl.begin(), hl.end());
     }
     tr.mark("10 light parents");
     HDP_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -851,12 +907,12 @@ namespace hdp {
 __global__ void k_pos_meta(int64_t n, const int32_t* __restrict__ lnode,
                            const int32_t* __restrict__ tree_id, const int32_t* __restrict__ t_doff,
                            const float* __restrict__ lsim, const int32_t* __restrict__ lc_start,
-                           const int64_t* __restrict__ rowoff, int4* lmeta, float* lsimf) {
+                           const int32_t* __restrict__ t_m, int4* lmeta, float* lsimf) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     int32_t v = lnode[k];
     // (node, lane-table offset, image column (set per call), lane count m)
-    lmeta[k] = make_int4(v, t_doff[tree_id[v]], -1, (int)(rowoff[k + 1] - rowoff[k]));
+    lmeta[k] = make_int4(v, t_doff[tree_id[v]], -1, t_m[tree_id[v]]);
     float s = lsim[k];
     lsimf[k] = (lc_start[k + 1] > lc_start[k]) ? -s : s;  // sign bit: has light children
 }
@@ -874,20 +930,169 @@ __global__ void k_lc_meta(int64_t nl, const int32_t* __restrict__ lc_list,
 __global__ void k_path_meta(int64_t np, const int32_t* __restrict__ list,
                             const int32_t* __restrict__ p_start, const int32_t* __restrict__ p_len,
                             const int32_t* __restrict__ p_par, const int32_t* __restrict__ p_tree,
-                            const int32_t* __restrict__ t_doff, const int64_t* __restrict__ rowoff,
-                            int4* info, longlong2* rows) {
+                            const int32_t* __restrict__ t_doff, const int32_t* __restrict__ t_m,
+                            const int64_t* __restrict__ rowoff, int4* info, longlong2* rows) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= np) return;
     int32_t pi = list[i];
     int32_t s = p_start[pi];
     int64_t r0 = rowoff[s];
-    int32_t m = (int32_t)(rowoff[s + 1] - r0);
+    int32_t m = t_m[p_tree[pi]];
     int32_t par = p_par[pi];
     info[i] = make_int4(s, p_len[pi], m, t_doff[p_tree[pi]]);
     rows[i] = make_longlong2(r0, par >= 0 ? rowoff[par] : -1);
 }
 
+__global__ void k_gather_i64(int64_t m, const int64_t* __restrict__ src,
+                             const int64_t* __restrict__ idx, int64_t* out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) out[i] = src[idx[i]];
+}
+
+// per short path: shared-memory weight (own rows, light-children rows, a
+// parent row, per-node and per-entry metadata, path metadata) and the size
+// of its parent row (0 at a root)
+__global__ void k_chunk_weight(int64_t ns, const int4* __restrict__ sinfo,
+                               const longlong2* __restrict__ srows,
+                               const int32_t* __restrict__ lc_start, int64_t* wt, int64_t* pm) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > ns) return;
+    if (i == ns) {
+        wt[i] = 0;
+        pm[i] = 0;
+        return;
+    }
+    int4 in = sinfo[i];
+    int64_t len = in.y, m = (in.z + 3) & ~3;
+    int64_t nlc = lc_start[in.x + in.y] - lc_start[in.x];
+    wt[i] = (len + nlc + 1) * m + 2 * len + 2 * nlc + 16;
+    pm[i] = srows[i].y >= 0 ? m : 0;
+}
+
+// lane count of every light-child entry (parent and child share the tree)
+__global__ void k_lc_m(int64_t nl, const int32_t* __restrict__ lc_list, const int4* __restrict__ lmeta,
+                       int64_t* out) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < nl) out[q] = (lmeta[lc_list[q]].w + 3) & ~3;
+    else if (q == nl) out[q] = 0;
+}
+
+// chunk_first over the short paths: path i (phase r) starts chunk
+// cbase[r] + ((W[i] - W0[r]) >> kChunkShift); every chunk id up to it that
+// no earlier path claimed starts at i.
+__global__ void k_chunk_fill(int64_t ns, int nph, const int64_t* __restrict__ soff,
+                             const int64_t* __restrict__ cbase, const int64_t* __restrict__ w0,
+                             const int64_t* __restrict__ W, int32_t* chunk_first) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ns) return;
+    int lo = 0, hi = nph - 1;  // phase r with soff[r] <= i < soff[r+1]
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (soff[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    const int r = lo;
+    int64_t c = cbase[r] + ((W[i] - w0[r]) >> kChunkShift);
+    int64_t cp = (i == soff[r]) ? cbase[r] - 1 : cbase[r] + ((W[i - 1] - w0[r]) >> kChunkShift);
+    for (int64_t q = cp + 1; q <= c; q++) chunk_first[q] = (int32_t)i;
+    if (i == soff[r + 1] - 1)
+        for (int64_t q = c + 1; q < cbase[r + 1]; q++) chunk_first[q] = (int32_t)(i + 1);
+}
+
+__global__ void k_chunk_desc(int64_t nc, const int32_t* __restrict__ chunk_first,
+                             const int4* __restrict__ sinfo, const longlong2* __restrict__ srows,
+                             const int32_t* __restrict__ lc_start, const int64_t* __restrict__ lc_rowoff,
+                             const int64_t* __restrict__ auxd, const int64_t* __restrict__ W,
+                             ChunkDesc* desc, unsigned long long* max_words) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    ChunkDesc d = {};
+    int p0 = chunk_first[c], p1 = chunk_first[c + 1];
+    d.p0 = p0;
+    d.np = p1 - p0;
+    if (p1 > p0) {
+        int4 f = sinfo[p0], l = sinfo[p1 - 1];
+        d.K0 = f.x;
+        d.nk = l.x + l.y - f.x;
+        d.L0 = lc_start[d.K0];
+        d.nl = lc_start[d.K0 + d.nk] - d.L0;
+        int64_t r0 = srows[p0].x, r1 = srows[p1 - 1].x + (int64_t)l.y * ((l.z + 3) & ~3);
+        d.a0 = r0 & ~3ll;
+        d.n4 = (int)((r1 - d.a0 + 3) >> 2);
+        d.lcr0 = lc_rowoff[d.L0];
+        d.naux_up = (int)(lc_rowoff[d.L0 + d.nl] - d.lcr0);
+        d.auxd0 = auxd[p0];
+        d.naux_dn = (int)(auxd[p1] - d.auxd0);
+        atomicMax(max_words, (unsigned long long)(W[p1] - W[p0]));
+    }
+    desc[c] = d;
+}
+
 }  // namespace hdp
+
+// chunk table of the short-path blocks (needs lmeta, lc rows and short_rows)
+static int build_chunks(hdp_forest* f) {
+    cudaStream_t st = f->st;
+    const int nph = (int)f->n_phases;
+    const int64_t ns = f->short_off[nph];
+    int32_t n_lc = 0;
+    HDP_TRY(to_host(&n_lc, f->lc_start.get() + f->n, 1, st));
+    DevBuf<int64_t> wt, W, pm, lcm;
+    HDP_TRY(wt.alloc(ns + 1, st));
+    HDP_TRY(W.alloc(ns + 1, st));
+    HDP_TRY(pm.alloc(ns + 1, st));
+    HDP_TRY(f->auxd.alloc(ns + 1, st));
+    HDP_TRY(lcm.alloc(n_lc + 1, st));
+    HDP_TRY(f->lc_rowoff.alloc(n_lc + 1, st));
+    k_chunk_weight<<<grid_for(ns + 1, 256), 256, 0, st>>>(ns, f->short_info.get(), f->short_rows.get(),
+                                                          f->lc_start.get(), wt.get(), pm.get()); note_launch();
+    k_lc_m<<<grid_for(n_lc + 1, 256), 256, 0, st>>>(n_lc, f->lc_list.get(), f->lmeta.get(), lcm.get()); note_launch();
+    HDP_TRY(exclusive_sum(wt.get(), W.get(), ns + 1, st));
+    HDP_TRY(exclusive_sum(pm.get(), f->auxd.get(), ns + 1, st));
+    HDP_TRY(exclusive_sum(lcm.get(), f->lc_rowoff.get(), n_lc + 1, st));
+    // cumulative weight at every phase boundary
+    std::vector<int64_t> so(f->short_off.begin(), f->short_off.end()), wb(nph + 1);
+    DevBuf<int64_t> dso, dwb, dcb;
+    HDP_TRY(dso.alloc(nph + 1, st));
+    HDP_TRY(dwb.alloc(nph + 1, st));
+    HDP_TRY(dcb.alloc(nph + 1, st));
+    HDP_CHECK_CUDA(cudaMemcpyAsync(dso.get(), so.data(), sizeof(int64_t) * (nph + 1),
+                                   cudaMemcpyHostToDevice, st));
+    k_gather_i64<<<grid_for(nph + 1, 64), 64, 0, st>>>(nph + 1, W.get(), dso.get(), dwb.get()); note_launch();
+    HDP_TRY(to_host(wb.data(), dwb.get(), nph + 1, st));
+    f->chunk_off.assign(nph + 1, 0);
+    for (int r = 0; r < nph; r++)
+        f->chunk_off[r + 1] = f->chunk_off[r] + ((wb[r + 1] - wb[r] + kChunkWords - 1) >> kChunkShift);
+    const int64_t nc = f->chunk_off[nph];
+    HDP_TRY(f->chunk_first.alloc(nc + 1, st));
+    HDP_TRY(f->chunk_desc.alloc(nc + 1, st));
+    int32_t last = (int32_t)ns;
+    HDP_CHECK_CUDA(cudaMemcpyAsync(f->chunk_first.get() + nc, &last, sizeof(int32_t),
+                                   cudaMemcpyHostToDevice, st));
+    f->chunk_words = 0;
+    if (nc > 0) {
+        std::vector<int64_t> cb(f->chunk_off.begin(), f->chunk_off.end());
+        HDP_CHECK_CUDA(cudaMemcpyAsync(dcb.get(), cb.data(), sizeof(int64_t) * (nph + 1),
+                                       cudaMemcpyHostToDevice, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(dwb.get(), wb.data(), sizeof(int64_t) * (nph + 1),
+                                       cudaMemcpyHostToDevice, st));
+        k_chunk_fill<<<grid_for(ns, 256), 256, 0, st>>>(ns, nph, dso.get(), dcb.get(), dwb.get(), W.get(),
+                                                        f->chunk_first.get()); note_launch();
+        DevBuf<unsigned long long> mx;
+        HDP_TRY(mx.alloc(1, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), st));
+        k_chunk_desc<<<grid_for(nc, 256), 256, 0, st>>>(nc, f->chunk_first.get(), f->short_info.get(),
+                                                        f->short_rows.get(), f->lc_start.get(),
+                                                        f->lc_rowoff.get(), f->auxd.get(), W.get(),
+                                                        f->chunk_desc.get(), mx.get()); note_launch();
+        HDP_CHECK_LAUNCH();
+        unsigned long long words = 0;
+        HDP_TRY(to_host(&words, mx.get(), 1, st));  // also orders the pageable copies above
+        f->chunk_words = (int64_t)words + 64;
+    }
+    f->chunks_ok = f->chunk_words <= kChunkMaxWords;
+    return HDP_OK;
+}
 
 static int lanes_finish(hdp_forest* f) {
     cudaStream_t st = f->st;
@@ -906,7 +1111,8 @@ static int lanes_finish(hdp_forest* f) {
     k_node_m<<<grid_for(n, B), B, 0, st>>>(n, f->tree_id.get(), f->t_m.get(), nm.get()); note_launch();
     HDP_TRY(exclusive_sum(nm.get(), f->nodeoff.get(), n + 1, st));
     HDP_CHECK_LAUNCH();
-    HDP_TRY(to_host(&f->total_entries, f->rowoff.get() + n, 1, st));
+    HDP_TRY(to_host(&f->total_entries, f->nodeoff.get() + n, 1, st));
+    HDP_TRY(to_host(&f->total_rows, f->rowoff.get() + n, 1, st));
     DevBuf<int32_t> mx;
     HDP_TRY(mx.alloc(1, st));
     HDP_TRY(reduce_max(f->t_m.get(), mx.get(), f->n_trees, st));
@@ -921,7 +1127,7 @@ static int lanes_finish(hdp_forest* f) {
     HDP_TRY(f->lc_row.alloc(n_lc + 1, st));
     HDP_TRY(f->lc_sim.alloc(n_lc + 1, st));
     k_pos_meta<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), f->tree_id.get(), f->t_doff.get(),
-                                            f->lsim.get(), f->lc_start.get(), f->rowoff.get(),
+                                            f->lsim.get(), f->lc_start.get(), f->t_m.get(),
                                             f->lmeta.get(),
                                             f->lsimf.get()); note_launch();
     if (n_lc > 0)
@@ -935,14 +1141,15 @@ static int lanes_finish(hdp_forest* f) {
     if (nl > 0)
         k_path_meta<<<grid_for(nl, B), B, 0, st>>>(nl, f->long_paths.get(), f->p_start.get(),
                                                   f->p_len.get(), f->p_par.get(), f->p_tree.get(),
-                                                  f->t_doff.get(), f->rowoff.get(),
+                                                  f->t_doff.get(), f->t_m.get(), f->rowoff.get(),
                                                   f->long_info.get(), f->long_rows.get()); note_launch();
     if (ns > 0)
         k_path_meta<<<grid_for(ns, B), B, 0, st>>>(ns, f->short_paths.get(), f->p_start.get(),
                                                   f->p_len.get(), f->p_par.get(), f->p_tree.get(),
-                                                  f->t_doff.get(), f->rowoff.get(),
+                                                  f->t_doff.get(), f->t_m.get(), f->rowoff.get(),
                                                   f->short_info.get(), f->short_rows.get()); note_launch();
     HDP_CHECK_LAUNCH();
+    HDP_TRY(build_chunks(f));
     tr.mark("lanes finish");
     f->lanes_set = 1;
     f->geom_w = -1;
@@ -1012,6 +1219,7 @@ int hdp_forest_set_lanes_range(hdp_forest* f, int x0, int nx, void* stream) {
     k_iota<<<grid_for(nx, 256), 256, 0, st>>>(nx, f->dlist.get(), x0); note_launch();
     HDP_CHECK_LAUNCH();
     f->range_x0 = x0;
+    f->max_d = x0 + nx - 1;
     return lanes_finish(f);
 }
 
@@ -1021,6 +1229,7 @@ int hdp_forest_set_lanes(hdp_forest* f, const uint32_t* tree_masks, int nw, void
     f->st = (cudaStream_t)stream;
     cudaStream_t st = f->st;
     f->range_x0 = -1;
+    f->max_d = 32 * nw - 1;
     HDP_TRY(f->t_m.alloc(f->n_trees, st));
     HDP_TRY(f->t_doff.alloc(f->n_trees + 1, st));
     k_lanes_count<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw, f->t_m.get()); note_launch();

@@ -13,6 +13,29 @@ constexpr int kShortPath = 8;
 // decoupled look-back in the aggregation kernels.
 constexpr int kSeg = 64;
 
+namespace hdp {
+// Short-path chunks: the short paths of a phase are cut into runs whose rows,
+// light-children rows, parent rows and metadata fit in shared memory; chunk
+// c of a phase holds the paths whose cumulative weight (4-byte words) falls
+// in the c-th window of kChunkWords.
+constexpr int kChunkShift = 12;
+constexpr int kChunkWords = 1 << kChunkShift;
+constexpr int kChunkMaxWords = 48 * 1024;  // 192 KB of shared memory
+
+struct alignas(16) ChunkDesc {
+    int p0, np;        // short-path list range
+    int K0, nk;        // layout positions of the chunk's nodes
+    int L0, nl;        // light-child entries of those nodes
+    int n4;            // float4 words of staged rows
+    int naux_up, naux_dn;
+    int pad0, pad1, pad2;
+    long long a0;      // first staged row float (16-byte aligned)
+    long long lcr0;    // lc_rowoff[L0]
+    long long auxd0;   // auxd[p0]
+    long long pad3;
+};
+}  // namespace hdp
+
 struct hdp_forest {
     cudaStream_t st = nullptr;
     int64_t n = 0;         // nodes
@@ -42,6 +65,8 @@ struct hdp_forest {
     // each list phase-major; host offsets per phase
     hdp::DevBuf<int32_t> long_paths, short_paths;
     std::vector<int64_t> long_off, short_off;
+    std::vector<int64_t> short_end;  // host: short paths of phase r occupy positions [phase_node[r], short_end[r])
+    std::vector<int64_t> lp_mid;     // host: light parents on long paths of phase r = [lp_mid[r], lp_off[r+1])
     hdp::DevBuf<int2> seg_tab;      // (long-path index, segment index from the head)
     std::vector<int64_t> seg_off;   // host: segments of phase r = [seg_off[r], seg_off[r+1])
     int64_t n_segs = 0;
@@ -49,10 +74,12 @@ struct hdp_forest {
     // disparity lanes per tree
     int lanes_set = 0;
     int max_m = 0;
+    int max_d = 0;                 // upper bound on any lane's disparity
     hdp::DevBuf<int32_t> t_m, t_doff, dlist;
-    hdp::DevBuf<int64_t> rowoff;   // layout order, n+1: hypothesis row offsets
+    hdp::DevBuf<int64_t> rowoff;   // layout order, n+1: row offsets (rows of ceil4(m) floats)
     hdp::DevBuf<int64_t> nodeoff;  // node-id order, n: pixel-major volume offsets
-    int64_t total_entries = 0;
+    int64_t total_entries = 0;     // sum of m over nodes (stored hypotheses)
+    int64_t total_rows = 0;        // floats of the row layout (every row padded to a multiple of 4)
     int range_x0 = -1;             // >= 0: every tree's lanes are x0 + j
 
     // packed metadata for the aggregation kernels (built with the lanes):
@@ -65,4 +92,14 @@ struct hdp_forest {
     hdp::DevBuf<longlong2> long_rows;   // (first row, parent's row or -1)
     hdp::DevBuf<int4> short_info;  // single-node paths: (position, m, lane offset, 0)
     hdp::DevBuf<longlong2> short_rows;
+    // chunks of the short-path row block of every phase: chunk c holds the
+    // short paths [chunk_first[c], chunk_first[c+1]) (indices into the short
+    // list), those whose first row falls in the c-th kChunkRows-float window
+    hdp::DevBuf<int32_t> chunk_first;
+    hdp::DevBuf<hdp::ChunkDesc> chunk_desc;
+    hdp::DevBuf<int64_t> lc_rowoff;  // per light-child entry: prefix of m (aux row offsets, up pass)
+    hdp::DevBuf<int64_t> auxd;       // per short path: prefix of m over paths with a parent (down pass)
+    std::vector<int64_t> chunk_off;  // host: chunks of phase r = [chunk_off[r], chunk_off[r+1])
+    int64_t chunk_words = 0;         // shared-memory words the largest chunk needs
+    int chunks_ok = 0;               // chunks fit in shared memory
 };

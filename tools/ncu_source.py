@@ -1,9 +1,10 @@
 """Print source lines with the most warp-stall samples from an ncu report.
-usage: python tools/ncu_source.py REPORT [min_pct] (needs ncu on PATH)"""
+usage: python tools/ncu_source.py REPORT [min_pct] [ncu filter args...] (needs ncu on PATH)"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 thr = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+extra = sys.argv[3:]  # e.g. -k regex:NAME --launch-skip 2 --launch-count 1
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"] + extra,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 def num(x):

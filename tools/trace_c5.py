@@ -12,7 +12,7 @@ def T(label, fn):
     torch.cuda.synchronize(); t = time.perf_counter(); r = fn(); torch.cuda.synchronize()
     print(f"{label:20s} {1e3*(time.perf_counter()-t):8.3f} ms", flush=True); return r
 H, W, d = spec.height, spec.width, spec.d_max
-for rep in range(2):
+for rep in range(3):
     print("rep", rep)
     il = E.to_f64(L); ir = E.to_f64(R)
     pl = E.prepare(il, False)[3]; pr = E.prepare(ir, False)[3]
@@ -22,4 +22,6 @@ for rep in range(2):
     T("set_lanes", lambda: f.set_lanes_range(0, d + 1))
     lev = E.Level(0, H, W, 3, d, il, ir, pl, pr)
     T("aggregate", lambda: f.aggregate(lev))
-    print("phases", f.n_phases, "paths", f.n_paths, "depth", f.max_depth, "mst rounds", rounds)
+    del f
+    T("full baseline", lambda: E.run_baseline_batch(L, R, d))
+    pass
