@@ -73,6 +73,7 @@ struct AggArgs {
     int atomic_keys;
     int store_all;  // store A for every node (volume requested), not only light parents
     int max_m;
+    int qsub, qsub_shift;  // chunk kernels: float4 lanes per path (power of 2 <= 32)
 };
 
 __device__ __forceinline__ int lane_disp(const AggArgs& a, int doff, int j) {
@@ -109,6 +110,10 @@ __device__ __forceinline__ void cp_async4(float* smem, const float* gmem, bool p
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -136,6 +141,11 @@ __device__ __forceinline__ Slot slot_of(const AggArgs& a) {
 
 constexpr int BU = 4;  // independent work items per thread (memory-level parallelism)
 
+// Cost of the padding lanes of a row (rows hold ceil4(m) floats).  Large
+// enough never to win an argmin, small enough that sums over a whole tree stay
+// finite (no inf, so no 0 * inf anywhere in the recurrences).
+constexpr float kPadCost = 1.0e30f;
+
 // b(v) = E(v) for every node of a phase, BU independent (node, lane) items
 // per thread; two load levels (metadata -> image planes).
 __global__ void __launch_bounds__(256) k_ecompute(AggArgs a, int64_t k0, int64_t nk) {
@@ -160,7 +170,7 @@ __global__ void __launch_bounds__(256) k_ecompute(AggArgs a, int64_t k0, int64_t
     for (int u = 0; u < BU; u++) {
         bool lv = ok[u] && j[u] < mt[u].w;
         int d = lv ? lane_disp(a, mt[u].y, j[u]) : 0;
-        v[u] = lv ? raw_cost(a, mt[u].x, mt[u].z, d, j[u]) : 0.0f;
+        v[u] = lv ? raw_cost(a, mt[u].x, mt[u].z, d, j[u]) : kPadCost;
     }
 #pragma unroll
     for (int u = 0; u < BU; u++)
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(256) k_ecost_pix(AggArgs a, const int32_t* __r
         const int mp = (mt.w + 3) & ~3;
         for (int j = sl; j < mp; j += a.sub) {
             if (j >= mt.w) {  // row padding
-                out[j] = 0.0f;
+                out[j] = kPadCost;
                 continue;
             }
             const int d = lane_disp(a, mt.y, j);
@@ -599,222 +609,296 @@ __global__ void __launch_bounds__(256) k_down_short(AggArgs a, int64_t s0, int64
 // follow touch only shared memory, and global traffic is the chunk's rows in,
 // the changed rows and the keys out.  One `sub`-lane group walks one path.
 
+constexpr int kChunkThreads = 256;  // one CTA per chunk
+
 struct ChunkSm {
-    int4* info;     // per path: (start, len, m, lane offset)
-    int* rowo;      // per path: offset of its first row in `own`
-    int* paro;      // down: offset of its parent row in `aux` (-1 at a root)
-    float* own;     // the chunk's rows
-    float* aux;
-    float* sim;     // per node: lsimf
-    int* nodei;     // up: lc_start - L0 (nk + 1); down: node id (nk)
-    float* lsim;    // up: per light-child entry, its similarity
-    int* loff;      // up: per entry, offset of its row in `aux`
+    int4* info;         // per path: (start, len, m, lane offset)
+    longlong2* prow;    // per path: (first row, parent's row or -1)
+    long long* auxd;    // down: per path, auxd (parent-row slot)
+    long long* lcr;     // up: per light-child entry (nl + 1), lc_rowoff
+    long long* lcrow;   // up: per entry, global row of the child
+    float* own;         // the chunk's rows
+    float* aux;         // light children's rows (up) / parent rows (down)
+    float* sim;         // per node: lsimf
+    int* nodei;         // up: lc_start (nk + 1)
+    float* lsim;        // up: per entry, similarity of the child
+    int4* meta;         // down: per node, lmeta (node, lane offset, column, m)
+    long long* nrow;    // down: per node, rowoff
 };
 
 template <bool UP>
 __device__ __forceinline__ ChunkSm carve(const ChunkDesc& d, float4* sm4) {
     ChunkSm s;
     s.info = reinterpret_cast<int4*>(sm4);
-    float4* p = sm4 + d.np;
+    s.prow = reinterpret_cast<longlong2*>(sm4 + d.np);
+    s.meta = reinterpret_cast<int4*>(sm4 + 2 * d.np);
+    float4* p = sm4 + 2 * d.np + (UP ? 0 : d.nk);
     s.own = reinterpret_cast<float*>(p);
     p += d.n4;
-    float* q = reinterpret_cast<float*>(p);
-    s.aux = q;
-    q += ((UP ? d.naux_up : d.naux_dn) + 3) & ~3;
+    s.aux = reinterpret_cast<float*>(p);
+    p += ((UP ? d.naux_up : d.naux_dn) + 3) >> 2;
+    long long* l = reinterpret_cast<long long*>(p);
+    s.auxd = l;
+    l += UP ? 0 : (d.np + 1) & ~1;
+    s.lcr = l;
+    l += UP ? (d.nl + 2) & ~1 : 0;
+    s.lcrow = l;
+    l += UP ? (d.nl + 1) & ~1 : 0;
+    s.nrow = l;
+    l += UP ? 0 : (d.nk + 1) & ~1;
+    float* q = reinterpret_cast<float*>(l);
     s.sim = q;
-    q += (d.nk + 3) & ~3;
+    q += d.nk;
     s.nodei = reinterpret_cast<int*>(q);
-    q += (d.nk + 4) & ~3;
-    s.rowo = reinterpret_cast<int*>(q);
-    q += (d.np + 3) & ~3;
-    s.paro = reinterpret_cast<int*>(q);
-    q += (d.np + 3) & ~3;
+    q += d.nk + 1;
     s.lsim = q;
-    q += (d.nl + 3) & ~3;
-    s.loff = reinterpret_cast<int*>(q);
     return s;
 }
 
-// 4-byte cp.async of `cnt` floats, lanes of one warp striding the row
-__device__ __forceinline__ void row_async(float* dst, const float* src, int cnt, int lane) {
-    for (int j = lane; j < cnt; j += 32) cp_async4(dst + j, src + j, true);
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4u(void* smem, const void* gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// 1-D TMA (bulk async copy) global -> shared, completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
+// 16-byte cp.async of a padded row of `cnt` floats (rows start 16-byte
+// aligned), lanes of one warp striding the row
+__device__ __forceinline__ void row_async(float* dst, const float* src, int cnt, int lane) {
+    for (int j = lane * 4; j < cnt; j += 128) cp_async16(dst + j, src + j);
+}
+
+// The CTA stages its chunk with asynchronous copies only (no load waits on
+// the issue path).  The row block and every auxiliary row (light children's
+// A_up on the way up, the parent's A on the way down) arrive by 1-D TMA bulk
+// copies completing on one mbarrier armed with the chunk's byte count; the
+// small metadata arrays come by cp.async (group 1: what the auxiliary-row
+// copies need, group 2: the rest).
 template <bool UP>
-__device__ __forceinline__ ChunkSm stage_chunk(const AggArgs& a, const ChunkDesc& d, float4* sm4) {
+__device__ __forceinline__ ChunkSm stage_chunk(const AggArgs& a, const ChunkDesc& d, float4* sm4,
+                                               unsigned long long* bar) {
     ChunkSm s = carve<UP>(d, sm4);
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-    const float4* src = reinterpret_cast<const float4*>(a.aup + d.a0);
-    for (int i = tid; i < d.n4; i += nt) reinterpret_cast<float4*>(s.own)[i] = src[i];
-    for (int i = tid; i < d.nk; i += nt) s.sim[i] = a.lsimf[d.K0 + i];
+    if (tid == 0) mbar_init(bar, 1);
+    for (int i = tid; i < d.np; i += nt) {
+        cp_async16(s.info + i, a.pinfo + d.p0 + i);
+        cp_async16(s.prow + i, a.prows + d.p0 + i);
+        if (!UP) cp_async8(s.auxd + i, a.auxd + d.p0 + i);
+    }
     if (UP) {
-        for (int i = tid; i <= d.nk; i += nt) s.nodei[i] = a.lc_start[d.K0 + i] - d.L0;
-        for (int i = tid; i < d.nl; i += nt) {
-            s.lsim[i] = a.lc_sim[d.L0 + i];
-            s.loff[i] = (int)(a.lc_rowoff[d.L0 + i] - d.lcr0);
-        }
+        for (int i = tid; i <= d.nl; i += nt) cp_async8(s.lcr + i, a.lc_rowoff + d.L0 + i);
+        for (int i = tid; i < d.nl; i += nt) cp_async8(s.lcrow + i, a.lc_row + d.L0 + i);
+    }
+    cp_commit();
+    for (int i = tid; i < d.nk; i += nt) cp_async4u(s.sim + i, a.lsimf + d.K0 + i);
+    if (UP) {
+        for (int i = tid; i <= d.nk; i += nt) cp_async4u(s.nodei + i, a.lc_start + d.K0 + i);
+        for (int i = tid; i < d.nl; i += nt) cp_async4u(s.lsim + i, a.lc_sim + d.L0 + i);
     } else {
-        for (int i = tid; i < d.nk; i += nt) s.nodei[i] = a.lmeta[d.K0 + i].x;
-    }
-    // path metadata, 32 paths per warp step; the auxiliary rows are issued as
-    // soon as their source offsets are known
-    for (int i0 = warp * 32; i0 < d.np; i0 += nw * 32) {
-        const int i = i0 + lane;
-        int4 in = make_int4(0, 0, 0, 0);
-        longlong2 rw = make_longlong2(0, -1);
-        int po = -1;
-        if (i < d.np) {
-            in = a.pinfo[d.p0 + i];
-            rw = a.prows[d.p0 + i];
-            s.info[i] = in;
-            s.rowo[i] = (int)(rw.x - d.a0);
-            if (!UP && rw.y >= 0) po = (int)(a.auxd[d.p0 + i] - d.auxd0);
-            s.paro[i] = po;
-        }
-        if (!UP) {
-            const int cnt = min(32, d.np - i0);
-            for (int t = 0; t < cnt; t++) {
-                const int pot = __shfl_sync(0xffffffffu, po, t);
-                const long long src_row = __shfl_sync(0xffffffffu, rw.y, t);
-                const int mt = __shfl_sync(0xffffffffu, in.z, t);
-                if (pot >= 0) row_async(s.aux + pot, a.aup + src_row, mt, lane);
-            }
-        }
-    }
-    if (UP) {
-        for (int e0 = warp * 32; e0 < d.nl; e0 += nw * 32) {
-            const int e = e0 + lane;
-            long long row = 0;
-            int off = 0, me = 0;
-            if (e < d.nl) {
-                row = a.lc_row[d.L0 + e];
-                const long long r0 = a.lc_rowoff[d.L0 + e];
-                off = (int)(r0 - d.lcr0);
-                me = (int)(a.lc_rowoff[d.L0 + e + 1] - r0);
-            }
-            const int cnt = min(32, d.nl - e0);
-            for (int t = 0; t < cnt; t++) {
-                const long long rt = __shfl_sync(0xffffffffu, row, t);
-                const int ot = __shfl_sync(0xffffffffu, off, t);
-                const int mt = __shfl_sync(0xffffffffu, me, t);
-                row_async(s.aux + ot, a.aup + rt, mt, lane);
-            }
+        for (int i = tid; i < d.nk; i += nt) {
+            cp_async16(s.meta + i, a.lmeta + d.K0 + i);
+            cp_async8(s.nrow + i, a.rowoff + d.K0 + i);
         }
     }
     cp_commit();
+    __syncthreads();  // barrier initialised
+    if (tid == 0) {
+        mbar_expect_tx(bar, (unsigned)d.n4 * 16u + (unsigned)(UP ? d.naux_up : d.naux_dn) * 4u);
+        bulk_g2s(s.own, a.aup + d.a0, (unsigned)d.n4 * 16u, bar);
+    }
+    cp_wait_one();
+    __syncthreads();  // group 1 visible to every thread
+    if (UP) {
+        for (int e = tid; e < d.nl; e += nt) {
+            const long long r0 = s.lcr[e];
+            bulk_g2s(s.aux + (r0 - d.lcr0), a.aup + s.lcrow[e], (unsigned)(s.lcr[e + 1] - r0) * 4u, bar);
+        }
+    } else {
+        for (int i = tid; i < d.np; i += nt) {
+            const long long pr = s.prow[i].y;
+            if (pr >= 0)
+                bulk_g2s(s.aux + (s.auxd[i] - d.auxd0), a.aup + pr, (unsigned)((s.info[i].z + 3) & ~3) * 4u, bar);
+        }
+    }
     cp_wait_all();
+    mbar_wait(bar, 0);
     __syncthreads();
     return s;
 }
 
 // Up pass: tail -> head, A_up(q) = (E(q) + sum_light s_c A_up(c)) + s_{q+1} A_up(q+1)
-// (the operation order of k_light + k_scan_up_short).  Changed rows are
-// stored; a lone leaf row (A_up = E) is left alone.
-__global__ void __launch_bounds__(256) k_up_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
-                                                  int64_t cbase) {
+// (the operation order of k_light + k_scan_up_short).  One thread per
+// (path, float4 column); changed rows are stored, a lone leaf row (A_up = E)
+// is left alone.
+__global__ void __launch_bounds__(kChunkThreads) k_up_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
+                                                            int64_t cbase) {
     extern __shared__ float4 sm4[];
     const ChunkDesc d = descs[cbase + blockIdx.x];
     if (d.np == 0) return;
-    const ChunkSm s = stage_chunk<true>(a, d, sm4);
-    const int lane = threadIdx.x & 31;
-    const int per = 32 >> a.sub_shift;
-    const int sl = lane & (a.sub - 1);
-    for (int pb = (int)(threadIdx.x >> 5) * per; pb < d.np; pb += (int)(blockDim.x >> 5) * per) {
-        const int pi = pb + (lane >> a.sub_shift);
-        if (pi >= d.np) break;  // no warp-collective operations below
+    __shared__ unsigned long long bar;
+    const ChunkSm s = stage_chunk<true>(a, d, sm4, &bar);
+    const float4* own4 = reinterpret_cast<const float4*>(s.own);
+    const float4* aux4 = reinterpret_cast<const float4*>(s.aux);
+    // with a uniform row width the (path, column) split is a multiply-high;
+    // otherwise each path takes a 32-column stride of threads
+    const int mqu = d.mqu;
+    const int items = mqu > 0 ? d.np * mqu : d.np << a.qsub_shift;
+    for (int t = threadIdx.x; t < items; t += blockDim.x) {
+        int pi, jq;
+        if (mqu > 0) {
+            pi = (int)__umulhi((unsigned)t, d.inv);
+            jq = t - pi * mqu;
+        } else {
+            pi = t >> a.qsub_shift;
+            jq = t & (a.qsub - 1);
+        }
         const int4 info = s.info[pi];
-        const int len = info.y, m = info.z, mp = (m + 3) & ~3;
-        float* srow = s.own + s.rowo[pi];
-        float* grow = a.aup + d.a0 + s.rowo[pi];
-        float sn = 0.0f;  // similarity of node q + 1
-        for (int q = len - 1; q >= 0; q--) {
-            const int kk = info.x - d.K0 + q;
-            const float f = s.sim[kk];
-            const bool has_l = __float_as_uint(f) >> 31;
-            const bool changed = has_l || q + 1 < len;
-            const int e0 = s.nodei[kk], e1 = s.nodei[kk + 1];
-            float* sq = srow + q * mp;
-            for (int j = sl; j < m; j += a.sub) {
-                float b = sq[j];
+        const int mq = (info.z + 3) >> 2;
+        const long long r0 = s.prow[pi].x;
+        const int k0 = info.x - d.K0;
+        for (; jq < mq; jq += a.qsub) {
+            const float4* col = own4 + ((r0 - d.a0) >> 2) + jq;
+            float4* gcol = reinterpret_cast<float4*>(a.aup + r0) + jq;
+            float4 xn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            float sn = 0.0f;  // similarity of node q + 1
+            for (int q = info.y - 1; q >= 0; q--) {
+                const float f = s.sim[k0 + q];
+                const bool has_l = __float_as_uint(f) >> 31;
+                const bool tail = q + 1 == info.y;
+                float4 b = col[q * mq];
                 if (has_l) {
-                    float x = s.lsim[e0] * s.aux[s.loff[e0] + j];
-                    for (int e = e0 + 1; e < e1; e++) x += s.lsim[e] * s.aux[s.loff[e] + j];
-                    b = b + x;
+                    const int e0 = s.nodei[k0 + q] - d.L0, e1 = s.nodei[k0 + q + 1] - d.L0;
+                    const float c0 = s.lsim[e0];
+                    const float4 v0 = aux4[((int)(s.lcr[e0] - d.lcr0) >> 2) + jq];
+                    float4 x = make_float4(c0 * v0.x, c0 * v0.y, c0 * v0.z, c0 * v0.w);
+                    for (int e = e0 + 1; e < e1; e++) {
+                        const float ce = s.lsim[e];
+                        const float4 v = aux4[((int)(s.lcr[e] - d.lcr0) >> 2) + jq];
+                        x.x += ce * v.x;
+                        x.y += ce * v.y;
+                        x.z += ce * v.z;
+                        x.w += ce * v.w;
+                    }
+                    b.x = b.x + x.x;
+                    b.y = b.y + x.y;
+                    b.z = b.z + x.z;
+                    b.w = b.w + x.w;
                 }
-                const float x = (q + 1 < len) ? b + sn * sq[mp + j] : b;
-                sq[j] = x;
-                if (changed) grow[q * mp + j] = x;
+                if (!tail) {
+                    b.x = b.x + sn * xn.x;
+                    b.y = b.y + sn * xn.y;
+                    b.z = b.z + sn * xn.z;
+                    b.w = b.w + sn * xn.w;
+                }
+                if (has_l || !tail) gcol[q * mq] = b;
+                xn = b;
+                sn = fabsf(f);
             }
-            sn = fabsf(f);
+            if (mqu > 0) break;  // uniform width: exactly one column per item
         }
     }
 }
 
 // Down pass fused with the first argmin: head -> tail,
 // A(q) = s_q A(q - 1) + (1 - s_q^2) A_up(q) with A(-1) = A(parent) (s = 0 at a
-// root); A is stored only where a light child will read it.
-__global__ void __launch_bounds__(256) k_down_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
-                                                    int64_t cbase) {
+// root), one thread per (path, float4 column), A kept in shared memory and
+// stored globally only where a light child will read it; then one thread
+// per node scans its row for the first minimum (aggregation.py:249).
+__global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
+                                                              int64_t cbase) {
     extern __shared__ float4 sm4[];
     const ChunkDesc d = descs[cbase + blockIdx.x];
     if (d.np == 0) return;
-    const ChunkSm s = stage_chunk<false>(a, d, sm4);
-    const int lane = threadIdx.x & 31;
-    const int per = 32 >> a.sub_shift;
-    const int sl = lane & (a.sub - 1);
-    const int width = a.sub;
-    for (int pb = (int)(threadIdx.x >> 5) * per; pb < d.np; pb += (int)(blockDim.x >> 5) * per) {
-        const int pi = pb + (lane >> a.sub_shift);
-        const bool valid = pi < d.np;
-        const int4 info = valid ? s.info[pi] : make_int4(0, 0, 0, 0);
-        const int len = info.y, m = info.z, mp = (m + 3) & ~3;
-        int lmax = len;
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, off));
-        const int ro = valid ? s.rowo[pi] : 0;
-        const int po = valid ? s.paro[pi] : -1;
-        float* srow = s.own + ro;
-        float* grow = a.aup + d.a0 + ro;
-        for (int q = 0; q < lmax; q++) {
-            const bool on = q < len;
-            const int kk = info.x - d.K0 + q;
-            const float f = on ? s.sim[kk] : 0.0f;
-            float sv = fabsf(f);
-            if (q == 0 && po < 0) sv = 0.0f;  // root: A = A_up
-            const bool st = on && (a.store_all || (__float_as_uint(f) >> 31));
-            const float w = 1.0f - sv * sv;
-            float* sq = srow + q * mp;
-            const float* prev = q == 0 ? s.aux + (po >= 0 ? po : 0) : sq - mp;
-            const bool has_prev = q > 0 || po >= 0;
-            uint32_t best = 0xffffffffu;
-            int bj = 0x7fffffff;
-            for (int j = sl; on && j < m; j += a.sub) {
-                const float yp = has_prev ? prev[j] : 0.0f;
-                const float y = sv * yp + w * sq[j];
-                sq[j] = y;
-                if (st) grow[q * mp + j] = y;
-                const uint32_t o = ord_f32(y);
-                if (o < best) {
-                    best = o;
-                    bj = j;
-                }
-            }
-            uint32_t mn = best;
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                uint32_t t = __shfl_xor_sync(0xffffffffu, mn, off);
-                if (off < width) mn = min(mn, t);
-            }
-            int jm = best == mn ? bj : 0x7fffffff;
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                int t = __shfl_xor_sync(0xffffffffu, jm, off);
-                if (off < width) jm = min(jm, t);
-            }
-            if (on && sl == 0 && a.keys && jm != 0x7fffffff)
-                a.keys[s.nodei[kk]] = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, info.w, jm);
+    __shared__ unsigned long long bar;
+    const ChunkSm s = stage_chunk<false>(a, d, sm4, &bar);
+    float4* own4 = reinterpret_cast<float4*>(s.own);
+    const float4* aux4 = reinterpret_cast<const float4*>(s.aux);
+    const int mqu = d.mqu;
+    const int items = mqu > 0 ? d.np * mqu : d.np << a.qsub_shift;
+    for (int t = threadIdx.x; t < items; t += blockDim.x) {
+        int pi, jq;
+        if (mqu > 0) {
+            pi = (int)__umulhi((unsigned)t, d.inv);
+            jq = t - pi * mqu;
+        } else {
+            pi = t >> a.qsub_shift;
+            jq = t & (a.qsub - 1);
         }
+        const int4 info = s.info[pi];
+        const int mq = (info.z + 3) >> 2;
+        const longlong2 pr = s.prow[pi];
+        const float* sim = s.sim + (info.x - d.K0);
+        for (; jq < mq; jq += a.qsub) {
+            float4* col = own4 + ((pr.x - d.a0) >> 2) + jq;
+            float4* gcol = reinterpret_cast<float4*>(a.aup + pr.x) + jq;
+            float4 yp = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (pr.y >= 0) yp = aux4[((s.auxd[pi] - d.auxd0) >> 2) + jq];
+            for (int q = 0; q < info.y; q++) {
+                const float f = sim[q];
+                const float sv = (q == 0 && pr.y < 0) ? 0.0f : fabsf(f);  // root: A = A_up
+                const float w = 1.0f - sv * sv;
+                const float4 u = col[q * mq];
+                float4 y;
+                y.x = sv * yp.x + w * u.x;
+                y.y = sv * yp.y + w * u.y;
+                y.z = sv * yp.z + w * u.z;
+                y.w = sv * yp.w + w * u.w;
+                col[q * mq] = y;
+                if (a.store_all || (__float_as_uint(f) >> 31)) gcol[q * mq] = y;
+                yp = y;
+            }
+            if (mqu > 0) break;
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < d.nk; i += blockDim.x) {
+        const int4 mt = s.meta[i];
+        const int mq = (mt.w + 3) >> 2;
+        const float4* row = reinterpret_cast<const float4*>(s.own + (s.nrow[i] - d.a0));
+        // the minimum (padding lanes hold kPadCost and never win), then the
+        // first lane holding it
+        float best = row[0].x;
+        for (int jq = 0; jq < mq; jq++) {
+            const float4 y = row[jq];
+            best = fminf(best, fminf(fminf(y.x, y.y), fminf(y.z, y.w)));
+        }
+        int bj = 0;
+        for (int jq = 0; jq < mq; jq++) {
+            const float4 y = row[jq];
+            if (y.x == best) { bj = 4 * jq; break; }
+            if (y.y == best) { bj = 4 * jq + 1; break; }
+            if (y.z == best) { bj = 4 * jq + 2; break; }
+            if (y.w == best) { bj = 4 * jq + 3; break; }
+        }
+        if (a.keys) a.keys[mt.x] = ((unsigned long long)ord_f32(best) << 32) | (uint32_t)lane_disp(a, mt.y, bj);
     }
 }
 
@@ -950,6 +1034,12 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.sub = f->max_m <= 16 ? std::max(4, pow2_at_least(f->max_m)) : 32;  // >= one padded row
     a.sub_shift = 0;
     while ((1 << a.sub_shift) < a.sub) a.sub_shift++;
+    {
+        const int mq = (f->max_m + 3) >> 2;
+        a.qsub = mq <= 16 ? pow2_at_least(mq) : 32;
+        a.qsub_shift = 0;
+        while ((1 << a.qsub_shift) < a.qsub) a.qsub_shift++;
+    }
     DevBuf<float> aup;
     DevBuf<unsigned long long> carry;
     DevBuf<int> tickets;
@@ -1004,7 +1094,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         k_ecost_pix<<<g, 256, use ? smem : 0, st>>>(a, f->lpos.get(), f->max_d, use); note_launch();
     }
     const bool chunks = f->chunks_ok != 0;
-    const size_t csmem = (size_t)f->chunk_words * sizeof(float);
+    const size_t csmem = (size_t)((f->chunk_words + 3) & ~3ll) * sizeof(float);
     sh.lc_rowoff = f->lc_rowoff.get();
     sh.auxd = f->auxd.get();
     if (chunks && csmem > 48 * 1024) {
@@ -1025,7 +1115,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
         if (chunks && nc > 0) {
-            k_up_chunk<<<(unsigned)nc, 256, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
+            k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
         } else if (!chunks && ns > 0) {
             k_scan_up_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
@@ -1040,7 +1130,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
         if (chunks && nc > 0) {
-            k_down_chunk<<<(unsigned)nc, 256, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
+            k_down_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
         } else if (!chunks && ns > 0) {
             k_down_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }

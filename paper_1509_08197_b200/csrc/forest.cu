@@ -965,7 +965,7 @@ __global__ void k_chunk_weight(int64_t ns, const int4* __restrict__ sinfo,
     int4 in = sinfo[i];
     int64_t len = in.y, m = (in.z + 3) & ~3;
     int64_t nlc = lc_start[in.x + in.y] - lc_start[in.x];
-    wt[i] = (len + nlc + 1) * m + 2 * len + 2 * nlc + 16;
+    wt[i] = (len + nlc + 1) * m + 8 * len + 5 * nlc + 16;
     pm[i] = srows[i].y >= 0 ? m : 0;
 }
 
@@ -1023,6 +1023,11 @@ __global__ void k_chunk_desc(int64_t nc, const int32_t* __restrict__ chunk_first
         d.naux_up = (int)(lc_rowoff[d.L0 + d.nl] - d.lcr0);
         d.auxd0 = auxd[p0];
         d.naux_dn = (int)(auxd[p1] - d.auxd0);
+        int mq = (f.z + 3) >> 2;
+        for (int p = p0 + 1; p < p1 && mq > 0; p++)
+            if (((sinfo[p].z + 3) >> 2) != mq) mq = 0;
+        d.mqu = mq;
+        d.inv = mq > 0 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
         atomicMax(max_words, (unsigned long long)(W[p1] - W[p0]));
     }
     desc[c] = d;
@@ -1090,7 +1095,9 @@ static int build_chunks(hdp_forest* f) {
         HDP_TRY(to_host(&words, mx.get(), 1, st));  // also orders the pageable copies above
         f->chunk_words = (int64_t)words + 64;
     }
-    f->chunks_ok = f->chunk_words <= kChunkMaxWords;
+    // rows of up to 32 float4 lanes: one lane group spans a row; wider rows
+    // take the per-path kernels (lane groups across CTAs)
+    f->chunks_ok = f->chunk_words <= kChunkMaxWords && f->max_m <= 128;
     return HDP_OK;
 }
 

@@ -18,9 +18,9 @@ namespace hdp {
 // light-children rows, parent rows and metadata fit in shared memory; chunk
 // c of a phase holds the paths whose cumulative weight (4-byte words) falls
 // in the c-th window of kChunkWords.
-constexpr int kChunkShift = 12;
+constexpr int kChunkShift = 13;
 constexpr int kChunkWords = 1 << kChunkShift;
-constexpr int kChunkMaxWords = 48 * 1024;  // 192 KB of shared memory
+constexpr int kChunkMaxWords = 48 * 1024;  // 192 KB of shared memory per chunk
 
 struct alignas(16) ChunkDesc {
     int p0, np;        // short-path list range
@@ -28,7 +28,9 @@ struct alignas(16) ChunkDesc {
     int L0, nl;        // light-child entries of those nodes
     int n4;            // float4 words of staged rows
     int naux_up, naux_dn;
-    int pad0, pad1, pad2;
+    int mqu;           // float4 columns of every row when all paths share m, else 0
+    unsigned inv;      // ceil(2^32 / mqu): t / mqu == umulhi(t, inv) for small t
+    int pad0;
     long long a0;      // first staged row float (16-byte aligned)
     long long lcr0;    // lc_rowoff[L0]
     long long auxd0;   // auxd[p0]
