@@ -63,6 +63,8 @@ struct AggArgs {
     float* aup;
     float* volume;
     unsigned long long* keys;
+    unsigned long long* agg;    // per (segment, lane): local map value x_loc / y_loc (epoch-tagged)
+    unsigned long long* aggp;   // per segment: local map product P / Q (epoch-tagged)
     unsigned long long* carry;  // per (segment, lane): (epoch << 32 | f32 bits), the
                                 // epoch tag doubles as the readiness flag
     unsigned epoch_up, epoch_down;
@@ -73,6 +75,8 @@ struct AggArgs {
     int atomic_keys;
     int store_all;  // store A for every node (volume requested), not only light parents
     int max_m;
+    int max_mp;            // max_m rounded up to a multiple of 4 (carry stride)
+    int qgroups;           // 32-float4 column groups of the widest row (segment kernels)
     int qsub, qsub_shift;  // chunk kernels: float4 lanes per path (power of 2 <= 32)
 };
 
@@ -184,45 +188,72 @@ __global__ void __launch_bounds__(256) k_ecompute(AggArgs a, int64_t k0, int64_t
 // node's layout row (the rows of one node are contiguous; m lanes -> m/32
 // coalesced stores per warp).
 constexpr int kETile = 64;
-__global__ void __launch_bounds__(256) k_ecost_pix(AggArgs a, const int32_t* __restrict__ lpos,
-                                                   int d_hi, int use_smem) {
+
+__device__ __forceinline__ float pix_cost(const AggArgs& a, float wc, const float4& L, const float4& R) {
+    float color;
+    if (a.c == 3)
+        color = (fabsf(L.x - R.x) + fabsf(L.y - R.y) + fabsf(L.z - R.z)) * (1.0f / 3.0f);
+    else
+        color = fabsf(L.x - R.x);
+    return wc * fminf(a.tc, color) + a.alpha * fminf(a.tg, fabsf(L.w - R.w));
+}
+
+// RANGE: lane j is disparity range_x0 + j (dense / slab lanes); otherwise the
+// tree's lane list.  SMEM: the right-image window fits in shared memory.
+template <bool RANGE, bool SMEM>
+__global__ void __launch_bounds__(256) k_ecost_pix(AggArgs a, const int32_t* __restrict__ lpos, int d_hi) {
     extern __shared__ float4 win[];
     const int64_t base = (int64_t)blockIdx.x * a.w;  // node id of column 0 of this image row
     const int c0 = (int)blockIdx.y * kETile;
     const int lo = max(0, c0 - d_hi), hi = min(a.w, c0 + kETile);
-    if (use_smem)
+    if (SMEM) {
         for (int i = threadIdx.x; i < hi - lo; i += blockDim.x) win[i] = __ldg(a.pr + base + lo + i);
-    __syncthreads();
+        __syncthreads();
+    }
+    const float4* rrow = a.pr + base;  // right-image row (global fallback)
     const int lane = threadIdx.x & 31;
-    const int per = 32 >> a.sub_shift;  // nodes per warp pass
-    const int sl = lane & (a.sub - 1);
-    for (int q = (threadIdx.x >> 5) * per + (lane >> a.sub_shift); q < kETile;
+    const int per = 32 >> a.qsub_shift;  // nodes per warp pass
+    const int sl = lane & (a.qsub - 1);
+    const float wc = 1.0f - a.alpha;
+    for (int q = (threadIdx.x >> 5) * per + (lane >> a.qsub_shift); q < kETile;
          q += (blockDim.x >> 5) * per) {
         const int col = c0 + q;
         if (col >= a.w) break;
         const int64_t node = base + col;
         const int kk = __ldg(lpos + node);
         const int4 mt = __ldg(a.lmeta + kk);
-        float* out = a.aup + __ldg(a.rowoff + kk);
+        float4* out = reinterpret_cast<float4*>(a.aup + __ldg(a.rowoff + kk));
         const float4 L = __ldg(a.pl + node);
-        const int mp = (mt.w + 3) & ~3;
-        for (int j = sl; j < mp; j += a.sub) {
-            if (j >= mt.w) {  // row padding
-                out[j] = kPadCost;
-                continue;
+        const int m = mt.w, mq = (m + 3) >> 2;
+        for (int jq = sl; jq < mq; jq += a.qsub) {
+            float e[4];
+            if (RANGE) {
+                const int x = col - (a.range_x0 + 4 * jq);  // right-image column of lane 4 jq
+                if (x - 3 >= 0 && 4 * jq + 3 < m) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        e[u] = pix_cost(a, wc, L, SMEM ? win[x - u - lo] : __ldg(rrow + x - u));
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (4 * jq + u >= m) e[u] = kPadCost;
+                        else if (x - u < 0) e[u] = a.border;
+                        else e[u] = pix_cost(a, wc, L, SMEM ? win[x - u - lo] : __ldg(rrow + x - u));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int j = 4 * jq + u;
+                    if (j >= m) {
+                        e[u] = kPadCost;
+                        continue;
+                    }
+                    const int x = col - a.dlist[mt.y + j];
+                    e[u] = x < 0 ? a.border : pix_cost(a, wc, L, SMEM ? win[x - lo] : __ldg(rrow + x));
+                }
             }
-            const int d = lane_disp(a, mt.y, j);
-            float e = a.border;
-            if (col - d >= 0) {
-                const float4 R = use_smem ? win[col - d - lo] : __ldg(a.pr + node - d);
-                float color;
-                if (a.c == 3)
-                    color = (fabsf(L.x - R.x) + fabsf(L.y - R.y) + fabsf(L.z - R.z)) * (1.0f / 3.0f);
-                else
-                    color = fabsf(L.x - R.x);
-                e = (1.0f - a.alpha) * fminf(a.tc, color) + a.alpha * fminf(a.tg, fabsf(L.w - R.w));
-            }
-            out[j] = e;
+            out[jq] = make_float4(e[0], e[1], e[2], e[3]);
         }
     }
 }
@@ -360,157 +391,317 @@ __device__ __forceinline__ float get_carry(const unsigned long long* p, unsigned
     return __uint_as_float((unsigned)(w & 0xffffffffu));
 }
 
-// Up pass over one segment (tail -> head).  Segments are taken by ticket in
-// reverse table order, so a path's tail segment comes first; the carry is
-// X_a = x_loc(a) + P * X_b with P = prod s_{a+1..b}.
-__global__ void __launch_bounds__(128) k_seg_up(AggArgs a, int64_t g0, int64_t ng, int* ctr) {
-    __shared__ float buf[4][kSeg][32];
-    __shared__ float ssim[4][kSeg + 1];
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int g = (int)blockIdx.y;
-    int t = warp_ticket(ctr + g);
-    if (t >= ng) return;
-    SegCtx c = seg_ctx(a, g0 + ng - 1 - t);
-    if (g * 32 >= c.m) return;
-    int j = g * 32 + lane;
-    bool act = j < c.m;
-    int cnt = c.b - c.a;
-    const float* base = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp + j;
-    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], base + (int64_t)i * c.mp, act);
-    cp_commit();
-    bool has_next = c.b < c.start + c.len;  // a segment toward the tail exists
-    for (int i = lane; i <= cnt; i += 32) {
-        int p = c.a + i;
-        ssim[warp][i] = (i < cnt || has_next) ? fabsf(a.lsimf[p]) : 0.0f;
+// 1-D TMA (bulk async copy) global -> shared, completing on an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void put_carry4(unsigned long long* p, unsigned epoch, const float4& v) {
+    put_carry(p, epoch, v.x);
+    put_carry(p + 1, epoch, v.y);
+    put_carry(p + 2, epoch, v.z);
+    put_carry(p + 3, epoch, v.w);
+}
+__device__ __forceinline__ float4 get_carry4(const unsigned long long* p, unsigned epoch) {
+    float4 v;
+    v.x = get_carry(p, epoch);
+    v.y = get_carry(p + 1, epoch);
+    v.z = get_carry(p + 2, epoch);
+    v.w = get_carry(p + 3, epoch);
+    return v;
+}
+
+__device__ __forceinline__ bool try_carry4(const unsigned long long* p, unsigned epoch, float4& v) {
+    unsigned long long w0, w1, w2, w3;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w0) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w1) : "l"(p + 1) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w2) : "l"(p + 2) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w3) : "l"(p + 3) : "memory");
+    v = make_float4(__uint_as_float((unsigned)w0), __uint_as_float((unsigned)w1),
+                    __uint_as_float((unsigned)w2), __uint_as_float((unsigned)w3));
+    return (unsigned)(w0 >> 32) == epoch && (unsigned)(w1 >> 32) == epoch &&
+           (unsigned)(w2 >> 32) == epoch && (unsigned)(w3 >> 32) == epoch;
+}
+__device__ __forceinline__ bool try_carry1(const unsigned long long* p, unsigned epoch, float& v) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    v = __uint_as_float((unsigned)w);
+    return (unsigned)(w >> 32) == epoch;
+}
+
+// Carry-in of a segment by decoupled look-back over the segments at offsets
+// dir, 2 dir, ... (toward the tail on the way up, toward the head on the way
+// down): stop at the first published inclusive carry (or past the path's end,
+// where the carry is `edge`), then apply the published local maps in between
+// in the serial chain's order, X = x_loc(k) + P(k) * X.  The arithmetic is
+// exactly the serial chain's, so the result does not depend on timing.
+__device__ __forceinline__ float4 seg_lookback(const AggArgs& a, int64_t gseg, int dir, int kmax,
+                                               unsigned epoch, int jq, bool act, float4 edge) {
+    const size_t lw = (size_t)a.max_mp;
+    int k = 1;
+    float4 X = edge;
+    while (k <= kmax) {
+        const int64_t gk = gseg + (int64_t)dir * k;
+        float4 v;
+        const bool inc = act ? try_carry4(a.carry + gk * lw + 4 * jq, epoch, v) : true;
+        if (__all_sync(0xffffffffu, inc)) {
+            X = v;
+            break;
+        }
+        float4 xl;
+        float P;
+        const bool agg = (act ? try_carry4(a.agg + gk * lw + 4 * jq, epoch, xl) : true) &&
+                         try_carry1(a.aggp + gk, epoch, P);
+        if (__all_sync(0xffffffffu, agg)) {
+            k++;
+            continue;
+        }
+        __nanosleep(20);
     }
-    cp_wait_all();
+    for (int kk = k - 1; kk >= 1; kk--) {
+        const int64_t gk = gseg + (int64_t)dir * kk;
+        float4 xl = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        float P = 0.0f;
+        if (act) try_carry4(a.agg + gk * lw + 4 * jq, epoch, xl);
+        try_carry1(a.aggp + gk, epoch, P);
+        X.x = xl.x + P * X.x;
+        X.y = xl.y + P * X.y;
+        X.z = xl.z + P * X.z;
+        X.w = xl.w + P * X.w;
+    }
+    return X;
+}
+
+// warp-uniform index i in [0, 64]: value of node a + i held in lanes of lo/hi
+// (i < 64), or `past` for i == 64
+__device__ __forceinline__ float seg_pick(float lo, float hi, float past, int i) {
+    const float l = __shfl_sync(0xffffffffu, lo, i & 31);
+    const float h = __shfl_sync(0xffffffffu, hi, i & 31);
+    return i < 32 ? l : (i < 64 ? h : past);
+}
+
+constexpr int kSegWarps = 4;  // segment warps per CTA
+
+// A segment's rows for this warp's column group: with one group (rows of at
+// most 128 floats) the segment is one contiguous span of the row layout and
+// arrives with a single bulk copy (row stride = the path's own mq in shared
+// memory); otherwise each row's 32-column slice arrives by its own copy (row
+// stride 32).  Returns the shared-memory row stride in float4.
+__device__ __forceinline__ int seg_stage(const AggArgs& a, const SegCtx& c, int g, float4* buf,
+                                         unsigned long long* bar, int lane) {
+    const int mq = c.mp >> 2;
+    const int cnt = c.b - c.a;
+    const float* src0 = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp;
+    if (lane == 0) mbar_init(bar, 1);
     __syncwarp();
-    // local pass with X_b = 0: x_loc(a) and P = prod_{t=a+1..b} s_t
-    float x = 0.0f, P = 1.0f;
+    if (a.qgroups == 1) {
+        if (lane == 0) {
+            const unsigned bytes = (unsigned)cnt * (unsigned)c.mp * 4u;
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(buf, src0, bytes, bar);
+        }
+        mbar_wait(bar, 0);
+        return mq;
+    }
+    const int wq = min(32, mq - 32 * g);
+    if (lane == 0) mbar_expect_tx(bar, (unsigned)cnt * (unsigned)wq * 16u);
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32)
+        bulk_g2s(buf + i * 32, src0 + (int64_t)i * c.mp + 128 * g, (unsigned)wq * 16u, bar);
+    mbar_wait(bar, 0);
+    return 32;
+}
+
+// Up pass over one segment (tail -> head), one warp per (segment, 32 float4
+// columns).  Segments are taken by ticket in reverse table order, so a
+// path's tail segment comes first; the carry is X_a = x_loc(a) + P * X_b with
+// P = prod s_{a+1..b}.
+__global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0, int64_t ng, int* ctr,
+                                                           int sq) {
+    extern __shared__ float4 sbuf[];
+    __shared__ unsigned long long bars[kSegWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = (int)blockIdx.y;
+    const int t = warp_ticket(ctr + g);
+    if (t >= ng) return;
+    const SegCtx c = seg_ctx(a, g0 + ng - 1 - t);
+    const int mq = c.mp >> 2;
+    if (g * 32 >= mq) return;
+    const int jq = g * 32 + lane;
+    const bool act = jq < mq;
+    const int cnt = c.b - c.a;
+    const bool has_next = c.b < c.start + c.len;
+    float4* buf = sbuf + warp * kSeg * sq;
+    const int rs = seg_stage(a, c, g, buf, &bars[warp], lane);
+    // s of node a + i (0 past the path's tail), i in [0, cnt]
+    const float s_lo = (lane < cnt || (lane == cnt && has_next)) ? fabsf(a.lsimf[c.a + lane]) : 0.0f;
+    const float s_hi = (32 + lane < cnt || (32 + lane == cnt && has_next)) ? fabsf(a.lsimf[c.a + 32 + lane]) : 0.0f;
+    const float s_past = (cnt == kSeg && has_next) ? fabsf(a.lsimf[c.b]) : 0.0f;
+    const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    float4 x = z;
+    float P = 1.0f;
+#pragma unroll 4
     for (int i = cnt - 1; i >= 0; i--) {
-        float sn = ssim[warp][i + 1];  // s of the node after i (0 past the tail)
-        x = buf[warp][i][lane] + sn * x;
+        const float sn = seg_pick(s_lo, s_hi, s_past, i + 1);
+        const float4 v = act ? buf[i * rs + lane] : z;
+        x.x = v.x + sn * x.x;
+        x.y = v.y + sn * x.y;
+        x.z = v.z + sn * x.z;
+        x.w = v.w + sn * x.w;
         P *= sn;
     }
-    float Xb = 0.0f;
-    if (has_next && act) Xb = get_carry(a.carry + (c.gseg + 1) * a.max_m + j, a.epoch_up);
-    if (act && c.s > 0) put_carry(a.carry + c.gseg * a.max_m + j, a.epoch_up, x + P * Xb);
+    if (c.s > 0) {  // the head side will need this segment's map
+        if (act) put_carry4(a.agg + c.gseg * a.max_mp + 4 * jq, a.epoch_up, x);
+        if (lane == 0) put_carry(a.aggp + c.gseg, a.epoch_up, P);
+    }
+    float4 Xb = z;
+    if (has_next) Xb = seg_lookback(a, c.gseg, +1, c.nseg - 1 - c.s, a.epoch_up, jq, act, z);
+    if (act && c.s > 0) {
+        float4 o;
+        o.x = x.x + P * Xb.x;
+        o.y = x.y + P * Xb.y;
+        o.z = x.z + P * Xb.z;
+        o.w = x.w + P * Xb.w;
+        put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_up, o);
+    }
     // final pass: exact recurrence from the true X_b
+    float4* rows = reinterpret_cast<float4*>(a.aup + c.row0) + (int64_t)(c.a - c.start) * mq + jq;
     x = Xb;
-    float* out = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp + j;
+#pragma unroll 4
     for (int i = cnt - 1; i >= 0; i--) {
-        x = buf[warp][i][lane] + ssim[warp][i + 1] * x;
-        if (act) out[(int64_t)i * c.mp] = x;
+        const float sn = seg_pick(s_lo, s_hi, s_past, i + 1);
+        const float4 v = act ? buf[i * rs + lane] : z;
+        x.x = v.x + sn * x.x;
+        x.y = v.y + sn * x.y;
+        x.z = v.z + sn * x.z;
+        x.w = v.w + sn * x.w;
+        if (act) rows[(int64_t)i * mq] = x;
     }
-}
-
-// warp transpose butterfly: lane l ends with the minimum key of node l
-__device__ __forceinline__ unsigned long long warp_min_per_node(unsigned long long (&key)[32],
-                                                                int lane) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        bool up_half = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; i++) {
-            unsigned long long send = up_half ? key[i] : key[i + o];
-            unsigned long long keep = up_half ? key[i + o] : key[i];
-            unsigned long long recv = __shfl_xor_sync(0xffffffffu, send, o);
-            key[i] = recv < keep ? recv : keep;
-        }
-    }
-    return key[0];
-}
-
-// First argmin of (cost, d) over the lanes of one item: `width` lanes
-// (power of two, aligned) or the full warp.  32-bit shuffle min on the
-// order-preserving cost, then the lowest lane holding it (lanes are in
-// ascending disparity order) supplies d.  Every lane gets the packed key.
-__device__ __forceinline__ unsigned long long group_argmin(bool act, float y, int d, int width,
-                                                           int lane) {
-    uint32_t o = act ? ord_f32(y) : 0xffffffffu;
-    uint32_t mn = o;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        uint32_t t = __shfl_xor_sync(0xffffffffu, mn, off);
-        if (off < width) mn = min(mn, t);
-    }
-    unsigned gmask = width == 32 ? 0xffffffffu : ((1u << width) - 1u) << (lane & ~(width - 1));
-    unsigned eq = __ballot_sync(0xffffffffu, o == mn) & gmask;
-    int dmin = __shfl_sync(0xffffffffu, d, __ffs(eq) - 1);
-    return ((unsigned long long)mn << 32) | (uint32_t)dmin;
-}
-
-__device__ __forceinline__ void store_key(const AggArgs& a, int32_t node, unsigned long long k) {
-    if (!a.keys) return;
-    if (a.atomic_keys)
-        atomicMin(&a.keys[node], k);
-    else
-        a.keys[node] = k;
 }
 
 // Down pass over one segment (head -> tail).  The carry is
 // Y_end = y_loc(b-1) + Q * Y_in with Q = prod_{t=a..b-1} s_t; the head of a
 // root path uses s = 0 so that A(root) = A_up(root).  The first argmin of
-// each node over this warp's 32 lanes is folded into the node's key with a
-// 64-bit min (several lane groups per node) or stored (one group); A is
-// written back only where a light child will read it.
-__global__ void __launch_bounds__(128) k_seg_down(AggArgs a, int64_t g0, int64_t ng, int* ctr) {
-    __shared__ float buf[4][kSeg][32];
-    __shared__ float ssim[4][kSeg];
-    __shared__ int32_t snode[4][kSeg];
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int g = (int)blockIdx.y;
-    int t = warp_ticket(ctr + g);
+// each node over this warp's columns is folded into the node's key (64-bit
+// min when several warps share a row, a store otherwise); A is written back
+// only where a light child will read it.
+__global__ void __launch_bounds__(32 * kSegWarps) k_seg_down(AggArgs a, int64_t g0, int64_t ng, int* ctr,
+                                                             int sq) {
+    extern __shared__ float4 sbuf[];
+    __shared__ unsigned long long bars[kSegWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = (int)blockIdx.y;
+    const int t = warp_ticket(ctr + g);
     if (t >= ng) return;
-    SegCtx c = seg_ctx(a, g0 + t);
-    if (g * 32 >= c.m) return;
-    int j = g * 32 + lane;
-    bool act = j < c.m;
-    int cnt = c.b - c.a;
-    float* rows = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp + j;
-    for (int i = 0; i < cnt; i++) cp_async4(&buf[warp][i][lane], rows + (int64_t)i * c.mp, act);
-    cp_commit();
-    unsigned long long lmask = 0;  // bit i: node a+i has light children
-    for (int i0 = 0; i0 < kSeg; i0 += 32) {
-        int i = i0 + lane;
-        float f = i < cnt ? a.lsimf[c.a + i] : 0.0f;
-        if (i < cnt) snode[warp][i] = a.lmeta[c.a + i].x;
+    const SegCtx c = seg_ctx(a, g0 + t);
+    const int mq = c.mp >> 2;
+    if (g * 32 >= mq) return;
+    const int jq = g * 32 + lane;
+    const bool act = jq < mq;
+    const int cnt = c.b - c.a;
+    float4* buf = sbuf + warp * kSeg * sq;
+    const int rs = seg_stage(a, c, g, buf, &bars[warp], lane);
+    // s (0 at a root head), light-children flag and node id of node a + i
+    float s_lo = 0.0f, s_hi = 0.0f;
+    int n_lo = 0, n_hi = 0;
+    unsigned long long lmask = 0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int i = 32 * h + lane;
+        const float f = i < cnt ? a.lsimf[c.a + i] : 0.0f;
         float sv = fabsf(f);
-        if (c.a + i == c.start && c.prow < 0) sv = 0.0f;  // root: A = A_up
-        if (i < cnt) ssim[warp][i] = sv;
-        unsigned b = __ballot_sync(0xffffffffu, i < cnt && (__float_as_uint(f) >> 31));
-        lmask |= (unsigned long long)b << i0;
+        if (c.a + i == c.start && c.prow < 0) sv = 0.0f;
+        const int nd = i < cnt ? a.lmeta[c.a + i].x : 0;
+        if (h == 0) {
+            s_lo = sv;
+            n_lo = nd;
+        } else {
+            s_hi = sv;
+            n_hi = nd;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, i < cnt && (__float_as_uint(f) >> 31));
+        lmask |= (unsigned long long)b << (32 * h);
     }
     if (a.store_all) lmask = ~0ull;
-    const int d = act ? lane_disp(a, c.doff, j) : 0;
-    cp_wait_all();
-    __syncwarp();
-    // local pass with Y_in = 0: y_loc(b-1) and Q = prod_{t=a..b-1} s_t
-    float yl = 0.0f, Q = 1.0f;
+    const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    // local pass with Y_in = 0
+    float4 yl = z;
+    float Q = 1.0f;
+#pragma unroll 4
     for (int i = 0; i < cnt; i++) {
-        float sv = ssim[warp][i];
-        yl = sv * yl + (1.0f - sv * sv) * buf[warp][i][lane];
+        const float sv = seg_pick(s_lo, s_hi, 0.0f, i);
+        const float w = 1.0f - sv * sv;
+        const float4 v = act ? buf[i * rs + lane] : z;
+        yl.x = sv * yl.x + w * v.x;
+        yl.y = sv * yl.y + w * v.y;
+        yl.z = sv * yl.z + w * v.z;
+        yl.w = sv * yl.w + w * v.w;
         Q *= sv;
     }
-    float Yin = 0.0f;
-    if (c.s == 0) {
-        if (c.prow >= 0 && act) Yin = a.aup[c.prow + j];  // A(parent), stored in place
-    } else if (act) {
-        Yin = get_carry(a.carry + (c.gseg - 1) * a.max_m + j, a.epoch_down);
+    if (c.s + 1 < c.nseg) {  // the tail side will need this segment's map
+        if (act) put_carry4(a.agg + c.gseg * a.max_mp + 4 * jq, a.epoch_down, yl);
+        if (lane == 0) put_carry(a.aggp + c.gseg, a.epoch_down, Q);
     }
-    // publish the tail-end carry before the final pass
-    if (act && c.s + 1 < c.nseg) put_carry(a.carry + c.gseg * a.max_m + j, a.epoch_down, yl + Q * Yin);
-    float y = Yin;
+    float4 Ypar = z;  // A(parent) enters at the path's head (0 at a root)
+    if (c.prow >= 0 && act) Ypar = reinterpret_cast<const float4*>(a.aup + c.prow)[jq];
+    const float4 Yin = c.s == 0 ? Ypar : seg_lookback(a, c.gseg, -1, c.s, a.epoch_down, jq, act, Ypar);
+    if (act && c.s + 1 < c.nseg) {
+        float4 o;
+        o.x = yl.x + Q * Yin.x;
+        o.y = yl.y + Q * Yin.y;
+        o.z = yl.z + Q * Yin.z;
+        o.w = yl.w + Q * Yin.w;
+        put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_down, o);
+    }
+    float4* rows = reinterpret_cast<float4*>(a.aup + c.row0) + (int64_t)(c.a - c.start) * mq + jq;
+    float4 y = Yin;
+    const int j0 = 4 * jq;
+#pragma unroll 4
     for (int i = 0; i < cnt; i++) {
-        float sv = ssim[warp][i];
-        y = sv * y + (1.0f - sv * sv) * buf[warp][i][lane];
-        if (act && ((lmask >> i) & 1ull)) rows[(int64_t)i * c.mp] = y;
-        unsigned long long key = group_argmin(act, y, d, 32, lane);
+        const float sv = seg_pick(s_lo, s_hi, 0.0f, i);
+        const float w = 1.0f - sv * sv;
+        const float4 v = act ? buf[i * rs + lane] : z;
+        y.x = sv * y.x + w * v.x;
+        y.y = sv * y.y + w * v.y;
+        y.z = sv * y.z + w * v.z;
+        y.w = sv * y.w + w * v.w;
+        if (act && ((lmask >> i) & 1ull)) rows[(int64_t)i * mq] = y;
+        // first minimum over this lane's four columns (padding never wins)
+        float best = y.x;
+        int bj = j0;
+        if (y.y < best) { best = y.y; bj = j0 + 1; }
+        if (y.z < best) { best = y.z; bj = j0 + 2; }
+        if (y.w < best) { best = y.w; bj = j0 + 3; }
+        const uint32_t ob = act ? ord_f32(best) : 0xffffffffu;
+        const uint32_t mn = __reduce_min_sync(0xffffffffu, ob);
+        const uint32_t jm = __reduce_min_sync(0xffffffffu, ob == mn ? (uint32_t)bj : 0xffffffffu);
+        const int node = __shfl_sync(0xffffffffu, i < 32 ? n_lo : n_hi, i & 31);
         if (lane == 0 && a.keys) {
+            const unsigned long long key = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, c.doff, (int)jm);
             if (a.atomic_keys)
-                atomicMin(&a.keys[snode[warp][i]], key);
+                atomicMin(&a.keys[node], key);
             else
-                a.keys[snode[warp][i]] = key;
+                a.keys[node] = key;
         }
     }
 }
@@ -665,31 +856,6 @@ __device__ __forceinline__ void cp_async4u(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_wait_one() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-// 1-D TMA (bulk async copy) global -> shared, completing on an mbarrier
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 // 16-byte cp.async of a padded row of `cnt` floats (rows start 16-byte
 // aligned), lanes of one warp striding the row
 __device__ __forceinline__ void row_async(float* dst, const float* src, int cnt, int lane) {
@@ -774,7 +940,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_up_chunk(AggArgs a, const Chu
     for (int t = threadIdx.x; t < items; t += blockDim.x) {
         int pi, jq;
         if (mqu > 0) {
-            pi = (int)__umulhi((unsigned)t, d.inv);
+            pi = mqu == 1 ? t : (int)__umulhi((unsigned)t, d.inv);
             jq = t - pi * mqu;
         } else {
             pi = t >> a.qsub_shift;
@@ -846,7 +1012,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
     for (int t = threadIdx.x; t < items; t += blockDim.x) {
         int pi, jq;
         if (mqu > 0) {
-            pi = (int)__umulhi((unsigned)t, d.inv);
+            pi = mqu == 1 ? t : (int)__umulhi((unsigned)t, d.inv);
             jq = t - pi * mqu;
         } else {
             pi = t >> a.qsub_shift;
@@ -1031,6 +1197,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.volume = volume;
     a.groups = (f->max_m + 31) / 32;
     a.max_m = f->max_m;
+    a.max_mp = (f->max_m + 3) & ~3;
+    a.qgroups = (a.max_mp / 4 + 31) / 32;
     a.sub = f->max_m <= 16 ? std::max(4, pow2_at_least(f->max_m)) : 32;  // >= one padded row
     a.sub_shift = 0;
     while ((1 << a.sub_shift) < a.sub) a.sub_shift++;
@@ -1046,7 +1214,12 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_TRY(aup.alloc(f->total_rows + 32, st));
     a.aup = aup.get();
     const int64_t nseg = f->n_segs;
-    HDP_TRY(carry.alloc(nseg * a.max_m + 1, st));
+    HDP_TRY(carry.alloc(nseg * a.max_mp + 1, st));
+    DevBuf<unsigned long long> aggb, aggpb;
+    HDP_TRY(aggb.alloc(nseg * a.max_mp + 1, st));
+    HDP_TRY(aggpb.alloc(nseg + 1, st));
+    a.agg = aggb.get();
+    a.aggp = aggpb.get();
     HDP_TRY(tickets.alloc(2 * f->n_phases * a.groups + 1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(tickets.get(), 0,
                                    sizeof(int) * (2 * f->n_phases * a.groups + 1), st));
@@ -1066,7 +1239,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     }
     a.keys = kp;
     // long-path nodes get one key contribution per 32-lane group
-    a.atomic_keys = (f->n_segs > 0 && a.groups > 1) ? 1 : 0;
+    a.atomic_keys = (f->n_segs > 0 && a.qgroups > 1) ? 1 : 0;
     if (a.atomic_keys) HDP_CHECK_CUDA(cudaMemsetAsync(kp, 0xff, sizeof(unsigned long long) * f->n, st));
     a.store_all = volume != nullptr;
     if (!cost_rows && (f->geom_w != a.w || f->geom_np != a.npix)) {
@@ -1075,7 +1248,15 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         f->geom_np = a.npix;
     }
 
-    AggArgs lg = a;  // segment kernels: one warp per (segment, 32 lanes)
+    AggArgs lg = a;  // segment kernels: one warp per (segment, 32 float4 columns)
+    // shared row stride (float4) of a staged segment: the widest row when one
+    // column group covers it, else 32
+    const int seg_sq = a.qgroups == 1 ? a.max_mp / 4 : 32;
+    const size_t seg_smem = (size_t)kSegWarps * kSeg * seg_sq * sizeof(float4);
+    if (seg_smem > 48 * 1024) {
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_seg_up, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)seg_smem));
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_seg_down, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)seg_smem));
+    }
     lg.sub = 32;
     lg.pinfo = f->long_info.get();
     lg.prows = f->long_rows.get();
@@ -1091,7 +1272,14 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         size_t smem = (size_t)(kETile + f->max_d) * sizeof(float4);
         int use = smem <= 48 * 1024;
         dim3 g((unsigned)rows, (unsigned)((a.w + kETile - 1) / kETile));
-        k_ecost_pix<<<g, 256, use ? smem : 0, st>>>(a, f->lpos.get(), f->max_d, use); note_launch();
+        if (a.range_x0 >= 0) {
+            if (use) k_ecost_pix<true, true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d);
+            else k_ecost_pix<true, false><<<g, 256, 0, st>>>(a, f->lpos.get(), f->max_d);
+        } else {
+            if (use) k_ecost_pix<false, true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d);
+            else k_ecost_pix<false, false><<<g, 256, 0, st>>>(a, f->lpos.get(), f->max_d);
+        }
+        note_launch();
     }
     const bool chunks = f->chunks_ok != 0;
     const size_t csmem = (size_t)((f->chunk_words + 3) & ~3ll) * sizeof(float);
@@ -1109,8 +1297,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         }
         int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
         if (ng > 0) {
-            k_seg_up<<<dim3(grid_for(ng * 32, 128), lg.groups), 128, 0, st>>>(
-                lg, g0, ng, a.tickets + (2 * r) * a.groups); note_launch();
+            k_seg_up<<<dim3(grid_for(ng * 32, 32 * kSegWarps), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
+                lg, g0, ng, a.tickets + (2 * r) * a.groups, seg_sq); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
@@ -1124,8 +1312,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     for (int64_t r = 0; r < f->n_phases; r++) {
         int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
         if (ng > 0) {
-            k_seg_down<<<dim3(grid_for(ng * 32, 128), lg.groups), 128, 0, st>>>(
-                lg, g0, ng, a.tickets + (2 * r + 1) * a.groups); note_launch();
+            k_seg_down<<<dim3(grid_for(ng * 32, 32 * kSegWarps), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
+                lg, g0, ng, a.tickets + (2 * r + 1) * a.groups, seg_sq); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;

@@ -1027,7 +1027,7 @@ __global__ void k_chunk_desc(int64_t nc, const int32_t* __restrict__ chunk_first
         for (int p = p0 + 1; p < p1 && mq > 0; p++)
             if (((sinfo[p].z + 3) >> 2) != mq) mq = 0;
         d.mqu = mq;
-        d.inv = mq > 0 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
+        d.inv = mq > 1 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
         atomicMax(max_words, (unsigned long long)(W[p1] - W[p0]));
     }
     desc[c] = d;
@@ -1098,6 +1098,10 @@ static int build_chunks(hdp_forest* f) {
     // rows of up to 32 float4 lanes: one lane group spans a row; wider rows
     // take the per-path kernels (lane groups across CTAs)
     f->chunks_ok = f->chunk_words <= kChunkMaxWords && f->max_m <= 128;
+    {
+        const char* e = getenv("HDP_NO_CHUNKS");  // A/B switch for diagnostics
+        if (e && e[0] == '1') f->chunks_ok = 0;
+    }
     return HDP_OK;
 }
 

@@ -11,7 +11,7 @@
 constexpr int kShortPath = 8;
 // Long paths are cut into segments of kSeg nodes, one warp each, chained by
 // decoupled look-back in the aggregation kernels.
-constexpr int kSeg = 64;
+constexpr int kSeg = 32;
 
 namespace hdp {
 // Short-path chunks: the short paths of a phase are cut into runs whose rows,
@@ -29,7 +29,7 @@ struct alignas(16) ChunkDesc {
     int n4;            // float4 words of staged rows
     int naux_up, naux_dn;
     int mqu;           // float4 columns of every row when all paths share m, else 0
-    unsigned inv;      // ceil(2^32 / mqu): t / mqu == umulhi(t, inv) for small t
+    unsigned inv;      // ceil(2^32 / mqu) for mqu > 1: t / mqu == umulhi(t, inv) for small t
     int pad0;
     long long a0;      // first staged row float (16-byte aligned)
     long long lcr0;    // lc_rowoff[L0]
