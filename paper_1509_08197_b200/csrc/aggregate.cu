@@ -198,6 +198,49 @@ __device__ __forceinline__ float pix_cost(const AggArgs& a, float wc, const floa
     return wc * fminf(a.tc, color) + a.alpha * fminf(a.tg, fabsf(L.w - R.w));
 }
 
+// Range lanes (lane j is disparity range_x0 + j, every row the same width):
+// one CTA per (image row, kETile columns); the tile's row offsets are looked
+// up once into shared memory, then threads take flat (node, float4) items,
+// four disparities and one 16-byte store each.
+template <bool SMEM>
+__global__ void __launch_bounds__(256) k_ecost_range(AggArgs a, const int32_t* __restrict__ lpos, int d_hi,
+                                                     int m, unsigned inv) {
+    extern __shared__ float4 win[];
+    __shared__ long long srow[kETile];
+    const int64_t base = (int64_t)blockIdx.x * a.w;  // node id of column 0 of this image row
+    const int c0 = (int)blockIdx.y * kETile;
+    const int lo = max(0, c0 - d_hi), hi = min(a.w, c0 + kETile);
+    const int nt = hi - c0;  // columns in this tile
+    if (SMEM)
+        for (int i = threadIdx.x; i < hi - lo; i += blockDim.x) win[i] = __ldg(a.pr + base + lo + i);
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) srow[i] = __ldg(a.rowoff + __ldg(lpos + base + c0 + i));
+    __syncthreads();
+    const float4* rrow = a.pr + base;  // right-image row (global fallback)
+    const int mq = (m + 3) >> 2;
+    const int items = nt * mq;
+    const float wc = 1.0f - a.alpha;
+    for (int t = threadIdx.x; t < items; t += blockDim.x) {
+        const int q = mq == 1 ? t : (int)__umulhi((unsigned)t, inv);
+        const int jq = t - q * mq;
+        const int col = c0 + q;
+        const float4 L = __ldg(a.pl + base + col);
+        const int x = col - (a.range_x0 + 4 * jq);  // right-image column of lane 4 jq
+        float e[4];
+        if (x - 3 >= 0 && 4 * jq + 3 < m) {
+#pragma unroll
+            for (int u = 0; u < 4; u++) e[u] = pix_cost(a, wc, L, SMEM ? win[x - u - lo] : __ldg(rrow + x - u));
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (4 * jq + u >= m) e[u] = kPadCost;
+                else if (x - u < 0) e[u] = a.border;
+                else e[u] = pix_cost(a, wc, L, SMEM ? win[x - u - lo] : __ldg(rrow + x - u));
+            }
+        }
+        reinterpret_cast<float4*>(a.aup + srow[q])[jq] = make_float4(e[0], e[1], e[2], e[3]);
+    }
+}
+
 // RANGE: lane j is disparity range_x0 + j (dense / slab lanes); otherwise the
 // tree's lane list.  SMEM: the right-image window fits in shared memory.
 template <bool RANGE, bool SMEM>
@@ -1273,8 +1316,10 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         int use = smem <= 48 * 1024;
         dim3 g((unsigned)rows, (unsigned)((a.w + kETile - 1) / kETile));
         if (a.range_x0 >= 0) {
-            if (use) k_ecost_pix<true, true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d);
-            else k_ecost_pix<true, false><<<g, 256, 0, st>>>(a, f->lpos.get(), f->max_d);
+            const int m = f->max_m, mq = (m + 3) >> 2;
+            const unsigned inv = mq > 1 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
+            if (use) k_ecost_range<true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d, m, inv);
+            else k_ecost_range<false><<<g, 256, 0, st>>>(a, f->lpos.get(), f->max_d, m, inv);
         } else {
             if (use) k_ecost_pix<false, true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d);
             else k_ecost_pix<false, false><<<g, 256, 0, st>>>(a, f->lpos.get(), f->max_d);

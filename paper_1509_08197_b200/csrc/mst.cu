@@ -21,7 +21,13 @@ __global__ void k_mst_init(int64_t n, int32_t* comp) {
     if (v < n) comp[v] = (int32_t)v;
 }
 
-__global__ void k_mst_reset(int64_t n, unsigned long long* best, int32_t* win) {
+// Rounds are launched in batches without a host check in between; every
+// kernel of round r first looks at the previous round's hook flag and does
+// nothing once a round has made no hooks (the forest is final).
+__device__ __forceinline__ bool converged(const int* prev) { return prev && *prev == 0; }
+
+__global__ void k_mst_reset(int64_t n, unsigned long long* best, int32_t* win, const int* prev) {
+    if (converged(prev)) return;
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v < n) {
         best[v] = ~0ull;
@@ -31,7 +37,8 @@ __global__ void k_mst_reset(int64_t n, unsigned long long* best, int32_t* win) {
 
 __global__ void k_mst_offer(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                             const uint64_t* __restrict__ key, const int32_t* __restrict__ comp,
-                            uint8_t* __restrict__ alive, unsigned long long* best) {
+                            uint8_t* __restrict__ alive, unsigned long long* best, const int* prev) {
+    if (converged(prev)) return;
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m || !alive[e]) return;
     int32_t cu = comp[eu[e]], cv = comp[ev[e]];
@@ -47,7 +54,8 @@ __global__ void k_mst_offer(int64_t m, const int32_t* __restrict__ eu, const int
 __global__ void k_mst_win(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                           const uint64_t* __restrict__ key, const int32_t* __restrict__ comp,
                           const uint8_t* __restrict__ alive, const unsigned long long* __restrict__ best,
-                          int32_t* win) {
+                          int32_t* win, const int* prev) {
+    if (converged(prev)) return;
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m || !alive[e]) return;
     int32_t cu = comp[eu[e]], cv = comp[ev[e]];
@@ -59,27 +67,33 @@ __global__ void k_mst_win(int64_t m, const int32_t* __restrict__ eu, const int32
 __global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                            const int32_t* __restrict__ comp, const int32_t* __restrict__ win,
                            int32_t* __restrict__ link, uint8_t* __restrict__ in_tree,
-                           int* __restrict__ hooks) {
+                           int* __restrict__ hooks, const int* prev) {
+    if (converged(prev)) return;
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    if (comp[v] != v) return;  // not a representative
-    int32_t e = win[v];
-    if (e < 0) {
-        link[v] = (int32_t)v;
-        return;
+    bool hooked = false;
+    if (v < n && comp[v] == v) {  // representatives only
+        int32_t e = win[v];
+        if (e < 0) {
+            link[v] = (int32_t)v;
+        } else {
+            int32_t a = comp[eu[e]], b = comp[ev[e]];
+            int32_t other = (a == v) ? b : a;
+            in_tree[e] = 1;
+            if (win[other] == e && v < other) {
+                link[v] = (int32_t)v;  // mutual minimum: the lower id stays the root
+            } else {
+                link[v] = other;
+                hooked = true;
+            }
+        }
     }
-    int32_t a = comp[eu[e]], b = comp[ev[e]];
-    int32_t other = (a == v) ? b : a;
-    in_tree[e] = 1;
-    if (win[other] == e && v < other) {
-        link[v] = (int32_t)v;  // mutual minimum: the lower id stays the root
-    } else {
-        link[v] = other;
-        atomicAdd(hooks, 1);
-    }
+    // "another round is needed": one flag write per warp, and only while unset
+    if (__ballot_sync(0xffffffffu, hooked) && (threadIdx.x & 31) == 0 && *(volatile int*)hooks == 0) *hooks = 1;
 }
 
-__global__ void k_mst_relabel(int64_t n, int32_t* __restrict__ comp, const int32_t* __restrict__ link) {
+__global__ void k_mst_relabel(int64_t n, int32_t* __restrict__ comp, const int32_t* __restrict__ link,
+                              const int* prev) {
+    if (converged(prev)) return;
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     int32_t r = comp[v];
@@ -95,13 +109,13 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
     DevBuf<int32_t> win, link;
     DevBuf<uint8_t> alive;
     DevBuf<int> hooks;
+    constexpr int kMaxRounds = 64, kBatch = 4;
     HDP_TRY(best.alloc(n, st));
     HDP_TRY(win.alloc(n, st));
     HDP_TRY(link.alloc(n, st));
     HDP_TRY(alive.alloc(m > 0 ? m : 1, st));
-    HDP_TRY(hooks.alloc(1, st));
-    int h_hooks_v = 0;
-    int* h_hooks = &h_hooks_v;  // 4 bytes: a pageable copy costs the same sync
+    HDP_TRY(hooks.alloc(kMaxRounds + kBatch, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(hooks.get(), 0, sizeof(int) * (kMaxRounds + kBatch), st));
     k_mst_init<<<grid_for(n, 256), 256, 0, st>>>(n, comp); note_launch();
     if (m > 0) {
         HDP_CHECK_CUDA(cudaMemsetAsync(alive.get(), 1, m, st));
@@ -109,21 +123,32 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
     }
     int rounds = 0;
     Tracer tr(st);
+    int hb[kBatch];
     while (m > 0) {
-        HDP_CHECK_CUDA(cudaMemsetAsync(hooks.get(), 0, sizeof(int), st));
-        k_mst_reset<<<grid_for(n, 256), 256, 0, st>>>(n, best.get(), win.get()); note_launch();
-        k_mst_offer<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get()); note_launch();
-        k_mst_win<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get(),
-                                                   win.get()); note_launch();
-        k_mst_hook<<<grid_for(n, 256), 256, 0, st>>>(n, eu, ev, comp, win.get(), link.get(),
-                                                    in_tree, hooks.get()); note_launch();
-        k_mst_relabel<<<grid_for(n, 256), 256, 0, st>>>(n, comp, link.get()); note_launch();
+        // kBatch rounds per host check; hooks[r] = 1 iff round r hooked anything
+        const int r0 = rounds;
+        for (int r = r0; r < r0 + kBatch; r++) {
+            const int* prev = r > 0 ? hooks.get() + r - 1 : nullptr;
+            int* hk = hooks.get() + r;
+            k_mst_reset<<<grid_for(n, 256), 256, 0, st>>>(n, best.get(), win.get(), prev); note_launch();
+            k_mst_offer<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get(), prev); note_launch();
+            k_mst_win<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get(),
+                                                       win.get(), prev); note_launch();
+            k_mst_hook<<<grid_for(n, 256), 256, 0, st>>>(n, eu, ev, comp, win.get(), link.get(),
+                                                        in_tree, hk, prev); note_launch();
+            k_mst_relabel<<<grid_for(n, 256), 256, 0, st>>>(n, comp, link.get(), prev); note_launch();
+        }
         HDP_CHECK_LAUNCH();
-        HDP_CHECK_CUDA(cudaMemcpyAsync(h_hooks, hooks.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(hb, hooks.get() + r0, sizeof(hb), cudaMemcpyDeviceToHost, st));
         HDP_CHECK_CUDA(cudaStreamSynchronize(st));
-        rounds++;
-        if (*h_hooks == 0) break;
-        if (rounds > 64) {
+        int k = 0;
+        while (k < kBatch && hb[k] != 0) k++;
+        if (k < kBatch) {  // round r0 + k made no hooks: it was the last
+            rounds = r0 + k + 1;
+            break;
+        }
+        rounds = r0 + kBatch;
+        if (rounds >= kMaxRounds) {
             set_error("boruvka did not converge (duplicate keys?)");
             return HDP_ERR_INTERNAL;
         }
