@@ -1184,6 +1184,42 @@ __global__ void k_keys_finish(int64_t n, const unsigned long long* __restrict__ 
     if (min_cost) min_cost[i] = unord_f32((uint32_t)(k >> 32));
 }
 
+// Per host thread and device: a second stream plus fork/join events.  Within
+// a phase the short-path chunks and the long-path kernels touch disjoint rows,
+// so they run concurrently (each alone leaves most of the GPU idle in the
+// small phases and in the look-back chains).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static int side_stream(SideStream** out) {
+    static thread_local SideStream per_dev[64];
+    int dev = 0;
+    HDP_CHECK_CUDA(cudaGetDevice(&dev));
+    HDP_REQUIRE(dev >= 0 && dev < 64, HDP_ERR_CONFIG, "device ordinal %d out of range", dev);
+    SideStream& ss = per_dev[dev];
+    if (!ss.s) {
+        HDP_CHECK_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+        HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+        HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+    }
+    *out = &ss;
+    return HDP_OK;
+}
+
+static int fork_side(const SideStream* ss, cudaStream_t st) {
+    HDP_CHECK_CUDA(cudaEventRecord(ss->fork, st));
+    HDP_CHECK_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+    return HDP_OK;
+}
+
+static int join_side(const SideStream* ss, cudaStream_t st) {
+    HDP_CHECK_CUDA(cudaEventRecord(ss->join, ss->s));
+    HDP_CHECK_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+    return HDP_OK;
+}
+
 static int pow2_at_least(int x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -1334,20 +1370,29 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         HDP_CHECK_CUDA(cudaFuncSetAttribute(k_up_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
         HDP_CHECK_CUDA(cudaFuncSetAttribute(k_down_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
     }
+    SideStream* ss = nullptr;
+    HDP_TRY(side_stream(&ss));
     for (int64_t r = f->n_phases - 1; r >= 0; r--) {
         // light parents on short paths are handled inside k_up_chunk
         int64_t p0 = chunks ? f->lp_mid[r] : f->lp_off[r], np = f->lp_off[r + 1] - p0;
+        int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
+        int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
+        const bool side = chunks && nc > 0 && (np > 0 || ng > 0);
+        if (side) {
+            HDP_TRY(fork_side(ss, st));
+            k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0); note_launch();
+        }
         if (np > 0) {
             k_light<<<packed_grid(a, (np + 3) / 4, 1, 256), 256, 0, st>>>(a, p0, np); note_launch();
         }
-        int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
         if (ng > 0) {
             k_seg_up<<<dim3(grid_for(ng * 32, 32 * kSegWarps), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
                 lg, g0, ng, a.tickets + (2 * r) * a.groups, seg_sq); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
-        int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
-        if (chunks && nc > 0) {
+        if (side) {
+            HDP_TRY(join_side(ss, st));
+        } else if (chunks && nc > 0) {
             k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
         } else if (!chunks && ns > 0) {
             k_scan_up_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
@@ -1356,13 +1401,20 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_CHECK_LAUNCH();
     for (int64_t r = 0; r < f->n_phases; r++) {
         int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
+        int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
+        const bool side = chunks && nc > 0 && ng > 0;
+        if (side) {
+            HDP_TRY(fork_side(ss, st));
+            k_down_chunk<<<(unsigned)nc, kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0); note_launch();
+        }
         if (ng > 0) {
             k_seg_down<<<dim3(grid_for(ng * 32, 32 * kSegWarps), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
                 lg, g0, ng, a.tickets + (2 * r + 1) * a.groups, seg_sq); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
-        int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
-        if (chunks && nc > 0) {
+        if (side) {
+            HDP_TRY(join_side(ss, st));
+        } else if (chunks && nc > 0) {
             k_down_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
         } else if (!chunks && ns > 0) {
             k_down_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
