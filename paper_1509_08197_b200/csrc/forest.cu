@@ -30,9 +30,28 @@ namespace hdp {
 int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, const uint64_t* key,
                 uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st);
 
-__global__ void k_flag_edges(int64_t m, const uint8_t* __restrict__ in_tree, int32_t* flags) {
+// In-tree flags, plus a check that the edge list is sorted by (eu, ev) with
+// eu < ev (grid edge lists are): then a stable sort of the arcs by source
+// alone already leaves every adjacency list in ascending order.
+__global__ void k_flag_edges(int64_t m, const uint8_t* __restrict__ in_tree, const int32_t* __restrict__ eu,
+                             const int32_t* __restrict__ ev, int32_t* flags, int* unsorted) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < m) flags[e] = in_tree ? (in_tree[e] ? 1 : 0) : 1;
+    bool bad = false;
+    if (e < m) {
+        flags[e] = in_tree ? (in_tree[e] ? 1 : 0) : 1;
+        const int32_t u = eu[e], v = ev[e];
+        bad = u >= v;
+        if (e + 1 < m) {
+            const int32_t u2 = eu[e + 1], v2 = ev[e + 1];
+            bad = bad || u > u2 || (u == u2 && v >= v2);
+        }
+    }
+    if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && *(volatile int*)unsorted == 0) *unsorted = 1;
+}
+
+__global__ void k_edge_count(int64_t m, const int32_t* __restrict__ flags, const int32_t* __restrict__ pos,
+                             int* out) {
+    out[0] = pos[m - 1] + flags[m - 1];
 }
 
 __global__ void k_compact_edges(int64_t m, const int32_t* __restrict__ flags,
@@ -53,7 +72,7 @@ __global__ void k_fill_int(int64_t n, int32_t* a, int32_t v) {
     if (i < n) a[i] = v;
 }
 
-__global__ void k_min_root(int64_t n, const int32_t* __restrict__ comp, int32_t* minid) {
+__global__ void k_min_root(int64_t n, const int32_t* __restrict__ comp, int32_t* minid, int32_t* csize) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool ok = v < n;
     int32_t c = ok ? comp[v] : -1;
@@ -61,16 +80,31 @@ __global__ void k_min_root(int64_t n, const int32_t* __restrict__ comp, int32_t*
     unsigned peers = __match_any_sync(0xffffffffu, c);
     int32_t mn = __reduce_min_sync(peers, ok ? (int32_t)v : INT_MAX);
     int leader = __ffs(peers) - 1;
-    if (ok && (int)(threadIdx.x & 31) == leader) atomicMin(&minid[c], mn);
+    if (ok && (int)(threadIdx.x & 31) == leader) {
+        atomicMin(&minid[c], mn);
+        atomicAdd(&csize[c], __popc(peers));
+    }
 }
 
 __global__ void k_root_flags(int64_t n, const int32_t* __restrict__ comp,
-                             const int32_t* __restrict__ minid, int32_t* root, int32_t* is_root) {
+                             const int32_t* __restrict__ minid, const int32_t* __restrict__ csize,
+                             int32_t* root, int32_t* is_root, int32_t* max_size) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    int32_t r = minid[comp[v]];
-    root[v] = r;
-    is_root[v] = (r == v) ? 1 : 0;
+    int32_t sz = 0;
+    if (v < n) {
+        int32_t c = comp[v];
+        int32_t r = minid[c];
+        root[v] = r;
+        is_root[v] = (r == v) ? 1 : 0;
+        if (r == v) sz = csize[c];
+    }
+    sz = __reduce_max_sync(0xffffffffu, sz);
+    if ((threadIdx.x & 31) == 0 && sz > 0) atomicMax(max_size, sz);
+}
+
+__global__ void k_tree_count(int64_t n, const int32_t* __restrict__ tindex, const int32_t* __restrict__ is_root,
+                             int32_t* out) {
+    out[0] = tindex[n - 1] + is_root[n - 1];
 }
 
 __global__ void k_tree_ids(int64_t n, const int32_t* __restrict__ root,
@@ -131,25 +165,30 @@ __global__ void k_tour_next(int64_t na, const int32_t* __restrict__ asrc,
     next[i] = nx;
 }
 
-__global__ void k_rank_init(int64_t na, int32_t* rank) {
+// list words: (next << 32 | rank), next = -1 at a list's end
+__global__ void k_rank_init(int64_t na, const int32_t* __restrict__ next, uint64_t* word) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < na) rank[i] = 1;
+    if (i < na) word[i] = ((uint64_t)(uint32_t)next[i] << 32) | 1u;
 }
 
-// Wyllie pointer jumping: rank = number of arcs from i to the end of its list.
-__global__ void k_rank_jump(int64_t na, const int32_t* __restrict__ next_in,
-                            const int32_t* __restrict__ rank_in, int32_t* next_out,
-                            int32_t* rank_out) {
+// Wyllie pointer jumping on packed words (one random 8-byte load per arc and
+// round): rank = number of arcs from i to the end of its list.
+__global__ void k_rank_jump(int64_t na, const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= na) return;
-    int32_t nx = next_in[i];
+    const uint64_t w = in[i];
+    const int32_t nx = (int32_t)(w >> 32);
     if (nx >= 0) {
-        rank_out[i] = rank_in[i] + rank_in[nx];
-        next_out[i] = next_in[nx];
+        const uint64_t w2 = in[nx];
+        out[i] = (w2 & 0xffffffff00000000ull) | (uint32_t)((uint32_t)w + (uint32_t)w2);
     } else {
-        rank_out[i] = rank_in[i];
-        next_out[i] = -1;
+        out[i] = w;
     }
+}
+
+__global__ void k_rank_unpack(int64_t na, const uint64_t* __restrict__ word, int32_t* rank) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) rank[i] = (int32_t)(uint32_t)word[i];
 }
 
 // Per tree: tour length L = rank of the root's first arc (0 for singletons).
@@ -517,13 +556,18 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(flags.alloc(m_in + 1, st));
     HDP_TRY(fpos.alloc(m_in + 1, st));
     int64_t m = 0;
+    bool lex = false;  // edge list sorted by (eu, ev), eu < ev
     if (m_in > 0) {
-        k_flag_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, in_tree, flags.get()); note_launch();
+        DevBuf<int> cnt;  // (tree edges, unsorted flag)
+        HDP_TRY(cnt.alloc(2, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(int), st));
+        k_flag_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, in_tree, eu, ev, flags.get(), cnt.get() + 1); note_launch();
         HDP_TRY(exclusive_sum(flags.get(), fpos.get(), m_in, st));
-        int32_t last_pos = 0, last_flag = 0;
-        HDP_TRY(to_host(&last_pos, fpos.get() + m_in - 1, 1, st));
-        HDP_TRY(to_host(&last_flag, flags.get() + m_in - 1, 1, st));
-        m = (int64_t)last_pos + last_flag;
+        k_edge_count<<<1, 1, 0, st>>>(m_in, flags.get(), fpos.get(), cnt.get()); note_launch();
+        int hc[2] = {0, 0};
+        HDP_TRY(to_host(hc, cnt.get(), 2, st));
+        m = hc[0];
+        lex = hc[1] == 0;
     }
     HDP_REQUIRE(m <= n - 1 || n == 0, HDP_ERR_DATA, "forest has %lld edges for %lld nodes (cycle)",
                 (long long)m, (long long)n);
@@ -559,16 +603,23 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(tindex.alloc(n, st));
     HDP_TRY(f->root.alloc(n, st));
     HDP_TRY(f->tree_id.alloc(n, st));
-    k_fill_int<<<grid_for(n, B), B, 0, st>>>(n, minid.get(), INT_MAX); note_launch();
-    k_min_root<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get()); note_launch();
-    k_root_flags<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get(), f->root.get(),
-                                              is_root.get()); note_launch();
-    HDP_TRY(exclusive_sum(is_root.get(), tindex.get(), n, st));
+    int32_t max_tree = 1;  // nodes in the largest tree
     {
-        int32_t a = 0, b = 0;
-        HDP_TRY(to_host(&a, tindex.get() + n - 1, 1, st));
-        HDP_TRY(to_host(&b, is_root.get() + n - 1, 1, st));
-        f->n_trees = (int64_t)a + b;
+        DevBuf<int32_t> csize, cnt;  // cnt = (trees, largest tree)
+        HDP_TRY(csize.alloc(n, st));
+        HDP_TRY(cnt.alloc(2, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(csize.get(), 0, n * sizeof(int32_t), st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(int32_t), st));
+        k_fill_int<<<grid_for(n, B), B, 0, st>>>(n, minid.get(), INT_MAX); note_launch();
+        k_min_root<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get(), csize.get()); note_launch();
+        k_root_flags<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get(), csize.get(), f->root.get(),
+                                                  is_root.get(), cnt.get() + 1); note_launch();
+        HDP_TRY(exclusive_sum(is_root.get(), tindex.get(), n, st));
+        k_tree_count<<<1, 1, 0, st>>>(n, tindex.get(), is_root.get(), cnt.get()); note_launch();
+        int32_t hc[2] = {0, 0};
+        HDP_TRY(to_host(hc, cnt.get(), 2, st));
+        f->n_trees = hc[0];
+        max_tree = hc[1] > 0 ? hc[1] : 1;
     }
     k_tree_ids<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), tindex.get(), f->tree_id.get()); note_launch();
     HDP_CHECK_LAUNCH();
@@ -592,7 +643,9 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     if (m > 0) {
         k_make_arcs<<<grid_for(m, B), B, 0, st>>>(m, tu.get(), tv.get(), tw.get(), akey.get(),
                                                  aw.get(), deg.get()); note_launch();
-        HDP_TRY(sort_pairs(akey.get(), akey2.get(), aw.get(), aw2.get(), na, 0,
+        // by (src, dst); with a lexicographic edge list the arcs of a source
+        // already come in ascending dst, so a stable sort on src suffices
+        HDP_TRY(sort_pairs(akey.get(), akey2.get(), aw.get(), aw2.get(), na, lex ? 32 : 0,
                            32 + bits_for(n), st));
     }
     HDP_TRY(exclusive_sum(deg.get(), adj_start.get(), n + 1, st));
@@ -608,12 +661,10 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
 
     tr.mark("3 csr adjacency");
     // ---- 4. Euler tour + list ranking
-    DevBuf<int32_t> twin, nxt, nxt2, rank, rank2, tlen, toff, tpos;
+    DevBuf<int32_t> twin, nxt, rank, tlen, toff, tpos;
     HDP_TRY(twin.alloc(na + 1, st));
     HDP_TRY(nxt.alloc(na + 1, st));
-    HDP_TRY(nxt2.alloc(na + 1, st));
     HDP_TRY(rank.alloc(na + 1, st));
-    HDP_TRY(rank2.alloc(na + 1, st));
     HDP_TRY(tlen.alloc(f->n_trees + 1, st));
     HDP_TRY(toff.alloc(f->n_trees + 1, st));
     HDP_TRY(tpos.alloc(na + 1, st));
@@ -621,14 +672,17 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     if (na > 0) {
         k_tour_next<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), adj_start.get(),
                                                   f->root.get(), twin.get(), nxt.get()); note_launch();
-        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, rank.get()); note_launch();
-        int rounds = ceil_log2(na + 1);
+        DevBuf<uint64_t> wa, wb;
+        HDP_TRY(wa.alloc(na, st));
+        HDP_TRY(wb.alloc(na, st));
+        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), wa.get()); note_launch();
+        // the longest list is the largest tree's tour, 2 (size - 1) arcs
+        int rounds = ceil_log2(2 * (int64_t)max_tree);
         for (int r = 0; r < rounds; r++) {
-            k_rank_jump<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), rank.get(), nxt2.get(),
-                                                      rank2.get()); note_launch();
-            std::swap(nxt.p, nxt2.p);
-            std::swap(rank.p, rank2.p);
+            k_rank_jump<<<grid_for(na, B), B, 0, st>>>(na, wa.get(), wb.get()); note_launch();
+            std::swap(wa.p, wb.p);
         }
+        k_rank_unpack<<<grid_for(na, B), B, 0, st>>>(na, wa.get(), rank.get()); note_launch();
         HDP_CHECK_LAUNCH();
     }
     k_tour_len<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), f->root.get(), f->tree_id.get(),
@@ -638,9 +692,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         k_tour_pos<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), f->tree_id.get(), tlen.get(),
                                                  rank.get(), tpos.get()); note_launch();
     nxt.release();
-    nxt2.release();
     rank.release();
-    rank2.release();
 
     tr.mark("4 euler tour+ranking");
     // ---- 5. orientation, sizes, depth
