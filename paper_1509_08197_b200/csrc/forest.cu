@@ -540,6 +540,142 @@ __global__ void k_node_m(int64_t n, const int32_t* __restrict__ tree_id,
     if (v < n) nm[v] = t_m[tree_id[v]];
 }
 
+// ---- device-count driven path/phase tables (steps 8-10): every count stays
+// on the device until one summary read at the end of the build.
+constexpr int kMaxPhases = 64;  // light depth <= log2(n) + 1
+enum { C_NP = 0, C_NPH, C_NL, C_NSEG, C_NLC, C_NLP, C_MAXD, C_COUNT };
+// per-phase table rows of the summary
+enum { P_FIRST = 0, P_NODE, P_LONG, P_SHORT, P_SEG, P_SEND, P_LP, P_LPM, P_ROWS };
+
+__global__ void k_path_flags_n(int64_t n, const int32_t* __restrict__ lnode,
+                               const int32_t* __restrict__ head, int32_t* flag) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) {
+        int32_t v = lnode[k];
+        flag[k] = head[v] == v ? 1 : 0;
+    } else if (k == n) {
+        flag[k] = 0;
+    }
+}
+
+// per path: length, parent position, tree, light depth, long flag; entries
+// past the path count get is_long = 0 so that a scan over n + 1 is exact
+__global__ void k_path_info_n(int64_t n, const int32_t* __restrict__ pidx, const int32_t* __restrict__ p_start,
+                              const int32_t* __restrict__ lnode, const int32_t* __restrict__ parent,
+                              const int32_t* __restrict__ lpos, const int32_t* __restrict__ tree_id,
+                              const int32_t* __restrict__ ld, int32_t* p_len, int32_t* p_par,
+                              int32_t* p_tree, int32_t* p_ld, int32_t* is_long) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int32_t np = pidx[n];
+    if (i >= np) {
+        is_long[i] = 0;
+        return;
+    }
+    int32_t s = p_start[i];
+    int32_t e = (i + 1 < np) ? p_start[i + 1] : (int32_t)n;
+    int32_t h = lnode[s];
+    p_len[i] = e - s;
+    p_par[i] = parent[h] == h ? -1 : lpos[parent[h]];
+    p_tree[i] = tree_id[h];
+    p_ld[i] = ld[h];
+    is_long[i] = (e - s) > kShortPath ? 1 : 0;
+}
+
+__global__ void k_path_counts(int64_t n, const int32_t* __restrict__ pidx, const int32_t* __restrict__ p_ld,
+                              int32_t* cnt) {
+    const int32_t np = pidx[n];
+    cnt[C_NP] = np;
+    cnt[C_NPH] = np > 0 ? p_ld[np - 1] + 1 : 0;
+}
+
+// first path of every phase (paths are phase-major)
+__global__ void k_phase_bounds_n(int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ p_ld,
+                                 int32_t* first) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t np = cnt[C_NP], nph = cnt[C_NPH];
+    if (i > np) return;
+    int a = (i == 0) ? -1 : p_ld[i - 1];
+    int b = (i == np) ? nph : p_ld[i];
+    for (int r = a + 1; r <= b; r++) first[r] = (int32_t)i;
+}
+
+__global__ void k_split_paths_n(int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ is_long,
+                                const int32_t* __restrict__ lexcl, int32_t* long_paths, int32_t* short_paths) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt[C_NP]) return;
+    int32_t l = lexcl[i];
+    if (is_long[i]) long_paths[l] = (int32_t)i;
+    else short_paths[i - l] = (int32_t)i;
+}
+
+// phase table rows FIRST, NODE, LONG, SHORT (r in [0, nph])
+__global__ void k_phase_tab(int64_t n, int32_t* cnt, const int32_t* __restrict__ first,
+                            const int32_t* __restrict__ p_start, const int32_t* __restrict__ lexcl, int32_t* ph) {
+    const int32_t np = cnt[C_NP], nph = cnt[C_NPH];
+    for (int r = threadIdx.x; r <= nph; r += blockDim.x) {
+        int32_t fi = first[r];
+        ph[P_FIRST * (kMaxPhases + 1) + r] = fi;
+        ph[P_NODE * (kMaxPhases + 1) + r] = fi < np ? p_start[fi] : (int32_t)n;
+        int32_t lo = lexcl[fi];
+        ph[P_LONG * (kMaxPhases + 1) + r] = lo;
+        ph[P_SHORT * (kMaxPhases + 1) + r] = fi - lo;
+    }
+    if (threadIdx.x == 0) cnt[C_NL] = lexcl[np];
+}
+
+// short-path block end of every phase (short paths come first in a phase)
+__global__ void k_phase_send(int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ short_paths,
+                             const int32_t* __restrict__ p_start, const int32_t* __restrict__ p_len, int32_t* ph) {
+    const int32_t nph = cnt[C_NPH];
+    const int32_t* so = ph + P_SHORT * (kMaxPhases + 1);
+    const int32_t* pn = ph + P_NODE * (kMaxPhases + 1);
+    for (int r = threadIdx.x; r <= nph; r += blockDim.x) {
+        int32_t e = (int32_t)n;
+        if (r < nph) {
+            if (so[r + 1] > so[r]) {
+                int32_t p = short_paths[so[r + 1] - 1];
+                e = p_start[p] + p_len[p];
+            } else {
+                e = pn[r];
+            }
+        }
+        ph[P_SEND * (kMaxPhases + 1) + r] = e;
+    }
+}
+
+__global__ void k_seg_count_n(int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ long_paths,
+                              const int32_t* __restrict__ p_len, int32_t* nseg) {
+    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l > n) return;
+    nseg[l] = l < cnt[C_NL] ? (p_len[long_paths[l]] + kSeg - 1) / kSeg : 0;
+}
+
+__global__ void k_seg_fill_n(int64_t n, const int32_t* __restrict__ cnt, const int32_t* __restrict__ nseg,
+                             const int32_t* __restrict__ soff, int2* seg_tab) {
+    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= cnt[C_NL]) return;
+    int32_t o = soff[l];
+    for (int s = 0; s < nseg[l]; s++) seg_tab[o + s] = make_int2((int)l, s);
+}
+
+// remaining rows (SEG, LP, LPM) and counts, then the packed summary
+__global__ void k_forest_summary(int64_t n, int32_t* cnt, const int32_t* __restrict__ soff,
+                                 const int32_t* __restrict__ lc_start, const int32_t* __restrict__ ex,
+                                 int32_t* ph) {
+    const int32_t nph = cnt[C_NPH];
+    for (int r = threadIdx.x; r <= nph; r += blockDim.x) {
+        ph[P_SEG * (kMaxPhases + 1) + r] = soff[ph[P_LONG * (kMaxPhases + 1) + r]];
+        ph[P_LP * (kMaxPhases + 1) + r] = ex[ph[P_NODE * (kMaxPhases + 1) + r]];
+        ph[P_LPM * (kMaxPhases + 1) + r] = ex[ph[P_SEND * (kMaxPhases + 1) + r]];
+    }
+    if (threadIdx.x == 0) {
+        cnt[C_NSEG] = soff[cnt[C_NL]];
+        cnt[C_NLC] = lc_start[n];
+        cnt[C_NLP] = ex[n];
+    }
+}
+
 }  // namespace hdp
 
 using namespace hdp;
@@ -716,14 +852,6 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         k_depth_gather<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), f->depth.get()); note_launch();
     }
     HDP_CHECK_LAUNCH();
-    {
-        DevBuf<int32_t> mx;
-        HDP_TRY(mx.alloc(1, st));
-        HDP_TRY(reduce_max(f->depth.get(), mx.get(), n, st));
-        int32_t h = 0;
-        HDP_TRY(to_host(&h, mx.get(), 1, st));
-        f->max_depth = h;
-    }
     aw2.release();
     twin.release();
 
@@ -739,7 +867,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                           f->size.get(), heavy.get()); note_launch();
     k_hp_init<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), hp.get(), dist.get()); note_launch();
     {
-        int rounds = ceil_log2(f->max_depth + 2);
+        int rounds = ceil_log2((int64_t)max_tree + 1);  // depth < the largest tree
         for (int r = 0; r < rounds; r++) {
             k_hp_jump<<<grid_for(n, B), B, 0, st>>>(n, hp.get(), dist.get(), hp2.get(), dist2.get()); note_launch();
             std::swap(hp.p, hp2.p);
@@ -768,7 +896,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(lkey2.alloc(n, st));
     HDP_TRY(lidx.alloc(n, st));
     HDP_TRY(f->lnode.alloc(n, st));
-    int dbits = bits_for(f->max_depth + 1), hbits = bits_for(n);
+    int dbits = bits_for(max_tree), hbits = bits_for(n);  // distance from a head < tree size
     // light depth <= log2(n) + 1 < 64 needs 6 bits, the long flag one more
     HDP_REQUIRE(hbits + dbits <= 57, HDP_ERR_CONFIG, "forest too large for the layout key");
     {
@@ -799,108 +927,59 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                f->lpos.get(), f->lsim.get()); note_launch();
 
     tr.mark("7 layout sort");
-    // ---- 8. paths and phases
+    // ---- 8. paths and phases (sizes bounded by n; counts stay on the device)
+    const int PH = kMaxPhases + 1;
+    DevBuf<int32_t> dcnt, dph;  // counters, per-phase table
+    HDP_TRY(dcnt.alloc(C_COUNT, st));
+    HDP_TRY(dph.alloc(P_ROWS * PH, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(dcnt.get(), 0, C_COUNT * sizeof(int32_t), st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(dph.get(), 0, P_ROWS * PH * sizeof(int32_t), st));
+    HDP_TRY(reduce_max(f->depth.get(), dcnt.get() + C_MAXD, n, st));
     DevBuf<int32_t> pflag, pidx;
-    HDP_TRY(pflag.alloc(n, st));
-    HDP_TRY(pidx.alloc(n, st));
-    k_path_flags<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), head, pflag.get()); note_launch();
-    HDP_TRY(exclusive_sum(pflag.get(), pidx.get(), n, st));
-    {
-        int32_t a = 0, b = 0;
-        HDP_TRY(to_host(&a, pidx.get() + n - 1, 1, st));
-        HDP_TRY(to_host(&b, pflag.get() + n - 1, 1, st));
-        f->n_paths = (int64_t)a + b;
-    }
-    HDP_TRY(f->p_start.alloc(f->n_paths, st));
-    HDP_TRY(f->p_len.alloc(f->n_paths, st));
-    HDP_TRY(f->p_par.alloc(f->n_paths, st));
-    HDP_TRY(f->p_tree.alloc(f->n_paths, st));
+    HDP_TRY(pflag.alloc(n + 1, st));
+    HDP_TRY(pidx.alloc(n + 1, st));
+    k_path_flags_n<<<grid_for(n + 1, B), B, 0, st>>>(n, f->lnode.get(), head, pflag.get()); note_launch();
+    HDP_TRY(exclusive_sum(pflag.get(), pidx.get(), n + 1, st));
+    HDP_TRY(f->p_start.alloc(n + 1, st));
+    HDP_TRY(f->p_len.alloc(n + 1, st));
+    HDP_TRY(f->p_par.alloc(n + 1, st));
+    HDP_TRY(f->p_tree.alloc(n + 1, st));
     k_path_fill<<<grid_for(n, B), B, 0, st>>>(n, pflag.get(), pidx.get(), f->p_start.get()); note_launch();
     DevBuf<int32_t> p_ld, is_long, lexcl, first;
-    HDP_TRY(p_ld.alloc(f->n_paths + 1, st));
-    HDP_TRY(is_long.alloc(f->n_paths + 1, st));
-    HDP_TRY(lexcl.alloc(f->n_paths + 1, st));
-    k_path_info<<<grid_for(f->n_paths, B), B, 0, st>>>(
-        f->n_paths, n, f->p_start.get(), f->lnode.get(), f->parent.get(), f->lpos.get(),
-        f->tree_id.get(), ld.get(), f->p_len.get(), f->p_par.get(), f->p_tree.get(), p_ld.get(),
-        is_long.get()); note_launch();
+    HDP_TRY(p_ld.alloc(n + 1, st));
+    HDP_TRY(is_long.alloc(n + 1, st));
+    HDP_TRY(lexcl.alloc(n + 1, st));
+    HDP_TRY(first.alloc(PH, st));
+    k_path_info_n<<<grid_for(n + 1, B), B, 0, st>>>(n, pidx.get(), f->p_start.get(), f->lnode.get(),
+                                                    f->parent.get(), f->lpos.get(), f->tree_id.get(), ld.get(),
+                                                    f->p_len.get(), f->p_par.get(), f->p_tree.get(), p_ld.get(),
+                                                    is_long.get()); note_launch();
+    k_path_counts<<<1, 1, 0, st>>>(n, pidx.get(), p_ld.get(), dcnt.get()); note_launch();
+    k_phase_bounds_n<<<grid_for(n + 1, B), B, 0, st>>>(n, dcnt.get(), p_ld.get(), first.get()); note_launch();
+    HDP_TRY(exclusive_sum(is_long.get(), lexcl.get(), n + 1, st));
+    HDP_TRY(f->long_paths.alloc(n + 1, st));
+    HDP_TRY(f->short_paths.alloc(n + 1, st));
+    k_split_paths_n<<<grid_for(n, B), B, 0, st>>>(n, dcnt.get(), is_long.get(), lexcl.get(), f->long_paths.get(),
+                                                  f->short_paths.get()); note_launch();
+    k_phase_tab<<<1, 64, 0, st>>>(n, dcnt.get(), first.get(), f->p_start.get(), lexcl.get(), dph.get()); note_launch();
+    k_phase_send<<<1, 64, 0, st>>>(n, dcnt.get(), f->short_paths.get(), f->p_start.get(), f->p_len.get(),
+                                   dph.get()); note_launch();
+    // segments of kSeg nodes over the long paths (head first), phase-major
+    DevBuf<int32_t> nseg, soff;
+    HDP_TRY(nseg.alloc(n + 1, st));
+    HDP_TRY(soff.alloc(n + 1, st));
+    k_seg_count_n<<<grid_for(n + 1, B), B, 0, st>>>(n, dcnt.get(), f->long_paths.get(), f->p_len.get(),
+                                                    nseg.get()); note_launch();
+    HDP_TRY(exclusive_sum(nseg.get(), soff.get(), n + 1, st));
+    HDP_TRY(f->seg_tab.alloc(n + 1, st));
+    k_seg_fill_n<<<grid_for(n, B), B, 0, st>>>(n, dcnt.get(), nseg.get(), soff.get(), f->seg_tab.get()); note_launch();
     HDP_CHECK_LAUNCH();
-    {
-        int32_t last_ld = 0;
-        HDP_TRY(to_host(&last_ld, p_ld.get() + f->n_paths - 1, 1, st));
-        f->n_phases = last_ld + 1;
-        HDP_TRY(first.alloc(f->n_phases + 1, st));
-        k_phase_bounds<<<grid_for(f->n_paths + 1, B), B, 0, st>>>(f->n_paths, p_ld.get(),
-                                                                  (int)f->n_phases, first.get()); note_launch();
-        HDP_CHECK_CUDA(cudaMemsetAsync(is_long.get() + f->n_paths, 0, sizeof(int32_t), st));
-        HDP_TRY(exclusive_sum(is_long.get(), lexcl.get(), f->n_paths + 1, st));
-        std::vector<int32_t> fh(f->n_phases + 1);
-        HDP_TRY(to_host(fh.data(), first.get(), f->n_phases + 1, st));
-        f->phase_off.assign(fh.begin(), fh.end());
-        // layout node ranges and long/short split offsets per phase
-        f->phase_node.assign(f->n_phases + 1, n);
-        f->long_off.assign(f->n_phases + 1, 0);
-        f->short_off.assign(f->n_phases + 1, 0);
-        {
-            DevBuf<int32_t> bnd;
-            HDP_TRY(bnd.alloc(2 * (f->n_phases + 1), st));
-            k_phase_gather<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(
-                f->n_phases + 1, first.get(), f->p_start.get(), lexcl.get(), f->n_paths, n,
-                bnd.get()); note_launch();
-            std::vector<int32_t> hb(2 * (f->n_phases + 1));
-            HDP_TRY(to_host(hb.data(), bnd.get(), 2 * (f->n_phases + 1), st));
-            for (int64_t r = 0; r <= f->n_phases; r++) {
-                f->phase_node[r] = hb[2 * r];
-                f->long_off[r] = hb[2 * r + 1];
-                f->short_off[r] = f->phase_off[r] - hb[2 * r + 1];
-            }
-        }
-        HDP_TRY(f->long_paths.alloc(f->long_off[f->n_phases] + 1, st));
-        HDP_TRY(f->short_paths.alloc(f->short_off[f->n_phases] + 1, st));
-        k_split_paths<<<grid_for(f->n_paths, B), B, 0, st>>>(f->n_paths, is_long.get(), lexcl.get(),
-                                                             f->long_paths.get(),
-                                                             f->short_paths.get()); note_launch();
-        HDP_CHECK_LAUNCH();
-        {
-            const int nph = (int)f->n_phases;
-            DevBuf<int64_t> dso, dpn, dse;
-            HDP_TRY(dso.alloc(nph + 1, st));
-            HDP_TRY(dpn.alloc(nph + 1, st));
-            HDP_TRY(dse.alloc(nph + 1, st));
-            HDP_CHECK_CUDA(cudaMemcpyAsync(dso.get(), f->short_off.data(), sizeof(int64_t) * (nph + 1),
-                                           cudaMemcpyHostToDevice, st));
-            HDP_CHECK_CUDA(cudaMemcpyAsync(dpn.get(), f->phase_node.data(), sizeof(int64_t) * (nph + 1),
-                                           cudaMemcpyHostToDevice, st));
-            k_short_end<<<grid_for(nph, 64), 64, 0, st>>>(nph, dso.get(), dpn.get(), f->short_paths.get(),
-                                                          f->p_start.get(), f->p_len.get(), dse.get()); note_launch();
-            f->short_end.assign(nph + 1, n);
-            HDP_TRY(to_host(f->short_end.data(), dse.get(), nph, st));
-        }
-        // segments of kSeg nodes over the long paths (head first), phase-major
-        int64_t nl = f->long_off[f->n_phases];
-        DevBuf<int32_t> nseg, soff, sb, sbh;
-        HDP_TRY(nseg.alloc(nl + 1, st));
-        HDP_TRY(soff.alloc(nl + 1, st));
-        k_seg_count<<<grid_for(nl + 1, B), B, 0, st>>>(nl, f->long_paths.get(), f->p_len.get(),
-                                                       nseg.get()); note_launch();
-        HDP_TRY(exclusive_sum(nseg.get(), soff.get(), nl + 1, st));
-        int32_t ns_total = 0;
-        HDP_TRY(to_host(&ns_total, soff.get() + nl, 1, st));
-        f->n_segs = ns_total;
-        HDP_TRY(f->seg_tab.alloc(ns_total + 1, st));
-        if (nl > 0)
-            k_seg_fill<<<grid_for(nl, B), B, 0, st>>>(nl, nseg.get(), soff.get(), f->seg_tab.get()); note_launch();
-        std::vector<int32_t> lo(f->n_phases + 1), so(f->n_phases + 1);
-        for (int64_t r = 0; r <= f->n_phases; r++) lo[r] = (int32_t)f->long_off[r];
-        HDP_TRY(sb.alloc(f->n_phases + 1, st));
-        HDP_TRY(sbh.alloc(f->n_phases + 1, st));
-        HDP_CHECK_CUDA(cudaMemcpyAsync(sb.get(), lo.data(), sizeof(int32_t) * (f->n_phases + 1),
-                                       cudaMemcpyHostToDevice, st));
-        k_gather_i32<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(f->n_phases + 1, soff.get(),
-                                                                   sb.get(), sbh.get()); note_launch();
-        HDP_TRY(to_host(so.data(), sbh.get(), f->n_phases + 1, st));
-        f->seg_off.assign(so.begin(), so.end());
-    }
+    pflag.release();
+    pidx.release();
+    p_ld.release();
+    is_long.release();
+    first.release();
+    nseg.release();
 
     tr.mark("8 paths/phases");
     // ---- 9. light-children CSR in layout order
@@ -911,9 +990,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     k_lc_count<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
                                              f->parent.get(), head, lcc.get()); note_launch();
     HDP_TRY(exclusive_sum(lcc.get(), f->lc_start.get(), n + 1, st));
-    int32_t n_lc = 0;
-    HDP_TRY(to_host(&n_lc, f->lc_start.get() + n, 1, st));
-    HDP_TRY(f->lc_list.alloc(n_lc + 1, st));
+    HDP_TRY(f->lc_list.alloc(n + 1, st));  // light children <= n - 1
     k_lc_fill<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
                                             f->parent.get(), head, f->lpos.get(),
                                             f->lc_start.get(), f->lc_list.get()); note_launch();
@@ -922,37 +999,47 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     tr.mark("9 light children");
     // ---- 10. light parents (positions with light children), phase-major
     {
-        DevBuf<int32_t> fl, ex, bnd, pn;
+        DevBuf<int32_t> fl, ex;
         HDP_TRY(fl.alloc(n + 1, st));
         HDP_TRY(ex.alloc(n + 1, st));
         k_lp_flags<<<grid_for(n + 1, B), B, 0, st>>>(n, f->lc_start.get(), fl.get()); note_launch();
         HDP_TRY(exclusive_sum(fl.get(), ex.get(), n + 1, st));
-        int32_t n_lp = 0;
-        HDP_TRY(to_host(&n_lp, ex.get() + n, 1, st));
-        HDP_TRY(f->lp_list.alloc(n_lp + 1, st));
+        HDP_TRY(f->lp_list.alloc(n + 1, st));
         k_lp_fill<<<grid_for(n, B), B, 0, st>>>(n, fl.get(), ex.get(), f->lp_list.get()); note_launch();
-        std::vector<int32_t> hp(f->n_phases + 1), hl(f->n_phases + 1);
-        for (int64_t r = 0; r <= f->n_phases; r++) hp[r] = (int32_t)f->phase_node[r];
-        HDP_TRY(pn.alloc(f->n_phases + 1, st));
-        HDP_TRY(bnd.alloc(f->n_phases + 1, st));
-        HDP_CHECK_CUDA(cudaMemcpyAsync(pn.get(), hp.data(), sizeof(int32_t) * (f->n_phases + 1),
-                                       cudaMemcpyHostToDevice, st));
-        k_gather_i32<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(f->n_phases + 1, ex.get(), pn.get(),
-                                                                   bnd.get()); note_launch();
-        HDP_TRY(to_host(hl.data(), bnd.get(), f->n_phases + 1, st));
-        f->lp_off.assign(hl.begin(), hl.end());
-        for (int64_t r = 0; r <= f->n_phases; r++) hp[r] = (int32_t)f->short_end[r];
-        HDP_CHECK_CUDA(cudaMemcpyAsync(pn.get(), hp.data(), sizeof(int32_t) * (f->n_phases + 1),
-                                       cudaMemcpyHostToDevice, st));
-        k_gather_i32<<<grid_for(f->n_phases + 1, 64), 64, 0, st>>>(f->n_phases + 1, ex.get(), pn.get(),
-                                                                   bnd.get()); note_launch();
-        HDP_TRY(to_host(hl.data(), bnd.get(), f->n_phases + 1, st));
-        f->lp_mid.assign(hl.begin(), hl.end());
+        k_forest_summary<<<1, 64, 0, st>>>(n, dcnt.get(), soff.get(), f->lc_start.get(), ex.get(), dph.get()); note_launch();
+        HDP_CHECK_LAUNCH();
+        // the one host read of steps 5-10: counts and the per-phase table
+        std::vector<int32_t> hbuf(C_COUNT + P_ROWS * PH);
+        HDP_CHECK_CUDA(cudaMemcpyAsync(hbuf.data(), dcnt.get(), C_COUNT * sizeof(int32_t),
+                                       cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(hbuf.data() + C_COUNT, dph.get(), P_ROWS * PH * sizeof(int32_t),
+                                       cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaStreamSynchronize(st));
+        const int32_t* hc = hbuf.data();
+        const int32_t* hp = hbuf.data() + C_COUNT;
+        f->n_paths = hc[C_NP];
+        f->n_phases = hc[C_NPH];
+        f->max_depth = hc[C_MAXD];
+        f->n_segs = hc[C_NSEG];
+        HDP_REQUIRE(f->n_phases >= 1 && f->n_phases <= kMaxPhases, HDP_ERR_INTERNAL,
+                    "light depth %lld out of range", (long long)f->n_phases);
+        auto row = [&](int k, std::vector<int64_t>& out) {
+            out.assign(f->n_phases + 1, 0);
+            for (int64_t r = 0; r <= f->n_phases; r++) out[r] = hp[k * PH + r];
+        };
+        row(P_FIRST, f->phase_off);
+        row(P_NODE, f->phase_node);
+        row(P_LONG, f->long_off);
+        row(P_SHORT, f->short_off);
+        row(P_SEG, f->seg_off);
+        row(P_SEND, f->short_end);
+        row(P_LP, f->lp_off);
+        row(P_LPM, f->lp_mid);
     }
     tr.mark("10 light parents");
-    HDP_CHECK_CUDA(cudaStreamSynchronize(st));
     return HDP_OK;
 }
+
 
 namespace hdp {
 
