@@ -337,21 +337,6 @@ __global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
     idx[v] = (int32_t)v;
 }
 
-__global__ void k_seg_count(int64_t nl, const int32_t* __restrict__ long_paths,
-                            const int32_t* __restrict__ p_len, int32_t* nseg) {
-    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (l < nl) nseg[l] = (p_len[long_paths[l]] + kSeg - 1) / kSeg;
-    else if (l == nl) nseg[l] = 0;
-}
-
-__global__ void k_seg_fill(int64_t nl, const int32_t* __restrict__ nseg,
-                           const int32_t* __restrict__ soff, int2* seg_tab) {
-    int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (l >= nl) return;
-    int32_t o = soff[l];
-    for (int s = 0; s < nseg[l]; s++) seg_tab[o + s] = make_int2((int)l, s);
-}
-
 __global__ void k_lp_flags(int64_t n, const int32_t* __restrict__ lc_start, int32_t* fl) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) fl[k] = lc_start[k + 1] > lc_start[k] ? 1 : 0;
@@ -382,81 +367,10 @@ __global__ void k_layout_pos(int64_t n, const int32_t* __restrict__ lnode,
     lsim[k] = (float)exp(-(double)pweight[v] / ((double)gamma * 255.0));
 }
 
-__global__ void k_path_flags(int64_t n, const int32_t* __restrict__ lnode,
-                             const int32_t* __restrict__ head, int32_t* flag) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int32_t v = lnode[k];
-    flag[k] = head[v] == v ? 1 : 0;
-}
-
 __global__ void k_path_fill(int64_t n, const int32_t* __restrict__ flag,
                             const int32_t* __restrict__ pidx, int32_t* p_start) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n && flag[k]) p_start[pidx[k]] = (int32_t)k;
-}
-
-__global__ void k_path_info(int64_t np, int64_t n, const int32_t* __restrict__ p_start,
-                            const int32_t* __restrict__ lnode, const int32_t* __restrict__ parent,
-                            const int32_t* __restrict__ lpos, const int32_t* __restrict__ tree_id,
-                            const int32_t* __restrict__ ld, int32_t* p_len, int32_t* p_par,
-                            int32_t* p_tree, int32_t* p_ld, int32_t* is_long) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= np) return;
-    int32_t s = p_start[i];
-    int32_t e = (i + 1 < np) ? p_start[i + 1] : (int32_t)n;
-    int32_t h = lnode[s];
-    p_len[i] = e - s;
-    p_par[i] = parent[h] == h ? -1 : lpos[parent[h]];
-    p_tree[i] = tree_id[h];
-    p_ld[i] = ld[h];
-    is_long[i] = (e - s) > kShortPath ? 1 : 0;
-}
-
-// first path index of every phase (paths are phase-major)
-__global__ void k_phase_bounds(int64_t np, const int32_t* __restrict__ p_ld, int nph,
-                               int32_t* first) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > np) return;
-    int a = (i == 0) ? -1 : p_ld[i - 1];
-    int b = (i == np) ? nph : p_ld[i];
-    for (int r = a + 1; r <= b; r++) first[r] = (int32_t)i;
-}
-
-// per phase: first layout position and the long-path prefix count at its start
-__global__ void k_phase_gather(int64_t nb, const int32_t* __restrict__ first,
-                               const int32_t* __restrict__ p_start,
-                               const int32_t* __restrict__ lexcl, int64_t np, int64_t n,
-                               int32_t* out) {
-    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nb) return;
-    int32_t pi = first[r];
-    out[2 * r] = pi < np ? p_start[pi] : (int32_t)n;
-    out[2 * r + 1] = lexcl[pi];
-}
-
-// end position of the short-path block of each phase (short paths first)
-__global__ void k_short_end(int nph, const int64_t* __restrict__ soff, const int64_t* __restrict__ pnode,
-                            const int32_t* __restrict__ short_paths, const int32_t* __restrict__ p_start,
-                            const int32_t* __restrict__ p_len, int64_t* out) {
-    int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= nph) return;
-    if (soff[r + 1] > soff[r]) {
-        int32_t p = short_paths[soff[r + 1] - 1];
-        out[r] = (int64_t)p_start[p] + p_len[p];
-    } else {
-        out[r] = pnode[r];
-    }
-}
-
-__global__ void k_split_paths(int64_t np, const int32_t* __restrict__ is_long,
-                              const int32_t* __restrict__ lpos_excl, int32_t* long_paths,
-                              int32_t* short_paths) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= np) return;
-    int32_t l = lpos_excl[i];
-    if (is_long[i]) long_paths[l] = (int32_t)i;
-    else short_paths[i - l] = (int32_t)i;
 }
 
 // light children of the node at layout position k, ascending id
@@ -929,11 +843,12 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     tr.mark("7 layout sort");
     // ---- 8. paths and phases (sizes bounded by n; counts stay on the device)
     const int PH = kMaxPhases + 1;
-    DevBuf<int32_t> dcnt, dph;  // counters, per-phase table
+    DevBuf<int32_t> dcnt;  // counters; f->dph holds the per-phase table
     HDP_TRY(dcnt.alloc(C_COUNT, st));
-    HDP_TRY(dph.alloc(P_ROWS * PH, st));
+    HDP_TRY(f->dph.alloc(P_ROWS * PH, st));
+    int32_t* dph = f->dph.get();
     HDP_CHECK_CUDA(cudaMemsetAsync(dcnt.get(), 0, C_COUNT * sizeof(int32_t), st));
-    HDP_CHECK_CUDA(cudaMemsetAsync(dph.get(), 0, P_ROWS * PH * sizeof(int32_t), st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(dph, 0, P_ROWS * PH * sizeof(int32_t), st));
     HDP_TRY(reduce_max(f->depth.get(), dcnt.get() + C_MAXD, n, st));
     DevBuf<int32_t> pflag, pidx;
     HDP_TRY(pflag.alloc(n + 1, st));
@@ -961,9 +876,9 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(f->short_paths.alloc(n + 1, st));
     k_split_paths_n<<<grid_for(n, B), B, 0, st>>>(n, dcnt.get(), is_long.get(), lexcl.get(), f->long_paths.get(),
                                                   f->short_paths.get()); note_launch();
-    k_phase_tab<<<1, 64, 0, st>>>(n, dcnt.get(), first.get(), f->p_start.get(), lexcl.get(), dph.get()); note_launch();
+    k_phase_tab<<<1, 64, 0, st>>>(n, dcnt.get(), first.get(), f->p_start.get(), lexcl.get(), dph); note_launch();
     k_phase_send<<<1, 64, 0, st>>>(n, dcnt.get(), f->short_paths.get(), f->p_start.get(), f->p_len.get(),
-                                   dph.get()); note_launch();
+                                   dph); note_launch();
     // segments of kSeg nodes over the long paths (head first), phase-major
     DevBuf<int32_t> nseg, soff;
     HDP_TRY(nseg.alloc(n + 1, st));
@@ -1006,13 +921,13 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         HDP_TRY(exclusive_sum(fl.get(), ex.get(), n + 1, st));
         HDP_TRY(f->lp_list.alloc(n + 1, st));
         k_lp_fill<<<grid_for(n, B), B, 0, st>>>(n, fl.get(), ex.get(), f->lp_list.get()); note_launch();
-        k_forest_summary<<<1, 64, 0, st>>>(n, dcnt.get(), soff.get(), f->lc_start.get(), ex.get(), dph.get()); note_launch();
+        k_forest_summary<<<1, 64, 0, st>>>(n, dcnt.get(), soff.get(), f->lc_start.get(), ex.get(), dph); note_launch();
         HDP_CHECK_LAUNCH();
         // the one host read of steps 5-10: counts and the per-phase table
         std::vector<int32_t> hbuf(C_COUNT + P_ROWS * PH);
         HDP_CHECK_CUDA(cudaMemcpyAsync(hbuf.data(), dcnt.get(), C_COUNT * sizeof(int32_t),
                                        cudaMemcpyDeviceToHost, st));
-        HDP_CHECK_CUDA(cudaMemcpyAsync(hbuf.data() + C_COUNT, dph.get(), P_ROWS * PH * sizeof(int32_t),
+        HDP_CHECK_CUDA(cudaMemcpyAsync(hbuf.data() + C_COUNT, dph, P_ROWS * PH * sizeof(int32_t),
                                        cudaMemcpyDeviceToHost, st));
         HDP_CHECK_CUDA(cudaStreamSynchronize(st));
         const int32_t* hc = hbuf.data();
@@ -1021,6 +936,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         f->n_phases = hc[C_NPH];
         f->max_depth = hc[C_MAXD];
         f->n_segs = hc[C_NSEG];
+        f->n_lc = hc[C_NLC];
         HDP_REQUIRE(f->n_phases >= 1 && f->n_phases <= kMaxPhases, HDP_ERR_INTERNAL,
                     "light depth %lld out of range", (long long)f->n_phases);
         auto row = [&](int k, std::vector<int64_t>& out) {
@@ -1082,12 +998,6 @@ __global__ void k_path_meta(int64_t np, const int32_t* __restrict__ list,
     rows[i] = make_longlong2(r0, par >= 0 ? rowoff[par] : -1);
 }
 
-__global__ void k_gather_i64(int64_t m, const int64_t* __restrict__ src,
-                             const int64_t* __restrict__ idx, int64_t* out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) out[i] = src[idx[i]];
-}
-
 // per short path: shared-memory weight (own rows, light-children rows, a
 // parent row, per-node and per-entry metadata, path metadata) and the size
 // of its parent row (0 at a root)
@@ -1117,34 +1027,44 @@ __global__ void k_lc_m(int64_t nl, const int32_t* __restrict__ lc_list, const in
 }
 
 // chunk_first over the short paths: path i (phase r) starts chunk
-// cbase[r] + ((W[i] - W0[r]) >> kChunkShift); every chunk id up to it that
+// cbase[r] + ((W[i] - W[so[r]]) >> kChunkShift); every chunk id up to it that
 // no earlier path claimed starts at i.
-__global__ void k_chunk_fill(int64_t ns, int nph, const int64_t* __restrict__ soff,
-                             const int64_t* __restrict__ cbase, const int64_t* __restrict__ w0,
-                             const int64_t* __restrict__ W, int32_t* chunk_first) {
+__global__ void k_chunk_fill(int64_t ns, int nph, const int32_t* __restrict__ so,
+                             const int64_t* __restrict__ cbase, const int64_t* __restrict__ W,
+                             int32_t* chunk_first) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ns) return;
-    int lo = 0, hi = nph - 1;  // phase r with soff[r] <= i < soff[r+1]
+    int lo = 0, hi = nph - 1;  // phase r with so[r] <= i < so[r+1]
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
-        if (soff[mid] <= i) lo = mid;
+        if (so[mid] <= i) lo = mid;
         else hi = mid - 1;
     }
     const int r = lo;
-    int64_t c = cbase[r] + ((W[i] - w0[r]) >> kChunkShift);
-    int64_t cp = (i == soff[r]) ? cbase[r] - 1 : cbase[r] + ((W[i - 1] - w0[r]) >> kChunkShift);
+    const int64_t w0 = W[so[r]];
+    int64_t c = cbase[r] + ((W[i] - w0) >> kChunkShift);
+    int64_t cp = (i == so[r]) ? cbase[r] - 1 : cbase[r] + ((W[i - 1] - w0) >> kChunkShift);
     for (int64_t q = cp + 1; q <= c; q++) chunk_first[q] = (int32_t)i;
-    if (i == soff[r + 1] - 1)
+    if (i == so[r + 1] - 1)
         for (int64_t q = c + 1; q < cbase[r + 1]; q++) chunk_first[q] = (int32_t)(i + 1);
 }
 
-__global__ void k_chunk_desc(int64_t nc, const int32_t* __restrict__ chunk_first,
+// chunks per phase from the cumulative weights (one thread; <= 64 phases)
+__global__ void k_chunk_plan(int nph, const int32_t* __restrict__ so, const int64_t* __restrict__ W,
+                             int64_t* cbase, int32_t* chunk_first) {
+    cbase[0] = 0;
+    for (int r = 0; r < nph; r++)
+        cbase[r + 1] = cbase[r] + ((W[so[r + 1]] - W[so[r]] + kChunkWords - 1) >> kChunkShift);
+    chunk_first[cbase[nph]] = so[nph];
+}
+
+__global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const int32_t* __restrict__ chunk_first,
                              const int4* __restrict__ sinfo, const longlong2* __restrict__ srows,
                              const int32_t* __restrict__ lc_start, const int64_t* __restrict__ lc_rowoff,
                              const int64_t* __restrict__ auxd, const int64_t* __restrict__ W,
                              ChunkDesc* desc, unsigned long long* max_words) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= nc) return;
+    if (c >= cbase[nph]) return;
     ChunkDesc d = {};
     int p0 = chunk_first[c], p1 = chunk_first[c + 1];
     d.p0 = p0;
@@ -1174,66 +1094,53 @@ __global__ void k_chunk_desc(int64_t nc, const int32_t* __restrict__ chunk_first
 
 }  // namespace hdp
 
-// chunk table of the short-path blocks (needs lmeta, lc rows and short_rows)
+// chunk table of the short-path blocks (needs lmeta, lc rows and short_rows);
+// one host read (chunks per phase, largest chunk)
 static int build_chunks(hdp_forest* f) {
     cudaStream_t st = f->st;
     const int nph = (int)f->n_phases;
-    const int64_t ns = f->short_off[nph];
-    int32_t n_lc = 0;
-    HDP_TRY(to_host(&n_lc, f->lc_start.get() + f->n, 1, st));
+    const int64_t n = f->n, ns = f->short_off[nph], n_lc = f->n_lc;
     DevBuf<int64_t> wt, W, pm, lcm;
     HDP_TRY(wt.alloc(ns + 1, st));
     HDP_TRY(W.alloc(ns + 1, st));
     HDP_TRY(pm.alloc(ns + 1, st));
-    HDP_TRY(f->auxd.alloc(ns + 1, st));
+    HDP_TRY(f->auxd.alloc(ns + 2, st));
     HDP_TRY(lcm.alloc(n_lc + 1, st));
-    HDP_TRY(f->lc_rowoff.alloc(n_lc + 1, st));
+    HDP_TRY(f->lc_rowoff.alloc(n_lc + 2, st));
     k_chunk_weight<<<grid_for(ns + 1, 256), 256, 0, st>>>(ns, f->short_info.get(), f->short_rows.get(),
                                                           f->lc_start.get(), wt.get(), pm.get()); note_launch();
     k_lc_m<<<grid_for(n_lc + 1, 256), 256, 0, st>>>(n_lc, f->lc_list.get(), f->lmeta.get(), lcm.get()); note_launch();
     HDP_TRY(exclusive_sum(wt.get(), W.get(), ns + 1, st));
     HDP_TRY(exclusive_sum(pm.get(), f->auxd.get(), ns + 1, st));
     HDP_TRY(exclusive_sum(lcm.get(), f->lc_rowoff.get(), n_lc + 1, st));
-    // cumulative weight at every phase boundary
-    std::vector<int64_t> so(f->short_off.begin(), f->short_off.end()), wb(nph + 1);
-    DevBuf<int64_t> dso, dwb, dcb;
-    HDP_TRY(dso.alloc(nph + 1, st));
-    HDP_TRY(dwb.alloc(nph + 1, st));
-    HDP_TRY(dcb.alloc(nph + 1, st));
-    HDP_CHECK_CUDA(cudaMemcpyAsync(dso.get(), so.data(), sizeof(int64_t) * (nph + 1),
-                                   cudaMemcpyHostToDevice, st));
-    k_gather_i64<<<grid_for(nph + 1, 64), 64, 0, st>>>(nph + 1, W.get(), dso.get(), dwb.get()); note_launch();
-    HDP_TRY(to_host(wb.data(), dwb.get(), nph + 1, st));
-    f->chunk_off.assign(nph + 1, 0);
-    for (int r = 0; r < nph; r++)
-        f->chunk_off[r + 1] = f->chunk_off[r] + ((wb[r + 1] - wb[r] + kChunkWords - 1) >> kChunkShift);
-    const int64_t nc = f->chunk_off[nph];
-    HDP_TRY(f->chunk_first.alloc(nc + 1, st));
-    HDP_TRY(f->chunk_desc.alloc(nc + 1, st));
-    int32_t last = (int32_t)ns;
-    HDP_CHECK_CUDA(cudaMemcpyAsync(f->chunk_first.get() + nc, &last, sizeof(int32_t),
-                                   cudaMemcpyHostToDevice, st));
-    f->chunk_words = 0;
-    if (nc > 0) {
-        std::vector<int64_t> cb(f->chunk_off.begin(), f->chunk_off.end());
-        HDP_CHECK_CUDA(cudaMemcpyAsync(dcb.get(), cb.data(), sizeof(int64_t) * (nph + 1),
-                                       cudaMemcpyHostToDevice, st));
-        HDP_CHECK_CUDA(cudaMemcpyAsync(dwb.get(), wb.data(), sizeof(int64_t) * (nph + 1),
-                                       cudaMemcpyHostToDevice, st));
-        k_chunk_fill<<<grid_for(ns, 256), 256, 0, st>>>(ns, nph, dso.get(), dcb.get(), dwb.get(), W.get(),
+    // chunk-count bound: every short path weighs at most (len + nlc + 1)(mp + 16)
+    const int64_t mp = (f->max_m + 3) & ~3;
+    const int64_t ncap = (((n + n_lc + ns) * (mp + 16)) >> kChunkShift) + nph + 2;
+    const int32_t* so = f->dph.get() + P_SHORT * (kMaxPhases + 1);
+    DevBuf<int64_t> cbase, hsum;  // hsum = (chunk bases..., largest chunk)
+    DevBuf<unsigned long long> mx;
+    HDP_TRY(cbase.alloc(nph + 1, st));
+    HDP_TRY(mx.alloc(1, st));
+    HDP_TRY(f->chunk_first.alloc(ncap + 1, st));
+    HDP_TRY(f->chunk_desc.alloc(ncap + 1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), st));
+    k_chunk_plan<<<1, 1, 0, st>>>(nph, so, W.get(), cbase.get(), f->chunk_first.get()); note_launch();
+    if (ns > 0)
+        k_chunk_fill<<<grid_for(ns, 256), 256, 0, st>>>(ns, nph, so, cbase.get(), W.get(),
                                                         f->chunk_first.get()); note_launch();
-        DevBuf<unsigned long long> mx;
-        HDP_TRY(mx.alloc(1, st));
-        HDP_CHECK_CUDA(cudaMemsetAsync(mx.get(), 0, sizeof(unsigned long long), st));
-        k_chunk_desc<<<grid_for(nc, 256), 256, 0, st>>>(nc, f->chunk_first.get(), f->short_info.get(),
-                                                        f->short_rows.get(), f->lc_start.get(),
-                                                        f->lc_rowoff.get(), f->auxd.get(), W.get(),
-                                                        f->chunk_desc.get(), mx.get()); note_launch();
-        HDP_CHECK_LAUNCH();
-        unsigned long long words = 0;
-        HDP_TRY(to_host(&words, mx.get(), 1, st));  // also orders the pageable copies above
-        f->chunk_words = (int64_t)words + 64;
-    }
+    k_chunk_desc<<<grid_for(ncap, 256), 256, 0, st>>>(cbase.get(), nph, f->chunk_first.get(), f->short_info.get(),
+                                                      f->short_rows.get(), f->lc_start.get(),
+                                                      f->lc_rowoff.get(), f->auxd.get(), W.get(),
+                                                      f->chunk_desc.get(), mx.get()); note_launch();
+    HDP_CHECK_LAUNCH();
+    std::vector<int64_t> h(nph + 2);
+    HDP_CHECK_CUDA(cudaMemcpyAsync(h.data(), cbase.get(), sizeof(int64_t) * (nph + 1), cudaMemcpyDeviceToHost, st));
+    HDP_CHECK_CUDA(cudaMemcpyAsync(h.data() + nph + 1, mx.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HDP_CHECK_CUDA(cudaStreamSynchronize(st));
+    HDP_REQUIRE(h[nph] <= ncap, HDP_ERR_INTERNAL, "chunk count %lld above its bound %lld", (long long)h[nph],
+                (long long)ncap);
+    f->chunk_off.assign(h.begin(), h.begin() + nph + 1);
+    f->chunk_words = h[nph] > 0 ? h[nph + 1] + 64 : 0;
     // rows of up to 32 float4 lanes: one lane group spans a row; wider rows
     // take the per-path kernels (lane groups across CTAs)
     f->chunks_ok = f->chunk_words <= kChunkMaxWords && f->max_m <= 128;
@@ -1244,7 +1151,15 @@ static int build_chunks(hdp_forest* f) {
     return HDP_OK;
 }
 
-static int lanes_finish(hdp_forest* f) {
+__global__ void k_lane_totals(int64_t n, const int64_t* __restrict__ nodeoff, const int64_t* __restrict__ rowoff,
+                              const int32_t* __restrict__ mx, int64_t* out) {
+    out[0] = nodeoff[n];
+    out[1] = rowoff[n];
+    out[2] = mx[0];
+}
+
+// uniform_m > 0: every tree has exactly that many lanes (totals known here)
+static int lanes_finish(hdp_forest* f, int uniform_m) {
     cudaStream_t st = f->st;
     Tracer tr(st);
     const int B = 256;
@@ -1261,17 +1176,25 @@ static int lanes_finish(hdp_forest* f) {
     k_node_m<<<grid_for(n, B), B, 0, st>>>(n, f->tree_id.get(), f->t_m.get(), nm.get()); note_launch();
     HDP_TRY(exclusive_sum(nm.get(), f->nodeoff.get(), n + 1, st));
     HDP_CHECK_LAUNCH();
-    HDP_TRY(to_host(&f->total_entries, f->nodeoff.get() + n, 1, st));
-    HDP_TRY(to_host(&f->total_rows, f->rowoff.get() + n, 1, st));
-    DevBuf<int32_t> mx;
-    HDP_TRY(mx.alloc(1, st));
-    HDP_TRY(reduce_max(f->t_m.get(), mx.get(), f->n_trees, st));
-    int32_t hm = 0;
-    HDP_TRY(to_host(&hm, mx.get(), 1, st));
-    f->max_m = hm;
+    if (uniform_m > 0) {
+        f->max_m = uniform_m;
+        f->total_entries = n * (int64_t)uniform_m;
+        f->total_rows = n * (int64_t)((uniform_m + 3) & ~3);
+    } else {
+        DevBuf<int32_t> mx;
+        DevBuf<int64_t> tot;
+        HDP_TRY(mx.alloc(1, st));
+        HDP_TRY(tot.alloc(3, st));
+        HDP_TRY(reduce_max(f->t_m.get(), mx.get(), f->n_trees, st));
+        k_lane_totals<<<1, 1, 0, st>>>(n, f->nodeoff.get(), f->rowoff.get(), mx.get(), tot.get()); note_launch();
+        int64_t ht[3] = {0, 0, 0};
+        HDP_TRY(to_host(ht, tot.get(), 3, st));
+        f->total_entries = ht[0];
+        f->total_rows = ht[1];
+        f->max_m = (int)ht[2];
+    }
     // packed metadata for the aggregation kernels
-    int32_t n_lc = 0;
-    HDP_TRY(to_host(&n_lc, f->lc_start.get() + n, 1, st));
+    const int64_t n_lc = f->n_lc;
     HDP_TRY(f->lmeta.alloc(n, st));
     HDP_TRY(f->lsimf.alloc(n, st));
     HDP_TRY(f->lc_row.alloc(n_lc + 1, st));
@@ -1370,7 +1293,7 @@ int hdp_forest_set_lanes_range(hdp_forest* f, int x0, int nx, void* stream) {
     HDP_CHECK_LAUNCH();
     f->range_x0 = x0;
     f->max_d = x0 + nx - 1;
-    return lanes_finish(f);
+    return lanes_finish(f, nx);
 }
 
 int hdp_forest_set_lanes(hdp_forest* f, const uint32_t* tree_masks, int nw, void* stream) {
@@ -1404,7 +1327,7 @@ int hdp_forest_set_lanes(hdp_forest* f, const uint32_t* tree_masks, int nw, void
         HDP_TRY(to_host(&h, mn.get(), 1, st));
         HDP_REQUIRE(h >= 1, HDP_ERR_INTERNAL, "a tree has an empty disparity interval");
     }
-    return lanes_finish(f);
+    return lanes_finish(f, 0);
 }
 
 int hdp_forest_entries(hdp_forest* f, int64_t* total, int64_t* node_offsets, void* stream) {

@@ -69,6 +69,8 @@ struct hdp_forest {
     std::vector<int64_t> long_off, short_off;
     std::vector<int64_t> short_end;  // host: short paths of phase r occupy positions [phase_node[r], short_end[r])
     std::vector<int64_t> lp_mid;     // host: light parents on long paths of phase r = [lp_mid[r], lp_off[r+1])
+    hdp::DevBuf<int32_t> dph;        // device copy of the per-phase tables (forest.cu P_* rows)
+    int64_t n_lc = 0;                // light-child entries
     hdp::DevBuf<int2> seg_tab;      // (long-path index, segment index from the head)
     std::vector<int64_t> seg_off;   // host: segments of phase r = [seg_off[r], seg_off[r+1])
     int64_t n_segs = 0;
