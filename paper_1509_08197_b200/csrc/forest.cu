@@ -337,6 +337,61 @@ __global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
     idx[v] = (int32_t)v;
 }
 
+// light depth of every node (scan of the light-edge tour steps)
+__global__ void k_light_depth(int64_t n, const int32_t* __restrict__ down_arc, const int32_t* __restrict__ lscan,
+                              int32_t* ld_out) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t a = down_arc[v];
+    ld_out[v] = a >= 0 ? lscan[a] : 0;
+}
+
+__global__ void k_head_flags(int64_t n, const int32_t* __restrict__ head, int32_t* hf) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) hf[v] = head[v] == v ? 1 : 0;
+    else if (v == n) hf[v] = 0;
+}
+
+// heads in ascending id with their layout class (light depth, long path)
+__global__ void k_head_keys(int64_t n, const int32_t* __restrict__ hf, const int32_t* __restrict__ hpos,
+                            const int32_t* __restrict__ ld, const int32_t* __restrict__ plen,
+                            uint8_t* hkey, int32_t* hval) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n || !hf[v]) return;
+    const int32_t i = hpos[v];
+    hkey[i] = (uint8_t)((ld[v] << 1) | (plen[v] > kShortPath ? 1 : 0));
+    hval[i] = (int32_t)v;
+}
+
+__global__ void k_head_lens(int64_t n, const int32_t* __restrict__ hpos, const int32_t* __restrict__ sorted,
+                            const int32_t* __restrict__ plen, int32_t* slen, int32_t* hrank) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int32_t nh = hpos[n];
+    if (i < nh) {
+        const int32_t h = sorted[i];
+        slen[i] = plen[h];
+        hrank[h] = (int32_t)i;
+    } else {
+        slen[i] = 0;
+    }
+}
+
+// layout position = first position of the node's path + distance from its head
+__global__ void k_layout_place(int64_t n, const int32_t* __restrict__ head, const int32_t* __restrict__ dist,
+                               const int32_t* __restrict__ hrank, const int32_t* __restrict__ pbase,
+                               const float* __restrict__ pweight, float gamma, int32_t* lnode, int32_t* lpos,
+                               float* lsim) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int32_t k = pbase[hrank[head[v]]] + dist[v];
+    lnode[k] = (int32_t)v;
+    lpos[v] = k;
+    // RootedForest.similarities (spanning_forest.py:184-188) in float64,
+    // rounded once to the f32 the aggregation runs in.
+    lsim[k] = (float)exp(-(double)pweight[v] / ((double)gamma * 255.0));
+}
+
 __global__ void k_lp_flags(int64_t n, const int32_t* __restrict__ lc_start, int32_t* fl) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) fl[k] = lc_start[k + 1] > lc_start[k] ? 1 : 0;
@@ -804,30 +859,43 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                     steps.get()); note_launch();
         HDP_TRY(inclusive_sum(steps.get(), scanned.get(), na, st));
     }
-    DevBuf<uint64_t> lkey, lkey2;
-    DevBuf<int32_t> lidx;
-    HDP_TRY(lkey.alloc(n, st));
-    HDP_TRY(lkey2.alloc(n, st));
-    HDP_TRY(lidx.alloc(n, st));
+    // Layout order (light depth, long path, head id, distance from the head):
+    // a stable 8-bit sort of the heads (already in id order) by (light depth,
+    // long), a prefix sum of their path lengths, and every node lands at its
+    // path's base + its distance from the head.
     HDP_TRY(f->lnode.alloc(n, st));
-    int dbits = bits_for(max_tree), hbits = bits_for(n);  // distance from a head < tree size
-    // light depth <= log2(n) + 1 < 64 needs 6 bits, the long flag one more
-    HDP_REQUIRE(hbits + dbits <= 57, HDP_ERR_CONFIG, "forest too large for the layout key");
+    HDP_TRY(f->lpos.alloc(n, st));
+    HDP_TRY(f->lsim.alloc(n, st));
+    k_light_depth<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), ld.get()); note_launch();
     {
-        DevBuf<int32_t> plen;
+        DevBuf<int32_t> plen, hf, hpos, hval, hsorted, slen, pbase, hrank;
+        DevBuf<uint8_t> hkey, hkey2;
         HDP_TRY(plen.alloc(n, st));
+        HDP_TRY(hf.alloc(n + 1, st));
+        HDP_TRY(hpos.alloc(n + 1, st));
+        HDP_TRY(hval.alloc(n, st));
+        HDP_TRY(hsorted.alloc(n, st));
+        HDP_TRY(slen.alloc(n + 1, st));
+        HDP_TRY(pbase.alloc(n + 1, st));
+        HDP_TRY(hrank.alloc(n, st));
+        HDP_TRY(hkey.alloc(n, st));
+        HDP_TRY(hkey2.alloc(n, st));
         HDP_CHECK_CUDA(cudaMemsetAsync(plen.get(), 0, n * sizeof(int32_t), st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(hkey.get(), 0xff, n, st));  // non-heads sort last
         k_path_len<<<grid_for(n, B), B, 0, st>>>(n, head, dist.get(), plen.get()); note_launch();
-        k_layout_keys<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), head, dist.get(),
-                                                    plen.get(), lkey.get(), lidx.get(), ld.get(),
-                                                    hbits, dbits); note_launch();
+        k_head_flags<<<grid_for(n + 1, B), B, 0, st>>>(n, head, hf.get()); note_launch();
+        HDP_TRY(exclusive_sum(hf.get(), hpos.get(), n + 1, st));
+        k_head_keys<<<grid_for(n, B), B, 0, st>>>(n, hf.get(), hpos.get(), ld.get(), plen.get(), hkey.get(),
+                                                  hval.get()); note_launch();
+        HDP_TRY(sort_pairs(hkey.get(), hkey2.get(), hval.get(), hsorted.get(), n, 0, 8, st));
+        k_head_lens<<<grid_for(n + 1, B), B, 0, st>>>(n, hpos.get(), hsorted.get(), plen.get(), slen.get(),
+                                                      hrank.get()); note_launch();
+        HDP_TRY(exclusive_sum(slen.get(), pbase.get(), n + 1, st));
+        k_layout_place<<<grid_for(n, B), B, 0, st>>>(n, head, dist.get(), hrank.get(), pbase.get(),
+                                                     f->pweight.get(), f->gamma, f->lnode.get(), f->lpos.get(),
+                                                     f->lsim.get()); note_launch();
         HDP_CHECK_LAUNCH();
     }
-    HDP_TRY(sort_pairs(lkey.get(), lkey2.get(), lidx.get(), f->lnode.get(), n, 0,
-                       std::min(64, dbits + hbits + 7), st));
-    lkey.release();
-    lkey2.release();
-    lidx.release();
     steps.release();
     scanned.release();
     tpos.release();
@@ -835,10 +903,6 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     tlen.release();
     down_arc.release();
     asrc.release();
-    HDP_TRY(f->lpos.alloc(n, st));
-    HDP_TRY(f->lsim.alloc(n, st));
-    k_layout_pos<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), f->pweight.get(), f->gamma,
-                                               f->lpos.get(), f->lsim.get()); note_launch();
 
     tr.mark("7 layout sort");
     // ---- 8. paths and phases (sizes bounded by n; counts stay on the device)
