@@ -165,24 +165,28 @@ __global__ void k_tour_next(int64_t na, const int32_t* __restrict__ asrc,
     next[i] = nx;
 }
 
+// Pointer jumping on packed words (pointer << 32 | count), ping-pong between
+// two buffers; the host launches an upper bound of rounds (a convergence flag
+// costs more than the rounds it saves: every block of the first waves writes it).
 // list words: (next << 32 | rank), next = -1 at a list's end
 __global__ void k_rank_init(int64_t na, const int32_t* __restrict__ next, uint64_t* word) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < na) word[i] = ((uint64_t)(uint32_t)next[i] << 32) | 1u;
 }
 
-// Wyllie pointer jumping on packed words (one random 8-byte load per arc and
-// round): rank = number of arcs from i to the end of its list.
+// Wyllie pointer jumping in place (see jump_done): rank = number of arcs
+// from i to the end of its list.
 __global__ void k_rank_jump(int64_t na, const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    const uint64_t w = in[i];
-    const int32_t nx = (int32_t)(w >> 32);
-    if (nx >= 0) {
-        const uint64_t w2 = in[nx];
-        out[i] = (w2 & 0xffffffff00000000ull) | (uint32_t)((uint32_t)w + (uint32_t)w2);
-    } else {
-        out[i] = w;
+    if (i < na) {
+        const uint64_t w = in[i];
+        const int32_t nx = (int32_t)(w >> 32);
+        if (nx >= 0) {
+            const uint64_t w2 = in[nx];
+            out[i] = (w2 & 0xffffffff00000000ull) | (uint32_t)((uint32_t)w + (uint32_t)w2);
+        } else {
+            out[i] = w;
+        }
     }
 }
 
@@ -270,29 +274,37 @@ __global__ void k_heavy(int64_t n, const int32_t* __restrict__ adj_start,
     heavy[x] = best;
 }
 
+// heavy-path heads: word = (heavy parent or self, distance)
 __global__ void k_hp_init(int64_t n, const int32_t* __restrict__ parent,
-                          const int32_t* __restrict__ heavy, int32_t* hp, int32_t* dist) {
+                          const int32_t* __restrict__ heavy, uint64_t* word) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     int32_t p = parent[v];
     bool on = (p != v) && heavy[p] == v;
-    hp[v] = on ? p : (int32_t)v;
-    dist[v] = on ? 1 : 0;
+    word[v] = ((uint64_t)(uint32_t)(on ? p : (int32_t)v) << 32) | (on ? 1u : 0u);
 }
 
-__global__ void k_hp_jump(int64_t n, const int32_t* __restrict__ hp_in,
-                          const int32_t* __restrict__ d_in, int32_t* hp_out, int32_t* d_out) {
+__global__ void k_hp_jump(int64_t n, const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) {
+        const uint64_t w = in[v];
+        const int32_t h = (int32_t)(w >> 32);
+        const uint64_t w2 = in[h];
+        const int32_t hh = (int32_t)(w2 >> 32);
+        if (hh != h) {
+            out[v] = ((uint64_t)(uint32_t)hh << 32) | (uint32_t)((uint32_t)w + (uint32_t)w2);
+        } else {
+            out[v] = w;
+        }
+    }
+}
+
+__global__ void k_hp_unpack(int64_t n, const uint64_t* __restrict__ word, int32_t* hp, int32_t* dist) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    int32_t h = hp_in[v];
-    int32_t hh = hp_in[h];
-    if (hh != h) {
-        hp_out[v] = hh;
-        d_out[v] = d_in[v] + d_in[h];
-    } else {
-        hp_out[v] = h;
-        d_out[v] = d_in[v];
-    }
+    const uint64_t w = word[v];
+    hp[v] = (int32_t)(w >> 32);
+    dist[v] = (int32_t)(uint32_t)w;
 }
 
 // light-edge steps for the light-depth scan: entering / leaving a path head.
@@ -780,9 +792,9 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         DevBuf<uint64_t> wa, wb;
         HDP_TRY(wa.alloc(na, st));
         HDP_TRY(wb.alloc(na, st));
-        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), wa.get()); note_launch();
         // the longest list is the largest tree's tour, 2 (size - 1) arcs
-        int rounds = ceil_log2(2 * (int64_t)max_tree);
+        const int rounds = ceil_log2(2 * (int64_t)max_tree);
+        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), wa.get()); note_launch();
         for (int r = 0; r < rounds; r++) {
             k_rank_jump<<<grid_for(na, B), B, 0, st>>>(na, wa.get(), wb.get()); note_launch();
             std::swap(wa.p, wb.p);
@@ -826,27 +838,26 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
 
     tr.mark("5 orient/depth");
     // ---- 6. heavy paths
-    DevBuf<int32_t> heavy, hp, hp2, dist, dist2;
+    DevBuf<int32_t> heavy, hp, dist;
     HDP_TRY(heavy.alloc(n, st));
     HDP_TRY(hp.alloc(n, st));
-    HDP_TRY(hp2.alloc(n, st));
     HDP_TRY(dist.alloc(n, st));
-    HDP_TRY(dist2.alloc(n, st));
     k_heavy<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), adst.get(), f->parent.get(),
                                           f->size.get(), heavy.get()); note_launch();
-    k_hp_init<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), hp.get(), dist.get()); note_launch();
     {
-        int rounds = ceil_log2((int64_t)max_tree + 1);  // depth < the largest tree
+        DevBuf<uint64_t> hw, hw2;
+        const int rounds = ceil_log2((int64_t)max_tree + 1);  // depth < the largest tree
+        HDP_TRY(hw.alloc(n, st));
+        HDP_TRY(hw2.alloc(n, st));
+        k_hp_init<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), hw.get()); note_launch();
         for (int r = 0; r < rounds; r++) {
-            k_hp_jump<<<grid_for(n, B), B, 0, st>>>(n, hp.get(), dist.get(), hp2.get(), dist2.get()); note_launch();
-            std::swap(hp.p, hp2.p);
-            std::swap(dist.p, dist2.p);
+            k_hp_jump<<<grid_for(n, B), B, 0, st>>>(n, hw.get(), hw2.get()); note_launch();
+            std::swap(hw.p, hw2.p);
         }
+        k_hp_unpack<<<grid_for(n, B), B, 0, st>>>(n, hw.get(), hp.get(), dist.get()); note_launch();
     }
     HDP_CHECK_LAUNCH();
     heavy.release();
-    hp2.release();
-    dist2.release();
     int32_t* head = hp.get();
 
     tr.mark("6 heavy paths");

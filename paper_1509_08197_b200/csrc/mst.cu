@@ -87,8 +87,8 @@ __global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ eu, const int3
             }
         }
     }
-    // "another round is needed": one flag write per warp, and only while unset
-    if (__ballot_sync(0xffffffffu, hooked) && (threadIdx.x & 31) == 0 && *(volatile int*)hooks == 0) *hooks = 1;
+    // "another round is needed": one guarded flag write per block
+    if (__syncthreads_or(hooked) && threadIdx.x == 0 && *(volatile int*)hooks == 0) *hooks = 1;
 }
 
 __global__ void k_mst_relabel(int64_t n, int32_t* __restrict__ comp, const int32_t* __restrict__ link,
