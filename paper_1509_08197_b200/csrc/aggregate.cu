@@ -303,34 +303,32 @@ __global__ void __launch_bounds__(256) k_ecost_pix(AggArgs a, const int32_t* __r
 
 // b(v) += sum_{light children c} s_c A_up(c) for the phase's light parents
 // (children in ascending id order, their A_up final since the deeper phase).
-// PU parents per thread; the first child of each is gathered up front.
+// One `qsub`-lane group per parent, float4 columns; the parent's metadata and
+// its first child's row are fetched before the remaining children are walked.
 __global__ void __launch_bounds__(256) k_light(AggArgs a, int64_t p0, int64_t np) {
-    Slot s = slot_of(a);
-    int32_t k[4], c0[4], c1[4];
-    int m[4];
-    bool ok[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-        int64_t it = s.item * 4 + u;
-        ok[u] = it < np;
-        k[u] = ok[u] ? a.lp_list[p0 + it] : 0;
-        m[u] = a.lmeta[k[u]].w;
-        c0[u] = a.lc_start[k[u]];
-        c1[u] = a.lc_start[k[u] + 1];
-        ok[u] = ok[u] && s.j < m[u];
-    }
-    float first[4], bv[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-        first[u] = ok[u] ? a.lc_sim[c0[u]] * a.aup[a.lc_row[c0[u]] + s.j] : 0.0f;
-        bv[u] = ok[u] ? a.aup[a.rowoff[k[u]] + s.j] : 0.0f;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-        if (!ok[u]) continue;
-        float x = first[u];
-        for (int32_t q = c0[u] + 1; q < c1[u]; q++) x += a.lc_sim[q] * a.aup[a.lc_row[q] + s.j];
-        a.aup[a.rowoff[k[u]] + s.j] = bv[u] + x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t it = t >> a.qsub_shift;
+    const int sl = (int)(t & (a.qsub - 1));
+    if (it >= np) return;
+    const int32_t k = a.lp_list[p0 + it];
+    const int m = a.lmeta[k].w, mq = (m + 3) >> 2;
+    const int32_t c0 = a.lc_start[k], c1 = a.lc_start[k + 1];
+    float4* row = reinterpret_cast<float4*>(a.aup + a.rowoff[k]);
+    const float s0 = a.lc_sim[c0];
+    const float4* r0 = reinterpret_cast<const float4*>(a.aup + a.lc_row[c0]);
+    for (int jq = sl; jq < mq; jq += a.qsub) {
+        const float4 v0 = r0[jq];
+        const float4 bv = row[jq];
+        float4 x = make_float4(s0 * v0.x, s0 * v0.y, s0 * v0.z, s0 * v0.w);
+        for (int32_t q = c0 + 1; q < c1; q++) {
+            const float sq = a.lc_sim[q];
+            const float4 v = reinterpret_cast<const float4*>(a.aup + a.lc_row[q])[jq];
+            x.x += sq * v.x;
+            x.y += sq * v.y;
+            x.z += sq * v.z;
+            x.w += sq * v.w;
+        }
+        row[jq] = make_float4(bv.x + x.x, bv.y + x.y, bv.z + x.z, bv.w + x.w);
     }
 }
 
@@ -1383,7 +1381,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
             k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0); note_launch();
         }
         if (np > 0) {
-            k_light<<<packed_grid(a, (np + 3) / 4, 1, 256), 256, 0, st>>>(a, p0, np); note_launch();
+            k_light<<<grid_for(np << a.qsub_shift, 256), 256, 0, st>>>(a, p0, np); note_launch();
         }
         if (ng > 0) {
             k_seg_up<<<dim3(grid_for(ng * 32, 32 * kSegWarps), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
