@@ -117,6 +117,17 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def agg_traffic():
+    """DRAM bytes per aggregation call from the committed ncu --set full capture
+    (profiles/r01_aggregate_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_aggregate_traffic.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["bytes_per_call"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def hbm_peak():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -283,7 +294,7 @@ def run_ours(args):
     algo_bytes = 8 * entries + 30 * nodes  # 8 B/hypothesis + 30 B/pixel
     achieved = algo_bytes / t_agg / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+            "frac": achieved / peak, "traffic": agg_traffic(), "peak_kind": peak_kind,
             "kernel": "hdp_aggregate_wta (fused cost + up/down passes + WTA, one call)",
             "kernel_ms": t_agg * 1e3, "algorithmic_bytes": algo_bytes}
     cpu = None
