@@ -89,6 +89,7 @@ constexpr int DR_THREADS = 1024;
 constexpr int DR_MAXS = 64;      // roots the multi-commit leader can absorb per round
 constexpr int DR_SCAN = 1024;    // window edges the leader may inspect per round
 constexpr int DR_HASH = 256;     // shared-memory hash set of the leader's roots
+constexpr int DR_NW = 8;         // mask words per root staged in shared memory (d_max < 256)
 
 __device__ __forceinline__ unsigned dr_hash(int32_t x) {
     return ((unsigned)x * 2654435761u) >> 24;  // top 8 bits
@@ -156,11 +157,24 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
     __shared__ uint8_t s_dec[DR_THREADS];
     __shared__ int32_t s_hash[DR_HASH];
     __shared__ unsigned long long s_best;
+    // per window edge: reservation stamps and masks of both (round-start)
+    // roots, staged for the multi-commit walk after the parallel commits
+    extern __shared__ unsigned long long s_dyn[];  // dynamic: DrStage
+    unsigned long long (*s_res)[DR_THREADS] = reinterpret_cast<unsigned long long (*)[DR_THREADS]>(s_dyn);
+    uint32_t (*s_msk)[DR_THREADS * DR_NW] =
+        reinterpret_cast<uint32_t (*)[DR_THREADS * DR_NW]>(s_dyn + 2 * DR_THREADS);
     int b = blockIdx.x;
     int tid = threadIdx.x;
     int lane = tid & 31, wid = tid >> 5;
     int32_t head = seg[b], end = seg[b + 1];
     unsigned int round = 0;
+#ifdef HDP_DR_PROFILE
+    long long t_ph[6] = {0, 0, 0, 0, 0, 0};
+    long long t0 = clock64(), t1;
+#define DR_TICK(k) do { __syncthreads(); t1 = clock64(); t_ph[k] += t1 - t0; t0 = t1; } while (0)
+#else
+#define DR_TICK(k) do { } while (0)
+#endif
     while (head < end) {
         int32_t win = min((int32_t)DR_THREADS, end - head);
         bool pend = tid < win;
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
             s_rb[tid] = rb;
             s_e[tid] = e;
         }
-        __syncthreads();
+        DR_TICK(0);
         if (pend && !decided) {
             unsigned long long xa = *((volatile unsigned long long*)&res[ra]);
             unsigned long long xb = *((volatile unsigned long long*)&res[rb]);
@@ -196,9 +210,19 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
             }
         }
         if (pend) s_dec[tid] = decided ? 1 : 0;
-        __syncthreads();
+        DR_TICK(1);
         if (leader) atomicMax(&s_best, ((unsigned long long)usz[keep] << 32) | (unsigned)tid);
-        __syncthreads();
+        if (pend && !decided) {
+            // neither changes during the walk: only the giant's own mask
+            // (held in registers) and uf/usz are written there
+            s_res[0][tid] = *((volatile unsigned long long*)&res[ra]);
+            s_res[1][tid] = *((volatile unsigned long long*)&res[rb]);
+            for (int k = 0; k < nw; k++) {
+                s_msk[0][tid * DR_NW + k] = tm[(int64_t)ra * nw + k];
+                s_msk[1][tid * DR_NW + k] = tm[(int64_t)rb * nw + k];
+            }
+        }
+        DR_TICK(2);
         // multi-commit for the largest merged tree of the round (the giant
         // whose edges would otherwise be decided one per round), by warp 0
         if (wid == 0 && s_best != 0ull) {
@@ -234,8 +258,10 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
                         continue;
                     }
                     int32_t y = qa ? __shfl_sync(0xffffffffu, gb, q) : __shfl_sync(0xffffffffu, ga, q);
-                    unsigned long long xy = *((volatile unsigned long long*)&res[y]);
-                    uint32_t ty = lane < nw ? tm[(int64_t)y * nw + lane] : 0u;
+                    // the other root's stamp and mask, staged by the whole CTA
+                    const int sb = qa ? 1 : 0;
+                    const unsigned long long xy = s_res[sb][gq];
+                    const uint32_t ty = lane < nw ? s_msk[sb][gq * DR_NW + lane] : 0u;
                     if (xy != dr_stamp(round, gq)) {  // y has an earlier pending edge
                         stop = true;
                         break;
@@ -266,7 +292,7 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
             }
             if (grew && lane < nw) tm[(int64_t)root * nw + lane] = tmk;
         }
-        __syncthreads();
+        DR_TICK(3);
         // stable compaction of the undecided window edges
         bool keepme = pend && !s_dec[tid];
         unsigned bal = __ballot_sync(0xffffffffu, keepme);
@@ -291,9 +317,15 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
         }
         head = new_head;
         round++;
-        __syncthreads();
+        DR_TICK(4);
     }
     if (tid == 0) atomicMax(rounds_out, (int)round);
+#ifdef HDP_DR_PROFILE
+    if (tid == 0 && b == 0)
+        printf("[dr] rounds %u  cycles/round: find+reserve %.0f  check+commit %.0f  best %.0f  multi %.0f  compact %.0f\n",
+               round, (double)t_ph[0] / round, (double)t_ph[1] / round, (double)t_ph[2] / round,
+               (double)t_ph[3] / round, (double)t_ph[4] / round);
+#endif
 }
 
 __global__ void k_uf_final(int64_t n, int32_t* uf, int nw, const uint32_t* __restrict__ tm,
@@ -365,7 +397,9 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
     k_uf_init<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
                                             uf.get(), usz.get(), tm.get(), res.get()); note_launch();
     HDP_CHECK_LAUNCH();
-    k_dr<<<batch, DR_THREADS, 0, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(),
+    constexpr size_t dr_smem = 2 * DR_THREADS * sizeof(unsigned long long) + 2 * DR_THREADS * DR_NW * sizeof(uint32_t);
+    HDP_CHECK_CUDA(cudaFuncSetAttribute(k_dr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dr_smem));
+    k_dr<<<batch, DR_THREADS, dr_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(),
                                        res.get(), nw, beta, in_tree, rounds.get()); note_launch();
     HDP_CHECK_LAUNCH();
     k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks); note_launch();
