@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
     long long t0 = clock64(), t1;
 #define DR_TICK(k) do { __syncthreads(); t1 = clock64(); t_ph[k] += t1 - t0; t0 = t1; } while (0)
 #else
-#define DR_TICK(k) do { } while (0)
+#define DR_TICK(k) __syncthreads()  // the round's phase barriers (timed in profile builds)
 #endif
     while (head < end) {
         int32_t win = min((int32_t)DR_THREADS, end - head);

@@ -12,7 +12,12 @@
 // relabelled by following hook chains.  Self-loops die.  HBM/L2-atomic bound.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
 #include "common.cuh"
+#include "prims.cuh"
 
 namespace hdp {
 
@@ -26,10 +31,16 @@ __global__ void k_mst_init(int64_t n, int32_t* comp) {
 // nothing once a round has made no hooks (the forest is final).
 __device__ __forceinline__ bool converged(const int* prev) { return prev && *prev == 0; }
 
-__global__ void k_mst_reset(int64_t n, unsigned long long* best, int32_t* win, const int* prev) {
+// `nodes` (optional): the representative list of the contracted phase; node
+// kernels then run over it instead of 0..n-1.
+__device__ __forceinline__ int64_t node_at(const int32_t* nodes, int64_t t) { return nodes ? nodes[t] : t; }
+
+__global__ void k_mst_reset(int64_t n, unsigned long long* best, int32_t* win, const int* prev,
+                            const int32_t* __restrict__ nodes) {
     if (converged(prev)) return;
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < n) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) {
+        const int64_t v = node_at(nodes, t);
         best[v] = ~0ull;
         win[v] = -1;
     }
@@ -64,26 +75,31 @@ __global__ void k_mst_win(int64_t m, const int32_t* __restrict__ eu, const int32
     if (best[cv] == k) win[cv] = (int32_t)e;
 }
 
+// eidx (optional): original edge index of each contracted edge
 __global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                            const int32_t* __restrict__ comp, const int32_t* __restrict__ win,
                            int32_t* __restrict__ link, uint8_t* __restrict__ in_tree,
-                           int* __restrict__ hooks, const int* prev) {
+                           int* __restrict__ hooks, const int* prev, const int32_t* __restrict__ nodes,
+                           const int32_t* __restrict__ eidx) {
     if (converged(prev)) return;
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool hooked = false;
-    if (v < n && comp[v] == v) {  // representatives only
-        int32_t e = win[v];
-        if (e < 0) {
-            link[v] = (int32_t)v;
-        } else {
-            int32_t a = comp[eu[e]], b = comp[ev[e]];
-            int32_t other = (a == v) ? b : a;
-            in_tree[e] = 1;
-            if (win[other] == e && v < other) {
-                link[v] = (int32_t)v;  // mutual minimum: the lower id stays the root
+    if (t < n) {
+        const int64_t v = node_at(nodes, t);
+        if (comp[v] == v) {  // representatives only
+            int32_t e = win[v];
+            if (e < 0) {
+                link[v] = (int32_t)v;
             } else {
-                link[v] = other;
-                hooked = true;
+                int32_t a = comp[eu[e]], b = comp[ev[e]];
+                int32_t other = (a == v) ? b : a;
+                in_tree[eidx ? eidx[e] : e] = 1;
+                if (win[other] == e && v < other) {
+                    link[v] = (int32_t)v;  // mutual minimum: the lower id stays the root
+                } else {
+                    link[v] = other;
+                    hooked = true;
+                }
             }
         }
     }
@@ -92,66 +108,168 @@ __global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ eu, const int3
 }
 
 __global__ void k_mst_relabel(int64_t n, int32_t* __restrict__ comp, const int32_t* __restrict__ link,
-                              const int* prev) {
+                              const int* prev, const int32_t* __restrict__ nodes) {
     if (converged(prev)) return;
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int64_t v = node_at(nodes, t);
     int32_t r = comp[v];
     while (link[r] != r) r = link[r];
     comp[v] = r;
 }
 
+// ---- contraction between the two phases: edges between distinct components
+// with endpoints relabelled to their representatives, and the representative
+// list.  Counts land in cnt[0] (edges), cnt[1] (representatives).
+__global__ void k_mst_cflags(int64_t m, int64_t n, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                             const int32_t* __restrict__ comp, int32_t* ef, int32_t* vf) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) ef[i] = comp[eu[i]] != comp[ev[i]] ? 1 : 0;
+    else if (i == m) ef[i] = 0;
+    if (i < n) vf[i] = comp[i] == i ? 1 : 0;
+    else if (i == n) vf[i] = 0;
+}
+
+__global__ void k_mst_counts(int64_t m, int64_t n, const int32_t* __restrict__ epos, const int32_t* __restrict__ vpos,
+                             int* cnt) {
+    cnt[0] = epos[m];
+    cnt[1] = vpos[n];
+}
+
+__global__ void k_mst_contract(int64_t m, int64_t n, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                               const uint64_t* __restrict__ key, const int32_t* __restrict__ comp,
+                               const int32_t* __restrict__ ef, const int32_t* __restrict__ epos,
+                               const int32_t* __restrict__ vf, const int32_t* __restrict__ vpos, int32_t* cu,
+                               int32_t* cv, uint64_t* ckey, int32_t* cidx, int32_t* reps) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m && ef[i]) {
+        const int32_t p = epos[i];
+        cu[p] = comp[eu[i]];
+        cv[p] = comp[ev[i]];
+        ckey[p] = key[i];
+        cidx[p] = (int32_t)i;
+    }
+    if (i < n && vf[i]) reps[vpos[i]] = (int32_t)i;
+}
+
+// every node: its phase-1 representative's final root
+__global__ void k_mst_final(int64_t n, int32_t* comp) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int32_t r = comp[v];
+    if (r != v) comp[v] = comp[r];  // representatives (r == v) already hold their final root
+}
+
 // Shared driver, also used by the connected-component labelling of rooted
-// forests (every edge key distinct).
+// forests (every edge key distinct).  Phase 1: kFull rounds over the whole
+// graph (components grow ~3x per round, so most edges become internal);
+// phase 2: the remaining rounds over the contracted graph (edges between
+// distinct components, relabelled to representatives).
 int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, const uint64_t* key,
                 uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st) {
+    constexpr int kMaxRounds = 64, kBatch = 4;
+    int kFull = 3;
+    {
+        const char* e = getenv("HDP_MST_FULL");  // A/B switch for diagnostics: no contraction
+        if (e && e[0] == '1') kFull = kMaxRounds;
+    }
     DevBuf<unsigned long long> best;
     DevBuf<int32_t> win, link;
     DevBuf<uint8_t> alive;
     DevBuf<int> hooks;
-    constexpr int kMaxRounds = 64, kBatch = 4;
     HDP_TRY(best.alloc(n, st));
     HDP_TRY(win.alloc(n, st));
     HDP_TRY(link.alloc(n, st));
     HDP_TRY(alive.alloc(m > 0 ? m : 1, st));
-    HDP_TRY(hooks.alloc(kMaxRounds + kBatch, st));
-    HDP_CHECK_CUDA(cudaMemsetAsync(hooks.get(), 0, sizeof(int) * (kMaxRounds + kBatch), st));
+    HDP_TRY(hooks.alloc(2 * kMaxRounds + 2, st));
+    int* cnt = hooks.get() + 2 * kMaxRounds;  // contraction counts
+    HDP_CHECK_CUDA(cudaMemsetAsync(hooks.get(), 0, sizeof(int) * (2 * kMaxRounds + 2), st));
     k_mst_init<<<grid_for(n, 256), 256, 0, st>>>(n, comp); note_launch();
     if (m > 0) {
         HDP_CHECK_CUDA(cudaMemsetAsync(alive.get(), 1, m, st));
         HDP_CHECK_CUDA(cudaMemsetAsync(in_tree, 0, m, st));
     }
+    // current graph: full, later contracted
+    const int32_t* gu = eu;
+    const int32_t* gv = ev;
+    const uint64_t* gk = key;
+    const int32_t* gidx = nullptr;
+    const int32_t* nodes = nullptr;
+    int64_t gm = m, gn = n;
+    DevBuf<int32_t> cu, cv, cidx, reps;
+    DevBuf<uint64_t> ckey;
     int rounds = 0;
+    bool contracted = false;
     Tracer tr(st);
-    int hb[kBatch];
     while (m > 0) {
-        // kBatch rounds per host check; hooks[r] = 1 iff round r hooked anything
         const int r0 = rounds;
-        for (int r = r0; r < r0 + kBatch; r++) {
+        const int nb = contracted ? kBatch : std::min(kFull, kMaxRounds - rounds);  // first batch = full graph
+        for (int r = r0; r < r0 + nb; r++) {
             const int* prev = r > 0 ? hooks.get() + r - 1 : nullptr;
             int* hk = hooks.get() + r;
-            k_mst_reset<<<grid_for(n, 256), 256, 0, st>>>(n, best.get(), win.get(), prev); note_launch();
-            k_mst_offer<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get(), prev); note_launch();
-            k_mst_win<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, key, comp, alive.get(), best.get(),
-                                                       win.get(), prev); note_launch();
-            k_mst_hook<<<grid_for(n, 256), 256, 0, st>>>(n, eu, ev, comp, win.get(), link.get(),
-                                                        in_tree, hk, prev); note_launch();
-            k_mst_relabel<<<grid_for(n, 256), 256, 0, st>>>(n, comp, link.get(), prev); note_launch();
+            k_mst_reset<<<grid_for(gn, 256), 256, 0, st>>>(gn, best.get(), win.get(), prev, nodes); note_launch();
+            if (gm > 0) {
+                k_mst_offer<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
+                                                               prev); note_launch();
+                k_mst_win<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
+                                                             win.get(), prev); note_launch();
+            }
+            k_mst_hook<<<grid_for(gn, 256), 256, 0, st>>>(gn, gu, gv, comp, win.get(), link.get(), in_tree, hk, prev,
+                                                         nodes, gidx); note_launch();
+            k_mst_relabel<<<grid_for(gn, 256), 256, 0, st>>>(gn, comp, link.get(), prev, nodes); note_launch();
+        }
+        DevBuf<int32_t> ef, epos, vf, vpos;
+        if (!contracted) {
+            // contraction counts ride along with the batch's hook flags
+            HDP_TRY(ef.alloc(m + 1, st));
+            HDP_TRY(epos.alloc(m + 1, st));
+            HDP_TRY(vf.alloc(n + 1, st));
+            HDP_TRY(vpos.alloc(n + 1, st));
+            k_mst_cflags<<<grid_for(std::max(m, n) + 1, 256), 256, 0, st>>>(m, n, eu, ev, comp, ef.get(), vf.get()); note_launch();
+            HDP_TRY(exclusive_sum(ef.get(), epos.get(), m + 1, st));
+            HDP_TRY(exclusive_sum(vf.get(), vpos.get(), n + 1, st));
+            k_mst_counts<<<1, 1, 0, st>>>(m, n, epos.get(), vpos.get(), cnt); note_launch();
         }
         HDP_CHECK_LAUNCH();
-        HDP_CHECK_CUDA(cudaMemcpyAsync(hb, hooks.get() + r0, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        std::vector<int> hb(std::max(nb, kBatch) + 2, 0);
+        HDP_CHECK_CUDA(cudaMemcpyAsync(hb.data(), hooks.get() + r0, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+        if (!contracted) HDP_CHECK_CUDA(cudaMemcpyAsync(hb.data() + nb, cnt, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
         HDP_CHECK_CUDA(cudaStreamSynchronize(st));
         int k = 0;
-        while (k < kBatch && hb[k] != 0) k++;
-        if (k < kBatch) {  // round r0 + k made no hooks: it was the last
+        while (k < nb && hb[k] != 0) k++;
+        if (k < nb) {  // round r0 + k made no hooks: it was the last
             rounds = r0 + k + 1;
             break;
         }
-        rounds = r0 + kBatch;
+        rounds = r0 + nb;
         if (rounds >= kMaxRounds) {
             set_error("boruvka did not converge (duplicate keys?)");
             return HDP_ERR_INTERNAL;
         }
+        if (!contracted) {
+            const int64_t m2 = hb[nb], n2 = hb[nb + 1];
+            HDP_TRY(cu.alloc(m2 + 1, st));
+            HDP_TRY(cv.alloc(m2 + 1, st));
+            HDP_TRY(ckey.alloc(m2 + 1, st));
+            HDP_TRY(cidx.alloc(m2 + 1, st));
+            HDP_TRY(reps.alloc(n2 + 1, st));
+            k_mst_contract<<<grid_for(std::max(m, n), 256), 256, 0, st>>>(
+                m, n, eu, ev, key, comp, ef.get(), epos.get(), vf.get(), vpos.get(), cu.get(), cv.get(), ckey.get(),
+                cidx.get(), reps.get()); note_launch();
+            if (m2 > 0) HDP_CHECK_CUDA(cudaMemsetAsync(alive.get(), 1, m2, st));
+            gu = cu.get();
+            gv = cv.get();
+            gk = ckey.get();
+            gidx = cidx.get();
+            nodes = reps.get();
+            gm = m2;
+            gn = n2;
+            contracted = true;
+        }
+    }
+    if (contracted) {
+        k_mst_final<<<grid_for(n, 256), 256, 0, st>>>(n, comp); note_launch();
+        HDP_CHECK_LAUNCH();
     }
     tr.mark("boruvka rounds");
     if (rounds_out) *rounds_out = rounds;
