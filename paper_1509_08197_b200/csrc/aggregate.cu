@@ -498,35 +498,78 @@ __device__ __forceinline__ bool try_carry1(const unsigned long long* p, unsigned
 // where the carry is `edge`), then apply the published local maps in between
 // in the serial chain's order, X = x_loc(k) + P(k) * X.  The arithmetic is
 // exactly the serial chain's, so the result does not depend on timing.
+// Probes kLB segments per step (all their words loaded before any test), so a
+// walk of d segments costs ~d / kLB memory latencies.
+constexpr int kLB = 4;
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
+
 __device__ __forceinline__ float4 seg_lookback(const AggArgs& a, int64_t gseg, int dir, int kmax,
                                                unsigned epoch, int jq, bool act, float4 edge) {
     const size_t lw = (size_t)a.max_mp;
     int k = 1;
     float4 X = edge;
     while (k <= kmax) {
-        const int64_t gk = gseg + (int64_t)dir * k;
-        float4 v;
-        const bool inc = act ? try_carry4(a.carry + gk * lw + 4 * jq, epoch, v) : true;
-        if (__all_sync(0xffffffffu, inc)) {
-            X = v;
+        const int nb = min(kLB, kmax - k + 1);
+        unsigned long long wi[kLB][4], wa[kLB][4], wp[kLB];
+#pragma unroll
+        for (int j = 0; j < kLB; j++) {
+            const int64_t gk = gseg + (int64_t)dir * (k + min(j, nb - 1));
+            const unsigned long long* pi = a.carry + gk * lw + 4 * jq;
+            const unsigned long long* pa = a.agg + gk * lw + 4 * jq;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                wi[j][c] = act ? ld_relaxed(pi + c) : ((unsigned long long)epoch << 32);
+                wa[j][c] = act ? ld_relaxed(pa + c) : ((unsigned long long)epoch << 32);
+            }
+            wp[j] = ld_relaxed(a.aggp + gk);
+        }
+        int stop = -1;   // first probed segment with an inclusive carry
+        int ready = 0;   // probed segments whose local map is published, in order
+        bool gap = false;
+#pragma unroll
+        for (int j = 0; j < kLB; j++) {
+            if (j >= nb || stop >= 0 || gap) continue;
+            bool iok = true, aok = (unsigned)(wp[j] >> 32) == epoch;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                iok = iok && (unsigned)(wi[j][c] >> 32) == epoch;
+                aok = aok && (unsigned)(wa[j][c] >> 32) == epoch;
+            }
+            if (__all_sync(0xffffffffu, iok)) {
+                stop = j;
+                X = make_float4(__uint_as_float((unsigned)wi[j][0]), __uint_as_float((unsigned)wi[j][1]),
+                                __uint_as_float((unsigned)wi[j][2]), __uint_as_float((unsigned)wi[j][3]));
+            } else if (__all_sync(0xffffffffu, aok)) {
+                ready = j + 1;
+            } else {
+                gap = true;
+            }
+        }
+        if (stop >= 0) {
+            k += stop;
             break;
         }
-        float4 xl;
-        float P;
-        const bool agg = (act ? try_carry4(a.agg + gk * lw + 4 * jq, epoch, xl) : true) &&
-                         try_carry1(a.aggp + gk, epoch, P);
-        if (__all_sync(0xffffffffu, agg)) {
-            k++;
+        if (ready > 0) {
+            k += ready;
             continue;
         }
         __nanosleep(20);
     }
+    // k: offset of the stop (an inclusive carry, or kmax + 1 past the end)
     for (int kk = k - 1; kk >= 1; kk--) {
         const int64_t gk = gseg + (int64_t)dir * kk;
         float4 xl = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        float P = 0.0f;
-        if (act) try_carry4(a.agg + gk * lw + 4 * jq, epoch, xl);
-        try_carry1(a.aggp + gk, epoch, P);
+        if (act) {
+            const unsigned long long* pa = a.agg + gk * lw + 4 * jq;
+            xl = make_float4(__uint_as_float((unsigned)__ldcg(pa)), __uint_as_float((unsigned)__ldcg(pa + 1)),
+                             __uint_as_float((unsigned)__ldcg(pa + 2)), __uint_as_float((unsigned)__ldcg(pa + 3)));
+        }
+        const float P = __uint_as_float((unsigned)__ldcg(a.aggp + gk));
         X.x = xl.x + P * X.x;
         X.y = xl.y + P * X.y;
         X.z = xl.z + P * X.z;
