@@ -87,7 +87,7 @@ __device__ __forceinline__ int32_t uf_find(int32_t* uf, int32_t x) {
 
 constexpr int DR_THREADS = 1024;
 constexpr int DR_MAXS = 64;      // roots the multi-commit leader can absorb per round
-constexpr int DR_SCAN = 1024;    // window edges the leader may inspect per round
+constexpr int DR_SCAN = 256;    // window edges the leader may inspect per round
 constexpr int DR_HASH = 256;     // shared-memory hash set of the leader's roots
 constexpr int DR_NW = 8;         // mask words per root staged in shared memory (d_max < 256)
 
