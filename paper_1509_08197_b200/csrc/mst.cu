@@ -65,18 +65,26 @@ __global__ void k_mst_offer(int64_t m, const int32_t* __restrict__ eu, const int
 __global__ void k_mst_win(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                           const uint64_t* __restrict__ key, const int32_t* __restrict__ comp,
                           const uint8_t* __restrict__ alive, const unsigned long long* __restrict__ best,
-                          int32_t* win, const int* prev) {
+                          int32_t* win, int32_t* wother, const int* prev) {
     if (converged(prev)) return;
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m || !alive[e]) return;
     int32_t cu = comp[eu[e]], cv = comp[ev[e]];
     unsigned long long k = key[e];
-    if (best[cu] == k) win[cu] = (int32_t)e;
-    if (best[cv] == k) win[cv] = (int32_t)e;
+    // the winner also records the component across it (saves the hook two
+    // dependent loads)
+    if (best[cu] == k) {
+        win[cu] = (int32_t)e;
+        wother[cu] = cv;
+    }
+    if (best[cv] == k) {
+        win[cv] = (int32_t)e;
+        wother[cv] = cu;
+    }
 }
 
 // eidx (optional): original edge index of each contracted edge
-__global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+__global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ wother,
                            const int32_t* __restrict__ comp, const int32_t* __restrict__ win,
                            int32_t* __restrict__ link, uint8_t* __restrict__ in_tree,
                            int* __restrict__ hooks, const int* prev, const int32_t* __restrict__ nodes,
@@ -91,8 +99,7 @@ __global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ eu, const int3
             if (e < 0) {
                 link[v] = (int32_t)v;
             } else {
-                int32_t a = comp[eu[e]], b = comp[ev[e]];
-                int32_t other = (a == v) ? b : a;
+                const int32_t other = wother[v];
                 in_tree[eidx ? eidx[e] : e] = 1;
                 if (win[other] == e && v < other) {
                     link[v] = (int32_t)v;  // mutual minimum: the lower id stays the root
@@ -170,15 +177,16 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
     constexpr int kMaxRounds = 64, kBatch = 4;
     int kFull = 3;
     {
-        const char* e = getenv("HDP_MST_FULL");  // A/B switch for diagnostics: no contraction
-        if (e && e[0] == '1') kFull = kMaxRounds;
+        const char* e = getenv("HDP_MST_FULL");  // diagnostics: full-graph rounds before contraction
+        if (e && e[0] >= '1' && e[0] <= '9') kFull = e[0] == '1' ? kMaxRounds : e[0] - '0';
     }
     DevBuf<unsigned long long> best;
-    DevBuf<int32_t> win, link;
+    DevBuf<int32_t> win, wother, link;
     DevBuf<uint8_t> alive;
     DevBuf<int> hooks;
     HDP_TRY(best.alloc(n, st));
     HDP_TRY(win.alloc(n, st));
+    HDP_TRY(wother.alloc(n, st));
     HDP_TRY(link.alloc(n, st));
     HDP_TRY(alive.alloc(m > 0 ? m : 1, st));
     HDP_TRY(hooks.alloc(2 * kMaxRounds + 2, st));
@@ -212,10 +220,10 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
                 k_mst_offer<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
                                                                prev); note_launch();
                 k_mst_win<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
-                                                             win.get(), prev); note_launch();
+                                                             win.get(), wother.get(), prev); note_launch();
             }
-            k_mst_hook<<<grid_for(gn, 256), 256, 0, st>>>(gn, gu, gv, comp, win.get(), link.get(), in_tree, hk, prev,
-                                                         nodes, gidx); note_launch();
+            k_mst_hook<<<grid_for(gn, 256), 256, 0, st>>>(gn, wother.get(), comp, win.get(), link.get(), in_tree, hk,
+                                                         prev, nodes, gidx); note_launch();
             k_mst_relabel<<<grid_for(gn, 256), 256, 0, st>>>(gn, comp, link.get(), prev, nodes); note_launch();
         }
         DevBuf<int32_t> ef, epos, vf, vpos;
