@@ -15,6 +15,8 @@
 // edges are compacted (order preserved) in front of the next window.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "prims.cuh"
 
@@ -328,6 +330,246 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
 #endif
 }
 
+// ---- whole-window rounds by conflict groups -------------------------------
+//
+// One CTA per stereo pair decides the NEXT GW edges of its sorted list in one
+// round.  The window's live edges and the distinct roots they touch form a
+// graph; its connected components ("groups") touch disjoint trees, so their
+// sequential outcomes are independent.  Each group is walked by one thread in
+// Kruskal order against shared-memory copies of its trees (local union-find,
+// sizes, masks) -- exactly the reference's loop (hdp_forest.py:185-203)
+// restricted to that group -- and the merges are written back to the global
+// union-find.  Every round decides the whole window, so rounds = edges / GW.
+constexpr int GW = 1024;          // window edges per round (= threads)
+constexpr int GSLOTS = 2 * GW;    // distinct roots a window can touch
+constexpr int GHASH = 4096;       // open-addressing table root -> slot
+
+struct GrpSmem {
+    int32_t e[GW], la[GW], lb[GW];    // per window position: edge, root slots
+    int32_t ord[GW], grp[GW];         // positions sorted (stably) by group; group of each
+    int32_t hkey[GHASH], hslot[GHASH];
+    int32_t sroot[GSLOTS], gp[GSLOTS], mp[GSLOTS], sz[GSLOTS];
+    uint32_t mask[GSLOTS * DR_NW];
+    uint8_t dirty[GSLOTS];
+    int nslots, changed;
+};
+
+__device__ __forceinline__ int grp_hash(int32_t k) {
+    return (int)(((uint32_t)k * 2654435761u) >> 16) & (GHASH - 1);
+}
+
+__device__ __forceinline__ void grp_insert(GrpSmem& s, int32_t k) {
+    int h = grp_hash(k);
+    while (true) {
+        const int32_t cur = atomicCAS(&s.hkey[h], -1, k);
+        if (cur == -1 || cur == k) return;
+        h = (h + 1) & (GHASH - 1);
+    }
+}
+
+__device__ __forceinline__ int grp_lookup(const GrpSmem& s, int32_t k) {
+    int h = grp_hash(k);
+    while (s.hkey[h] != k) h = (h + 1) & (GHASH - 1);
+    return s.hslot[h];
+}
+
+__device__ __forceinline__ int grp_find(int32_t* p, int x) {
+    while (p[x] != x) {
+        const int g = p[p[x]];
+        p[x] = g;  // path halving: stores an ancestor (race-safe)
+        x = g;
+    }
+    return x;
+}
+
+__global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
+                                            const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                                            int32_t* uf, int32_t* usz, uint32_t* tm, int nw, double beta,
+                                            uint8_t* in_tree, int* rounds_out) {
+    extern __shared__ unsigned long long g_dyn[];
+    GrpSmem& s = *reinterpret_cast<GrpSmem*>(g_dyn);
+    typedef cub::BlockRadixSort<uint32_t, GW, 1, int32_t> Sort;
+    __shared__ typename Sort::TempStorage sort_tmp;
+    // rule 2 as an exact integer test: merge iff inter >= thr[uni], where thr[u]
+    // is the least i with !(RN(i / u) < beta) (RN(i / u) is monotone in i)
+    __shared__ int16_t thr[8 * 32 + 1];
+    const int b = blockIdx.x, tid = threadIdx.x;
+    for (int u = tid; u <= 32 * nw; u += GW) {
+        int i = 0;
+        if (u > 0)
+            while (i <= u && __ddiv_rn((double)i, (double)u) < beta) i++;
+        thr[u] = (int16_t)i;
+    }
+    int32_t head = seg[b];
+    const int32_t end = seg[b + 1];
+    int round = 0;
+#ifdef HDP_DR_PROFILE
+    long long g_ph[7] = {0, 0, 0, 0, 0, 0, 0}, g_t0 = clock64(), g_t1;
+    int g_maxrun = 0;
+#define G_TICK(k) do { __syncthreads(); g_t1 = clock64(); g_ph[k] += g_t1 - g_t0; g_t0 = g_t1; } while (0)
+#else
+#define G_TICK(k) do { } while (0)
+#endif
+    while (head < end) {
+        const int w = min(GW - 1, end - head);
+        // 1. roots of the window's edges
+        for (int i = tid; i < GHASH; i += GW) s.hkey[i] = -1;
+        if (tid == 0) s.nslots = 0;
+        int32_t e = -1, ra = 0, rb = 0;
+        bool live = false;
+        if (tid < w) {
+            e = order[head + tid];
+            ra = uf_find(uf, eu[e]);
+            rb = uf_find(uf, ev[e]);
+            live = ra != rb;  // a cycle: rejected at once (hdp_forest.py:190-191)
+        }
+        __syncthreads();
+        G_TICK(0);
+        if (live) {
+            grp_insert(s, ra);
+            grp_insert(s, rb);
+        }
+        __syncthreads();
+        // 2. a slot per distinct root, holding the tree's current size and mask
+        for (int h0 = 0; h0 < GHASH; h0 += GW) {
+            const int h = h0 + tid;
+            const int32_t k = s.hkey[h];
+            // one atomic per warp for the slot numbers
+            const unsigned occ = __ballot_sync(0xffffffffu, k >= 0);
+            int base = 0;
+            if ((tid & 31) == 0 && occ) base = atomicAdd(&s.nslots, __popc(occ));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (k >= 0) {
+                const int sl = base + __popc(occ & ((1u << (tid & 31)) - 1u));
+                s.hslot[h] = sl;
+                s.sroot[sl] = k;
+            }
+        }
+        __syncthreads();
+        // the slots' tree state, every global load of the round issued together
+        for (int sl = tid; sl < s.nslots; sl += GW) {
+            const int32_t k = s.sroot[sl];
+            s.gp[sl] = sl;
+            s.mp[sl] = sl;
+            s.dirty[sl] = 0;
+            s.sz[sl] = usz[k];
+            for (int i = 0; i < nw; i++) s.mask[sl * DR_NW + i] = tm[(int64_t)k * nw + i];
+        }
+        __syncthreads();
+        int la = 0, lb = 0;
+        if (live) {
+            la = grp_lookup(s, ra);
+            lb = grp_lookup(s, rb);
+        }
+        s.e[tid] = e;
+        s.la[tid] = la;
+        s.lb[tid] = lb;
+        G_TICK(1);
+        // 3. groups = connected components of (slots, live edges)
+        while (true) {
+            if (tid == 0) s.changed = 0;
+            __syncthreads();
+            if (live) {
+                const int ga = grp_find(s.gp, la), gb = grp_find(s.gp, lb);
+                if (ga != gb) {
+                    atomicMin(&s.gp[max(ga, gb)], min(ga, gb));
+                    s.changed = 1;
+                }
+            }
+            __syncthreads();
+            if (!s.changed) break;
+            __syncthreads();
+        }
+        G_TICK(2);
+        // 4. positions sorted by group alone: the radix sort is stable and the
+        // input is in window (Kruskal) order, so every group becomes one run in
+        // Kruskal order.  Group 2047 = not live (a window of GW - 1 edges
+        // touches at most 2 GW - 2 roots, so no live group has that slot).
+        uint32_t key[1] = {live ? (uint32_t)grp_find(s.gp, la) : 2047u};
+        int32_t val[1] = {tid};
+        __syncthreads();
+        Sort(sort_tmp).Sort(key, val, 0, 11);
+        s.ord[tid] = val[0];
+        s.grp[tid] = key[0] == 2047u ? -1 : (int)key[0];
+        __syncthreads();
+        G_TICK(3);
+        // 5. one thread per group walks its run
+        {
+            const int g = s.grp[tid];
+            if (g >= 0 && (tid == 0 || s.grp[tid - 1] != g)) {
+            int n_g = 0;
+            // the next edge's indices are fetched while this one is decided
+            int pos_n = s.ord[tid];
+            int la_n = s.la[pos_n], lb_n = s.lb[pos_n];
+            for (int q = tid; q < GW && s.grp[q] == g; q++) {
+                n_g++;
+                const int pos = pos_n, la_q = la_n, lb_q = lb_n;
+                if (q + 1 < GW) {
+                    pos_n = s.ord[q + 1];
+                    la_n = s.la[pos_n];
+                    lb_n = s.lb[pos_n];
+                }
+                const int x = grp_find(s.mp, la_q), y = grp_find(s.mp, lb_q);
+                if (x == y) continue;  // joined earlier in this window: a cycle
+                int inter = 0, uni = 0;
+                for (int i = 0; i < nw; i++) {
+                    const uint32_t p = s.mask[x * DR_NW + i], r = s.mask[y * DR_NW + i];
+                    inter += __popc(p & r);
+                    uni += __popc(p | r);
+                }
+                // rule 2 (hdp_forest.py:195) through the exact threshold table
+                if (inter < thr[uni]) continue;
+                int keep = x, gone = y;  // union by size, as dr_union
+                if (s.sz[x] < s.sz[y]) {
+                    keep = y;
+                    gone = x;
+                }
+                s.mp[gone] = keep;
+                s.sz[keep] += s.sz[gone];
+                for (int i = 0; i < nw; i++) s.mask[keep * DR_NW + i] |= s.mask[gone * DR_NW + i];
+                s.dirty[keep] = 1;
+                s.dirty[gone] = 1;
+                in_tree[s.e[pos]] = 1;
+            }
+#ifdef HDP_DR_PROFILE
+            if (n_g > g_maxrun) g_maxrun = n_g;
+#endif
+            }
+        }
+        __syncthreads();
+        G_TICK(4);
+        // 6. write the merged trees back
+        for (int sl = tid; sl < s.nslots; sl += GW) {
+            if (!s.dirty[sl]) continue;
+            const int r = grp_find(s.mp, sl);
+            const int32_t k = s.sroot[sl];
+            if (r != sl) {
+                uf[k] = s.sroot[r];
+            } else {
+                usz[k] = s.sz[sl];
+                for (int i = 0; i < nw; i++) tm[(int64_t)k * nw + i] = s.mask[sl * DR_NW + i];
+            }
+        }
+        __syncthreads();
+        G_TICK(5);
+        head += w;
+        round++;
+    }
+    if (tid == 0) atomicMax(rounds_out, round);
+#ifdef HDP_DR_PROFILE
+    g_maxrun = __reduce_max_sync(0xffffffffu, g_maxrun);
+    __shared__ int s_mr;
+    if (tid == 0) s_mr = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) atomicMax(&s_mr, g_maxrun);
+    __syncthreads();
+    if (tid == 0 && b == 0)
+        printf("[grp] rounds %d cyc/round roots %.0f slots %.0f cc %.0f sort %.0f walk %.0f wb %.0f  max run %d\n",
+               round, (double)g_ph[0] / round, (double)g_ph[1] / round, (double)g_ph[2] / round,
+               (double)g_ph[3] / round, (double)g_ph[4] / round, (double)g_ph[5] / round, s_mr);
+#endif
+}
+
 __global__ void k_uf_final(int64_t n, int32_t* uf, int nw, const uint32_t* __restrict__ tm,
                            int32_t* comp, uint32_t* tree_masks) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -397,10 +639,19 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
     k_uf_init<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
                                             uf.get(), usz.get(), tm.get(), res.get()); note_launch();
     HDP_CHECK_LAUNCH();
-    constexpr size_t dr_smem = 2 * DR_THREADS * sizeof(unsigned long long) + 2 * DR_THREADS * DR_NW * sizeof(uint32_t);
-    HDP_CHECK_CUDA(cudaFuncSetAttribute(k_dr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dr_smem));
-    k_dr<<<batch, DR_THREADS, dr_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(),
-                                       res.get(), nw, beta, in_tree, rounds.get()); note_launch();
+    const char* alg = getenv("HDP_HDPF_DR");  // diagnostics: the reservation kernel instead of groups
+    if (alg && alg[0] == '1') {
+        constexpr size_t dr_smem =
+            2 * DR_THREADS * sizeof(unsigned long long) + 2 * DR_THREADS * DR_NW * sizeof(uint32_t);
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_dr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dr_smem));
+        k_dr<<<batch, DR_THREADS, dr_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(),
+                                                 res.get(), nw, beta, in_tree, rounds.get()); note_launch();
+    } else {
+        constexpr size_t g_smem = sizeof(GrpSmem);
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+        k_grp<<<batch, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(), nw, beta,
+                                         in_tree, rounds.get()); note_launch();
+    }
     HDP_CHECK_LAUNCH();
     k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks); note_launch();
     HDP_CHECK_LAUNCH();
