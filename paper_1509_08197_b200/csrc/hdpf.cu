@@ -501,6 +501,11 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
             // the next edge's indices are fetched while this one is decided
             int pos_n = s.ord[tid];
             int la_n = s.la[pos_n], lb_n = s.lb[pos_n];
+            // register copy of the last surviving root (runs mostly grow one
+            // tree): its size and mask are read from / flushed to shared
+            // memory only when the cached root changes
+            int cr = -1, csz = 0;
+            uint32_t cm[DR_NW];
             for (int q = tid; q < GW && s.grp[q] == g; q++) {
                 n_g++;
                 const int pos = pos_n, la_q = la_n, lb_q = lb_n;
@@ -509,27 +514,53 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                     la_n = s.la[pos_n];
                     lb_n = s.lb[pos_n];
                 }
-                const int x = grp_find(s.mp, la_q), y = grp_find(s.mp, lb_q);
+                int x = grp_find(s.mp, la_q), y = grp_find(s.mp, lb_q);
                 if (x == y) continue;  // joined earlier in this window: a cycle
+                if (y == cr) {  // keep the cached root in x
+                    y = x;
+                    x = cr;
+                }
+                if (x != cr) {  // switch the cache to x
+                    if (cr >= 0) {
+                        s.sz[cr] = csz;
+                        for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
+                    }
+                    cr = x;
+                    csz = s.sz[x];
+#pragma unroll
+                    for (int i = 0; i < DR_NW; i++) cm[i] = i < nw ? s.mask[x * DR_NW + i] : 0u;
+                }
                 int inter = 0, uni = 0;
-                for (int i = 0; i < nw; i++) {
-                    const uint32_t p = s.mask[x * DR_NW + i], r = s.mask[y * DR_NW + i];
-                    inter += __popc(p & r);
-                    uni += __popc(p | r);
+                uint32_t my[DR_NW];
+#pragma unroll
+                for (int i = 0; i < DR_NW; i++) {
+                    my[i] = i < nw ? s.mask[y * DR_NW + i] : 0u;
+                    inter += __popc(cm[i] & my[i]);
+                    uni += __popc(cm[i] | my[i]);
                 }
                 // rule 2 (hdp_forest.py:195) through the exact threshold table
                 if (inter < thr[uni]) continue;
-                int keep = x, gone = y;  // union by size, as dr_union
-                if (s.sz[x] < s.sz[y]) {
-                    keep = y;
-                    gone = x;
-                }
-                s.mp[gone] = keep;
-                s.sz[keep] += s.sz[gone];
-                for (int i = 0; i < nw; i++) s.mask[keep * DR_NW + i] |= s.mask[gone * DR_NW + i];
-                s.dirty[keep] = 1;
-                s.dirty[gone] = 1;
+                const int ysz = s.sz[y];
+                s.dirty[x] = 1;
+                s.dirty[y] = 1;
                 in_tree[s.e[pos]] = 1;
+                if (csz < ysz) {  // union by size, as dr_union: y survives
+                    s.mp[x] = y;
+                    s.sz[y] = csz + ysz;
+#pragma unroll
+                    for (int i = 0; i < DR_NW; i++)
+                        if (i < nw) s.mask[y * DR_NW + i] = cm[i] | my[i];
+                    cr = -1;  // x is absorbed: its cached state is not needed any more
+                } else {
+                    s.mp[y] = x;
+                    csz += ysz;
+#pragma unroll
+                    for (int i = 0; i < DR_NW; i++) cm[i] |= my[i];
+                }
+            }
+            if (cr >= 0) {
+                s.sz[cr] = csz;
+                for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
             }
 #ifdef HDP_DR_PROFILE
             if (n_g > g_maxrun) g_maxrun = n_g;
