@@ -190,6 +190,65 @@ __global__ void k_rank_jump(int64_t na, const uint64_t* __restrict__ in, uint64_
     }
 }
 
+// ---- ruling-set list ranking: rulers are every kRuler-th arc plus every list
+// head; each ruler walks its sublist to the next ruler (owner, offset), the
+// rulers alone are ranked by pointer jumping, and rank = ruler rank - offset.
+constexpr int kRuler = 8;
+
+__global__ void k_has_pred(int64_t na, const int32_t* __restrict__ next, uint8_t* hp) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na && next[i] >= 0) hp[next[i]] = 1;
+}
+
+__global__ void k_ruler_flags(int64_t na, const uint8_t* __restrict__ hp, int32_t* flag) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) flag[i] = (i % kRuler == 0 || !hp[i]) ? 1 : 0;
+    else if (i == na) flag[i] = 0;
+}
+
+__global__ void k_ruler_list(int64_t na, const int32_t* __restrict__ flag, const int32_t* __restrict__ rid,
+                             int32_t* list) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na && flag[i]) list[rid[i]] = (int32_t)i;
+}
+
+// one thread per ruler: walk to the next ruler (or the list's end)
+__global__ void k_ruler_walk(int64_t na, const int32_t* __restrict__ rid, const int32_t* __restrict__ list,
+                             const int32_t* __restrict__ flag, const int32_t* __restrict__ next, int32_t* owner,
+                             int32_t* local, uint64_t* word) {
+    int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rid[na]) return;
+    int32_t cur = list[r], cnt = 0, nx;
+    while (true) {
+        owner[cur] = (int32_t)r;
+        local[cur] = cnt++;
+        nx = next[cur];
+        if (nx < 0 || flag[nx]) break;
+        cur = nx;
+    }
+    word[r] = ((uint64_t)(uint32_t)(nx < 0 ? -1 : rid[nx]) << 32) | (uint32_t)cnt;
+}
+
+__global__ void k_rank_jump_n(const int32_t* __restrict__ count, const uint64_t* __restrict__ in,
+                              uint64_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= *count) return;
+    const uint64_t w = in[i];
+    const int32_t nx = (int32_t)(w >> 32);
+    if (nx >= 0) {
+        const uint64_t w2 = in[nx];
+        out[i] = (w2 & 0xffffffff00000000ull) | (uint32_t)((uint32_t)w + (uint32_t)w2);
+    } else {
+        out[i] = w;
+    }
+}
+
+__global__ void k_rank_final(int64_t na, const int32_t* __restrict__ owner, const int32_t* __restrict__ local,
+                             const uint64_t* __restrict__ rword, int32_t* rank) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) rank[i] = (int32_t)((uint32_t)rword[owner[i]] - (uint32_t)local[i]);
+}
+
 __global__ void k_rank_unpack(int64_t na, const uint64_t* __restrict__ word, int32_t* rank) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < na) rank[i] = (int32_t)(uint32_t)word[i];
@@ -789,17 +848,33 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     if (na > 0) {
         k_tour_next<<<grid_for(na, B), B, 0, st>>>(na, asrc.get(), adst.get(), adj_start.get(),
                                                   f->root.get(), twin.get(), nxt.get()); note_launch();
+        // ruling-set ranking; rulers <= ceil(na / kRuler) + one head per tree
+        const int64_t rmax = (na + kRuler - 1) / kRuler + f->n_trees + 1;
+        DevBuf<uint8_t> hpred;
+        DevBuf<int32_t> rflag, rid, rlist, owner, local;
         DevBuf<uint64_t> wa, wb;
-        HDP_TRY(wa.alloc(na, st));
-        HDP_TRY(wb.alloc(na, st));
-        // the longest list is the largest tree's tour, 2 (size - 1) arcs
+        HDP_TRY(hpred.alloc(na, st));
+        HDP_TRY(rflag.alloc(na + 1, st));
+        HDP_TRY(rid.alloc(na + 1, st));
+        HDP_TRY(rlist.alloc(rmax, st));
+        HDP_TRY(owner.alloc(na, st));
+        HDP_TRY(local.alloc(na, st));
+        HDP_TRY(wa.alloc(rmax, st));
+        HDP_TRY(wb.alloc(rmax, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(hpred.get(), 0, na, st));
+        k_has_pred<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), hpred.get()); note_launch();
+        k_ruler_flags<<<grid_for(na + 1, B), B, 0, st>>>(na, hpred.get(), rflag.get()); note_launch();
+        HDP_TRY(exclusive_sum(rflag.get(), rid.get(), na + 1, st));
+        k_ruler_list<<<grid_for(na, B), B, 0, st>>>(na, rflag.get(), rid.get(), rlist.get()); note_launch();
+        k_ruler_walk<<<grid_for(rmax, 128), 128, 0, st>>>(na, rid.get(), rlist.get(), rflag.get(), nxt.get(),
+                                                          owner.get(), local.get(), wa.get()); note_launch();
+        // the longest ruler chain is at most the largest tree's tour, 2 (size - 1) arcs
         const int rounds = ceil_log2(2 * (int64_t)max_tree);
-        k_rank_init<<<grid_for(na, B), B, 0, st>>>(na, nxt.get(), wa.get()); note_launch();
         for (int r = 0; r < rounds; r++) {
-            k_rank_jump<<<grid_for(na, B), B, 0, st>>>(na, wa.get(), wb.get()); note_launch();
+            k_rank_jump_n<<<grid_for(rmax, B), B, 0, st>>>(rid.get() + na, wa.get(), wb.get()); note_launch();
             std::swap(wa.p, wb.p);
         }
-        k_rank_unpack<<<grid_for(na, B), B, 0, st>>>(na, wa.get(), rank.get()); note_launch();
+        k_rank_final<<<grid_for(na, B), B, 0, st>>>(na, owner.get(), local.get(), wa.get(), rank.get()); note_launch();
         HDP_CHECK_LAUNCH();
     }
     k_tour_len<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), f->root.get(), f->tree_id.get(),
