@@ -425,9 +425,14 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
         }
         __syncthreads();
         G_TICK(0);
-        if (live) {
-            grp_insert(s, ra);
-            grp_insert(s, rb);
+        {
+            // one insert per distinct root per warp (the largest tree's root is
+            // touched by a large share of the window)
+            const unsigned pa = __match_any_sync(0xffffffffu, live ? ra : -1);
+            const unsigned pb = __match_any_sync(0xffffffffu, live ? rb : -1);
+            const int lane = tid & 31;
+            if (live && __ffs(pa) - 1 == lane) grp_insert(s, ra);
+            if (live && __ffs(pb) - 1 == lane) grp_insert(s, rb);
         }
         __syncthreads();
         // 2. a slot per distinct root, holding the tree's current size and mask
