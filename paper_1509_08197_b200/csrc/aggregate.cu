@@ -74,6 +74,7 @@ struct AggArgs {
     int sub_shift;
     int atomic_keys;
     int store_all;  // store A for every node (volume requested), not only light parents
+    int seg_light;  // the segment up pass gathers the light children itself (no k_light)
     int max_m;
     int max_mp;            // max_m rounded up to a multiple of 4 (carry stride)
     int qgroups;           // 32-float4 column groups of the widest row (segment kernels)
@@ -639,6 +640,62 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0
     const bool has_next = c.b < c.start + c.len;
     float4* buf = sbuf + warp * kSeg * sq;
     const int rs = seg_stage(a, c, g, buf, &bars[warp], lane);
+    if (a.seg_light) {
+        // light children (final since the deeper phases) of the segment's nodes:
+        // b(v) = E(v) + (s_c0 A_up(c0) + s_c1 A_up(c1) + ...), the operation
+        // order of k_light.  The segment's entries are one contiguous CSR range.
+        const int E0 = a.lc_start[c.a], E1 = a.lc_start[c.b];
+        if (E1 > E0) {
+            const int e0n = lane < cnt ? a.lc_start[c.a + lane] : 0;
+            const int e1n = lane < cnt ? a.lc_start[c.a + lane + 1] : 0;
+            float4 xacc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            for (int eb = E0; eb < E1; eb += 32) {
+                const int e = eb + lane, ne = min(32, E1 - eb);
+                long long rowe = 0;
+                float sime = 0.0f;
+                if (e < E1) {
+                    rowe = a.lc_row[e];
+                    sime = a.lc_sim[e];
+                }
+                for (int j0 = 0; j0 < ne; j0 += 8) {
+                    float4 v[8];
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const long long r = __shfl_sync(0xffffffffu, rowe, (j0 + j) & 31);
+                        v[j] = (j0 + j < ne && act) ? reinterpret_cast<const float4*>(a.aup + r)[jq]
+                                                    : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        if (j0 + j >= ne) break;
+                        const int ee = eb + j0 + j;
+                        const float sc = __shfl_sync(0xffffffffu, sime, j0 + j);
+                        const unsigned own = __ballot_sync(0xffffffffu, lane < cnt && e0n <= ee && ee < e1n);
+                        const int i = __ffs(own) - 1;
+                        const bool first = ee == __shfl_sync(0xffffffffu, e0n, i);
+                        const bool last = ee + 1 == __shfl_sync(0xffffffffu, e1n, i);
+                        if (first) {
+                            xacc = make_float4(sc * v[j].x, sc * v[j].y, sc * v[j].z, sc * v[j].w);
+                        } else {
+                            xacc.x += sc * v[j].x;
+                            xacc.y += sc * v[j].y;
+                            xacc.z += sc * v[j].z;
+                            xacc.w += sc * v[j].w;
+                        }
+                        if (last && act) {
+                            float4 b = buf[i * rs + lane];
+                            b.x = b.x + xacc.x;
+                            b.y = b.y + xacc.y;
+                            b.z = b.z + xacc.z;
+                            b.w = b.w + xacc.w;
+                            buf[i * rs + lane] = b;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
     // s of node a + i (0 past the path's tail), i in [0, cnt]
     const float s_lo = (lane < cnt || (lane == cnt && has_next)) ? fabsf(a.lsimf[c.a + lane]) : 0.0f;
     const float s_hi = (32 + lane < cnt || (32 + lane == cnt && has_next)) ? fabsf(a.lsimf[c.a + 32 + lane]) : 0.0f;
@@ -1364,6 +1421,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.atomic_keys = (f->n_segs > 0 && a.qgroups > 1) ? 1 : 0;
     if (a.atomic_keys) HDP_CHECK_CUDA(cudaMemsetAsync(kp, 0xff, sizeof(unsigned long long) * f->n, st));
     a.store_all = volume != nullptr;
+    a.seg_light = f->chunks_ok ? 1 : 0;
     if (!cost_rows && (f->geom_w != a.w || f->geom_np != a.npix)) {
         k_fill_cols<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, f->lmeta.get(), a.npix, a.w); note_launch();
         f->geom_w = a.w;
@@ -1417,7 +1475,9 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_TRY(side_stream(&ss));
     for (int64_t r = f->n_phases - 1; r >= 0; r--) {
         // light parents on short paths are handled inside k_up_chunk
-        int64_t p0 = chunks ? f->lp_mid[r] : f->lp_off[r], np = f->lp_off[r + 1] - p0;
+        // light parents on short paths are handled by k_up_chunk, those on long
+        // paths by k_seg_up (seg_light); k_light only in the fallback path
+        int64_t p0 = f->lp_off[r], np = chunks ? 0 : f->lp_off[r + 1] - p0;
         int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0;
         int64_t g0 = f->seg_off[r], ng = f->seg_off[r + 1] - g0;
         const bool side = chunks && nc > 0 && (np > 0 || ng > 0);
