@@ -59,3 +59,21 @@ def test_hdp_c2_size_teacher_forced(gmm_text):
         assert int(o.stored_entries[0]) == r.stored_entries, f"level {o.level} entries"
         got = o.disparity[0].cpu().numpy()
         assert_disp_parity(got, r.disparity, r.min_cost, r.second_cost, f"level {o.level}")
+
+
+def test_dense_wide_rows_match_oracle():
+    """C5-style rows (d_max 512, 513 lanes: wider than one 32-float4 column
+    group) on a smaller image: the per-path short kernels and the segment
+    scans with several column groups and 64-bit key minima."""
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import SceneSpec, make_scene
+    from oracle import oracle as O
+
+    sc = make_scene(SceneSpec(5, 120, 720, 512, 24, 0.4, 8.0, 1), 0)
+    L, R = sc.pair.left.data, sc.pair.right.data
+    out = E.run_baseline_batch(dev(L[None]), dev(R[None]), 512)
+    ref = O.run_baseline(L, R, 512)
+    got = out.disparity[0].cpu().numpy()
+    assert_disp_parity(got, ref.disparity, ref.min_cost, ref.second_cost, "d512")
+    same = got == ref.disparity
+    assert_cost_parity(out.min_cost[0].cpu().numpy()[same], ref.min_cost[same], "d512 costs")
