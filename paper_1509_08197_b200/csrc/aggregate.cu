@@ -1188,6 +1188,32 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
         }
     }
     __syncthreads();
+    if (a.max_mp >= 128) {
+        // wide rows (a chunk holds few of them): one warp per node, lanes over
+        // float4 columns, each lane keeping its first minimum, then redux
+        const int lane = threadIdx.x & 31;
+        for (int i = threadIdx.x >> 5; i < d.nk; i += blockDim.x >> 5) {
+            const int4 mt = s.meta[i];
+            const int m = mt.w, mq = (m + 3) >> 2;
+            const float4* row = reinterpret_cast<const float4*>(s.own + (s.nrow[i] - d.a0));
+            float best = __int_as_float(0x7f800000);  // +inf
+            int bj = 0x7fffffff;
+            for (int jq = lane; jq < mq; jq += 32) {
+                const float4 y = row[jq];
+                const int j = 4 * jq;  // padding lanes hold kPadCost and never win
+                if (y.x < best) { best = y.x; bj = j; }
+                if (y.y < best) { best = y.y; bj = j + 1; }
+                if (y.z < best) { best = y.z; bj = j + 2; }
+                if (y.w < best) { best = y.w; bj = j + 3; }
+            }
+            const uint32_t ob = bj == 0x7fffffff ? 0xffffffffu : ord_f32(best);
+            const uint32_t mn = __reduce_min_sync(0xffffffffu, ob);
+            const uint32_t jm = __reduce_min_sync(0xffffffffu, ob == mn ? (uint32_t)bj : 0xffffffffu);
+            if (lane == 0 && a.keys)
+                a.keys[mt.x] = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, mt.y, (int)jm);
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < d.nk; i += blockDim.x) {
         const int4 mt = s.meta[i];
         const int mq = (mt.w + 3) >> 2;

@@ -1293,7 +1293,7 @@ static int build_chunks(hdp_forest* f) {
     f->chunk_words = h[nph] > 0 ? h[nph + 1] + 64 : 0;
     // rows of up to 32 float4 lanes: one lane group spans a row; wider rows
     // take the per-path kernels (lane groups across CTAs)
-    f->chunks_ok = f->chunk_words <= kChunkMaxWords && f->max_m <= 128;
+    f->chunks_ok = f->chunk_words <= kChunkMaxWords;
     {
         const char* e = getenv("HDP_NO_CHUNKS");  // A/B switch for diagnostics
         if (e && e[0] == '1') f->chunks_ok = 0;
