@@ -217,28 +217,21 @@ __global__ void __launch_bounds__(256) k_ecost_range(AggArgs a, const int32_t* _
     for (int i = threadIdx.x; i < nt; i += blockDim.x) srow[i] = __ldg(a.rowoff + __ldg(lpos + base + c0 + i));
     __syncthreads();
     const float4* rrow = a.pr + base;  // right-image row (global fallback)
-    const int mq = (m + 3) >> 2;
-    const int items = nt * mq;
+    // one disparity per thread: adjacent threads read adjacent window pixels
+    // (conflict-free 16-byte shared loads) and store adjacent floats
+    const int mp = (m + 3) & ~3;
+    const int items = nt * mp;
     const float wc = 1.0f - a.alpha;
     for (int t = threadIdx.x; t < items; t += blockDim.x) {
-        const int q = mq == 1 ? t : (int)__umulhi((unsigned)t, inv);
-        const int jq = t - q * mq;
+        const int q = (int)__umulhi((unsigned)t, inv);  // t / mp
+        const int j = t - q * mp;
         const int col = c0 + q;
-        const float4 L = __ldg(a.pl + base + col);
-        const int x = col - (a.range_x0 + 4 * jq);  // right-image column of lane 4 jq
-        float e[4];
-        if (x - 3 >= 0 && 4 * jq + 3 < m) {
-#pragma unroll
-            for (int u = 0; u < 4; u++) e[u] = pix_cost(a, wc, L, SMEM ? win[x - u - lo] : __ldg(rrow + x - u));
-        } else {
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                if (4 * jq + u >= m) e[u] = kPadCost;
-                else if (x - u < 0) e[u] = a.border;
-                else e[u] = pix_cost(a, wc, L, SMEM ? win[x - u - lo] : __ldg(rrow + x - u));
-            }
-        }
-        reinterpret_cast<float4*>(a.aup + srow[q])[jq] = make_float4(e[0], e[1], e[2], e[3]);
+        const int x = col - (a.range_x0 + j);  // right-image column of lane j
+        float e;
+        if (j >= m) e = kPadCost;
+        else if (x < 0) e = a.border;
+        else e = pix_cost(a, wc, __ldg(a.pl + base + col), SMEM ? win[x - lo] : __ldg(rrow + x));
+        a.aup[srow[q] + j] = e;
     }
 }
 
@@ -1479,8 +1472,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         int use = smem <= 48 * 1024;
         dim3 g((unsigned)rows, (unsigned)((a.w + kETile - 1) / kETile));
         if (a.range_x0 >= 0) {
-            const int m = f->max_m, mq = (m + 3) >> 2;
-            const unsigned inv = mq > 1 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
+            const int m = f->max_m, mp = (m + 3) & ~3;
+            const unsigned inv = (unsigned)((0x100000000ull + mp - 1) / mp);  // t / mp by multiply-high
             if (use) k_ecost_range<true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d, m, inv);
             else k_ecost_range<false><<<g, 256, 0, st>>>(a, f->lpos.get(), f->max_d, m, inv);
         } else {
