@@ -217,21 +217,26 @@ __global__ void __launch_bounds__(256) k_ecost_range(AggArgs a, const int32_t* _
     for (int i = threadIdx.x; i < nt; i += blockDim.x) srow[i] = __ldg(a.rowoff + __ldg(lpos + base + c0 + i));
     __syncthreads();
     const float4* rrow = a.pr + base;  // right-image row (global fallback)
-    // one disparity per thread: adjacent threads read adjacent window pixels
-    // (conflict-free 16-byte shared loads) and store adjacent floats
+    // one warp per node, lanes over disparities: adjacent lanes read adjacent
+    // window pixels (conflict-free 16-byte shared loads) and store adjacent
+    // floats; the left pixel is loaded once per node
     const int mp = (m + 3) & ~3;
-    const int items = nt * mp;
     const float wc = 1.0f - a.alpha;
-    for (int t = threadIdx.x; t < items; t += blockDim.x) {
-        const int q = (int)__umulhi((unsigned)t, inv);  // t / mp
-        const int j = t - q * mp;
+    const int lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    (void)inv;
+    for (int q = threadIdx.x >> 5; q < nt; q += nwarp) {
         const int col = c0 + q;
-        const int x = col - (a.range_x0 + j);  // right-image column of lane j
-        float e;
-        if (j >= m) e = kPadCost;
-        else if (x < 0) e = a.border;
-        else e = pix_cost(a, wc, __ldg(a.pl + base + col), SMEM ? win[x - lo] : __ldg(rrow + x));
-        a.aup[srow[q] + j] = e;
+        const float4 L = __ldg(a.pl + base + col);
+        float* out = a.aup + srow[q];
+        const int xl = col - a.range_x0;  // right-image column of lane 0
+        for (int j = lane; j < mp; j += 32) {
+            const int x = xl - j;
+            float e;
+            if (j >= m) e = kPadCost;
+            else if (x < 0) e = a.border;
+            else e = pix_cost(a, wc, L, SMEM ? win[x - lo] : __ldg(rrow + x));
+            out[j] = e;
+        }
     }
 }
 
