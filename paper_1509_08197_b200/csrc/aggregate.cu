@@ -208,13 +208,17 @@ __global__ void __launch_bounds__(256) k_ecost_range(AggArgs a, const int32_t* _
                                                      int m, unsigned inv) {
     extern __shared__ float4 win[];
     __shared__ long long srow[kETile];
+    __shared__ float4 sL[kETile];
     const int64_t base = (int64_t)blockIdx.x * a.w;  // node id of column 0 of this image row
     const int c0 = (int)blockIdx.y * kETile;
     const int lo = max(0, c0 - d_hi), hi = min(a.w, c0 + kETile);
     const int nt = hi - c0;  // columns in this tile
     if (SMEM)
         for (int i = threadIdx.x; i < hi - lo; i += blockDim.x) win[i] = __ldg(a.pr + base + lo + i);
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) srow[i] = __ldg(a.rowoff + __ldg(lpos + base + c0 + i));
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+        srow[i] = __ldg(a.rowoff + __ldg(lpos + base + c0 + i));
+        sL[i] = __ldg(a.pl + base + c0 + i);
+    }
     __syncthreads();
     const float4* rrow = a.pr + base;  // right-image row (global fallback)
     // one warp per node, lanes over disparities: adjacent lanes read adjacent
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(256) k_ecost_range(AggArgs a, const int32_t* _
     (void)inv;
     for (int q = threadIdx.x >> 5; q < nt; q += nwarp) {
         const int col = c0 + q;
-        const float4 L = __ldg(a.pl + base + col);
+        const float4 L = sL[q];
         float* out = a.aup + srow[q];
         const int xl = col - a.range_x0;  // right-image column of lane 0
         for (int j = lane; j < mp; j += 32) {
