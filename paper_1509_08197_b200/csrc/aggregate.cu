@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(256) k_ecompute(AggArgs a, int64_t k0, int64_t
 // each hypothesis costs one shared load and one 4-byte global store into the
 // node's layout row (the rows of one node are contiguous; m lanes -> m/32
 // coalesced stores per warp).
-constexpr int kETile = 64;
+constexpr int kETile = 128;
 
 __device__ __forceinline__ float pix_cost(const AggArgs& a, float wc, const float4& L, const float4& R) {
     float color;
