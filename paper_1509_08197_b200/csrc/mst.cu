@@ -12,6 +12,8 @@
 // relabelled by following hook chains.  Self-loops die.  HBM/L2-atomic bound.
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -159,6 +161,86 @@ __global__ void k_mst_contract(int64_t m, int64_t n, const int32_t* __restrict__
     if (i < n && vf[i]) reps[vpos[i]] = (int32_t)i;
 }
 
+// The contracted phase in ONE cooperative launch: the rounds' steps are
+// separated by grid-wide barriers instead of kernel boundaries, and the loop
+// stops on the device at the first round without hooks (no host checks).
+__global__ void __launch_bounds__(256) k_mst_coop(int64_t gm, int64_t gn, const int32_t* __restrict__ gu,
+                                                  const int32_t* __restrict__ gv, const uint64_t* __restrict__ gk,
+                                                  const int32_t* __restrict__ gidx, const int32_t* __restrict__ reps,
+                                                  int32_t* comp, uint8_t* alive, unsigned long long* best,
+                                                  int32_t* win, int32_t* wother, int32_t* link, uint8_t* in_tree,
+                                                  int* flags, int max_rounds, int* rounds_out) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t tid = (int64_t)grid.thread_rank(), nthr = (int64_t)grid.size();
+    int r = 0;
+    while (r < max_rounds) {
+        for (int64_t t = tid; t < gn; t += nthr) {
+            const int32_t v = reps[t];
+            best[v] = ~0ull;
+            win[v] = -1;
+        }
+        grid.sync();
+        for (int64_t e = tid; e < gm; e += nthr) {
+            if (!alive[e]) continue;
+            const int32_t cu = comp[gu[e]], cv = comp[gv[e]];
+            if (cu == cv) {
+                alive[e] = 0;
+                continue;
+            }
+            const unsigned long long k = gk[e];
+            if (k < best[cu]) atomicMin(&best[cu], k);
+            if (k < best[cv]) atomicMin(&best[cv], k);
+        }
+        grid.sync();
+        for (int64_t e = tid; e < gm; e += nthr) {
+            if (!alive[e]) continue;
+            const int32_t cu = comp[gu[e]], cv = comp[gv[e]];
+            const unsigned long long k = gk[e];
+            if (best[cu] == k) {
+                win[cu] = (int32_t)e;
+                wother[cu] = cv;
+            }
+            if (best[cv] == k) {
+                win[cv] = (int32_t)e;
+                wother[cv] = cu;
+            }
+        }
+        grid.sync();
+        bool hooked = false;
+        for (int64_t t = tid; t < gn; t += nthr) {
+            const int32_t v = reps[t];
+            if (comp[v] != v) continue;
+            const int32_t e = win[v];
+            if (e < 0) {
+                link[v] = v;
+                continue;
+            }
+            const int32_t other = wother[v];
+            in_tree[gidx[e]] = 1;
+            if (win[other] == e && v < other) {
+                link[v] = v;  // mutual minimum: the lower id stays the root
+            } else {
+                link[v] = other;
+                hooked = true;
+            }
+        }
+        if (__syncthreads_or(hooked) && threadIdx.x == 0 && *(volatile int*)(flags + r) == 0) flags[r] = 1;
+        grid.sync();
+        for (int64_t t = tid; t < gn; t += nthr) {
+            const int32_t v = reps[t];
+            int32_t x = comp[v];
+            while (link[x] != x) x = link[x];
+            comp[v] = x;
+        }
+        grid.sync();
+        const bool more = *(volatile int*)(flags + r) != 0;
+        r++;
+        if (!more) break;  // round r - 1 made no hooks: the forest is final
+    }
+    if (tid == 0) *rounds_out = r;
+}
+
 // every node: its phase-1 representative's final root
 __global__ void k_mst_final(int64_t n, int32_t* comp) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -176,6 +258,11 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
                 uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st) {
     constexpr int kMaxRounds = 64, kBatch = 4;
     int kFull = 3;
+    bool coop = true;  // the contracted phase as one cooperative launch
+    {
+        const char* e = getenv("HDP_MST_COOP");  // diagnostics: 0 = batched launches
+        if (e && e[0] == '0') coop = false;
+    }
     {
         const char* e = getenv("HDP_MST_FULL");  // diagnostics: full-graph rounds before contraction
         if (e && e[0] >= '1' && e[0] <= '9') kFull = e[0] == '1' ? kMaxRounds : e[0] - '0';
@@ -273,6 +360,33 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
             gm = m2;
             gn = n2;
             contracted = true;
+            if (coop) {
+                int nb = 0, dev = 0, nsm = 0;
+                HDP_CHECK_CUDA(cudaGetDevice(&dev));
+                HDP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+                HDP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mst_coop, 256, 0));
+                int* fl = hooks.get() + kMaxRounds;  // per-round hook flags of this phase (zeroed)
+                int* rc = hooks.get() + 2 * kMaxRounds - 1;
+                int max_r = kMaxRounds - rounds - 1;
+                int64_t gm_ = gm, gn_ = gn;
+                uint8_t* al = alive.get();
+                unsigned long long* bs = best.get();
+                int32_t *wi = win.get(), *wo = wother.get(), *lk = link.get();
+                int32_t* cp = comp;
+                void* args[] = {(void*)&gm_, (void*)&gn_, (void*)&gu, (void*)&gv, (void*)&gk, (void*)&gidx,
+                                (void*)&nodes, (void*)&cp, (void*)&al, (void*)&bs, (void*)&wi, (void*)&wo,
+                                (void*)&lk, (void*)&in_tree, (void*)&fl, (void*)&max_r, (void*)&rc};
+                HDP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)k_mst_coop, dim3(nb * nsm), dim3(256), args,
+                                                           0, st)); note_launch();
+                int hr = 0;
+                HDP_TRY(to_host(&hr, rc, 1, st));
+                rounds += hr;
+                if (hr >= max_r) {
+                    set_error("boruvka did not converge (duplicate keys?)");
+                    return HDP_ERR_INTERNAL;
+                }
+                break;
+            }
         }
     }
     if (contracted) {
