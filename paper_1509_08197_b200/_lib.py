@@ -13,7 +13,8 @@ import os
 from .errors import ConfigError, DataError, InternalError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhdpstereo.so")
+# HDP_LIB: load another build of the library (A/B comparisons of build variants)
+LIB_PATH = os.environ.get("HDP_LIB") or os.path.join(_HERE, "libhdpstereo.so")
 ABI_VERSION = 1
 
 _P = C.c_void_p

@@ -28,6 +28,10 @@
 //          k_down_short short paths
 // A is written back in place only where a light child will read it.
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <cstdio>
+#include <string>
+#include <vector>
 
 #include <algorithm>
 #include <atomic>
@@ -46,6 +50,7 @@ struct AggArgs {
     const int4* pinfo;      // per path of the launch list: (start, len, m, lane offset)
     const longlong2* prows; // (first row, parent's row or -1)
     const int2* seg_tab;    // (long-path index, segment index from the head)
+    const SegDesc* seg_desc;  // per segment: rows, parent row, light-child range
     const int32_t* dlist;
     const int64_t* rowoff;
     const int32_t* lp_list;
@@ -381,32 +386,69 @@ __global__ void __launch_bounds__(256) k_scan_up_short(AggArgs a, int64_t s0, in
     }
 }
 
+// Diagnostics build (-DHDP_AGG_PROFILE): per-CTA / per-warp globaltimer stamps
+// of the staging and compute steps, read back by hdp_debug_prof.
+#ifdef HDP_AGG_PROFILE
+constexpr unsigned kProfMax = 1u << 20;
+__device__ unsigned long long g_prof[kProfMax * 8];
+__device__ unsigned g_prof_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned smid() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+    return r;
+}
+#define PROF_DECL unsigned long long _pt0 = gtimer(), _pt1 = 0, _pt2 = 0, _pt3 = 0, _pt4 = 0
+#define PROF_T(k) (_pt##k = gtimer())
+#define PROF_PUT(kind, lead, aux)                                                                     \
+    do {                                                                                              \
+        if (lead) {                                                                                   \
+            const unsigned _i = atomicAdd(&g_prof_n, 1u);                                             \
+            if (_i < kProfMax) {                                                                      \
+                unsigned long long* _r = g_prof + (size_t)_i * 8;                                     \
+                _r[0] = ((unsigned long long)(kind) << 56) | ((unsigned long long)smid() << 40) |     \
+                        (unsigned long long)(unsigned)(aux);                                          \
+                _r[1] = _pt0; _r[2] = _pt1; _r[3] = _pt2; _r[4] = _pt3; _r[5] = _pt4; _r[6] = gtimer(); \
+            }                                                                                         \
+        }                                                                                             \
+    } while (0)
+#else
+#define PROF_DECL
+#define PROF_T(k)
+#define PROF_PUT(kind, lead, aux)
+#endif
+
 // ---------------------------------------------------------------- segments
 
 struct SegCtx {
-    int32_t start, len, m, doff, mp;
-    int64_t row0, prow;
-    int32_t a, b;    // segment node range [a, b) (layout positions)
+    int32_t doff, mp;
+    int64_t rowa, prow;  // first row of the segment, the path's parent row
+    int32_t a, b;        // segment node range [a, b) (layout positions)
+    int32_t e0, e1;      // light-child entries of the segment's nodes
     int s, nseg;
-    int64_t gseg;    // global segment index
+    bool has_next;       // more segments toward the tail
+    int64_t gseg;        // global segment index
 };
 
 __device__ __forceinline__ SegCtx seg_ctx(const AggArgs& a, int64_t gseg) {
-    int2 st = a.seg_tab[gseg];
-    int4 info = a.pinfo[st.x];
-    longlong2 rows = a.prows[st.x];
+    const int4* p = reinterpret_cast<const int4*>(a.seg_desc + gseg);
+    const int4 w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2);
     SegCtx c;
-    c.start = info.x;
-    c.len = info.y;
-    c.m = info.z;
-    c.mp = (info.z + 3) & ~3;
-    c.doff = info.w;
-    c.row0 = rows.x;
-    c.prow = rows.y;
-    c.s = st.y;
-    c.nseg = (c.len + kSeg - 1) / kSeg;
-    c.a = c.start + c.s * kSeg;
-    c.b = min(c.start + c.len, c.a + kSeg);
+    c.rowa = ((long long)(unsigned)w0.y << 32) | (unsigned)w0.x;
+    c.prow = ((long long)(unsigned)w0.w << 32) | (unsigned)w0.z;
+    c.a = w1.x;
+    c.b = w1.x + w1.y;
+    c.e0 = w1.z;
+    c.e1 = w1.w;
+    c.mp = w2.x;
+    c.doff = w2.y;
+    c.s = w2.z;
+    c.nseg = w2.w;
+    c.has_next = c.s + 1 < c.nseg;
     c.gseg = gseg;
     return c;
 }
@@ -433,6 +475,12 @@ __device__ __forceinline__ float get_carry(const unsigned long long* p, unsigned
         __nanosleep(20);
     }
     return __uint_as_float((unsigned)(w & 0xffffffffu));
+}
+
+// orders this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA) accesses: needed before a bulk copy reuses a buffer
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 // 1-D TMA (bulk async copy) global -> shared, completing on an mbarrier
@@ -581,12 +629,12 @@ __device__ __forceinline__ float4 seg_lookback(const AggArgs& a, int64_t gseg, i
     return X;
 }
 
-// warp-uniform index i in [0, 64]: value of node a + i held in lanes of lo/hi
-// (i < 64), or `past` for i == 64
-__device__ __forceinline__ float seg_pick(float lo, float hi, float past, int i) {
+// warp-uniform index i in [0, 32]: value of node a + i held in lane i of lo
+// (i < 32), or `past` for i == 32 (segments have at most kSeg = 32 nodes)
+static_assert(kSeg == 32, "segment lanes hold one node each");
+__device__ __forceinline__ float seg_pick(float lo, float past, int i) {
     const float l = __shfl_sync(0xffffffffu, lo, i & 31);
-    const float h = __shfl_sync(0xffffffffu, hi, i & 31);
-    return i < 32 ? l : (i < 64 ? h : past);
+    return i < 32 ? l : past;
 }
 
 constexpr int kSegWarps = 4;  // segment warps per CTA
@@ -596,12 +644,14 @@ constexpr int kSegWarps = 4;  // segment warps per CTA
 // arrives with a single bulk copy (row stride = the path's own mq in shared
 // memory); otherwise each row's 32-column slice arrives by its own copy (row
 // stride 32).  Returns the shared-memory row stride in float4.
-__device__ __forceinline__ int seg_stage(const AggArgs& a, const SegCtx& c, int g, float4* buf,
-                                         unsigned long long* bar, int lane) {
+__device__ __forceinline__ int seg_stage_issue(const AggArgs& a, const SegCtx& c, int g, float4* buf,
+                                               unsigned long long* bar, int lane) {
     const int mq = c.mp >> 2;
     const int cnt = c.b - c.a;
-    const float* src0 = a.aup + c.row0 + (int64_t)(c.a - c.start) * c.mp;
-    if (lane == 0) mbar_init(bar, 1);
+    const float* src0 = a.aup + c.rowa;
+    // every lane is done with the previous segment's buffer, and its generic
+    // shared-memory accesses are ordered before the bulk copy's writes
+    fence_proxy_async();
     __syncwarp();
     if (a.qgroups == 1) {
         if (lane == 0) {
@@ -609,7 +659,6 @@ __device__ __forceinline__ int seg_stage(const AggArgs& a, const SegCtx& c, int 
             mbar_expect_tx(bar, bytes);
             bulk_g2s(buf, src0, bytes, bar);
         }
-        mbar_wait(bar, 0);
         return mq;
     }
     const int wq = min(32, mq - 32 * g);
@@ -617,55 +666,93 @@ __device__ __forceinline__ int seg_stage(const AggArgs& a, const SegCtx& c, int 
     __syncwarp();
     for (int i = lane; i < cnt; i += 32)
         bulk_g2s(buf + i * 32, src0 + (int64_t)i * c.mp + 128 * g, (unsigned)wq * 16u, bar);
-    mbar_wait(bar, 0);
     return 32;
+}
+__device__ __forceinline__ void seg_stage_wait(unsigned long long* bar, unsigned& par) {
+    mbar_wait(bar, par);
+    par ^= 1u;
+}
+__device__ __forceinline__ int seg_stage(const AggArgs& a, const SegCtx& c, int g, float4* buf,
+                                         unsigned long long* bar, unsigned& par, int lane) {
+    const int rs = seg_stage_issue(a, c, g, buf, bar, lane);
+    seg_stage_wait(bar, par);
+    return rs;
 }
 
 // Up pass over one segment (tail -> head), one warp per (segment, 32 float4
 // columns).  Segments are taken by ticket in reverse table order, so a
 // path's tail segment comes first; the carry is X_a = x_loc(a) + P * X_b with
 // P = prod s_{a+1..b}.
-__global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0, int64_t ng, int* ctr,
-                                                           int sq) {
-    extern __shared__ float4 sbuf[];
-    __shared__ unsigned long long bars[kSegWarps];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = (int)blockIdx.y;
-    const int t = warp_ticket(ctr + g);
-    if (t >= ng) return;
-    const SegCtx c = seg_ctx(a, g0 + ng - 1 - t);
+__device__ __forceinline__ void seg_up_item(const AggArgs& a, int64_t gseg, int g, float4* buf,
+                                            unsigned long long* bar, unsigned& par, int lane) {
+    PROF_DECL;
+    const SegCtx c = seg_ctx(a, gseg);
     const int mq = c.mp >> 2;
     if (g * 32 >= mq) return;
     const int jq = g * 32 + lane;
     const bool act = jq < mq;
     const int cnt = c.b - c.a;
-    const bool has_next = c.b < c.start + c.len;
-    float4* buf = sbuf + warp * kSeg * sq;
-    const int rs = seg_stage(a, c, g, buf, &bars[warp], lane);
+    const bool has_next = c.has_next;
+    const int rs = seg_stage_issue(a, c, g, buf, bar, lane);
+    // while the segment's rows are in flight: the similarities, the light
+    // children's CSR range and the first batch of their rows
+    const float s_lo = (lane < cnt || (lane == cnt && has_next)) ? fabsf(a.lsimf[c.a + lane]) : 0.0f;
+    const float s_past = (cnt == kSeg && has_next) ? fabsf(a.lsimf[c.b]) : 0.0f;
+    int E0 = 0, E1 = 0, e0n = 0, e1n = 0;
+    long long rowe = 0;
+    float sime = 0.0f;
+    float4 vpre[8];
+    if (a.seg_light) {
+        E0 = c.e0;
+        E1 = c.e1;
+        if (E1 > E0) {
+            // per node: its entries [e0n, e1n) (lane cnt - 1 ends at E1)
+            const int en = lane < cnt ? a.lc_start[c.a + lane] : E1;
+            const int nx = __shfl_sync(0xffffffffu, en, (lane + 1) & 31);  // every lane shuffles
+            e0n = en;
+            e1n = lane == 31 ? E1 : nx;
+            if (E0 + lane < E1) {
+                rowe = a.lc_row[E0 + lane];
+                sime = a.lc_sim[E0 + lane];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const long long r = __shfl_sync(0xffffffffu, rowe, j);
+                vpre[j] = (E0 + j < E1 && act) ? reinterpret_cast<const float4*>(a.aup + r)[jq]
+                                               : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            }
+        }
+    }
+    seg_stage_wait(bar, par);
+    PROF_T(1);
     if (a.seg_light) {
         // light children (final since the deeper phases) of the segment's nodes:
         // b(v) = E(v) + (s_c0 A_up(c0) + s_c1 A_up(c1) + ...), the operation
         // order of k_light.  The segment's entries are one contiguous CSR range.
-        const int E0 = a.lc_start[c.a], E1 = a.lc_start[c.b];
         if (E1 > E0) {
-            const int e0n = lane < cnt ? a.lc_start[c.a + lane] : 0;
-            const int e1n = lane < cnt ? a.lc_start[c.a + lane + 1] : 0;
             float4 xacc = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             for (int eb = E0; eb < E1; eb += 32) {
                 const int e = eb + lane, ne = min(32, E1 - eb);
-                long long rowe = 0;
-                float sime = 0.0f;
-                if (e < E1) {
-                    rowe = a.lc_row[e];
-                    sime = a.lc_sim[e];
+                if (eb != E0) {
+                    rowe = 0;
+                    sime = 0.0f;
+                    if (e < E1) {
+                        rowe = a.lc_row[e];
+                        sime = a.lc_sim[e];
+                    }
                 }
                 for (int j0 = 0; j0 < ne; j0 += 8) {
                     float4 v[8];
+                    if (eb == E0 && j0 == 0) {
 #pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        const long long r = __shfl_sync(0xffffffffu, rowe, (j0 + j) & 31);
-                        v[j] = (j0 + j < ne && act) ? reinterpret_cast<const float4*>(a.aup + r)[jq]
-                                                    : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                        for (int j = 0; j < 8; j++) v[j] = vpre[j];
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; j++) {
+                            const long long r = __shfl_sync(0xffffffffu, rowe, (j0 + j) & 31);
+                            v[j] = (j0 + j < ne && act) ? reinterpret_cast<const float4*>(a.aup + r)[jq]
+                                                        : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                        }
                     }
 #pragma unroll
                     for (int j = 0; j < 8; j++) {
@@ -698,29 +785,28 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0
             __syncwarp();
         }
     }
-    // s of node a + i (0 past the path's tail), i in [0, cnt]
-    const float s_lo = (lane < cnt || (lane == cnt && has_next)) ? fabsf(a.lsimf[c.a + lane]) : 0.0f;
-    const float s_hi = (32 + lane < cnt || (32 + lane == cnt && has_next)) ? fabsf(a.lsimf[c.a + 32 + lane]) : 0.0f;
-    const float s_past = (cnt == kSeg && has_next) ? fabsf(a.lsimf[c.b]) : 0.0f;
+    PROF_T(2);
     const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     float4 x = z;
     float P = 1.0f;
+    if (c.s > 0) {  // the head side will need this segment's map (local pass)
 #pragma unroll 4
-    for (int i = cnt - 1; i >= 0; i--) {
-        const float sn = seg_pick(s_lo, s_hi, s_past, i + 1);
-        const float4 v = act ? buf[i * rs + lane] : z;
-        x.x = v.x + sn * x.x;
-        x.y = v.y + sn * x.y;
-        x.z = v.z + sn * x.z;
-        x.w = v.w + sn * x.w;
-        P *= sn;
-    }
-    if (c.s > 0) {  // the head side will need this segment's map
+        for (int i = cnt - 1; i >= 0; i--) {
+            const float sn = seg_pick(s_lo, s_past, i + 1);
+            const float4 v = act ? buf[i * rs + lane] : z;
+            x.x = v.x + sn * x.x;
+            x.y = v.y + sn * x.y;
+            x.z = v.z + sn * x.z;
+            x.w = v.w + sn * x.w;
+            P *= sn;
+        }
         if (act) put_carry4(a.agg + c.gseg * a.max_mp + 4 * jq, a.epoch_up, x);
         if (lane == 0) put_carry(a.aggp + c.gseg, a.epoch_up, P);
     }
+    PROF_T(3);
     float4 Xb = z;
     if (has_next) Xb = seg_lookback(a, c.gseg, +1, c.nseg - 1 - c.s, a.epoch_up, jq, act, z);
+    PROF_T(4);
     if (act && c.s > 0) {
         float4 o;
         o.x = x.x + P * Xb.x;
@@ -730,17 +816,38 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0
         put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_up, o);
     }
     // final pass: exact recurrence from the true X_b
-    float4* rows = reinterpret_cast<float4*>(a.aup + c.row0) + (int64_t)(c.a - c.start) * mq + jq;
+    float4* rows = reinterpret_cast<float4*>(a.aup + c.rowa) + jq;
     x = Xb;
 #pragma unroll 4
     for (int i = cnt - 1; i >= 0; i--) {
-        const float sn = seg_pick(s_lo, s_hi, s_past, i + 1);
+        const float sn = seg_pick(s_lo, s_past, i + 1);
         const float4 v = act ? buf[i * rs + lane] : z;
         x.x = v.x + sn * x.x;
         x.y = v.y + sn * x.y;
         x.z = v.z + sn * x.z;
         x.w = v.w + sn * x.w;
         if (act) rows[(int64_t)i * mq] = x;
+    }
+    PROF_PUT(3, lane == 0, cnt | (c.s << 8) | ((has_next ? 1 : 0) << 30));
+}
+
+// Persistent: each warp takes segment tickets until the phase's are gone (a
+// warp finishes its segment before taking the next, so every segment a
+// look-back waits on is held by a running warp).
+__global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0, int64_t ng, int* ctr,
+                                                           int sq) {
+    extern __shared__ float4 sbuf[];
+    __shared__ unsigned long long bars[kSegWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = (int)blockIdx.y;
+    float4* buf = sbuf + warp * kSeg * sq;
+    if (lane == 0) mbar_init(&bars[warp], 1);
+    __syncwarp();
+    unsigned par = 0;
+    for (;;) {
+        const int t = warp_ticket(ctr + g);
+        if (t >= ng) break;
+        seg_up_item(a, g0 + ng - 1 - t, g, buf, &bars[warp], par, lane);
     }
 }
 
@@ -750,66 +857,49 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0
 // each node over this warp's columns is folded into the node's key (64-bit
 // min when several warps share a row, a store otherwise); A is written back
 // only where a light child will read it.
-__global__ void __launch_bounds__(32 * kSegWarps) k_seg_down(AggArgs a, int64_t g0, int64_t ng, int* ctr,
-                                                             int sq) {
-    extern __shared__ float4 sbuf[];
-    __shared__ unsigned long long bars[kSegWarps];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = (int)blockIdx.y;
-    const int t = warp_ticket(ctr + g);
-    if (t >= ng) return;
-    const SegCtx c = seg_ctx(a, g0 + t);
+__device__ __forceinline__ void seg_down_item(const AggArgs& a, int64_t gseg, int g, float4* buf,
+                                              unsigned long long* bar, unsigned& par, int lane) {
+    PROF_DECL;
+    const SegCtx c = seg_ctx(a, gseg);
     const int mq = c.mp >> 2;
     if (g * 32 >= mq) return;
     const int jq = g * 32 + lane;
     const bool act = jq < mq;
     const int cnt = c.b - c.a;
-    float4* buf = sbuf + warp * kSeg * sq;
-    const int rs = seg_stage(a, c, g, buf, &bars[warp], lane);
-    // s (0 at a root head), light-children flag and node id of node a + i
-    float s_lo = 0.0f, s_hi = 0.0f;
-    int n_lo = 0, n_hi = 0;
-    unsigned long long lmask = 0;
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-        const int i = 32 * h + lane;
-        const float f = i < cnt ? a.lsimf[c.a + i] : 0.0f;
-        float sv = fabsf(f);
-        if (c.a + i == c.start && c.prow < 0) sv = 0.0f;
-        const int nd = i < cnt ? a.lmeta[c.a + i].x : 0;
-        if (h == 0) {
-            s_lo = sv;
-            n_lo = nd;
-        } else {
-            s_hi = sv;
-            n_hi = nd;
-        }
-        const unsigned b = __ballot_sync(0xffffffffu, i < cnt && (__float_as_uint(f) >> 31));
-        lmask |= (unsigned long long)b << (32 * h);
-    }
-    if (a.store_all) lmask = ~0ull;
+    const int rs = seg_stage_issue(a, c, g, buf, bar, lane);
+    // while the rows are in flight: s (0 at a root head), light-children flag
+    // and node id of node a + i, and the parent's row
+    const float f_me = lane < cnt ? a.lsimf[c.a + lane] : 0.0f;
+    const float s_lo = (c.s == 0 && lane == 0 && c.prow < 0) ? 0.0f : fabsf(f_me);
+    const int n_lo = lane < cnt ? a.lmeta[c.a + lane].x : 0;
+    unsigned lmask = __ballot_sync(0xffffffffu, lane < cnt && (__float_as_uint(f_me) >> 31));
+    if (a.store_all) lmask = ~0u;
     const float4 z = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    // local pass with Y_in = 0
+    float4 Ypar = z;  // A(parent) enters at the path's head (0 at a root)
+    if (c.prow >= 0 && act) Ypar = reinterpret_cast<const float4*>(a.aup + c.prow)[jq];
+    seg_stage_wait(bar, par);
+    PROF_T(1);
+    // local pass with Y_in = 0, only where the tail side needs this segment's map
     float4 yl = z;
     float Q = 1.0f;
+    if (c.s + 1 < c.nseg) {
 #pragma unroll 4
-    for (int i = 0; i < cnt; i++) {
-        const float sv = seg_pick(s_lo, s_hi, 0.0f, i);
-        const float w = 1.0f - sv * sv;
-        const float4 v = act ? buf[i * rs + lane] : z;
-        yl.x = sv * yl.x + w * v.x;
-        yl.y = sv * yl.y + w * v.y;
-        yl.z = sv * yl.z + w * v.z;
-        yl.w = sv * yl.w + w * v.w;
-        Q *= sv;
-    }
-    if (c.s + 1 < c.nseg) {  // the tail side will need this segment's map
+        for (int i = 0; i < cnt; i++) {
+            const float sv = seg_pick(s_lo, 0.0f, i);
+            const float w = 1.0f - sv * sv;
+            const float4 v = act ? buf[i * rs + lane] : z;
+            yl.x = sv * yl.x + w * v.x;
+            yl.y = sv * yl.y + w * v.y;
+            yl.z = sv * yl.z + w * v.z;
+            yl.w = sv * yl.w + w * v.w;
+            Q *= sv;
+        }
         if (act) put_carry4(a.agg + c.gseg * a.max_mp + 4 * jq, a.epoch_down, yl);
         if (lane == 0) put_carry(a.aggp + c.gseg, a.epoch_down, Q);
     }
-    float4 Ypar = z;  // A(parent) enters at the path's head (0 at a root)
-    if (c.prow >= 0 && act) Ypar = reinterpret_cast<const float4*>(a.aup + c.prow)[jq];
+    PROF_T(2);
     const float4 Yin = c.s == 0 ? Ypar : seg_lookback(a, c.gseg, -1, c.s, a.epoch_down, jq, act, Ypar);
+    PROF_T(3);
     if (act && c.s + 1 < c.nseg) {
         float4 o;
         o.x = yl.x + Q * Yin.x;
@@ -818,19 +908,19 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_down(AggArgs a, int64_t 
         o.w = yl.w + Q * Yin.w;
         put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_down, o);
     }
-    float4* rows = reinterpret_cast<float4*>(a.aup + c.row0) + (int64_t)(c.a - c.start) * mq + jq;
+    float4* rows = reinterpret_cast<float4*>(a.aup + c.rowa) + jq;
     float4 y = Yin;
     const int j0 = 4 * jq;
 #pragma unroll 4
     for (int i = 0; i < cnt; i++) {
-        const float sv = seg_pick(s_lo, s_hi, 0.0f, i);
+        const float sv = seg_pick(s_lo, 0.0f, i);
         const float w = 1.0f - sv * sv;
         const float4 v = act ? buf[i * rs + lane] : z;
         y.x = sv * y.x + w * v.x;
         y.y = sv * y.y + w * v.y;
         y.z = sv * y.z + w * v.z;
         y.w = sv * y.w + w * v.w;
-        if (act && ((lmask >> i) & 1ull)) rows[(int64_t)i * mq] = y;
+        if (act && ((lmask >> i) & 1u)) rows[(int64_t)i * mq] = y;
         // first minimum over this lane's four columns (padding never wins)
         float best = y.x;
         int bj = j0;
@@ -840,7 +930,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_down(AggArgs a, int64_t 
         const uint32_t ob = act ? ord_f32(best) : 0xffffffffu;
         const uint32_t mn = __reduce_min_sync(0xffffffffu, ob);
         const uint32_t jm = __reduce_min_sync(0xffffffffu, ob == mn ? (uint32_t)bj : 0xffffffffu);
-        const int node = __shfl_sync(0xffffffffu, i < 32 ? n_lo : n_hi, i & 31);
+        const int node = __shfl_sync(0xffffffffu, n_lo, i);
         if (lane == 0 && a.keys) {
             const unsigned long long key = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, c.doff, (int)jm);
             if (a.atomic_keys)
@@ -848,6 +938,24 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_down(AggArgs a, int64_t 
             else
                 a.keys[node] = key;
         }
+    }
+    PROF_PUT(4, lane == 0, cnt | (c.s << 8) | ((c.s + 1 < c.nseg ? 1 : 0) << 30));
+}
+
+__global__ void __launch_bounds__(32 * kSegWarps) k_seg_down(AggArgs a, int64_t g0, int64_t ng, int* ctr,
+                                                             int sq) {
+    extern __shared__ float4 sbuf[];
+    __shared__ unsigned long long bars[kSegWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = (int)blockIdx.y;
+    float4* buf = sbuf + warp * kSeg * sq;
+    if (lane == 0) mbar_init(&bars[warp], 1);
+    __syncwarp();
+    unsigned par = 0;
+    for (;;) {
+        const int t = warp_ticket(ctr + g);
+        if (t >= ng) break;
+        seg_down_item(a, g0 + t, g, buf, &bars[warp], par, lane);
     }
 }
 
@@ -947,6 +1055,7 @@ __global__ void __launch_bounds__(256) k_down_short(AggArgs a, int64_t s0, int64
 
 constexpr int kChunkThreads = 256;  // one CTA per chunk
 
+
 struct ChunkSm {
     int4* info;         // per path: (start, len, m, lane offset)
     longlong2* prow;    // per path: (first row, parent's row or -1)
@@ -1015,10 +1124,9 @@ __device__ __forceinline__ void row_async(float* dst, const float* src, int cnt,
 // copies need, group 2: the rest).
 template <bool UP>
 __device__ __forceinline__ ChunkSm stage_chunk(const AggArgs& a, const ChunkDesc& d, float4* sm4,
-                                               unsigned long long* bar) {
+                                               unsigned long long* bar, unsigned par) {
     ChunkSm s = carve<UP>(d, sm4);
     const int tid = threadIdx.x, nt = blockDim.x;
-    if (tid == 0) mbar_init(bar, 1);
     for (int i = tid; i < d.np; i += nt) {
         cp_async16(s.info + i, a.pinfo + d.p0 + i);
         cp_async16(s.prow + i, a.prows + d.p0 + i);
@@ -1060,7 +1168,7 @@ __device__ __forceinline__ ChunkSm stage_chunk(const AggArgs& a, const ChunkDesc
         }
     }
     cp_wait_all();
-    mbar_wait(bar, 0);
+    mbar_wait(bar, par);
     __syncthreads();
     return s;
 }
@@ -1070,12 +1178,19 @@ __device__ __forceinline__ ChunkSm stage_chunk(const AggArgs& a, const ChunkDesc
 // (path, float4 column); changed rows are stored, a lone leaf row (A_up = E)
 // is left alone.
 __global__ void __launch_bounds__(kChunkThreads) k_up_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
-                                                            int64_t cbase) {
+                                                            int64_t cbase, int64_t nc) {
     extern __shared__ float4 sm4[];
-    const ChunkDesc d = descs[cbase + blockIdx.x];
-    if (d.np == 0) return;
     __shared__ unsigned long long bar;
-    const ChunkSm s = stage_chunk<true>(a, d, sm4, &bar);
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    unsigned par = 0;
+    for (int64_t ci = blockIdx.x; ci < nc; ci += gridDim.x) {
+    PROF_DECL;
+    const ChunkDesc d = descs[cbase + ci];
+    if (d.np == 0) continue;
+    PROF_T(1);
+    const ChunkSm s = stage_chunk<true>(a, d, sm4, &bar, par);
+    par ^= 1u;
+    PROF_T(2);
     const float4* own4 = reinterpret_cast<const float4*>(s.own);
     const float4* aux4 = reinterpret_cast<const float4*>(s.aux);
     // with a uniform row width the (path, column) split is a multiply-high;
@@ -1136,6 +1251,13 @@ __global__ void __launch_bounds__(kChunkThreads) k_up_chunk(AggArgs a, const Chu
             if (mqu > 0) break;  // uniform width: exactly one column per item
         }
     }
+    fence_proxy_async();  // the next chunk's bulk copies overwrite shared memory
+    __syncthreads();
+#ifdef HDP_AGG_PROFILE
+    PROF_T(3);
+    PROF_PUT(1, threadIdx.x == 0, d.nk);
+#endif
+    }
 }
 
 // Down pass fused with the first argmin: head -> tail,
@@ -1144,12 +1266,19 @@ __global__ void __launch_bounds__(kChunkThreads) k_up_chunk(AggArgs a, const Chu
 // stored globally only where a light child will read it; then one thread
 // per node scans its row for the first minimum (aggregation.py:249).
 __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
-                                                              int64_t cbase) {
+                                                              int64_t cbase, int64_t nc) {
     extern __shared__ float4 sm4[];
-    const ChunkDesc d = descs[cbase + blockIdx.x];
-    if (d.np == 0) return;
     __shared__ unsigned long long bar;
-    const ChunkSm s = stage_chunk<false>(a, d, sm4, &bar);
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    unsigned par = 0;
+    for (int64_t ci = blockIdx.x; ci < nc; ci += gridDim.x) {
+    PROF_DECL;
+    const ChunkDesc d = descs[cbase + ci];
+    if (d.np == 0) continue;
+    PROF_T(1);
+    const ChunkSm s = stage_chunk<false>(a, d, sm4, &bar, par);
+    par ^= 1u;
+    PROF_T(2);
     float4* own4 = reinterpret_cast<float4*>(s.own);
     const float4* aux4 = reinterpret_cast<const float4*>(s.aux);
     const int mqu = d.mqu;
@@ -1190,6 +1319,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
         }
     }
     __syncthreads();
+    PROF_T(3);
     if (a.max_mp >= 128) {
         // wide rows (a chunk holds few of them): one warp per node, lanes over
         // float4 columns, each lane keeping its first minimum, then redux
@@ -1214,8 +1344,7 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
             if (lane == 0 && a.keys)
                 a.keys[mt.x] = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, mt.y, (int)jm);
         }
-        return;
-    }
+    } else
     for (int i = threadIdx.x; i < d.nk; i += blockDim.x) {
         const int4 mt = s.meta[i];
         const int mq = (mt.w + 3) >> 2;
@@ -1236,6 +1365,13 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
             if (y.w == best) { bj = 4 * jq + 3; break; }
         }
         if (a.keys) a.keys[mt.x] = ((unsigned long long)ord_f32(best) << 32) | (uint32_t)lane_disp(a, mt.y, bj);
+    }
+    fence_proxy_async();  // the next chunk's bulk copies overwrite shared memory
+    __syncthreads();
+#ifdef HDP_AGG_PROFILE
+    PROF_T(4);
+    PROF_PUT(2, threadIdx.x == 0, d.nk);
+#endif
     }
 }
 
@@ -1348,6 +1484,11 @@ static int join_side(const SideStream* ss, cudaStream_t st) {
     return HDP_OK;
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);  // diagnostics / tuning switches
+    return e && *e ? atoi(e) : dflt;
+}
+
 static int pow2_at_least(int x) {
     int p = 1;
     while (p < x) p <<= 1;
@@ -1365,6 +1506,57 @@ static dim3 packed_grid(const AggArgs& a, int64_t items, int bu, int block) {
 }  // namespace hdp
 
 using namespace hdp;
+
+// HDP_AGG_TRACE=1: events between the aggregation's phases (no synchronisation
+// until the end of the call), printed with each phase's chunk / segment counts
+struct PhaseClock {
+    bool on = false;
+    cudaStream_t st;
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::string> what;
+    explicit PhaseClock(cudaStream_t s) : st(s) {
+        const char* e = getenv("HDP_AGG_TRACE");
+        on = e && e[0] == '1';
+        if (on) mark("start", 0, 0);
+    }
+    void mark(const char* w, int64_t nc, int64_t ng) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev.push_back(e);
+        char buf[96];
+        snprintf(buf, sizeof(buf), "%-6s chunks %6lld segs %6lld", w, (long long)nc, (long long)ng);
+        what.push_back(buf);
+    }
+    void report() {
+        if (!on) return;
+        cudaEventSynchronize(ev.back());
+        for (size_t i = 1; i < ev.size(); i++) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, "[agg] %s %8.1f us\n", what[i].c_str(), 1e3 * ms);
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+        ev.clear();
+    }
+};
+
+#ifdef HDP_AGG_PROFILE
+// records of 8 words: kind << 56 | smid << 40 | aux, then globaltimer stamps;
+// returns the record count and resets it
+extern "C" __attribute__((visibility("default"))) long long hdp_debug_prof(void* host, long long max_rec) {
+    unsigned n = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&n, g_prof_n, sizeof(n));
+    if (n > kProfMax) n = kProfMax;
+    const long long k = n < max_rec ? n : max_rec;
+    if (host && k > 0) cudaMemcpyFromSymbol(host, g_prof, (size_t)k * 64);
+    const unsigned zero = 0;
+    cudaMemcpyToSymbol(g_prof_n, &zero, sizeof(zero));
+    return (long long)n;
+}
+#endif
 
 extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const float* packed_r,
                                  int h, int w, int c, float alpha, float tau_c, float tau_g,
@@ -1384,6 +1576,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.pinfo = nullptr;
     a.prows = nullptr;
     a.seg_tab = f->seg_tab.get();
+    a.seg_desc = f->seg_desc.get();
     a.dlist = f->dlist.get();
     a.rowoff = f->rowoff.get();
     a.lp_list = f->lp_list.get();
@@ -1491,6 +1684,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         }
         note_launch();
     }
+    PhaseClock pc(st);
+    pc.mark("ecost", 0, 0);
     const bool chunks = f->chunks_ok != 0;
     const size_t csmem = (size_t)((f->chunk_words + 3) & ~3ll) * sizeof(float);
     sh.lc_rowoff = f->lc_rowoff.get();
@@ -1501,6 +1696,23 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     }
     SideStream* ss = nullptr;
     HDP_TRY(side_stream(&ss));
+    // Chunk and segment kernels of one phase run side by side only if neither
+    // takes every SM slot (the block scheduler dispatches one kernel's CTAs
+    // before the next one's).  Both are persistent loops; HDP_CHUNK_SHARE /
+    // HDP_SEG_SHARE (CTAs per SM) cap their grids when a phase has both kinds.
+    // Measured at C2: capped grids (2 + 3 per SM) are slower than one kernel
+    // after the other (register file), so the default is uncapped.
+    int nsm = 148, dev = 0;
+    HDP_CHECK_CUDA(cudaGetDevice(&dev));
+    HDP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    static const int chunk_share = env_int("HDP_CHUNK_SHARE", 0), seg_share = env_int("HDP_SEG_SHARE", 0);
+    auto cgrid = [&](int64_t nc, bool both) -> unsigned {
+        return (unsigned)(both && chunk_share > 0 ? std::min<int64_t>(nc, (int64_t)chunk_share * nsm) : nc);
+    };
+    auto sgrid = [&](int64_t ng, bool both) -> unsigned {
+        const int64_t need = grid_for(ng * 32, 32 * kSegWarps);
+        return (unsigned)(both && seg_share > 0 ? std::min<int64_t>(need, (int64_t)seg_share * nsm) : need);
+    };
     for (int64_t r = f->n_phases - 1; r >= 0; r--) {
         // light parents on short paths are handled inside k_up_chunk
         // light parents on short paths are handled by k_up_chunk, those on long
@@ -1511,23 +1723,25 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         const bool side = chunks && nc > 0 && (np > 0 || ng > 0);
         if (side) {
             HDP_TRY(fork_side(ss, st));
-            k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0); note_launch();
+            k_up_chunk<<<cgrid(nc, ng > 0), kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0, nc);
+            note_launch();
         }
         if (np > 0) {
             k_light<<<grid_for(np << a.qsub_shift, 256), 256, 0, st>>>(a, p0, np); note_launch();
         }
         if (ng > 0) {
-            k_seg_up<<<dim3(grid_for(ng * 32, 32 * kSegWarps), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
+            k_seg_up<<<dim3(sgrid(ng, side), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
                 lg, g0, ng, a.tickets + (2 * r) * a.groups, seg_sq); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (side) {
             HDP_TRY(join_side(ss, st));
         } else if (chunks && nc > 0) {
-            k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
+            k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
         } else if (!chunks && ns > 0) {
             k_scan_up_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
+        pc.mark("up", nc, ng);
     }
     HDP_CHECK_LAUNCH();
     for (int64_t r = 0; r < f->n_phases; r++) {
@@ -1536,20 +1750,22 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         const bool side = chunks && nc > 0 && ng > 0;
         if (side) {
             HDP_TRY(fork_side(ss, st));
-            k_down_chunk<<<(unsigned)nc, kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0); note_launch();
+            k_down_chunk<<<cgrid(nc, ng > 0), kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0, nc);
+            note_launch();
         }
         if (ng > 0) {
-            k_seg_down<<<dim3(grid_for(ng * 32, 32 * kSegWarps), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
+            k_seg_down<<<dim3(sgrid(ng, side), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
                 lg, g0, ng, a.tickets + (2 * r + 1) * a.groups, seg_sq); note_launch();
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (side) {
             HDP_TRY(join_side(ss, st));
         } else if (chunks && nc > 0) {
-            k_down_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0); note_launch();
+            k_down_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
         } else if (!chunks && ns > 0) {
             k_down_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
+        pc.mark("down", nc, ng);
     }
     HDP_CHECK_LAUNCH();
     if (volume) {
@@ -1558,6 +1774,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     if (disp || min_cost) {
         k_keys_finish<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp, disp, min_cost); note_launch();
     }
+    pc.mark("finish", 0, 0);
+    pc.report();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

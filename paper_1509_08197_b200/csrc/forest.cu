@@ -1308,6 +1308,29 @@ __global__ void k_lane_totals(int64_t n, const int64_t* __restrict__ nodeoff, co
     out[2] = mx[0];
 }
 
+__global__ void k_seg_desc(int64_t n, const int2* __restrict__ seg_tab, const int4* __restrict__ info,
+                           const longlong2* __restrict__ rows, const int32_t* __restrict__ lc_start,
+                           SegDesc* out) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const int2 t = seg_tab[g];
+    const int4 in = info[t.x];
+    const longlong2 r = rows[t.x];
+    SegDesc d;
+    d.mp = (in.z + 3) & ~3;
+    d.doff = in.w;
+    d.s = t.y;
+    d.nseg = (in.y + kSeg - 1) / kSeg;
+    d.a = in.x + t.y * kSeg;
+    const int b = min(in.x + in.y, d.a + kSeg);
+    d.cnt = b - d.a;
+    d.rowa = r.x + (long long)(d.a - in.x) * d.mp;
+    d.prow = r.y;
+    d.e0 = lc_start[d.a];
+    d.e1 = lc_start[b];
+    out[g] = d;
+}
+
 // uniform_m > 0: every tree has exactly that many lanes (totals known here)
 static int lanes_finish(hdp_forest* f, int uniform_m) {
     cudaStream_t st = f->st;
@@ -1371,6 +1394,12 @@ static int lanes_finish(hdp_forest* f, int uniform_m) {
                                                   f->p_len.get(), f->p_par.get(), f->p_tree.get(),
                                                   f->t_doff.get(), f->t_m.get(), f->rowoff.get(),
                                                   f->short_info.get(), f->short_rows.get()); note_launch();
+    if (f->n_segs > 0) {
+        HDP_TRY(f->seg_desc.alloc(f->n_segs, st));
+        k_seg_desc<<<grid_for(f->n_segs, B), B, 0, st>>>(f->n_segs, f->seg_tab.get(), f->long_info.get(),
+                                                        f->long_rows.get(), f->lc_start.get(),
+                                                        f->seg_desc.get()); note_launch();
+    }
     HDP_CHECK_LAUNCH();
     HDP_TRY(build_chunks(f));
     tr.mark("lanes finish");

@@ -8,7 +8,10 @@
 
 // Heavy paths of at most this many nodes are aggregated register-resident
 // (one thread per (path, lane)); longer ones by a warp walking staged chunks.
-constexpr int kShortPath = 8;
+#ifndef HDP_SHORT_PATH
+#define HDP_SHORT_PATH 8
+#endif
+constexpr int kShortPath = HDP_SHORT_PATH;
 // Long paths are cut into segments of kSeg nodes, one warp each, chained by
 // decoupled look-back in the aggregation kernels.
 constexpr int kSeg = 32;
@@ -35,6 +38,17 @@ struct alignas(16) ChunkDesc {
     long long lcr0;    // lc_rowoff[L0]
     long long auxd0;   // auxd[p0]
     long long pad3;
+};
+// One long-path segment, everything its warp needs in one 48-byte record
+// (built with the lanes): the aggregation kernels start staging after a
+// single dependent load instead of a chain through the path tables.
+struct alignas(16) SegDesc {
+    long long rowa;    // row offset (floats) of the segment's first node
+    long long prow;    // the path's parent row, -1 at a root path
+    int a, cnt;        // first layout position, nodes (<= kSeg)
+    int e0, e1;        // light-child entries of the segment's nodes
+    int mp, doff;      // padded row width (floats), lane offset of the tree
+    int s, nseg;       // segment index from the head, segments of the path
 };
 }  // namespace hdp
 
@@ -72,6 +86,7 @@ struct hdp_forest {
     hdp::DevBuf<int32_t> dph;        // device copy of the per-phase tables (forest.cu P_* rows)
     int64_t n_lc = 0;                // light-child entries
     hdp::DevBuf<int2> seg_tab;      // (long-path index, segment index from the head)
+    hdp::DevBuf<hdp::SegDesc> seg_desc;  // per segment, built with the lanes
     std::vector<int64_t> seg_off;   // host: segments of phase r = [seg_off[r], seg_off[r+1])
     int64_t n_segs = 0;
 

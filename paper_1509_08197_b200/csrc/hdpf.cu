@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ s
                         if (lane == 0) s_dec[gq] = 1;  // now inside one tree
                         continue;
                     }
-                    int32_t y = qa ? __shfl_sync(0xffffffffu, gb, q) : __shfl_sync(0xffffffffu, ga, q);
+                    const int32_t gbq = __shfl_sync(0xffffffffu, gb, q), gaq = __shfl_sync(0xffffffffu, ga, q);
+                    int32_t y = qa ? gbq : gaq;
                     // the other root's stamp and mask, staged by the whole CTA
                     const int sb = qa ? 1 : 0;
                     const unsigned long long xy = s_res[sb][gq];
