@@ -551,7 +551,12 @@ __device__ __forceinline__ bool try_carry1(const unsigned long long* p, unsigned
 // exactly the serial chain's, so the result does not depend on timing.
 // Probes kLB segments per step (all their words loaded before any test), so a
 // walk of d segments costs ~d / kLB memory latencies.
-constexpr int kLB = 4;
+// (per kernel: kLB probes cost 18 kLB registers; the up pass, which also holds
+// light-child rows, probes 2, the down pass 4 -- both stay at 5 CTAs / SM)
+#ifndef HDP_KLB_UP
+#define HDP_KLB_UP 2
+#endif
+constexpr int kLBUp = HDP_KLB_UP, kLBDown = 4;
 
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
     unsigned long long w;
@@ -559,6 +564,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
     return w;
 }
 
+template <int kLB>
 __device__ __forceinline__ float4 seg_lookback(const AggArgs& a, int64_t gseg, int dir, int kmax,
                                                unsigned epoch, int jq, bool act, float4 edge) {
     const size_t lw = (size_t)a.max_mp;
@@ -683,10 +689,15 @@ __device__ __forceinline__ int seg_stage(const AggArgs& a, const SegCtx& c, int 
 // columns).  Segments are taken by ticket in reverse table order, so a
 // path's tail segment comes first; the carry is X_a = x_loc(a) + P * X_b with
 // P = prod s_{a+1..b}.
-__device__ __forceinline__ void seg_up_item(const AggArgs& a, int64_t gseg, int g, float4* buf,
+// light-child rows loaded per batch (registers: 4 per row)
+#ifndef HDP_GATHER
+#define HDP_GATHER 4
+#endif
+constexpr int kGather = HDP_GATHER;
+
+__device__ __forceinline__ void seg_up_item(const AggArgs& a, const SegCtx& c, int g, float4* buf,
                                             unsigned long long* bar, unsigned& par, int lane) {
     PROF_DECL;
-    const SegCtx c = seg_ctx(a, gseg);
     const int mq = c.mp >> 2;
     if (g * 32 >= mq) return;
     const int jq = g * 32 + lane;
@@ -701,7 +712,7 @@ __device__ __forceinline__ void seg_up_item(const AggArgs& a, int64_t gseg, int 
     int E0 = 0, E1 = 0, e0n = 0, e1n = 0;
     long long rowe = 0;
     float sime = 0.0f;
-    float4 vpre[8];
+    float4 vpre[kGather];
     if (a.seg_light) {
         E0 = c.e0;
         E1 = c.e1;
@@ -716,7 +727,7 @@ __device__ __forceinline__ void seg_up_item(const AggArgs& a, int64_t gseg, int 
                 sime = a.lc_sim[E0 + lane];
             }
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
+            for (int j = 0; j < kGather; j++) {
                 const long long r = __shfl_sync(0xffffffffu, rowe, j);
                 vpre[j] = (E0 + j < E1 && act) ? reinterpret_cast<const float4*>(a.aup + r)[jq]
                                                : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -741,21 +752,21 @@ __device__ __forceinline__ void seg_up_item(const AggArgs& a, int64_t gseg, int 
                         sime = a.lc_sim[e];
                     }
                 }
-                for (int j0 = 0; j0 < ne; j0 += 8) {
-                    float4 v[8];
+                for (int j0 = 0; j0 < ne; j0 += kGather) {
+                    float4 v[kGather];
                     if (eb == E0 && j0 == 0) {
 #pragma unroll
-                        for (int j = 0; j < 8; j++) v[j] = vpre[j];
+                        for (int j = 0; j < kGather; j++) v[j] = vpre[j];
                     } else {
 #pragma unroll
-                        for (int j = 0; j < 8; j++) {
+                        for (int j = 0; j < kGather; j++) {
                             const long long r = __shfl_sync(0xffffffffu, rowe, (j0 + j) & 31);
                             v[j] = (j0 + j < ne && act) ? reinterpret_cast<const float4*>(a.aup + r)[jq]
                                                         : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                         }
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; j++) {
+                    for (int j = 0; j < kGather; j++) {
                         if (j0 + j >= ne) break;
                         const int ee = eb + j0 + j;
                         const float sc = __shfl_sync(0xffffffffu, sime, j0 + j);
@@ -805,7 +816,7 @@ __device__ __forceinline__ void seg_up_item(const AggArgs& a, int64_t gseg, int 
     }
     PROF_T(3);
     float4 Xb = z;
-    if (has_next) Xb = seg_lookback(a, c.gseg, +1, c.nseg - 1 - c.s, a.epoch_up, jq, act, z);
+    if (has_next) Xb = seg_lookback<kLBUp>(a, c.gseg, +1, c.nseg - 1 - c.s, a.epoch_up, jq, act, z);
     PROF_T(4);
     if (act && c.s > 0) {
         float4 o;
@@ -844,10 +855,12 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0
     if (lane == 0) mbar_init(&bars[warp], 1);
     __syncwarp();
     unsigned par = 0;
+    // (taking the next ticket while the current segment runs was measured
+    // slower: a ticket held by a busy warp stalls the look-backs behind it)
     for (;;) {
         const int t = warp_ticket(ctr + g);
         if (t >= ng) break;
-        seg_up_item(a, g0 + ng - 1 - t, g, buf, &bars[warp], par, lane);
+        seg_up_item(a, seg_ctx(a, g0 + ng - 1 - t), g, buf, &bars[warp], par, lane);
     }
 }
 
@@ -857,10 +870,9 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_up(AggArgs a, int64_t g0
 // each node over this warp's columns is folded into the node's key (64-bit
 // min when several warps share a row, a store otherwise); A is written back
 // only where a light child will read it.
-__device__ __forceinline__ void seg_down_item(const AggArgs& a, int64_t gseg, int g, float4* buf,
+__device__ __forceinline__ void seg_down_item(const AggArgs& a, const SegCtx& c, int g, float4* buf,
                                               unsigned long long* bar, unsigned& par, int lane) {
     PROF_DECL;
-    const SegCtx c = seg_ctx(a, gseg);
     const int mq = c.mp >> 2;
     if (g * 32 >= mq) return;
     const int jq = g * 32 + lane;
@@ -898,7 +910,7 @@ __device__ __forceinline__ void seg_down_item(const AggArgs& a, int64_t gseg, in
         if (lane == 0) put_carry(a.aggp + c.gseg, a.epoch_down, Q);
     }
     PROF_T(2);
-    const float4 Yin = c.s == 0 ? Ypar : seg_lookback(a, c.gseg, -1, c.s, a.epoch_down, jq, act, Ypar);
+    const float4 Yin = c.s == 0 ? Ypar : seg_lookback<kLBDown>(a, c.gseg, -1, c.s, a.epoch_down, jq, act, Ypar);
     PROF_T(3);
     if (act && c.s + 1 < c.nseg) {
         float4 o;
@@ -955,7 +967,7 @@ __global__ void __launch_bounds__(32 * kSegWarps) k_seg_down(AggArgs a, int64_t 
     for (;;) {
         const int t = warp_ticket(ctr + g);
         if (t >= ng) break;
-        seg_down_item(a, g0 + t, g, buf, &bars[warp], par, lane);
+        seg_down_item(a, seg_ctx(a, g0 + t), g, buf, &bars[warp], par, lane);
     }
 }
 
@@ -1177,7 +1189,10 @@ __device__ __forceinline__ ChunkSm stage_chunk(const AggArgs& a, const ChunkDesc
 // (the operation order of k_light + k_scan_up_short).  One thread per
 // (path, float4 column); changed rows are stored, a lone leaf row (A_up = E)
 // is left alone.
-__global__ void __launch_bounds__(kChunkThreads) k_up_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
+#ifndef HDP_UP_CHUNK_MINB
+#define HDP_UP_CHUNK_MINB 5
+#endif
+__global__ void __launch_bounds__(kChunkThreads, HDP_UP_CHUNK_MINB) k_up_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
                                                             int64_t cbase, int64_t nc) {
     extern __shared__ float4 sm4[];
     __shared__ unsigned long long bar;
