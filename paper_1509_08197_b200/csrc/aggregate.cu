@@ -249,6 +249,68 @@ __global__ void __launch_bounds__(256) k_ecost_range(AggArgs a, const int32_t* _
     }
 }
 
+// Range lanes, rows of at most 32 U floats (the common case): the same tile,
+// but the window is staged from virtual column c0 - x0 - (mp - 1) (columns
+// left of the image zero-filled), so lane j of the node in tile column q reads
+// window entry q + mp - 1 - j with no clamping: one base address per node,
+// compile-time offsets for the U lane blocks, border / padding by selects.
+// Roughly 15 instructions per hypothesis (was ~50: the k_ecost_range loop
+// was issue-bound at 92 % in ncu).
+template <int U>
+__global__ void __launch_bounds__(256) k_ecost_range_u(AggArgs a, const int32_t* __restrict__ lpos, int m) {
+    extern __shared__ float4 win[];
+    __shared__ long long srow[kETile];
+    __shared__ float4 sL[kETile];
+    const int64_t base = (int64_t)blockIdx.x * a.w;  // node id of column 0 of this image row
+    const int c0 = (int)blockIdx.y * kETile;
+    const int mp = (m + 3) & ~3;
+    const int v0 = c0 - a.range_x0 - (mp - 1);  // column of window entry 0
+    const int hi = min(a.w, c0 + kETile);
+    const int nt = hi - c0;
+    const int nwin = hi - v0;
+    for (int i = threadIdx.x; i < nwin; i += 256) {
+        const int x = v0 + i;
+        win[i] = x >= 0 ? __ldg(a.pr + base + x) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+    for (int i = threadIdx.x; i < nt; i += 256) {
+        srow[i] = __ldg(a.rowoff + __ldg(lpos + base + c0 + i));
+        sL[i] = __ldg(a.pl + base + c0 + i);
+    }
+    __syncthreads();
+    const float wc = 1.0f - a.alpha;
+    const float border = a.border;
+    const int lane = threadIdx.x & 31;
+    // blocks 0 .. U-2 are full (32 (U-1) < mp) and hold no padding lanes
+    // (m > mp - 4 >= 32 (U-1) - 3 and mp is a multiple of 4 > 32 (U-1));
+    // only the last block needs the row-end guard and the padding select
+    const int jl = lane + 32 * (U - 1);
+    for (int q = threadIdx.x >> 5; q < nt; q += 8) {
+        const float4 L = sL[q];
+        float* out = a.aup + srow[q] + lane;
+        const int xl = c0 + q - a.range_x0;  // lanes j > xl reach left of the image
+        const float4* wp = win + (q + mp - 1 - lane);
+        if (xl >= mp - 1) {  // warp-uniform: no lane reaches the border
+#pragma unroll
+            for (int u = 0; u < U - 1; u++) out[32 * u] = pix_cost(a, wc, L, wp[-32 * u]);
+            if (jl < mp) {
+                const float e = pix_cost(a, wc, L, wp[-32 * (U - 1)]);
+                out[32 * (U - 1)] = jl >= m ? kPadCost : e;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U - 1; u++) {
+                const float e = pix_cost(a, wc, L, wp[-32 * u]);
+                out[32 * u] = lane + 32 * u > xl ? border : e;
+            }
+            if (jl < mp) {
+                float e = pix_cost(a, wc, L, wp[-32 * (U - 1)]);
+                e = jl > xl ? border : e;
+                out[32 * (U - 1)] = jl >= m ? kPadCost : e;
+            }
+        }
+    }
+}
+
 // RANGE: lane j is disparity range_x0 + j (dense / slab lanes); otherwise the
 // tree's lane list.  SMEM: the right-image window fits in shared memory.
 template <bool RANGE, bool SMEM>
@@ -1691,7 +1753,22 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         if (a.range_x0 >= 0) {
             const int m = f->max_m, mp = (m + 3) & ~3;
             const unsigned inv = (unsigned)((0x100000000ull + mp - 1) / mp);  // t / mp by multiply-high
-            if (use) k_ecost_range<true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d, m, inv);
+            const int U = (mp + 31) / 32;
+            const size_t usmem = (size_t)(kETile + a.range_x0 + mp - 1) * sizeof(float4);
+            bool done = false;
+            if (usmem <= 48 * 1024 && U <= 17) {
+                done = true;
+                switch (U) {
+#define HDP_ECU(n) case n: k_ecost_range_u<n><<<g, 256, usmem, st>>>(a, f->lpos.get(), m); break;
+                    HDP_ECU(1) HDP_ECU(2) HDP_ECU(3) HDP_ECU(4) HDP_ECU(5) HDP_ECU(6) HDP_ECU(7) HDP_ECU(8)
+                    HDP_ECU(9) HDP_ECU(10) HDP_ECU(11) HDP_ECU(12) HDP_ECU(13) HDP_ECU(14) HDP_ECU(15)
+                    HDP_ECU(16) HDP_ECU(17)
+#undef HDP_ECU
+                    default: done = false;
+                }
+            }
+            if (done) {
+            } else if (use) k_ecost_range<true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d, m, inv);
             else k_ecost_range<false><<<g, 256, 0, st>>>(a, f->lpos.get(), f->max_d, m, inv);
         } else {
             if (use) k_ecost_pix<false, true><<<g, 256, smem, st>>>(a, f->lpos.get(), f->max_d);
