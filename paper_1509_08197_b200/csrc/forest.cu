@@ -113,26 +113,73 @@ __global__ void k_tree_ids(int64_t n, const int32_t* __restrict__ root,
     if (v < n) tree_id[v] = tindex[root[v]];
 }
 
-__global__ void k_make_arcs(int64_t m, const int32_t* __restrict__ tu, const int32_t* __restrict__ tv,
-                            const float* __restrict__ tw, uint64_t* akey, float* aw,
-                            int32_t* deg) {
+// CSR adjacency without a global sort: arcs are dropped into their source's
+// slots (atomic cursor per source), then every source orders its few slots by
+// destination (insertion sort; heap sort for the rare high-degree node).
+__global__ void k_arc_degree(int64_t m, const int32_t* __restrict__ tu, const int32_t* __restrict__ tv,
+                             int32_t* deg) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m) return;
-    int32_t u = tu[e], v = tv[e];
-    akey[2 * e] = ((uint64_t)(uint32_t)u << 32) | (uint32_t)v;
-    akey[2 * e + 1] = ((uint64_t)(uint32_t)v << 32) | (uint32_t)u;
-    aw[2 * e] = tw[e];
-    aw[2 * e + 1] = tw[e];
-    atomicAdd(&deg[u], 1);
-    atomicAdd(&deg[v], 1);
+    atomicAdd(&deg[tu[e]], 1);
+    atomicAdd(&deg[tv[e]], 1);
 }
 
-__global__ void k_arc_unpack(int64_t na, const uint64_t* __restrict__ akey, int32_t* asrc,
-                             int32_t* adst) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    asrc[i] = (int32_t)(akey[i] >> 32);
-    adst[i] = (int32_t)(akey[i] & 0xffffffffu);
+__global__ void k_arc_place(int64_t m, const int32_t* __restrict__ tu, const int32_t* __restrict__ tv,
+                            const float* __restrict__ tw, const int32_t* __restrict__ adj_start,
+                            int32_t* cur, int32_t* asrc, int32_t* adst, float* aw) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const int32_t u = tu[e], v = tv[e];
+    const float w = tw[e];
+    const int32_t su = adj_start[u] + atomicAdd(&cur[u], 1);
+    const int32_t sv = adj_start[v] + atomicAdd(&cur[v], 1);
+    asrc[su] = u;
+    adst[su] = v;
+    aw[su] = w;
+    asrc[sv] = v;
+    adst[sv] = u;
+    aw[sv] = w;
+}
+
+__device__ void adj_sift(int32_t* d, float* w, int root, int cnt) {
+    for (;;) {
+        int c = 2 * root + 1;
+        if (c >= cnt) return;
+        if (c + 1 < cnt && d[c + 1] > d[c]) c++;
+        if (d[root] >= d[c]) return;
+        int32_t td = d[root]; d[root] = d[c]; d[c] = td;
+        float tw = w[root]; w[root] = w[c]; w[c] = tw;
+        root = c;
+    }
+}
+
+__global__ void k_arc_sort(int64_t n, const int32_t* __restrict__ adj_start, int32_t* adst, float* aw) {
+    int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
+    const int32_t a = adj_start[x], cnt = adj_start[x + 1] - a;
+    int32_t* d = adst + a;
+    float* w = aw + a;
+    if (cnt <= 16) {
+        for (int i = 1; i < cnt; i++) {
+            const int32_t kd = d[i];
+            const float kw = w[i];
+            int j = i - 1;
+            while (j >= 0 && d[j] > kd) {
+                d[j + 1] = d[j];
+                w[j + 1] = w[j];
+                j--;
+            }
+            d[j + 1] = kd;
+            w[j + 1] = kw;
+        }
+        return;
+    }
+    for (int r = cnt / 2 - 1; r >= 0; r--) adj_sift(d, w, r, cnt);
+    for (int end = cnt - 1; end > 0; end--) {
+        int32_t td = d[0]; d[0] = d[end]; d[end] = td;
+        float tw = w[0]; w[0] = w[end]; w[end] = tw;
+        adj_sift(d, w, 0, end);
+    }
 }
 
 // twin arc (y -> x) of arc i = (x -> y): binary search in y's sorted list.
@@ -806,34 +853,29 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     tr.mark("2 components/roots");
     // ---- 3. CSR adjacency (arcs sorted by (src, dst))
     const int64_t na = 2 * m;
-    DevBuf<uint64_t> akey, akey2;
-    DevBuf<float> aw, aw2;
+    DevBuf<float> aw2;
     DevBuf<int32_t> deg, adj_start, asrc, adst;
-    HDP_TRY(akey.alloc(na + 1, st));
-    HDP_TRY(akey2.alloc(na + 1, st));
-    HDP_TRY(aw.alloc(na + 1, st));
     HDP_TRY(aw2.alloc(na + 1, st));
     HDP_TRY(deg.alloc(n + 1, st));
     HDP_TRY(adj_start.alloc(n + 1, st));
+    HDP_TRY(asrc.alloc(na + 1, st));
+    HDP_TRY(adst.alloc(na + 1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(deg.get(), 0, (n + 1) * sizeof(int32_t), st));
     if (m > 0) {
-        k_make_arcs<<<grid_for(m, B), B, 0, st>>>(m, tu.get(), tv.get(), tw.get(), akey.get(),
-                                                 aw.get(), deg.get()); note_launch();
-        // by (src, dst); with a lexicographic edge list the arcs of a source
-        // already come in ascending dst, so a stable sort on src suffices
-        HDP_TRY(sort_pairs(akey.get(), akey2.get(), aw.get(), aw2.get(), na, lex ? 32 : 0,
-                           32 + bits_for(n), st));
+        k_arc_degree<<<grid_for(m, B), B, 0, st>>>(m, tu.get(), tv.get(), deg.get()); note_launch();
     }
     HDP_TRY(exclusive_sum(deg.get(), adj_start.get(), n + 1, st));
+    if (m > 0) {
+        // deg doubles as the per-source cursor
+        HDP_CHECK_CUDA(cudaMemsetAsync(deg.get(), 0, (n + 1) * sizeof(int32_t), st));
+        k_arc_place<<<grid_for(m, B), B, 0, st>>>(m, tu.get(), tv.get(), tw.get(), adj_start.get(), deg.get(),
+                                                 asrc.get(), adst.get(), aw2.get()); note_launch();
+        k_arc_sort<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), adst.get(), aw2.get()); note_launch();
+    }
+    (void)lex;
     tu.release();
     tv.release();
     tw.release();
-    akey.release();
-    aw.release();
-    HDP_TRY(asrc.alloc(na + 1, st));
-    HDP_TRY(adst.alloc(na + 1, st));
-    if (na > 0) k_arc_unpack<<<grid_for(na, B), B, 0, st>>>(na, akey2.get(), asrc.get(), adst.get()); note_launch();
-    akey2.release();
 
     tr.mark("3 csr adjacency");
     // ---- 4. Euler tour + list ranking
