@@ -353,11 +353,15 @@ __global__ void k_root_init(int64_t n, const int32_t* __restrict__ root,
 }
 
 __global__ void k_depth_gather(int64_t n, const int32_t* __restrict__ down_arc,
-                               const int32_t* __restrict__ scanned, int32_t* depth) {
+                               const int32_t* __restrict__ scanned, int32_t* depth, int32_t* dmax) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    int32_t a = down_arc[v];
-    if (a >= 0) depth[v] = scanned[a];
+    int32_t d = 0;
+    if (v < n) {
+        int32_t a = down_arc[v];
+        if (a >= 0) depth[v] = d = scanned[a];
+    }
+    d = __reduce_max_sync(0xffffffffu, d);
+    if ((threadIdx.x & 31) == 0 && d > 0) atomicMax(dmax, d);
 }
 
 // heavy child: largest subtree among children, ties -> lower id (adjacency
@@ -381,36 +385,99 @@ __global__ void k_heavy(int64_t n, const int32_t* __restrict__ adj_start,
 }
 
 // heavy-path heads: word = (heavy parent or self, distance)
-__global__ void k_hp_init(int64_t n, const int32_t* __restrict__ parent,
-                          const int32_t* __restrict__ heavy, uint64_t* word) {
+// Heavy-path heads and distances by a ruling set.  Rulers: every path head
+// (root or light child) and every heavy child at a depth divisible by kHpRuler.
+// Each node walks up (< kHpRuler parent steps) to its nearest ruler; the
+// non-head rulers, about n / kHpRuler of them, pointer-jump to their heads.
+constexpr int kHpRuler = 8;
+
+// pr[v] = parent | ruler flag << 31
+__global__ void k_hp_flags(int64_t n, const int32_t* __restrict__ parent, const int32_t* __restrict__ heavy,
+                           const int32_t* __restrict__ depth, int32_t* pr) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    int32_t p = parent[v];
-    bool on = (p != v) && heavy[p] == v;
-    word[v] = ((uint64_t)(uint32_t)(on ? p : (int32_t)v) << 32) | (on ? 1u : 0u);
+    const int32_t p = parent[v];
+    const bool on = (p != v) && heavy[p] == v;  // heavy child: not a head
+    const bool ruler = !on || depth[v] % kHpRuler == 0;
+    pr[v] = p | (ruler ? (int32_t)0x80000000 : 0);
 }
 
-__global__ void k_hp_jump(int64_t n, const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
+__device__ __forceinline__ uint64_t hp_word(int32_t ptr, int32_t d) {
+    return ((uint64_t)(uint32_t)ptr << 32) | (uint32_t)d;
+}
+
+// near[v] = (nearest ruler at or above v, steps); heads get the terminal word
+// in both jump buffers, non-head rulers their next ruler up and a list slot
+__global__ void k_hp_walk(int64_t n, const int32_t* __restrict__ pr, const int32_t* __restrict__ parent,
+                          const int32_t* __restrict__ heavy, uint64_t* nearw, uint64_t* wa, uint64_t* wb,
+                          int32_t* list, int32_t* cnt) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool listed = false;
     if (v < n) {
+        int32_t x = pr[v];
+        int32_t cur = (int32_t)v, s = 0;
+        while (x >= 0) {  // not a ruler: one step up the heavy path
+            cur = x;
+            s++;
+            x = pr[cur];
+        }
+        nearw[v] = hp_word(cur, s);
+        const int32_t p = parent[v];
+        const bool head = !((p != v) && heavy[p] == v);
+        if (head) {
+            wa[v] = wb[v] = hp_word((int32_t)v, 0);
+        } else if (s == 0) {  // a non-head ruler: its next ruler up
+            int32_t c = p, t = 1;
+            int32_t y = pr[c];
+            while (y >= 0) {
+                c = y;
+                t++;
+                y = pr[c];
+            }
+            wa[v] = hp_word(c, t);
+            listed = true;
+        }
+    }
+    // warp-aggregated list append (order is irrelevant for pointer jumping)
+    const unsigned m = __ballot_sync(0xffffffffu, listed);
+    int base = 0;
+    const int lane = threadIdx.x & 31;
+    if (lane == 0 && m) base = atomicAdd(cnt, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (listed) list[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)v;
+}
+
+// a chain of non-head rulers is at most max depth / kHpRuler + 1 long
+__device__ __forceinline__ long long hp_chain(const int32_t* dmax) { return (long long)*dmax / kHpRuler + 1; }
+
+__global__ void k_hp_jump(const int32_t* __restrict__ list, const int32_t* __restrict__ cnt,
+                          const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+                          const int32_t* __restrict__ dmax, int r) {
+    if ((1ll << r) >= hp_chain(dmax)) return;
+    const int32_t nl = *cnt;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = list[i];
         const uint64_t w = in[v];
         const int32_t h = (int32_t)(w >> 32);
         const uint64_t w2 = in[h];
         const int32_t hh = (int32_t)(w2 >> 32);
-        if (hh != h) {
-            out[v] = ((uint64_t)(uint32_t)hh << 32) | (uint32_t)((uint32_t)w + (uint32_t)w2);
-        } else {
-            out[v] = w;
-        }
+        out[v] = hh != h ? hp_word(hh, (int32_t)((uint32_t)w + (uint32_t)w2)) : w;
     }
 }
 
-__global__ void k_hp_unpack(int64_t n, const uint64_t* __restrict__ word, int32_t* hp, int32_t* dist) {
+// the jumped words are in buffer a after an even number of executed rounds
+__global__ void k_hp_unpack(int64_t n, const uint64_t* __restrict__ nearw, const uint64_t* __restrict__ a,
+                            const uint64_t* __restrict__ b, const int32_t* __restrict__ dmax, int rounds,
+                            int32_t* hp, int32_t* dist) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    const uint64_t w = word[v];
+    const long long ch = hp_chain(dmax);
+    int done = 0;
+    while (done < rounds && (1ll << done) < ch) done++;
+    const uint64_t nw = nearw[v];
+    const uint64_t w = ((done & 1) ? b : a)[(int32_t)(nw >> 32)];
     hp[v] = (int32_t)(w >> 32);
-    dist[v] = (int32_t)(uint32_t)w;
+    dist[v] = (int32_t)((uint32_t)nw + (uint32_t)w);
 }
 
 // light-edge steps for the light-depth scan: entering / leaving a path head.
@@ -934,7 +1001,9 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(f->pweight.alloc(n, st));
     HDP_TRY(f->size.alloc(n, st));
     HDP_TRY(f->depth.alloc(n, st));
-    DevBuf<int32_t> down_arc, steps, scanned;
+    DevBuf<int32_t> down_arc, steps, scanned, dmax;
+    HDP_TRY(dmax.alloc(1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(dmax.get(), 0, sizeof(int32_t), st));
     HDP_TRY(down_arc.alloc(n, st));
     HDP_TRY(steps.alloc(na + 1, st));
     HDP_TRY(scanned.alloc(na + 1, st));
@@ -947,7 +1016,8 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                f->parent.get(), f->pweight.get(), f->size.get(),
                                                down_arc.get(), steps.get()); note_launch();
         HDP_TRY(inclusive_sum(steps.get(), scanned.get(), na, st));
-        k_depth_gather<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), f->depth.get()); note_launch();
+        k_depth_gather<<<grid_for(n, B), B, 0, st>>>(n, down_arc.get(), scanned.get(), f->depth.get(),
+                                                     dmax.get()); note_launch();
     }
     HDP_CHECK_LAUNCH();
     aw2.release();
@@ -962,16 +1032,29 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     k_heavy<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), adst.get(), f->parent.get(),
                                           f->size.get(), heavy.get()); note_launch();
     {
-        DevBuf<uint64_t> hw, hw2;
-        const int rounds = ceil_log2((int64_t)max_tree + 1);  // depth < the largest tree
+        DevBuf<uint64_t> hw, hw2, nearw;
+        DevBuf<int32_t> pr, hlist, hcnt;
+        // ruler chains are at most (largest tree) / kHpRuler + 1 long
+        const int rounds = ceil_log2((int64_t)max_tree / kHpRuler + 2);
         HDP_TRY(hw.alloc(n, st));
         HDP_TRY(hw2.alloc(n, st));
-        k_hp_init<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), hw.get()); note_launch();
+        HDP_TRY(nearw.alloc(n, st));
+        HDP_TRY(pr.alloc(n, st));
+        HDP_TRY(hlist.alloc(n, st));
+        HDP_TRY(hcnt.alloc(1, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(hcnt.get(), 0, sizeof(int32_t), st));
+        k_hp_flags<<<grid_for(n, B), B, 0, st>>>(n, f->parent.get(), heavy.get(), f->depth.get(), pr.get()); note_launch();
+        uint64_t* ba = hw.get();
+        uint64_t* bb = hw2.get();
+        k_hp_walk<<<grid_for(n, B), B, 0, st>>>(n, pr.get(), f->parent.get(), heavy.get(), nearw.get(), ba, bb,
+                                                hlist.get(), hcnt.get()); note_launch();
+        const int jg = (int)std::min<int64_t>(grid_for(n / kHpRuler + 1, B), 148 * 8);
         for (int r = 0; r < rounds; r++) {
-            k_hp_jump<<<grid_for(n, B), B, 0, st>>>(n, hw.get(), hw2.get()); note_launch();
-            std::swap(hw.p, hw2.p);
+            k_hp_jump<<<jg, B, 0, st>>>(hlist.get(), hcnt.get(), (r & 1) ? bb : ba, (r & 1) ? ba : bb, dmax.get(), r);
+            note_launch();
         }
-        k_hp_unpack<<<grid_for(n, B), B, 0, st>>>(n, hw.get(), hp.get(), dist.get()); note_launch();
+        k_hp_unpack<<<grid_for(n, B), B, 0, st>>>(n, nearw.get(), ba, bb, dmax.get(), rounds, hp.get(), dist.get());
+        note_launch();
     }
     HDP_CHECK_LAUNCH();
     heavy.release();
