@@ -1421,27 +1421,43 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
             if (lane == 0 && a.keys)
                 a.keys[mt.x] = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, mt.y, (int)jm);
         }
-    } else
-    for (int i = threadIdx.x; i < d.nk; i += blockDim.x) {
-        const int4 mt = s.meta[i];
-        const int mq = (mt.w + 3) >> 2;
-        const float4* row = reinterpret_cast<const float4*>(s.own + (s.nrow[i] - d.a0));
-        // the minimum (padding lanes hold kPadCost and never win), then the
-        // first lane holding it
-        float best = row[0].x;
-        for (int jq = 0; jq < mq; jq++) {
-            const float4 y = row[jq];
-            best = fminf(best, fminf(fminf(y.x, y.y), fminf(y.z, y.w)));
+    } else {
+        // four threads per node, each keeping the first minimum of its
+        // interleaved float4 columns, then (value, lane) minima over the four
+        // (smallest value, then smallest index: np.argmin's first minimum)
+        const int sub = threadIdx.x & 3;
+        for (int i0 = 0; i0 < d.nk; i0 += kChunkThreads / 4) {
+            const int i = i0 + (threadIdx.x >> 2);
+            const bool ok = i < d.nk;
+            int4 mt = make_int4(0, 0, 0, 0);
+            float best = __int_as_float(0x7f800000);
+            int bj = 0x7fffffff;
+            if (ok) {
+                mt = s.meta[i];
+                const int mq = (mt.w + 3) >> 2;
+                const float4* row = reinterpret_cast<const float4*>(s.own + (s.nrow[i] - d.a0));
+                for (int jq = sub; jq < mq; jq += 4) {
+                    const float4 y = row[jq];
+                    const int j = 4 * jq;  // padding lanes hold kPadCost and never win
+                    if (y.x < best) { best = y.x; bj = j; }
+                    if (y.y < best) { best = y.y; bj = j + 1; }
+                    if (y.z < best) { best = y.z; bj = j + 2; }
+                    if (y.w < best) { best = y.w; bj = j + 3; }
+                }
+            }
+            uint32_t ob = bj == 0x7fffffff ? 0xffffffffu : ord_f32(best);
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                const uint32_t o2 = __shfl_xor_sync(0xffffffffu, ob, off);
+                const int j2 = __shfl_xor_sync(0xffffffffu, bj, off);
+                if (o2 < ob || (o2 == ob && j2 < bj)) {
+                    ob = o2;
+                    bj = j2;
+                }
+            }
+            if (ok && sub == 0 && a.keys)
+                a.keys[mt.x] = ((unsigned long long)ob << 32) | (uint32_t)lane_disp(a, mt.y, bj);
         }
-        int bj = 0;
-        for (int jq = 0; jq < mq; jq++) {
-            const float4 y = row[jq];
-            if (y.x == best) { bj = 4 * jq; break; }
-            if (y.y == best) { bj = 4 * jq + 1; break; }
-            if (y.z == best) { bj = 4 * jq + 2; break; }
-            if (y.w == best) { bj = 4 * jq + 3; break; }
-        }
-        if (a.keys) a.keys[mt.x] = ((unsigned long long)ord_f32(best) << 32) | (uint32_t)lane_disp(a, mt.y, bj);
     }
     fence_proxy_async();  // the next chunk's bulk copies overwrite shared memory
     __syncthreads();

@@ -174,13 +174,13 @@ __global__ void __launch_bounds__(256) k_mst_coop(int64_t gm, int64_t gn, const 
     cg::grid_group grid = cg::this_grid();
     const int64_t tid = (int64_t)grid.thread_rank(), nthr = (int64_t)grid.size();
     int r = 0;
+    for (int64_t t = tid; t < gn; t += nthr) {
+        const int32_t v = reps[t];
+        best[v] = ~0ull;
+        win[v] = -1;
+    }
+    grid.sync();
     while (r < max_rounds) {
-        for (int64_t t = tid; t < gn; t += nthr) {
-            const int32_t v = reps[t];
-            best[v] = ~0ull;
-            win[v] = -1;
-        }
-        grid.sync();
         for (int64_t e = tid; e < gm; e += nthr) {
             if (!alive[e]) continue;
             const int32_t cu = comp[gu[e]], cv = comp[gv[e]];
@@ -227,11 +227,15 @@ __global__ void __launch_bounds__(256) k_mst_coop(int64_t gm, int64_t gn, const 
         }
         if (__syncthreads_or(hooked) && threadIdx.x == 0 && *(volatile int*)(flags + r) == 0) flags[r] = 1;
         grid.sync();
+        // relabel, and reset the next round's minima (hook, the last reader of
+        // win, is behind the barrier above)
         for (int64_t t = tid; t < gn; t += nthr) {
             const int32_t v = reps[t];
             int32_t x = comp[v];
             while (link[x] != x) x = link[x];
             comp[v] = x;
+            best[v] = ~0ull;
+            win[v] = -1;
         }
         grid.sync();
         const bool more = *(volatile int*)(flags + r) != 0;
@@ -365,6 +369,14 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
                 HDP_CHECK_CUDA(cudaGetDevice(&dev));
                 HDP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
                 HDP_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_mst_coop, 256, 0));
+                {
+                    // a grid barrier costs more with more CTAs: cap the grid
+                    static const int cap = [] {
+                        const char* e = getenv("HDP_MST_COOP_BPS");  // tuning: CTAs per SM
+                        return e && *e ? atoi(e) : 0;
+                    }();
+                    if (cap > 0 && cap < nb) nb = cap;
+                }
                 int* fl = hooks.get() + kMaxRounds;  // per-round hook flags of this phase (zeroed)
                 int* rc = hooks.get() + 2 * kMaxRounds - 1;
                 int max_r = kMaxRounds - rounds - 1;
