@@ -984,7 +984,6 @@ __device__ __forceinline__ void seg_down_item(const AggArgs& a, const SegCtx& c,
     }
     float4* rows = reinterpret_cast<float4*>(a.aup + c.rowa) + jq;
     float4 y = Yin;
-    const int j0 = 4 * jq;
 #pragma unroll 4
     for (int i = 0; i < cnt; i++) {
         const float sv = seg_pick(s_lo, 0.0f, i);
@@ -994,23 +993,49 @@ __device__ __forceinline__ void seg_down_item(const AggArgs& a, const SegCtx& c,
         y.y = sv * y.y + w * v.y;
         y.z = sv * y.z + w * v.z;
         y.w = sv * y.w + w * v.w;
-        if (act && ((lmask >> i) & 1u)) rows[(int64_t)i * mq] = y;
-        // first minimum over this lane's four columns (padding never wins)
-        float best = y.x;
-        int bj = j0;
-        if (y.y < best) { best = y.y; bj = j0 + 1; }
-        if (y.z < best) { best = y.z; bj = j0 + 2; }
-        if (y.w < best) { best = y.w; bj = j0 + 3; }
-        const uint32_t ob = act ? ord_f32(best) : 0xffffffffu;
-        const uint32_t mn = __reduce_min_sync(0xffffffffu, ob);
-        const uint32_t jm = __reduce_min_sync(0xffffffffu, ob == mn ? (uint32_t)bj : 0xffffffffu);
-        const int node = __shfl_sync(0xffffffffu, n_lo, i);
-        if (lane == 0 && a.keys) {
-            const unsigned long long key = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, c.doff, (int)jm);
-            if (a.atomic_keys)
-                atomicMin(&a.keys[node], key);
-            else
-                a.keys[node] = key;
+        if (act) {
+            if ((lmask >> i) & 1u) rows[(int64_t)i * mq] = y;
+            buf[i * rs + lane] = y;  // A replaces A_up in the staged rows
+        }
+    }
+    __syncwarp();
+    // first minimum of every node over this warp's columns: four lanes per
+    // node over interleaved float4 columns, then (value, index) minima
+    if (a.keys) {
+        const int wq = min(32, mq - 32 * g);  // float4 columns of this group
+        const int sub = lane & 3;
+        for (int i0 = 0; i0 < cnt; i0 += 8) {
+            const int i = i0 + (lane >> 2);
+            float best = __int_as_float(0x7f800000);
+            int bj = 0x7fffffff;
+            if (i < cnt) {
+                for (int l = sub; l < wq; l += 4) {
+                    const float4 yv = buf[i * rs + l];
+                    const int j = 4 * (32 * g + l);  // padding lanes hold kPadCost and never win
+                    if (yv.x < best) { best = yv.x; bj = j; }
+                    if (yv.y < best) { best = yv.y; bj = j + 1; }
+                    if (yv.z < best) { best = yv.z; bj = j + 2; }
+                    if (yv.w < best) { best = yv.w; bj = j + 3; }
+                }
+            }
+            uint32_t ob = bj == 0x7fffffff ? 0xffffffffu : ord_f32(best);
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                const uint32_t o2 = __shfl_xor_sync(0xffffffffu, ob, off);
+                const int j2 = __shfl_xor_sync(0xffffffffu, bj, off);
+                if (o2 < ob || (o2 == ob && j2 < bj)) {
+                    ob = o2;
+                    bj = j2;
+                }
+            }
+            const int node = __shfl_sync(0xffffffffu, n_lo, i & 31);
+            if (i < cnt && sub == 0 && bj != 0x7fffffff) {
+                const unsigned long long key = ((unsigned long long)ob << 32) | (uint32_t)lane_disp(a, c.doff, bj);
+                if (a.atomic_keys)
+                    atomicMin(&a.keys[node], key);
+                else
+                    a.keys[node] = key;
+            }
         }
     }
     PROF_PUT(4, lane == 0, cnt | (c.s << 8) | ((c.s + 1 < c.nseg ? 1 : 0) << 30));
