@@ -193,6 +193,21 @@ void hdp_forest_destroy(hdp_forest *f);
 int hdp_keys_unpack(const uint64_t *keys, int64_t n, int32_t *disp, float *min_cost,
                     void *stream);
 
+/* --------------------------------------------------------- whole pipeline */
+/* run_baseline_pipeline (aggregation.py:263-358) for a batch of pairs in one
+ * call: u8 -> f64, prepare_layer, build_edge_list, MST, rooted forest, lanes
+ * [x0, x0+nx), fused cost + aggregation + first argmin.  left/right (B,H,W,C)
+ * uint8 on the device; disp (B,H,W) int32, min_cost (B,H,W) f32; n_trees
+ * (B, nullable) int64 = trees per pair.  The batch is cut into n_sub
+ * sub-batches that run concurrently on their own streams (the tree build of
+ * one overlaps the aggregation of another); the caller's stream waits for
+ * all of them.  agg_ms (n_sub, nullable): device time of each sub-batch's
+ * hdp_aggregate_wta call (synchronises the workers once at the end). */
+int hdp_dense_pipeline(const uint8_t *left, const uint8_t *right, int batch, int h, int w, int c,
+                       int d_max, int x0, int nx, float alpha, float tau_c, float tau_g, float gamma,
+                       int n_sub, int32_t *disp, float *min_cost, int64_t *n_trees, float *agg_ms,
+                       void *stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -618,7 +618,10 @@ __device__ __forceinline__ bool try_carry1(const unsigned long long* p, unsigned
 #ifndef HDP_KLB_UP
 #define HDP_KLB_UP 2
 #endif
-constexpr int kLBUp = HDP_KLB_UP, kLBDown = 4;
+#ifndef HDP_KLB_DOWN
+#define HDP_KLB_DOWN 4
+#endif
+constexpr int kLBUp = HDP_KLB_UP, kLBDown = HDP_KLB_DOWN;
 
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
     unsigned long long w;

@@ -846,7 +846,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(flags.alloc(m_in + 1, st));
     HDP_TRY(fpos.alloc(m_in + 1, st));
     int64_t m = 0;
-    bool lex = false;  // edge list sorted by (eu, ev), eu < ev
+    bool lex = false;  // edge list sorted by (eu, ev), eu < ev (diagnostic)
     if (m_in > 0) {
         DevBuf<int> cnt;  // (tree edges, unsorted flag)
         HDP_TRY(cnt.alloc(2, st));

@@ -21,7 +21,10 @@ namespace hdp {
 // light-children rows, parent rows and metadata fit in shared memory; chunk
 // c of a phase holds the paths whose cumulative weight (4-byte words) falls
 // in the c-th window of kChunkWords.
-constexpr int kChunkShift = 13;
+#ifndef HDP_CHUNK_SHIFT
+#define HDP_CHUNK_SHIFT 13
+#endif
+constexpr int kChunkShift = HDP_CHUNK_SHIFT;
 constexpr int kChunkWords = 1 << kChunkShift;
 constexpr int kChunkMaxWords = 48 * 1024;  // 192 KB of shared memory per chunk
 

@@ -1,0 +1,260 @@
+// Dense full-range baseline pipeline (run_baseline_pipeline, aggregation.py:
+// 263-358, for a batch of pairs) as ONE host call, with the batch cut into
+// sub-batches that run concurrently on their own streams from a small pool of
+// persistent host threads.
+//
+// Why: the tree build of a sub-batch (Boruvka, Euler tour, list ranking,
+// heavy-path layout) is a chain of ~70 latency-bound kernels with a few host
+// reads for table sizes, and the fused aggregation is HBM-bound; on a single
+// stream the GPU alternates between the two.  With two sub-batches in flight
+// the one's tree build overlaps the other's aggregation, and no Python runs
+// between the steps.  Every sub-batch calls exactly the library's public
+// entry points (hdp_prepare, hdp_grid_edges, hdp_mst, hdp_forest_create,
+// hdp_aggregate_wta ...), so the results are those of the step-by-step path.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/hdp_stereo.h"
+#include "common.cuh"
+
+namespace hdp {
+
+void keep_pool_memory();
+
+// Persistent workers: job i of a call runs on worker i (its own thread-local
+// stream); the caller blocks until every job has returned.
+class Workers {
+public:
+    static Workers& get() {
+        static Workers w;
+        return w;
+    }
+    void run(std::vector<std::function<void()>>& jobs) {
+        std::unique_lock<std::mutex> lk(mu_);
+        while ((int)threads_.size() < (int)jobs.size()) {
+            const int id = (int)threads_.size();
+            slot_.push_back(nullptr);
+            threads_.emplace_back([this, id] { loop(id); });
+        }
+        pending_ = (int)jobs.size();
+        for (size_t i = 0; i < jobs.size(); i++) slot_[i] = &jobs[i];
+        gen_++;
+        cv_.notify_all();
+        done_cv_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+private:
+    Workers() = default;
+    ~Workers() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            gen_++;
+        }
+        cv_.notify_all();
+        for (auto& t : threads_) t.join();
+    }
+    void loop(int id) {
+        unsigned long long seen = 0;
+        for (;;) {
+            std::function<void()>* job = nullptr;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && slot_[id] != nullptr); });
+                if (stop_) return;
+                seen = gen_;
+                job = slot_[id];
+                slot_[id] = nullptr;
+            }
+            (*job)();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> threads_;
+    std::vector<std::function<void()>*> slot_;
+    unsigned long long gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+};
+
+struct SubStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t done = nullptr, a0 = nullptr, a1 = nullptr;
+};
+static int sub_stream(SubStream** out) {
+    static thread_local SubStream per_dev[64];
+    int dev = 0;
+    HDP_CHECK_CUDA(cudaGetDevice(&dev));
+    HDP_REQUIRE(dev >= 0 && dev < 64, HDP_ERR_CONFIG, "device ordinal %d out of range", dev);
+    SubStream& ss = per_dev[dev];
+    if (!ss.s) {
+        HDP_CHECK_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+        HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.done, cudaEventDisableTiming));
+        HDP_CHECK_CUDA(cudaEventCreate(&ss.a0));
+        HDP_CHECK_CUDA(cudaEventCreate(&ss.a1));
+    }
+    *out = &ss;
+    return HDP_OK;
+}
+
+#define HDP_PCALL(expr)                 \
+    do {                                \
+        const int _st = (expr);         \
+        if (_st != HDP_OK) return _st;  \
+    } while (0)
+
+struct DenseJob {
+    const uint8_t* left;
+    const uint8_t* right;
+    int nb, h, w, c, d_max, x0, nx;
+    float alpha, tau_c, tau_g, gamma;
+    int32_t* disp;
+    float* min_cost;
+    int64_t* n_trees;
+    float* agg_ms;
+    cudaEvent_t start;
+    cudaEvent_t* done_out;
+};
+
+// one sub-batch, every step through the public entry points
+static int dense_sub(const DenseJob& j) {
+    SubStream* ss = nullptr;
+    HDP_TRY(sub_stream(&ss));
+    cudaStream_t st = ss->s;
+    HDP_CHECK_CUDA(cudaStreamWaitEvent(st, j.start, 0));
+    const int64_t npp = (int64_t)j.h * j.w, n = (int64_t)j.nb * npp;
+    const int64_t epp = 2 * npp - j.h - j.w, m = (int64_t)j.nb * epp;
+    DevBuf<double> il, ir;
+    DevBuf<float> pl, pr, ew;
+    DevBuf<int32_t> eu, ev, comp;
+    DevBuf<uint64_t> key;
+    DevBuf<uint8_t> in_tree;
+    HDP_TRY(il.alloc(n * j.c, st));
+    HDP_TRY(ir.alloc(n * j.c, st));
+    HDP_TRY(pl.alloc(n * 4, st));
+    HDP_TRY(pr.alloc(n * 4, st));
+    HDP_PCALL(hdp_u8_to_f64(j.left, il.get(), n * j.c, st));
+    HDP_PCALL(hdp_u8_to_f64(j.right, ir.get(), n * j.c, st));
+    HDP_PCALL(hdp_prepare(il.get(), j.nb, j.h, j.w, j.c, nullptr, nullptr, nullptr, pl.get(), st));
+    HDP_PCALL(hdp_prepare(ir.get(), j.nb, j.h, j.w, j.c, nullptr, nullptr, nullptr, pr.get(), st));
+    ir.release();
+    HDP_TRY(eu.alloc(m + 1, st));
+    HDP_TRY(ev.alloc(m + 1, st));
+    HDP_TRY(ew.alloc(m + 1, st));
+    HDP_TRY(key.alloc(m + 1, st));
+    HDP_TRY(in_tree.alloc(m + 1, st));
+    HDP_TRY(comp.alloc(n, st));
+    HDP_PCALL(hdp_grid_edges(il.get(), j.nb, j.h, j.w, j.c, eu.get(), ev.get(), ew.get(), key.get(), st));
+    il.release();
+    HDP_PCALL(hdp_mst(n, m, eu.get(), ev.get(), key.get(), in_tree.get(), comp.get(), nullptr, st));
+    key.release();
+    hdp_forest* f = nullptr;
+    HDP_PCALL(hdp_forest_create(n, m, eu.get(), ev.get(), ew.get(), in_tree.get(), comp.get(), j.gamma, &f, st));
+    int rc = hdp_forest_set_lanes_range(f, j.x0, j.nx, st);
+    if (rc == HDP_OK) {
+        if (j.agg_ms) HDP_CHECK_CUDA(cudaEventRecord(ss->a0, st));
+        rc = hdp_aggregate_wta(f, pl.get(), pr.get(), j.h, j.w, j.c, j.alpha, j.tau_c, j.tau_g, nullptr, j.disp,
+                               j.min_cost, nullptr, nullptr, st);
+        if (j.agg_ms) HDP_CHECK_CUDA(cudaEventRecord(ss->a1, st));
+    }
+    if (rc == HDP_OK && j.n_trees) rc = hdp_forest_pair_stats(f, j.nb, npp, j.n_trees, nullptr, st);
+    hdp_forest_destroy(f);
+    if (rc != HDP_OK) return rc;
+    if (j.agg_ms) {
+        HDP_CHECK_CUDA(cudaEventSynchronize(ss->a1));
+        HDP_CHECK_CUDA(cudaEventElapsedTime(j.agg_ms, ss->a0, ss->a1));
+    }
+    HDP_CHECK_CUDA(cudaEventRecord(ss->done, st));
+    *j.done_out = ss->done;
+    return HDP_OK;
+}
+
+}  // namespace hdp
+
+using namespace hdp;
+
+extern "C" int hdp_dense_pipeline(const uint8_t* left, const uint8_t* right, int batch, int h, int w, int c,
+                                  int d_max, int x0, int nx, float alpha, float tau_c, float tau_g, float gamma,
+                                  int n_sub, int32_t* disp, float* min_cost, int64_t* n_trees, float* agg_ms,
+                                  void* stream) {
+    HDP_REQUIRE(batch >= 1 && h >= 1 && w >= 1 && (c == 1 || c == 3), HDP_ERR_CONFIG, "bad batch geometry");
+    HDP_REQUIRE(d_max >= 1, HDP_ERR_CONFIG, "d_max must be >= 1, got %d", d_max);
+    HDP_REQUIRE(x0 >= 0 && nx >= 1 && x0 + nx <= d_max + 1, HDP_ERR_CONFIG, "bad lane range [%d, %d)", x0, x0 + nx);
+    HDP_REQUIRE(disp != nullptr && min_cost != nullptr, HDP_ERR_CONFIG, "outputs required");
+    cudaStream_t caller = (cudaStream_t)stream;
+    int dev = 0;
+    HDP_CHECK_CUDA(cudaGetDevice(&dev));
+    if (n_sub < 1) n_sub = 1;
+    if (n_sub > batch) n_sub = batch;
+    if (n_sub > 16) n_sub = 16;
+    cudaEvent_t start;
+    HDP_CHECK_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    HDP_CHECK_CUDA(cudaEventRecord(start, caller));
+    const int64_t npp = (int64_t)h * w;
+    std::vector<DenseJob> jobs(n_sub);
+    std::vector<int> status(n_sub, HDP_OK);
+    std::vector<std::string> errs(n_sub);
+    std::vector<cudaEvent_t> done(n_sub, nullptr);
+    std::vector<std::function<void()>> fns;
+    int b0 = 0;
+    for (int i = 0; i < n_sub; i++) {
+        const int nb = batch / n_sub + (i < batch % n_sub ? 1 : 0);
+        DenseJob& j = jobs[i];
+        j.left = left + (int64_t)b0 * npp * c;
+        j.right = right + (int64_t)b0 * npp * c;
+        j.nb = nb;
+        j.h = h;
+        j.w = w;
+        j.c = c;
+        j.d_max = d_max;
+        j.x0 = x0;
+        j.nx = nx;
+        j.alpha = alpha;
+        j.tau_c = tau_c;
+        j.tau_g = tau_g;
+        j.gamma = gamma;
+        j.disp = disp + (int64_t)b0 * npp;
+        j.min_cost = min_cost + (int64_t)b0 * npp;
+        j.n_trees = n_trees ? n_trees + b0 : nullptr;
+        j.agg_ms = agg_ms ? agg_ms + i : nullptr;
+        j.start = start;
+        j.done_out = &done[i];
+        fns.emplace_back([&, i, dev] {
+            if (cudaSetDevice(dev) != cudaSuccess) {
+                status[i] = HDP_ERR_CUDA;
+                errs[i] = "cudaSetDevice failed in a pipeline worker";
+                return;
+            }
+            keep_pool_memory();
+            status[i] = dense_sub(jobs[i]);
+            if (status[i] != HDP_OK) errs[i] = hdp_last_error();
+        });
+        b0 += nb;
+    }
+    if (n_sub == 1) {
+        fns[0]();  // no worker for a single sub-batch
+    } else {
+        Workers::get().run(fns);
+    }
+    int rc = HDP_OK;
+    for (int i = 0; i < n_sub; i++) {
+        if (status[i] != HDP_OK && rc == HDP_OK) {
+            rc = status[i];
+            set_error("%s", errs[i].c_str());
+        }
+        if (done[i]) cudaStreamWaitEvent(caller, done[i], 0);
+    }
+    cudaEventDestroy(start);  // destruction is deferred until the waits complete
+    return rc;
+}

@@ -14,6 +14,7 @@ Entry points:
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -405,6 +406,40 @@ def _forest_layer(lev: Level, eu, ev, ew, in_tree, comp, gamma, cost, masks=None
     return f, disp, mc, keys, vol
 
 
+# sub-batches of the one-call dense pipeline (hdp_dense_pipeline): the tree
+# build of one overlaps the aggregation of another
+DENSE_SUB_BATCHES = int(os.environ.get("HDP_DENSE_SUB", "1"))
+
+
+def run_baseline_fused(left_u8, right_u8, d_max: int, gamma: float = 0.1,
+                       cost: CostConsts = CostConsts(), x0: int = 0, nx: int | None = None,
+                       n_sub: int | None = None, agg_ms=None) -> LevelOut:
+    """run_baseline_batch for plain MST trees in ONE library call
+    (hdp_dense_pipeline): the batch runs as concurrent sub-batches on their own
+    streams.  agg_ms: optional list that receives each sub-batch's aggregation
+    time (ms, device events)."""
+    torch = _t()
+    if d_max < 1:
+        raise ConfigError(f"d_max must be >= 1, got {d_max}")
+    b, h, w, c = left_u8.shape
+    nx = d_max + 1 if nx is None else nx
+    n_sub = DENSE_SUB_BATCHES if n_sub is None else n_sub
+    n_sub = max(1, min(n_sub, b))
+    dev = left_u8.device
+    disp = torch.empty(b * h * w, dtype=torch.int32, device=dev)
+    mc = torch.empty(b * h * w, dtype=torch.float32, device=dev)
+    ntrees = np.zeros(b, np.int64)
+    ams = np.zeros(n_sub, np.float32) if agg_ms is not None else None
+    L.call("hdp_dense_pipeline", L.ptr(left_u8.contiguous()), L.ptr(right_u8.contiguous()), b, h, w, c,
+           d_max, x0, nx, cost.alpha, cost.tau_color, cost.tau_grad, gamma, n_sub, L.ptr(disp), L.ptr(mc),
+           ntrees.ctypes.data, ams.ctypes.data if ams is not None else None, L.stream())
+    if agg_ms is not None:
+        agg_ms.extend(float(x) for x in ams)
+    stored = np.full(b, h * w * nx, np.int64)
+    ratio = np.array([float(s) / (h * w) / (d_max + 1) for s in stored])
+    return LevelOut(0, h, w, d_max, disp.view(b, h, w), mc.view(b, h, w), ntrees, stored, ratio, {}, None)
+
+
 def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
                        cost: CostConsts = CostConsts(), tree_kind: str = "mst", seed: int = 0,
                        x0: int = 0, nx: int | None = None, want_volume=False, want_keys=False,
@@ -416,6 +451,9 @@ def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
         raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
     if d_max < 1:
         raise ConfigError(f"d_max must be >= 1, got {d_max}")
+    if (tree_kind == "mst" and DENSE_SUB_BATCHES > 0 and not (want_volume or want_keys or keep_forest
+                                                             or timing or probe is not None)):
+        return run_baseline_fused(left_u8, right_u8, d_max, gamma, cost, x0, nx)
     clock = _Clock(timing)
     t0 = time.perf_counter()
     b, h, w, c = left_u8.shape

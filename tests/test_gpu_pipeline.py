@@ -94,3 +94,46 @@ def test_hdp_c1_teacher_forced(gmm_text):
     # free-running result vs the reference golden: same up to tie cascades
     final = outs[-1].disparity[0].cpu().numpy()
     assert (final != g["c1_hdp_l0_disp"]).mean() < 0.01
+
+
+@pytest.mark.parametrize("n_sub", [1, 2, 3])
+def test_dense_pipeline_one_call_matches_step_by_step(n_sub):
+    """hdp_dense_pipeline (one library call, sub-batches on their own streams
+    from the worker pool) returns exactly what the step-by-step engine path
+    returns, for every split of the batch; per-pair tree counts too."""
+    import torch
+
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import CONFIGS, make_scene
+
+    spec = CONFIGS[2]
+    scenes = [make_scene(spec, i) for i in range(3)]
+    crop = (slice(0, 96), slice(0, 160))
+    L = dev(np.stack([s.pair.left.data[crop] for s in scenes]))
+    R = dev(np.stack([s.pair.right.data[crop] for s in scenes]))
+    ref = E.run_baseline_batch(L, R, spec.d_max, timing=True)  # step-by-step path
+    got = E.run_baseline_fused(L, R, spec.d_max, n_sub=n_sub)
+    torch.cuda.synchronize()
+    assert torch.equal(got.disparity, ref.disparity)
+    assert torch.equal(got.min_cost, ref.min_cost)
+    np.testing.assert_array_equal(got.n_trees, ref.n_trees)
+    np.testing.assert_array_equal(got.stored_entries, ref.stored_entries)
+
+
+def test_dense_pipeline_slab_lanes_match():
+    """A disparity slab [x0, x0+nx) through the one-call pipeline equals the
+    step-by-step slab (the multi-GPU split's per-rank call)."""
+    import torch
+
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import CONFIGS, make_scene
+
+    spec = CONFIGS[2]
+    s = make_scene(spec, 5)
+    L = dev(s.pair.left.data[None, :80, :120])
+    R = dev(s.pair.right.data[None, :80, :120])
+    ref = E.run_baseline_batch(L, R, spec.d_max, x0=17, nx=30, timing=True)
+    got = E.run_baseline_fused(L, R, spec.d_max, x0=17, nx=30)
+    torch.cuda.synchronize()
+    assert torch.equal(got.disparity, ref.disparity)
+    assert torch.equal(got.min_cost, ref.min_cost)
