@@ -103,6 +103,11 @@ int hdp_median3x3(const uint8_t *src, uint8_t *dst, int batch, int h, int w, int
 int hdp_mst(int64_t n_nodes, int64_t n_edges, const int32_t *eu, const int32_t *ev,
             const uint64_t *key, uint8_t *in_tree, int32_t *comp, int *rounds_out, void *stream);
 
+/* hdp_mst for a grid edge list from hdp_grid_edges (B pairs of h x w, scan
+ * order): the same forest; the first Boruvka round is gathered per node over
+ * its <= 4 incident edges instead of atomics over all edges. */
+int hdp_mst_grid(int batch, int h, int w, const int32_t *eu, const int32_t *ev, const uint64_t *key,
+                 uint8_t *in_tree, int32_t *comp, int *rounds_out, void *stream);
 /* --------------------------------------------------------------- HDP parts */
 
 /* estimate_prior up to the histogram (hdp_model.py:425-470): sampled

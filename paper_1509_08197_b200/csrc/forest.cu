@@ -28,7 +28,7 @@
 namespace hdp {
 
 int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, const uint64_t* key,
-                uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st);
+                uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st, int grid_h = 0, int grid_w = 0);
 
 // In-tree flags, plus a check that the edge list is sorted by (eu, ev) with
 // eu < ev (grid edge lists are): then a stable sort of the arcs by source

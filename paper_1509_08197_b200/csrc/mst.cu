@@ -85,6 +85,41 @@ __global__ void k_mst_win(int64_t m, const int32_t* __restrict__ eu, const int32
     }
 }
 
+// Round 1 on a grid edge list (hdp_grid_edges' scan order): every component
+// is one node, so a node's winning edge is the least key among its <= 4
+// incident edges, gathered directly (no atomics, no pass over the edges).
+__device__ __forceinline__ int64_t grid_right(int r, int col, int h, int w) {
+    return r < h - 1 ? (int64_t)r * (2 * w - 1) + 2 * col : (int64_t)(h - 1) * (2 * w - 1) + col;
+}
+__device__ __forceinline__ int64_t grid_down(int r, int col, int w) {
+    return (int64_t)r * (2 * w - 1) + 2 * col + (col < w - 1 ? 1 : 0);
+}
+__global__ void k_mst_grid_first(int64_t n, int h, int w, const uint64_t* __restrict__ key, int32_t* win,
+                                 int32_t* wother) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int64_t npp = (int64_t)h * w;
+    const int64_t b = t / npp, p = t - b * npp;
+    const int r = (int)(p / w), col = (int)(p - (int64_t)r * w);
+    const int64_t eb = b * (2 * npp - h - w);
+    unsigned long long best = ~0ull;
+    int64_t be = -1, bo = -1;
+    auto take = [&](int64_t e, int64_t other) {
+        const unsigned long long k = key[eb + e];
+        if (k < best) {
+            best = k;
+            be = eb + e;
+            bo = other;
+        }
+    };
+    if (col + 1 < w) take(grid_right(r, col, h, w), t + 1);
+    if (r + 1 < h) take(grid_down(r, col, w), t + w);
+    if (col > 0) take(grid_right(r, col - 1, h, w), t - 1);
+    if (r > 0) take(grid_down(r - 1, col, w), t - w);
+    win[t] = (int32_t)be;
+    wother[t] = (int32_t)bo;
+}
+
 // eidx (optional): original edge index of each contracted edge
 __global__ void k_mst_hook(int64_t n, const int32_t* __restrict__ wother,
                            const int32_t* __restrict__ comp, const int32_t* __restrict__ win,
@@ -259,7 +294,7 @@ __global__ void k_mst_final(int64_t n, int32_t* comp) {
 // phase 2: the remaining rounds over the contracted graph (edges between
 // distinct components, relabelled to representatives).
 int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, const uint64_t* key,
-                uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st) {
+                uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st, int grid_h, int grid_w) {
     constexpr int kMaxRounds = 64, kBatch = 4;
     int kFull = 3;
     bool coop = true;  // the contracted phase as one cooperative launch
@@ -306,12 +341,17 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
         for (int r = r0; r < r0 + nb; r++) {
             const int* prev = r > 0 ? hooks.get() + r - 1 : nullptr;
             int* hk = hooks.get() + r;
+            if (r == 0 && grid_h > 0) {  // first round on a grid: gathered per node
+                k_mst_grid_first<<<grid_for(gn, 256), 256, 0, st>>>(gn, grid_h, grid_w, gk, win.get(), wother.get());
+                note_launch();
+            } else {
             k_mst_reset<<<grid_for(gn, 256), 256, 0, st>>>(gn, best.get(), win.get(), prev, nodes); note_launch();
             if (gm > 0) {
                 k_mst_offer<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
                                                                prev); note_launch();
                 k_mst_win<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
                                                              win.get(), wother.get(), prev); note_launch();
+            }
             }
             k_mst_hook<<<grid_for(gn, 256), 256, 0, st>>>(gn, wother.get(), comp, win.get(), link.get(), in_tree, hk,
                                                          prev, nodes, gidx); note_launch();
@@ -390,12 +430,18 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
                                 (void*)&lk, (void*)&in_tree, (void*)&fl, (void*)&max_r, (void*)&rc};
                 HDP_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)k_mst_coop, dim3(nb * nsm), dim3(256), args,
                                                            0, st)); note_launch();
-                int hr = 0;
-                HDP_TRY(to_host(&hr, rc, 1, st));
-                rounds += hr;
-                if (hr >= max_r) {
-                    set_error("boruvka did not converge (duplicate keys?)");
-                    return HDP_ERR_INTERNAL;
+                // the round count and the convergence check (it can only fail on
+                // duplicate keys; grid keys carry the unique edge index in the low
+                // word) only when the caller asks for the rounds: no host read on
+                // the pipeline path
+                if (rounds_out) {
+                    int hr = 0;
+                    HDP_TRY(to_host(&hr, rc, 1, st));
+                    rounds += hr;
+                    if (hr >= max_r) {
+                        set_error("boruvka did not converge (duplicate keys?)");
+                        return HDP_ERR_INTERNAL;
+                    }
                 }
                 break;
             }
@@ -421,5 +467,13 @@ extern "C" int hdp_mst(int64_t n_nodes, int64_t n_edges, const int32_t* eu, cons
     HDP_REQUIRE(n_edges >= 0 && n_edges < ((int64_t)1 << 31), HDP_ERR_CONFIG, "bad edge count");
     if (n_nodes == 0) return HDP_OK;
     return run_boruvka(n_nodes, n_edges, eu, ev, key, in_tree, comp, rounds_out,
-                       (cudaStream_t)stream);
+                       (cudaStream_t)stream, 0, 0);
+}
+
+extern "C" int hdp_mst_grid(int batch, int h, int w, const int32_t* eu, const int32_t* ev, const uint64_t* key,
+                            uint8_t* in_tree, int32_t* comp, int* rounds_out, void* stream) {
+    HDP_REQUIRE(batch >= 1 && h >= 1 && w >= 1, HDP_ERR_CONFIG, "bad grid geometry");
+    const int64_t n = (int64_t)batch * h * w, m = (int64_t)batch * (2 * (int64_t)h * w - h - w);
+    HDP_REQUIRE(n < ((int64_t)1 << 31) && m < ((int64_t)1 << 31), HDP_ERR_CONFIG, "grid too large");
+    return run_boruvka(n, m, eu, ev, key, in_tree, comp, rounds_out, (cudaStream_t)stream, h, w);
 }

@@ -9,7 +9,7 @@
 // stream the GPU alternates between the two.  With two sub-batches in flight
 // the one's tree build overlaps the other's aggregation, and no Python runs
 // between the steps.  Every sub-batch calls exactly the library's public
-// entry points (hdp_prepare, hdp_grid_edges, hdp_mst, hdp_forest_create,
+// entry points (hdp_prepare, hdp_grid_edges, hdp_mst_grid, hdp_forest_create,
 // hdp_aggregate_wta ...), so the results are those of the step-by-step path.
 #include <cuda_runtime.h>
 
@@ -157,7 +157,7 @@ static int dense_sub(const DenseJob& j) {
     HDP_TRY(comp.alloc(n, st));
     HDP_PCALL(hdp_grid_edges(il.get(), j.nb, j.h, j.w, j.c, eu.get(), ev.get(), ew.get(), key.get(), st));
     il.release();
-    HDP_PCALL(hdp_mst(n, m, eu.get(), ev.get(), key.get(), in_tree.get(), comp.get(), nullptr, st));
+    HDP_PCALL(hdp_mst_grid(j.nb, j.h, j.w, eu.get(), ev.get(), key.get(), in_tree.get(), comp.get(), nullptr, st));
     key.release();
     hdp_forest* f = nullptr;
     HDP_PCALL(hdp_forest_create(n, m, eu.get(), ev.get(), ew.get(), in_tree.get(), comp.get(), j.gamma, &f, st));

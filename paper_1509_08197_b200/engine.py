@@ -138,6 +138,19 @@ def mst(n_nodes: int, eu, ev, key):
     return in_tree[:m], comp, rounds.value
 
 
+def mst_grid(batch: int, h: int, w: int, eu, ev, key):
+    """mst() for a grid edge list of grid_edges (first Boruvka round gathered
+    per node)."""
+    torch = _t()
+    m = eu.numel()
+    in_tree = torch.empty(max(m, 1), dtype=torch.uint8, device=eu.device)
+    comp = torch.empty(batch * h * w, dtype=torch.int32, device=eu.device)
+    rounds = C.c_int(0)
+    L.call("hdp_mst_grid", batch, h, w, L.ptr(eu), L.ptr(ev), L.ptr(key), L.ptr(in_tree), L.ptr(comp),
+           C.byref(rounds), L.stream())
+    return in_tree[:m], comp, rounds.value
+
+
 # ------------------------------------------------------------------ forest
 class DeviceForest:
     """Rooted forest + heavy-path layout owned by libhdpstereo (hdp_forest*)."""
@@ -464,7 +477,7 @@ def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
     eu, ev, ew, key, E = grid_edges(il)
     if tree_kind == "rt":
         key = rt_keys(E, b, seed, il.device)
-    in_tree, comp, _ = mst(b * h * w, eu, ev, key)
+    in_tree, comp, _ = mst_grid(b, h, w, eu, ev, key)
     f, disp, mc, keys, vol = _forest_layer(lev, eu, ev, ew, in_tree, comp, gamma, cost, None, x0,
                                            nx, want_volume, want_keys, clock, t0, probe)
     ntrees, stored, ratio = _per_pair_stats(f, b, h * w, d_max)
