@@ -290,6 +290,34 @@ __global__ void k_rank_jump_n(const int32_t* __restrict__ count, const uint64_t*
     }
 }
 
+// Asynchronous pointer jumping, all rounds in one launch.  A word is (next,
+// sum over [self, next)) and is read and written as one 64-bit access, so a
+// word read at any time is a valid jump: combining it with the word of its
+// target, stale or fresh, gives another valid (shorter) jump.  Each thread
+// jumps its own entry until it reaches the list end; no grid barrier, and
+// threads started late find mostly-finished chains.
+__device__ __forceinline__ uint64_t ld_word(const uint64_t* p) {
+    uint64_t w;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
+__device__ __forceinline__ void st_word(uint64_t* p, uint64_t w) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__global__ void k_rank_jump_async(const int32_t* __restrict__ count, uint64_t* word) {
+    const int32_t nr = *count;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t w = ld_word(word + i);
+        for (;;) {
+            const int32_t nx = (int32_t)(w >> 32);
+            if (nx < 0) break;
+            const uint64_t w2 = ld_word(word + nx);
+            w = (w2 & 0xffffffff00000000ull) | (uint32_t)((uint32_t)w + (uint32_t)w2);
+            st_word(word + i, w);
+        }
+    }
+}
+
 __global__ void k_rank_final(int64_t na, const int32_t* __restrict__ owner, const int32_t* __restrict__ local,
                              const uint64_t* __restrict__ rword, int32_t* rank) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -449,6 +477,24 @@ __global__ void k_hp_walk(int64_t n, const int32_t* __restrict__ pr, const int32
 
 // a chain of non-head rulers is at most max depth / kHpRuler + 1 long
 __device__ __forceinline__ long long hp_chain(const int32_t* dmax) { return (long long)*dmax / kHpRuler + 1; }
+
+// heavy-path ruler words, jumped asynchronously (see k_rank_jump_async); a
+// head's word points at itself
+__global__ void k_hp_jump_async(const int32_t* __restrict__ list, const int32_t* __restrict__ cnt, uint64_t* word) {
+    const int32_t nl = *cnt;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = list[i];
+        uint64_t w = ld_word(word + v);
+        for (;;) {
+            const int32_t h = (int32_t)(w >> 32);
+            const uint64_t w2 = ld_word(word + h);
+            const int32_t hh = (int32_t)(w2 >> 32);
+            if (hh == h) break;  // h is a head
+            w = hp_word(hh, (int32_t)((uint32_t)w + (uint32_t)w2));
+            st_word(word + v, w);
+        }
+    }
+}
 
 __global__ void k_hp_jump(const int32_t* __restrict__ list, const int32_t* __restrict__ cnt,
                           const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
@@ -834,6 +880,16 @@ __global__ void k_forest_summary(int64_t n, int32_t* cnt, const int32_t* __restr
 
 using namespace hdp;
 
+// pointer jumping without grid barriers (one launch); HDP_SYNC_JUMP=1: the
+// round-synchronous launches (diagnostics / A-B)
+static bool async_jump() {
+    static const bool on = [] {
+        const char* e = getenv("HDP_SYNC_JUMP");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const int32_t* ev,
                         const float* ew, const uint8_t* in_tree, const int32_t* comp_in) {
     cudaStream_t st = f->st;
@@ -979,9 +1035,13 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                           owner.get(), local.get(), wa.get()); note_launch();
         // the longest ruler chain is at most the largest tree's tour, 2 (size - 1) arcs
         const int rounds = ceil_log2(2 * (int64_t)max_tree);
-        for (int r = 0; r < rounds; r++) {
-            k_rank_jump_n<<<grid_for(rmax, B), B, 0, st>>>(rid.get() + na, wa.get(), wb.get()); note_launch();
-            std::swap(wa.p, wb.p);
+        if (async_jump()) {
+            k_rank_jump_async<<<grid_for(rmax, B), B, 0, st>>>(rid.get() + na, wa.get()); note_launch();
+        } else {
+            for (int r = 0; r < rounds; r++) {
+                k_rank_jump_n<<<grid_for(rmax, B), B, 0, st>>>(rid.get() + na, wa.get(), wb.get()); note_launch();
+                std::swap(wa.p, wb.p);
+            }
         }
         k_rank_final<<<grid_for(na, B), B, 0, st>>>(na, owner.get(), local.get(), wa.get(), rank.get()); note_launch();
         HDP_CHECK_LAUNCH();
@@ -1049,11 +1109,17 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         k_hp_walk<<<grid_for(n, B), B, 0, st>>>(n, pr.get(), f->parent.get(), heavy.get(), nearw.get(), ba, bb,
                                                 hlist.get(), hcnt.get()); note_launch();
         const int jg = (int)std::min<int64_t>(grid_for(n / kHpRuler + 1, B), 148 * 8);
-        for (int r = 0; r < rounds; r++) {
-            k_hp_jump<<<jg, B, 0, st>>>(hlist.get(), hcnt.get(), (r & 1) ? bb : ba, (r & 1) ? ba : bb, dmax.get(), r);
-            note_launch();
+        if (async_jump()) {
+            k_hp_jump_async<<<jg, B, 0, st>>>(hlist.get(), hcnt.get(), ba); note_launch();
+            // zero rounds executed: the unpack reads buffer a
+            k_hp_unpack<<<grid_for(n, B), B, 0, st>>>(n, nearw.get(), ba, bb, dmax.get(), 0, hp.get(), dist.get());
+        } else {
+            for (int r = 0; r < rounds; r++) {
+                k_hp_jump<<<jg, B, 0, st>>>(hlist.get(), hcnt.get(), (r & 1) ? bb : ba, (r & 1) ? ba : bb, dmax.get(), r);
+                note_launch();
+            }
+            k_hp_unpack<<<grid_for(n, B), B, 0, st>>>(n, nearw.get(), ba, bb, dmax.get(), rounds, hp.get(), dist.get());
         }
-        k_hp_unpack<<<grid_for(n, B), B, 0, st>>>(n, nearw.get(), ba, bb, dmax.get(), rounds, hp.get(), dist.get());
         note_launch();
     }
     HDP_CHECK_LAUNCH();
