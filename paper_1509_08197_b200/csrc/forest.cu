@@ -240,7 +240,10 @@ __global__ void k_rank_jump(int64_t na, const uint64_t* __restrict__ in, uint64_
 // ---- ruling-set list ranking: rulers are every kRuler-th arc plus every list
 // head; each ruler walks its sublist to the next ruler (owner, offset), the
 // rulers alone are ranked by pointer jumping, and rank = ruler rank - offset.
-constexpr int kRuler = 8;
+#ifndef HDP_RULER
+#define HDP_RULER 16
+#endif
+constexpr int kRuler = HDP_RULER;
 
 __global__ void k_has_pred(int64_t na, const int32_t* __restrict__ next, uint8_t* hp) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -417,7 +420,10 @@ __global__ void k_heavy(int64_t n, const int32_t* __restrict__ adj_start,
 // (root or light child) and every heavy child at a depth divisible by kHpRuler.
 // Each node walks up (< kHpRuler parent steps) to its nearest ruler; the
 // non-head rulers, about n / kHpRuler of them, pointer-jump to their heads.
-constexpr int kHpRuler = 8;
+#ifndef HDP_HP_RULER
+#define HDP_HP_RULER 16
+#endif
+constexpr int kHpRuler = HDP_HP_RULER;
 
 // pr[v] = parent | ruler flag << 31
 __global__ void k_hp_flags(int64_t n, const int32_t* __restrict__ parent, const int32_t* __restrict__ heavy,

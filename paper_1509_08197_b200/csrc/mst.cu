@@ -190,7 +190,11 @@ __global__ void k_mst_contract(int64_t m, int64_t n, const int32_t* __restrict__
         const int32_t p = epos[i];
         cu[p] = comp[eu[i]];
         cv[p] = comp[ev[i]];
-        ckey[p] = key[i];
+        // low word re-keyed to the contracted index: order-preserving (the
+        // compaction keeps edge order, and keys are only compared within a
+        // component, i.e. within one pair's run of the list), and the minimum
+        // key of a component names its winning edge directly
+        ckey[p] = (key[i] & 0xffffffff00000000ull) | (uint32_t)p;
         cidx[p] = (int32_t)i;
     }
     if (i < n && vf[i]) reps[vpos[i]] = (int32_t)i;
@@ -209,11 +213,9 @@ __global__ void __launch_bounds__(256) k_mst_coop(int64_t gm, int64_t gn, const 
     cg::grid_group grid = cg::this_grid();
     const int64_t tid = (int64_t)grid.thread_rank(), nthr = (int64_t)grid.size();
     int r = 0;
-    for (int64_t t = tid; t < gn; t += nthr) {
-        const int32_t v = reps[t];
-        best[v] = ~0ull;
-        win[v] = -1;
-    }
+    (void)win;
+    (void)wother;
+    for (int64_t t = tid; t < gn; t += nthr) best[reps[t]] = ~0ull;
     grid.sync();
     while (r < max_rounds) {
         for (int64_t e = tid; e < gm; e += nthr) {
@@ -228,32 +230,21 @@ __global__ void __launch_bounds__(256) k_mst_coop(int64_t gm, int64_t gn, const 
             if (k < best[cv]) atomicMin(&best[cv], k);
         }
         grid.sync();
-        for (int64_t e = tid; e < gm; e += nthr) {
-            if (!alive[e]) continue;
-            const int32_t cu = comp[gu[e]], cv = comp[gv[e]];
-            const unsigned long long k = gk[e];
-            if (best[cu] == k) {
-                win[cu] = (int32_t)e;
-                wother[cu] = cv;
-            }
-            if (best[cv] == k) {
-                win[cv] = (int32_t)e;
-                wother[cv] = cu;
-            }
-        }
-        grid.sync();
+        // hook: the component's minimum key carries its winning edge
         bool hooked = false;
         for (int64_t t = tid; t < gn; t += nthr) {
             const int32_t v = reps[t];
             if (comp[v] != v) continue;
-            const int32_t e = win[v];
-            if (e < 0) {
+            const unsigned long long k = best[v];
+            if (k == ~0ull) {
                 link[v] = v;
                 continue;
             }
-            const int32_t other = wother[v];
+            const int32_t e = (int32_t)(uint32_t)k;
+            const int32_t cu = comp[gu[e]], cv = comp[gv[e]];
+            const int32_t other = cu == v ? cv : cu;
             in_tree[gidx[e]] = 1;
-            if (win[other] == e && v < other) {
+            if (best[other] == k && v < other) {
                 link[v] = v;  // mutual minimum: the lower id stays the root
             } else {
                 link[v] = other;
@@ -263,14 +254,13 @@ __global__ void __launch_bounds__(256) k_mst_coop(int64_t gm, int64_t gn, const 
         if (__syncthreads_or(hooked) && threadIdx.x == 0 && *(volatile int*)(flags + r) == 0) flags[r] = 1;
         grid.sync();
         // relabel, and reset the next round's minima (hook, the last reader of
-        // win, is behind the barrier above)
+        // best, is behind the barrier above)
         for (int64_t t = tid; t < gn; t += nthr) {
             const int32_t v = reps[t];
             int32_t x = comp[v];
             while (link[x] != x) x = link[x];
             comp[v] = x;
             best[v] = ~0ull;
-            win[v] = -1;
         }
         grid.sync();
         const bool more = *(volatile int*)(flags + r) != 0;
