@@ -94,8 +94,8 @@ __device__ __forceinline__ int64_t grid_right(int r, int col, int h, int w) {
 __device__ __forceinline__ int64_t grid_down(int r, int col, int w) {
     return (int64_t)r * (2 * w - 1) + 2 * col + (col < w - 1 ? 1 : 0);
 }
-__global__ void k_mst_grid_first(int64_t n, int h, int w, const uint64_t* __restrict__ key, int32_t* win,
-                                 int32_t* wother) {
+__global__ void k_mst_grid_first(int64_t n, int h, int w, const uint64_t* __restrict__ key,
+                                 unsigned long long* best_out) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const int64_t npp = (int64_t)h * w;
@@ -116,8 +116,52 @@ __global__ void k_mst_grid_first(int64_t n, int h, int w, const uint64_t* __rest
     if (r + 1 < h) take(grid_down(r, col, w), t + w);
     if (col > 0) take(grid_right(r, col - 1, h, w), t - 1);
     if (r > 0) take(grid_down(r - 1, col, w), t - w);
-    win[t] = (int32_t)be;
-    wother[t] = (int32_t)bo;
+    (void)be;
+    (void)bo;
+    best_out[t] = best;
+}
+
+// Grid rounds: the low word of a grid key is the edge's index within its
+// pair and a component never spans pairs, so the component's minimum key
+// names its winning edge: (pair of v) * edges per pair + low word.  Hook
+// without a separate winner pass.
+__global__ void k_mst_hook_grid(int64_t n, int64_t npp, int64_t epp, const int32_t* __restrict__ eu,
+                                const int32_t* __restrict__ ev, const int32_t* __restrict__ comp,
+                                const unsigned long long* __restrict__ best, int32_t* __restrict__ link,
+                                uint8_t* __restrict__ in_tree, int* __restrict__ hooks, const int* prev) {
+    if (converged(prev)) return;
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool hooked = false;
+    if (v < n && comp[v] == v) {
+        const unsigned long long k = best[v];
+        if (k == ~0ull) {
+            link[v] = (int32_t)v;
+        } else {
+            const int64_t e = (v / npp) * epp + (int64_t)(uint32_t)k;
+            const int32_t cu = comp[eu[e]], cv = comp[ev[e]];
+            const int32_t other = cu == (int32_t)v ? cv : cu;
+            in_tree[e] = 1;
+            if (best[other] == k && v < other) {
+                link[v] = (int32_t)v;  // mutual minimum: the lower id stays the root
+            } else {
+                link[v] = other;
+                hooked = true;
+            }
+        }
+    }
+    if (__syncthreads_or(hooked) && threadIdx.x == 0 && *(volatile int*)hooks == 0) *hooks = 1;
+}
+
+// relabel by the hook chains and reset the next round's minima
+__global__ void k_mst_relabel_reset(int64_t n, int32_t* __restrict__ comp, const int32_t* __restrict__ link,
+                                    unsigned long long* __restrict__ best, const int* prev) {
+    if (converged(prev)) return;
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    int32_t r = comp[v];
+    while (link[r] != r) r = link[r];
+    comp[v] = r;
+    best[v] = ~0ull;
 }
 
 // eidx (optional): original edge index of each contracted edge
@@ -331,10 +375,24 @@ int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, cons
         for (int r = r0; r < r0 + nb; r++) {
             const int* prev = r > 0 ? hooks.get() + r - 1 : nullptr;
             int* hk = hooks.get() + r;
-            if (r == 0 && grid_h > 0) {  // first round on a grid: gathered per node
-                k_mst_grid_first<<<grid_for(gn, 256), 256, 0, st>>>(gn, grid_h, grid_w, gk, win.get(), wother.get());
+            if (grid_h > 0 && !contracted) {
+                // grid rounds: the first gathered per node, then offer -> hook (winner
+                // from the key) -> relabel + reset
+                const int64_t npp = (int64_t)grid_h * grid_w, epp = 2 * npp - grid_h - grid_w;
+                if (r == 0) {
+                    k_mst_grid_first<<<grid_for(gn, 256), 256, 0, st>>>(gn, grid_h, grid_w, gk, best.get());
+                } else {
+                    k_mst_offer<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
+                                                                   prev);
+                }
                 note_launch();
-            } else {
+                k_mst_hook_grid<<<grid_for(gn, 256), 256, 0, st>>>(gn, npp, epp, gu, gv, comp, best.get(), link.get(),
+                                                                   in_tree, hk, prev); note_launch();
+                k_mst_relabel_reset<<<grid_for(gn, 256), 256, 0, st>>>(gn, comp, link.get(), best.get(), prev);
+                note_launch();
+                continue;
+            }
+            {
             k_mst_reset<<<grid_for(gn, 256), 256, 0, st>>>(gn, best.get(), win.get(), prev, nodes); note_launch();
             if (gm > 0) {
                 k_mst_offer<<<grid_for(gm, 256), 256, 0, st>>>(gm, gu, gv, gk, comp, alive.get(), best.get(),
