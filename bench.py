@@ -298,8 +298,10 @@ def run_ours(args):
     achieved = algo_bytes / t_agg / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": agg_traffic(), "peak_kind": peak_kind,
-            "kernel": f"hdp_aggregate_wta (fused cost + up/down passes + WTA), one call per sub-batch "
-                      f"of {B // n_sub} pairs, timed while the other sub-batch's tree build runs beside it",
+            "kernel": ("hdp_aggregate_wta (fused cost + up/down passes + WTA), one call per step"
+                       if n_sub == 1 else
+                       f"hdp_aggregate_wta (fused cost + up/down passes + WTA), one call per sub-batch of "
+                       f"{B // n_sub} pairs, timed while the other sub-batches run beside it"),
             "kernel_ms": t_agg * 1e3, "algorithmic_bytes": algo_bytes}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

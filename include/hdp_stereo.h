@@ -66,6 +66,9 @@ int hdp_block_mean(const double *src, double *dst, int batch, int h, int w, int 
 int hdp_prepare(const double *img, int batch, int h, int w, int c, double *unit, double *gray,
                 double *grad, float *packed, void *stream);
 
+/* prepare_layer's packed plane straight from uint8 (B,H,W,C): bit-identical
+ * to hdp_u8_to_f64 followed by hdp_prepare (unit = RN(I/255) by table). */
+int hdp_prepare_u8(const uint8_t *img, int batch, int h, int w, int c, float *packed, void *stream);
 /* Stable ascending argsort of 64-bit keys (radix): perm[i] = index of the
  * i-th smallest key, ties in index order -- numpy argsort(kind="stable") on
  * the keys (mst_edge_order, spanning_forest.py:96-107, on weight-bit keys). */
@@ -87,6 +90,9 @@ int hdp_cost_volume(const float *packed_l, const float *packed_r, int batch, int
 int hdp_grid_edges(const double *img, int batch, int h, int w, int c, int32_t *eu, int32_t *ev,
                    float *ew, uint64_t *key, void *stream);
 
+/* hdp_grid_edges from uint8 (B,H,W,C): the same edges, weights and keys. */
+int hdp_grid_edges_u8(const uint8_t *img, int batch, int h, int w, int c, int32_t *eu, int32_t *ev,
+                      float *ew, uint64_t *key, void *stream);
 /* The same edges' weights in float64 (EdgeList.weight, spanning_forest.py:
  * 33-49), for the host-facing API. */
 int hdp_grid_edge_weights64(const double *img, int batch, int h, int w, int c, double *ew,

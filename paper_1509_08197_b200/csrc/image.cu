@@ -164,6 +164,75 @@ __global__ void k_prepare(const double* __restrict__ img, int batch, int h, int 
     if (packed) packed[t] = make_float4((float)u[0], (float)u[1], (float)u[2], (float)g);
 }
 
+// prepare_layer from uint8 directly (the pipeline's level 0): unit = RN(I/255)
+// from a 256-entry table built with the same IEEE division, gray and the
+// central-difference gradient in k_prepare's exact operation order, so the
+// packed plane is bit-identical to u8 -> f64 -> k_prepare.
+__device__ __forceinline__ double gray_lut(const uint8_t* px, int c, const double* lut) {
+    if (c == 3) return __fma_rn(lut[px[2]], 0.114, __fma_rn(lut[px[0]], 0.299, __dmul_rn(lut[px[1]], 0.587)));
+    return lut[px[0]];
+}
+__global__ void __launch_bounds__(256) k_prepare_u8(const uint8_t* __restrict__ img, int batch, int h, int w,
+                                                    int c, float4* __restrict__ packed) {
+    __shared__ double lut[256];
+    lut[threadIdx.x] = __ddiv_rn((double)threadIdx.x, 255.0);
+    __syncthreads();
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = (int64_t)batch * h * w;
+    if (t >= n) return;
+    const int x = (int)(t % w);
+    const uint8_t* px = img + t * c;
+    double g;
+    if (w == 1) {
+        g = 0.0;
+    } else if (x == 0) {
+        g = __dsub_rn(gray_lut(px + c, c, lut), gray_lut(px, c, lut));
+    } else if (x == w - 1) {
+        g = __dsub_rn(gray_lut(px, c, lut), gray_lut(px - c, c, lut));
+    } else {
+        g = __ddiv_rn(__dsub_rn(gray_lut(px + c, c, lut), gray_lut(px - c, c, lut)), 2.0);
+    }
+    const double u0 = lut[px[0]];
+    const double u1 = c == 3 ? lut[px[1]] : 0.0, u2 = c == 3 ? lut[px[2]] : 0.0;
+    packed[t] = make_float4((float)u0, (float)u1, (float)u2, (float)g);
+}
+
+// build_edge_list from uint8 (weights = max channel |difference|, integers:
+// exactly k_grid_edges' values)
+__global__ void k_grid_edges_u8(const uint8_t* __restrict__ img, int batch, int h, int w, int c,
+                                int32_t* __restrict__ eu, int32_t* __restrict__ ev, float* __restrict__ ew,
+                                uint64_t* __restrict__ key) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t n = (int64_t)h * w;
+    if (t >= (int64_t)batch * n) return;
+    int b = t / n;
+    int64_t p = t % n;
+    int r = p / w, col = p % w;
+    int64_t E = 2 * n - h - w;
+    int64_t ebase = (int64_t)b * E;
+    const uint8_t* px = img + t * c;
+    if (col + 1 < w) {
+        int m = 0;
+        for (int k = 0; k < c; k++) m = max(m, abs((int)px[k] - (int)px[c + k]));
+        int64_t idx = (r < h - 1) ? (int64_t)r * (2 * w - 1) + 2 * col : (int64_t)(h - 1) * (2 * w - 1) + col;
+        float wf = (float)m;
+        eu[ebase + idx] = (int32_t)t;
+        ev[ebase + idx] = (int32_t)(t + 1);
+        if (ew) ew[ebase + idx] = wf;
+        key[ebase + idx] = ((uint64_t)__float_as_uint(wf) << 32) | (uint64_t)idx;
+    }
+    if (r + 1 < h) {
+        int m = 0;
+        for (int k = 0; k < c; k++) m = max(m, abs((int)px[k] - (int)px[(int64_t)w * c + k]));
+        int64_t idx = (int64_t)r * (2 * w - 1) + 2 * col + (col < w - 1 ? 1 : 0);
+        float wf = (float)m;
+        eu[ebase + idx] = (int32_t)t;
+        ev[ebase + idx] = (int32_t)(t + w);
+        if (ew) ew[ebase + idx] = wf;
+        key[ebase + idx] = ((uint64_t)__float_as_uint(wf) << 32) | (uint64_t)idx;
+    }
+}
+
 __device__ __forceinline__ float cost_f32(float4 L, float4 R, int c, float alpha, float tc,
                                           float tg) {
     float color;
@@ -289,6 +358,28 @@ int hdp_prepare(const double* img, int batch, int h, int w, int c, double* unit,
     if (n <= 0) return HDP_OK;
     k_prepare<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(img, batch, h, w, c, unit,
                                                                    gray, grad, (float4*)packed); note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+int hdp_prepare_u8(const uint8_t* img, int batch, int h, int w, int c, float* packed, void* stream) {
+    HDP_REQUIRE(c == 1 || c == 3, HDP_ERR_DATA, "channels must be 1 or 3, got %d", c);
+    int64_t n = (int64_t)batch * h * w;
+    if (n <= 0) return HDP_OK;
+    k_prepare_u8<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(img, batch, h, w, c, (float4*)packed);
+    note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+int hdp_grid_edges_u8(const uint8_t* img, int batch, int h, int w, int c, int32_t* eu, int32_t* ev, float* ew,
+                      uint64_t* key, void* stream) {
+    int64_t n = (int64_t)h * w;
+    HDP_REQUIRE(2 * n - h - w < ((int64_t)1 << 32), HDP_ERR_CONFIG, "too many edges per pair");
+    HDP_REQUIRE((int64_t)batch * n < ((int64_t)1 << 31), HDP_ERR_CONFIG, "too many nodes");
+    if (batch * n <= 0) return HDP_OK;
+    k_grid_edges_u8<<<grid_for(batch * n, 256), 256, 0, (cudaStream_t)stream>>>(img, batch, h, w, c, eu, ev, ew,
+                                                                                key); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

@@ -9,7 +9,7 @@
 // stream the GPU alternates between the two.  With two sub-batches in flight
 // the one's tree build overlaps the other's aggregation, and no Python runs
 // between the steps.  Every sub-batch calls exactly the library's public
-// entry points (hdp_prepare, hdp_grid_edges, hdp_mst_grid, hdp_forest_create,
+// entry points (hdp_prepare_u8, hdp_grid_edges_u8, hdp_mst_grid, hdp_forest_create,
 // hdp_aggregate_wta ...), so the results are those of the step-by-step path.
 #include <cuda_runtime.h>
 
@@ -135,28 +135,21 @@ static int dense_sub(const DenseJob& j) {
     HDP_CHECK_CUDA(cudaStreamWaitEvent(st, j.start, 0));
     const int64_t npp = (int64_t)j.h * j.w, n = (int64_t)j.nb * npp;
     const int64_t epp = 2 * npp - j.h - j.w, m = (int64_t)j.nb * epp;
-    DevBuf<double> il, ir;
     DevBuf<float> pl, pr, ew;
     DevBuf<int32_t> eu, ev, comp;
     DevBuf<uint64_t> key;
     DevBuf<uint8_t> in_tree;
-    HDP_TRY(il.alloc(n * j.c, st));
-    HDP_TRY(ir.alloc(n * j.c, st));
     HDP_TRY(pl.alloc(n * 4, st));
     HDP_TRY(pr.alloc(n * 4, st));
-    HDP_PCALL(hdp_u8_to_f64(j.left, il.get(), n * j.c, st));
-    HDP_PCALL(hdp_u8_to_f64(j.right, ir.get(), n * j.c, st));
-    HDP_PCALL(hdp_prepare(il.get(), j.nb, j.h, j.w, j.c, nullptr, nullptr, nullptr, pl.get(), st));
-    HDP_PCALL(hdp_prepare(ir.get(), j.nb, j.h, j.w, j.c, nullptr, nullptr, nullptr, pr.get(), st));
-    ir.release();
+    HDP_PCALL(hdp_prepare_u8(j.left, j.nb, j.h, j.w, j.c, pl.get(), st));
+    HDP_PCALL(hdp_prepare_u8(j.right, j.nb, j.h, j.w, j.c, pr.get(), st));
     HDP_TRY(eu.alloc(m + 1, st));
     HDP_TRY(ev.alloc(m + 1, st));
     HDP_TRY(ew.alloc(m + 1, st));
     HDP_TRY(key.alloc(m + 1, st));
     HDP_TRY(in_tree.alloc(m + 1, st));
     HDP_TRY(comp.alloc(n, st));
-    HDP_PCALL(hdp_grid_edges(il.get(), j.nb, j.h, j.w, j.c, eu.get(), ev.get(), ew.get(), key.get(), st));
-    il.release();
+    HDP_PCALL(hdp_grid_edges_u8(j.left, j.nb, j.h, j.w, j.c, eu.get(), ev.get(), ew.get(), key.get(), st));
     HDP_PCALL(hdp_mst_grid(j.nb, j.h, j.w, eu.get(), ev.get(), key.get(), in_tree.get(), comp.get(), nullptr, st));
     key.release();
     hdp_forest* f = nullptr;

@@ -178,3 +178,28 @@ def test_hdpf_exact():
         flat = np.concatenate([[wi * 32 + b for wi, x in enumerate(row) for b in range(32)
                                 if (int(x) >> b) & 1] for row in tm_h])
         np.testing.assert_array_equal(flat, g[p + "iv_flat"])
+
+
+@pytest.mark.parametrize("c,shape", [(3, (2, 37, 53)), (1, (1, 20, 1)), (3, (1, 1, 9))])
+def test_u8_prepare_and_edges_match_f64_path(c, shape):
+    """hdp_prepare_u8 / hdp_grid_edges_u8 (the one-call pipeline's level 0)
+    are bit-identical to u8 -> f64 -> hdp_prepare / hdp_grid_edges."""
+    import torch
+
+    from paper_1509_08197_b200 import _lib as L
+    from paper_1509_08197_b200 import engine as E
+
+    rng = np.random.default_rng(7)
+    b, h, w = shape
+    u8 = dev(rng.integers(0, 256, (b, h, w, c), dtype=np.uint8))
+    _, _, _, packed = E.prepare(E.to_f64(u8), False)
+    pk = torch.empty_like(packed)
+    L.call("hdp_prepare_u8", L.ptr(u8), b, h, w, c, L.ptr(pk), L.stream())
+    assert torch.equal(pk, packed)
+    eu, ev, ew, key, n_e = E.grid_edges(E.to_f64(u8))
+    if b * n_e:
+        eu2, ev2, ew2, key2 = (torch.empty_like(x) for x in (eu, ev, ew, key))
+        L.call("hdp_grid_edges_u8", L.ptr(u8), b, h, w, c, L.ptr(eu2), L.ptr(ev2), L.ptr(ew2), L.ptr(key2),
+               L.stream())
+        for x, y in ((eu, eu2), (ev, ev2), (ew, ew2), (key, key2)):
+            assert torch.equal(x, y)
