@@ -1288,9 +1288,13 @@ __global__ void __launch_bounds__(kChunkThreads, HDP_UP_CHUNK_MINB) k_up_chunk(A
     __shared__ unsigned long long bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     unsigned par = 0;
+    ChunkDesc dn;
+    if (blockIdx.x < nc) dn = descs[cbase + blockIdx.x];
     for (int64_t ci = blockIdx.x; ci < nc; ci += gridDim.x) {
     PROF_DECL;
-    const ChunkDesc d = descs[cbase + ci];
+    const ChunkDesc d = dn;
+    // a persistent CTA fetches its next descriptor while this chunk runs
+    if (ci + gridDim.x < nc) dn = descs[cbase + ci + gridDim.x];
     if (d.np == 0) continue;
     PROF_T(1);
     const ChunkSm s = stage_chunk<true>(a, d, sm4, &bar, par);
@@ -1376,9 +1380,13 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
     __shared__ unsigned long long bar;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     unsigned par = 0;
+    ChunkDesc dn;
+    if (blockIdx.x < nc) dn = descs[cbase + blockIdx.x];
     for (int64_t ci = blockIdx.x; ci < nc; ci += gridDim.x) {
     PROF_DECL;
-    const ChunkDesc d = descs[cbase + ci];
+    const ChunkDesc d = dn;
+    // a persistent CTA fetches its next descriptor while this chunk runs
+    if (ci + gridDim.x < nc) dn = descs[cbase + ci + gridDim.x];
     if (d.np == 0) continue;
     PROF_T(1);
     const ChunkSm s = stage_chunk<false>(a, d, sm4, &bar, par);
@@ -1842,8 +1850,11 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_CHECK_CUDA(cudaGetDevice(&dev));
     HDP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     static const int chunk_share = env_int("HDP_CHUNK_SHARE", 0), seg_share = env_int("HDP_SEG_SHARE", 0);
+    static const int chunk_persist = env_int("HDP_CHUNK_PERSIST", 0);  // CTAs per SM, 0 = one chunk per CTA
     auto cgrid = [&](int64_t nc, bool both) -> unsigned {
-        return (unsigned)(both && chunk_share > 0 ? std::min<int64_t>(nc, (int64_t)chunk_share * nsm) : nc);
+        int64_t g = both && chunk_share > 0 ? std::min<int64_t>(nc, (int64_t)chunk_share * nsm) : nc;
+        if (chunk_persist > 0) g = std::min<int64_t>(g, (int64_t)chunk_persist * nsm);
+        return (unsigned)g;
     };
     auto sgrid = [&](int64_t ng, bool both) -> unsigned {
         const int64_t need = grid_for(ng * 32, 32 * kSegWarps);
@@ -1873,7 +1884,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         if (side) {
             HDP_TRY(join_side(ss, st));
         } else if (chunks && nc > 0) {
-            k_up_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
+            k_up_chunk<<<cgrid(nc, false), kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
         } else if (!chunks && ns > 0) {
             k_scan_up_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
@@ -1897,7 +1908,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         if (side) {
             HDP_TRY(join_side(ss, st));
         } else if (chunks && nc > 0) {
-            k_down_chunk<<<(unsigned)nc, kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
+            k_down_chunk<<<cgrid(nc, false), kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
         } else if (!chunks && ns > 0) {
             k_down_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
