@@ -347,7 +347,7 @@ constexpr int GHASH = 4096;       // open-addressing table root -> slot
 
 struct GrpSmem {
     int32_t e[GW], la[GW], lb[GW];    // per window position: edge, root slots
-    int32_t ord[GW], grp[GW];         // positions sorted (stably) by group; group of each
+    int32_t ord[GW], grp[GW];         // next position of the same group (window order); group of each
     int32_t hkey[GHASH], hslot[GHASH];
     int32_t sroot[GSLOTS], gp[GSLOTS], mp[GSLOTS], sz[GSLOTS];
     uint32_t mask[GSLOTS * DR_NW];
@@ -389,8 +389,6 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                                             uint8_t* in_tree, int* rounds_out) {
     extern __shared__ unsigned long long g_dyn[];
     GrpSmem& s = *reinterpret_cast<GrpSmem*>(g_dyn);
-    typedef cub::BlockRadixSort<uint32_t, GW, 1, int32_t> Sort;
-    __shared__ typename Sort::TempStorage sort_tmp;
     // rule 2 as an exact integer test: merge iff inter >= thr[uni], where thr[u]
     // is the least i with !(RN(i / u) < beta) (RN(i / u) is monotone in i)
     __shared__ int16_t thr[8 * 32 + 1];
@@ -487,36 +485,60 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
             __syncthreads();
         }
         G_TICK(2);
-        // 4. positions sorted by group alone: the radix sort is stable and the
-        // input is in window (Kruskal) order, so every group becomes one run in
-        // Kruskal order.  Group 2047 = not live (a window of GW - 1 edges
-        // touches at most 2 GW - 2 roots, so no live group has that slot).
-        uint32_t key[1] = {live ? (uint32_t)grp_find(s.gp, la) : 2047u};
-        int32_t val[1] = {tid};
+        // 4. per-group lists in window (Kruskal) order: ord[i] = the next window
+        // position of i's group (-1 at the end).  Inside a warp the next
+        // occurrence is the next higher peer lane; from a warp's last occurrence
+        // the list continues in the next warp holding the group (a per-group
+        // warp bitmask), at that warp's first lane of the group.  The group's
+        // first occurrence walks it (no sort).
+        uint32_t* wm = reinterpret_cast<uint32_t*>(s.hslot);  // the hash slots are no longer read
+        for (int i = tid; i < GSLOTS; i += GW) wm[i] = 0u;
+        const int g = live ? grp_find(s.gp, la) : -1;
+        s.grp[tid] = g;
         __syncthreads();
-        Sort(sort_tmp).Sort(key, val, 0, 11);
-        s.ord[tid] = val[0];
-        s.grp[tid] = key[0] == 2047u ? -1 : (int)key[0];
+        const int lane = tid & 31, warp = tid >> 5;
+        const unsigned peers = __match_any_sync(0xffffffffu, g);
+        const bool lowest = __ffs(peers) - 1 == lane;
+        if (g >= 0 && lowest) atomicOr(&wm[g], 1u << warp);
+        __syncthreads();
+        bool walker = false;
+        if (g >= 0) {
+            const unsigned higher = peers & ~((2u << lane) - 1u);
+            int nx = -1;
+            const uint32_t m = wm[g];
+            if (higher) {
+                nx = warp * 32 + __ffs(higher) - 1;
+            } else {
+                const uint32_t later = warp == 31 ? 0u : (m & ~((2u << warp) - 1u));
+                if (later) {
+                    const int w2 = __ffs(later) - 1;
+                    int j = 0;
+                    while (s.grp[w2 * 32 + j] != g) j++;
+                    nx = w2 * 32 + j;
+                }
+            }
+            s.ord[tid] = nx;
+            walker = lowest && warp == __ffs(m) - 1;
+        }
         __syncthreads();
         G_TICK(3);
-        // 5. one thread per group walks its run
-        {
-            const int g = s.grp[tid];
-            if (g >= 0 && (tid == 0 || s.grp[tid - 1] != g)) {
+        // 5. the first occurrence of every group walks its list
+        if (walker) {
+            {
             int n_g = 0;
             // the next edge's indices are fetched while this one is decided
-            int pos_n = s.ord[tid];
+            int pos_n = tid;
             int la_n = s.la[pos_n], lb_n = s.lb[pos_n];
             // register copy of the last surviving root (runs mostly grow one
             // tree): its size and mask are read from / flushed to shared
             // memory only when the cached root changes
             int cr = -1, csz = 0;
             uint32_t cm[DR_NW];
-            for (int q = tid; q < GW && s.grp[q] == g; q++) {
+            while (pos_n >= 0) {
                 n_g++;
                 const int pos = pos_n, la_q = la_n, lb_q = lb_n;
-                if (q + 1 < GW) {
-                    pos_n = s.ord[q + 1];
+                pos_n = s.ord[pos];
+                if (pos_n >= 0) {
                     la_n = s.la[pos_n];
                     lb_n = s.lb[pos_n];
                 }
