@@ -383,6 +383,17 @@ __device__ __forceinline__ int grp_find(int32_t* p, int x) {
     return x;
 }
 
+// read-only find for the sequential walk: no path-halving stores, so the two
+// finds of an edge are independent loads (union by size keeps paths short)
+__device__ __forceinline__ int grp_find_ro(const int32_t* p, int x) {
+    int y = p[x];
+    while (y != x) {
+        x = y;
+        y = p[x];
+    }
+    return x;
+}
+
 __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
                                             const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                                             int32_t* uf, int32_t* usz, uint32_t* tm, int nw, double beta,
@@ -542,7 +553,7 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                     la_n = s.la[pos_n];
                     lb_n = s.lb[pos_n];
                 }
-                int x = grp_find(s.mp, la_q), y = grp_find(s.mp, lb_q);
+                int x = grp_find_ro(s.mp, la_q), y = grp_find_ro(s.mp, lb_q);
                 if (x == y) continue;  // joined earlier in this window: a cycle
                 if (y == cr) {  // keep the cached root in x
                     y = x;
