@@ -571,18 +571,26 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     return outs
 
 
-def run_baseline_host(left_u8: np.ndarray, right_u8: np.ndarray, d_max: int, **kw):
+def run_baseline_host(left_u8: np.ndarray, right_u8: np.ndarray, d_max: int, out=None, **kw):
     """Host-buffer entry point: (B, H, W, C) uint8 numpy (pinned if the caller
     wants async copies) -> (disparity (B, H, W) int32, min_cost (B, H, W)
-    float32) numpy.  The copies in both directions are part of the call."""
+    float32) numpy.  The copies in both directions are part of the call.
+    out: optional (disparity, min_cost) host tensors / arrays to fill (pinned:
+    the device->host copies then run as DMA on the stream, one synchronise)."""
     torch = _t()
     dev = L.device()
     lt = torch.from_numpy(left_u8) if isinstance(left_u8, np.ndarray) else left_u8
     rt = torch.from_numpy(right_u8) if isinstance(right_u8, np.ndarray) else right_u8
     ld = lt.to(dev, non_blocking=True)
     rd = rt.to(dev, non_blocking=True)
-    out = run_baseline_batch(ld, rd, d_max, **kw)
-    return out.disparity.cpu().numpy(), out.min_cost.cpu().numpy()
+    res = run_baseline_batch(ld, rd, d_max, **kw)
+    if out is None:
+        return res.disparity.cpu().numpy(), res.min_cost.cpu().numpy()
+    od, oc = (torch.from_numpy(o) if isinstance(o, np.ndarray) else o for o in out)
+    od.copy_(res.disparity, non_blocking=True)
+    oc.copy_(res.min_cost, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return od.numpy(), oc.numpy()
 
 
 def run_hdp_host(left_u8, right_u8, d_max: int, model, **kw):

@@ -137,3 +137,25 @@ def test_dense_pipeline_slab_lanes_match():
     torch.cuda.synchronize()
     assert torch.equal(got.disparity, ref.disparity)
     assert torch.equal(got.min_cost, ref.min_cost)
+
+
+def test_host_entry_with_pinned_outputs():
+    """run_baseline_host(out=pinned buffers) returns the same maps as the
+    default (fresh arrays) path and fills the given buffers."""
+    import torch
+
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import CONFIGS, make_scene
+
+    spec = CONFIGS[2]
+    scenes = [make_scene(spec, i) for i in range(2)]
+    Lh = np.stack([s.pair.left.data[:64, :100] for s in scenes])
+    Rh = np.stack([s.pair.right.data[:64, :100] for s in scenes])
+    d0, c0 = E.run_baseline_host(Lh, Rh, spec.d_max)
+    od = torch.empty(d0.shape, dtype=torch.int32).pin_memory()
+    oc = torch.empty(c0.shape, dtype=torch.float32).pin_memory()
+    d1, c1 = E.run_baseline_host(torch.from_numpy(Lh).pin_memory(), torch.from_numpy(Rh).pin_memory(),
+                                 spec.d_max, out=(od, oc))
+    np.testing.assert_array_equal(d1, d0)
+    np.testing.assert_array_equal(c1, c0)
+    np.testing.assert_array_equal(od.numpy(), d0)
