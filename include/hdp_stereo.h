@@ -125,6 +125,12 @@ int hdp_prior_counts(const double *unit_l, const double *grad_l, const double *u
                      int stride, int window, int max_offset, double alpha, double tau_c,
                      double tau_g, int64_t *counts, int64_t *kept, void *stream);
 
+/* predict_intervals (hdp_model.py:498-525) for nrows rows of Bayes matrices
+ * (rows x ncols f64, ncols <= 256): stable descending order, sequential
+ * running mass, first P/(c+P) < delta stops; out masks (nrows, nw) u32
+ * bitsets over the columns (pack of DisparityIntervalTable.masks()). */
+int hdp_predict_masks(const double *bayes, int64_t nrows, int ncols, double delta, uint32_t *masks, int nw,
+                      void *stream);
 /* assign_pixel_intervals (hdp_forest.py:91-123): pixel_row[g] =
  * parent_disp[b, r/S, c/S]; DATA error if a parent disparity is outside
  * [0, n_rows). */

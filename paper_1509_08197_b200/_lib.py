@@ -39,6 +39,7 @@ SIGNATURES = {
     "hdp_mst": (_I, [_I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "hdp_prepare_u8": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "hdp_grid_edges_u8": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "hdp_predict_masks": (_I, [_P, _I64, _I, _D, _P, _I, _P]),
     "hdp_mst_grid": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "hdp_prior_counts": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _D, _D, _D,
                               _P, _P, _P]),

@@ -155,9 +155,83 @@ __global__ void k_assign_rows(const int32_t* __restrict__ pd, int batch, int ph,
     rows[t] = v;
 }
 
+// predict_intervals (hdp_model.py:498-525) for every (pair, parent row) on
+// the device: one warp per row of the Bayes matrix.  The stable descending
+// order is a rank count (greater values first, equal values in index order --
+// np.argsort(-P, kind="stable")); lane 0 then runs the running mass in that
+// order exactly as np.cumsum (sequential) and stops at the first
+// P / (c + P) < delta; the chosen ranks become the row's bitset, one ballot
+// per 32 columns (lane l of register r holds column 32 r + l).
+constexpr int kPmMaxCols = 256;
+__global__ void __launch_bounds__(256) k_predict_masks(const double* __restrict__ bayes, int64_t nrows, int ncols,
+                                                       double delta, uint32_t* __restrict__ masks, int nw) {
+    __shared__ double sv[8][kPmMaxCols];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * 8 + wib;
+    if (row >= nrows) return;
+    const double* pr = bayes + row * ncols;
+    double v[8];
+    int rk[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const int j = 32 * r + lane;
+        v[r] = j < ncols ? pr[j] : 0.0;
+        rk[r] = 0;
+    }
+#pragma unroll
+    for (int rj = 0; rj < 8; rj++) {
+        if (32 * rj >= ncols) break;
+        for (int sj = 0; sj < 32; sj++) {
+            const int j = 32 * rj + sj;
+            if (j >= ncols) break;
+            const double vj = __shfl_sync(0xffffffffu, v[rj], sj);
+#pragma unroll
+            for (int r = 0; r < 8; r++) {
+                const int i = 32 * r + lane;
+                rk[r] += (vj > v[r] || (vj == v[r] && j < i)) ? 1 : 0;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r++)
+        if (32 * r + lane < ncols) sv[wib][rk[r]] = v[r];
+    __syncwarp();
+    int k = ncols;
+    if (lane == 0) {
+        double c = sv[wib][0];
+        for (int t = 1; t < ncols; t++) {
+            const double p = sv[wib][t];
+            if (__ddiv_rn(p, __dadd_rn(c, p)) < delta) {
+                k = t;
+                break;
+            }
+            c = __dadd_rn(c, p);
+        }
+    }
+    k = __shfl_sync(0xffffffffu, k, 0);
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const unsigned word = __ballot_sync(0xffffffffu, 32 * r + lane < ncols && rk[r] < k);
+        if (lane == 0 && r < nw) masks[row * nw + r] = word;
+    }
+}
+
 }  // namespace hdp
 
 using namespace hdp;
+
+extern "C" int hdp_predict_masks(const double* bayes, int64_t nrows, int ncols, double delta, uint32_t* masks,
+                                 int nw, void* stream) {
+    HDP_REQUIRE(ncols >= 1 && ncols <= kPmMaxCols, HDP_ERR_CONFIG, "interval table has %d columns (max %d)", ncols,
+                kPmMaxCols);
+    HDP_REQUIRE(nw == (ncols + 31) / 32, HDP_ERR_CONFIG, "mask words %d do not cover %d columns", nw, ncols);
+    if (nrows <= 0) return HDP_OK;
+    k_predict_masks<<<(unsigned)((nrows + 7) / 8), 256, 0, (cudaStream_t)stream>>>(bayes, nrows, ncols, delta, masks,
+                                                                                   nw);
+    note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
 
 extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, const double* unit_r,
                                 const double* grad_r, int batch, int h, int w, int c, int d_max,

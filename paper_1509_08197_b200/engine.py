@@ -294,6 +294,19 @@ def predict_masks(bayes, delta: float):
     return chosen
 
 
+def predict_masks_device(bayes, delta: float, device):
+    """predict_masks + pack_masks on the device (hdp_predict_masks): (B, rows,
+    cols) f64 host Bayes matrices -> (B, rows, nw) int32-viewed u32 bitsets on
+    `device`, bit-identical to the host functions."""
+    torch = _t()
+    b, rows, cols = bayes.shape
+    nw = (cols + 31) // 32
+    bd = torch.from_numpy(np.ascontiguousarray(bayes, dtype=np.float64)).to(device, non_blocking=True)
+    out = torch.empty((b, rows, nw), dtype=torch.int32, device=device)
+    L.call("hdp_predict_masks", L.ptr(bd), b * rows, cols, float(delta), L.ptr(out), nw, L.stream())
+    return out
+
+
 def pack_masks(chosen) -> np.ndarray:
     """(…, d+1) bool -> (…, nw) uint32 bitsets."""
     d1 = chosen.shape[-1]
@@ -543,9 +556,9 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
         priors = priors_from_counts(counts_h, kept_h)
         cond = conditional_matrix(model.layers[level], lev.d_max, lv[level + 1].d_max, block_size)
         bm, _ = bayes_batched(cond, priors)
-        chosen = predict_masks(bm, delta0 * block_size**level)
-        row_masks = torch.from_numpy(pack_masks(chosen).view(np.int32)).to(lev.img_l.device)
-        rows = assign_rows(parent.contiguous(), lev.h, lev.w, block_size, chosen.shape[1])
+        row_masks = predict_masks_device(bm, delta0 * block_size**level, lev.img_l.device)
+        chosen = predict_masks(bm, delta0 * block_size**level) if keep else None
+        rows = assign_rows(parent.contiguous(), lev.h, lev.w, block_size, bm.shape[1])
         t0 = lclock.lap("predict", t0)
         eu, ev, ew, key, E = grid_edges(lev.img_l)
         if tree_kind == "rt":

@@ -203,3 +203,22 @@ def test_u8_prepare_and_edges_match_f64_path(c, shape):
                L.stream())
         for x, y in ((eu, eu2), (ev, ev2), (ew, ew2), (key, key2)):
             assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("cols,delta", [(81, 0.064), (17, 0.004), (241, 0.004), (2, 0.5), (33, 0.9)])
+def test_predict_masks_device_matches_host(cols, delta):
+    """hdp_predict_masks == pack_masks(predict_masks(...)) bit for bit, with
+    heavy ties (quantised probabilities) and zero rows made uniform."""
+    import torch
+
+    from paper_1509_08197_b200 import engine as E
+
+    rng = np.random.default_rng(cols)
+    b, rows = 3, 23
+    raw = np.floor(rng.random((b, rows, cols)) ** 4 * 16) / 16  # many exact ties and zeros
+    raw[0, 0] = 0.0
+    rs = raw.sum(-1, keepdims=True)
+    bayes = np.where(rs > 0, raw / np.where(rs > 0, rs, 1), 1.0 / cols)
+    want = E.pack_masks(E.predict_masks(bayes, delta)).view(np.int32)
+    got = E.predict_masks_device(bayes, delta, torch.device("cuda")).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
