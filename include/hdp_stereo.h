@@ -177,6 +177,9 @@ int hdp_forest_export(const hdp_forest *f, int32_t *parent, int32_t *depth, int3
  * every tree gets x0 .. x0+nx-1 (dense baseline / a disparity slab). */
 int hdp_forest_set_lanes(hdp_forest *f, const uint32_t *tree_masks, int nw, void *stream);
 int hdp_forest_set_lanes_range(hdp_forest *f, int x0, int nx, void *stream);
+/* set_lanes from per-node masks (n_nodes, nw) valid at every node (hdp_hdpf's
+ * tree_masks): each tree's mask is read at its root. */
+int hdp_forest_set_lanes_nodes(hdp_forest *f, const uint32_t *node_masks, int nw, void *stream);
 
 /* Stored entries sum_p |interval(tree(p))| (hdp_forest.py:144-148) and,
  * optionally, the per-node offsets of the pixel-major volume layout. */

@@ -51,6 +51,7 @@ SIGNATURES = {
     "hdp_forest_export": (_I, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "hdp_forest_set_lanes": (_I, [_P, _P, _I, _P]),
     "hdp_forest_set_lanes_range": (_I, [_P, _I, _I, _P]),
+    "hdp_forest_set_lanes_nodes": (_I, [_P, _P, _I, _P]),
     "hdp_forest_entries": (_I, [_P, C.POINTER(_I64), _P, _P]),
     "hdp_aggregate_wta": (_I, [_P, _P, _P, _I, _I, _I, _F, _F, _F, _P, _P, _P, _P, _P, _P]),
     "hdp_forest_pair_stats": (_I, [_P, _I, _I64, _P, _P, _P]),

@@ -709,12 +709,28 @@ __global__ void k_iota(int64_t n, int32_t* a, int32_t x0) {
     if (i < n) a[i] = x0 + (int32_t)i;
 }
 
-__global__ void k_lanes_count(int64_t nt, const uint32_t* __restrict__ masks, int nw, int32_t* t_m) {
+// lanes per tree; the smallest count lands in *mn (an empty interval is an
+// error, cost_volume.py:212-213)
+__global__ void k_lanes_count(int64_t nt, const uint32_t* __restrict__ masks, int nw, int32_t* t_m, int32_t* mn) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= nt) return;
-    int c = 0;
-    for (int i = 0; i < nw; i++) c += __popc(masks[t * nw + i]);
-    t_m[t] = c;
+    int c = 0x7fffffff;
+    if (t < nt) {
+        c = 0;
+        for (int i = 0; i < nw; i++) c += __popc(masks[t * nw + i]);
+        t_m[t] = c;
+    }
+    c = __reduce_min_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c != 0x7fffffff) atomicMin(mn, c);
+}
+
+// per-node masks (valid at every node, e.g. hdp_hdpf's tree_masks) -> per tree,
+// read at each tree's root
+__global__ void k_tree_masks(int64_t n, const int32_t* __restrict__ root, const int32_t* __restrict__ tree_id,
+                             const uint32_t* __restrict__ node_masks, int nw, uint32_t* out) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n || root[v] != v) return;
+    const int64_t t = tree_id[v];
+    for (int i = 0; i < nw; i++) out[t * nw + i] = node_masks[v * nw + i];
 }
 
 __global__ void k_lanes_fill(int64_t nt, const uint32_t* __restrict__ masks, int nw,
@@ -1655,6 +1671,17 @@ int hdp_forest_export(const hdp_forest* f, int32_t* parent, int32_t* depth, int3
     return HDP_OK;
 }
 
+int hdp_forest_set_lanes_nodes(hdp_forest* f, const uint32_t* node_masks, int nw, void* stream) {
+    HDP_REQUIRE(f != nullptr, HDP_ERR_CONFIG, "null forest");
+    HDP_REQUIRE(nw >= 1, HDP_ERR_CONFIG, "mask width must be >= 1 word");
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf<uint32_t> tm;
+    HDP_TRY(tm.alloc((size_t)f->n_trees * nw + 1, st));
+    k_tree_masks<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, f->root.get(), f->tree_id.get(), node_masks, nw,
+                                                      tm.get()); note_launch();
+    return hdp_forest_set_lanes(f, tm.get(), nw, stream);
+}
+
 int hdp_forest_set_lanes_range(hdp_forest* f, int x0, int nx, void* stream) {
     HDP_REQUIRE(f != nullptr, HDP_ERR_CONFIG, "null forest");
     HDP_REQUIRE(nx >= 1 && x0 >= 0, HDP_ERR_CONFIG, "empty disparity range");
@@ -1681,28 +1708,25 @@ int hdp_forest_set_lanes(hdp_forest* f, const uint32_t* tree_masks, int nw, void
     f->max_d = 32 * nw - 1;
     HDP_TRY(f->t_m.alloc(f->n_trees, st));
     HDP_TRY(f->t_doff.alloc(f->n_trees + 1, st));
-    k_lanes_count<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw, f->t_m.get()); note_launch();
+    DevBuf<int32_t> mn;  // (min lanes, last offset, last count)
+    HDP_TRY(mn.alloc(3, st));
+    const int32_t big = 0x7fffffff;
+    HDP_CHECK_CUDA(cudaMemcpyAsync(mn.get(), &big, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    k_lanes_count<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw, f->t_m.get(), mn.get());
+    note_launch();
     HDP_TRY(exclusive_sum(f->t_m.get(), f->t_doff.get(), f->n_trees, st));
-    int32_t a = 0, b = 0;
-    HDP_TRY(to_host(&a, f->t_doff.get() + f->n_trees - 1, 1, st));
-    HDP_TRY(to_host(&b, f->t_m.get() + f->n_trees - 1, 1, st));
-    HDP_TRY(f->dlist.alloc((size_t)a + b + 1, st));
+    // one host read for the list size and the empty-interval check
+    HDP_CHECK_CUDA(cudaMemcpyAsync(mn.get() + 1, f->t_doff.get() + f->n_trees - 1, sizeof(int32_t),
+                                   cudaMemcpyDeviceToDevice, st));
+    HDP_CHECK_CUDA(cudaMemcpyAsync(mn.get() + 2, f->t_m.get() + f->n_trees - 1, sizeof(int32_t),
+                                   cudaMemcpyDeviceToDevice, st));
+    int32_t h[3] = {0, 0, 0};
+    HDP_TRY(to_host(h, mn.get(), 3, st));
+    HDP_REQUIRE(h[0] >= 1, HDP_ERR_INTERNAL, "a tree has an empty disparity interval");
+    HDP_TRY(f->dlist.alloc((size_t)h[1] + h[2] + 1, st));
     k_lanes_fill<<<grid_for(f->n_trees, 256), 256, 0, st>>>(f->n_trees, tree_masks, nw,
                                                             f->t_doff.get(), f->dlist.get()); note_launch();
     HDP_CHECK_LAUNCH();
-    {
-        DevBuf<int32_t> mn;
-        // every tree needs a non-empty interval (cost_volume.py:212-213)
-        HDP_TRY(mn.alloc(1, st));
-        size_t bytes = 0;
-        HDP_CHECK_CUDA(cub::DeviceReduce::Min(nullptr, bytes, f->t_m.get(), mn.get(), (int)f->n_trees, st));
-        DevBuf<char> tmp;
-        HDP_TRY(tmp.alloc(bytes, st));
-        HDP_CHECK_CUDA(cub::DeviceReduce::Min(tmp.get(), bytes, f->t_m.get(), mn.get(), (int)f->n_trees, st));
-        int32_t h = 0;
-        HDP_TRY(to_host(&h, mn.get(), 1, st));
-        HDP_REQUIRE(h >= 1, HDP_ERR_INTERNAL, "a tree has an empty disparity interval");
-    }
     return lanes_finish(f, 0);
 }
 

@@ -189,6 +189,11 @@ class DeviceForest:
         L.call("hdp_forest_set_lanes_range", self._h, int(x0), int(nx), L.stream())
         self._entries()
 
+    def set_lanes_nodes(self, node_masks):
+        """node_masks: (n, nw) int32/uint32 bitsets valid at every node (hdpf)."""
+        L.call("hdp_forest_set_lanes_nodes", self._h, L.ptr(node_masks), node_masks.shape[1], L.stream())
+        self._entries()
+
     def set_lanes(self, tree_masks):
         """tree_masks: (n_trees, nw) int32/uint32 bitsets on the device."""
         L.call("hdp_forest_set_lanes", self._h, L.ptr(tree_masks), tree_masks.shape[1], L.stream())
@@ -539,7 +544,7 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     eu, ev, ew, key, E = grid_edges(top.img_l)
     if tree_kind == "rt":
         key = rt_keys(E, b, seed, top.img_l.device)
-    in_tree, comp, _ = mst(b * top.h * top.w, eu, ev, key)
+    in_tree, comp, _ = mst_grid(b, top.h, top.w, eu, ev, key)
     lclock = _Clock(timing)
     f, disp, mc, _, vol = _forest_layer(top, eu, ev, ew, in_tree, comp, gamma, cost, None,
                                         want_volume=want_volume, clock=lclock, t0=t0)
@@ -566,22 +571,27 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
         in_tree, comp, tmasks, rounds = hdpf(b, lev.h * lev.w, E, eu, ev, key, rows,
                                              row_masks.contiguous(), beta)
         fo = DeviceForest(b * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
-        roots = fo.export()["root"]
-        ar = torch.arange(fo.n, device=roots.device, dtype=torch.int32)
-        root_ids = torch.nonzero(roots == ar).flatten()
-        fo.set_lanes(tmasks[root_ids].contiguous())
+        fo.set_lanes_nodes(tmasks.contiguous())
         t0 = lclock.lap("forest", t0)
         disp, mc, _, vol = fo.aggregate(lev, cost, want_volume=want_volume)
         lclock.lap("cost_aggregate", t0)
         o = finish(lev, fo, disp, mc, vol, dict(lclock.acc))
         o.extra.update(counts=counts_h, kept=kept_h, chosen=chosen if keep else None,
                        dr_rounds=rounds,
-                       tree_masks=(tmasks[root_ids].cpu().numpy().view(np.uint32)
-                                   if keep else None))
+                       tree_masks=(_tree_masks_host(fo, tmasks) if keep else None))
         if on_level is not None:
             on_level(o)
         parent = o.disparity if teacher is None or level not in teacher else teacher[level]
     return outs
+
+
+def _tree_masks_host(fo: DeviceForest, tmasks):
+    """Per-tree masks (trees numbered by root id) on the host (keep=True)."""
+    torch = _t()
+    roots = fo.export()["root"]
+    ar = torch.arange(fo.n, device=roots.device, dtype=torch.int32)
+    root_ids = torch.nonzero(roots == ar).flatten()
+    return tmasks[root_ids].cpu().numpy().view(np.uint32)
 
 
 def run_baseline_host(left_u8: np.ndarray, right_u8: np.ndarray, d_max: int, out=None, **kw):
