@@ -307,17 +307,25 @@ __device__ __forceinline__ uint64_t ld_word(const uint64_t* p) {
 __device__ __forceinline__ void st_word(uint64_t* p, uint64_t w) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
+// The grid is resident (at most the CTAs the GPU holds at once) and sweeps
+// its entries one jump each until all are done: every chain then shortens
+// like synchronous rounds (O(log length) sweeps).  A non-resident thread
+// would find its successors not started yet and walk long chains hop by hop.
 __global__ void k_rank_jump_async(const int32_t* __restrict__ count, uint64_t* word) {
     const int32_t nr = *count;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t w = ld_word(word + i);
-        for (;;) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (;;) {
+        bool more = false;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += stride) {
+            uint64_t w = ld_word(word + i);
             const int32_t nx = (int32_t)(w >> 32);
-            if (nx < 0) break;
+            if (nx < 0) continue;
             const uint64_t w2 = ld_word(word + nx);
             w = (w2 & 0xffffffff00000000ull) | (uint32_t)((uint32_t)w + (uint32_t)w2);
             st_word(word + i, w);
+            more = more || (int32_t)(w >> 32) >= 0;
         }
+        if (!more) break;
     }
 }
 
@@ -488,17 +496,20 @@ __device__ __forceinline__ long long hp_chain(const int32_t* dmax) { return (lon
 // head's word points at itself
 __global__ void k_hp_jump_async(const int32_t* __restrict__ list, const int32_t* __restrict__ cnt, uint64_t* word) {
     const int32_t nl = *cnt;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = list[i];
-        uint64_t w = ld_word(word + v);
-        for (;;) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (;;) {
+        bool more = false;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
+            const int32_t v = list[i];
+            const uint64_t w = ld_word(word + v);
             const int32_t h = (int32_t)(w >> 32);
             const uint64_t w2 = ld_word(word + h);
             const int32_t hh = (int32_t)(w2 >> 32);
-            if (hh == h) break;  // h is a head
-            w = hp_word(hh, (int32_t)((uint32_t)w + (uint32_t)w2));
-            st_word(word + v, w);
+            if (hh == h) continue;  // h is a head: done
+            st_word(word + v, hp_word(hh, (int32_t)((uint32_t)w + (uint32_t)w2)));
+            more = true;
         }
+        if (!more) break;
     }
 }
 
@@ -902,6 +913,20 @@ __global__ void k_forest_summary(int64_t n, int32_t* cnt, const int32_t* __restr
 
 using namespace hdp;
 
+// CTAs of `block` threads for `items`, capped at what the GPU holds resident
+// (the asynchronous jump kernels rely on all their threads running at once)
+static unsigned resident_grid(int64_t items, int block) {
+    static int cap = 0;
+    if (cap == 0) {
+        int dev = 0, nsm = 148, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&per, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+        cap = nsm * std::max(1, per / block);
+    }
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(items, block), cap));
+}
+
 // pointer jumping without grid barriers (one launch); HDP_SYNC_JUMP=1: the
 // round-synchronous launches (diagnostics / A-B)
 static bool async_jump() {
@@ -1057,8 +1082,10 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                           owner.get(), local.get(), wa.get()); note_launch();
         // the longest ruler chain is at most the largest tree's tour, 2 (size - 1) arcs
         const int rounds = ceil_log2(2 * (int64_t)max_tree);
-        if (async_jump()) {
-            k_rank_jump_async<<<grid_for(rmax, B), B, 0, st>>>(rid.get() + na, wa.get()); note_launch();
+        // asynchronous jumping pays while the ruler chains are short; one giant
+        // tour (C5: 715k rulers in one chain) converges faster in synchronous rounds
+        if (async_jump() && 2 * (int64_t)max_tree / kRuler <= (1 << 16)) {
+            k_rank_jump_async<<<resident_grid(rmax, B), B, 0, st>>>(rid.get() + na, wa.get()); note_launch();
         } else {
             for (int r = 0; r < rounds; r++) {
                 k_rank_jump_n<<<grid_for(rmax, B), B, 0, st>>>(rid.get() + na, wa.get(), wb.get()); note_launch();
@@ -1132,7 +1159,8 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                 hlist.get(), hcnt.get()); note_launch();
         const int jg = (int)std::min<int64_t>(grid_for(n / kHpRuler + 1, B), 148 * 8);
         if (async_jump()) {
-            k_hp_jump_async<<<jg, B, 0, st>>>(hlist.get(), hcnt.get(), ba); note_launch();
+            k_hp_jump_async<<<resident_grid(n / kHpRuler + 1, B), B, 0, st>>>(hlist.get(), hcnt.get(), ba);
+            note_launch();
             // zero rounds executed: the unpack reads buffer a
             k_hp_unpack<<<grid_for(n, B), B, 0, st>>>(n, nearw.get(), ba, bb, dmax.get(), 0, hp.get(), dist.get());
         } else {
