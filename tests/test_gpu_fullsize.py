@@ -77,3 +77,20 @@ def test_dense_wide_rows_match_oracle():
     assert_disp_parity(got, ref.disparity, ref.min_cost, ref.second_cost, "d512")
     same = got == ref.disparity
     assert_cost_parity(out.min_cost[0].cpu().numpy()[same], ref.min_cost[same], "d512 costs")
+
+
+def test_dense_giant_tree_matches_oracle():
+    """One 600x1000 pair (600 k nodes, one tree): the Euler-tour ranking takes
+    the synchronous rounds here (a single ruler chain above 64 k rulers, as at
+    C5), the smaller configurations the asynchronous jumps."""
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import SceneSpec, make_scene
+    from oracle import oracle as O
+
+    sc = make_scene(SceneSpec(5, 600, 1000, 12, 40, 0.3, 8.0, 1), 0)
+    out = E.run_baseline_batch(dev(sc.pair.left.data[None]), dev(sc.pair.right.data[None]), 12)
+    ref = O.run_baseline(sc.pair.left.data, sc.pair.right.data, 12)
+    got = out.disparity[0].cpu().numpy()
+    assert_disp_parity(got, ref.disparity, ref.min_cost, ref.second_cost, "giant tree")
+    same = got == ref.disparity
+    assert_cost_parity(out.min_cost[0].cpu().numpy()[same], ref.min_cost[same], "giant tree costs")
