@@ -116,6 +116,66 @@ __device__ int warp_wta(const PriorArgs& a, const double* su, const double* sg, 
     return bx;
 }
 
+// The 7 x 7 window (the reference default) with numpy's summation split over
+// lanes: element q >= 1 of the window goes to accumulator (q - 1) & 7, and each
+// accumulator is a sequential sum of 6 elements, so lane group g (8 lanes)
+// evaluates disparity x0 + g and lane k of the group accumulates chain k;
+// the pairwise tree ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) is three xor-shuffle
+// levels (IEEE addition is commutative), lane 0 adds `first`.  Four disparities
+// per warp step instead of one per lane: no per-element branches, and the
+// window geometry of a lane (6 rows/columns) is fixed per centre.
+__device__ int warp_wta7(const PriorArgs& a, const double* su, const double* sg, const double* du,
+                         const double* dg, int64_t base, int cr, int cc, int sign) {
+    const int lane = threadIdx.x & 31, k = lane & 7, g = lane >> 3;
+    const int64_t ro0 = base + (int64_t)min(max(cr - 3, 0), a.h - 1) * a.w;
+    const int col0 = min(max(cc - 3, 0), a.w - 1);
+    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    int bx = 0x7fffffff;
+    for (int x0 = 0; x0 <= a.d_max; x0 += 4) {
+        const int x = x0 + g;
+        const bool ok = x <= a.d_max;
+        double acc = 0.0;
+        if (ok) {
+#pragma unroll 1
+            for (int t = 0; t < 6; t++) {
+                const int q = k + 1 + 8 * t;  // window element 1..48
+                const int dr = q / 7, dc = q - 7 * dr;
+                const int64_t ro = base + (int64_t)min(max(cr + dr - 3, 0), a.h - 1) * a.w;
+                const int col = min(max(cc + dc - 3, 0), a.w - 1);
+                const int dcol = col + sign * x;
+                const double v = (dcol >= 0 && dcol < a.w) ? px_cost(a, su, sg, du, dg, ro + col, ro + dcol)
+                                                           : a.border;
+                acc = t == 0 ? v : __dadd_rn(acc, v);
+            }
+        }
+        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+        if (k == 0 && ok) {
+            const int dcol = col0 + sign * x;
+            const double first = (dcol >= 0 && dcol < a.w) ? px_cost(a, su, sg, du, dg, ro0 + col0, ro0 + dcol)
+                                                           : a.border;
+            const double v = __ddiv_rn(__dadd_rn(first, acc), 49.0);
+            if (v < best) {  // x ascends per group: strict < keeps the first minimum
+                best = v;
+                bx = x;
+            }
+        }
+    }
+    // first minimum over the four groups (lanes 0, 8, 16, 24)
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+        if (ob < best || (ob == best && ox < bx)) {
+            best = ob;
+            bx = ox;
+        }
+    }
+    return __shfl_sync(0xffffffffu, bx, 0);
+}
+
+template <bool W7>
 __global__ void __launch_bounds__(256) k_prior(PriorArgs a, int batch) {
     int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int64_t per = (int64_t)a.nrc * a.ncc;
@@ -127,10 +187,12 @@ __global__ void __launch_bounds__(256) k_prior(PriorArgs a, int batch) {
     int cr = (rs + min(rs + a.stride, a.h) - 1) / 2;
     int cc = (cs + min(cs + a.stride, a.w) - 1) / 2;
     int64_t base = (int64_t)b * a.h * a.w;
-    int dl = warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
+    int dl = W7 ? warp_wta7(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1)
+                : warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
     int mc = cc - dl;
     if (mc < 0) return;  // infeasible (hdp_model.py:458-459)
-    int dr = warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
+    int dr = W7 ? warp_wta7(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1)
+                : warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
     int diff = dl - dr;
     if (diff < 0) diff = -diff;
     if ((threadIdx.x & 31) == 0 && diff <= a.max_offset) {
@@ -258,7 +320,11 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
     a.kept = (unsigned long long*)kept;
     int64_t warps = (int64_t)a.nrc * a.ncc * batch;
     if (warps == 0) return HDP_OK;
-    k_prior<<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch); note_launch();
+    if (window == 7)
+        k_prior<true><<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch);
+    else
+        k_prior<false><<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch);
+    note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }
