@@ -1584,6 +1584,11 @@ __global__ void k_keys_finish(int64_t n, const unsigned long long* __restrict__ 
 struct SideStream {
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    // segments of a phase that also has chunks: a high-priority stream, so the
+    // block scheduler hands freed SM slots to pending segment CTAs first and the
+    // two kinds actually run side by side (HDP_SEG_PRIO=0: off)
+    cudaStream_t hi = nullptr;
+    cudaEvent_t hjoin = nullptr;
 };
 
 static int side_stream(SideStream** out) {
@@ -1596,6 +1601,10 @@ static int side_stream(SideStream** out) {
         HDP_CHECK_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
         HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
         HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+        int lo = 0, hi = 0;
+        HDP_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        HDP_CHECK_CUDA(cudaStreamCreateWithPriority(&ss.hi, cudaStreamNonBlocking, hi));
+        HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.hjoin, cudaEventDisableTiming));
     }
     *out = &ss;
     return HDP_OK;
@@ -1610,6 +1619,15 @@ static int fork_side(const SideStream* ss, cudaStream_t st) {
 static int join_side(const SideStream* ss, cudaStream_t st) {
     HDP_CHECK_CUDA(cudaEventRecord(ss->join, ss->s));
     HDP_CHECK_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+    return HDP_OK;
+}
+static int fork_hi(const SideStream* ss) {  // after fork_side: the fork event is recorded
+    HDP_CHECK_CUDA(cudaStreamWaitEvent(ss->hi, ss->fork, 0));
+    return HDP_OK;
+}
+static int join_hi(const SideStream* ss, cudaStream_t st) {
+    HDP_CHECK_CUDA(cudaEventRecord(ss->hjoin, ss->hi));
+    HDP_CHECK_CUDA(cudaStreamWaitEvent(st, ss->hjoin, 0));
     return HDP_OK;
 }
 
@@ -1850,6 +1868,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_CHECK_CUDA(cudaGetDevice(&dev));
     HDP_CHECK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     static const int chunk_share = env_int("HDP_CHUNK_SHARE", 0), seg_share = env_int("HDP_SEG_SHARE", 0);
+    static const bool seg_prio = env_int("HDP_SEG_PRIO", 1) != 0;
     static const int chunk_persist = env_int("HDP_CHUNK_PERSIST", 0);  // CTAs per SM, 0 = one chunk per CTA
     auto cgrid = [&](int64_t nc, bool both) -> unsigned {
         int64_t g = both && chunk_share > 0 ? std::min<int64_t>(nc, (int64_t)chunk_share * nsm) : nc;
@@ -1877,8 +1896,11 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
             k_light<<<grid_for(np << a.qsub_shift, 256), 256, 0, st>>>(a, p0, np); note_launch();
         }
         if (ng > 0) {
-            k_seg_up<<<dim3(sgrid(ng, side), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
+            const bool hp = side && seg_prio;
+            if (hp) HDP_TRY(fork_hi(ss));
+            k_seg_up<<<dim3(sgrid(ng, side), lg.qgroups), 32 * kSegWarps, seg_smem, hp ? ss->hi : st>>>(
                 lg, g0, ng, a.tickets + (2 * r) * a.groups, seg_sq); note_launch();
+            if (hp) HDP_TRY(join_hi(ss, st));
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (side) {
@@ -1901,8 +1923,11 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
             note_launch();
         }
         if (ng > 0) {
-            k_seg_down<<<dim3(sgrid(ng, side), lg.qgroups), 32 * kSegWarps, seg_smem, st>>>(
+            const bool hp = side && seg_prio;
+            if (hp) HDP_TRY(fork_hi(ss));
+            k_seg_down<<<dim3(sgrid(ng, side), lg.qgroups), 32 * kSegWarps, seg_smem, hp ? ss->hi : st>>>(
                 lg, g0, ng, a.tickets + (2 * r + 1) * a.groups, seg_sq); note_launch();
+            if (hp) HDP_TRY(join_hi(ss, st));
         }
         int64_t s0 = f->short_off[r], ns = f->short_off[r + 1] - s0;
         if (side) {
