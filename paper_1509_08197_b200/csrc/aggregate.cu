@@ -9,24 +9,22 @@
 //
 // Work follows the heavy-path layout of forest.cu (phases = light depth,
 // every heavy path contiguous, the rows of one path contiguous because all
-// its nodes share the tree's lane count m).  Per phase:
-//   up   : k_ecompute   b(v) = E(v), all nodes of the phase in parallel (E
-//                       recomputed from the packed image planes)
-//          k_light      b(v) += sum_{light c} s_c A_up(c) for light parents
-//          k_seg_up     A_up(v) = b(v) + s_h A_up(h) along paths > kShortPath
-//                       nodes, cut into kSeg-node segments, one warp per
-//                       (segment, 32 lanes): the segment is staged into shared
-//                       memory with cp.async, a local pass yields its carry
-//                       map (scalar product P, local value), carries are
-//                       chained tail -> head by decoupled look-back (warps take
-//                       segments by ticket, so a warp only waits on earlier
-//                       tickets), and a second pass from shared memory writes
-//                       the results
-//          k_scan_up_short  register-resident walk of paths <= kShortPath
-//   down : k_seg_down   the same for A (head -> tail), fused with the per-node
-//                       first argmin (transpose butterfly, 31 shuffles / 32 nodes)
-//          k_down_short short paths
-// A is written back in place only where a light child will read it.
+// its nodes share the tree's lane count m; rows padded to 16 bytes).
+//   E pre-pass  k_ecost_range_u / k_ecost_pix: E(v) for every node in pixel
+//               order into the node's row (right-image window staged per tile)
+//   up, per phase (deepest light depth first):
+//     k_up_chunk  short paths, CTA-staged chunks (1-D TMA): A_up = b + s A_up(next),
+//                 b = E + sum of the light children's s A_up
+//     k_seg_up    long paths in 32-node segments, one warp per (segment, 32
+//                 float4 columns); carries chained by deterministic decoupled
+//                 look-back (bit-identical to the serial chain)
+//   down, per phase (root phase first):
+//     k_down_chunk / k_seg_down  A = s A(prev) + (1 - s^2) A_up, then the
+//                 first argmin of every node folded into its (cost, d) key
+//   k_keys_finish  keys -> disparity + min cost
+// A is written back only where a light child will read it (or the volume is
+// requested).  Fallbacks for layouts without chunks: k_light, k_scan_up_short,
+// k_down_short; for cost rows given by the caller: k_ecompute.
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include <cstdio>
@@ -1504,43 +1502,6 @@ __global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const C
     }
 }
 
-// First argmin per layout position (aggregation.py:249: np.argmin, smallest
-// disparity on ties).  Rows are read in layout order (streaming); with sub
-// < 32 several short rows share a warp, otherwise one warp scans a row.
-__global__ void __launch_bounds__(256) k_wta(AggArgs a, int64_t n) {
-    Slot s = slot_of(a);
-    int lane = threadIdx.x & 31;
-    bool valid = s.item < n;
-    int4 mt = valid ? a.lmeta[s.item] : make_int4(0, 0, 0, 0);
-    int64_t row = valid ? a.rowoff[s.item] : 0;
-    uint32_t best = 0xffffffffu;
-    int bj = 0x7fffffff;
-    int width = a.sub < 32 ? a.sub : 32;
-    int step = width;
-    // sub == 32: lane j0 scans j0, j0+32, ... ; keep the first minimum
-    for (int jj = (a.sub < 32 ? s.j : lane); valid && jj < mt.w; jj += step) {
-        uint32_t o = ord_f32(a.aup[row + jj]);
-        if (o < best) {
-            best = o;
-            bj = jj;
-        }
-    }
-    uint32_t mn = best;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        uint32_t t = __shfl_xor_sync(0xffffffffu, mn, off);
-        if (off < width) mn = min(mn, t);
-    }
-    int jm = (best == mn) ? bj : 0x7fffffff;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        int t = __shfl_xor_sync(0xffffffffu, jm, off);
-        if (off < width) jm = min(jm, t);
-    }
-    if (valid && (lane & (width - 1)) == 0 && a.keys && jm != 0x7fffffff)
-        a.keys[mt.x] = ((unsigned long long)mn << 32) | (uint32_t)lane_disp(a, mt.y, jm);
-}
-
 // Pixel-major copy of the final aggregated volume (parity / API use only).
 __global__ void __launch_bounds__(256) k_volume_copy(AggArgs a, int64_t n) {
     Slot s = slot_of(a);
@@ -1556,11 +1517,6 @@ __global__ void __launch_bounds__(256) k_volume_copy(AggArgs a, int64_t n) {
 __global__ void k_fill_cols(int64_t n, int4* lmeta, int32_t npix, int32_t w) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n) lmeta[k].z = (lmeta[k].x % npix) % w;
-}
-
-__global__ void k_keys_init(int64_t n, unsigned long long* keys) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) keys[i] = ~0ull;
 }
 
 __device__ __forceinline__ float unord_f32(uint32_t u) {

@@ -212,31 +212,6 @@ __global__ void k_tour_next(int64_t na, const int32_t* __restrict__ asrc,
     next[i] = nx;
 }
 
-// Pointer jumping on packed words (pointer << 32 | count), ping-pong between
-// two buffers; the host launches an upper bound of rounds (a convergence flag
-// costs more than the rounds it saves: every block of the first waves writes it).
-// list words: (next << 32 | rank), next = -1 at a list's end
-__global__ void k_rank_init(int64_t na, const int32_t* __restrict__ next, uint64_t* word) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < na) word[i] = ((uint64_t)(uint32_t)next[i] << 32) | 1u;
-}
-
-// Wyllie pointer jumping in place (see jump_done): rank = number of arcs
-// from i to the end of its list.
-__global__ void k_rank_jump(int64_t na, const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < na) {
-        const uint64_t w = in[i];
-        const int32_t nx = (int32_t)(w >> 32);
-        if (nx >= 0) {
-            const uint64_t w2 = in[nx];
-            out[i] = (w2 & 0xffffffff00000000ull) | (uint32_t)((uint32_t)w + (uint32_t)w2);
-        } else {
-            out[i] = w;
-        }
-    }
-}
-
 // ---- ruling-set list ranking: rulers are every kRuler-th arc plus every list
 // head; each ruler walks its sublist to the next ruler (owner, offset), the
 // rulers alone are ranked by pointer jumping, and rank = ruler rank - offset.
@@ -333,11 +308,6 @@ __global__ void k_rank_final(int64_t na, const int32_t* __restrict__ owner, cons
                              const uint64_t* __restrict__ rword, int32_t* rank) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < na) rank[i] = (int32_t)((uint32_t)rword[owner[i]] - (uint32_t)local[i]);
-}
-
-__global__ void k_rank_unpack(int64_t na, const uint64_t* __restrict__ word, int32_t* rank) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < na) rank[i] = (int32_t)(uint32_t)word[i];
 }
 
 // Per tree: tour length L = rank of the root's first arc (0 for singletons).
@@ -567,24 +537,6 @@ __global__ void k_path_len(int64_t n, const int32_t* __restrict__ head,
     if (v < n) atomicMax(&plen[head[v]], dist[v] + 1);
 }
 
-// layout key (light depth, long path, head, distance from head): within a
-// phase the short paths come first, so their rows form one contiguous block
-__global__ void k_layout_keys(int64_t n, const int32_t* __restrict__ down_arc,
-                              const int32_t* __restrict__ lscan, const int32_t* __restrict__ head,
-                              const int32_t* __restrict__ dist, const int32_t* __restrict__ plen,
-                              uint64_t* key, int32_t* idx, int32_t* ld_out, int hbits, int dbits) {
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    int32_t a = down_arc[v];
-    int32_t ld = a >= 0 ? lscan[a] : 0;
-    ld_out[v] = ld;
-    int32_t h = head[v];
-    uint64_t lg = plen[h] > kShortPath ? 1ull : 0ull;
-    key[v] = ((uint64_t)ld << (1 + hbits + dbits)) | (lg << (hbits + dbits)) |
-             ((uint64_t)(uint32_t)h << dbits) | (uint64_t)dist[v];
-    idx[v] = (int32_t)v;
-}
-
 // light depth of every node (scan of the light-edge tour steps)
 __global__ void k_light_depth(int64_t n, const int32_t* __restrict__ down_arc, const int32_t* __restrict__ lscan,
                               int32_t* ld_out) {
@@ -650,24 +602,6 @@ __global__ void k_lp_fill(int64_t n, const int32_t* __restrict__ fl, const int32
                           int32_t* list) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < n && fl[k]) list[ex[k]] = (int32_t)k;
-}
-
-__global__ void k_gather_i32(int64_t m, const int32_t* __restrict__ src,
-                             const int32_t* __restrict__ idx, int32_t* out) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < m) out[i] = src[idx[i]];
-}
-
-__global__ void k_layout_pos(int64_t n, const int32_t* __restrict__ lnode,
-                             const float* __restrict__ pweight, float gamma, int32_t* lpos,
-                             float* lsim) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int32_t v = lnode[k];
-    lpos[v] = (int32_t)k;
-    // RootedForest.similarities (spanning_forest.py:184-188) in float64,
-    // rounded once to the f32 the aggregation runs in.
-    lsim[k] = (float)exp(-(double)pweight[v] / ((double)gamma * 255.0));
 }
 
 __global__ void k_path_fill(int64_t n, const int32_t* __restrict__ flag,
