@@ -1507,22 +1507,37 @@ __global__ void k_seg_desc(int64_t n, const int2* __restrict__ seg_tab, const in
 }
 
 // uniform_m > 0: every tree has exactly that many lanes (totals known here)
+namespace hdp {
+__global__ void k_uniform_offsets(int64_t n, int m, int mp, int64_t* rowoff, int64_t* nodeoff) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    rowoff[i] = i * mp;
+    nodeoff[i] = i * m;
+}
+}  // namespace hdp
+
 static int lanes_finish(hdp_forest* f, int uniform_m) {
     cudaStream_t st = f->st;
     Tracer tr(st);
     const int B = 256;
     const int64_t n = f->n;
-    DevBuf<int64_t> rm, nm;
-    HDP_TRY(rm.alloc(n + 1, st));
-    HDP_TRY(nm.alloc(n + 1, st));
     HDP_TRY(f->rowoff.alloc(n + 1, st));
     HDP_TRY(f->nodeoff.alloc(n + 1, st));
-    k_row_m<<<grid_for(n + 1, B), B, 0, st>>>(n, f->lnode.get(), f->tree_id.get(), f->t_m.get(),
-                                              rm.get()); note_launch();
-    HDP_TRY(exclusive_sum(rm.get(), f->rowoff.get(), n + 1, st));
-    HDP_CHECK_CUDA(cudaMemsetAsync(nm.get() + n, 0, sizeof(int64_t), st));
-    k_node_m<<<grid_for(n, B), B, 0, st>>>(n, f->tree_id.get(), f->t_m.get(), nm.get()); note_launch();
-    HDP_TRY(exclusive_sum(nm.get(), f->nodeoff.get(), n + 1, st));
+    if (uniform_m > 0) {
+        // every row is m lanes (padded to mp): the offsets are multiples
+        k_uniform_offsets<<<grid_for(n + 1, B), B, 0, st>>>(n, uniform_m, (uniform_m + 3) & ~3, f->rowoff.get(),
+                                                            f->nodeoff.get()); note_launch();
+    } else {
+        DevBuf<int64_t> rm, nm;
+        HDP_TRY(rm.alloc(n + 1, st));
+        HDP_TRY(nm.alloc(n + 1, st));
+        k_row_m<<<grid_for(n + 1, B), B, 0, st>>>(n, f->lnode.get(), f->tree_id.get(), f->t_m.get(),
+                                                  rm.get()); note_launch();
+        HDP_TRY(exclusive_sum(rm.get(), f->rowoff.get(), n + 1, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(nm.get() + n, 0, sizeof(int64_t), st));
+        k_node_m<<<grid_for(n, B), B, 0, st>>>(n, f->tree_id.get(), f->t_m.get(), nm.get()); note_launch();
+        HDP_TRY(exclusive_sum(nm.get(), f->nodeoff.get(), n + 1, st));
+    }
     HDP_CHECK_LAUNCH();
     if (uniform_m > 0) {
         f->max_m = uniform_m;
