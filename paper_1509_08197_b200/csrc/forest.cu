@@ -1421,6 +1421,15 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
 
 // chunk table of the short-path blocks (needs lmeta, lc rows and short_rows);
 // one host read (chunks per phase, largest chunk)
+namespace hdp {
+__global__ void k_uniform_offsets(int64_t n, int m, int mp, int64_t* rowoff, int64_t* nodeoff) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    rowoff[i] = i * mp;
+    if (nodeoff) nodeoff[i] = i * m;
+}
+}  // namespace hdp
+
 static int build_chunks(hdp_forest* f) {
     cudaStream_t st = f->st;
     const int nph = (int)f->n_phases;
@@ -1434,10 +1443,17 @@ static int build_chunks(hdp_forest* f) {
     HDP_TRY(f->lc_rowoff.alloc(n_lc + 2, st));
     k_chunk_weight<<<grid_for(ns + 1, 256), 256, 0, st>>>(ns, f->short_info.get(), f->short_rows.get(),
                                                           f->lc_start.get(), wt.get(), pm.get()); note_launch();
-    k_lc_m<<<grid_for(n_lc + 1, 256), 256, 0, st>>>(n_lc, f->lc_list.get(), f->lmeta.get(), lcm.get()); note_launch();
     HDP_TRY(exclusive_sum(wt.get(), W.get(), ns + 1, st));
     HDP_TRY(exclusive_sum(pm.get(), f->auxd.get(), ns + 1, st));
-    HDP_TRY(exclusive_sum(lcm.get(), f->lc_rowoff.get(), n_lc + 1, st));
+    if (f->range_x0 >= 0) {  // uniform rows: the light-child row offsets are multiples
+        const int mpu = (f->max_m + 3) & ~3;
+        k_uniform_offsets<<<grid_for(n_lc + 1, 256), 256, 0, st>>>(n_lc, f->max_m, mpu, f->lc_rowoff.get(), nullptr);
+        note_launch();
+    } else {
+        k_lc_m<<<grid_for(n_lc + 1, 256), 256, 0, st>>>(n_lc, f->lc_list.get(), f->lmeta.get(), lcm.get());
+        note_launch();
+        HDP_TRY(exclusive_sum(lcm.get(), f->lc_rowoff.get(), n_lc + 1, st));
+    }
     // chunk-count bound: every short path weighs at most (len + nlc + 1)(mp + 16)
     const int64_t mp = (f->max_m + 3) & ~3;
     const int64_t ncap = (((n + n_lc + ns) * (mp + 16)) >> kChunkShift) + nph + 2;
@@ -1507,15 +1523,6 @@ __global__ void k_seg_desc(int64_t n, const int2* __restrict__ seg_tab, const in
 }
 
 // uniform_m > 0: every tree has exactly that many lanes (totals known here)
-namespace hdp {
-__global__ void k_uniform_offsets(int64_t n, int m, int mp, int64_t* rowoff, int64_t* nodeoff) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > n) return;
-    rowoff[i] = i * mp;
-    nodeoff[i] = i * m;
-}
-}  // namespace hdp
-
 static int lanes_finish(hdp_forest* f, int uniform_m) {
     cudaStream_t st = f->st;
     Tracer tr(st);
