@@ -1372,7 +1372,10 @@ __global__ void __launch_bounds__(kChunkThreads, HDP_UP_CHUNK_MINB) k_up_chunk(A
 // root), one thread per (path, float4 column), A kept in shared memory and
 // stored globally only where a light child will read it; then one thread
 // per node scans its row for the first minimum (aggregation.py:249).
-__global__ void __launch_bounds__(kChunkThreads) k_down_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
+#ifndef HDP_DOWN_CHUNK_MINB
+#define HDP_DOWN_CHUNK_MINB 5
+#endif
+__global__ void __launch_bounds__(kChunkThreads, HDP_DOWN_CHUNK_MINB) k_down_chunk(AggArgs a, const ChunkDesc* __restrict__ descs,
                                                               int64_t cbase, int64_t nc) {
     extern __shared__ float4 sm4[];
     __shared__ unsigned long long bar;
