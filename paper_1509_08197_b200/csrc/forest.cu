@@ -159,6 +159,34 @@ __global__ void k_arc_sort(int64_t n, const int32_t* __restrict__ adj_start, int
     const int32_t a = adj_start[x], cnt = adj_start[x + 1] - a;
     int32_t* d = adst + a;
     float* w = aw + a;
+    if (cnt <= 4) {  // grid trees: at most 4 neighbours, sorted in registers
+        int32_t kd[4];
+        float kw[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            kd[i] = i < cnt ? d[i] : INT_MAX;
+            kw[i] = i < cnt ? w[i] : 0.0f;
+        }
+#pragma unroll
+        for (int i = 1; i < 4; i++)
+#pragma unroll
+            for (int j = i; j > 0; j--)
+                if (kd[j - 1] > kd[j]) {
+                    const int32_t td = kd[j - 1];
+                    kd[j - 1] = kd[j];
+                    kd[j] = td;
+                    const float tw = kw[j - 1];
+                    kw[j - 1] = kw[j];
+                    kw[j] = tw;
+                }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+            if (i < cnt) {
+                d[i] = kd[i];
+                w[i] = kw[i];
+            }
+        return;
+    }
     if (cnt <= 16) {
         for (int i = 1; i < cnt; i++) {
             const int32_t kd = d[i];
