@@ -222,11 +222,14 @@ int hdp_keys_unpack(const uint64_t *keys, int64_t n, int32_t *disp, float *min_c
  * sub-batches that run concurrently on their own streams (the tree build of
  * one overlaps the aggregation of another); the caller's stream waits for
  * all of them.  agg_ms (n_sub, nullable): device time of each sub-batch's
- * hdp_aggregate_wta call (synchronises the workers once at the end). */
+ * hdp_aggregate_wta call (synchronises the workers once at the end).
+ * right_ready (a cudaEvent_t, nullable): the right image is read only after
+ * this event (it is first needed after the tree build, so its host->device
+ * copy can still be running on another stream while the trees are built). */
 int hdp_dense_pipeline(const uint8_t *left, const uint8_t *right, int batch, int h, int w, int c,
                        int d_max, int x0, int nx, float alpha, float tau_c, float tau_g, float gamma,
                        int n_sub, int32_t *disp, float *min_cost, int64_t *n_trees, float *agg_ms,
-                       void *stream);
+                       void *right_ready, void *stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -57,7 +57,7 @@ SIGNATURES = {
     "hdp_forest_pair_stats": (_I, [_P, _I, _I64, _P, _P, _P]),
     "hdp_forest_destroy": (None, [_P]),
     "hdp_keys_unpack": (_I, [_P, _I64, _P, _P, _P]),
-    "hdp_dense_pipeline": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _F, _F, _F, _I, _P, _P, _P, _P, _P]),
+    "hdp_dense_pipeline": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _F, _F, _F, _I, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

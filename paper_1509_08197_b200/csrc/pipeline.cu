@@ -124,6 +124,7 @@ struct DenseJob {
     int64_t* n_trees;
     float* agg_ms;
     cudaEvent_t start;
+    cudaEvent_t right_ready;
     cudaEvent_t* done_out;
 };
 
@@ -142,7 +143,6 @@ static int dense_sub(const DenseJob& j) {
     HDP_TRY(pl.alloc(n * 4, st));
     HDP_TRY(pr.alloc(n * 4, st));
     HDP_PCALL(hdp_prepare_u8(j.left, j.nb, j.h, j.w, j.c, pl.get(), st));
-    HDP_PCALL(hdp_prepare_u8(j.right, j.nb, j.h, j.w, j.c, pr.get(), st));
     HDP_TRY(eu.alloc(m + 1, st));
     HDP_TRY(ev.alloc(m + 1, st));
     HDP_TRY(ew.alloc(m + 1, st));
@@ -155,6 +155,10 @@ static int dense_sub(const DenseJob& j) {
     hdp_forest* f = nullptr;
     HDP_PCALL(hdp_forest_create(n, m, eu.get(), ev.get(), ew.get(), in_tree.get(), comp.get(), j.gamma, &f, st));
     int rc = hdp_forest_set_lanes_range(f, j.x0, j.nx, st);
+    // the right image is needed only from here on (the tree build reads the left
+    // one): a caller may still be copying it in (right_ready)
+    if (rc == HDP_OK && j.right_ready) rc = cudaStreamWaitEvent(st, j.right_ready, 0) == cudaSuccess ? HDP_OK : HDP_ERR_CUDA;
+    if (rc == HDP_OK) rc = hdp_prepare_u8(j.right, j.nb, j.h, j.w, j.c, pr.get(), st);
     if (rc == HDP_OK) {
         if (j.agg_ms) HDP_CHECK_CUDA(cudaEventRecord(ss->a0, st));
         rc = hdp_aggregate_wta(f, pl.get(), pr.get(), j.h, j.w, j.c, j.alpha, j.tau_c, j.tau_g, nullptr, j.disp,
@@ -180,7 +184,7 @@ using namespace hdp;
 extern "C" int hdp_dense_pipeline(const uint8_t* left, const uint8_t* right, int batch, int h, int w, int c,
                                   int d_max, int x0, int nx, float alpha, float tau_c, float tau_g, float gamma,
                                   int n_sub, int32_t* disp, float* min_cost, int64_t* n_trees, float* agg_ms,
-                                  void* stream) {
+                                  void* right_ready, void* stream) {
     HDP_REQUIRE(batch >= 1 && h >= 1 && w >= 1 && (c == 1 || c == 3), HDP_ERR_CONFIG, "bad batch geometry");
     HDP_REQUIRE(d_max >= 1, HDP_ERR_CONFIG, "d_max must be >= 1, got %d", d_max);
     HDP_REQUIRE(x0 >= 0 && nx >= 1 && x0 + nx <= d_max + 1, HDP_ERR_CONFIG, "bad lane range [%d, %d)", x0, x0 + nx);
@@ -222,6 +226,7 @@ extern "C" int hdp_dense_pipeline(const uint8_t* left, const uint8_t* right, int
         j.n_trees = n_trees ? n_trees + b0 : nullptr;
         j.agg_ms = agg_ms ? agg_ms + i : nullptr;
         j.start = start;
+        j.right_ready = (cudaEvent_t)right_ready;
         j.done_out = &done[i];
         fns.emplace_back([&, i, dev] {
             if (cudaSetDevice(dev) != cudaSuccess) {

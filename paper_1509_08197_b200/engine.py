@@ -444,7 +444,7 @@ DENSE_SUB_BATCHES = int(os.environ.get("HDP_DENSE_SUB", "1"))
 
 def run_baseline_fused(left_u8, right_u8, d_max: int, gamma: float = 0.1,
                        cost: CostConsts = CostConsts(), x0: int = 0, nx: int | None = None,
-                       n_sub: int | None = None, agg_ms=None) -> LevelOut:
+                       n_sub: int | None = None, agg_ms=None, right_ready=None) -> LevelOut:
     """run_baseline_batch for plain MST trees in ONE library call
     (hdp_dense_pipeline): the batch runs as concurrent sub-batches on their own
     streams.  agg_ms: optional list that receives each sub-batch's aggregation
@@ -463,7 +463,8 @@ def run_baseline_fused(left_u8, right_u8, d_max: int, gamma: float = 0.1,
     ams = np.zeros(n_sub, np.float32) if agg_ms is not None else None
     L.call("hdp_dense_pipeline", L.ptr(left_u8.contiguous()), L.ptr(right_u8.contiguous()), b, h, w, c,
            d_max, x0, nx, cost.alpha, cost.tau_color, cost.tau_grad, gamma, n_sub, L.ptr(disp), L.ptr(mc),
-           ntrees.ctypes.data, ams.ctypes.data if ams is not None else None, L.stream())
+           ntrees.ctypes.data, ams.ctypes.data if ams is not None else None,
+           right_ready.cuda_event if right_ready is not None else None, L.stream())
     if agg_ms is not None:
         agg_ms.extend(float(x) for x in ams)
     stored = np.full(b, h * w * nx, np.int64)
@@ -585,6 +586,17 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     return outs
 
 
+_SIDE: dict = {}
+
+
+def _side_stream():
+    torch = _t()
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream(device=dev)
+    return _SIDE[dev]
+
+
 def _tree_masks_host(fo: DeviceForest, tmasks):
     """Per-tree masks (trees numbered by root id) on the host (keep=True)."""
     torch = _t()
@@ -605,8 +617,20 @@ def run_baseline_host(left_u8: np.ndarray, right_u8: np.ndarray, d_max: int, out
     lt = torch.from_numpy(left_u8) if isinstance(left_u8, np.ndarray) else left_u8
     rt = torch.from_numpy(right_u8) if isinstance(right_u8, np.ndarray) else right_u8
     ld = lt.to(dev, non_blocking=True)
-    rd = rt.to(dev, non_blocking=True)
-    res = run_baseline_batch(ld, rd, d_max, **kw)
+    if not kw and DENSE_SUB_BATCHES > 0:
+        # the right image is first read after the tree build: copy it on a side
+        # stream while the left one's trees are built
+        side = _side_stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            rd = rt.to(dev, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(side)
+        rd.record_stream(torch.cuda.current_stream())
+        res = run_baseline_fused(ld, rd, d_max, right_ready=ready)
+    else:
+        rd = rt.to(dev, non_blocking=True)
+        res = run_baseline_batch(ld, rd, d_max, **kw)
     if out is None:
         return res.disparity.cpu().numpy(), res.min_cost.cpu().numpy()
     od, oc = (torch.from_numpy(o) if isinstance(o, np.ndarray) else o for o in out)
