@@ -562,7 +562,11 @@ __global__ void k_light_steps(int64_t na, const int32_t* __restrict__ asrc,
 __global__ void k_path_len(int64_t n, const int32_t* __restrict__ head,
                            const int32_t* __restrict__ dist, int32_t* plen) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < n) atomicMax(&plen[head[v]], dist[v] + 1);
+    // one atomic per (warp, path): neighbouring ids often share a heavy path
+    const int32_t h = v < n ? head[v] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, h);
+    const int32_t l = __reduce_max_sync(peers, v < n ? dist[v] + 1 : 0);
+    if (v < n && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMax(&plen[h], l);
 }
 
 // light depth of every node (scan of the light-edge tour steps)
@@ -1417,9 +1421,10 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
                              const int64_t* __restrict__ auxd, const int64_t* __restrict__ W,
                              ChunkDesc* desc, unsigned long long* max_words) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= cbase[nph]) return;
+    const bool live = c < cbase[nph];
+    unsigned long long words = 0;
     ChunkDesc d = {};
-    int p0 = chunk_first[c], p1 = chunk_first[c + 1];
+    int p0 = live ? chunk_first[c] : 0, p1 = live ? chunk_first[c + 1] : 0;
     d.p0 = p0;
     d.np = p1 - p0;
     if (p1 > p0) {
@@ -1440,9 +1445,12 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
             if (((sinfo[p].z + 3) >> 2) != mq) mq = 0;
         d.mqu = mq;
         d.inv = mq > 1 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
-        atomicMax(max_words, (unsigned long long)(W[p1] - W[p0]));
+        words = (unsigned long long)(W[p1] - W[p0]);
     }
-    desc[c] = d;
+    if (live) desc[c] = d;
+    // one atomic per warp (a same-address atomic per chunk serialised in L2)
+    words = __reduce_max_sync(0xffffffffu, (unsigned)words);
+    if ((threadIdx.x & 31) == 0 && words) atomicMax(max_words, words);
 }
 
 }  // namespace hdp
