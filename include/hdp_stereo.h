@@ -119,11 +119,12 @@ int hdp_mst_grid(int batch, int h, int w, const int32_t *eu, const int32_t *ev, 
 /* estimate_prior up to the histogram (hdp_model.py:425-470): sampled
  * windowed WTA in both directions, float64 bit-exact with the reference,
  * cross-check |dL - dR| <= max_offset.  counts (B, d_max+1) int64;
- * kept (B) int64 = number of surviving samples. */
+ * kept (B) int64 = number of surviving samples.  max_ctas > 0 caps the grid
+ * (the kernel strides over the centres), leaving SM slots to other streams. */
 int hdp_prior_counts(const double *unit_l, const double *grad_l, const double *unit_r,
                      const double *grad_r, int batch, int h, int w, int c, int d_max,
                      int stride, int window, int max_offset, double alpha, double tau_c,
-                     double tau_g, int64_t *counts, int64_t *kept, void *stream);
+                     double tau_g, int64_t *counts, int64_t *kept, int max_ctas, void *stream);
 
 /* predict_intervals (hdp_model.py:498-525) for nrows rows of Bayes matrices
  * (rows x ncols f64, ncols <= 256): stable descending order, sequential

@@ -176,10 +176,7 @@ __device__ int warp_wta7(const PriorArgs& a, const double* su, const double* sg,
 }
 
 template <bool W7>
-__global__ void __launch_bounds__(256) k_prior(PriorArgs a, int batch) {
-    int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int64_t per = (int64_t)a.nrc * a.ncc;
-    if (wid >= per * batch) return;
+__device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, int64_t wid) {
     int b = (int)(wid / per);
     int k = (int)(wid % per);
     int i = k / a.ncc, j = k % a.ncc;
@@ -201,6 +198,14 @@ __global__ void __launch_bounds__(256) k_prior(PriorArgs a, int batch) {
     }
 }
 
+template <bool W7>
+__global__ void __launch_bounds__(256) k_prior(PriorArgs a, int batch) {
+    const int64_t per = (int64_t)a.nrc * a.ncc;
+    const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+    // grid-stride over sample centres (a capped grid leaves SMs to other streams)
+    for (int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wid < per * batch; wid += nwarp)
+        prior_centre<W7>(a, per, wid);
+}
 __global__ void k_assign_rows(const int32_t* __restrict__ pd, int batch, int ph, int pw, int h,
                               int w, int s, int n_rows, int32_t* __restrict__ rows, int* bad) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -298,7 +303,7 @@ extern "C" int hdp_predict_masks(const double* bayes, int64_t nrows, int ncols, 
 extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, const double* unit_r,
                                 const double* grad_r, int batch, int h, int w, int c, int d_max,
                                 int stride, int window, int max_offset, double alpha, double tau_c,
-                                double tau_g, int64_t* counts, int64_t* kept, void* stream) {
+                                double tau_g, int64_t* counts, int64_t* kept, int max_ctas, void* stream) {
     HDP_REQUIRE(stride >= 1 && window >= 1 && window % 2 == 1, HDP_ERR_CONFIG,
                 "sample_stride must be >= 1 and window odd and positive");
     HDP_REQUIRE(window * window <= 129, HDP_ERR_CONFIG, "window larger than 11 not supported");
@@ -320,10 +325,12 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
     a.kept = (unsigned long long*)kept;
     int64_t warps = (int64_t)a.nrc * a.ncc * batch;
     if (warps == 0) return HDP_OK;
+    unsigned grid = (unsigned)grid_for(warps * 32, 256);
+    if (max_ctas > 0 && (unsigned)max_ctas < grid) grid = (unsigned)max_ctas;
     if (window == 7)
-        k_prior<true><<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch);
+        k_prior<true><<<grid, 256, 0, st>>>(a, batch);
     else
-        k_prior<false><<<grid_for(warps * 32, 256), 256, 0, st>>>(a, batch);
+        k_prior<false><<<grid, 256, 0, st>>>(a, batch);
     note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;

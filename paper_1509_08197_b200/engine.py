@@ -323,7 +323,12 @@ def pack_masks(chosen) -> np.ndarray:
     return (bits * weights).sum(axis=-1).astype(np.uint32)
 
 
-def prior_counts(lev: Level, stride=5, window=7, max_offset=1, cost: CostConsts = CostConsts()):
+# CTAs of the early (side-stream) prior launches; 0 = one warp per centre, uncapped
+PRIOR_SIDE_CTAS = int(os.environ.get("HDP_PRIOR_SIDE_CTAS", "0"))
+
+
+def prior_counts(lev: Level, stride=5, window=7, max_offset=1, cost: CostConsts = CostConsts(),
+                 max_ctas: int = 0):
     torch = _t()
     b = lev.img_l.shape[0]
     dev = lev.img_l.device
@@ -331,7 +336,7 @@ def prior_counts(lev: Level, stride=5, window=7, max_offset=1, cost: CostConsts 
     kept = torch.empty(b, dtype=torch.int64, device=dev)
     L.call("hdp_prior_counts", L.ptr(lev.unit_l), L.ptr(lev.grad_l), L.ptr(lev.unit_r),
            L.ptr(lev.grad_r), b, lev.h, lev.w, lev.c, lev.d_max, stride, window, max_offset,
-           cost.alpha, cost.tau_color, cost.tau_grad, L.ptr(counts), L.ptr(kept), L.stream())
+           cost.alpha, cost.tau_color, cost.tau_grad, L.ptr(counts), L.ptr(kept), int(max_ctas), L.stream())
     return counts, kept
 
 
@@ -525,12 +530,60 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     if d_max // block_size**levels < 1:
         raise ConfigError(f"d_max={d_max} collapses to {d_max // block_size**levels} after "
                           f"{levels} levels of /{block_size}; reduce levels or block_size")
+    if not timing:
+        # The sampled priors of all levels depend only on that level's images:
+        # they run on a side stream from the start, beside the coarser levels'
+        # tree builds (HDPF keeps one SM per pair busy), while the level loop
+        # runs on a high-priority stream so the block scheduler serves it first.
+        caller = torch.cuda.current_stream()
+        pri, hi = _hdp_streams()
+        pri.wait_stream(caller)
+        hi.wait_stream(caller)
+        with torch.cuda.stream(hi):
+            outs = _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0,
+                                   beta, cost, tree_kind, seed, teacher, keep, want_volume, timing,
+                                   on_level, prior_stream=pri)
+        caller.wait_stream(hi)
+        for o in outs:
+            o.disparity.record_stream(caller)
+            o.min_cost.record_stream(caller)
+            if o.extra.get("volume") is not None:
+                o.extra["volume"].record_stream(caller)
+        return outs
+    return _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0, beta,
+                           cost, tree_kind, seed, teacher, keep, want_volume, timing, on_level)
+
+
+_HDP_STREAMS: dict = {}
+
+
+def _hdp_streams():
+    """(prior stream, high-priority level stream) per device."""
+    torch = _t()
+    dev = torch.cuda.current_device()
+    if dev not in _HDP_STREAMS:
+        _HDP_STREAMS[dev] = (torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev, priority=-1))
+    return _HDP_STREAMS[dev]
+
+
+def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0, beta, cost,
+                    tree_kind, seed, teacher, keep, want_volume, timing, on_level, prior_stream=None):
+    torch = _t()
     clock = _Clock(timing)
     t0 = time.perf_counter()
     b = left_u8.shape[0]
     lv = build_levels(left_u8, right_u8, d_max, levels, block_size, True)
     t0 = clock.lap("pyramid", t0)
     outs: list[LevelOut] = []
+    early = {}
+    if prior_stream is not None:
+        prior_stream.wait_stream(torch.cuda.current_stream())  # the levels' planes
+        with torch.cuda.stream(prior_stream):
+            for level in range(levels - 1, -1, -1):
+                c_, k_ = prior_counts(lv[level], cost=cost, max_ctas=PRIOR_SIDE_CTAS)
+                ev = torch.cuda.Event()
+                ev.record(prior_stream)
+                early[level] = (c_, k_, ev)
 
     def finish(lev, f, disp, mc, vol, stage):
         ntrees, stored, ratio = _per_pair_stats(f, b, lev.h * lev.w, lev.d_max)
@@ -557,7 +610,11 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
         lev = lv[level]
         t0 = time.perf_counter()
         lclock = _Clock(timing)
-        counts, kept = prior_counts(lev, cost=cost)
+        if level in early:
+            counts, kept, ev = early[level]
+            torch.cuda.current_stream().wait_event(ev)
+        else:
+            counts, kept = prior_counts(lev, cost=cost)
         counts_h, kept_h = counts.cpu().numpy(), kept.cpu().numpy()
         priors = priors_from_counts(counts_h, kept_h)
         cond = conditional_matrix(model.layers[level], lev.d_max, lv[level + 1].d_max, block_size)

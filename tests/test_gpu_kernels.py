@@ -137,6 +137,10 @@ def test_prior_counts_match_reference():
         oc, ok = O.prior_counts(g[tag + "_left"], g[tag + "_right"], d)
         np.testing.assert_array_equal(counts[0], oc)
         assert kept[0] == ok
+        # a capped grid (the side-stream launches) strides over the centres
+        c2, k2 = E.prior_counts(lev, max_ctas=3)
+        np.testing.assert_array_equal(c2.cpu().numpy(), counts)
+        np.testing.assert_array_equal(k2.cpu().numpy(), kept)
 
 
 def _table(sizes, flat):
