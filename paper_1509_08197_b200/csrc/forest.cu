@@ -916,27 +916,33 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(fpos.alloc(m_in + 1, st));
     int64_t m = 0;
     bool lex = false;  // edge list sorted by (eu, ev), eu < ev (diagnostic)
+    // with a component labelling given, the tree-edge count is read together
+    // with the tree count below (one host read less): buffers take the bound
+    const bool defer_m = comp_in != nullptr;
+    DevBuf<int> ecnt;  // (tree edges, unsorted flag)
+    HDP_TRY(ecnt.alloc(2, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(ecnt.get(), 0, 2 * sizeof(int), st));
     if (m_in > 0) {
-        DevBuf<int> cnt;  // (tree edges, unsorted flag)
-        HDP_TRY(cnt.alloc(2, st));
-        HDP_CHECK_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(int), st));
-        k_flag_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, in_tree, eu, ev, flags.get(), cnt.get() + 1); note_launch();
+        k_flag_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, in_tree, eu, ev, flags.get(), ecnt.get() + 1); note_launch();
         HDP_TRY(exclusive_sum(flags.get(), fpos.get(), m_in, st));
-        k_edge_count<<<1, 1, 0, st>>>(m_in, flags.get(), fpos.get(), cnt.get()); note_launch();
-        int hc[2] = {0, 0};
-        HDP_TRY(to_host(hc, cnt.get(), 2, st));
-        m = hc[0];
-        lex = hc[1] == 0;
+        k_edge_count<<<1, 1, 0, st>>>(m_in, flags.get(), fpos.get(), ecnt.get()); note_launch();
+        if (!defer_m) {
+            int hc[2] = {0, 0};
+            HDP_TRY(to_host(hc, ecnt.get(), 2, st));
+            m = hc[0];
+            lex = hc[1] == 0;
+            HDP_REQUIRE(m <= n - 1 || n == 0, HDP_ERR_DATA, "forest has %lld edges for %lld nodes (cycle)",
+                        (long long)m, (long long)n);
+        }
     }
-    HDP_REQUIRE(m <= n - 1 || n == 0, HDP_ERR_DATA, "forest has %lld edges for %lld nodes (cycle)",
-                (long long)m, (long long)n);
+    const int64_t mcap = defer_m ? m_in : m;  // rows of the compacted edge arrays
     DevBuf<int32_t> tu, tv;
     DevBuf<float> tw;
     DevBuf<uint64_t> tkey;
-    HDP_TRY(tu.alloc(m + 1, st));
-    HDP_TRY(tv.alloc(m + 1, st));
-    HDP_TRY(tw.alloc(m + 1, st));
-    HDP_TRY(tkey.alloc(m + 1, st));
+    HDP_TRY(tu.alloc(mcap + 1, st));
+    HDP_TRY(tv.alloc(mcap + 1, st));
+    HDP_TRY(tw.alloc(mcap + 1, st));
+    HDP_TRY(tkey.alloc(mcap + 1, st));
     if (m_in > 0)
         k_compact_edges<<<grid_for(m_in, B), B, 0, st>>>(m_in, flags.get(), fpos.get(), eu, ev, ew,
                                                         tu.get(), tv.get(), tw.get(), tkey.get()); note_launch();
@@ -964,21 +970,27 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(f->tree_id.alloc(n, st));
     int32_t max_tree = 1;  // nodes in the largest tree
     {
-        DevBuf<int32_t> csize, cnt;  // cnt = (trees, largest tree)
+        DevBuf<int32_t> csize, cnt;  // cnt = (trees, largest tree, tree edges)
         HDP_TRY(csize.alloc(n, st));
-        HDP_TRY(cnt.alloc(2, st));
+        HDP_TRY(cnt.alloc(3, st));
         HDP_CHECK_CUDA(cudaMemsetAsync(csize.get(), 0, n * sizeof(int32_t), st));
         HDP_CHECK_CUDA(cudaMemsetAsync(cnt.get(), 0, 2 * sizeof(int32_t), st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(cnt.get() + 2, ecnt.get(), sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
         k_fill_int<<<grid_for(n, B), B, 0, st>>>(n, minid.get(), INT_MAX); note_launch();
         k_min_root<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get(), csize.get()); note_launch();
         k_root_flags<<<grid_for(n, B), B, 0, st>>>(n, comp.get(), minid.get(), csize.get(), f->root.get(),
                                                   is_root.get(), cnt.get() + 1); note_launch();
         HDP_TRY(exclusive_sum(is_root.get(), tindex.get(), n, st));
         k_tree_count<<<1, 1, 0, st>>>(n, tindex.get(), is_root.get(), cnt.get()); note_launch();
-        int32_t hc[2] = {0, 0};
-        HDP_TRY(to_host(hc, cnt.get(), 2, st));
+        int32_t hc[3] = {0, 0, 0};
+        HDP_TRY(to_host(hc, cnt.get(), 3, st));
         f->n_trees = hc[0];
         max_tree = hc[1] > 0 ? hc[1] : 1;
+        if (defer_m) {
+            m = hc[2];
+            HDP_REQUIRE(m <= n - 1 || n == 0, HDP_ERR_DATA, "forest has %lld edges for %lld nodes (cycle)",
+                        (long long)m, (long long)n);
+        }
     }
     k_tree_ids<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), tindex.get(), f->tree_id.get()); note_launch();
     HDP_CHECK_LAUNCH();
