@@ -915,7 +915,6 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(flags.alloc(m_in + 1, st));
     HDP_TRY(fpos.alloc(m_in + 1, st));
     int64_t m = 0;
-    bool lex = false;  // edge list sorted by (eu, ev), eu < ev (diagnostic)
     // with a component labelling given, the tree-edge count is read together
     // with the tree count below (one host read less): buffers take the bound
     const bool defer_m = comp_in != nullptr;
@@ -930,7 +929,6 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
             int hc[2] = {0, 0};
             HDP_TRY(to_host(hc, ecnt.get(), 2, st));
             m = hc[0];
-            lex = hc[1] == 0;
             HDP_REQUIRE(m <= n - 1 || n == 0, HDP_ERR_DATA, "forest has %lld edges for %lld nodes (cycle)",
                         (long long)m, (long long)n);
         }
@@ -1020,7 +1018,6 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
                                                  asrc.get(), adst.get(), aw2.get()); note_launch();
         k_arc_sort<<<grid_for(n, B), B, 0, st>>>(n, adj_start.get(), adst.get(), aw2.get()); note_launch();
     }
-    (void)lex;
     tu.release();
     tv.release();
     tw.release();
