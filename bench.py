@@ -1,15 +1,21 @@
 """Benchmark of the HDP stereo hot path on B200 (contract: DESIGN.md §6).
 
-Workload (BASELINE.json configs[1] = C2): a batch of 8 synthetic pairs
-463x370 RGB, d_max 80, per GPU.  One step = the dense full-range MST pipeline
+Headline (default --config c5): BASELINE.json configs[4], the largest
+configuration and the one north_star quotes the aggregation roofline on: one
+synthetic 2880x1988 RGB pair, d_max 512, dense full-range MST pipeline
 (run_baseline_pipeline: edges -> MST -> rooting/layout -> fused cost +
-two-pass aggregation + WTA) over the batch; `value` is aggregated
-pixel-disparity hypotheses per second (Gpd/s) over all GPUs.  The 3-level
-HDP pipeline on the same batch is timed the same way and reported under
-"hdp".  Multi-GPU (torchrun): every rank owns its own 8 pairs (weak scaling,
-no data-path collective).
+two-pass aggregation + WTA).  `value` = aggregated pixel-disparity hypotheses
+per second (Gpd/s, 2.94 G hypotheses per pair).  Under torchrun (N > 1) the
+pair is split into N disparity slabs, one per rank, whose packed (cost, d)
+keys meet in one NCCL all-reduce(MIN) inside the timed step (strong scaling).
+
+Legs in the same JSON line (`legs`), each with value / e2e / roofline /
+cpu_baseline: C2 dense (8 pairs 463x370 d80), C2 HDP (3 levels, half preset),
+C4 HDP (64 pairs 1390x1110 d240, 5 levels, full preset).  Under torchrun every
+rank runs its own pairs of the batched legs (weak scaling, no collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c5|c2|c2_hdp|c4_hdp] [--legs c2,c2_hdp,c4_hdp|none]
 """
 
 from __future__ import annotations
@@ -28,37 +34,73 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-CONFIG_ID = 2
-LEVELS = 3
+# workload definitions: BASELINE.json configs, SURVEY.md §8d presets
+WORKLOADS = {
+    "c5": dict(cid=5, kind="dense", batch=1,
+               desc="C5: 1 pair 2880x1988 RGB d_max 512, dense MST full range"),
+    "c2": dict(cid=2, kind="dense", batch=8,
+               desc="C2: 8 pairs/GPU 463x370 RGB d_max 80, dense MST full range"),
+    "c2_hdp": dict(cid=2, kind="hdp", batch=8, levels=3, size_class="half",
+                   desc="C2: 8 pairs/GPU 463x370 RGB d_max 80, HDP 3 levels (half preset), MST"),
+    "c4_hdp": dict(cid=4, kind="hdp", batch=64, levels=5, size_class="full",
+                   desc="C4: 64 pairs/GPU 1390x1110 RGB d_max 240, HDP 5 levels (full preset), MST "
+                        "(the reference has no segment tree, SURVEY A24)"),
+}
+METRIC = "aggregated pixel-disparity hypotheses/s (Gpd/s) and stereo pairs/s, vs HBM roofline"
+L2_NOTE = "256 MiB buffer written between timed steps (L2 is 126 MB)"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-hdp", action="store_true")
+    ap.add_argument("--config", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--legs", default="c2,c2_hdp,c4_hdp")
+    ap.add_argument("--leg-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-pairs", type=int, default=8)
     return ap.parse_args()
 
 
-def load_model():
-    from paper_1509_08197_b200.hdp_model import GmmModel
+def host_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"os_cpu_count": os.cpu_count(), "lscpu_model": model}
 
+
+def load_model_text():
     with open(os.path.join(REPO, "tests", "golden", "default.gmm")) as fh:
-        return GmmModel.parse(fh.read())
+        return fh.read()
 
 
-def batch_for_rank(rank: int):
+def scenes_for(name: str, rank: int, batch: int | None = None):
     from paper_1509_08197_b200.synthetic import CONFIGS, make_scene
 
-    spec = CONFIGS[CONFIG_ID]
-    scenes = [make_scene(spec, rank * spec.batch + i) for i in range(spec.batch)]
-    L = np.stack([s.pair.left.data for s in scenes])
-    R = np.stack([s.pair.right.data for s in scenes])
-    return spec, L, R
+    wl = WORKLOADS[name]
+    spec = CONFIGS[wl["cid"]]
+    b = wl["batch"] if batch is None else batch
+    # C5 is one pair shared by all ranks (slabs); batched legs: own pairs per rank
+    start = 0 if wl["cid"] == 5 else rank * b
+    return spec, [make_scene(spec, start + i) for i in range(b)]
+
+
+def config_dict(name: str, world: int, batch: int):
+    wl = WORKLOADS[name]
+    d = {"workload": wl["desc"], "config_id": wl["cid"], "pairs_per_gpu": batch,
+         "pipeline": "dense" if wl["kind"] == "dense" else f"hdp levels={wl['levels']} {wl['size_class']}",
+         "l2": L2_NOTE}
+    if wl["cid"] == 5:
+        d["parallelism"] = f"disparity slabs x{world}, NCCL all-reduce(MIN) of packed keys"
+    else:
+        d["parallelism"] = f"pairs sharded, {world} rank(s)"
+    return d
 
 
 class ClockSampler:
@@ -117,10 +159,11 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def agg_traffic():
-    """DRAM bytes per aggregation call from the committed ncu --set full capture
-    (profiles/r01_aggregate_traffic.json), or None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_aggregate_traffic.json")
+def committed_traffic(name: str):
+    """DRAM bytes (read + write) of one launch of the leg's dominant kernel
+    call from this round's committed ncu --set full capture
+    (profiles/r02_traffic_<leg>.json, tools/ncu_traffic.py), or None."""
+    path = os.path.join(REPO, "profiles", f"r02_traffic_{name}.json")
     try:
         with open(path) as fh:
             return float(json.load(fh)["bytes_per_call"])
@@ -132,101 +175,177 @@ def hbm_peak():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
         with open(path) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except (OSError, KeyError, ValueError):
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cpu_baseline_dense(L, R, d_max, pairs, hdp=False, model=None):
-    """The reference algorithm on host cores: the CPU oracle (C restatement
-    of treestereo, oracle/), one pair per thread (ctypes releases the GIL)."""
+# ------------------------------------------------------------ CPU reference
+def cpu_threads():
+    return max(1, os.cpu_count() or 1)
+
+
+def cpu_dense_pairs(L, R, d_max, n_pairs):
+    """The reference algorithm (oracle C port of treestereo, float64) on the
+    host cores: one pair per thread (ctypes releases the GIL)."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as O
 
     O.lib()
-    n = min(pairs, L.shape[0])
-    cores = min(n, os.cpu_count() or 1)
-
-    def one(i):
-        if hdp:
-            return O.run_hdp(L[i], R[i], d_max, model, levels=LEVELS)
-        return O.run_baseline(L[i], R[i], d_max)
-
+    n = min(n_pairs, len(L))
+    threads = min(n, cpu_threads())
     t = time.perf_counter()
-    with ThreadPoolExecutor(cores) as ex:
-        list(ex.map(one, range(n)))
-    return time.perf_counter() - t, n, cores
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda i: O.run_baseline(L[i], R[i], d_max), range(n)))
+    return time.perf_counter() - t, n, threads
+
+
+def cpu_hdp_pairs(L, R, d_max, levels, size_class, n_pairs):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+
+    O.lib()
+    model = O.parse_gmm(load_model_text())
+    n = min(n_pairs, len(L))
+    threads = min(n, cpu_threads())
+    t = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        outs = list(ex.map(lambda i: O.run_hdp(L[i], R[i], d_max, model, levels=levels,
+                                                size_class=size_class), range(n)))
+    hyps = sum(sum(o.stored_entries for o in oo) for oo in outs)
+    return time.perf_counter() - t, n, threads, hyps
+
+
+def cpu_c5_sample(L, R, d_max):
+    """Bounded sample of the C5 pair on the host: the full tree build
+    (single-threaded, as in the reference) plus ONE round of the streamed
+    aggregation -- every thread one disparity chunk of the size a full run
+    uses (oracle.chunk_plan); the full pair's time is the tree plus that round
+    times the rounds a full run needs.  Returns (t_pair, info)."""
+    from oracle import oracle as O
+
+    O.lib()
+    threads = min(cpu_threads(), 64)
+    I = np.asarray(L, np.float64)
+    h, w = I.shape[:2]
+    t0 = time.perf_counter()
+    u, v, wt = O.build_edge_list(I)
+    forest = O.build_hdpf(u, v, wt, h * w, O.full_masks(h * w, 0), 0, 0.0, O.mst_edge_order(wt))
+    t1 = time.perf_counter()
+    chunk = O.chunk_plan(h * w, d_max, threads)
+    n_chunks = -(-(d_max + 1) // chunk)
+    starts = [i * chunk for i in range(min(threads, n_chunks))]
+    O.run_baseline_chunked(L, R, d_max, chunk=chunk, threads=threads, forest=forest, starts=starts)
+    t2 = time.perf_counter()
+    rounds = -(-n_chunks // threads)
+    t_pair = (t1 - t0) + (t2 - t1) * rounds
+    return t_pair, {"threads": threads, "lanes": len(starts) * chunk, "chunk": chunk, "rounds": rounds,
+                    "tree_s": t1 - t0, "round_s": t2 - t1}
+
+
+def cpu_leg(name, Lh, Rh, spec):
+    """cpu_baseline object for a leg (rank 0, N=1)."""
+    wl = WORKLOADS[name]
+    npx = spec.height * spec.width
+    if wl["cid"] == 5:
+        t, info = cpu_c5_sample(Lh[0], Rh[0], spec.d_max)
+        return {"value": npx * (spec.d_max + 1) / t / 1e9, "unit": "Gpd/s", "cores": info["threads"],
+                "kind": "port", "pairs_per_s": 1.0 / t,
+                "sample": (f"C5 pair: full tree build ({info['tree_s']:.1f} s, 1 thread) + one round of "
+                           f"{info['threads']} disparity chunks of {info['chunk']} lanes "
+                           f"({info['round_s']:.1f} s); a full pair needs {info['rounds']} rounds: "
+                           f"{t:.1f} s per pair"), **host_info()}
+    if wl["kind"] == "dense":
+        dt, n, thr = cpu_dense_pairs(Lh, Rh, spec.d_max, len(Lh))
+        return {"value": n * npx * (spec.d_max + 1) / dt / 1e9, "unit": "Gpd/s", "cores": thr,
+                "kind": "port", "pairs_per_s": n / dt,
+                "sample": f"{n} pairs of the leg's batch, one pair per thread", **host_info()}
+    n_pairs = min(len(Lh), 16 if wl["cid"] == 4 else 8, cpu_threads())
+    dt, n, thr, hyps = cpu_hdp_pairs(Lh, Rh, spec.d_max, wl["levels"], wl["size_class"], n_pairs)
+    return {"value": hyps / dt / 1e9, "unit": "Gpd/s", "cores": thr, "kind": "port",
+            "pairs_per_s": n / dt,
+            "sample": f"{n} of the leg's {len(Lh)} pairs, one pair per thread (HDP stored entries "
+                      f"over all levels per second)", **host_info()}
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port), rank 0 only."""
+    """--impl reference: the reference's CPU path (the oracle C port; the
+    Python reference cannot travel to the GPU box) on all host cores, rank 0."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import oracle as O
-
-    spec, L, R = batch_for_rank(0)
-    hyps = L.shape[0] * spec.height * spec.width * (spec.d_max + 1)
-    times = []
+    name = args.config
+    wl = WORKLOADS[name]
+    spec, scenes = scenes_for(name, 0)
+    Lh = np.stack([s.pair.left.data for s in scenes])
+    Rh = np.stack([s.pair.right.data for s in scenes])
+    npx = spec.height * spec.width
+    times, sample = [], None
     for s in range(args.warmup + args.steps):
-        dt, n, cores = cpu_baseline_dense(L, R, spec.d_max, L.shape[0])
+        if wl["cid"] == 5:
+            t, info = cpu_c5_sample(Lh[0], Rh[0], spec.d_max)
+            hyps, cores = npx * (spec.d_max + 1), info["threads"]
+            sample = (f"per step: the C5 tree build + one round of {cores} chunks of {info['chunk']} lanes; "
+                      f"a full pair = tree + {info['rounds']} rounds (extrapolated)")
+        elif wl["kind"] == "dense":
+            t, n, cores = cpu_dense_pairs(Lh, Rh, spec.d_max, len(Lh))
+            hyps = n * npx * (spec.d_max + 1)
+            sample = f"per step: {n} pairs, one per thread"
+        else:
+            n_pairs = min(len(Lh), cpu_threads())
+            t, n, cores, hyps = cpu_hdp_pairs(Lh, Rh, spec.d_max, wl["levels"], wl["size_class"], n_pairs)
+            sample = f"per step: {n} pairs, one per thread"
         if s >= args.warmup:
-            times.append(dt)
-    t = sum(times) / len(times)
-    value = hyps / t / 1e9
-    model_layers = O.parse_gmm(open(os.path.join(REPO, "tests", "golden", "default.gmm")).read())
-    hdp_t, hn, _ = cpu_baseline_dense(L, R, spec.d_max, L.shape[0], hdp=True, model=model_layers)
+            times.append((t, hyps))
+    t = sum(x[0] for x in times) / len(times)
+    value = statistics.mean(x[1] / x[0] for x in times) / 1e9
     line = {
-        "impl": "reference", "metric": "aggregated pixel-disparity hypotheses/s (dense MST, C2)",
-        "value": value, "unit": "Gpd/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2: 8 pairs 463x370 RGB d_max 80, dense MST full range",
-                   "batch": int(L.shape[0])},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gpd/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong" if wl["cid"] == 5 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Voronoi scenes, SURVEY §8d)",
+        "config": config_dict(name, args.gpus, len(Lh)),
         "cpu_baseline": {"value": value, "unit": "Gpd/s", "cores": cores, "kind": "port",
-                         "sample": f"{L.shape[0]} C2 pairs per step, one pair per thread"},
+                         "sample": sample, **host_info()},
         "e2e": {"value": value, "unit": "Gpd/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "hdp": {"pairs_per_s": hn / hdp_t, "ms_per_step": hdp_t * 1e3},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args):
-    import torch
+# ------------------------------------------------------------------ GPU arm
+class Runner:
+    def __init__(self, args):
+        import torch
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
+        self.torch = torch
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1509_08197_b200 import _lib
-    from paper_1509_08197_b200 import engine as E
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist = dist
+        from paper_1509_08197_b200 import _lib
 
-    lib = _lib.load()
-    spec, Lh, Rh = batch_for_rank(rank)
-    B, H, W = Lh.shape[:3]
-    d_max = spec.d_max
-    N = B * H * W
-    hyps = N * (d_max + 1)
-    Ld = torch.from_numpy(Lh).cuda()
-    Rd = torch.from_numpy(Rh).cuda()
-    Lp = torch.from_numpy(Lh).pin_memory()
-    Rp = torch.from_numpy(Rh).pin_memory()
-    model = load_model()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        self.lib = _lib.load()
+        self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+        self.args = args
 
-    def timed(fn, steps, warmup):
+    def timed(self, fn, steps, warmup):
+        """Device-timed steps (CUDA events on the current stream), L2 flushed
+        and a barrier before each; returns per-step ms."""
+        torch = self.torch
         ms = []
         for s in range(warmup + steps):
-            flush.fill_(float(s))  # evict L2 (126 MB) between steps, untimed
+            self.flush.fill_(float(s))
             torch.cuda.synchronize()
-            if dist:
-                dist.barrier()
+            if self.dist:
+                self.dist.barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -237,103 +356,198 @@ def run_ours(args):
                 ms.append(e0.elapsed_time(e1))
         return ms
 
-
-    agg_ms: list = []
-
-    def dense(timed_step):
-        # one library call per step (hdp_dense_pipeline: sub-batches on their own
-        # streams); each sub-batch's aggregation call is timed with device events
-        E.run_baseline_fused(Ld, Rd, d_max, agg_ms=agg_ms if timed_step else None)
-
-    # warm-up + timed dense steps with clocks sampled during the timed region
-    with ClockSampler(local) as clk:
-        l0 = lib.hdp_launch_count()
-        dense_ms = timed(dense, args.steps, args.warmup)
-        launches = (lib.hdp_launch_count() - l0) // (args.steps + args.warmup)
-    n_sub = max(1, min(E.DENSE_SUB_BATCHES, B))
-    entries, nodes = hyps / n_sub, N / n_sub  # per aggregation call (one sub-batch)
-
-    # results land in pinned host buffers (allocated once, like the inputs)
-    Od = torch.empty((B, H, W), dtype=torch.int32).pin_memory()
-    Oc = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
-
-    def e2e(timed_step):
-        E.run_baseline_host(Lp, Rp, d_max, out=(Od, Oc))
-
-    e2e_ms = timed(e2e, args.steps, 1)
-
-    hdp = None
-    if not args.no_hdp:
-        hdp_info = {}
-
-        def hdp_step(timed_step):
-            outs = E.run_hdp_batch(Ld, Rd, d_max, model, levels=LEVELS)
-            hdp_info["hyps"] = int(sum(int(o.stored_entries.sum()) for o in outs))
-            hdp_info["ratios"] = [float(np.mean(o.search_ratio)) for o in outs]
-            hdp_info["rounds"] = [o.extra.get("dr_rounds") for o in outs]
-
-        hdp_ms = timed(hdp_step, args.steps, max(1, args.warmup))
-        hdp = {"ms_per_step": statistics.mean(hdp_ms), "hyps_per_step": hdp_info["hyps"],
-               "levels": LEVELS, "search_ratios_top_to_0": hdp_info["ratios"],
-               "hdpf_rounds_top_to_0": hdp_info["rounds"]}
-
-    def reduce_max(x):
-        if not dist:
+    def reduce_max(self, x):
+        if not self.dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
-    t_dense = reduce_max(sum(dense_ms) / 1e3)  # seconds for K steps, max over ranks
-    t_e2e = reduce_max(sum(e2e_ms) / 1e3)
-    if hdp:
-        t_hdp = reduce_max(sum(hdp_ms) / 1e3)
-        hdp["pairs_per_s"] = world * B * args.steps / t_hdp
-        hdp["gpd_per_s"] = world * hdp["hyps_per_step"] * args.steps / t_hdp / 1e9
-        hdp["ms_per_step"] = t_hdp / args.steps * 1e3
-    if rank != 0:
-        if dist:
-            dist.destroy_process_group()
+    # ---- dense legs (C5 headline, C2)
+    def dense(self, name, steps, warmup, with_cpu):
+        torch = self.torch
+        from paper_1509_08197_b200 import aggregation as A
+        from paper_1509_08197_b200 import engine as E
+        from paper_1509_08197_b200.distributed import run_slab_baseline, slab
+
+        spec, scenes = scenes_for(name, self.rank)
+        wl = WORKLOADS[name]
+        Lh = np.stack([s.pair.left.data for s in scenes])
+        Rh = np.stack([s.pair.right.data for s in scenes])
+        B, H, W = Lh.shape[:3]
+        d_max = spec.d_max
+        slabs = wl["cid"] == 5 and self.world > 1
+        x0, nx = slab(d_max, self.rank, self.world) if slabs else (0, d_max + 1)
+        Ld = torch.from_numpy(Lh).cuda()
+        Rd = torch.from_numpy(Rh).cuda()
+        agg_ms: list = []
+
+        def step(timed_step):
+            if slabs:
+                run_slab_baseline(Ld, Rd, d_max, self.rank, self.world)
+            else:
+                E.run_baseline_fused(Ld, Rd, d_max, agg_ms=agg_ms if timed_step else None)
+
+        l0 = self.lib.hdp_launch_count()
+        dev_ms = self.timed(step, steps, warmup)
+        launches = (self.lib.hdp_launch_count() - l0) // (steps + warmup)
+        # per-rank slab aggregation time (the roofline kernel) from a probe run
+        if slabs:
+            E.run_baseline_fused(Ld, Rd, d_max, x0=x0, nx=nx, agg_ms=agg_ms)
+
+        pairs = [s.pair for s in scenes]
+
+        def e2e(timed_step):
+            # the reference-signature API: StereoPair in (host numpy), PipelineResult out
+            if slabs:
+                ld, rd, ready = E.stage_pairs([p.left.data for p in pairs], [p.right.data for p in pairs])
+                torch.cuda.current_stream().wait_event(ready)
+                dd, cc = run_slab_baseline(ld, rd, d_max, self.rank, self.world)
+                dd.cpu().numpy(), cc.cpu().numpy()
+            else:
+                A.run_baseline_pipeline_batch(pairs)
+
+        e2e_ms = self.timed(e2e, steps, 1)
+        hyps = B * H * W * (d_max + 1)
+        n_lanes = nx
+        t_dev = self.reduce_max(sum(dev_ms) / 1e3)
+        t_e2e = self.reduce_max(sum(e2e_ms) / 1e3)
+        units = hyps if slabs else self.world * hyps  # slabs: one pair shared by all ranks
+        pairs_done = B if slabs else self.world * B
+        out = {
+            "value": units * steps / t_dev / 1e9, "unit": "Gpd/s",
+            "ms_per_step": t_dev / steps * 1e3, "pairs_per_s": pairs_done * steps / t_dev,
+            "scaling": "strong" if slabs else "weak",
+            "config": config_dict(name, self.world, B),
+            "e2e": {"value": units * steps / t_e2e / 1e9, "unit": "Gpd/s",
+                    "h2d_bytes_per_step": int(Lh.nbytes + Rh.nbytes),
+                    "d2h_bytes_per_step": int(B * H * W * 4 * 2),
+                    "path": "aggregation.run_baseline_pipeline_batch (StereoPair list in, "
+                            "PipelineResult list out)" if not slabs else
+                            "pinned staging + distributed.run_slab_baseline + D2H"},
+            "gpu_launches": int(launches),
+        }
+        t_agg = statistics.mean(agg_ms) / 1e3
+        entries = B * H * W * n_lanes
+        algo = 8 * entries + 30 * B * H * W  # 8 B/hypothesis + 30 B/pixel
+        peak, peak_kind = hbm_peak()
+        out["roofline"] = {
+            "bound": "hbm", "achieved": algo / t_agg / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": algo / t_agg / 1e9 / peak, "traffic": committed_traffic(name), "peak_kind": peak_kind,
+            "kernel": "hdp_aggregate_wta (fused cost + up/down passes + WTA), one call per step"
+                      + (" (this rank's slab)" if slabs else ""),
+            "kernel_ms": t_agg * 1e3, "algorithmic_bytes": algo,
+            "algorithmic_bytes_rule": "8 B per hypothesis (A-up written + read) + 30 B per pixel",
+            "share_of_step": t_agg * 1e3 / (t_dev / steps * 1e3)}
+        if with_cpu:
+            out["cpu_baseline"] = cpu_leg(name, Lh, Rh, spec)
+        return out
+
+    # ---- HDP legs
+    def hdp(self, name, steps, warmup, with_cpu):
+        torch = self.torch
+        from paper_1509_08197_b200 import aggregation as A
+        from paper_1509_08197_b200 import engine as E
+        from paper_1509_08197_b200.aggregation import SIZE_CLASS_PRESETS, AggregationParams
+        from paper_1509_08197_b200.hdp_model import GmmModel
+
+        wl = WORKLOADS[name]
+        spec, scenes = scenes_for(name, self.rank)
+        Lh = np.stack([s.pair.left.data for s in scenes])
+        Rh = np.stack([s.pair.right.data for s in scenes])
+        B = Lh.shape[0]
+        model = GmmModel.parse(load_model_text())
+        pre = SIZE_CLASS_PRESETS[wl["size_class"]]
+        Ld = torch.from_numpy(Lh).cuda()
+        Rd = torch.from_numpy(Rh).cuda()
+        info = {}
+
+        def step(timed_step):
+            outs = E.run_hdp_batch(Ld, Rd, spec.d_max, model, levels=wl["levels"], delta0=pre["delta0"],
+                                   beta=pre["beta"])
+            if "hyps" not in info:
+                info["hyps"] = int(sum(int(o.stored_entries.sum()) for o in outs))
+                info["nodes"] = int(sum(B * o.h * o.w for o in outs))
+                info["ratios"] = [float(np.mean(o.search_ratio)) for o in outs]
+                info["rounds"] = [o.extra.get("dr_rounds") for o in outs]
+
+        l0 = self.lib.hdp_launch_count()
+        dev_ms = self.timed(step, steps, warmup)
+        launches = (self.lib.hdp_launch_count() - l0) // (steps + warmup)
+        pairs = [s.pair for s in scenes]
+        params = AggregationParams(levels=wl["levels"], size_class=wl["size_class"])
+        stage = {}
+
+        def e2e(timed_step):
+            res = A.run_hdp_pipeline_batch(pairs, model, params)
+            stage.update(res[0].metrics["seconds"])
+
+        e2e_ms = self.timed(e2e, steps, 1)
+        t_dev = self.reduce_max(sum(dev_ms) / 1e3)
+        t_e2e = self.reduce_max(sum(e2e_ms) / 1e3)
+        hyps = info["hyps"]
+        algo = 8 * hyps + 30 * info["nodes"]
+        peak, peak_kind = hbm_peak()
+        npx = spec.height * spec.width
+        out = {
+            "value": self.world * hyps * steps / t_dev / 1e9, "unit": "Gpd/s",
+            "ms_per_step": t_dev / steps * 1e3, "pairs_per_s": self.world * B * steps / t_dev,
+            "dense_equivalent_gpd_s": self.world * B * npx * (spec.d_max + 1) * steps / t_dev / 1e9,
+            "scaling": "weak", "config": config_dict(name, self.world, B),
+            "hyps_per_step": hyps, "levels": wl["levels"],
+            "search_ratios_top_to_0": info["ratios"], "hdpf_rounds_top_to_0": info["rounds"],
+            "e2e": {"value": self.world * hyps * steps / t_e2e / 1e9, "unit": "Gpd/s",
+                    "pairs_per_s": self.world * B * steps / t_e2e,
+                    "h2d_bytes_per_step": int(Lh.nbytes + Rh.nbytes),
+                    "d2h_bytes_per_step": int(8 * info["nodes"]),  # int32 d + f32 cost, every level
+                    "path": "aggregation.run_hdp_pipeline_batch (StereoPair list in, PipelineResult "
+                            "list out, every level's maps)",
+                    "stage_seconds_pair0": stage},
+            "roofline": {"bound": "hbm", "achieved": algo / (t_dev / steps) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": algo / (t_dev / steps) / 1e9 / peak,
+                         "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "whole HDP step (every level: prior, HDPF, tree build, aggregation); "
+                                   "latency-bound, not bandwidth-bound",
+                         "algorithmic_bytes": algo,
+                         "algorithmic_bytes_rule": "sum over levels of 8 B x stored entries + 30 B x pixels"},
+            "gpu_launches": int(launches),
+        }
+        if with_cpu:
+            out["cpu_baseline"] = cpu_leg(name, Lh, Rh, spec)
+        return out
+
+    def leg(self, name, steps, warmup, with_cpu):
+        if WORKLOADS[name]["kind"] == "dense":
+            return self.dense(name, steps, warmup, with_cpu)
+        return self.hdp(name, steps, warmup, with_cpu)
+
+
+def run_ours(args):
+    r = Runner(args)
+    with_cpu = r.world == 1 and not args.no_cpu_baseline
+    with ClockSampler(r.local) as clk:
+        head = r.leg(args.config, args.steps, args.warmup, with_cpu and r.rank == 0)
+    clocks = clk.summary()
+    legs = {}
+    names = [x for x in args.legs.split(",") if x and x != "none" and x != args.config]
+    for name in names:
+        legs[name] = r.leg(name, args.leg_steps, max(3, min(args.warmup, 3)), with_cpu and r.rank == 0)
+    if r.rank != 0:
+        if r.dist:
+            r.dist.destroy_process_group()
         return
-    value = world * hyps * args.steps / t_dense / 1e9
-    peak, peak_kind = hbm_peak()
-    t_agg = statistics.mean(agg_ms) / 1e3
-    algo_bytes = 8 * entries + 30 * nodes  # 8 B/hypothesis + 30 B/pixel
-    achieved = algo_bytes / t_agg / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": agg_traffic(), "peak_kind": peak_kind,
-            "kernel": ("hdp_aggregate_wta (fused cost + up/down passes + WTA), one call per step"
-                       if n_sub == 1 else
-                       f"hdp_aggregate_wta (fused cost + up/down passes + WTA), one call per sub-batch of "
-                       f"{B // n_sub} pairs, timed while the other sub-batches run beside it"),
-            "kernel_ms": t_agg * 1e3, "algorithmic_bytes": algo_bytes}
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        dt, n, cores = cpu_baseline_dense(Lh, Rh, d_max, args.cpu_pairs)
-        cpu = {"value": n * H * W * (d_max + 1) / dt / 1e9, "unit": "Gpd/s", "cores": cores,
-               "kind": "port", "sample": f"{n} C2 pairs (dense MST), one pair per thread"}
     line = {
-        "metric": "aggregated pixel-disparity hypotheses/s (dense MST, C2)",
-        "value": value, "unit": "Gpd/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_dense / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded Voronoi scenes, SURVEY §8d)",
-        "config": {"workload": "C2: 8 pairs/GPU 463x370 RGB d_max 80, dense MST full range",
-                   "batch_per_gpu": B, "pairs_per_s": world * B * args.steps / t_dense,
-                   "l2": "256 MiB buffer written between timed steps",
-                   "parallelism": f"pairs sharded, {world} rank(s)"},
-        "e2e": {"value": world * hyps * args.steps / t_e2e / 1e9, "unit": "Gpd/s",
-                "h2d_bytes_per_step": int(Lh.nbytes + Rh.nbytes),
-                "d2h_bytes_per_step": int(N * 4 * 2)},
-        "roofline": roof,
-        "cpu_baseline": cpu,
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
-        "hdp": hdp,
+        "metric": METRIC, "value": head["value"], "unit": "Gpd/s", "n_gpus": r.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+        "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Voronoi scenes of BASELINE.json's configs, SURVEY §8d)",
+        "config": head["config"], "pairs_per_s": head["pairs_per_s"],
+        "e2e": head["e2e"], "roofline": head["roofline"], "cpu_baseline": head.get("cpu_baseline"),
+        "gpu_launches": head["gpu_launches"], "clocks": clocks, "legs": legs,
     }
     print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    if r.dist:
+        r.dist.destroy_process_group()
 
 
 def main():

@@ -202,6 +202,13 @@ int hdp_aggregate_wta(hdp_forest *f, const float *packed_l, const float *packed_
                       int32_t *disp, float *min_cost, uint64_t *keys, float *volume,
                       void *stream);
 
+/* Stage timing of hdp_aggregate_wta (PipelineResult.metrics["seconds"],
+ * aggregation.py:401-416): when on, every call records device events at
+ * entry, after the raw matching-cost pass and at exit; stage_ms waits for the
+ * last call and returns its cost and aggregation (+ WTA) times in ms. */
+int hdp_forest_set_timing(hdp_forest *f, int on);
+int hdp_forest_stage_ms(const hdp_forest *f, float *cost_ms, float *aggregate_ms);
+
 /* Per pair of a batch (nodes_per_pair consecutive node ids each): tree count
  * (LayerResult.n_trees) and stored entries (LayerResult.stored_entries,
  * aggregation.py:418-426); host output arrays of length batch. */
@@ -210,9 +217,16 @@ int hdp_forest_pair_stats(const hdp_forest *f, int batch, int64_t nodes_per_pair
 
 void hdp_forest_destroy(hdp_forest *f);
 
-/* keys -> (disp, min_cost) for keys combined across slabs (NCCL min). */
-int hdp_keys_unpack(const uint64_t *keys, int64_t n, int32_t *disp, float *min_cost,
-                    void *stream);
+/* Disparity-slab keys (the C5 split): u64 = order-preserving
+ * f32 cost << 32 | d, so the u64 minimum over slabs is the reference's first
+ * argmin over the full range (strict '<' chunk fold, aggregation.py:320-326).
+ * signed_order != 0 flips the top bit: int64 order == u64 order, for NCCL's
+ * signed int64 MIN reduction.  pack: (disp, min_cost) -> keys; unpack: the
+ * inverse, for keys combined across slabs. */
+int hdp_keys_pack(const int32_t *disp, const float *min_cost, int64_t n, int signed_order,
+                  uint64_t *keys, void *stream);
+int hdp_keys_unpack(const uint64_t *keys, int64_t n, int signed_order, int32_t *disp,
+                    float *min_cost, void *stream);
 
 /* --------------------------------------------------------- whole pipeline */
 /* run_baseline_pipeline (aggregation.py:263-358) for a batch of pairs in one

@@ -420,12 +420,12 @@ class LevelOut:
     counts: np.ndarray | None = None
 
 
-def _layer_wta(left_I, right_I, d_max, forest: DForest, gamma, want_volume=False):
+def _layer_wta(left_I, right_I, d_max, forest: DForest, gamma, want_volume=False, prepared=None):
     """masked_cost_volume + aggregate_tree + WTA (cost_volume.py:183-236,
     aggregation.py:182-256), evaluated tree by tree on each tree's interval.
     Returns (disparity, best, second[, entries, ent_off])."""
     h, w = left_I.shape[:2]
-    L, R = prepare_layer(left_I), prepare_layer(right_I)
+    L, R = prepared if prepared is not None else (prepare_layer(left_I), prepare_layer(right_I))
     c = L.unit.shape[2]
     n = h * w
     base = forest.base
@@ -466,6 +466,82 @@ def run_baseline(left_u8, right_u8, d_max, gamma=0.1, tree_kind="mst", seed=0) -
     forest = build_hdpf(u, v, wt, h * w, full_masks(h * w, d_max), d_max, 0.0, order)
     d, c, c2 = _layer_wta(I_l, I_r, d_max, forest, gamma)
     return LevelOut(0, d, c, c2, 1.0, forest.n_trees, h * w * (d_max + 1), forest)
+
+
+def merge_best(a, b):
+    """Fold two (disparity, best, second) partial WTA results over disjoint
+    disparity chunks, `a` holding the smaller disparities: strict `<` keeps
+    `a` on exact ties (the global first argmin, aggregation.py:320-326);
+    `second` stays the second-smallest aggregated cost over both chunks."""
+    da, ba, sa = a
+    db, bb, sb = b
+    take_b = bb < ba
+    d = np.where(take_b, db, da)
+    best = np.where(take_b, bb, ba)
+    second = np.where(take_b, np.minimum(ba, sb), np.minimum(sa, bb))
+    return d, best, second
+
+
+def _mem_budget(default=24 << 30) -> int:
+    """Host bytes the chunked oracle may hold at once: 24 GiB or 40 % of the
+    available memory, whichever is smaller."""
+    try:
+        with open("/proc/meminfo") as fh:
+            for ln in fh:
+                if ln.startswith("MemAvailable:"):
+                    return int(min(default, 0.4 * int(ln.split()[1]) * 1024))
+    except OSError:
+        pass
+    return default
+
+
+def chunk_plan(n: int, d_max: int, threads: int, mem_budget: int | None = None):
+    """Disparity chunk size of the streamed oracle: as many lanes per thread
+    as the memory budget allows (up + down float64 passes, 16 B per lane and
+    pixel), like the reference's STREAM_ENTRY_BUDGET streaming."""
+    mem_budget = _mem_budget() if mem_budget is None else mem_budget
+    return int(max(1, min(d_max + 1, mem_budget // max(1, threads * 16 * n))))
+
+
+def run_baseline_chunked(left_u8, right_u8, d_max, gamma=0.1, chunk=None, threads=None,
+                         forest=None, starts=None) -> LevelOut:
+    """run_baseline for pairs whose full float64 volume does not fit in host
+    memory (C5: 5.7 M px x 513 lanes): the reference's own disparity
+    streaming (aggregation.py:311-326), chunks on a thread pool (the C
+    routine releases the GIL), partial results folded by merge_best.  The
+    tree is built once and both layers prepared once, as the reference does.
+    `starts` restricts the run to the chunks beginning at those disparities
+    (a timing sample)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from dataclasses import replace
+
+    I_l = np.asarray(left_u8, np.float64)
+    I_r = np.asarray(right_u8, np.float64)
+    h, w = I_l.shape[:2]
+    n = h * w
+    if forest is None:
+        u, v, wt = build_edge_list(I_l)
+        forest = build_hdpf(u, v, wt, n, full_masks(n, 0), 0, 0.0, mst_edge_order(wt))
+    threads = threads or min(os.cpu_count() or 1, 64)
+    chunk = chunk or chunk_plan(n, d_max, threads)
+    if starts is None:
+        starts = list(range(0, d_max + 1, chunk))
+    prepared = (prepare_layer(I_l), prepare_layer(I_r))
+
+    def one(x0):
+        xs = np.arange(x0, min(x0 + chunk, d_max + 1), dtype=np.int64)
+        f = replace(forest, intervals=[xs] * forest.n_trees, d_max=d_max)
+        d, c, c2 = _layer_wta(I_l, I_r, d_max, f, gamma, prepared=prepared)
+        return d.ravel(), c.ravel(), c2.ravel()
+
+    with ThreadPoolExecutor(threads) as ex:
+        parts = list(ex.map(one, starts))
+    acc = parts[0]
+    for p in parts[1:]:
+        acc = merge_best(acc, p)
+    d, c, c2 = acc
+    return LevelOut(0, d.reshape(h, w).astype(np.int32), c.reshape(h, w), c2.reshape(h, w), 1.0,
+                    forest.n_trees, n * (d_max + 1), forest)
 
 
 def assign_rows(parent_disp: np.ndarray, ch: int, cw: int, s: int) -> np.ndarray:

@@ -183,7 +183,10 @@ def winner_takes_all(volume: SparseCostVolume) -> DisparityMap:
 
 
 # ------------------------------------------------------------ pipelines
-def _stack_pairs(pairs: list[StereoPair], median_prefilter: bool):
+def _stack_pairs(pairs: list[StereoPair], median_prefilter: bool, defer_right: bool = False):
+    """Host pairs -> device (B,H,W,C) uint8 batches through pinned staging
+    (engine.stage_pairs).  With defer_right the right eye's copy may still be
+    in flight: the returned event must be waited on before it is read."""
     if not pairs:
         raise DataError("empty batch")
     shape, d = pairs[0].left.data.shape, pairs[0].d_max
@@ -191,17 +194,17 @@ def _stack_pairs(pairs: list[StereoPair], median_prefilter: bool):
         if p.left.data.shape != shape or p.d_max != d:
             raise DataError("batched pairs must share geometry and d_max")
     torch = E._t()
-    dev = L.device()
-    Lh = np.stack([p.left.data for p in pairs])
-    Rh = np.stack([p.right.data for p in pairs])
-    Ld, Rd = torch.from_numpy(Lh).to(dev), torch.from_numpy(Rh).to(dev)
+    Ld, Rd, ready = E.stage_pairs([p.left.data for p in pairs], [p.right.data for p in pairs])
+    if median_prefilter or not defer_right:
+        torch.cuda.current_stream().wait_event(ready)
+        ready = None
     if median_prefilter:
-        b, h, w, c = Lh.shape
+        b, h, w, c = Ld.shape
         Lm, Rm = torch.empty_like(Ld), torch.empty_like(Rd)
         L.call("hdp_median3x3", L.ptr(Ld), L.ptr(Lm), b, h, w, c, L.stream())
         L.call("hdp_median3x3", L.ptr(Rd), L.ptr(Rm), b, h, w, c, L.stream())
         Ld, Rd = Lm, Rm
-    return Ld, Rd, d
+    return Ld, Rd, d, ready
 
 
 def _dmap(a: np.ndarray) -> DisparityMap:
@@ -218,10 +221,17 @@ def run_baseline_pipeline_batch(pairs: list[StereoPair], params: AggregationPara
     if tree_kind not in ("mst", "rt"):
         raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
     t_start = time.perf_counter()
-    Ld, Rd, d_max = _stack_pairs(pairs, median_prefilter)
-    out = E.run_baseline_batch(Ld, Rd, d_max, params.gamma, cost_params.consts(), tree_kind,
-                               params.seed, keep_forest=on_forest is not None, timing=True)
-    total = time.perf_counter() - t_start
+    fused = tree_kind == "mst" and on_forest is None
+    Ld, Rd, d_max, ready = _stack_pairs(pairs, median_prefilter, defer_right=fused)
+    # stage times come from device events (no synchronisation between stages);
+    # plain MST batches take the one-call dense pipeline, which reads the right
+    # eye only after the tree build (its copy overlaps the build)
+    if fused:
+        out = E.run_baseline_fused(Ld, Rd, d_max, params.gamma, cost_params.consts(),
+                                   right_ready=ready, timing=True)
+    else:
+        out = E.run_baseline_batch(Ld, Rd, d_max, params.gamma, cost_params.consts(), tree_kind,
+                                   params.seed, keep_forest=on_forest is not None, timing=True)
     disp = out.disparity.cpu().numpy()
     cost = out.min_cost.cpu().numpy().astype(np.float64)
     b, h, w = disp.shape
@@ -268,7 +278,7 @@ def run_hdp_pipeline_batch(pairs: list[StereoPair], model: GmmModel,
         raise DataError(f"model covers {model.n_layers} level transitions, run needs "
                         f"{params.levels}")
     t_start = time.perf_counter()
-    Ld, Rd, d_max = _stack_pairs(pairs, median_prefilter)
+    Ld, Rd, d_max, _ = _stack_pairs(pairs, median_prefilter)
     if on_forest is not None and len(pairs) != 1:
         raise ConfigError("on_forest is supported for single-pair calls")
 
@@ -285,25 +295,27 @@ def run_hdp_pipeline_batch(pairs: list[StereoPair], model: GmmModel,
             words = o.extra["tree_masks"]
         on_forest(o.level, disparity_forest_from_device(o.forest, words, o.d_max))
 
+    # the prior side stream and the level stream keep overlapping; stage times
+    # are device events resolved after the run (aggregation.py:401-416 keys)
     outs = E.run_hdp_batch(Ld, Rd, d_max, model, params.levels, params.block_size, params.gamma,
                            params.delta0, params.beta, cost_params.consts(), tree_kind,
                            params.seed, keep=on_forest is not None, timing=True, on_level=hook)
-    total = time.perf_counter() - t_start
     b = len(pairs)
     disps = [o.disparity.cpu().numpy() for o in outs]
     costs = [o.min_cost.cpu().numpy().astype(np.float64) for o in outs]
+    total = time.perf_counter() - t_start
     stage = {"pyramid": 0.0, "predict": 0.0, "forest": 0.0, "cost": 0.0, "aggregate": 0.0}
     for o in outs:
-        stage["predict"] += o.timings.get("predict", 0.0)
-        stage["forest"] += o.timings.get("forest", 0.0)
-        stage["aggregate"] += o.timings.get("cost_aggregate", 0.0)
+        for k in stage:
+            stage[k] += o.timings.get(k, 0.0)
     stage["total"] = total
     h0, w0 = outs[-1].h, outs[-1].w
     res = []
     for i in range(b):
         layers = [LayerResult(o.level, _dmap(disps[k][i]), costs[k][i], float(o.search_ratio[i]),
                               int(o.n_trees[i]), int(o.stored_entries[i]),
-                              {"cost": 0.0, "aggregate": o.timings.get("cost_aggregate", 0.0)})
+                              {"cost": o.timings.get("cost", 0.0),
+                               "aggregate": o.timings.get("aggregate", 0.0)})
                   for k, o in enumerate(outs)]
         by_level = sorted(layers, key=lambda lr: lr.level)
         metrics = {"method": f"hdp-{tree_kind}", "tree": tree_kind, "hdp": True,

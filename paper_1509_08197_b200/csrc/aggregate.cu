@@ -1673,6 +1673,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
                 "need either cost rows or image planes");
     HDP_REQUIRE(cost_rows || (int64_t)h * w < ((int64_t)1 << 31), HDP_ERR_CONFIG, "image too large");
     cudaStream_t st = (cudaStream_t)stream;
+    if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[0], st));
     AggArgs a;
     a.lmeta = f->lmeta.get();
     a.lsimf = f->lsimf.get();
@@ -1805,6 +1806,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         }
         note_launch();
     }
+    if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[1], st));
     PhaseClock pc(st);
     pc.mark("ecost", 0, 0);
     const bool chunks = f->chunks_ok != 0;
@@ -1907,6 +1909,27 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     }
     pc.mark("finish", 0, 0);
     pc.report();
+    if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[2], st));
     HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+extern "C" int hdp_forest_set_timing(hdp_forest* f, int on) {
+    HDP_REQUIRE(f != nullptr, HDP_ERR_CONFIG, "null forest");
+    if (on)
+        for (auto& e : f->tev)
+            if (!e) HDP_CHECK_CUDA(cudaEventCreate(&e));
+    f->timing = on ? 1 : 0;
+    return HDP_OK;
+}
+
+extern "C" int hdp_forest_stage_ms(const hdp_forest* f, float* cost_ms, float* aggregate_ms) {
+    HDP_REQUIRE(f != nullptr && f->timing, HDP_ERR_CONFIG, "forest timing is off");
+    HDP_CHECK_CUDA(cudaEventSynchronize(f->tev[2]));
+    float a = 0.0f, b = 0.0f;
+    HDP_CHECK_CUDA(cudaEventElapsedTime(&a, f->tev[0], f->tev[1]));
+    HDP_CHECK_CUDA(cudaEventElapsedTime(&b, f->tev[1], f->tev[2]));
+    if (cost_ms) *cost_ms = a;
+    if (aggregate_ms) *aggregate_ms = b;
     return HDP_OK;
 }

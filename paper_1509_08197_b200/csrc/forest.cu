@@ -984,11 +984,13 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
         HDP_TRY(to_host(hc, cnt.get(), 3, st));
         f->n_trees = hc[0];
         max_tree = hc[1] > 0 ? hc[1] : 1;
-        if (defer_m) {
-            m = hc[2];
-            HDP_REQUIRE(m <= n - 1 || n == 0, HDP_ERR_DATA, "forest has %lld edges for %lld nodes (cycle)",
-                        (long long)m, (long long)n);
-        }
+        if (defer_m) m = hc[2];
+        // an acyclic edge set on n nodes with t components has exactly n - t
+        // edges; a cycle, a self-loop or a repeated edge leaves more (the
+        // Euler tour would then hold closed circuits that never terminate)
+        HDP_REQUIRE(m == n - f->n_trees, HDP_ERR_DATA,
+                    "edge set is not a forest: %lld edges, %lld nodes, %lld components (cycle, self-loop "
+                    "or repeated edge)", (long long)m, (long long)n, (long long)f->n_trees);
     }
     k_tree_ids<<<grid_for(n, B), B, 0, st>>>(n, f->root.get(), tindex.get(), f->tree_id.get()); note_launch();
     HDP_CHECK_LAUNCH();

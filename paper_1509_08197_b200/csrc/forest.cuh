@@ -124,4 +124,13 @@ struct hdp_forest {
     std::vector<int64_t> chunk_off;  // host: chunks of phase r = [chunk_off[r], chunk_off[r+1])
     int64_t chunk_words = 0;         // shared-memory words the largest chunk needs
     int chunks_ok = 0;               // chunks fit in shared memory
+
+    // optional stage timing of hdp_aggregate_wta (hdp_forest_set_timing):
+    // events at entry, after the raw-cost pass, at exit
+    int timing = 0;
+    cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+    ~hdp_forest() {
+        for (auto& e : tev)
+            if (e) cudaEventDestroy(e);
+    }
 };

@@ -303,16 +303,29 @@ __global__ void k_iota32(int64_t n, int32_t* a) {
     if (i < n) a[i] = (int32_t)i;
 }
 
-__global__ void k_keys_unpack(const uint64_t* __restrict__ keys, int64_t n, int32_t* disp,
+// keys of hdp_aggregate_wta: u64 = ord(f32 cost) << 32 | d, ord the
+// order-preserving map of IEEE floats onto u32; with signed_order the top bit
+// is flipped so that int64 order equals u64 order (NCCL reduces int64)
+__global__ void k_keys_unpack(const uint64_t* __restrict__ keys, int64_t n, int signed_order, int32_t* disp,
                               float* min_cost) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
-    uint64_t k = keys[t];
+    uint64_t k = keys[t] ^ (signed_order ? 0x8000000000000000ull : 0ull);
     uint32_t u = (uint32_t)(k >> 32);
     // inverse of the order-preserving encoding used by hdp_aggregate_wta
     uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
     if (disp) disp[t] = (int32_t)(k & 0xffffffffu);
     if (min_cost) min_cost[t] = __uint_as_float(b);
+}
+
+__global__ void k_keys_pack(const int32_t* __restrict__ disp, const float* __restrict__ min_cost, int64_t n,
+                            int signed_order, uint64_t* __restrict__ keys) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    uint32_t b = __float_as_uint(min_cost[t]);
+    uint32_t o = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    uint64_t k = ((uint64_t)o << 32) | (uint32_t)disp[t];
+    keys[t] = k ^ (signed_order ? 0x8000000000000000ull : 0ull);
 }
 
 }  // namespace hdp
@@ -422,10 +435,21 @@ int hdp_argsort_u64(const uint64_t* keys, int64_t n, int32_t* perm, void* stream
     return sort_pairs(keys, kout.get(), idx.get(), perm, n, 0, 64, st);
 }
 
-int hdp_keys_unpack(const uint64_t* keys, int64_t n, int32_t* disp, float* min_cost,
+int hdp_keys_unpack(const uint64_t* keys, int64_t n, int signed_order, int32_t* disp, float* min_cost,
                     void* stream) {
     if (n <= 0) return HDP_OK;
-    k_keys_unpack<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(keys, n, disp, min_cost); note_launch();
+    k_keys_unpack<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(keys, n, signed_order, disp, min_cost);
+    note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+int hdp_keys_pack(const int32_t* disp, const float* min_cost, int64_t n, int signed_order, uint64_t* keys,
+                  void* stream) {
+    if (n <= 0) return HDP_OK;
+    HDP_REQUIRE(disp && min_cost && keys, HDP_ERR_CONFIG, "null buffer");
+    k_keys_pack<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(disp, min_cost, n, signed_order, keys);
+    note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

@@ -38,6 +38,9 @@ public:
         return w;
     }
     void run(std::vector<std::function<void()>>& jobs) {
+        // one call at a time: the slots, the pending count and the generation
+        // belong to the call in flight (done_cv_.wait releases mu_ below)
+        std::lock_guard<std::mutex> call(call_mu_);
         std::unique_lock<std::mutex> lk(mu_);
         while ((int)threads_.size() < (int)jobs.size()) {
             const int id = (int)threads_.size();
@@ -79,7 +82,7 @@ private:
             if (--pending_ == 0) done_cv_.notify_all();
         }
     }
-    std::mutex mu_;
+    std::mutex call_mu_, mu_;
     std::condition_variable cv_, done_cv_;
     std::vector<std::thread> threads_;
     std::vector<std::function<void()>*> slot_;

@@ -61,15 +61,21 @@ def allreduce_min_keys(keys, group=None):
     return keys
 
 
-def run_slab_baseline(left_u8, right_u8, d_max: int, rank: int, world: int, group=None, **kw):
-    """Dense MST pipeline on one pair, disparity slab of this rank, then the
-    key all-reduce.  Returns (disparity int32, min_cost f32) device tensors."""
+def run_slab_baseline(left_u8, right_u8, d_max: int, rank: int, world: int, group=None,
+                      gamma: float = 0.1, cost=None):
+    """Dense MST pipeline on one pair for this rank's disparity slab (the
+    one-call pipeline, every rank rebuilding the same deterministic MST), then
+    one all-reduce(MIN) over the packed keys in int64 order.  Returns
+    (disparity int32, min_cost f32) device tensors of the full range."""
     from . import engine as E
 
     x0, nx = slab(d_max, rank, world)
-    out = E.run_baseline_batch(left_u8, right_u8, d_max, x0=x0, nx=nx, want_keys=True, **kw)
-    keys = out.extra["keys"]
-    if world > 1:
-        allreduce_min_keys(keys, group)
-    disp, mc = E.keys_unpack(keys)
+    out = E.run_baseline_fused(left_u8, right_u8, d_max, gamma, cost or E.CostConsts(), x0=x0, nx=nx)
+    if world == 1:
+        return out.disparity, out.min_cost
+    import torch.distributed as dist
+
+    keys = E.keys_pack(out.disparity, out.min_cost, signed_order=True)
+    dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
+    disp, mc = E.keys_unpack(keys, signed_order=True)
     return disp.view(out.disparity.shape), mc.view(out.min_cost.shape)

@@ -15,7 +15,6 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -174,6 +173,17 @@ class DeviceForest:
                 pass
             self._h = None
 
+    def enable_timing(self):
+        """Record device events around the cost and aggregation stages of
+        every aggregate() call (hdp_forest_set_timing)."""
+        L.call("hdp_forest_set_timing", self._h, 1)
+
+    def stage_seconds(self) -> tuple[float, float]:
+        """(cost, aggregate) seconds of the last aggregate() call; waits for it."""
+        a, b = C.c_float(), C.c_float()
+        L.call("hdp_forest_stage_ms", self._h, C.byref(a), C.byref(b))
+        return a.value / 1e3, b.value / 1e3
+
     def export(self):
         torch = _t()
         dev = L.device()
@@ -232,13 +242,24 @@ class DeviceForest:
         return disp, mc, keys, vol
 
 
-def keys_unpack(keys):
+def keys_unpack(keys, signed_order: bool = False):
     torch = _t()
     n = keys.numel()
     disp = torch.empty(n, dtype=torch.int32, device=keys.device)
     mc = torch.empty(n, dtype=torch.float32, device=keys.device)
-    L.call("hdp_keys_unpack", L.ptr(keys), n, L.ptr(disp), L.ptr(mc), L.stream())
+    L.call("hdp_keys_unpack", L.ptr(keys), n, int(signed_order), L.ptr(disp), L.ptr(mc), L.stream())
     return disp, mc
+
+
+def keys_pack(disp, min_cost, signed_order: bool = False):
+    """(disparity, min cost) -> u64 slab keys (int64 tensor; signed_order:
+    top bit flipped for an int64 MIN reduction)."""
+    torch = _t()
+    n = disp.numel()
+    keys = torch.empty(n, dtype=torch.int64, device=disp.device)
+    L.call("hdp_keys_pack", L.ptr(disp.contiguous()), L.ptr(min_cost.contiguous()), n, int(signed_order),
+           L.ptr(keys), L.stream())
+    return keys
 
 
 # ------------------------------------------------------------------ tables
@@ -406,40 +427,80 @@ def _per_pair_stats(f: DeviceForest, batch: int, npp: int, d_max: int):
 
 
 class _Clock:
+    """Stage timers from CUDA events recorded on the current stream: no
+    synchronisation inside the pipeline (the stages keep overlapping the side
+    streams); durations are resolved once the caller has the results."""
+
     def __init__(self, on: bool):
         self.on = on
+        self.marks: list = []
+        self.forests: list = []  # forests whose aggregate() stages were timed
         self.acc: dict = {}
+        self.last = self._record() if on else None
 
-    def lap(self, key, t0):
+    @staticmethod
+    def _record():
+        ev = L.torch_mod().cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def lap(self, key, t0=None):
+        """Charge the time since the previous mark to `key`."""
         if not self.on:
-            return time.perf_counter()
-        L.torch_mod().cuda.synchronize()
-        t1 = time.perf_counter()
-        self.acc[key] = self.acc.get(key, 0.0) + (t1 - t0)
-        return t1
+            return None
+        ev = self._record()
+        self.marks.append((key, self.last, ev))
+        self.last = ev
+        return None
+
+    def add(self, key, seconds: float):
+        self.acc[key] = self.acc.get(key, 0.0) + seconds
+
+    def resolve(self) -> dict:
+        for key, a, b in self.marks:
+            if key.startswith("_"):
+                continue
+            b.synchronize()
+            self.add(key, a.elapsed_time(b) / 1e3)
+        for f in self.forests:
+            c, a = f.stage_seconds()
+            self.add("cost", c)
+            self.add("aggregate", a)
+        self.marks, self.forests = [], []
+        return self.acc
 
 
 def _forest_layer(lev: Level, eu, ev, ew, in_tree, comp, gamma, cost, masks=None,
-                  x0=0, nx=None, want_volume=False, want_keys=False, clock=None, t0=None,
-                  probe=None):
+                  x0=0, nx=None, want_volume=False, want_keys=False, clock=None, probe=None):
     f = DeviceForest(lev.img_l.shape[0] * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
     if masks is None:
         f.set_lanes_range(x0, lev.d_max + 1 if nx is None else nx)
     else:
         f.set_lanes(masks)
-    if clock is not None:
-        t0 = clock.lap("forest", t0)
+    disp, mc, keys, vol = _aggregate_timed(f, lev, cost, clock, probe, want_volume=want_volume,
+                                           want_keys=want_keys)
+    return f, disp, mc, keys, vol
+
+
+def _aggregate_timed(f: DeviceForest, lev: Level, cost, clock=None, probe=None, **kw):
+    """f.aggregate with the stage clock: the tree build up to here is charged
+    to "forest"; the cost and aggregation stages come from the library's own
+    events (resolved later by clock.resolve)."""
+    if clock is not None and clock.on:
+        clock.lap("forest")
+        f.enable_timing()
     if probe is not None:  # CUDA events around the fused aggregation (bench roofline)
         ev0 = _t().cuda.Event(enable_timing=True)
         ev1 = _t().cuda.Event(enable_timing=True)
         ev0.record()
-    disp, mc, keys, vol = f.aggregate(lev, cost, want_volume=want_volume, want_keys=want_keys)
+    out = f.aggregate(lev, cost, **kw)
     if probe is not None:
         ev1.record()
         probe.append((ev0, ev1, f.total_entries, f.n))
-    if clock is not None:
-        clock.lap("cost_aggregate", t0)
-    return f, disp, mc, keys, vol
+    if clock is not None and clock.on:
+        clock.lap("_cost_aggregate")
+        clock.forests.append(f)
+    return out
 
 
 # sub-batches of the one-call dense pipeline (hdp_dense_pipeline): the tree
@@ -449,11 +510,13 @@ DENSE_SUB_BATCHES = int(os.environ.get("HDP_DENSE_SUB", "1"))
 
 def run_baseline_fused(left_u8, right_u8, d_max: int, gamma: float = 0.1,
                        cost: CostConsts = CostConsts(), x0: int = 0, nx: int | None = None,
-                       n_sub: int | None = None, agg_ms=None, right_ready=None) -> LevelOut:
+                       n_sub: int | None = None, agg_ms=None, right_ready=None,
+                       timing: bool = False) -> LevelOut:
     """run_baseline_batch for plain MST trees in ONE library call
     (hdp_dense_pipeline): the batch runs as concurrent sub-batches on their own
     streams.  agg_ms: optional list that receives each sub-batch's aggregation
-    time (ms, device events)."""
+    time (ms, device events).  timing: fill LevelOut.timings with the
+    reference's stage keys ("forest", "cost_aggregate") from device events."""
     torch = _t()
     if d_max < 1:
         raise ConfigError(f"d_max must be >= 1, got {d_max}")
@@ -465,34 +528,73 @@ def run_baseline_fused(left_u8, right_u8, d_max: int, gamma: float = 0.1,
     disp = torch.empty(b * h * w, dtype=torch.int32, device=dev)
     mc = torch.empty(b * h * w, dtype=torch.float32, device=dev)
     ntrees = np.zeros(b, np.int64)
-    ams = np.zeros(n_sub, np.float32) if agg_ms is not None else None
+    want_ms = agg_ms is not None or timing
+    ams = np.zeros(n_sub, np.float32) if want_ms else None
+    if timing:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
     L.call("hdp_dense_pipeline", L.ptr(left_u8.contiguous()), L.ptr(right_u8.contiguous()), b, h, w, c,
            d_max, x0, nx, cost.alpha, cost.tau_color, cost.tau_grad, gamma, n_sub, L.ptr(disp), L.ptr(mc),
            ntrees.ctypes.data, ams.ctypes.data if ams is not None else None,
            right_ready.cuda_event if right_ready is not None else None, L.stream())
+    timings = {}
+    if timing:
+        e1.record()
+        e1.synchronize()
+        total = e0.elapsed_time(e1) / 1e3
+        agg = float(ams.max()) / 1e3
+        timings = {"forest": max(0.0, total - agg), "cost_aggregate": agg}
     if agg_ms is not None:
         agg_ms.extend(float(x) for x in ams)
     stored = np.full(b, h * w * nx, np.int64)
     ratio = np.array([float(s) / (h * w) / (d_max + 1) for s in stored])
-    return LevelOut(0, h, w, d_max, disp.view(b, h, w), mc.view(b, h, w), ntrees, stored, ratio, {}, None)
+    return LevelOut(0, h, w, d_max, disp.view(b, h, w), mc.view(b, h, w), ntrees, stored, ratio,
+                    timings, None)
+
+
+def level_keys(img, E: int, level: int, block_size: int, key):
+    """Kruskal keys of a pyramid level's grid edges.  hdp_grid_edges keys on
+    the f32 weight bits, exact for uint8 images and every S=2 level (dyadic
+    block means).  Other block sizes give non-dyadic means whose
+    f32 weights can merge distinct float64 weights: those levels are keyed on
+    the stable rank of the float64 weights (mst_edge_order's order,
+    spanning_forest.py:96-107) instead."""
+    if level == 0 or block_size == 2:
+        return key
+    torch = _t()
+    b, h, w, c = img.shape
+    dev = img.device
+    w64 = torch.empty(b * E, dtype=torch.float64, device=dev)
+    L.call("hdp_grid_edge_weights64", L.ptr(img), b, h, w, c, L.ptr(w64), L.stream())
+    bits = w64.view(torch.int64)  # monotone for non-negative weights
+    idx = torch.arange(E, dtype=torch.int64, device=dev)
+    out = torch.empty(b * E, dtype=torch.int64, device=dev)
+    perm = torch.empty(E, dtype=torch.int32, device=dev)
+    rank = torch.empty(E, dtype=torch.int64, device=dev)
+    for i in range(b):
+        L.call("hdp_argsort_u64", L.ptr(bits[i * E:(i + 1) * E]), E, L.ptr(perm), L.stream())
+        rank[perm.long()] = idx
+        out[i * E:(i + 1) * E] = (rank << 32) | idx
+    return out
 
 
 def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
                        cost: CostConsts = CostConsts(), tree_kind: str = "mst", seed: int = 0,
                        x0: int = 0, nx: int | None = None, want_volume=False, want_keys=False,
-                       keep_forest=False, timing=False, probe=None) -> LevelOut:
+                       keep_forest=False, timing=False, probe=None, stepwise=False) -> LevelOut:
     """Full-range aggregation over one MST per pair (aggregation.py:274-358).
     left/right: (B, H, W, C) uint8 device tensors.  [x0, x0+nx) restricts the
-    disparity lanes (a slab of the multi-GPU split); default full range."""
+    disparity lanes (a slab of the multi-GPU split); default full range.
+    MST runs without extra outputs take the one-call pipeline; `stepwise`
+    forces the stage-by-stage path (same results, used to test the former)."""
     if tree_kind not in ("mst", "rt"):
         raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
     if d_max < 1:
         raise ConfigError(f"d_max must be >= 1, got {d_max}")
-    if (tree_kind == "mst" and DENSE_SUB_BATCHES > 0 and not (want_volume or want_keys or keep_forest
-                                                             or timing or probe is not None)):
-        return run_baseline_fused(left_u8, right_u8, d_max, gamma, cost, x0, nx)
+    if (tree_kind == "mst" and DENSE_SUB_BATCHES > 0 and not stepwise
+            and not (want_volume or want_keys or keep_forest or probe is not None)):
+        return run_baseline_fused(left_u8, right_u8, d_max, gamma, cost, x0, nx, timing=timing)
     clock = _Clock(timing)
-    t0 = time.perf_counter()
     b, h, w, c = left_u8.shape
     il, ir = to_f64(left_u8), to_f64(right_u8)
     _, _, _, pl = prepare(il, False)
@@ -503,10 +605,14 @@ def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
         key = rt_keys(E, b, seed, il.device)
     in_tree, comp, _ = mst_grid(b, h, w, eu, ev, key)
     f, disp, mc, keys, vol = _forest_layer(lev, eu, ev, ew, in_tree, comp, gamma, cost, None, x0,
-                                           nx, want_volume, want_keys, clock, t0, probe)
+                                           nx, want_volume, want_keys, clock, probe)
     ntrees, stored, ratio = _per_pair_stats(f, b, h * w, d_max)
+    acc = clock.resolve() if timing else {}
+    timings = ({"forest": acc.get("forest", 0.0),
+                "cost_aggregate": acc.get("cost", 0.0) + acc.get("aggregate", 0.0)}
+               if timing else {})
     out = LevelOut(0, h, w, d_max, disp.view(b, h, w), mc.view(b, h, w), ntrees, stored, ratio,
-                   dict(clock.acc), f if keep_forest else None)
+                   timings, f if keep_forest else None)
     out.extra["keys"] = keys
     out.extra["volume"] = vol
     return out
@@ -521,7 +627,9 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
 
     `model` exposes .layers[l] with .weights/.means/.sigmas (GmmModel).
     `teacher`: optional {level: (B, h_l, w_l) int32 device map} handed to the
-    next finer level instead of this level's own result (teacher forcing)."""
+    next finer level instead of this level's own result (teacher forcing).
+    timing: per-level stage times from device events (LevelOut.timings keys
+    "pyramid" (top level only), "predict", "forest", "cost", "aggregate")."""
     torch = _t()
     if tree_kind not in ("mst", "rt"):
         raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
@@ -530,28 +638,28 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     if d_max // block_size**levels < 1:
         raise ConfigError(f"d_max={d_max} collapses to {d_max // block_size**levels} after "
                           f"{levels} levels of /{block_size}; reduce levels or block_size")
-    if not timing:
-        # The sampled priors of all levels depend only on that level's images:
-        # they run on a side stream from the start, beside the coarser levels'
-        # tree builds (HDPF keeps one SM per pair busy), while the level loop
-        # runs on a high-priority stream so the block scheduler serves it first.
-        caller = torch.cuda.current_stream()
-        pri, hi = _hdp_streams()
-        pri.wait_stream(caller)
-        hi.wait_stream(caller)
-        with torch.cuda.stream(hi):
-            outs = _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0,
-                                   beta, cost, tree_kind, seed, teacher, keep, want_volume, timing,
-                                   on_level, prior_stream=pri)
-        caller.wait_stream(hi)
-        for o in outs:
-            o.disparity.record_stream(caller)
-            o.min_cost.record_stream(caller)
-            if o.extra.get("volume") is not None:
-                o.extra["volume"].record_stream(caller)
-        return outs
-    return _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0, beta,
-                           cost, tree_kind, seed, teacher, keep, want_volume, timing, on_level)
+    # The sampled priors of all levels depend only on that level's images:
+    # they run on a side stream from the start, beside the coarser levels'
+    # tree builds (HDPF keeps one SM per pair busy), while the level loop
+    # runs on a high-priority stream so the block scheduler serves it first.
+    caller = torch.cuda.current_stream()
+    pri, hi = _hdp_streams()
+    pri.wait_stream(caller)
+    hi.wait_stream(caller)
+    with torch.cuda.stream(hi):
+        outs = _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0,
+                               beta, cost, tree_kind, seed, teacher, keep, want_volume, timing,
+                               on_level, prior_stream=pri)
+    caller.wait_stream(hi)
+    for o in outs:
+        o.disparity.record_stream(caller)
+        o.min_cost.record_stream(caller)
+        if o.extra.get("volume") is not None:
+            o.extra["volume"].record_stream(caller)
+        clk = o.extra.pop("clock", None)
+        if clk is not None:
+            o.timings = dict(clk.resolve())
+    return outs
 
 
 _HDP_STREAMS: dict = {}
@@ -570,10 +678,9 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
                     tree_kind, seed, teacher, keep, want_volume, timing, on_level, prior_stream=None):
     torch = _t()
     clock = _Clock(timing)
-    t0 = time.perf_counter()
     b = left_u8.shape[0]
     lv = build_levels(left_u8, right_u8, d_max, levels, block_size, True)
-    t0 = clock.lap("pyramid", t0)
+    clock.lap("pyramid")
     outs: list[LevelOut] = []
     early = {}
     if prior_stream is not None:
@@ -585,12 +692,14 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
                 ev.record(prior_stream)
                 early[level] = (c_, k_, ev)
 
-    def finish(lev, f, disp, mc, vol, stage):
+    def finish(lev, f, disp, mc, vol, clk):
         ntrees, stored, ratio = _per_pair_stats(f, b, lev.h * lev.w, lev.d_max)
         o = LevelOut(lev.level, lev.h, lev.w, lev.d_max, disp.view(b, lev.h, lev.w),
-                     mc.view(b, lev.h, lev.w), ntrees, stored, ratio, stage,
+                     mc.view(b, lev.h, lev.w), ntrees, stored, ratio, {},
                      f if keep else None)
         o.extra["volume"] = vol
+        if timing:
+            o.extra["clock"] = clk
         outs.append(o)
         return o
 
@@ -598,17 +707,17 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
     eu, ev, ew, key, E = grid_edges(top.img_l)
     if tree_kind == "rt":
         key = rt_keys(E, b, seed, top.img_l.device)
+    else:
+        key = level_keys(top.img_l, E, levels, block_size, key)
     in_tree, comp, _ = mst_grid(b, top.h, top.w, eu, ev, key)
-    lclock = _Clock(timing)
     f, disp, mc, _, vol = _forest_layer(top, eu, ev, ew, in_tree, comp, gamma, cost, None,
-                                        want_volume=want_volume, clock=lclock, t0=t0)
-    o = finish(top, f, disp, mc, vol, dict(lclock.acc))
+                                        want_volume=want_volume, clock=clock)
+    o = finish(top, f, disp, mc, vol, clock)
     if on_level is not None:
         on_level(o)
     parent = o.disparity if teacher is None or levels not in teacher else teacher[levels]
     for level in range(levels - 1, -1, -1):
         lev = lv[level]
-        t0 = time.perf_counter()
         lclock = _Clock(timing)
         if level in early:
             counts, kept, ev = early[level]
@@ -622,18 +731,18 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
         row_masks = predict_masks_device(bm, delta0 * block_size**level, lev.img_l.device)
         chosen = predict_masks(bm, delta0 * block_size**level) if keep else None
         rows = assign_rows(parent.contiguous(), lev.h, lev.w, block_size, bm.shape[1])
-        t0 = lclock.lap("predict", t0)
+        lclock.lap("predict")
         eu, ev, ew, key, E = grid_edges(lev.img_l)
         if tree_kind == "rt":
             key = rt_keys(E, b, seed, lev.img_l.device)
+        else:
+            key = level_keys(lev.img_l, E, level, block_size, key)
         in_tree, comp, tmasks, rounds = hdpf(b, lev.h * lev.w, E, eu, ev, key, rows,
                                              row_masks.contiguous(), beta)
         fo = DeviceForest(b * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
         fo.set_lanes_nodes(tmasks.contiguous())
-        t0 = lclock.lap("forest", t0)
-        disp, mc, _, vol = fo.aggregate(lev, cost, want_volume=want_volume)
-        lclock.lap("cost_aggregate", t0)
-        o = finish(lev, fo, disp, mc, vol, dict(lclock.acc))
+        disp, mc, _, vol = _aggregate_timed(fo, lev, cost, lclock, want_volume=want_volume)
+        o = finish(lev, fo, disp, mc, vol, lclock)
         o.extra.update(counts=counts_h, kept=kept_h, chosen=chosen if keep else None,
                        dr_rounds=rounds,
                        tree_masks=(_tree_masks_host(fo, tmasks) if keep else None))
@@ -661,6 +770,54 @@ def _tree_masks_host(fo: DeviceForest, tmasks):
     ar = torch.arange(fo.n, device=roots.device, dtype=torch.int32)
     root_ids = torch.nonzero(roots == ar).flatten()
     return tmasks[root_ids].cpu().numpy().view(np.uint32)
+
+
+_STAGE: dict = {}
+
+
+def stage_pairs(lefts, rights):
+    """Host -> device for a list of same-shape (H, W, C) uint8 images per eye:
+    the images are stacked straight into cached pinned buffers and copied
+    asynchronously, the left eye on the current stream, the right eye on a
+    side stream (the dense pipeline first reads it after the tree build).
+    Returns (left (B,H,W,C), right, right_ready event): the caller makes its
+    stream wait for right_ready before reading the right eye (or hands it to
+    hdp_dense_pipeline, which waits only where the right eye is first read)."""
+    torch = _t()
+    dev = L.device()
+    shape = (len(lefts),) + tuple(np.shape(lefts[0]))
+    key = (dev.index, shape)
+    st = _STAGE.get(key)
+    if st is None:
+        st = [torch.empty(shape, dtype=torch.uint8).pin_memory(),
+              torch.empty(shape, dtype=torch.uint8).pin_memory(), None]
+        _STAGE[key] = st
+    pl, pr, last = st
+    if last is not None:  # the previous call's copies out of these buffers are done
+        last.synchronize()
+    np.stack(lefts, out=pl.numpy())
+    ld = pl.to(dev, non_blocking=True)
+    side = _side_stream()
+    side.wait_stream(torch.cuda.current_stream())
+    np.stack(rights, out=pr.numpy())
+    with torch.cuda.stream(side):
+        rd = pr.to(dev, non_blocking=True)
+        ready = torch.cuda.Event()
+        ready.record(side)
+    rd.record_stream(torch.cuda.current_stream())
+    done = torch.cuda.Event()
+    done.record()
+    st[2] = _Both(done, ready)
+    return ld, rd, ready
+
+
+class _Both:
+    def __init__(self, *events):
+        self.events = events
+
+    def synchronize(self):
+        for e in self.events:
+            e.synchronize()
 
 
 def run_baseline_host(left_u8: np.ndarray, right_u8: np.ndarray, d_max: int, out=None, **kw):

@@ -49,6 +49,7 @@ class Scene:
     pair: StereoPair
     gt_left: DisparityMap
     occlusion: np.ndarray
+    brightness_offset: int = 0  # global offset added to the right image (C3)
 
 
 def _voronoi_labels(h: int, w: int, sx: np.ndarray, sy: np.ndarray) -> np.ndarray:
@@ -142,6 +143,7 @@ def make_scene(spec: SceneSpec, pair_index: int = 0) -> Scene:
         ok = dst_c >= 0
         right[src_r[ok], dst_c[ok]] = left[src_r[ok], src_c[ok]]
         winner_col[src_r[ok], dst_c[ok]] = src_c[ok]
+    off = 0
     if spec.brightness_frac > 0.0 and rng.uniform() < spec.brightness_frac:
         off = int(rng.integers(-15, 16))
         right = np.clip(right.astype(np.int32) + off, 0, 255).astype(np.uint8)
@@ -152,7 +154,7 @@ def make_scene(spec: SceneSpec, pair_index: int = 0) -> Scene:
     pair = StereoPair(RasterImage(left), RasterImage(right), d_max,
                       name=f"c{spec.config_id}-{pair_index}")
     gt = DisparityMap(values=disp, valid=np.ones((h, w), bool))
-    return Scene(pair=pair, gt_left=gt, occlusion=occluded)
+    return Scene(pair=pair, gt_left=gt, occlusion=occluded, brightness_offset=off)
 
 
 def make_batch(config_id: int, batch: int | None = None, start: int = 0) -> list[Scene]:

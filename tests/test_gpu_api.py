@@ -449,3 +449,104 @@ def test_slabs_combine_to_full_range():
         comb = ks if comb is None else torch.minimum(comb, ks)
     disp, _ = E.keys_unpack(keys_to_signed(comb))
     np.testing.assert_array_equal(disp.cpu().numpy(), full.disparity.cpu().numpy().ravel())
+    # keys packed from the one-call pipeline's (disparity, cost) slabs, in int64 order
+    comb = None
+    for r in range(3):
+        x0, nx = slab(40, r, 3)
+        o = E.run_baseline_fused(Ld, Rd, 40, x0=x0, nx=nx)
+        ks = E.keys_pack(o.disparity, o.min_cost, signed_order=True)
+        comb = ks if comb is None else torch.minimum(comb, ks)
+    disp, mc = E.keys_unpack(comb, signed_order=True)
+    np.testing.assert_array_equal(disp.cpu().numpy(), full.disparity.cpu().numpy().ravel())
+    np.testing.assert_array_equal(mc.cpu().numpy(), full.min_cost.cpu().numpy().ravel())
+
+
+def test_pipeline_metrics_seconds_filled(gmm_text):
+    """PipelineResult.metrics["seconds"] carries every stage key of the
+    reference (aggregation.py:347-357, :401-416), from device events."""
+    from paper_1509_08197_b200.aggregation import AggregationParams, run_baseline_pipeline, run_hdp_pipeline
+    from paper_1509_08197_b200.hdp_model import GmmModel
+    from paper_1509_08197_b200.raster_io import RasterImage, StereoPair
+
+    g = golden("pipelines.npz")
+    pair = StereoPair(RasterImage(g["c1_left"]), RasterImage(g["c1_right"]), 16)
+    base = run_baseline_pipeline(pair, AggregationParams())
+    sec = base.metrics["seconds"]
+    assert set(sec) == {"forest", "cost_aggregate", "total"}
+    assert sec["forest"] > 0 and sec["cost_aggregate"] > 0 and sec["total"] >= sec["cost_aggregate"]
+    res = run_hdp_pipeline(pair, GmmModel.parse(gmm_text), AggregationParams(levels=2))
+    sec = res.metrics["seconds"]
+    assert set(sec) == {"pyramid", "predict", "forest", "cost", "aggregate", "total"}
+    for k in ("pyramid", "predict", "forest", "cost", "aggregate"):
+        assert sec[k] > 0, k
+    for lr in res.layers:
+        assert set(lr.timings) == {"cost", "aggregate"} and lr.timings["cost"] > 0
+
+
+@pytest.mark.parametrize("method", ["mst", "rt", "hdp+mst", "m+hdp+rt"])
+def test_run_method_dispatch(method, gmm_text):
+    """evaluation.run_method (evaluation.py:154-167): the label selects the
+    pipeline, tree kind and prefilter; results equal the direct calls."""
+    from paper_1509_08197_b200.aggregation import AggregationParams, run_baseline_pipeline, run_hdp_pipeline
+    from paper_1509_08197_b200.errors import ConfigError
+    from paper_1509_08197_b200.evaluation import parse_method, run_method
+    from paper_1509_08197_b200.hdp_model import GmmModel
+
+    from paper_1509_08197_b200.synthetic import CONFIGS, make_scene
+
+    sc = make_scene(CONFIGS[1], 2)
+    model = GmmModel.parse(gmm_text)
+    params = AggregationParams(levels=2, seed=4)
+    median, hdp, tree = parse_method(method)
+    got = run_method(sc.pair, method, params, model=model)
+    if hdp:
+        want = run_hdp_pipeline(sc.pair, model, params, tree_kind=tree, median_prefilter=median)
+        with pytest.raises(ConfigError):
+            run_method(sc.pair, method, params)  # HDP needs the offset model
+    else:
+        want = run_baseline_pipeline(sc.pair, params, tree_kind=tree, median_prefilter=median)
+    np.testing.assert_array_equal(got.disparity.values, want.disparity.values)
+    assert got.metrics["method"] == want.metrics["method"]
+    assert got.metrics["tree"] == tree and got.metrics["hdp"] == hdp
+    assert got.metrics["median_prefilter"] == median
+
+
+def test_forest_from_edges_rejects_cycles():
+    """An edge set with a cycle, a self-loop or a repeated edge is not a
+    forest: DataError instead of a non-terminating Euler tour."""
+    from paper_1509_08197_b200.errors import DataError
+    from paper_1509_08197_b200.spanning_forest import forest_from_edges
+
+    tri = (np.array([0, 1, 0]), np.array([1, 2, 2]), np.ones(3))
+    loop = (np.array([0, 1]), np.array([1, 1]), np.ones(2))
+    dup = (np.array([0, 0]), np.array([1, 1]), np.ones(2))
+    for u, v, w in (tri, loop, dup):
+        with pytest.raises(DataError):
+            forest_from_edges(4, u, v, w)
+    ok = forest_from_edges(4, np.array([0, 1]), np.array([1, 2]), np.ones(2))
+    assert ok.n_trees == 2
+
+
+def test_hdp_block_size_3_matches_oracle(gmm_text):
+    """block_size 3 gives non-dyadic pyramid means: the levels above 0 are
+    keyed on the float64 weight order, so their forests stay the reference's."""
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.hdp_model import GmmModel
+    from paper_1509_08197_b200.synthetic import SceneSpec, make_scene
+    from oracle import oracle as O
+
+    import torch
+
+    sc = make_scene(SceneSpec(13, 90, 120, 27, 10, 0.3, 8.0, 1), 0)
+    L, R = sc.pair.left.data, sc.pair.right.data
+    outs = E.run_hdp_batch(torch.from_numpy(L[None]).cuda(), torch.from_numpy(R[None]).cuda(), 27, GmmModel.parse(gmm_text), levels=2,
+                           block_size=3, keep=True)
+    teacher = {o.level: o.disparity[0].cpu().numpy() for o in outs}
+    ref = O.run_hdp(L, R, 27, O.parse_gmm(gmm_text), levels=2, s=3, teacher=teacher, keep=True)
+    for o, r in zip(outs, ref):
+        assert int(o.n_trees[0]) == r.n_trees and int(o.stored_entries[0]) == r.stored_entries
+        ex = {k: v.cpu().numpy() for k, v in o.forest.export().items()}
+        np.testing.assert_array_equal(ex["parent"], r.forest.base.parent, f"level {o.level}")
+        got = o.disparity[0].cpu().numpy()
+        band = (r.second_cost - r.min_cost) <= 1e-5 * np.abs(r.min_cost)
+        assert not ((got != r.disparity) & ~band).any(), f"level {o.level}"

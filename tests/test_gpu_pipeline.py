@@ -111,7 +111,7 @@ def test_dense_pipeline_one_call_matches_step_by_step(n_sub):
     crop = (slice(0, 96), slice(0, 160))
     L = dev(np.stack([s.pair.left.data[crop] for s in scenes]))
     R = dev(np.stack([s.pair.right.data[crop] for s in scenes]))
-    ref = E.run_baseline_batch(L, R, spec.d_max, timing=True)  # step-by-step path
+    ref = E.run_baseline_batch(L, R, spec.d_max, stepwise=True)  # step-by-step path
     got = E.run_baseline_fused(L, R, spec.d_max, n_sub=n_sub)
     torch.cuda.synchronize()
     assert torch.equal(got.disparity, ref.disparity)
@@ -132,7 +132,7 @@ def test_dense_pipeline_slab_lanes_match():
     s = make_scene(spec, 5)
     L = dev(s.pair.left.data[None, :80, :120])
     R = dev(s.pair.right.data[None, :80, :120])
-    ref = E.run_baseline_batch(L, R, spec.d_max, x0=17, nx=30, timing=True)
+    ref = E.run_baseline_batch(L, R, spec.d_max, x0=17, nx=30, stepwise=True)
     got = E.run_baseline_fused(L, R, spec.d_max, x0=17, nx=30)
     torch.cuda.synchronize()
     assert torch.equal(got.disparity, ref.disparity)
