@@ -208,7 +208,25 @@ def _stack_pairs(pairs: list[StereoPair], median_prefilter: bool, defer_right: b
 
 
 def _dmap(a: np.ndarray) -> DisparityMap:
-    return DisparityMap(values=a.astype(np.int32), valid=np.ones(a.shape, dtype=bool))
+    return DisparityMap(values=a.astype(np.int32, copy=False), valid=np.ones(a.shape, dtype=bool))
+
+
+def _to_host(*tensors):
+    """Device results -> fresh host numpy arrays: min costs widened to float64
+    (the reference's dtype) on the device, then one asynchronous DMA per
+    tensor into page-locked memory from torch's caching host allocator (no
+    page faults on the hot path) and a single synchronise.  The arrays own
+    their pinned blocks; the block returns to the cache when they are freed."""
+    torch = E._t()
+    outs = []
+    for t in tensors:
+        if t.dtype == torch.float32:
+            t = t.to(torch.float64)
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in outs]
 
 
 def run_baseline_pipeline_batch(pairs: list[StereoPair], params: AggregationParams | None = None,
@@ -232,8 +250,8 @@ def run_baseline_pipeline_batch(pairs: list[StereoPair], params: AggregationPara
     else:
         out = E.run_baseline_batch(Ld, Rd, d_max, params.gamma, cost_params.consts(), tree_kind,
                                    params.seed, keep_forest=on_forest is not None, timing=True)
-    disp = out.disparity.cpu().numpy()
-    cost = out.min_cost.cpu().numpy().astype(np.float64)
+    disp, cost = _to_host(out.disparity, out.min_cost)
+    total = time.perf_counter() - t_start
     b, h, w = disp.shape
     if on_forest is not None:
         if b != 1:
@@ -301,8 +319,8 @@ def run_hdp_pipeline_batch(pairs: list[StereoPair], model: GmmModel,
                            params.delta0, params.beta, cost_params.consts(), tree_kind,
                            params.seed, keep=on_forest is not None, timing=True, on_level=hook)
     b = len(pairs)
-    disps = [o.disparity.cpu().numpy() for o in outs]
-    costs = [o.min_cost.cpu().numpy().astype(np.float64) for o in outs]
+    host = _to_host(*[t for o in outs for t in (o.disparity, o.min_cost)])
+    disps, costs = host[0::2], host[1::2]
     total = time.perf_counter() - t_start
     stage = {"pyramid": 0.0, "predict": 0.0, "forest": 0.0, "cost": 0.0, "aggregate": 0.0}
     for o in outs:
