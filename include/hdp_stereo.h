@@ -126,6 +126,12 @@ int hdp_prior_counts(const double *unit_l, const double *grad_l, const double *u
                      int stride, int window, int max_offset, double alpha, double tau_c,
                      double tau_g, int64_t *counts, int64_t *kept, int max_ctas, void *stream);
 
+/* Self-check of the prior's correctly rounded division by a constant
+ * (x / b as RN(q + (x - q b) RN(1/b)), q = RN(x RN(1/b))) against the IEEE
+ * division __ddiv_rn, for b in {3, 49, 25} on n seeded inputs in [0, 4);
+ * *mismatches (host) = number of differing quotients.  Synchronises. */
+int hdp_check_exact_division(int64_t n, uint64_t seed, int64_t *mismatches, void *stream);
+
 /* predict_intervals (hdp_model.py:498-525) for nrows rows of Bayes matrices
  * (rows x ncols f64, ncols <= 256): stable descending order, sequential
  * running mass, first P/(c+P) < delta stops; out masks (nrows, nw) u32

@@ -43,6 +43,7 @@ SIGNATURES = {
     "hdp_mst_grid": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "hdp_prior_counts": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _D, _D, _D,
                               _P, _P, _I, _P]),
+    "hdp_check_exact_division": (_I, [_I64, C.c_uint64, _P, _P]),
     "hdp_assign_rows": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P]),
     "hdp_hdpf": (_I, [_I, _I64, _I64, _P, _P, _P, _P, _P, _I, _I, _D, _P, _P, _P, _P, _P]),
     "hdp_forest_create": (_I, [_I64, _I64, _P, _P, _P, _P, _P, _F, C.POINTER(_P), _P]),

@@ -23,16 +23,43 @@ struct PriorArgs {
     int h, w, c, d_max, stride, window, max_offset;
     int nrc, ncc;  // centre grid
     double one_minus_alpha, alpha, tc, tg, border;
+    double inv_c, inv_win;  // RN(1/c), RN(1/window^2) for div_rn_by
     unsigned long long* counts;
     unsigned long long* kept;
+    // 7 x 7 path: per pixel a 32-byte record (u0, u1, u2, grad) of each image
+    // (channels past C unused), stored as two planes of 16-byte halves so
+    // that 32 lanes reading 32 consecutive pixels touch 512 contiguous bytes
+    const double2* pl;  // left: (u0, u1) plane, then the (u2, grad) plane
+    const double2* pr;
+    int64_t plane;      // elements per plane
 };
+
+__global__ void k_pack_px(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
+                          double2* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = make_double2(u[i * c], c > 1 ? u[i * c + 1] : 0.0);
+    out[n + i] = make_double2(c > 2 ? u[i * c + 2] : 0.0, g[i]);
+}
+
+// RN(x / b) for b > 0 given y = RN(1 / b): q = RN(x y) is within one ulp of
+// x / b, the remainder r = x - q b is exact in one FMA, and RN(q + r y) is the
+// correctly rounded quotient (Markstein's theorem; no overflow or underflow
+// for the [0, 3] sums here).  Three FP64 instructions instead of the
+// reciprocal-iteration sequence of an IEEE division; hdp_check_exact_division
+// compares it with __ddiv_rn.
+__device__ __forceinline__ double div_rn_by(double x, double b, double y) {
+    const double q = __dmul_rn(x, y);
+    const double r = __fma_rn(-q, b, x);
+    return __fma_rn(r, y, q);
+}
 
 __device__ __forceinline__ double px_cost(const PriorArgs& a, const double* su, const double* sg,
                                           const double* du, const double* dg, int64_t p,
                                           int64_t q) {
     double acc = fabs(__dsub_rn(su[p * a.c], du[q * a.c]));
     for (int k = 1; k < a.c; k++) acc = __dadd_rn(acc, fabs(__dsub_rn(su[p * a.c + k], du[q * a.c + k])));
-    double color = __ddiv_rn(acc, (double)a.c);
+    double color = div_rn_by(acc, (double)a.c, a.inv_c);
     double gd = fabs(__dsub_rn(sg[p], dg[q]));
     double v = __dmul_rn(a.one_minus_alpha, color < a.tc ? color : a.tc);
     double t = __dmul_rn(a.alpha, gd < a.tg ? gd : a.tg);
@@ -89,7 +116,7 @@ __device__ double window_cost(const PriorArgs& a, const double* su, const double
         res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
                         __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
     }
-    return __ddiv_rn(__dadd_rn(first, res), (double)nwin);
+    return div_rn_by(__dadd_rn(first, res), (double)nwin, a.inv_win);
 }
 
 // warp-wide windowed WTA: first minimum over x = 0..d_max
@@ -121,50 +148,117 @@ __device__ int warp_wta(const PriorArgs& a, const double* su, const double* sg, 
 // accumulator is a sequential sum of 6 elements, so lane group g (8 lanes)
 // evaluates disparity x0 + g and lane k of the group accumulates chain k;
 // the pairwise tree ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) is three xor-shuffle
-// levels (IEEE addition is commutative), lane 0 adds `first`.  Four disparities
-// per warp step instead of one per lane: no per-element branches, and the
-// window geometry of a lane (6 rows/columns) is fixed per centre.
-__device__ int warp_wta7(const PriorArgs& a, const double* su, const double* sg, const double* du,
-                         const double* dg, int64_t base, int cr, int cc, int sign) {
-    const int lane = threadIdx.x & 31, k = lane & 7, g = lane >> 3;
-    const int64_t ro0 = base + (int64_t)min(max(cr - 3, 0), a.h - 1) * a.w;
-    const int col0 = min(max(cc - 3, 0), a.w - 1);
+// levels (IEEE addition is commutative), lane 0 adds `first`.  A lane's six
+// window elements are fixed per centre: their row offsets, columns and source
+// pixels (C channels + gradient) are loaded into registers once, so the
+// disparity loop only loads the matched pixels and runs the cost arithmetic.
+template <int C>
+__device__ __forceinline__ double rec_cost(const double4 L, const double4 R, double tc, double tg, double oma,
+                                           double al, double inv_c) {
+    double acc = fabs(__dsub_rn(L.x, R.x));
+    if (C > 1) acc = __dadd_rn(acc, fabs(__dsub_rn(L.y, R.y)));
+    if (C > 2) acc = __dadd_rn(acc, fabs(__dsub_rn(L.z, R.z)));
+    const double color = C == 1 ? acc : div_rn_by(acc, (double)C, inv_c);
+    const double gd = fabs(__dsub_rn(L.w, R.w));
+    const double v = __dmul_rn(oma, color < tc ? color : tc);
+    const double t2 = __dmul_rn(al, gd < tg ? gd : tg);
+    return __dadd_rn(v, t2);
+}
+
+__device__ __forceinline__ double4 ld_rec(const double2* plane01, int64_t plane, int64_t i) {
+    const double2 a = __ldg(plane01 + i), b = __ldg(plane01 + plane + i);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// The 7 x 7 window (the reference default): one warp per sample centre, one
+// disparity per lane (x = lane, lane + 32, ...).  A lane evaluates all 49
+// window elements of its disparity in numpy's order: element 0 is `first`,
+// element q >= 1 goes to accumulator (q - 1) & 7 (six sequential additions
+// each), then ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) and first + that, divided
+// by 49 -- np.add.reduce over the 49 values (verified bit-exact).  The
+// window's source pixels are staged once per centre in shared memory (read
+// as broadcasts); the matched pixels of the 32 lanes are 32 consecutive
+// 32-byte records.  Fully unrolled: no shuffles, no divergent lanes, the
+// geometry is compile-time per element.
+constexpr int kPriorWarps = 8;
+
+// Window-mean cost of one lane's disparity (offset `off` = sign * x) over
+// the staged 7 x 7 window.  Element q >= 1 goes to accumulator (q - 1) & 7 =
+// (dc - dr - 1) mod 8: V[dc] names that accumulator in row dr when V is
+// rotated right by one register per row.  Accumulators start at +0 (0 + v == v
+// exactly).  FAST: every matched column is inside the image (no tests).
+template <int C, bool FAST>
+__device__ __forceinline__ double window_at(const double4* win, const double2* db, int64_t plane, int ro0,
+                                            const int* colv, int off, int cr, int h, int w, double tc, double tg,
+                                            double oma, double al, double inv_c, double inv_win, double border) {
+    auto elem = [&](int dr, int ro, int dc) -> double {
+        const int dcol = colv[dc] + off;
+        if (FAST || (dcol >= 0 && dcol < w))
+            return rec_cost<C>(win[7 * dr + dc], ld_rec(db, plane, ro + dcol), tc, tg, oma, al, inv_c);
+        return border;
+    };
+    double V[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) V[j] = 0.0;
+    const double first = elem(0, ro0, 0);
+#pragma unroll
+    for (int dc = 1; dc < 7; dc++) V[dc] = elem(0, ro0, dc);
+#pragma unroll 1
+    for (int dr = 1; dr < 7; dr++) {
+        const int ro = min(max(cr + dr - 3, 0), h - 1) * w;
+        const double t = V[7];
+#pragma unroll
+        for (int j = 7; j > 0; j--) V[j] = V[j - 1];
+        V[0] = t;
+#pragma unroll
+        for (int dc = 0; dc < 7; dc++) V[dc] = __dadd_rn(V[dc], elem(dr, ro, dc));
+    }
+    // after row 6, accumulator i is V[(i - 1) mod 8]
+    const double res = __dadd_rn(__dadd_rn(__dadd_rn(V[7], V[0]), __dadd_rn(V[1], V[2])),
+                                 __dadd_rn(__dadd_rn(V[3], V[4]), __dadd_rn(V[5], V[6])));
+    return div_rn_by(__dadd_rn(first, res), 49.0, inv_win);
+}
+
+template <int C>
+__device__ int warp_wta7(const PriorArgs& a, const double2* src, const double2* dst, int64_t base, int cr, int cc,
+                         int sign, double4* win) {
+    const int lane = threadIdx.x & 31;
+    int rowo[7], colv[7];
+#pragma unroll
+    for (int i = 0; i < 7; i++) {
+        rowo[i] = min(max(cr + i - 3, 0), a.h - 1) * a.w;
+        colv[i] = min(max(cc + i - 3, 0), a.w - 1);
+    }
+    for (int q = lane; q < 49; q += 32) {
+        const int dr = q / 7, dc = q - 7 * dr;
+        win[q] = ld_rec(src, a.plane, base + (int64_t)min(max(cr + dr - 3, 0), a.h - 1) * a.w +
+                                          min(max(cc + dc - 3, 0), a.w - 1));
+    }
+    __syncwarp();
+    const double2* db = dst + base;
+    const int64_t plane = a.plane;
+    const double tc = a.tc, tg = a.tg, oma = a.one_minus_alpha, al = a.alpha, border = a.border;
+    const double inv_c = a.inv_c, inv_win = a.inv_win;
+    // disparities whose matched columns are inside the image for every element
+    const int safe = sign < 0 ? colv[0] : a.w - 1 - colv[6];
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int bx = 0x7fffffff;
-    for (int x0 = 0; x0 <= a.d_max; x0 += 4) {
-        const int x = x0 + g;
-        const bool ok = x <= a.d_max;
-        double acc = 0.0;
-        if (ok) {
-#pragma unroll 1
-            for (int t = 0; t < 6; t++) {
-                const int q = k + 1 + 8 * t;  // window element 1..48
-                const int dr = q / 7, dc = q - 7 * dr;
-                const int64_t ro = base + (int64_t)min(max(cr + dr - 3, 0), a.h - 1) * a.w;
-                const int col = min(max(cc + dc - 3, 0), a.w - 1);
-                const int dcol = col + sign * x;
-                const double v = (dcol >= 0 && dcol < a.w) ? px_cost(a, su, sg, du, dg, ro + col, ro + dcol)
-                                                           : a.border;
-                acc = t == 0 ? v : __dadd_rn(acc, v);
-            }
-        }
-        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
-        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
-        acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
-        if (k == 0 && ok) {
-            const int dcol = col0 + sign * x;
-            const double first = (dcol >= 0 && dcol < a.w) ? px_cost(a, su, sg, du, dg, ro0 + col0, ro0 + dcol)
-                                                           : a.border;
-            const double v = __ddiv_rn(__dadd_rn(first, acc), 49.0);
-            if (v < best) {  // x ascends per group: strict < keeps the first minimum
-                best = v;
-                bx = x;
-            }
+    const int w = a.w, h = a.h, d_max = a.d_max;
+    for (int x0 = 0; x0 <= d_max; x0 += 32) {
+        const int x = x0 + lane;
+        const int off = sign * min(x, d_max);  // lanes past d_max: an in-range disparity, result unused
+        const double v = (x0 + 31 <= safe && x0 + 31 <= d_max)  // warp-uniform: no border tests
+                             ? window_at<C, true>(win, db, plane, rowo[0], colv, off, cr, h, w, tc, tg, oma, al,
+                                                  inv_c, inv_win, border)
+                             : window_at<C, false>(win, db, plane, rowo[0], colv, off, cr, h, w, tc, tg, oma, al,
+                                                   inv_c, inv_win, border);
+        if (x <= d_max && v < best) {  // x ascends per lane: strict < keeps the first minimum
+            best = v;
+            bx = x;
         }
     }
-    // first minimum over the four groups (lanes 0, 8, 16, 24)
 #pragma unroll
-    for (int o = 8; o <= 16; o <<= 1) {
+    for (int o = 16; o >= 1; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
         const int ox = __shfl_xor_sync(0xffffffffu, bx, o);
         if (ob < best || (ob == best && ox < bx)) {
@@ -172,11 +266,12 @@ __device__ int warp_wta7(const PriorArgs& a, const double* su, const double* sg,
             bx = ox;
         }
     }
-    return __shfl_sync(0xffffffffu, bx, 0);
+    __syncwarp();  // `win` is rewritten by the next call
+    return bx;
 }
 
-template <bool W7>
-__device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, int64_t wid) {
+template <int W7>  // 0: any window; 1 / 3: 7 x 7 window, 1 / 3 channels
+__device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, int64_t wid, double4* win) {
     int b = (int)(wid / per);
     int k = (int)(wid % per);
     int i = k / a.ncc, j = k % a.ncc;
@@ -184,12 +279,14 @@ __device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, in
     int cr = (rs + min(rs + a.stride, a.h) - 1) / 2;
     int cc = (cs + min(cs + a.stride, a.w) - 1) / 2;
     int64_t base = (int64_t)b * a.h * a.w;
-    int dl = W7 ? warp_wta7(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1)
-                : warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
+    int dl;
+    if constexpr (W7 > 0) dl = warp_wta7<W7>(a, a.pl, a.pr, base, cr, cc, -1, win);
+    else dl = warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
     int mc = cc - dl;
     if (mc < 0) return;  // infeasible (hdp_model.py:458-459)
-    int dr = W7 ? warp_wta7(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1)
-                : warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
+    int dr;
+    if constexpr (W7 > 0) dr = warp_wta7<W7>(a, a.pr, a.pl, base, cr, mc, +1, win);
+    else dr = warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
     int diff = dl - dr;
     if (diff < 0) diff = -diff;
     if ((threadIdx.x & 31) == 0 && diff <= a.max_offset) {
@@ -198,13 +295,14 @@ __device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, in
     }
 }
 
-template <bool W7>
-__global__ void __launch_bounds__(256) k_prior(PriorArgs a, int batch) {
+template <int W7>
+__global__ void __launch_bounds__(256, 2) k_prior(PriorArgs a, int batch) {
     const int64_t per = (int64_t)a.nrc * a.ncc;
     const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
+    __shared__ double4 win[kPriorWarps][49];  // the 7 x 7 path's staged window, per warp
     // grid-stride over sample centres (a capped grid leaves SMs to other streams)
     for (int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wid < per * batch; wid += nwarp)
-        prior_centre<W7>(a, per, wid);
+        prior_centre<W7>(a, per, wid, win[threadIdx.x >> 5]);
 }
 __global__ void k_assign_rows(const int32_t* __restrict__ pd, int batch, int ph, int pw, int h,
                               int w, int s, int n_rows, int32_t* __restrict__ rows, int* bad) {
@@ -327,12 +425,68 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
     if (warps == 0) return HDP_OK;
     unsigned grid = (unsigned)grid_for(warps * 32, 256);
     if (max_ctas > 0 && (unsigned)max_ctas < grid) grid = (unsigned)max_ctas;
-    if (window == 7)
-        k_prior<true><<<grid, 256, 0, st>>>(a, batch);
+    a.inv_c = 1.0 / (double)c;  // host IEEE: RN(1/c)
+    a.inv_win = 1.0 / (double)(window * window);
+    DevBuf<double2> pk;
+    a.pl = a.pr = nullptr;
+    a.plane = (int64_t)batch * h * w;
+    if (window == 7) {
+        const int64_t n = a.plane;
+        HDP_TRY(pk.alloc(4 * n, st));
+        k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk.get()); note_launch();
+        k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk.get() + 2 * n); note_launch();
+        a.pl = pk.get();
+        a.pr = pk.get() + 2 * n;
+    }
+    if (window == 7 && c == 3)
+        k_prior<3><<<grid, 256, 0, st>>>(a, batch);
+    else if (window == 7)
+        k_prior<1><<<grid, 256, 0, st>>>(a, batch);
     else
-        k_prior<false><<<grid, 256, 0, st>>>(a, batch);
+        k_prior<0><<<grid, 256, 0, st>>>(a, batch);
     note_launch();
     HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+namespace hdp {
+__global__ void k_check_div(int64_t n, unsigned long long seed, unsigned long long* bad) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // splitmix64 -> x in [0, 4): random mantissas over every binade below 4,
+    // plus sums of three |k/255 - j/255| differences (the prior's inputs)
+    unsigned long long z = seed + (unsigned long long)i * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    double x;
+    if (i & 1) {
+        const int e = (int)(z >> 52) % 40;  // exponent: [2^-38, 4)
+        x = ldexp(1.0 + (double)(z & 0xFFFFFFFFFFFFFull) * 0x1p-52, 1 - e);
+    } else {
+        const int k0 = z & 255, k1 = (z >> 8) & 255, k2 = (z >> 16) & 255;
+        const int j0 = (z >> 24) & 255, j1 = (z >> 32) & 255, j2 = (z >> 40) & 255;
+        x = __dadd_rn(__dadd_rn(fabs(__dsub_rn(k0 / 255.0, j0 / 255.0)), fabs(__dsub_rn(k1 / 255.0, j1 / 255.0))),
+                      fabs(__dsub_rn(k2 / 255.0, j2 / 255.0)));
+    }
+    const double b[3] = {3.0, 49.0, 25.0};
+    for (int t = 0; t < 3; t++)
+        if (div_rn_by(x, b[t], 1.0 / b[t]) != __ddiv_rn(x, b[t])) atomicAdd(bad, 1ull);
+}
+}  // namespace hdp
+
+extern "C" int hdp_check_exact_division(int64_t n, uint64_t seed, int64_t* mismatches, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf<unsigned long long> bad;
+    HDP_TRY(bad.alloc(1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), st));
+    if (n > 0) {
+        k_check_div<<<grid_for(n, 256), 256, 0, st>>>(n, seed, bad.get());
+        note_launch();
+    }
+    HDP_CHECK_LAUNCH();
+    HDP_CHECK_CUDA(cudaMemcpyAsync(mismatches, bad.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HDP_CHECK_CUDA(cudaStreamSynchronize(st));
     return HDP_OK;
 }
 

@@ -226,3 +226,16 @@ def test_predict_masks_device_matches_host(cols, delta):
     want = E.pack_masks(E.predict_masks(bayes, delta)).view(np.int32)
     got = E.predict_masks_device(bayes, delta, torch.device("cuda")).cpu().numpy()
     np.testing.assert_array_equal(got, want)
+
+
+def test_prior_division_is_ieee_exact():
+    """The prior's division by a constant (Markstein: RN(q + r RN(1/b))) equals
+    the IEEE quotient on 2^24 seeded inputs for b = 3, 49, 25."""
+    import ctypes
+
+    from paper_1509_08197_b200 import _lib as L
+
+    L.device()
+    bad = ctypes.c_int64(-1)
+    L.call("hdp_check_exact_division", 1 << 24, 12345, ctypes.byref(bad), L.stream())
+    assert bad.value == 0
