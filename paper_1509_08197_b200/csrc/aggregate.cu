@@ -1674,6 +1674,31 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_REQUIRE(cost_rows || (int64_t)h * w < ((int64_t)1 << 31), HDP_ERR_CONFIG, "image too large");
     cudaStream_t st = (cudaStream_t)stream;
     if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[0], st));
+    // wide dense rows (a disparity range of >= HDP_WIDE_MIN lanes, no volume
+    // output): register-streaming kernels with the raw cost fused into the up
+    // pass (wide.cu)
+    if (!cost_rows && !volume && f->range_x0 >= 0 && wide_min_lanes() > 0 && f->max_m >= wide_min_lanes()) {
+        HDP_REQUIRE(f->n % w == 0, HDP_ERR_CONFIG, "node count is not a whole number of image rows");
+        if (f->geom_w != w || f->geom_np != h * w) {
+            k_fill_cols<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, f->lmeta.get(), h * w, w); note_launch();
+            f->geom_w = w;
+            f->geom_np = h * w;
+        }
+        DevBuf<unsigned long long> kb;
+        unsigned long long* kp = (unsigned long long*)keys;
+        if (!kp) {
+            HDP_TRY(kb.alloc(f->n, st));
+            kp = kb.get();
+        }
+        if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[1], st));  // the cost is fused: no stage of its own
+        HDP_TRY(wide_aggregate(f, packed_l, packed_r, c, alpha, tau_c, tau_g, kp, st));
+        if (disp || min_cost) {
+            k_keys_finish<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp, disp, min_cost); note_launch();
+        }
+        if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[2], st));
+        HDP_CHECK_LAUNCH();
+        return HDP_OK;
+    }
     AggArgs a;
     a.lmeta = f->lmeta.get();
     a.lsimf = f->lsimf.get();
@@ -1715,6 +1740,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         a.qsub_shift = 0;
         while ((1 << a.qsub_shift) < a.qsub) a.qsub_shift++;
     }
+    PhaseClock pc(st);  // HDP_AGG_TRACE=1: per-stage device times on stderr
     DevBuf<float> aup;
     DevBuf<unsigned long long> carry;
     DevBuf<int> tickets;
@@ -1730,10 +1756,15 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_TRY(tickets.alloc(2 * f->n_phases * a.groups + 1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(tickets.get(), 0,
                                    sizeof(int) * (2 * f->n_phases * a.groups + 1), st));
-    // fresh epochs per call: stale words in recycled pool memory never match
-    static std::atomic<unsigned> g_epoch{1};
-    unsigned ep = g_epoch.fetch_add(2);
-    if (ep == 0u || ep + 1 == 0u) ep = g_epoch.fetch_add(2);
+    // fresh epochs per call.  A carry word is (epoch << 32 | f32 bits) and the
+    // tag doubles as the readiness flag, so a stale word in recycled pool
+    // memory must never carry the current tag: epochs live in the NaN range
+    // 0x7f800001..0x7fffffff, a pattern none of the library's buffers stores
+    // in a 32-bit high word (finite floats, ids, sizes, sort keys), and every
+    // call takes two fresh ones (4 M calls before the cycle repeats).
+    static std::atomic<unsigned> g_epoch{0};
+    const unsigned raw = g_epoch.fetch_add(1) % 0x3FFFFFu;
+    const unsigned ep = 0x7f800001u + 2u * raw;
     a.carry = carry.get();
     a.epoch_up = ep;
     a.epoch_down = ep + 1;
@@ -1747,7 +1778,8 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.keys = kp;
     // long-path nodes get one key contribution per 32-lane group
     a.atomic_keys = (f->n_segs > 0 && a.qgroups > 1) ? 1 : 0;
-    if (a.atomic_keys) HDP_CHECK_CUDA(cudaMemsetAsync(kp, 0xff, sizeof(unsigned long long) * f->n, st));
+    static const bool poison = env_int("HDP_KEYS_POISON", 0) != 0;  // diagnostics: unwritten keys read as -1
+    if (a.atomic_keys || poison) HDP_CHECK_CUDA(cudaMemsetAsync(kp, 0xff, sizeof(unsigned long long) * f->n, st));
     a.store_all = volume != nullptr;
     a.seg_light = f->chunks_ok ? 1 : 0;
     if (!cost_rows && (f->geom_w != a.w || f->geom_np != a.npix)) {
@@ -1807,7 +1839,6 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         note_launch();
     }
     if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[1], st));
-    PhaseClock pc(st);
     pc.mark("ecost", 0, 0);
     const bool chunks = f->chunks_ok != 0;
     const size_t csmem = (size_t)((f->chunk_words + 3) & ~3ll) * sizeof(float);

@@ -14,7 +14,10 @@
 constexpr int kShortPath = HDP_SHORT_PATH;
 // Long paths are cut into segments of kSeg nodes, one warp each, chained by
 // decoupled look-back in the aggregation kernels.
-constexpr int kSeg = 32;
+#ifndef HDP_SEG
+#define HDP_SEG 32
+#endif
+constexpr int kSeg = HDP_SEG;
 
 namespace hdp {
 // Short-path chunks: the short paths of a phase are cut into runs whose rows,
@@ -134,3 +137,11 @@ struct hdp_forest {
             if (e) cudaEventDestroy(e);
     }
 };
+
+namespace hdp {
+// wide.cu: aggregation + first argmin for dense rows of >= wide_min_lanes()
+// lanes (keys: u64 first-argmin keys per node, written with atomicMin)
+int wide_min_lanes();
+int wide_aggregate(hdp_forest* f, const float* packed_l, const float* packed_r, int c, float alpha, float tau_c,
+                   float tau_g, unsigned long long* keys, cudaStream_t st);
+}  // namespace hdp
