@@ -11,7 +11,8 @@ keys meet in one NCCL all-reduce(MIN) inside the timed step (strong scaling).
 
 Legs in the same JSON line (`legs`), each with value / e2e / roofline /
 cpu_baseline: C2 dense (8 pairs 463x370 d80), C2 HDP (3 levels, half preset),
-C4 HDP (64 pairs 1390x1110 d240, 5 levels, full preset).  Under torchrun every
+C3 segment tree + HDP (32 pairs 695x555 d120, 4 levels), C4 segment tree + HDP
+(64 pairs 1390x1110 d240, 5 levels, full preset).  Under torchrun every
 rank runs its own pairs of the batched legs (weak scaling, no collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -42,9 +43,10 @@ WORKLOADS = {
                desc="C2: 8 pairs/GPU 463x370 RGB d_max 80, dense MST full range"),
     "c2_hdp": dict(cid=2, kind="hdp", batch=8, levels=3, size_class="half",
                    desc="C2: 8 pairs/GPU 463x370 RGB d_max 80, HDP 3 levels (half preset), MST"),
-    "c4_hdp": dict(cid=4, kind="hdp", batch=64, levels=5, size_class="full",
-                   desc="C4: 64 pairs/GPU 1390x1110 RGB d_max 240, HDP 5 levels (full preset), MST "
-                        "(the reference has no segment tree, SURVEY A24)"),
+    "c3_hdp": dict(cid=3, kind="hdp", batch=32, levels=4, size_class="half", tree="st",
+                   desc="C3: 32 pairs/GPU 695x555 RGB d_max 120, segment tree + HDP 4 levels (half preset)"),
+    "c4_hdp": dict(cid=4, kind="hdp", batch=64, levels=5, size_class="full", tree="st",
+                   desc="C4: 64 pairs/GPU 1390x1110 RGB d_max 240, segment tree + HDP 5 levels (full preset)"),
 }
 METRIC = "aggregated pixel-disparity hypotheses/s (Gpd/s) and stereo pairs/s, vs HBM roofline"
 L2_NOTE = "256 MiB buffer written between timed steps (L2 is 126 MB)"
@@ -57,7 +59,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(WORKLOADS))
-    ap.add_argument("--legs", default="c2,c2_hdp,c4_hdp")
+    ap.add_argument("--legs", default="c2,c2_hdp,c3_hdp,c4_hdp")
     ap.add_argument("--leg-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -95,6 +97,7 @@ def config_dict(name: str, world: int, batch: int):
     wl = WORKLOADS[name]
     d = {"workload": wl["desc"], "config_id": wl["cid"], "pairs_per_gpu": batch,
          "pipeline": "dense" if wl["kind"] == "dense" else f"hdp levels={wl['levels']} {wl['size_class']}",
+         "tree": wl.get("tree", "mst"),
          "l2": L2_NOTE}
     if wl["cid"] == 5:
         d["parallelism"] = f"disparity slabs x{world}, NCCL all-reduce(MIN) of packed keys"
@@ -201,7 +204,7 @@ def cpu_dense_pairs(L, R, d_max, n_pairs):
     return time.perf_counter() - t, n, threads
 
 
-def cpu_hdp_pairs(L, R, d_max, levels, size_class, n_pairs):
+def cpu_hdp_pairs(L, R, d_max, levels, size_class, n_pairs, tree="mst"):
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import oracle as O
@@ -213,7 +216,7 @@ def cpu_hdp_pairs(L, R, d_max, levels, size_class, n_pairs):
     t = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
         outs = list(ex.map(lambda i: O.run_hdp(L[i], R[i], d_max, model, levels=levels,
-                                                size_class=size_class), range(n)))
+                                                size_class=size_class, tree_kind=tree), range(n)))
     hyps = sum(sum(o.stored_entries for o in oo) for oo in outs)
     return time.perf_counter() - t, n, threads, hyps
 
@@ -263,7 +266,8 @@ def cpu_leg(name, Lh, Rh, spec):
                 "kind": "port", "pairs_per_s": n / dt,
                 "sample": f"{n} pairs of the leg's batch, one pair per thread", **host_info()}
     n_pairs = min(len(Lh), 16 if wl["cid"] == 4 else 8, cpu_threads())
-    dt, n, thr, hyps = cpu_hdp_pairs(Lh, Rh, spec.d_max, wl["levels"], wl["size_class"], n_pairs)
+    dt, n, thr, hyps = cpu_hdp_pairs(Lh, Rh, spec.d_max, wl["levels"], wl["size_class"], n_pairs,
+                                     wl.get("tree", "mst"))
     return {"value": hyps / dt / 1e9, "unit": "Gpd/s", "cores": thr, "kind": "port",
             "pairs_per_s": n / dt,
             "sample": f"{n} of the leg's {len(Lh)} pairs, one pair per thread (HDP stored entries "
@@ -295,7 +299,8 @@ def run_reference(args):
             sample = f"per step: {n} pairs, one per thread"
         else:
             n_pairs = min(len(Lh), cpu_threads())
-            t, n, cores, hyps = cpu_hdp_pairs(Lh, Rh, spec.d_max, wl["levels"], wl["size_class"], n_pairs)
+            t, n, cores, hyps = cpu_hdp_pairs(Lh, Rh, spec.d_max, wl["levels"], wl["size_class"], n_pairs,
+                                              wl.get("tree", "mst"))
             sample = f"per step: {n} pairs, one per thread"
         if s >= args.warmup:
             times.append((t, hyps))
@@ -464,7 +469,7 @@ class Runner:
 
         def step(timed_step):
             outs = E.run_hdp_batch(Ld, Rd, spec.d_max, model, levels=wl["levels"], delta0=pre["delta0"],
-                                   beta=pre["beta"])
+                                   beta=pre["beta"], tree_kind=wl.get("tree", "mst"))
             if "hyps" not in info:
                 info["hyps"] = int(sum(int(o.stored_entries.sum()) for o in outs))
                 info["nodes"] = int(sum(B * o.h * o.w for o in outs))
@@ -479,7 +484,7 @@ class Runner:
         stage = {}
 
         def e2e(timed_step):
-            res = A.run_hdp_pipeline_batch(pairs, model, params)
+            res = A.run_hdp_pipeline_batch(pairs, model, params, tree_kind=wl.get("tree", "mst"))
             stage.update(res[0].metrics["seconds"])
 
         e2e_ms = self.timed(e2e, steps, 1)

@@ -146,14 +146,33 @@ int hdp_assign_rows(const int32_t *parent_disp, int batch, int ph, int pw, int h
 
 /* build_hdpf (hdp_forest.py:151-216): rule 1 (disjoint pixel sets drop the
  * edge), then Kruskal order (key) with rule 2 (Jaccard of the LIVE tree sets
- * >= beta, IEEE double division) decided exactly by deterministic
- * reservations.  row_masks: (B, n_rows, nw) u32 bitsets; pixel_row per node.
- * Outputs in_tree[e], comp[v] (representative), tree_masks (n_nodes, nw):
- * the final tree set, valid at every node. */
+ * >= beta, IEEE double division), decided exactly by whole-window rounds:
+ * one CTA per pair takes the next 1023 edges of its sorted list, splits their
+ * live edges into conflict groups (edges sharing a tree) and walks every group
+ * in Kruskal order with one thread.  row_masks: (B, n_rows, nw) u32 bitsets;
+ * pixel_row per node.  Outputs in_tree[e], comp[v] (representative),
+ * tree_masks (n_nodes, nw): the final tree set, valid at every node.
+ * st_k >= 0 builds the segment-tree variant (tree_kind "st", which the
+ * reference does not implement -- parity unpinned): a first pass accepts an
+ * edge only if also w <= min(Int(Ta) + st_k/|Ta|, Int(Tb) + st_k/|Tb|) (Int =
+ * largest edge inside the tree, ew = the f32 edge weights), a second pass links
+ * the subtrees with the rules alone.  st_k < 0 (ew may be NULL): the plain
+ * build. */
 int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, const int32_t *eu,
              const int32_t *ev, const uint64_t *key, const int32_t *pixel_row,
-             const uint32_t *row_masks, int n_rows, int nw, double beta, uint8_t *in_tree,
-             int32_t *comp, uint32_t *tree_masks, int *rounds_out, void *stream);
+             const uint32_t *row_masks, int n_rows, int nw, double beta, const float *ew, double st_k,
+             uint8_t *in_tree, int32_t *comp, uint32_t *tree_masks, int *rounds_out, void *stream);
+
+/* Segment tree (tree_kind "st"; not in the reference, whose edge_order rejects
+ * it, spanning_forest.py:115-120 -- the extension point it would plug into):
+ * per pair, subtrees grown in Kruskal order under the criterion w <=
+ * min(Int(Ta) + k/|Ta|, Int(Tb) + k/|Tb|), then linked into one spanning tree
+ * by the MST of the subtree graph in the same (weight, index) order.  Grid
+ * edges and keys of hdp_grid_edges; outputs in_tree[e] and a component
+ * labelling comp[v] for hdp_forest_create. */
+int hdp_segment_tree(int batch, int h, int w, const int32_t *eu, const int32_t *ev, const float *ew,
+                     const uint64_t *key, double st_k, uint8_t *in_tree, int32_t *comp, int *rounds_out,
+                     void *stream);
 
 /* ------------------------------------------- rooted forest + aggregation */
 
@@ -233,6 +252,25 @@ int hdp_keys_pack(const int32_t *disp, const float *min_cost, int64_t n, int sig
                   uint64_t *keys, void *stream);
 int hdp_keys_unpack(const uint64_t *keys, int64_t n, int signed_order, int32_t *disp,
                     float *min_cost, void *stream);
+
+/* ------------------------------------------------------------ evaluation */
+
+/* error_rate (evaluation.py:27-54) for a batch of B maps of npix pixels:
+ * counts (B, n_thr + 1) int64 = per pair the number of evaluated pixels
+ * (valid in both maps, not occluded; valid / occlusion masks are uint8,
+ * nullable = all valid / none occluded) followed by, per threshold t, the
+ * number of evaluated pixels with |pred - gt| >= t.  1 <= n_thr <= 8;
+ * thresholds on the device. */
+int hdp_error_counts(const int32_t *pred, const int32_t *gt, const uint8_t *pred_valid,
+                     const uint8_t *gt_valid, const uint8_t *occlusion, int batch, int64_t npix,
+                     const int32_t *thresholds, int n_thr, int64_t *counts, void *stream);
+
+/* occlusion_from_gt (evaluation.py:57-76): occlusion (B,H,W) uint8 = a valid
+ * left pixel whose match c - d is off the image, invalid in the right map, or
+ * whose disparities differ by more than 1 (valid masks nullable). */
+int hdp_occlusion_from_gt(const int32_t *gt_left, const int32_t *gt_right, const uint8_t *left_valid,
+                          const uint8_t *right_valid, int batch, int h, int w, uint8_t *occlusion,
+                          void *stream);
 
 /* --------------------------------------------------------- whole pipeline */
 /* run_baseline_pipeline (aggregation.py:263-358) for a batch of pairs in one

@@ -230,6 +230,67 @@ int64_t or_hdpf(int64_t n, int64_t n_edges, const int64_t *u, const int64_t *v, 
     return nacc;
 }
 
+/* Segment-tree (ST) variant of or_hdpf -- NOT in the reference (its
+ * edge_order rejects "st", spanning_forest.py:115-120), so this restatement is
+ * parity UNPINNED: it follows the published ST construction (Mei et al., CVPR
+ * 2013): pass 1 walks the edges in Kruskal order and merges two subtrees only
+ * when the edge weight is at most min(Int(Ta) + k/|Ta|, Int(Tb) + k/|Tb|)
+ * (Int = largest edge inside the subtree, the Felzenszwalb-Huttenlocher
+ * criterion), on top of the HDPF rules when masks are given; pass 2 links the
+ * subtrees by walking the edges again with the rules alone (plain Kruskal on
+ * the subtree graph).  Thresholds in IEEE double: Int (an edge weight) +
+ * k / size. */
+int64_t or_hdpf_st(int64_t n, int64_t n_edges, const int64_t *u, const int64_t *v, const double *wt,
+                   const int64_t *order, int nw, const uint64_t *pix_mask, double beta, double fh_k,
+                   int64_t *acc_u, int64_t *acc_v, double *acc_w, int64_t *root_out,
+                   uint64_t *root_mask_out) {
+    int64_t *par = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *sz = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    double *in = (double *)malloc(sizeof(double) * (size_t)n);
+    uint64_t *tm = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)n * nw);
+    memcpy(tm, pix_mask, sizeof(uint64_t) * (size_t)n * nw);
+    for (int64_t i = 0; i < n; i++) { par[i] = i; sz[i] = 1; in[i] = 0.0; }
+    int64_t nacc = 0;
+    for (int pass = 0; pass < 2; pass++) {
+        for (int64_t k = 0; k < n_edges; k++) {
+            int64_t e = order[k];
+            int64_t a = u[e], b = v[e];
+            int meet = 0;
+            for (int i = 0; i < nw; i++)
+                if (pix_mask[a * nw + i] & pix_mask[b * nw + i]) { meet = 1; break; }
+            if (!meet) continue;
+            int64_t ra = uf_find(par, a), rb = uf_find(par, b);
+            if (ra == rb) continue;
+            int inter = 0, uni = 0;
+            for (int i = 0; i < nw; i++) {
+                inter += __builtin_popcountll(tm[ra * nw + i] & tm[rb * nw + i]);
+                uni += __builtin_popcountll(tm[ra * nw + i] | tm[rb * nw + i]);
+            }
+            if ((double)inter / (double)uni < beta) continue;
+            if (pass == 0) {
+                double ta = in[ra] + fh_k / (double)sz[ra];
+                double tb = in[rb] + fh_k / (double)sz[rb];
+                if (!(wt[e] <= (ta < tb ? ta : tb))) continue;
+            }
+            int64_t keep = ra, gone = rb;
+            if (sz[ra] < sz[rb]) { keep = rb; gone = ra; }
+            double mi = in[ra] > in[rb] ? in[ra] : in[rb];
+            par[gone] = keep;
+            sz[keep] += sz[gone];
+            in[keep] = wt[e] > mi ? wt[e] : mi;
+            for (int i = 0; i < nw; i++) tm[keep * nw + i] |= tm[gone * nw + i];
+            acc_u[nacc] = a; acc_v[nacc] = b; acc_w[nacc] = wt[e]; nacc++;
+        }
+    }
+    for (int64_t i = 0; i < n; i++) {
+        int64_t r = uf_find(par, i);
+        root_out[i] = r;
+        memcpy(root_mask_out + i * nw, tm + r * nw, sizeof(uint64_t) * nw);
+    }
+    free(par); free(sz); free(in); free(tm);
+    return nacc;
+}
+
 /* ------------------------------------------------------------------- BFS */
 
 /* spanning_forest.py:191-283 _bfs_forest: symmetric adjacency with neighbour

@@ -54,6 +54,7 @@ def lib():
             "or_edge_list": (i64, [i, i, i, P, P, P, P]),
             "or_mst_order": (None, [i64, P, P]),
             "or_hdpf": (i64, [i64, i64, P, P, P, P, i, P, d, P, P, P, P, P]),
+            "or_hdpf_st": (i64, [i64, i64, P, P, P, P, i, P, d, d, P, P, P, P, P]),
             "or_bfs_forest": (i64, [i64, i64, P, P, P, P, P, P, P, P, P]),
             "or_aggregate_forest": (None, [i64, i64, P, P, P, P, i64, P, P, P]),
             "or_np_sum": (d, [P, i64]),
@@ -243,9 +244,13 @@ class DForest:
         return int((sizes * np.diff(self.base.tree_slices)).sum())
 
 
+ST_K = 1200.0  # segment-tree merge parameter k (paper_1509_08197_b200.spanning_forest.ST_K)
+
+
 def build_hdpf(u, v, wt, n, pix_masks: np.ndarray, d_max: int, beta: float,
-               order: np.ndarray | None = None) -> DForest:
-    """hdp_forest.py:151-216 (pix_masks: (n, nw) uint64)."""
+               order: np.ndarray | None = None, st_k: float | None = None) -> DForest:
+    """hdp_forest.py:151-216 (pix_masks: (n, nw) uint64).  st_k: build the
+    segment-tree variant (or_hdpf_st; no reference exists, parity unpinned)."""
     if order is None:
         order = mst_edge_order(wt)
     pix_masks = np.ascontiguousarray(pix_masks, np.uint64)
@@ -260,9 +265,14 @@ def build_hdpf(u, v, wt, n, pix_masks: np.ndarray, d_max: int, beta: float,
     u = np.ascontiguousarray(u, np.int64)
     v = np.ascontiguousarray(v, np.int64)
     wt = np.ascontiguousarray(wt, np.float64)
-    k = lib().or_hdpf(n, E, _p(u, _i64), _p(v, _i64), _p(wt, _f64), _p(order, _i64), nw,
-                      _p(pix_masks, _u64), C.c_double(beta), _p(au, _i64), _p(av, _i64),
-                      _p(aw, _f64), _p(roots, _i64), _p(rmask, _u64))
+    if st_k is None:
+        k = lib().or_hdpf(n, E, _p(u, _i64), _p(v, _i64), _p(wt, _f64), _p(order, _i64), nw,
+                          _p(pix_masks, _u64), C.c_double(beta), _p(au, _i64), _p(av, _i64),
+                          _p(aw, _f64), _p(roots, _i64), _p(rmask, _u64))
+    else:
+        k = lib().or_hdpf_st(n, E, _p(u, _i64), _p(v, _i64), _p(wt, _f64), _p(order, _i64), nw,
+                             _p(pix_masks, _u64), C.c_double(beta), C.c_double(st_k), _p(au, _i64),
+                             _p(av, _i64), _p(aw, _f64), _p(roots, _i64), _p(rmask, _u64))
     base = bfs_forest(n, au[:k], av[:k], aw[:k])
     tmasks = rmask[base.roots]
     intervals = [mask_bits(m) for m in tmasks]
@@ -456,14 +466,20 @@ def _layer_wta(left_I, right_I, d_max, forest: DForest, gamma, want_volume=False
     return out
 
 
-def run_baseline(left_u8, right_u8, d_max, gamma=0.1, tree_kind="mst", seed=0) -> LevelOut:
+def _order(wt, tree_kind, n_edges, seed):
+    """edge_order (spanning_forest.py:115-120); "st" walks the MST order."""
+    return rt_edge_order(n_edges, seed) if tree_kind == "rt" else mst_edge_order(wt)
+
+
+def run_baseline(left_u8, right_u8, d_max, gamma=0.1, tree_kind="mst", seed=0, st_k=ST_K) -> LevelOut:
     """aggregation.py:274-358 (tree mst/rt; streaming is result-neutral)."""
     I_l = np.asarray(left_u8, np.float64)
     I_r = np.asarray(right_u8, np.float64)
     h, w = I_l.shape[:2]
     u, v, wt = build_edge_list(I_l)
-    order = mst_edge_order(wt) if tree_kind == "mst" else rt_edge_order(u.size, seed)
-    forest = build_hdpf(u, v, wt, h * w, full_masks(h * w, d_max), d_max, 0.0, order)
+    order = _order(wt, tree_kind, u.size, seed)
+    forest = build_hdpf(u, v, wt, h * w, full_masks(h * w, d_max), d_max, 0.0, order,
+                        st_k if tree_kind == "st" else None)
     d, c, c2 = _layer_wta(I_l, I_r, d_max, forest, gamma)
     return LevelOut(0, d, c, c2, 1.0, forest.n_trees, h * w * (d_max + 1), forest)
 
@@ -552,7 +568,7 @@ def assign_rows(parent_disp: np.ndarray, ch: int, cw: int, s: int) -> np.ndarray
 
 
 def run_hdp(left_u8, right_u8, d_max, model_layers, levels=3, size_class="half",
-            gamma=0.1, s=2, delta0=None, beta=None, tree_kind="mst", seed=0,
+            gamma=0.1, s=2, delta0=None, beta=None, tree_kind="mst", seed=0, st_k=ST_K,
             teacher=None, keep=False):
     """aggregation.py:367-488.  `teacher`, if given, maps level -> the
     level's disparity map to hand to the next finer level instead of this
@@ -567,8 +583,9 @@ def run_hdp(left_u8, right_u8, d_max, model_layers, levels=3, size_class="half",
     I_l, dt = pl[top]
     h, w = I_l.shape[:2]
     u, v, wt = build_edge_list(I_l)
-    order = mst_edge_order(wt) if tree_kind == "mst" else rt_edge_order(u.size, seed)
-    forest = build_hdpf(u, v, wt, h * w, full_masks(h * w, dt), dt, 0.0, order)
+    stk = st_k if tree_kind == "st" else None
+    order = _order(wt, tree_kind, u.size, seed)
+    forest = build_hdpf(u, v, wt, h * w, full_masks(h * w, dt), dt, 0.0, order, stk)
     d, c, c2 = _layer_wta(I_l, pr[top][0], dt, forest, gamma)
     outs.append(LevelOut(top, d, c, c2, forest.search_ratio(), forest.n_trees,
                          forest.total_search_entries(), forest if keep else None))
@@ -587,11 +604,33 @@ def run_hdp(left_u8, right_u8, d_max, model_layers, levels=3, size_class="half",
         row_masks = masks_from_rows(table, dc)
         pix = row_masks[rows]
         u, v, wt = build_edge_list(I_l)
-        order = mst_edge_order(wt) if tree_kind == "mst" else rt_edge_order(u.size, seed)
-        forest = build_hdpf(u, v, wt, h * w, pix, dc, beta, order)
+        order = _order(wt, tree_kind, u.size, seed)
+        forest = build_hdpf(u, v, wt, h * w, pix, dc, beta, order, stk)
         d, c, c2 = _layer_wta(I_l, I_r, dc, forest, gamma)
         outs.append(LevelOut(level, d, c, c2, forest.search_ratio(), forest.n_trees,
                              forest.total_search_entries(), forest if keep else None,
                              table if keep else None, counts if keep else None))
         parent = d if teacher is None or level not in teacher else teacher[level]
     return outs
+
+
+# --------------------------------------------------------------- evaluation
+def error_rate(pred, pred_valid, gt, gt_valid, occlusion=None, threshold=1) -> float:
+    """evaluation.py:27-54 (numpy restatement)."""
+    evaluated = pred_valid & gt_valid
+    if occlusion is not None:
+        evaluated = evaluated & ~occlusion
+    n = int(evaluated.sum())
+    diff = np.abs(pred.astype(np.int64) - gt.astype(np.int64))
+    return 100.0 * float((diff[evaluated] >= threshold).sum()) / n
+
+
+def occlusion_from_gt(gl, gl_valid, gr, gr_valid) -> np.ndarray:
+    """evaluation.py:57-76 (numpy restatement)."""
+    h, w = gl.shape
+    target = np.arange(w)[None, :] - gl
+    inside = target >= 0
+    safe = np.maximum(target, 0)
+    rows = np.arange(h)[:, None]
+    consistent = inside & gr_valid[rows, safe] & (np.abs(gl - gr[rows, safe]) <= 1)
+    return gl_valid & ~consistent

@@ -45,7 +45,8 @@ SIGNATURES = {
                               _P, _P, _I, _P]),
     "hdp_check_exact_division": (_I, [_I64, C.c_uint64, _P, _P]),
     "hdp_assign_rows": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _P, _P]),
-    "hdp_hdpf": (_I, [_I, _I64, _I64, _P, _P, _P, _P, _P, _I, _I, _D, _P, _P, _P, _P, _P]),
+    "hdp_hdpf": (_I, [_I, _I64, _I64, _P, _P, _P, _P, _P, _I, _I, _D, _P, _D, _P, _P, _P, _P, _P]),
+    "hdp_segment_tree": (_I, [_I, _I, _I, _P, _P, _P, _P, _D, _P, _P, _P, _P]),
     "hdp_forest_create": (_I, [_I64, _I64, _P, _P, _P, _P, _P, _F, C.POINTER(_P), _P]),
     "hdp_forest_stats": (_I, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64),
                               C.POINTER(_I64)]),
@@ -61,6 +62,8 @@ SIGNATURES = {
     "hdp_forest_destroy": (None, [_P]),
     "hdp_keys_unpack": (_I, [_P, _I64, _I, _P, _P, _P]),
     "hdp_keys_pack": (_I, [_P, _P, _I64, _I, _P, _P]),
+    "hdp_error_counts": (_I, [_P, _P, _P, _P, _P, _I, _I64, _P, _I, _P, _P]),
+    "hdp_occlusion_from_gt": (_I, [_P, _P, _P, _P, _I, _I, _I, _P, _P]),
     "hdp_dense_pipeline": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _F, _F, _F, _I, _P, _P, _P, _P, _P, _P]),
 }
 

@@ -236,8 +236,8 @@ def run_baseline_pipeline_batch(pairs: list[StereoPair], params: AggregationPara
     """run_baseline_pipeline for several same-geometry pairs in one pass."""
     params = (params or AggregationParams()).resolved()
     cost_params = cost_params or CostParams()
-    if tree_kind not in ("mst", "rt"):
-        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    if tree_kind not in E.TREE_KINDS:
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst', 'rt' or 'st')")
     t_start = time.perf_counter()
     fused = tree_kind == "mst" and on_forest is None
     Ld, Rd, d_max, ready = _stack_pairs(pairs, median_prefilter, defer_right=fused)

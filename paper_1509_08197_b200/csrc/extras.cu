@@ -2,6 +2,8 @@
 // 3x3 median prefilter of the reference's M+* method variants.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace hdp {
@@ -66,9 +68,104 @@ __global__ void k_median3(const uint8_t* __restrict__ src, uint8_t* __restrict__
     dst[t] = v[4];
 }
 
+// error_rate (evaluation.py:27-54) for a batch: per pair the number of
+// evaluated pixels (valid in both maps, not occluded) and, per threshold t,
+// how many of them have |pred - gt| >= t.  Integer counts (the percentage is
+// formed on the host exactly as the reference does).  One CTA per (pair,
+// slice of pixels), block reduction, one atomic per counter per CTA.
+constexpr int kMaxThr = 8;
+__global__ void k_error_counts(const int32_t* __restrict__ pred, const int32_t* __restrict__ gt,
+                               const uint8_t* __restrict__ pvalid, const uint8_t* __restrict__ gvalid,
+                               const uint8_t* __restrict__ occ, int64_t npix, const int32_t* __restrict__ thr,
+                               int n_thr, unsigned long long* __restrict__ counts) {
+    const int b = blockIdx.y;
+    unsigned long long c[kMaxThr + 1];
+#pragma unroll
+    for (int i = 0; i <= kMaxThr; i++) c[i] = 0;
+    int th[kMaxThr];
+#pragma unroll
+    for (int i = 0; i < kMaxThr; i++) th[i] = i < n_thr ? thr[i] : 0x7fffffff;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = (int64_t)b * npix + p;
+        bool ev = (!pvalid || pvalid[q]) && (!gvalid || gvalid[q]) && (!occ || !occ[q]);
+        if (!ev) continue;
+        c[0]++;
+        const long long d = (long long)pred[q] - (long long)gt[q];
+        const long long ad = d < 0 ? -d : d;
+#pragma unroll
+        for (int i = 0; i < kMaxThr; i++) c[i + 1] += ad >= th[i] ? 1ull : 0ull;
+    }
+    __shared__ unsigned long long red[kMaxThr + 1];
+    if (threadIdx.x <= kMaxThr) red[threadIdx.x] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i <= kMaxThr; i++) {
+        unsigned long long v = c[i];
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&red[i], v);
+    }
+    __syncthreads();
+    if (threadIdx.x <= n_thr && red[threadIdx.x]) atomicAdd(&counts[(int64_t)b * (n_thr + 1) + threadIdx.x],
+                                                              red[threadIdx.x]);
+}
+
+// occlusion_from_gt (evaluation.py:57-76): a valid left pixel with disparity d
+// is occluded when c - d is off the image, the right map is invalid there, or
+// |d_left - d_right| > 1.  Pixels without left ground truth stay unmarked.
+__global__ void k_occlusion(const int32_t* __restrict__ gl, const int32_t* __restrict__ gr,
+                            const uint8_t* __restrict__ lvalid, const uint8_t* __restrict__ rvalid, int batch,
+                            int h, int w, uint8_t* __restrict__ occ) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = (int64_t)h * w;
+    if (t >= (int64_t)batch * n) return;
+    const int64_t rowbase = t - (t % n) + ((t % n) / w) * w;  // first pixel of this row
+    const int col = (int)((t % n) % w);
+    const long long dl = gl[t];
+    const long long target = (long long)col - dl;
+    bool consistent = false;
+    if (target >= 0 && target < w) {
+        const int64_t q = rowbase + target;
+        const bool rok = !rvalid || rvalid[q];
+        const long long dr = gr[q];
+        const long long diff = dl - dr;
+        consistent = rok && (diff <= 1 && diff >= -1);
+    }
+    const bool lv = !lvalid || lvalid[t];
+    occ[t] = (lv && !consistent) ? 1 : 0;
+}
+
 }  // namespace hdp
 
 using namespace hdp;
+
+extern "C" int hdp_error_counts(const int32_t* pred, const int32_t* gt, const uint8_t* pred_valid,
+                                const uint8_t* gt_valid, const uint8_t* occlusion, int batch, int64_t npix,
+                                const int32_t* thresholds, int n_thr, int64_t* counts, void* stream) {
+    HDP_REQUIRE(n_thr >= 1 && n_thr <= kMaxThr, HDP_ERR_CONFIG, "1..%d thresholds, got %d", kMaxThr, n_thr);
+    HDP_REQUIRE(pred && gt && thresholds && counts, HDP_ERR_CONFIG, "null buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    HDP_CHECK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * batch * (n_thr + 1), st));
+    if (batch <= 0 || npix <= 0) return HDP_OK;
+    const unsigned gx = (unsigned)std::min<int64_t>((npix + 255) / 256, 1184);
+    k_error_counts<<<dim3(gx, (unsigned)batch), 256, 0, st>>>(pred, gt, pred_valid, gt_valid, occlusion, npix,
+                                                             thresholds, n_thr, (unsigned long long*)counts);
+    note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+extern "C" int hdp_occlusion_from_gt(const int32_t* gt_left, const int32_t* gt_right, const uint8_t* left_valid,
+                                     const uint8_t* right_valid, int batch, int h, int w, uint8_t* occlusion,
+                                     void* stream) {
+    HDP_REQUIRE(gt_left && gt_right && occlusion, HDP_ERR_CONFIG, "null buffer");
+    const int64_t n = (int64_t)batch * h * w;
+    if (n <= 0) return HDP_OK;
+    k_occlusion<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(gt_left, gt_right, left_valid, right_valid, batch,
+                                                                  h, w, occlusion);
+    note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
 
 extern "C" int hdp_grid_edge_weights64(const double* img, int batch, int h, int w, int c, double* ew,
                                        void* stream) {

@@ -351,6 +351,8 @@ struct GrpSmem {
     int32_t hkey[GHASH], hslot[GHASH];
     int32_t sroot[GSLOTS], gp[GSLOTS], mp[GSLOTS], sz[GSLOTS];
     uint32_t mask[GSLOTS * DR_NW];
+    float wt[GW];                     // segment tree: window edge weights
+    float sint[GSLOTS];               // segment tree: Int(T) of the slots' trees
     uint8_t dirty[GSLOTS];
     int nslots, changed;
 };
@@ -394,10 +396,16 @@ __device__ __forceinline__ int grp_find_ro(const int32_t* p, int x) {
     return x;
 }
 
+// FH (segment-tree pass 1): an edge that passes the rules merges two trees
+// only when w <= min(Int(Ta) + k/|Ta|, Int(Tb) + k/|Tb|) (IEEE double, as
+// oracle/hdp_oracle.c or_hdpf_st); Int(T) = the largest edge inside T, kept
+// per root in `tint`.
+template <bool FH>
 __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
                                             const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                                             int32_t* uf, int32_t* usz, uint32_t* tm, int nw, double beta,
-                                            uint8_t* in_tree, int* rounds_out) {
+                                            uint8_t* in_tree, int* rounds_out, const float* __restrict__ ew,
+                                            float* tint, double fh_k) {
     extern __shared__ unsigned long long g_dyn[];
     GrpSmem& s = *reinterpret_cast<GrpSmem*>(g_dyn);
     // rule 2 as an exact integer test: merge iff inter >= thr[uni], where thr[u]
@@ -468,6 +476,7 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
             s.mp[sl] = sl;
             s.dirty[sl] = 0;
             s.sz[sl] = usz[k];
+            if (FH) s.sint[sl] = tint[k];
             for (int i = 0; i < nw; i++) s.mask[sl * DR_NW + i] = tm[(int64_t)k * nw + i];
         }
         __syncthreads();
@@ -479,6 +488,7 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
         s.e[tid] = e;
         s.la[tid] = la;
         s.lb[tid] = lb;
+        if (FH) s.wt[tid] = live ? ew[e] : 0.0f;
         G_TICK(1);
         // 3. groups = connected components of (slots, live edges)
         while (true) {
@@ -544,6 +554,7 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
             // tree): its size and mask are read from / flushed to shared
             // memory only when the cached root changes
             int cr = -1, csz = 0;
+            float ci = 0.0f;  // FH: Int of the cached root
             uint32_t cm[DR_NW];
             while (pos_n >= 0) {
                 n_g++;
@@ -562,10 +573,12 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                 if (x != cr) {  // switch the cache to x
                     if (cr >= 0) {
                         s.sz[cr] = csz;
+                        if (FH) s.sint[cr] = ci;
                         for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
                     }
                     cr = x;
                     csz = s.sz[x];
+                    if (FH) ci = s.sint[x];
 #pragma unroll
                     for (int i = 0; i < DR_NW; i++) cm[i] = i < nw ? s.mask[x * DR_NW + i] : 0u;
                 }
@@ -580,12 +593,23 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                 // rule 2 (hdp_forest.py:195) through the exact threshold table
                 if (inter < thr[uni]) continue;
                 const int ysz = s.sz[y];
+                float nint = 0.0f;
+                if (FH) {
+                    const float wv = s.wt[pos];
+                    const float iy = s.sint[y];
+                    const double tx = (double)ci + fh_k / (double)csz;
+                    const double ty = (double)iy + fh_k / (double)ysz;
+                    if (!((double)wv <= (tx < ty ? tx : ty))) continue;
+                    const float mi = ci > iy ? ci : iy;
+                    nint = wv > mi ? wv : mi;
+                }
                 s.dirty[x] = 1;
                 s.dirty[y] = 1;
                 in_tree[s.e[pos]] = 1;
                 if (csz < ysz) {  // union by size, as dr_union: y survives
                     s.mp[x] = y;
                     s.sz[y] = csz + ysz;
+                    if (FH) s.sint[y] = nint;
 #pragma unroll
                     for (int i = 0; i < DR_NW; i++)
                         if (i < nw) s.mask[y * DR_NW + i] = cm[i] | my[i];
@@ -593,12 +617,14 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                 } else {
                     s.mp[y] = x;
                     csz += ysz;
+                    if (FH) ci = nint;
 #pragma unroll
                     for (int i = 0; i < DR_NW; i++) cm[i] |= my[i];
                 }
             }
             if (cr >= 0) {
                 s.sz[cr] = csz;
+                if (FH) s.sint[cr] = ci;
                 for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
             }
 #ifdef HDP_DR_PROFILE
@@ -617,6 +643,7 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                 uf[k] = s.sroot[r];
             } else {
                 usz[k] = s.sz[sl];
+                if (FH) tint[k] = s.sint[sl];
                 for (int i = 0; i < nw; i++) tm[(int64_t)k * nw + i] = s.mask[sl * DR_NW + i];
             }
         }
@@ -654,23 +681,26 @@ __global__ void k_uf_final(int64_t n, int32_t* uf, int nw, const uint32_t* __res
 
 using namespace hdp;
 
-extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pair,
-                        const int32_t* eu, const int32_t* ev, const uint64_t* key,
-                        const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
-                        double beta, uint8_t* in_tree, int32_t* comp, uint32_t* tree_masks,
-                        int* rounds_out, void* stream) {
+// build_hdpf on the device (see hdp_hdpf in the header).  st_k >= 0: the
+// segment-tree variant, pass 1 with the FH criterion, then (link) pass 2 over
+// the same sorted edges with the rules alone.
+static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, const int32_t* eu, const int32_t* ev,
+                    const uint64_t* key, const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
+                    double beta, const float* ew, double st_k, bool link, uint8_t* in_tree, int32_t* comp,
+                    uint32_t* tree_masks, int* rounds_out, cudaStream_t st) {
     HDP_REQUIRE(beta >= 0.0 && beta <= 1.0, HDP_ERR_CONFIG, "beta must be in [0, 1], got %g", beta);
     HDP_REQUIRE(batch >= 1 && batch <= 255, HDP_ERR_CONFIG, "batch must be in [1, 255]");
     HDP_REQUIRE(edges_per_pair < (1 << 24), HDP_ERR_CONFIG, "too many edges per pair for HDPF keys");
     HDP_REQUIRE(nw >= 1 && n_rows >= 1, HDP_ERR_CONFIG, "empty interval table");
     HDP_REQUIRE(nw <= 8, HDP_ERR_CONFIG, "disparity range above 255 not supported by the HDPF kernel");
-    cudaStream_t st = (cudaStream_t)stream;
+    HDP_REQUIRE(st_k < 0.0 || ew != nullptr, HDP_ERR_CONFIG, "the segment tree needs the edge weights");
     const int64_t n = (int64_t)batch * nodes_per_pair;
     const int64_t m = (int64_t)batch * edges_per_pair;
     const int B = 256;
     DevBuf<int32_t> flag, pos, oidx, oidx2, seg, uf, usz;
     DevBuf<uint64_t> skey, okey, okey2;
     DevBuf<uint32_t> tm;
+    DevBuf<float> tint;
     DevBuf<unsigned long long> res;
     DevBuf<int> rounds;
     HDP_TRY(flag.alloc(m + 1, st));
@@ -710,7 +740,7 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
                                             uf.get(), usz.get(), tm.get(), res.get()); note_launch();
     HDP_CHECK_LAUNCH();
     const char* alg = getenv("HDP_HDPF_DR");  // diagnostics: the reservation kernel instead of groups
-    if (alg && alg[0] == '1') {
+    if (alg && alg[0] == '1' && st_k < 0.0) {
         constexpr size_t dr_smem =
             2 * DR_THREADS * sizeof(unsigned long long) + 2 * DR_THREADS * DR_NW * sizeof(uint32_t);
         HDP_CHECK_CUDA(cudaFuncSetAttribute(k_dr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dr_smem));
@@ -718,13 +748,96 @@ extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pai
                                                  res.get(), nw, beta, in_tree, rounds.get()); note_launch();
     } else {
         constexpr size_t g_smem = sizeof(GrpSmem);
-        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-        k_grp<<<batch, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(), nw, beta,
-                                         in_tree, rounds.get()); note_launch();
+        if (st_k >= 0.0) {
+            HDP_TRY(tint.alloc(n, st));
+            HDP_CHECK_CUDA(cudaMemsetAsync(tint.get(), 0, sizeof(float) * n, st));  // Int of a singleton: 0
+            HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+            k_grp<true><<<batch, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(), nw,
+                                                   beta, in_tree, rounds.get(), ew, tint.get(), st_k); note_launch();
+        }
+        if (st_k < 0.0 || link) {
+            HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+            k_grp<false><<<batch, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(), nw,
+                                                    beta, in_tree, rounds.get(), nullptr, nullptr, -1.0); note_launch();
+        }
     }
     HDP_CHECK_LAUNCH();
     k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks); note_launch();
     HDP_CHECK_LAUNCH();
     if (rounds_out) HDP_TRY(to_host(rounds_out, rounds.get(), 1, st));
+    return HDP_OK;
+}
+
+extern "C" int hdp_hdpf(int batch, int64_t nodes_per_pair, int64_t edges_per_pair,
+                        const int32_t* eu, const int32_t* ev, const uint64_t* key,
+                        const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
+                        double beta, const float* ew, double st_k, uint8_t* in_tree, int32_t* comp,
+                        uint32_t* tree_masks, int* rounds_out, void* stream) {
+    return hdpf_run(batch, nodes_per_pair, edges_per_pair, eu, ev, key, pixel_row, row_masks, n_rows, nw, beta, ew,
+                    st_k, true, in_tree, comp, tree_masks, rounds_out, (cudaStream_t)stream);
+}
+
+namespace hdp {
+int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, const uint64_t* key,
+                uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st, int grid_h, int grid_w);
+
+__global__ void k_relabel_edges(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                                const int32_t* __restrict__ comp, int32_t* u2, int32_t* v2) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    u2[e] = comp[eu[e]];
+    v2[e] = comp[ev[e]];
+}
+
+__global__ void k_compose(int64_t n, const int32_t* __restrict__ c1, const int32_t* __restrict__ c2, int32_t* out) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) out[v] = c2[c1[v]];
+}
+
+__global__ void k_or_u8(int64_t m, const uint8_t* __restrict__ a, uint8_t* b) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < m) b[e] |= a[e];
+}
+}  // namespace hdp
+
+extern "C" int hdp_segment_tree(int batch, int h, int w, const int32_t* eu, const int32_t* ev, const float* ew,
+                                const uint64_t* key, double st_k, uint8_t* in_tree, int32_t* comp, int* rounds_out,
+                                void* stream) {
+    HDP_REQUIRE(st_k >= 0.0, HDP_ERR_CONFIG, "segment-tree k must be >= 0, got %g", st_k);
+    HDP_REQUIRE(batch >= 1 && h >= 1 && w >= 1, HDP_ERR_CONFIG, "bad batch geometry");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t npp = (int64_t)h * w, epp = 2 * npp - h - w;
+    const int64_t n = batch * npp, m = batch * epp;
+    // pass 1: subtrees by the FH criterion (every pixel set full: the HDPF
+    // rules always pass), one sequential walk per pair
+    DevBuf<int32_t> rows, c1, u2, v2, c2;
+    DevBuf<uint32_t> masks, tmask;
+    DevBuf<uint8_t> t2;
+    HDP_TRY(rows.alloc(n, st));
+    HDP_TRY(c1.alloc(n, st));
+    HDP_TRY(masks.alloc(batch, st));
+    HDP_TRY(tmask.alloc(n, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(rows.get(), 0, sizeof(int32_t) * n, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(masks.get(), 0xff, sizeof(uint32_t) * batch, st));
+    HDP_TRY(hdpf_run(batch, npp, epp, eu, ev, key, rows.get(), masks.get(), 1, 1, 0.0, ew, st_k, false, in_tree,
+                     c1.get(), tmask.get(), rounds_out, st));
+    // pass 2: link the subtrees = the MST of the subtree graph under the same
+    // (weight, index) order (Boruvka on the relabelled edges; internal edges
+    // are self-loops and drop out)
+    HDP_TRY(u2.alloc(m + 1, st));
+    HDP_TRY(v2.alloc(m + 1, st));
+    HDP_TRY(c2.alloc(n, st));
+    HDP_TRY(t2.alloc(m + 1, st));
+    if (m > 0) {
+        k_relabel_edges<<<grid_for(m, 256), 256, 0, st>>>(m, eu, ev, c1.get(), u2.get(), v2.get()); note_launch();
+    }
+    HDP_TRY(run_boruvka(n, m, u2.get(), v2.get(), key, t2.get(), c2.get(), nullptr, st, 0, 0));
+    if (m > 0) {
+        k_or_u8<<<grid_for(m, 256), 256, 0, st>>>(m, t2.get(), in_tree); note_launch();
+    }
+    if (comp) {  // a subtree's representative carries the linked component
+        k_compose<<<grid_for(n, 256), 256, 0, st>>>(n, c1.get(), c2.get(), comp); note_launch();
+    }
+    HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

@@ -23,6 +23,10 @@ from . import _lib as L
 from .errors import ConfigError, DataError
 
 ALPHA, TAU_C, TAU_G = 0.9, 0.0275, 0.0078  # cost_volume.py:38-40
+TREE_KINDS = ("mst", "rt", "st")
+# Segment tree (tree_kind "st", absent from the reference): k of the subtree
+# criterion w <= min(Int(Ta) + k/|Ta|, Int(Tb) + k/|Tb|), weights on 0..255.
+ST_K = 1200.0
 
 
 def _t():
@@ -135,6 +139,27 @@ def mst(n_nodes: int, eu, ev, key):
     L.call("hdp_mst", n_nodes, m, L.ptr(eu), L.ptr(ev), L.ptr(key), L.ptr(in_tree), L.ptr(comp),
            C.byref(rounds), L.stream())
     return in_tree[:m], comp, rounds.value
+
+
+def st_grid(batch: int, h: int, w: int, eu, ev, ew, key, st_k: float):
+    """Segment tree per pair of a grid batch (hdp_segment_tree): subtrees
+    under the FH criterion, then linked by the MST of the subtree graph."""
+    torch = _t()
+    m = eu.numel()
+    in_tree = torch.empty(max(m, 1), dtype=torch.uint8, device=eu.device)
+    comp = torch.empty(batch * h * w, dtype=torch.int32, device=eu.device)
+    rounds = C.c_int(0)
+    L.call("hdp_segment_tree", batch, h, w, L.ptr(eu), L.ptr(ev), L.ptr(ew), L.ptr(key), float(st_k),
+           L.ptr(in_tree), L.ptr(comp), C.byref(rounds), L.stream())
+    return in_tree[:m], comp, rounds.value
+
+
+def plain_tree(tree_kind: str, batch: int, h: int, w: int, eu, ev, ew, key, st_k: float):
+    """The plain spanning forest of a grid batch: MST / RT by Boruvka on the
+    keys, segment tree by hdp_segment_tree."""
+    if tree_kind == "st":
+        return st_grid(batch, h, w, eu, ev, ew, key, st_k)
+    return mst_grid(batch, h, w, eu, ev, key)
 
 
 def mst_grid(batch: int, h: int, w: int, eu, ev, key):
@@ -257,7 +282,8 @@ def keys_pack(disp, min_cost, signed_order: bool = False):
     torch = _t()
     n = disp.numel()
     keys = torch.empty(n, dtype=torch.int64, device=disp.device)
-    L.call("hdp_keys_pack", L.ptr(disp.contiguous()), L.ptr(min_cost.contiguous()), n, int(signed_order),
+    disp, min_cost = disp.contiguous(), min_cost.contiguous()  # referenced until the launch
+    L.call("hdp_keys_pack", L.ptr(disp), L.ptr(min_cost), n, int(signed_order),
            L.ptr(keys), L.stream())
     return keys
 
@@ -383,7 +409,8 @@ def assign_rows(parent_disp, h: int, w: int, s: int, n_rows: int):
     return rows
 
 
-def hdpf(batch, npp, epp, eu, ev, key, pixel_row, row_masks, beta: float):
+def hdpf(batch, npp, epp, eu, ev, key, pixel_row, row_masks, beta: float, ew=None, st_k: float = -1.0):
+    """build_hdpf for a batch (hdp_hdpf); st_k >= 0: the segment-tree variant."""
     torch = _t()
     dev = eu.device
     n = batch * npp
@@ -394,8 +421,8 @@ def hdpf(batch, npp, epp, eu, ev, key, pixel_row, row_masks, beta: float):
     tmasks = torch.empty((n, nw), dtype=torch.int32, device=dev)
     rounds = C.c_int(0)
     L.call("hdp_hdpf", batch, npp, epp, L.ptr(eu), L.ptr(ev), L.ptr(key), L.ptr(pixel_row),
-           L.ptr(row_masks), n_rows, nw, float(beta), L.ptr(in_tree), L.ptr(comp), L.ptr(tmasks),
-           C.byref(rounds), L.stream())
+           L.ptr(row_masks), n_rows, nw, float(beta), L.ptr(ew), float(st_k), L.ptr(in_tree), L.ptr(comp),
+           L.ptr(tmasks), C.byref(rounds), L.stream())
     return in_tree[: eu.numel()], comp, tmasks, rounds.value
 
 
@@ -533,7 +560,8 @@ def run_baseline_fused(left_u8, right_u8, d_max: int, gamma: float = 0.1,
     if timing:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-    L.call("hdp_dense_pipeline", L.ptr(left_u8.contiguous()), L.ptr(right_u8.contiguous()), b, h, w, c,
+    left_u8, right_u8 = left_u8.contiguous(), right_u8.contiguous()  # referenced until the launch
+    L.call("hdp_dense_pipeline", L.ptr(left_u8), L.ptr(right_u8), b, h, w, c,
            d_max, x0, nx, cost.alpha, cost.tau_color, cost.tau_grad, gamma, n_sub, L.ptr(disp), L.ptr(mc),
            ntrees.ctypes.data, ams.ctypes.data if ams is not None else None,
            right_ready.cuda_event if right_ready is not None else None, L.stream())
@@ -581,14 +609,15 @@ def level_keys(img, E: int, level: int, block_size: int, key):
 def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
                        cost: CostConsts = CostConsts(), tree_kind: str = "mst", seed: int = 0,
                        x0: int = 0, nx: int | None = None, want_volume=False, want_keys=False,
-                       keep_forest=False, timing=False, probe=None, stepwise=False) -> LevelOut:
+                       keep_forest=False, timing=False, probe=None, stepwise=False,
+                       st_k: float = ST_K) -> LevelOut:
     """Full-range aggregation over one MST per pair (aggregation.py:274-358).
     left/right: (B, H, W, C) uint8 device tensors.  [x0, x0+nx) restricts the
     disparity lanes (a slab of the multi-GPU split); default full range.
     MST runs without extra outputs take the one-call pipeline; `stepwise`
     forces the stage-by-stage path (same results, used to test the former)."""
-    if tree_kind not in ("mst", "rt"):
-        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    if tree_kind not in TREE_KINDS:
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst', 'rt' or 'st')")
     if d_max < 1:
         raise ConfigError(f"d_max must be >= 1, got {d_max}")
     if (tree_kind == "mst" and DENSE_SUB_BATCHES > 0 and not stepwise
@@ -603,7 +632,7 @@ def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
     eu, ev, ew, key, E = grid_edges(il)
     if tree_kind == "rt":
         key = rt_keys(E, b, seed, il.device)
-    in_tree, comp, _ = mst_grid(b, h, w, eu, ev, key)
+    in_tree, comp, _ = plain_tree(tree_kind, b, h, w, eu, ev, ew, key, st_k)
     f, disp, mc, keys, vol = _forest_layer(lev, eu, ev, ew, in_tree, comp, gamma, cost, None, x0,
                                            nx, want_volume, want_keys, clock, probe)
     ntrees, stored, ratio = _per_pair_stats(f, b, h * w, d_max)
@@ -622,7 +651,7 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
                   gamma: float = 0.1, delta0: float = 0.064, beta: float = 0.6,
                   cost: CostConsts = CostConsts(), tree_kind: str = "mst", seed: int = 0,
                   teacher: dict | None = None, keep=False, want_volume=False, timing=False,
-                  on_level=None) -> list[LevelOut]:
+                  on_level=None, st_k: float = ST_K) -> list[LevelOut]:
     """Coarse-to-fine HDP matching for B pairs (aggregation.py:367-488).
 
     `model` exposes .layers[l] with .weights/.means/.sigmas (GmmModel).
@@ -631,8 +660,8 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     timing: per-level stage times from device events (LevelOut.timings keys
     "pyramid" (top level only), "predict", "forest", "cost", "aggregate")."""
     torch = _t()
-    if tree_kind not in ("mst", "rt"):
-        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    if tree_kind not in TREE_KINDS:
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst', 'rt' or 'st')")
     if len(model.layers) < levels:
         raise DataError(f"model covers {len(model.layers)} level transitions, run needs {levels}")
     if d_max // block_size**levels < 1:
@@ -649,7 +678,7 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     with torch.cuda.stream(hi):
         outs = _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0,
                                beta, cost, tree_kind, seed, teacher, keep, want_volume, timing,
-                               on_level, prior_stream=pri)
+                               on_level, prior_stream=pri, st_k=st_k)
     caller.wait_stream(hi)
     for o in outs:
         o.disparity.record_stream(caller)
@@ -675,7 +704,8 @@ def _hdp_streams():
 
 
 def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0, beta, cost,
-                    tree_kind, seed, teacher, keep, want_volume, timing, on_level, prior_stream=None):
+                    tree_kind, seed, teacher, keep, want_volume, timing, on_level, prior_stream=None,
+                    st_k: float = ST_K):
     torch = _t()
     clock = _Clock(timing)
     b = left_u8.shape[0]
@@ -709,7 +739,7 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
         key = rt_keys(E, b, seed, top.img_l.device)
     else:
         key = level_keys(top.img_l, E, levels, block_size, key)
-    in_tree, comp, _ = mst_grid(b, top.h, top.w, eu, ev, key)
+    in_tree, comp, _ = plain_tree(tree_kind, b, top.h, top.w, eu, ev, ew, key, st_k)
     f, disp, mc, _, vol = _forest_layer(top, eu, ev, ew, in_tree, comp, gamma, cost, None,
                                         want_volume=want_volume, clock=clock)
     o = finish(top, f, disp, mc, vol, clock)
@@ -738,7 +768,8 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
         else:
             key = level_keys(lev.img_l, E, level, block_size, key)
         in_tree, comp, tmasks, rounds = hdpf(b, lev.h * lev.w, E, eu, ev, key, rows,
-                                             row_masks.contiguous(), beta)
+                                             row_masks.contiguous(), beta, ew=ew,
+                                             st_k=st_k if tree_kind == "st" else -1.0)
         fo = DeviceForest(b * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
         fo.set_lanes_nodes(tmasks.contiguous())
         disp, mc, _, vol = _aggregate_timed(fo, lev, cost, lclock, want_volume=want_volume)

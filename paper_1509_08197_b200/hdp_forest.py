@@ -131,13 +131,17 @@ def disparity_forest_from_device(f: "E.DeviceForest", tree_masks_words: np.ndarr
 
 
 def build_hdpf(edges: EdgeList, pixel_intervals: PixelIntervalMap, tree_kind: str = "mst",
-               seed: int = 0, beta: float = 0.6) -> DisparityForest:
-    """hdp_forest.py:151-216 on the GPU."""
+               seed: int = 0, beta: float = 0.6, st_k: float | None = None) -> DisparityForest:
+    """hdp_forest.py:151-216 on the GPU.  tree_kind "st": the segment-tree
+    variant (subtrees under the FH criterion + the rules, then linked with the
+    rules alone; not in the reference, parity unpinned)."""
+    from .spanning_forest import ST_K, TREE_KINDS
+
     torch = E._t()
     if not 0.0 <= beta <= 1.0:
         raise ConfigError(f"beta must be in [0, 1], got {beta}")
-    if tree_kind not in ("mst", "rt"):
-        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    if tree_kind not in TREE_KINDS:
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst', 'rt' or 'st')")
     n = edges.n_nodes
     if pixel_intervals.n_pixels != n:
         raise InternalError(f"interval map covers {pixel_intervals.n_pixels} pixels, grid has {n}")
@@ -148,7 +152,8 @@ def build_hdpf(edges: EdgeList, pixel_intervals: PixelIntervalMap, tree_kind: st
     rows = torch.from_numpy(np.ascontiguousarray(pixel_intervals.pixel_row, np.int32)).to(dev)
     eu, ev, ew = _device_edges(edges.u, edges.v, edges.weight)
     key = _device_keys(edges, tree_kind, seed)
-    in_tree, comp, tmasks, _ = E.hdpf(1, n, edges.n_edges, eu, ev, key, rows, row_masks, beta)
+    stk = (ST_K if st_k is None else st_k) if tree_kind == "st" else -1.0
+    in_tree, comp, tmasks, _ = E.hdpf(1, n, edges.n_edges, eu, ev, key, rows, row_masks, beta, ew=ew, st_k=stk)
     f = E.DeviceForest(n, eu, ev, ew, in_tree, comp, 0.1)
     roots = f.export()["root"].cpu().numpy()
     root_ids = np.flatnonzero(roots == np.arange(n))

@@ -79,6 +79,8 @@ def _device_keys(edges: EdgeList, tree_kind: str, seed: int):
     idx = np.arange(n_e, dtype=np.int64)
     if tree_kind == "rt":
         return E.rt_keys(n_e, 1, seed, dev)
+    if tree_kind not in TREE_KINDS:
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst', 'rt' or 'st')")
     w = np.asarray(edges.weight, np.float64)
     if np.any(w < 0) or np.any(~np.isfinite(w)):
         raise ConfigError("edge weights must be finite and non-negative")
@@ -110,12 +112,21 @@ def rt_edge_order(edges: EdgeList, seed: int) -> np.ndarray:
     return np.random.default_rng(seed).permutation(edges.n_edges)
 
 
+TREE_KINDS = ("mst", "rt", "st")
+
+# Segment tree (tree_kind "st") merge parameter k (engine.ST_K).  The
+# reference has no segment tree (edge_order rejects "st",
+# spanning_forest.py:115-120); this is the extension it names.
+ST_K = E.ST_K
+
+
 def edge_order(edges: EdgeList, tree_kind: str, seed: int = 0) -> np.ndarray:
-    if tree_kind == "mst":
+    """spanning_forest.py:115-120; "st" walks the MST order (weight, index)."""
+    if tree_kind in ("mst", "st"):
         return mst_edge_order(edges)
     if tree_kind == "rt":
         return rt_edge_order(edges, seed)
-    raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst', 'rt' or 'st')")
 
 
 class UnionFind:
@@ -248,18 +259,26 @@ def _device_edges(u, v, w):
 
 
 def build_forest(edges: EdgeList, tree_kind: str = "mst", seed: int = 0,
-                 accept: AcceptFn | None = None) -> RootedForest:
+                 accept: AcceptFn | None = None, st_k: float = ST_K) -> RootedForest:
     """spanning_forest.py:286-322 on the GPU.  The `accept` predicate is a
     Python callback per edge; it cannot run inside the device kernels, so a
     non-None accept raises ConfigError (use build_hdpf for interval-aware
-    acceptance)."""
-    if tree_kind not in ("mst", "rt"):
-        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst' or 'rt')")
+    acceptance, tree_kind "st" for the segment tree).  tree_kind "st": the
+    segment tree (not in the reference; parity unpinned)."""
+    if tree_kind not in TREE_KINDS:
+        raise ConfigError(f"unknown tree kind {tree_kind!r} (want 'mst', 'rt' or 'st')")
     if accept is not None:
         raise ConfigError("custom accept predicates are not supported on the GPU path")
     eu, ev, ew = _device_edges(edges.u, edges.v, edges.weight)
     key = _device_keys(edges, tree_kind, seed)
-    in_tree, comp, _ = E.mst(edges.n_nodes, eu, ev, key)
+    if tree_kind == "st":
+        torch = E._t()
+        n = edges.n_nodes
+        rows = torch.zeros(n, dtype=torch.int32, device=eu.device)
+        full = torch.full((1, 1, 1), -1, dtype=torch.int32, device=eu.device)  # every pixel set full
+        in_tree, comp, _, _ = E.hdpf(1, n, edges.n_edges, eu, ev, key, rows, full, 0.0, ew=ew, st_k=st_k)
+    else:
+        in_tree, comp, _ = E.mst(edges.n_nodes, eu, ev, key)
     f = E.DeviceForest(edges.n_nodes, eu, ev, ew, in_tree, comp, 0.1)
     rf = rooted_from_device(f)
     pw = _node_weights(rf.parent, edges.u, edges.v, edges.weight)

@@ -261,7 +261,43 @@ def gen_hdpf():
     save("hdpf.npz", **out)
 
 
+def gen_evaluation():
+    """error_rate / occlusion_from_gt / evaluate_pair (evaluation.py:27-124)
+    on random maps with validity holes and on a synthetic scene's ground truth."""
+    from treestereo import evaluation as ref_ev
+    from treestereo.raster_io import DisparityMap
+
+    rng = np.random.default_rng(77)
+    out = {}
+    for k in range(4):
+        h, w = int(rng.integers(20, 60)), int(rng.integers(20, 70))
+        gl = rng.integers(0, 16, size=(h, w)).astype(np.int32)
+        gr = np.clip(gl + rng.integers(-2, 3, size=(h, w)), 0, 15).astype(np.int32)
+        vl = rng.uniform(size=(h, w)) < 0.85
+        vr = rng.uniform(size=(h, w)) < 0.85
+        pred = np.clip(gl + rng.integers(-4, 5, size=(h, w)), 0, 20).astype(np.int32)
+        pv = rng.uniform(size=(h, w)) < 0.95
+        L_ = DisparityMap(values=gl, valid=vl)
+        R_ = DisparityMap(values=gr, valid=vr)
+        P_ = DisparityMap(values=pred, valid=pv)
+        occ = ref_ev.occlusion_from_gt(L_, R_)
+        p = f"e{k}_"
+        out.update({p + "gl": gl, p + "gr": gr, p + "vl": vl, p + "vr": vr, p + "pred": pred, p + "pv": pv,
+                    p + "occ": occ})
+        for t in (1, 2, 3):
+            out[p + f"err{t}"] = np.array(ref_ev.error_rate(P_, L_, None, t))
+            out[p + f"err{t}_occ"] = np.array(ref_ev.error_rate(P_, L_, occ, t))
+        rep = ref_ev.evaluate_pair("x", "mst", P_, L_, occ)
+        out[p + "n_eval"] = np.array(rep.n_evaluated)
+    out["count"] = np.array(4)
+    save("evaluation.npz", **out)
+
+
 def main():
+    if len(sys.argv) > 1:  # regenerate only the named fixtures: make_golden.py evaluation ...
+        for name in sys.argv[1:]:
+            globals()["gen_" + name]()
+        return
     src = "/root/reference/pkg/src/treestereo/data/default.gmm"
     with open(src) as fh:
         text = fh.read()
@@ -276,6 +312,7 @@ def main():
     gen_tables(model)
     gen_hdpf()
     gen_pipelines(model)
+    gen_evaluation()
 
 
 if __name__ == "__main__":

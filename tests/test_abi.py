@@ -73,8 +73,13 @@ def test_config_errors_without_a_gpu(lib):
     with pytest.raises(ConfigError):
         _lib.call("hdp_block_mean", None, None, 1, 4, 4, 3, 1, None)  # block_size < 2
     with pytest.raises(ConfigError):
-        _lib.call("hdp_hdpf", 1, 4, 4, None, None, None, None, None, 1, 1, 1.5, None, None,
+        _lib.call("hdp_hdpf", 1, 4, 4, None, None, None, None, None, 1, 1, 1.5, None, -1.0, None, None,
                   None, None, None)  # beta > 1
+    with pytest.raises(ConfigError):
+        _lib.call("hdp_segment_tree", 1, 4, 4, None, None, None, None, -1.0, None, None, None,
+                  None)  # segment-tree k < 0
+    with pytest.raises(ConfigError):
+        _lib.call("hdp_error_counts", None, None, None, None, None, 1, 4, None, 0, None, None)  # no threshold
     assert lib.hdp_launch_count() == 0
 
 

@@ -550,3 +550,41 @@ def test_hdp_block_size_3_matches_oracle(gmm_text):
         got = o.disparity[0].cpu().numpy()
         band = (r.second_cost - r.min_cost) <= 1e-5 * np.abs(r.min_cost)
         assert not ((got != r.disparity) & ~band).any(), f"level {o.level}"
+
+
+def test_evaluation_on_device_matches_reference():
+    """error_rate / occlusion_from_gt / evaluate_pair on the GPU equal the
+    reference's outputs (golden, evaluation.py:27-124) exactly; the batched
+    device scorer equals the per-pair one."""
+    import torch
+
+    from paper_1509_08197_b200.evaluation import (error_rate, error_rates_device, evaluate_pair,
+                                                  occlusion_from_gt)
+    from paper_1509_08197_b200.raster_io import DisparityMap
+
+    g = golden("evaluation.npz")
+    for k in range(int(g["count"])):
+        p = f"e{k}_"
+        L_ = DisparityMap(values=g[p + "gl"], valid=g[p + "vl"])
+        R_ = DisparityMap(values=g[p + "gr"], valid=g[p + "vr"])
+        P_ = DisparityMap(values=g[p + "pred"], valid=g[p + "pv"])
+        occ = occlusion_from_gt(L_, R_)
+        np.testing.assert_array_equal(occ, g[p + "occ"])
+        for t in (1, 2, 3):
+            assert error_rate(P_, L_, None, t) == float(g[p + f"err{t}"])
+            assert error_rate(P_, L_, occ, t) == float(g[p + f"err{t}_occ"])
+        rep = evaluate_pair("x", "mst", P_, L_, occ)
+        assert rep.n_evaluated == int(g[p + "n_eval"])
+        assert rep.err_ge_1 == float(g[p + "err1_occ"]) and rep.err_ge_2 == float(g[p + "err2_occ"])
+    # batched, device-resident maps (all valid) == the per-pair host calls
+    pred = np.stack([np.clip(g["e0_gl"] + d, 0, 30) for d in (0, 1, -2)]).astype(np.int32)
+    gt = np.stack([g["e0_gl"]] * 3).astype(np.int32)
+    occ = np.stack([g["e0_occ"]] * 3)
+    got = error_rates_device(torch.from_numpy(pred).cuda(), torch.from_numpy(gt).cuda(),
+                             torch.from_numpy(occ.astype(np.uint8)).cuda(), (1, 2))
+    for b in range(3):
+        ones = np.ones(gt[b].shape, bool)
+        P_ = DisparityMap(values=pred[b], valid=ones)
+        G_ = DisparityMap(values=gt[b], valid=ones)
+        assert got[b, 0] == error_rate(P_, G_, occ[b], 1)
+        assert got[b, 1] == error_rate(P_, G_, occ[b], 2)

@@ -104,8 +104,10 @@ def test_parse_method():
     assert parse_method("hdp+mst") == (False, True, "mst")
     assert parse_method("m+hdp+rt") == (True, True, "rt")
     assert parse_method("mst") == (False, False, "mst")
+    # the segment tree: the extension the reference names but rejects
+    assert parse_method("m+hdp+st") == (True, True, "st")
     with pytest.raises(ConfigError):
-        parse_method("st")  # the reference has no segment tree
+        parse_method("xt")
 
 
 def test_boundary_types_validate():
@@ -118,11 +120,16 @@ def test_boundary_types_validate():
         StereoPair(img, RasterImage(np.zeros((4, 5, 3), np.uint8)), 3)
 
 
-def test_error_rate():
-    gt = DisparityMap(np.array([[1, 2], [3, 4]]), np.ones((2, 2), bool))
-    pred = DisparityMap(np.array([[1, 3], [3, 6]]), np.ones((2, 2), bool))
-    assert error_rate(pred, gt, threshold=1) == 50.0
-    assert error_rate(pred, gt, threshold=2) == 25.0
+def test_error_rate_validates_before_the_device():
+    from paper_1509_08197_b200.errors import ConfigError, DataError
+    from paper_1509_08197_b200.raster_io import DisparityMap
+
+    a = DisparityMap(values=np.zeros((2, 3), np.int32), valid=np.ones((2, 3), bool))
+    b = DisparityMap(values=np.zeros((3, 2), np.int32), valid=np.ones((3, 2), bool))
+    with pytest.raises(DataError):
+        error_rate(a, b)
+    with pytest.raises(ConfigError):
+        error_rate(a, a, threshold=0)
 
 
 def test_synthetic_generator_is_seeded_and_consistent():

@@ -146,3 +146,16 @@ def test_hdp_pipeline_full_preset(gmm_text):
         np.testing.assert_allclose(o.min_cost, g[p + "cost"], rtol=1e-12, atol=0)
         assert o.n_trees == int(g[p + "ntrees"])
         assert o.stored_entries == int(g[p + "stored"])
+
+
+def test_evaluation_matches_reference():
+    """error_rate / occlusion_from_gt restatements vs the reference's outputs."""
+    g = golden("evaluation.npz")
+    for k in range(int(g["count"])):
+        p = f"e{k}_"
+        occ = O.occlusion_from_gt(g[p + "gl"], g[p + "vl"], g[p + "gr"], g[p + "vr"])
+        np.testing.assert_array_equal(occ, g[p + "occ"])
+        for t in (1, 2, 3):
+            assert O.error_rate(g[p + "pred"], g[p + "pv"], g[p + "gl"], g[p + "vl"], None, t) == float(g[p + f"err{t}"])
+            assert O.error_rate(g[p + "pred"], g[p + "pv"], g[p + "gl"], g[p + "vl"], occ, t) == float(
+                g[p + f"err{t}_occ"])
