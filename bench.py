@@ -16,7 +16,7 @@ C3 segment tree + HDP (32 pairs 695x555 d120, 4 levels), C4 segment tree + HDP
 rank runs its own pairs of the batched legs (weak scaling, no collective).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c5|c2|c2_hdp|c4_hdp] [--legs c2,c2_hdp,c4_hdp|none]
+                  [--config c5|c2|c2_hdp|c3_hdp|c4_hdp] [--legs c2,c2_hdp,c3_hdp,c4_hdp|none]
 """
 
 from __future__ import annotations

@@ -667,6 +667,31 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
 #endif
 }
 
+// segment-tree pass 2: keep the sorted edges whose endpoints are still in
+// different trees after pass 1 (an edge inside a tree stays inside: trees
+// only grow), order preserved
+__global__ void k_live_edges(int64_t ms, const int32_t* __restrict__ order, const int32_t* __restrict__ eu,
+                             const int32_t* __restrict__ ev, int32_t* uf, int32_t* flag) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ms) return;
+    const int32_t e = order[i];
+    flag[i] = uf_find(uf, eu[e]) != uf_find(uf, ev[e]) ? 1 : 0;
+}
+
+__global__ void k_compact_order(int64_t ms, const int32_t* __restrict__ order, const int32_t* __restrict__ flag,
+                                const int32_t* __restrict__ pos, int32_t* out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ms && flag[i]) out[pos[i]] = order[i];
+}
+
+__global__ void k_seg_remap(int batch, int64_t ms, const int32_t* __restrict__ seg, const int32_t* __restrict__ flag,
+                            const int32_t* __restrict__ pos, int32_t* seg2) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > batch) return;
+    const int32_t s0 = seg[b];
+    seg2[b] = s0 < ms ? pos[s0] : (ms > 0 ? pos[ms - 1] + flag[ms - 1] : 0);
+}
+
 __global__ void k_uf_final(int64_t n, int32_t* uf, int nw, const uint32_t* __restrict__ tm,
                            int32_t* comp, uint32_t* tree_masks) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -755,9 +780,27 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
             k_grp<true><<<batch, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(), nw,
                                                    beta, in_tree, rounds.get(), ew, tint.get(), st_k); note_launch();
         }
+        const int32_t* order2 = oidx2.get();
+        const int32_t* seg2p = seg.get();
+        DevBuf<int32_t> lflag, lpos, oidx3, seg2;
+        if (st_k >= 0.0 && link && ms > 0) {
+            // pass 2 walks only the edges still between two trees
+            HDP_TRY(lflag.alloc(ms + 1, st));
+            HDP_TRY(lpos.alloc(ms + 1, st));
+            HDP_TRY(oidx3.alloc(ms + 1, st));
+            HDP_TRY(seg2.alloc(batch + 1, st));
+            k_live_edges<<<grid_for(ms, B), B, 0, st>>>(ms, oidx2.get(), eu, ev, uf.get(), lflag.get()); note_launch();
+            HDP_TRY(exclusive_sum(lflag.get(), lpos.get(), ms, st));
+            k_compact_order<<<grid_for(ms, B), B, 0, st>>>(ms, oidx2.get(), lflag.get(), lpos.get(), oidx3.get());
+            note_launch();
+            k_seg_remap<<<grid_for(batch + 1, B), B, 0, st>>>(batch, ms, seg.get(), lflag.get(), lpos.get(),
+                                                               seg2.get()); note_launch();
+            order2 = oidx3.get();
+            seg2p = seg2.get();
+        }
         if (st_k < 0.0 || link) {
             HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-            k_grp<false><<<batch, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(), nw,
+            k_grp<false><<<batch, GW, g_smem, st>>>(seg2p, order2, eu, ev, uf.get(), usz.get(), tm.get(), nw,
                                                     beta, in_tree, rounds.get(), nullptr, nullptr, -1.0); note_launch();
         }
     }
