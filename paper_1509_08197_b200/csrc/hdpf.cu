@@ -15,6 +15,7 @@
 // edges are compacted (order preserved) in front of the next window.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -709,29 +710,23 @@ using namespace hdp;
 // build_hdpf on the device (see hdp_hdpf in the header).  st_k >= 0: the
 // segment-tree variant, pass 1 with the FH criterion, then (link) pass 2 over
 // the same sorted edges with the rules alone.
-static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, const int32_t* eu, const int32_t* ev,
-                    const uint64_t* key, const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
-                    double beta, const float* ew, double st_k, bool link, uint8_t* in_tree, int32_t* comp,
-                    uint32_t* tree_masks, int* rounds_out, cudaStream_t st) {
-    HDP_REQUIRE(beta >= 0.0 && beta <= 1.0, HDP_ERR_CONFIG, "beta must be in [0, 1], got %g", beta);
-    HDP_REQUIRE(batch >= 1 && batch <= 255, HDP_ERR_CONFIG, "batch must be in [1, 255]");
-    HDP_REQUIRE(edges_per_pair < (1 << 24), HDP_ERR_CONFIG, "too many edges per pair for HDPF keys");
-    HDP_REQUIRE(nw >= 1 && n_rows >= 1, HDP_ERR_CONFIG, "empty interval table");
-    HDP_REQUIRE(nw <= 8, HDP_ERR_CONFIG, "disparity range above 255 not supported by the HDPF kernel");
-    HDP_REQUIRE(st_k < 0.0 || ew != nullptr, HDP_ERR_CONFIG, "the segment tree needs the edge weights");
-    const int64_t n = (int64_t)batch * nodes_per_pair;
-    const int64_t m = (int64_t)batch * edges_per_pair;
+// One slice of at most kHdpfSlice pairs (edges [e0, e0 + nb * epp)): rule 1,
+// the per-pair Kruskal sort, and the window rounds on the batch-wide
+// union-find state (node ids are global over the batch).
+constexpr int kHdpfSlice = 255;  // pairs per k_grp launch (9 pair bits in the sort key)
+
+static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, const int32_t* eu, const int32_t* ev,
+                      const uint64_t* key, const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
+                      double beta, const float* ew, double st_k, bool link, uint8_t* in_tree, int32_t* uf,
+                      int32_t* usz, uint32_t* tm, float* tint, unsigned long long* res, int* rounds,
+                      cudaStream_t st) {
+    const int64_t m = (int64_t)nb * edges_per_pair;
     const int B = 256;
-    DevBuf<int32_t> flag, pos, oidx, oidx2, seg, uf, usz;
+    DevBuf<int32_t> flag, pos, oidx, oidx2, seg;
     DevBuf<uint64_t> skey, okey, okey2;
-    DevBuf<uint32_t> tm;
-    DevBuf<float> tint;
-    DevBuf<unsigned long long> res;
-    DevBuf<int> rounds;
     HDP_TRY(flag.alloc(m + 1, st));
     HDP_TRY(pos.alloc(m + 1, st));
     HDP_TRY(skey.alloc(m + 1, st));
-    if (m > 0) HDP_CHECK_CUDA(cudaMemsetAsync(in_tree, 0, m, st));
     int64_t ms = 0;
     if (m > 0) {
         k_rule1<<<grid_for(m, B), B, 0, st>>>(m, eu, ev, key, pixel_row, row_masks, nodes_per_pair,
@@ -746,7 +741,7 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
     HDP_TRY(okey2.alloc(ms + 1, st));
     HDP_TRY(oidx.alloc(ms + 1, st));
     HDP_TRY(oidx2.alloc(ms + 1, st));
-    HDP_TRY(seg.alloc(batch + 1, st));
+    HDP_TRY(seg.alloc(nb + 1, st));
     if (m > 0)
         k_select<<<grid_for(m, B), B, 0, st>>>(m, flag.get(), pos.get(), skey.get(), okey.get(),
                                                oidx.get()); note_launch();
@@ -754,7 +749,74 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
     pos.release();
     skey.release();
     HDP_TRY(sort_pairs(okey.get(), okey2.get(), oidx.get(), oidx2.get(), ms, 0, 63, st));
-    k_seg_bounds<<<grid_for(ms + 1, B), B, 0, st>>>(ms, okey2.get(), batch, seg.get()); note_launch();
+    k_seg_bounds<<<grid_for(ms + 1, B), B, 0, st>>>(ms, okey2.get(), nb, seg.get()); note_launch();
+    HDP_CHECK_LAUNCH();
+    const char* alg = getenv("HDP_HDPF_DR");  // diagnostics: the reservation kernel instead of groups
+    if (alg && alg[0] == '1' && st_k < 0.0) {
+        constexpr size_t dr_smem =
+            2 * DR_THREADS * sizeof(unsigned long long) + 2 * DR_THREADS * DR_NW * sizeof(uint32_t);
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_dr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dr_smem));
+        k_dr<<<nb, DR_THREADS, dr_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf, usz, tm, res, nw, beta, in_tree,
+                                              rounds); note_launch();
+        HDP_CHECK_LAUNCH();
+        return HDP_OK;
+    }
+    constexpr size_t g_smem = sizeof(GrpSmem);
+    if (st_k >= 0.0) {
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+        k_grp<true><<<nb, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf, usz, tm, nw, beta, in_tree, rounds,
+                                            ew, tint, st_k); note_launch();
+    }
+    const int32_t* order2 = oidx2.get();
+    const int32_t* seg2p = seg.get();
+    DevBuf<int32_t> lflag, lpos, oidx3, seg2;
+    if (st_k >= 0.0 && link && ms > 0) {
+        // pass 2 walks only the edges still between two trees
+        HDP_TRY(lflag.alloc(ms + 1, st));
+        HDP_TRY(lpos.alloc(ms + 1, st));
+        HDP_TRY(oidx3.alloc(ms + 1, st));
+        HDP_TRY(seg2.alloc(nb + 1, st));
+        k_live_edges<<<grid_for(ms, B), B, 0, st>>>(ms, oidx2.get(), eu, ev, uf, lflag.get()); note_launch();
+        HDP_TRY(exclusive_sum(lflag.get(), lpos.get(), ms, st));
+        k_compact_order<<<grid_for(ms, B), B, 0, st>>>(ms, oidx2.get(), lflag.get(), lpos.get(), oidx3.get());
+        note_launch();
+        k_seg_remap<<<grid_for(nb + 1, B), B, 0, st>>>(nb, ms, seg.get(), lflag.get(), lpos.get(), seg2.get());
+        note_launch();
+        order2 = oidx3.get();
+        seg2p = seg2.get();
+    }
+    if (st_k < 0.0 || link) {
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+        k_grp<false><<<nb, GW, g_smem, st>>>(seg2p, order2, eu, ev, uf, usz, tm, nw, beta, in_tree, rounds, nullptr,
+                                             nullptr, -1.0); note_launch();
+    }
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+// build_hdpf on the device (see hdp_hdpf in the header).  st_k >= 0: the
+// segment-tree variant, pass 1 with the FH criterion, then (link) pass 2 over
+// the same sorted edges with the rules alone.  Batches of any size: slices of
+// kHdpfSlice pairs share the batch-wide union-find state.
+static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, const int32_t* eu, const int32_t* ev,
+                    const uint64_t* key, const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
+                    double beta, const float* ew, double st_k, bool link, uint8_t* in_tree, int32_t* comp,
+                    uint32_t* tree_masks, int* rounds_out, cudaStream_t st) {
+    HDP_REQUIRE(beta >= 0.0 && beta <= 1.0, HDP_ERR_CONFIG, "beta must be in [0, 1], got %g", beta);
+    HDP_REQUIRE(batch >= 1, HDP_ERR_CONFIG, "batch must be >= 1");
+    HDP_REQUIRE(edges_per_pair < (1 << 24), HDP_ERR_CONFIG, "too many edges per pair for HDPF keys");
+    HDP_REQUIRE(nw >= 1 && n_rows >= 1, HDP_ERR_CONFIG, "empty interval table");
+    HDP_REQUIRE(nw <= 8, HDP_ERR_CONFIG, "disparity range above 255 not supported by the HDPF kernel");
+    HDP_REQUIRE(st_k < 0.0 || ew != nullptr, HDP_ERR_CONFIG, "the segment tree needs the edge weights");
+    const int64_t n = (int64_t)batch * nodes_per_pair;
+    const int64_t m = (int64_t)batch * edges_per_pair;
+    const int B = 256;
+    DevBuf<int32_t> uf, usz;
+    DevBuf<uint32_t> tm;
+    DevBuf<float> tint;
+    DevBuf<unsigned long long> res;
+    DevBuf<int> rounds;
+    if (m > 0) HDP_CHECK_CUDA(cudaMemsetAsync(in_tree, 0, m, st));
     HDP_TRY(uf.alloc(n, st));
     HDP_TRY(usz.alloc(n, st));
     HDP_TRY(tm.alloc(n * nw, st));
@@ -763,48 +825,18 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
     HDP_CHECK_CUDA(cudaMemsetAsync(rounds.get(), 0, sizeof(int), st));
     k_uf_init<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
                                             uf.get(), usz.get(), tm.get(), res.get()); note_launch();
-    HDP_CHECK_LAUNCH();
-    const char* alg = getenv("HDP_HDPF_DR");  // diagnostics: the reservation kernel instead of groups
-    if (alg && alg[0] == '1' && st_k < 0.0) {
-        constexpr size_t dr_smem =
-            2 * DR_THREADS * sizeof(unsigned long long) + 2 * DR_THREADS * DR_NW * sizeof(uint32_t);
-        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_dr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dr_smem));
-        k_dr<<<batch, DR_THREADS, dr_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(),
-                                                 res.get(), nw, beta, in_tree, rounds.get()); note_launch();
-    } else {
-        constexpr size_t g_smem = sizeof(GrpSmem);
-        if (st_k >= 0.0) {
-            HDP_TRY(tint.alloc(n, st));
-            HDP_CHECK_CUDA(cudaMemsetAsync(tint.get(), 0, sizeof(float) * n, st));  // Int of a singleton: 0
-            HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-            k_grp<true><<<batch, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf.get(), usz.get(), tm.get(), nw,
-                                                   beta, in_tree, rounds.get(), ew, tint.get(), st_k); note_launch();
-        }
-        const int32_t* order2 = oidx2.get();
-        const int32_t* seg2p = seg.get();
-        DevBuf<int32_t> lflag, lpos, oidx3, seg2;
-        if (st_k >= 0.0 && link && ms > 0) {
-            // pass 2 walks only the edges still between two trees
-            HDP_TRY(lflag.alloc(ms + 1, st));
-            HDP_TRY(lpos.alloc(ms + 1, st));
-            HDP_TRY(oidx3.alloc(ms + 1, st));
-            HDP_TRY(seg2.alloc(batch + 1, st));
-            k_live_edges<<<grid_for(ms, B), B, 0, st>>>(ms, oidx2.get(), eu, ev, uf.get(), lflag.get()); note_launch();
-            HDP_TRY(exclusive_sum(lflag.get(), lpos.get(), ms, st));
-            k_compact_order<<<grid_for(ms, B), B, 0, st>>>(ms, oidx2.get(), lflag.get(), lpos.get(), oidx3.get());
-            note_launch();
-            k_seg_remap<<<grid_for(batch + 1, B), B, 0, st>>>(batch, ms, seg.get(), lflag.get(), lpos.get(),
-                                                               seg2.get()); note_launch();
-            order2 = oidx3.get();
-            seg2p = seg2.get();
-        }
-        if (st_k < 0.0 || link) {
-            HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-            k_grp<false><<<batch, GW, g_smem, st>>>(seg2p, order2, eu, ev, uf.get(), usz.get(), tm.get(), nw,
-                                                    beta, in_tree, rounds.get(), nullptr, nullptr, -1.0); note_launch();
-        }
+    if (st_k >= 0.0) {
+        HDP_TRY(tint.alloc(n, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(tint.get(), 0, sizeof(float) * n, st));  // Int of a singleton: 0
     }
     HDP_CHECK_LAUNCH();
+    for (int b0 = 0; b0 < batch; b0 += kHdpfSlice) {
+        const int nb = std::min(kHdpfSlice, batch - b0);
+        const int64_t e0 = (int64_t)b0 * edges_per_pair;
+        HDP_TRY(hdpf_slice(nb, nodes_per_pair, edges_per_pair, eu + e0, ev + e0, key + e0, pixel_row, row_masks,
+                           n_rows, nw, beta, ew ? ew + e0 : nullptr, st_k, link, in_tree + e0, uf.get(), usz.get(),
+                           tm.get(), tint.get(), res.get(), rounds.get(), st));
+    }
     k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks); note_launch();
     HDP_CHECK_LAUNCH();
     if (rounds_out) HDP_TRY(to_host(rounds_out, rounds.get(), 1, st));

@@ -804,6 +804,15 @@ def _tree_masks_host(fo: DeviceForest, tmasks):
 
 
 _STAGE: dict = {}
+_STAGER = []
+
+
+def _stager():
+    if not _STAGER:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _STAGER.append(ThreadPoolExecutor(1, thread_name_prefix="hdp-stage"))
+    return _STAGER[0]
 
 
 def stage_pairs(lefts, rights):
@@ -826,11 +835,14 @@ def stage_pairs(lefts, rights):
     pl, pr, last = st
     if last is not None:  # the previous call's copies out of these buffers are done
         last.synchronize()
+    # the right eye is stacked on a helper thread while this one stacks the
+    # left eye and starts its copy (numpy releases the GIL while copying)
+    fut = _stager().submit(np.stack, rights, out=pr.numpy())
     np.stack(lefts, out=pl.numpy())
     ld = pl.to(dev, non_blocking=True)
     side = _side_stream()
     side.wait_stream(torch.cuda.current_stream())
-    np.stack(rights, out=pr.numpy())
+    fut.result()
     with torch.cuda.stream(side):
         rd = pr.to(dev, non_blocking=True)
         ready = torch.cuda.Event()

@@ -588,3 +588,26 @@ def test_evaluation_on_device_matches_reference():
         G_ = DisparityMap(values=gt[b], valid=ones)
         assert got[b, 0] == error_rate(P_, G_, occ[b], 1)
         assert got[b, 1] == error_rate(P_, G_, occ[b], 2)
+
+
+def test_hdpf_batches_beyond_one_launch():
+    """hdp_hdpf slices batches above 255 pairs (9 pair bits in the sort key)
+    over several launches on one union-find: 260 small pairs equal their
+    single-pair forests."""
+    import torch
+
+    from paper_1509_08197_b200 import engine as E
+
+    rng = np.random.default_rng(5)
+    b, h, w, d = 260, 6, 7, 7
+    img = torch.from_numpy(rng.integers(0, 256, size=(b, h, w, 3)).astype(np.uint8)).cuda()
+    il = E.to_f64(img)
+    eu, ev, ew, key, nE = E.grid_edges(il)
+    rows = torch.from_numpy(rng.integers(0, 4, size=b * h * w).astype(np.int32)).cuda()
+    masks = torch.from_numpy(rng.integers(1, 255, size=(b, 4, 1)).astype(np.int32)).cuda()
+    in_tree, comp, tm, _ = E.hdpf(b, h * w, nE, eu, ev, key, rows, masks, 0.5)
+    for i in (0, 131, 255, 259):
+        sl = slice(i * nE, (i + 1) * nE)
+        one = E.hdpf(1, h * w, nE, eu[sl] - i * h * w, ev[sl] - i * h * w, key[sl],
+                     rows[i * h * w:(i + 1) * h * w].contiguous(), masks[i:i + 1].contiguous(), 0.5)
+        assert torch.equal(one[0], in_tree[sl])
