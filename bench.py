@@ -319,6 +319,20 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def accuracy(scenes, disp_dev):
+    """err >= 1 / >= 2 px of the final maps against the scenes' ground truth
+    (non-occluded pixels), scored on the device (evaluation.error_rates_device)."""
+    import torch
+
+    from paper_1509_08197_b200.evaluation import error_rates_device
+
+    gt = torch.from_numpy(np.stack([s.gt_left.values for s in scenes]).astype(np.int32)).cuda()
+    occ = torch.from_numpy(np.stack([s.occlusion for s in scenes]).astype(np.uint8)).cuda()
+    r = error_rates_device(disp_dev.contiguous(), gt, occ, (1, 2))
+    return {"err_ge_1_pct": float(r[:, 0].mean()), "err_ge_2_pct": float(r[:, 1].mean()),
+            "pixels": "non-occluded", "scored": "on the device (hdp_error_counts)"}
+
+
 # ------------------------------------------------------------------ GPU arm
 class Runner:
     def __init__(self, args):
@@ -413,6 +427,9 @@ class Runner:
                 A.run_baseline_pipeline_batch(pairs)
 
         e2e_ms = self.timed(e2e, steps, 1)
+        acc = None
+        if not slabs:
+            acc = accuracy(scenes, E.run_baseline_fused(Ld, Rd, d_max).disparity)
         hyps = B * H * W * (d_max + 1)
         n_lanes = nx
         t_dev = self.reduce_max(sum(dev_ms) / 1e3)
@@ -431,6 +448,7 @@ class Runner:
                             "PipelineResult list out)" if not slabs else
                             "pinned staging + distributed.run_slab_baseline + D2H"},
             "gpu_launches": int(launches),
+            "accuracy": acc,
         }
         t_agg = statistics.mean(agg_ms) / 1e3
         entries = B * H * W * n_lanes
@@ -471,6 +489,7 @@ class Runner:
             outs = E.run_hdp_batch(Ld, Rd, spec.d_max, model, levels=wl["levels"], delta0=pre["delta0"],
                                    beta=pre["beta"], tree_kind=wl.get("tree", "mst"))
             if "hyps" not in info:
+                info["final"] = outs[-1].disparity
                 info["hyps"] = int(sum(int(o.stored_entries.sum()) for o in outs))
                 info["nodes"] = int(sum(B * o.h * o.w for o in outs))
                 info["ratios"] = [float(np.mean(o.search_ratio)) for o in outs]
@@ -516,6 +535,7 @@ class Runner:
                          "algorithmic_bytes": algo,
                          "algorithmic_bytes_rule": "sum over levels of 8 B x stored entries + 30 B x pixels"},
             "gpu_launches": int(launches),
+            "accuracy": accuracy(scenes, info["final"]),
         }
         if with_cpu:
             out["cpu_baseline"] = cpu_leg(name, Lh, Rh, spec)
@@ -548,7 +568,7 @@ def run_ours(args):
         "data": "synthetic (seeded Voronoi scenes of BASELINE.json's configs, SURVEY §8d)",
         "config": head["config"], "pairs_per_s": head["pairs_per_s"],
         "e2e": head["e2e"], "roofline": head["roofline"], "cpu_baseline": head.get("cpu_baseline"),
-        "gpu_launches": head["gpu_launches"], "clocks": clocks, "legs": legs,
+        "gpu_launches": head["gpu_launches"], "accuracy": head.get("accuracy"), "clocks": clocks, "legs": legs,
     }
     print(json.dumps(line), flush=True)
     if r.dist:

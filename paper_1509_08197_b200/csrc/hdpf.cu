@@ -1,18 +1,20 @@
 // Disparity-tree forest (HDPF) build, exact with the reference's sequential
-// Kruskal-with-rules (hdp_forest.py:151-216).
+// Kruskal-with-rules (hdp_forest.py:151-216), and the segment-tree variant.
 //
 // Rule 1 (pixel sets disjoint -> drop) is a static per-edge filter; the
 // survivors are sorted per pair by the Kruskal key (weight, scan index).
 // Rule 2 compares the LIVE tree sets of the two components at the moment the
 // edge is reached, so the result depends on the order of merges; a plain
-// connected-components / Boruvka formulation is not equivalent.  We decide
-// the edges with deterministic reservations: one CTA per stereo pair walks
-// the sorted edge list in windows; every undecided window edge finds its two
-// roots and reserves both with an atomicMax of a (round, -position) stamp;
-// an edge that holds both reservations has no earlier pending edge touching
-// either tree, so its sequential outcome is already determined and it is
-// decided now (rule 2 + union).  Self-loops are dropped at once.  Undecided
-// edges are compacted (order preserved) in front of the next window.
+// connected-components / Boruvka formulation is not equivalent.  The default
+// kernel, k_grp, decides whole windows of 1023 edges per round, one CTA per
+// pair: the window's live edges and the roots they touch form conflict groups
+// (components in shared memory); groups touch disjoint trees, so each is
+// walked independently by one thread in Kruskal order against shared-memory
+// copies of its trees; merges are written back to the global union-find.
+// k_grp<true> adds the segment-tree criterion w <= min(Int(A) + k/|A|,
+// Int(B) + k/|B|) (hdp_segment_tree, tree kind "st").  k_dr, the earlier
+// deterministic-reservations kernel (an edge is decided once it holds the
+// reservation of both its roots), stays behind HDP_HDPF_DR=1 for diagnostics.
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -1,8 +1,9 @@
 """Disparity-aware spanning forests (drop-in for treestereo.hdp_forest).
 
 build_hdpf runs rule 1 + order-exact Kruskal with rule 2 on the GPU
-(deterministic reservations, hdpf.cu); plain_disparity_forest (beta = 0, full
-range) is exactly the MST and uses Boruvka."""
+(whole-window rounds by conflict groups, hdpf.cu k_grp; tree_kind "st" adds
+the segment-tree criterion); plain_disparity_forest (beta = 0, full range) is
+exactly the MST and uses Boruvka."""
 
 from __future__ import annotations
 
