@@ -19,11 +19,15 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "prims.cuh"
 
 namespace hdp {
+
+int run_boruvka(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev, const uint64_t* key,
+                uint8_t* in_tree, int32_t* comp, int* rounds_out, cudaStream_t st, int grid_h, int grid_w);
 
 __device__ __forceinline__ const uint32_t* pix_mask(const uint32_t* row_masks,
                                                    const int32_t* pixel_row, int32_t node,
@@ -695,6 +699,53 @@ __global__ void k_seg_remap(int batch, int64_t ms, const int32_t* __restrict__ s
     seg2[b] = s0 < ms ? pos[s0] : (ms > 0 ? pos[ms - 1] + flag[ms - 1] : 0);
 }
 
+// Static classification for the mask-homogeneous fast path (hdpf_run).
+// While every tree's set equals the pixel mask of each of its members, an
+// edge reached between two trees is accepted iff the endpoints' masks are
+// equal and non-empty (Jaccard 1 >= beta), and rejected otherwise -- unless
+// the masks differ, intersect and still pass rule 2 (inter / union >= beta,
+// the reference's float64 test): only such a "cross-pass" edge could ever
+// merge two different sets.  With no cross-pass edge in a pair, induction over
+// the Kruskal sequence keeps every tree homogeneous, so build_hdpf
+// (hdp_forest.py:185-201) accepts exactly the edges plain Kruskal accepts on
+// the equal-mask subgraph: its unique minimum spanning forest under the
+// (weight, index) keys.  Edges outside that subgraph become self-loops (u, u),
+// which Boruvka drops.
+__global__ void k_hdpf_classify(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
+                                const int32_t* __restrict__ pixel_row, const uint32_t* __restrict__ row_masks,
+                                int64_t npp, int64_t epp, int n_rows, int nw, double beta, int32_t* u2,
+                                int32_t* v2, int* cross) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const int32_t a = eu[e], b = ev[e];
+    const int ra = pixel_row[a], rb = pixel_row[b];
+    const int64_t pair = e / epp;
+    const uint32_t* ma = row_masks + (pair * n_rows + ra) * nw;
+    const uint32_t* mb = row_masks + (pair * n_rows + rb) * nw;
+    bool eq = true;
+    int inter = 0, uni = 0;
+    for (int i = 0; i < nw; i++) {
+        const uint32_t x = __ldg(ma + i), y = ra == rb ? x : __ldg(mb + i);
+        eq = eq && x == y;
+        inter += __popc(x & y);
+        uni += __popc(x | y);
+    }
+    const bool keep = eq && inter > 0;
+    if (!eq && inter > 0 && !(__ddiv_rn((double)inter, (double)uni) < beta)) atomicOr(cross + pair, 1);
+    u2[e] = a;
+    v2[e] = keep ? b : a;
+}
+
+// tree sets of the homogeneous forest: every node's own pixel mask
+__global__ void k_hdpf_node_masks(int64_t n, const int32_t* __restrict__ pixel_row,
+                                  const uint32_t* __restrict__ row_masks, int64_t npp, int n_rows, int nw,
+                                  uint32_t* tree_masks) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const uint32_t* pm = pix_mask(row_masks, pixel_row, (int32_t)v, npp, n_rows, nw);
+    for (int i = 0; i < nw; i++) tree_masks[v * nw + i] = pm[i];
+}
+
 __global__ void k_uf_final(int64_t n, int32_t* uf, int nw, const uint32_t* __restrict__ tm,
                            int32_t* comp, uint32_t* tree_masks) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -813,6 +864,33 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
     const int64_t n = (int64_t)batch * nodes_per_pair;
     const int64_t m = (int64_t)batch * edges_per_pair;
     const int B = 256;
+    const char* fe = getenv("HDP_HDPF_FAST");  // diagnostics / tests: 0 = always the window kernel
+    const bool fast_off = fe && fe[0] == '0';
+    if (st_k < 0.0 && !fast_off && m > 0) {
+        // mask-homogeneous fast path (k_hdpf_classify): exact whenever no pair
+        // has a cross-pass edge, which one flag read decides
+        DevBuf<int32_t> u2, v2;
+        DevBuf<int> cross;
+        HDP_TRY(u2.alloc(m, st));
+        HDP_TRY(v2.alloc(m, st));
+        HDP_TRY(cross.alloc(batch, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(cross.get(), 0, sizeof(int) * batch, st));
+        k_hdpf_classify<<<grid_for(m, B), B, 0, st>>>(m, eu, ev, pixel_row, row_masks, nodes_per_pair,
+                                                      edges_per_pair, n_rows, nw, beta, u2.get(), v2.get(),
+                                                      cross.get()); note_launch();
+        HDP_CHECK_LAUNCH();
+        std::vector<int> cr(batch, 0);
+        HDP_TRY(to_host(cr.data(), cross.get(), batch, st));
+        bool any = false;
+        for (int x : cr) any = any || x != 0;
+        if (!any) {
+            HDP_TRY(run_boruvka(n, m, u2.get(), v2.get(), key, in_tree, comp, rounds_out, st, 0, 0));
+            k_hdpf_node_masks<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
+                                                            tree_masks); note_launch();
+            HDP_CHECK_LAUNCH();
+            return HDP_OK;
+        }
+    }
     DevBuf<int32_t> uf, usz;
     DevBuf<uint32_t> tm;
     DevBuf<float> tint;

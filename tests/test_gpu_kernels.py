@@ -148,8 +148,14 @@ def _table(sizes, flat):
     return [flat[offs[i]:offs[i + 1]] for i in range(len(sizes))]
 
 
-def test_hdpf_exact():
+@pytest.mark.parametrize("fast", ["1", "0"])
+def test_hdpf_exact(fast, monkeypatch):
+    """Golden build_hdpf forests, through the mask-homogeneous fast path where it
+    applies (cases 0 and 2 have no cross-pass edge, 1 and 3 do and fall back to
+    the window kernel) and with the window kernel forced (HDP_HDPF_FAST=0)."""
     import torch
+
+    monkeypatch.setenv("HDP_HDPF_FAST", fast)
 
     from paper_1509_08197_b200 import engine as E
     from oracle import oracle as O
