@@ -736,6 +736,25 @@ __global__ void k_hdpf_classify(int64_t m, const int32_t* __restrict__ eu, const
     v2[e] = keep ? b : a;
 }
 
+// segment-tree pass 2 (homogeneous): an equal-mask edge (u2 != v2 after
+// k_hdpf_classify) joins the pass-1 roots of its endpoints
+__global__ void k_hdpf_relabel_roots(int64_t m, int32_t* uf, int32_t* u2, int32_t* v2) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const int32_t a = u2[e], b = v2[e];
+    if (a == b) return;
+    const int32_t ra = uf_find(uf, a), rb = uf_find(uf, b);
+    u2[e] = ra;
+    v2[e] = ra == rb ? ra : rb;
+}
+
+__global__ void k_hdpf_link_final(int64_t m, int64_t n, const uint8_t* __restrict__ t2, uint8_t* in_tree,
+                                  int32_t* uf, const int32_t* __restrict__ c2, int32_t* comp) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m && t2[i]) in_tree[i] = 1;
+    if (i < n) comp[i] = c2[uf_find(uf, (int32_t)i)];
+}
+
 // tree sets of the homogeneous forest: every node's own pixel mask
 __global__ void k_hdpf_node_masks(int64_t n, const int32_t* __restrict__ pixel_row,
                                   const uint32_t* __restrict__ row_masks, int64_t npp, int n_rows, int nw,
@@ -866,10 +885,14 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
     const int B = 256;
     const char* fe = getenv("HDP_HDPF_FAST");  // diagnostics / tests: 0 = always the window kernel
     const bool fast_off = fe && fe[0] == '0';
-    if (st_k < 0.0 && !fast_off && m > 0) {
-        // mask-homogeneous fast path (k_hdpf_classify): exact whenever no pair
-        // has a cross-pass edge, which one flag read decides
-        DevBuf<int32_t> u2, v2;
+    // mask-homogeneous fast path (k_hdpf_classify): exact whenever no pair has
+    // a cross-pass edge, which one flag read decides.  Plain HDPF: the whole
+    // forest is the MSF of the equal-mask subgraph.  Segment tree with rules
+    // (link): pass 1 (FH) keeps the trees homogeneous too, so pass 2 is the MSF
+    // of the equal-mask edges between pass-1 trees.
+    DevBuf<int32_t> u2, v2;
+    bool homog = false;
+    if ((st_k < 0.0 || link) && !fast_off && m > 0) {
         DevBuf<int> cross;
         HDP_TRY(u2.alloc(m, st));
         HDP_TRY(v2.alloc(m, st));
@@ -881,9 +904,9 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
         HDP_CHECK_LAUNCH();
         std::vector<int> cr(batch, 0);
         HDP_TRY(to_host(cr.data(), cross.get(), batch, st));
-        bool any = false;
-        for (int x : cr) any = any || x != 0;
-        if (!any) {
+        homog = true;
+        for (int x : cr) homog = homog && x == 0;
+        if (homog && st_k < 0.0) {
             HDP_TRY(run_boruvka(n, m, u2.get(), v2.get(), key, in_tree, comp, rounds_out, st, 0, 0));
             k_hdpf_node_masks<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
                                                             tree_masks); note_launch();
@@ -914,10 +937,26 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
         const int nb = std::min(kHdpfSlice, batch - b0);
         const int64_t e0 = (int64_t)b0 * edges_per_pair;
         HDP_TRY(hdpf_slice(nb, nodes_per_pair, edges_per_pair, eu + e0, ev + e0, key + e0, pixel_row, row_masks,
-                           n_rows, nw, beta, ew ? ew + e0 : nullptr, st_k, link, in_tree + e0, uf.get(), usz.get(),
-                           tm.get(), tint.get(), res.get(), rounds.get(), st));
+                           n_rows, nw, beta, ew ? ew + e0 : nullptr, st_k, link && !homog, in_tree + e0, uf.get(),
+                           usz.get(), tm.get(), tint.get(), res.get(), rounds.get(), st));
     }
-    k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks); note_launch();
+    if (homog) {
+        // segment tree, pass 2 on homogeneous pass-1 trees: Boruvka over the
+        // equal-mask edges relabelled to their pass-1 roots (edges inside a
+        // tree become self-loops), then comp = the linked component of the root
+        DevBuf<int32_t> c2;
+        DevBuf<uint8_t> t2;
+        HDP_TRY(c2.alloc(n, st));
+        HDP_TRY(t2.alloc(m, st));
+        k_hdpf_relabel_roots<<<grid_for(m, B), B, 0, st>>>(m, uf.get(), u2.get(), v2.get()); note_launch();
+        HDP_TRY(run_boruvka(n, m, u2.get(), v2.get(), key, t2.get(), c2.get(), nullptr, st, 0, 0));
+        k_hdpf_link_final<<<grid_for(std::max(m, n), B), B, 0, st>>>(m, n, t2.get(), in_tree, uf.get(), c2.get(),
+                                                                     comp); note_launch();
+        k_hdpf_node_masks<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
+                                                        tree_masks); note_launch();
+    } else {
+        k_uf_final<<<grid_for(n, B), B, 0, st>>>(n, uf.get(), nw, tm.get(), comp, tree_masks); note_launch();
+    }
     HDP_CHECK_LAUNCH();
     if (rounds_out) HDP_TRY(to_host(rounds_out, rounds.get(), 1, st));
     return HDP_OK;
