@@ -39,14 +39,18 @@ __device__ __forceinline__ const uint32_t* pix_mask(const uint32_t* row_masks,
 __global__ void k_rule1(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                         const uint64_t* __restrict__ key, const int32_t* __restrict__ pixel_row,
                         const uint32_t* __restrict__ row_masks, int64_t npp, int64_t epp,
-                        int n_rows, int nw, int32_t* flag, uint64_t* skey) {
+                        int n_rows, int nw, int32_t* flag, uint64_t* skey, const int32_t* __restrict__ keep_v2) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m) return;
     int32_t a = eu[e], b = ev[e];
-    const uint32_t* ma = pix_mask(row_masks, pixel_row, a, npp, n_rows, nw);
-    const uint32_t* mb = pix_mask(row_masks, pixel_row, b, npp, n_rows, nw);
     bool meet = false;
-    for (int i = 0; i < nw; i++) meet |= (ma[i] & mb[i]) != 0;
+    if (keep_v2) {  // mask-homogeneous: only the equal-mask edges can ever merge
+        meet = keep_v2[e] != a;
+    } else {
+        const uint32_t* ma = pix_mask(row_masks, pixel_row, a, npp, n_rows, nw);
+        const uint32_t* mb = pix_mask(row_masks, pixel_row, b, npp, n_rows, nw);
+        for (int i = 0; i < nw; i++) meet |= (ma[i] & mb[i]) != 0;
+    }
     flag[e] = meet ? 1 : 0;
     uint64_t k = key[e];
     uint64_t pair = (uint64_t)(e / epp);
@@ -407,8 +411,17 @@ __device__ __forceinline__ int grp_find_ro(const int32_t* p, int x) {
 // only when w <= min(Int(Ta) + k/|Ta|, Int(Tb) + k/|Tb|) (IEEE double, as
 // oracle/hdp_oracle.c or_hdpf_st); Int(T) = the largest edge inside T, kept
 // per root in `tint`.
-template <bool FH>
-__global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
+// MASKS = false: every tree keeps a single set that never changes (the
+// mask-homogeneous case, where the caller has already dropped every edge the
+// rules reject; or one interval row for all pixels): no sets are staged,
+// compared or merged.
+constexpr int kFhDivTab = 256;  // fh_k / s for sizes below this, from a table
+#ifndef HDP_GRP_MINB
+#define HDP_GRP_MINB 1
+#endif
+
+template <bool FH, bool MASKS>
+__global__ void __launch_bounds__(GW, HDP_GRP_MINB) k_grp(const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
                                             const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                                             int32_t* uf, int32_t* usz, uint32_t* tm, int nw, double beta,
                                             uint8_t* in_tree, int* rounds_out, const float* __restrict__ ew,
@@ -418,13 +431,18 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
     // rule 2 as an exact integer test: merge iff inter >= thr[uni], where thr[u]
     // is the least i with !(RN(i / u) < beta) (RN(i / u) is monotone in i)
     __shared__ int16_t thr[8 * 32 + 1];
+    __shared__ double kdiv[FH ? kFhDivTab : 1];  // FH: RN(fh_k / s), the oracle's division
     const int b = blockIdx.x, tid = threadIdx.x;
-    for (int u = tid; u <= 32 * nw; u += GW) {
-        int i = 0;
-        if (u > 0)
-            while (i <= u && __ddiv_rn((double)i, (double)u) < beta) i++;
-        thr[u] = (int16_t)i;
-    }
+    if (MASKS)
+        for (int u = tid; u <= 32 * nw; u += GW) {
+            int i = 0;
+            if (u > 0)
+                while (i <= u && __ddiv_rn((double)i, (double)u) < beta) i++;
+            thr[u] = (int16_t)i;
+        }
+    if (FH)
+        for (int i = tid; i < kFhDivTab; i += GW) kdiv[i] = i > 0 ? __ddiv_rn(fh_k, (double)i) : 0.0;
+    auto fh_tau = [&](int sz) -> double { return sz < kFhDivTab ? kdiv[sz] : __ddiv_rn(fh_k, (double)sz); };
     int32_t head = seg[b];
     const int32_t end = seg[b + 1];
     int round = 0;
@@ -484,7 +502,8 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
             s.dirty[sl] = 0;
             s.sz[sl] = usz[k];
             if (FH) s.sint[sl] = tint[k];
-            for (int i = 0; i < nw; i++) s.mask[sl * DR_NW + i] = tm[(int64_t)k * nw + i];
+            if (MASKS)
+                for (int i = 0; i < nw; i++) s.mask[sl * DR_NW + i] = tm[(int64_t)k * nw + i];
         }
         __syncthreads();
         int la = 0, lb = 0;
@@ -562,6 +581,7 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
             // memory only when the cached root changes
             int cr = -1, csz = 0;
             float ci = 0.0f;  // FH: Int of the cached root
+            double ctx = 0.0;  // FH: its threshold Int + k / size
             uint32_t cm[DR_NW];
             while (pos_n >= 0) {
                 n_g++;
@@ -581,31 +601,39 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                     if (cr >= 0) {
                         s.sz[cr] = csz;
                         if (FH) s.sint[cr] = ci;
-                        for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
+                        if (MASKS)
+                            for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
                     }
                     cr = x;
                     csz = s.sz[x];
-                    if (FH) ci = s.sint[x];
+                    if (FH) {
+                        ci = s.sint[x];
+                        ctx = (double)ci + fh_tau(csz);
+                    }
+                    if (MASKS) {
 #pragma unroll
-                    for (int i = 0; i < DR_NW; i++) cm[i] = i < nw ? s.mask[x * DR_NW + i] : 0u;
+                        for (int i = 0; i < DR_NW; i++) cm[i] = i < nw ? s.mask[x * DR_NW + i] : 0u;
+                    }
                 }
-                int inter = 0, uni = 0;
                 uint32_t my[DR_NW];
+                if (MASKS) {
+                    int inter = 0, uni = 0;
 #pragma unroll
-                for (int i = 0; i < DR_NW; i++) {
-                    my[i] = i < nw ? s.mask[y * DR_NW + i] : 0u;
-                    inter += __popc(cm[i] & my[i]);
-                    uni += __popc(cm[i] | my[i]);
+                    for (int i = 0; i < DR_NW; i++) {
+                        my[i] = i < nw ? s.mask[y * DR_NW + i] : 0u;
+                        inter += __popc(cm[i] & my[i]);
+                        uni += __popc(cm[i] | my[i]);
+                    }
+                    // rule 2 (hdp_forest.py:195) through the exact threshold table
+                    if (inter < thr[uni]) continue;
                 }
-                // rule 2 (hdp_forest.py:195) through the exact threshold table
-                if (inter < thr[uni]) continue;
                 const int ysz = s.sz[y];
                 float nint = 0.0f;
                 if (FH) {
                     const float wv = s.wt[pos];
                     const float iy = s.sint[y];
-                    const double tx = (double)ci + fh_k / (double)csz;
-                    const double ty = (double)iy + fh_k / (double)ysz;
+                    const double tx = ctx;  // (double)Int(x) + k / |x|, cached with the root
+                    const double ty = (double)iy + fh_tau(ysz);
                     if (!((double)wv <= (tx < ty ? tx : ty))) continue;
                     const float mi = ci > iy ? ci : iy;
                     nint = wv > mi ? wv : mi;
@@ -617,22 +645,30 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
                     s.mp[x] = y;
                     s.sz[y] = csz + ysz;
                     if (FH) s.sint[y] = nint;
+                    if (MASKS) {
 #pragma unroll
-                    for (int i = 0; i < DR_NW; i++)
-                        if (i < nw) s.mask[y * DR_NW + i] = cm[i] | my[i];
+                        for (int i = 0; i < DR_NW; i++)
+                            if (i < nw) s.mask[y * DR_NW + i] = cm[i] | my[i];
+                    }
                     cr = -1;  // x is absorbed: its cached state is not needed any more
                 } else {
                     s.mp[y] = x;
                     csz += ysz;
-                    if (FH) ci = nint;
+                    if (FH) {
+                        ci = nint;
+                        ctx = (double)ci + fh_tau(csz);
+                    }
+                    if (MASKS) {
 #pragma unroll
-                    for (int i = 0; i < DR_NW; i++) cm[i] |= my[i];
+                        for (int i = 0; i < DR_NW; i++) cm[i] |= my[i];
+                    }
                 }
             }
             if (cr >= 0) {
                 s.sz[cr] = csz;
                 if (FH) s.sint[cr] = ci;
-                for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
+                if (MASKS)
+                    for (int i = 0; i < nw; i++) s.mask[cr * DR_NW + i] = cm[i];
             }
 #ifdef HDP_DR_PROFILE
             if (n_g > g_maxrun) g_maxrun = n_g;
@@ -651,7 +687,8 @@ __global__ void __launch_bounds__(GW) k_grp(const int32_t* __restrict__ seg, con
             } else {
                 usz[k] = s.sz[sl];
                 if (FH) tint[k] = s.sint[sl];
-                for (int i = 0; i < nw; i++) tm[(int64_t)k * nw + i] = s.mask[sl * DR_NW + i];
+                if (MASKS)
+                    for (int i = 0; i < nw; i++) tm[(int64_t)k * nw + i] = s.mask[sl * DR_NW + i];
             }
         }
         __syncthreads();
@@ -791,7 +828,10 @@ static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, co
                       const uint64_t* key, const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
                       double beta, const float* ew, double st_k, bool link, uint8_t* in_tree, int32_t* uf,
                       int32_t* usz, uint32_t* tm, float* tint, unsigned long long* res, int* rounds,
-                      cudaStream_t st) {
+                      const int32_t* keep_v2, cudaStream_t st) {
+    // no set ever changes: one interval row, or homogeneous trees over the
+    // equal-mask edges (keep_v2)
+    const bool masks = !(keep_v2 || n_rows == 1);
     const int64_t m = (int64_t)nb * edges_per_pair;
     const int B = 256;
     DevBuf<int32_t> flag, pos, oidx, oidx2, seg;
@@ -802,7 +842,8 @@ static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, co
     int64_t ms = 0;
     if (m > 0) {
         k_rule1<<<grid_for(m, B), B, 0, st>>>(m, eu, ev, key, pixel_row, row_masks, nodes_per_pair,
-                                              edges_per_pair, n_rows, nw, flag.get(), skey.get()); note_launch();
+                                              edges_per_pair, n_rows, nw, flag.get(), skey.get(), keep_v2);
+        note_launch();
         HDP_TRY(exclusive_sum(flag.get(), pos.get(), m, st));
         int32_t a = 0, b2 = 0;
         HDP_TRY(to_host(&a, pos.get() + m - 1, 1, st));
@@ -835,9 +876,10 @@ static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, co
     }
     constexpr size_t g_smem = sizeof(GrpSmem);
     if (st_k >= 0.0) {
-        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-        k_grp<true><<<nb, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf, usz, tm, nw, beta, in_tree, rounds,
-                                            ew, tint, st_k); note_launch();
+        auto kern = masks ? k_grp<true, true> : k_grp<true, false>;
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+        kern<<<nb, GW, g_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf, usz, tm, nw, beta, in_tree, rounds, ew, tint,
+                                     st_k); note_launch();
     }
     const int32_t* order2 = oidx2.get();
     const int32_t* seg2p = seg.get();
@@ -858,9 +900,10 @@ static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, co
         seg2p = seg2.get();
     }
     if (st_k < 0.0 || link) {
-        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_grp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-        k_grp<false><<<nb, GW, g_smem, st>>>(seg2p, order2, eu, ev, uf, usz, tm, nw, beta, in_tree, rounds, nullptr,
-                                             nullptr, -1.0); note_launch();
+        auto kern = masks ? k_grp<false, true> : k_grp<false, false>;
+        HDP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+        kern<<<nb, GW, g_smem, st>>>(seg2p, order2, eu, ev, uf, usz, tm, nw, beta, in_tree, rounds, nullptr, nullptr,
+                                     -1.0); note_launch();
     }
     HDP_CHECK_LAUNCH();
     return HDP_OK;
@@ -938,7 +981,8 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
         const int64_t e0 = (int64_t)b0 * edges_per_pair;
         HDP_TRY(hdpf_slice(nb, nodes_per_pair, edges_per_pair, eu + e0, ev + e0, key + e0, pixel_row, row_masks,
                            n_rows, nw, beta, ew ? ew + e0 : nullptr, st_k, link && !homog, in_tree + e0, uf.get(),
-                           usz.get(), tm.get(), tint.get(), res.get(), rounds.get(), st));
+                           usz.get(), tm.get(), tint.get(), res.get(), rounds.get(), homog ? v2.get() + e0 : nullptr,
+                           st));
     }
     if (homog) {
         // segment tree, pass 2 on homogeneous pass-1 trees: Boruvka over the

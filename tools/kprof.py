@@ -61,3 +61,13 @@ s = sum(tot.values())
 print(f"kernel time sum {s / reps / 1e3:.2f} ms per step, {sum(cnt.values()) // reps} launches per step")
 for k, v in sorted(tot.items(), key=lambda x: -x[1])[:40]:
     print(f"  {v / reps / 1e3:9.3f} ms {100 * v / s:5.1f}% {cnt[k] // reps:5d}  {k}")
+if os.environ.get("KPROF_TIMELINE"):
+    pat = os.environ["KPROF_TIMELINE"].split(",")
+    evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    t0 = min(e.time_range.start for e in evs)
+    print("timeline (ms from first kernel): start end dur name")
+    for e in sorted(evs, key=lambda e: e.time_range.start):
+        if any(p in e.name for p in pat):
+            print(f"  {(e.time_range.start - t0) / 1e3:9.3f} {(e.time_range.end - t0) / 1e3:9.3f} "
+                  f"{(e.time_range.end - e.time_range.start) / 1e3:8.3f}  {e.name[:60]}")
+    print(f"  last kernel end {(max(e.time_range.end for e in evs) - t0) / 1e3:.3f}")
