@@ -1580,6 +1580,33 @@ static int join_side(const SideStream* ss, cudaStream_t st) {
     HDP_CHECK_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
     return HDP_OK;
 }
+// one phase's chunks, small class then big class (forest.cu k_chunk_split)
+template <typename G>
+static int up_chunks(const AggArgs& sh, const hdp_forest* f, int64_t r, const G& cgrid, bool both, size_t ssmem,
+                     size_t csmem, cudaStream_t s) {
+    const int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0, nb = f->chunk_big[r], ns = nc - nb;
+    if (ns > 0) {
+        k_up_chunk<<<cgrid(ns, both), kChunkThreads, ssmem, s>>>(sh, f->chunk_desc.get(), c0, ns); note_launch();
+    }
+    if (nb > 0) {
+        k_up_chunk<<<cgrid(nb, both), kChunkThreads, csmem, s>>>(sh, f->chunk_desc.get(), c0 + ns, nb); note_launch();
+    }
+    return HDP_OK;
+}
+template <typename G>
+static int down_chunks(const AggArgs& sh, const hdp_forest* f, int64_t r, const G& cgrid, bool both, size_t ssmem,
+                       size_t csmem, cudaStream_t s) {
+    const int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0, nb = f->chunk_big[r], ns = nc - nb;
+    if (ns > 0) {
+        k_down_chunk<<<cgrid(ns, both), kChunkThreads, ssmem, s>>>(sh, f->chunk_desc.get(), c0, ns); note_launch();
+    }
+    if (nb > 0) {
+        k_down_chunk<<<cgrid(nb, both), kChunkThreads, csmem, s>>>(sh, f->chunk_desc.get(), c0 + ns, nb);
+        note_launch();
+    }
+    return HDP_OK;
+}
+
 static int fork_hi(const SideStream* ss) {  // after fork_side: the fork event is recorded
     HDP_CHECK_CUDA(cudaStreamWaitEvent(ss->hi, ss->fork, 0));
     return HDP_OK;
@@ -1842,6 +1869,9 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     pc.mark("ecost", 0, 0);
     const bool chunks = f->chunks_ok != 0;
     const size_t csmem = (size_t)((f->chunk_words + 3) & ~3ll) * sizeof(float);
+    // the small-chunk class (forest.cuh kChunkSmallWords) launches with less
+    // shared memory, so more of its CTAs are resident
+    const size_t ssmem = std::min(csmem, (size_t)kChunkSmallWords * sizeof(float));
     sh.lc_rowoff = f->lc_rowoff.get();
     sh.auxd = f->auxd.get();
     if (chunks && csmem > 48 * 1024) {
@@ -1881,8 +1911,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         const bool side = chunks && nc > 0 && (np > 0 || ng > 0);
         if (side) {
             HDP_TRY(fork_side(ss, st));
-            k_up_chunk<<<cgrid(nc, ng > 0), kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0, nc);
-            note_launch();
+            HDP_TRY(up_chunks(sh, f, r, cgrid, ng > 0, ssmem, csmem, ss->s));
         }
         if (np > 0) {
             k_light<<<grid_for(np << a.qsub_shift, 256), 256, 0, st>>>(a, p0, np); note_launch();
@@ -1898,7 +1927,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         if (side) {
             HDP_TRY(join_side(ss, st));
         } else if (chunks && nc > 0) {
-            k_up_chunk<<<cgrid(nc, false), kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
+            HDP_TRY(up_chunks(sh, f, r, cgrid, false, ssmem, csmem, st));
         } else if (!chunks && ns > 0) {
             k_scan_up_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }
@@ -1911,8 +1940,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         const bool side = chunks && nc > 0 && ng > 0;
         if (side) {
             HDP_TRY(fork_side(ss, st));
-            k_down_chunk<<<cgrid(nc, ng > 0), kChunkThreads, csmem, ss->s>>>(sh, f->chunk_desc.get(), c0, nc);
-            note_launch();
+            HDP_TRY(down_chunks(sh, f, r, cgrid, ng > 0, ssmem, csmem, ss->s));
         }
         if (ng > 0) {
             const bool hp = side && seg_prio;
@@ -1925,7 +1953,7 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
         if (side) {
             HDP_TRY(join_side(ss, st));
         } else if (chunks && nc > 0) {
-            k_down_chunk<<<cgrid(nc, false), kChunkThreads, csmem, st>>>(sh, f->chunk_desc.get(), c0, nc); note_launch();
+            HDP_TRY(down_chunks(sh, f, r, cgrid, false, ssmem, csmem, st));
         } else if (!chunks && ns > 0) {
             k_down_short<<<grid_for(ns * sh.sub, 256), 256, 0, st>>>(sh, s0, ns); note_launch();
         }

@@ -1457,6 +1457,7 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
         d.mqu = mq;
         d.inv = mq > 1 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
         words = (unsigned long long)(W[p1] - W[p0]);
+        d.pad0 = (int)words;
     }
     if (live) desc[c] = d;
     // one atomic per warp (a same-address atomic per chunk serialised in L2)
@@ -1464,6 +1465,32 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
     if ((threadIdx.x & 31) == 0 && words) atomicMax(max_words, words);
 }
 
+// chunk size classes: big[c] = the chunk needs more than kChunkSmallWords
+__global__ void k_chunk_big_flags(int64_t nc, const ChunkDesc* __restrict__ desc, int32_t* big) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < nc) big[c] = desc[c].pad0 + 64 > kChunkSmallWords ? 1 : 0;
+}
+
+// stable partition of every phase's chunks: small ones first, then big ones
+// (bpos = exclusive scan of the big flags); nbig[r] = big chunks of phase r
+__global__ void k_chunk_split(int64_t nc, int nph, const int64_t* __restrict__ cbase,
+                              const int32_t* __restrict__ bpos, const ChunkDesc* __restrict__ in, ChunkDesc* out,
+                              int64_t* nbig) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < nph) nbig[c] = bpos[cbase[c + 1]] - bpos[cbase[c]];
+    if (c >= nc) return;
+    int lo = 0, hi = nph - 1;  // phase r with cbase[r] <= c < cbase[r + 1]
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cbase[mid] <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    const int64_t b0 = bpos[cbase[lo]], nb = bpos[cbase[lo + 1]] - b0;
+    const int64_t ns = cbase[lo + 1] - cbase[lo] - nb;
+    const int64_t lb = bpos[c] - b0, ls = (c - cbase[lo]) - lb;
+    const bool isbig = bpos[c + 1] != bpos[c];
+    out[cbase[lo] + (isbig ? ns + lb : ls)] = in[c];
+}
 }  // namespace hdp
 
 // chunk table of the short-path blocks (needs lmeta, lc rows and short_rows);
@@ -1521,14 +1548,51 @@ static int build_chunks(hdp_forest* f) {
                                                       f->lc_rowoff.get(), f->auxd.get(), W.get(),
                                                       f->chunk_desc.get(), mx.get()); note_launch();
     HDP_CHECK_LAUNCH();
-    std::vector<int64_t> h(nph + 2);
+    // size classes (k_chunk_split): the chunk count is only known on the
+    // device, so the class passes run over the bound ncap
+    DevBuf<int32_t> bflag, bpos;
+    DevBuf<ChunkDesc> split;
+    DevBuf<int64_t> nbig;
+    HDP_TRY(bflag.alloc(ncap + 1, st));
+    HDP_TRY(bpos.alloc(ncap + 1, st));
+    HDP_TRY(split.alloc(ncap + 1, st));
+    HDP_TRY(nbig.alloc(nph + 1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(bflag.get(), 0, sizeof(int32_t) * (ncap + 1), st));
+    k_chunk_big_flags<<<grid_for(ncap, 256), 256, 0, st>>>(ncap, f->chunk_desc.get(), bflag.get()); note_launch();
+    HDP_TRY(exclusive_sum(bflag.get(), bpos.get(), ncap + 1, st));
+    k_chunk_split<<<grid_for(std::max<int64_t>(ncap, nph), 256), 256, 0, st>>>(
+        ncap, nph, cbase.get(), bpos.get(), f->chunk_desc.get(), split.get(), nbig.get()); note_launch();
+    HDP_CHECK_LAUNCH();
+    std::vector<int64_t> h(nph + 2), hb(nph + 1);
     HDP_CHECK_CUDA(cudaMemcpyAsync(h.data(), cbase.get(), sizeof(int64_t) * (nph + 1), cudaMemcpyDeviceToHost, st));
     HDP_CHECK_CUDA(cudaMemcpyAsync(h.data() + nph + 1, mx.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HDP_CHECK_CUDA(cudaMemcpyAsync(hb.data(), nbig.get(), sizeof(int64_t) * nph, cudaMemcpyDeviceToHost, st));
     HDP_CHECK_CUDA(cudaStreamSynchronize(st));
+    f->chunk_desc = std::move(split);  // the partitioned table (chunks past the count are never read)
+    f->chunk_big.assign(hb.begin(), hb.begin() + nph);
     HDP_REQUIRE(h[nph] <= ncap, HDP_ERR_INTERNAL, "chunk count %lld above its bound %lld", (long long)h[nph],
                 (long long)ncap);
     f->chunk_off.assign(h.begin(), h.begin() + nph + 1);
     f->chunk_words = h[nph] > 0 ? h[nph + 1] + 64 : 0;
+    if (getenv("HDP_CHUNK_STATS")) {  // diagnostics: chunk weight histogram
+        std::vector<ChunkDesc> hd(h[nph]);
+        std::vector<int64_t> hw(ns + 1);
+        HDP_CHECK_CUDA(cudaMemcpyAsync(hd.data(), f->chunk_desc.get(), sizeof(ChunkDesc) * h[nph],
+                                       cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(hw.data(), W.get(), sizeof(int64_t) * (ns + 1), cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaStreamSynchronize(st));
+        int64_t hist[12] = {0};
+        double tot = 0;
+        for (const ChunkDesc& d : hd) {
+            const int64_t w = hw[d.p0 + d.np] - hw[d.p0];
+            tot += (double)w;
+            hist[std::min<int64_t>(11, w >> 11)]++;
+        }
+        fprintf(stderr, "[chunks] %lld chunks, mean %.0f words, max %lld; per 2K words:", (long long)h[nph],
+                tot / std::max<int64_t>(1, h[nph]), (long long)h[nph + 1]);
+        for (int i = 0; i < 12; i++) fprintf(stderr, " %lld", (long long)hist[i]);
+        fprintf(stderr, "\n");
+    }
     // rows of up to 32 float4 lanes: one lane group spans a row; wider rows
     // take the per-path kernels (lane groups across CTAs)
     f->chunks_ok = f->chunk_words <= kChunkMaxWords;

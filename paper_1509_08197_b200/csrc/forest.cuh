@@ -30,6 +30,14 @@ namespace hdp {
 constexpr int kChunkShift = HDP_CHUNK_SHIFT;
 constexpr int kChunkWords = 1 << kChunkShift;
 constexpr int kChunkMaxWords = 48 * 1024;  // 192 KB of shared memory per chunk
+// Chunks are launched in two classes per phase: at most kChunkSmallWords
+// (most of them; five CTAs per SM fit) and the rest with the largest chunk's
+// shared memory.  The window scheme makes a chunk kChunkWords plus at most one
+// path, so one size for all would cap residency by the rare heavy chunk.
+#ifndef HDP_CHUNK_SMALL
+#define HDP_CHUNK_SMALL (10 * 1024)
+#endif
+constexpr int kChunkSmallWords = HDP_CHUNK_SMALL;
 
 struct alignas(16) ChunkDesc {
     int p0, np;        // short-path list range
@@ -125,6 +133,7 @@ struct hdp_forest {
     hdp::DevBuf<int64_t> lc_rowoff;  // per light-child entry: prefix of m (aux row offsets, up pass)
     hdp::DevBuf<int64_t> auxd;       // per short path: prefix of m over paths with a parent (down pass)
     std::vector<int64_t> chunk_off;  // host: chunks of phase r = [chunk_off[r], chunk_off[r+1])
+    std::vector<int64_t> chunk_big;  // host: of those, the last chunk_big[r] exceed kChunkSmallWords
     int64_t chunk_words = 0;         // shared-memory words the largest chunk needs
     int chunks_ok = 0;               // chunks fit in shared memory
 
