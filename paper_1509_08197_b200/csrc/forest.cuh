@@ -9,7 +9,7 @@
 // Heavy paths of at most this many nodes are aggregated register-resident
 // (one thread per (path, lane)); longer ones by a warp walking staged chunks.
 #ifndef HDP_SHORT_PATH
-#define HDP_SHORT_PATH 8
+#define HDP_SHORT_PATH 12
 #endif
 constexpr int kShortPath = HDP_SHORT_PATH;
 // Long paths are cut into segments of kSeg nodes, one warp each, chained by
