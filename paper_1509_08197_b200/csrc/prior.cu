@@ -296,7 +296,10 @@ __device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, in
 }
 
 template <int W7>
-__global__ void __launch_bounds__(256, 2) k_prior(PriorArgs a, int batch) {
+#ifndef HDP_PRIOR_MINB
+#define HDP_PRIOR_MINB 3
+#endif
+__global__ void __launch_bounds__(256, HDP_PRIOR_MINB) k_prior(PriorArgs a, int batch) {
     const int64_t per = (int64_t)a.nrc * a.ncc;
     const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
     __shared__ double4 win[kPriorWarps][49];  // the 7 x 7 path's staged window, per warp
