@@ -713,14 +713,21 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
     clock.lap("pyramid")
     outs: list[LevelOut] = []
     early = {}
-    if prior_stream is not None:
-        prior_stream.wait_stream(torch.cuda.current_stream())  # the levels' planes
+
+    def launch_prior(level):
+        # the prior of `level` on the side stream, started once everything
+        # queued so far on the level stream has run: called right after the
+        # coarser level's forest (the window kernel of the segment tree needs
+        # whole SMs, which a running prior grid would keep busy), so it
+        # overlaps that level's tree build and aggregation
+        if prior_stream is None or level < 0:
+            return
+        prior_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(prior_stream):
-            for level in range(levels - 1, -1, -1):
-                c_, k_ = prior_counts(lv[level], cost=cost, max_ctas=PRIOR_SIDE_CTAS)
-                ev = torch.cuda.Event()
-                ev.record(prior_stream)
-                early[level] = (c_, k_, ev)
+            c_, k_ = prior_counts(lv[level], cost=cost, max_ctas=PRIOR_SIDE_CTAS)
+            ev_ = torch.cuda.Event()
+            ev_.record(prior_stream)
+            early[level] = (c_, k_, ev_)
 
     def finish(lev, f, disp, mc, vol, clk):
         ntrees, stored, ratio = _per_pair_stats(f, b, lev.h * lev.w, lev.d_max)
@@ -740,6 +747,7 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
     else:
         key = level_keys(top.img_l, E, levels, block_size, key)
     in_tree, comp, _ = plain_tree(tree_kind, b, top.h, top.w, eu, ev, ew, key, st_k)
+    launch_prior(levels - 1)
     f, disp, mc, _, vol = _forest_layer(top, eu, ev, ew, in_tree, comp, gamma, cost, None,
                                         want_volume=want_volume, clock=clock)
     o = finish(top, f, disp, mc, vol, clock)
@@ -770,6 +778,7 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
         in_tree, comp, tmasks, rounds = hdpf(b, lev.h * lev.w, E, eu, ev, key, rows,
                                              row_masks.contiguous(), beta, ew=ew,
                                              st_k=st_k if tree_kind == "st" else -1.0)
+        launch_prior(level - 1)
         fo = DeviceForest(b * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
         fo.set_lanes_nodes(tmasks.contiguous())
         disp, mc, _, vol = _aggregate_timed(fo, lev, cost, lclock, want_volume=want_volume)
