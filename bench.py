@@ -443,7 +443,7 @@ class Runner:
             "config": config_dict(name, self.world, B),
             "e2e": {"value": units * steps / t_e2e / 1e9, "unit": "Gpd/s",
                     "h2d_bytes_per_step": int(Lh.nbytes + Rh.nbytes),
-                    "d2h_bytes_per_step": int(B * H * W * 4 * 2),
+                    "d2h_bytes_per_step": int(B * H * W * (4 + 8)),  # int32 disparity + float64 min cost
                     "path": "aggregation.run_baseline_pipeline_batch (StereoPair list in, "
                             "PipelineResult list out)" if not slabs else
                             "pinned staging + distributed.run_slab_baseline + D2H"},

@@ -706,7 +706,10 @@ __device__ __forceinline__ float seg_pick(float lo, float past, int i) {
     return i < 32 ? l : past;
 }
 
-constexpr int kSegWarps = 4;  // segment warps per CTA
+#ifndef HDP_SEG_WARPS
+#define HDP_SEG_WARPS 4
+#endif
+constexpr int kSegWarps = HDP_SEG_WARPS;  // segment warps per CTA
 
 // A segment's rows for this warp's column group: with one group (rows of at
 // most 128 floats) the segment is one contiguous span of the row layout and
