@@ -39,7 +39,8 @@ __device__ __forceinline__ const uint32_t* pix_mask(const uint32_t* row_masks,
 __global__ void k_rule1(int64_t m, const int32_t* __restrict__ eu, const int32_t* __restrict__ ev,
                         const uint64_t* __restrict__ key, const int32_t* __restrict__ pixel_row,
                         const uint32_t* __restrict__ row_masks, int64_t npp, int64_t epp,
-                        int n_rows, int nw, int32_t* flag, uint64_t* skey, const int32_t* __restrict__ keep_v2) {
+                        int n_rows, int nw, int32_t* flag, uint64_t* skey, const int32_t* __restrict__ keep_v2,
+                        int32_t* nonstd) {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m) return;
     int32_t a = eu[e], b = ev[e];
@@ -54,6 +55,10 @@ __global__ void k_rule1(int64_t m, const int32_t* __restrict__ eu, const int32_t
     flag[e] = meet ? 1 : 0;
     uint64_t k = key[e];
     uint64_t pair = (uint64_t)(e / epp);
+    // keys whose low 24 bits are the edge's index in its pair (hdp_grid_edges,
+    // rank keys) let the sort skip those bits: it is stable and its input is
+    // in edge order
+    if ((k & 0xffffffull) != (uint64_t)(e - (int64_t)pair * epp)) *nonstd = 1;
     // (pair, weight bits, scan index): weights are non-negative floats < 2^31
     skey[e] = (pair << 55) | ((k >> 32) << 24) | (k & 0xffffffull);
 }
@@ -832,23 +837,30 @@ static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, co
     // no set ever changes: one interval row, or homogeneous trees over the
     // equal-mask edges (keep_v2)
     const bool masks = !(keep_v2 || n_rows == 1);
+    bool std_keys = false;
     const int64_t m = (int64_t)nb * edges_per_pair;
     const int B = 256;
-    DevBuf<int32_t> flag, pos, oidx, oidx2, seg;
+    DevBuf<int32_t> flag, pos, oidx, oidx2, seg, nonstd;
     DevBuf<uint64_t> skey, okey, okey2;
+    HDP_TRY(nonstd.alloc(1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(nonstd.get(), 0, sizeof(int32_t), st));
     HDP_TRY(flag.alloc(m + 1, st));
     HDP_TRY(pos.alloc(m + 1, st));
     HDP_TRY(skey.alloc(m + 1, st));
     int64_t ms = 0;
     if (m > 0) {
         k_rule1<<<grid_for(m, B), B, 0, st>>>(m, eu, ev, key, pixel_row, row_masks, nodes_per_pair,
-                                              edges_per_pair, n_rows, nw, flag.get(), skey.get(), keep_v2);
+                                              edges_per_pair, n_rows, nw, flag.get(), skey.get(), keep_v2,
+                                              nonstd.get());
         note_launch();
         HDP_TRY(exclusive_sum(flag.get(), pos.get(), m, st));
-        int32_t a = 0, b2 = 0;
-        HDP_TRY(to_host(&a, pos.get() + m - 1, 1, st));
-        HDP_TRY(to_host(&b2, flag.get() + m - 1, 1, st));
+        int32_t a = 0, b2 = 0, ns = 0;
+        HDP_CHECK_CUDA(cudaMemcpyAsync(&a, pos.get() + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(&b2, flag.get() + m - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaMemcpyAsync(&ns, nonstd.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        HDP_CHECK_CUDA(cudaStreamSynchronize(st));
         ms = (int64_t)a + b2;
+        std_keys = ns == 0;
     }
     HDP_TRY(okey.alloc(ms + 1, st));
     HDP_TRY(okey2.alloc(ms + 1, st));
@@ -861,7 +873,14 @@ static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, co
     flag.release();
     pos.release();
     skey.release();
-    HDP_TRY(sort_pairs(okey.get(), okey2.get(), oidx.get(), oidx2.get(), ms, 0, 63, st));
+    {
+        // (pair, weight, index) keys: with standard keys the index bits are
+        // implied by the (stable) sort's input order, and only the pair bits
+        // the slice uses are sorted
+        int pb = 0;
+        while ((1 << pb) < nb) pb++;
+        HDP_TRY(sort_pairs(okey.get(), okey2.get(), oidx.get(), oidx2.get(), ms, std_keys ? 24 : 0, 55 + pb, st));
+    }
     k_seg_bounds<<<grid_for(ms + 1, B), B, 0, st>>>(ms, okey2.get(), nb, seg.get()); note_launch();
     HDP_CHECK_LAUNCH();
     const char* alg = getenv("HDP_HDPF_DR");  // diagnostics: the reservation kernel instead of groups

@@ -42,6 +42,20 @@ __global__ void k_pack_px(const double* __restrict__ u, const double* __restrict
     out[n + i] = make_double2(c > 2 ? u[i * c + 2] : 0.0, g[i]);
 }
 
+// 3 channels, two pixels per thread with 16-byte loads and stores (the planes
+// are 16-byte aligned: cudaMalloc'd / torch tensors); n even
+__global__ void k_pack_px3(const double2* __restrict__ u, const double2* __restrict__ g, int64_t n2,
+                           double2* __restrict__ out, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n2) return;
+    const double2 a = __ldg(u + 3 * i), b = __ldg(u + 3 * i + 1), c = __ldg(u + 3 * i + 2), gg = __ldg(g + i);
+    // pixel 2i: (a.x, a.y, b.x), pixel 2i + 1: (b.y, c.x, c.y)
+    out[2 * i] = make_double2(a.x, a.y);
+    out[2 * i + 1] = make_double2(b.y, c.x);
+    out[n + 2 * i] = make_double2(b.x, gg.x);
+    out[n + 2 * i + 1] = make_double2(c.y, gg.y);
+}
+
 // RN(x / b) for b > 0 given y = RN(1 / b): q = RN(x y) is within one ulp of
 // x / b, the remainder r = x - q b is exact in one FMA, and RN(q + r y) is the
 // correctly rounded quotient (Markstein's theorem; no overflow or underflow
@@ -436,8 +450,17 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
     if (window == 7) {
         const int64_t n = a.plane;
         HDP_TRY(pk.alloc(4 * n, st));
-        k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk.get()); note_launch();
-        k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk.get() + 2 * n); note_launch();
+        const bool v2 = c == 3 && n % 2 == 0 && ((uintptr_t)unit_l | (uintptr_t)grad_l | (uintptr_t)unit_r |
+                                                 (uintptr_t)grad_r) % 16 == 0;
+        if (v2) {
+            k_pack_px3<<<grid_for(n / 2, 256), 256, 0, st>>>((const double2*)unit_l, (const double2*)grad_l, n / 2,
+                                                            pk.get(), n); note_launch();
+            k_pack_px3<<<grid_for(n / 2, 256), 256, 0, st>>>((const double2*)unit_r, (const double2*)grad_r, n / 2,
+                                                            pk.get() + 2 * n, n); note_launch();
+        } else {
+            k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk.get()); note_launch();
+            k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk.get() + 2 * n); note_launch();
+        }
         a.pl = pk.get();
         a.pr = pk.get() + 2 * n;
     }
