@@ -146,10 +146,15 @@ int hdp_assign_rows(const int32_t *parent_disp, int batch, int ph, int pw, int h
 
 /* build_hdpf (hdp_forest.py:151-216): rule 1 (disjoint pixel sets drop the
  * edge), then Kruskal order (key) with rule 2 (Jaccard of the LIVE tree sets
- * >= beta, IEEE double division), decided exactly by whole-window rounds:
- * one CTA per pair takes the next 1023 edges of its sorted list, splits their
- * live edges into conflict groups (edges sharing a tree) and walks every group
- * in Kruskal order with one thread.  row_masks: (B, n_rows, nw) u32 bitsets;
+ * >= beta, IEEE double division).  Exact fast path: when no edge of the batch
+ * is "cross-pass" (endpoint masks differ, intersect and pass rule 2
+ * statically), every tree keeps one pixel mask and the forest is the MSF of
+ * the equal-mask edges (Boruvka).  Otherwise, decided exactly by whole-window
+ * rounds: one CTA per pair takes the next 1023 edges of its sorted list,
+ * splits their live edges into conflict groups (edges sharing a tree) and
+ * walks every group in Kruskal order with one thread.  Keys: (weight or rank
+ * bits << 32 | index of the edge in its pair); the low 24 bits break ties.
+ * row_masks: (B, n_rows, nw) u32 bitsets;
  * pixel_row per node.  Outputs in_tree[e], comp[v] (representative),
  * tree_masks (n_nodes, nw): the final tree set, valid at every node.
  * st_k >= 0 builds the segment-tree variant (tree_kind "st", which the

@@ -4,9 +4,12 @@
 // Rule 1 (pixel sets disjoint -> drop) is a static per-edge filter; the
 // survivors are sorted per pair by the Kruskal key (weight, scan index).
 // Rule 2 compares the LIVE tree sets of the two components at the moment the
-// edge is reached, so the result depends on the order of merges; a plain
-// connected-components / Boruvka formulation is not equivalent.  The default
-// kernel, k_grp, decides whole windows of 1023 edges per round, one CTA per
+// edge is reached, so the result depends on the order of merges; in general a
+// plain connected-components / Boruvka formulation is not equivalent.  It is
+// when no edge is "cross-pass" (k_hdpf_classify): then every tree keeps one
+// pixel mask and the forest is the MSF of the equal-mask edges -- the fast
+// path hdpf_run takes after one flag read.  The general kernel, k_grp,
+// decides whole windows of 1023 edges per round, one CTA per
 // pair: the window's live edges and the roots they touch form conflict groups
 // (components in shared memory); groups touch disjoint trees, so each is
 // walked independently by one thread in Kruskal order against shared-memory

@@ -1,9 +1,11 @@
 """Disparity-aware spanning forests (drop-in for treestereo.hdp_forest).
 
-build_hdpf runs rule 1 + order-exact Kruskal with rule 2 on the GPU
-(whole-window rounds by conflict groups, hdpf.cu k_grp; tree_kind "st" adds
-the segment-tree criterion); plain_disparity_forest (beta = 0, full range) is
-exactly the MST and uses Boruvka."""
+build_hdpf runs rule 1 + order-exact Kruskal with rule 2 on the GPU: when no
+edge's endpoint masks differ, intersect and pass rule 2 statically, every tree
+keeps one pixel mask and the forest is the MSF of the equal-mask edges
+(Boruvka); otherwise whole-window rounds by conflict groups (hdpf.cu k_grp;
+tree_kind "st" adds the segment-tree criterion).  plain_disparity_forest
+(beta = 0, full range) is exactly the MST and uses Boruvka."""
 
 from __future__ import annotations
 
