@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--skip-hdp", action="store_true")
     ap.add_argument("--skip-dense", action="store_true")
+    ap.add_argument("--tree", default="mst")
     a = ap.parse_args()
     spec = CONFIGS[a.config]
     t = time.time()
@@ -53,7 +54,7 @@ def main():
             torch.cuda.synchronize()
             t = time.perf_counter()
             outs = E.run_hdp_batch(L, R, spec.d_max, model, levels=a.levels, delta0=d0, beta=beta,
-                                   timing=True)
+                                   timing=True, tree_kind=a.tree)
             torch.cuda.synchronize()
             tot = time.perf_counter() - t
             print(f"hdp rep{rep}: total {tot*1e3:.2f} ms", flush=True)
