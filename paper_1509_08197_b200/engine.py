@@ -372,6 +372,9 @@ def pack_masks(chosen) -> np.ndarray:
 
 # CTAs of the early (side-stream) prior launches; 0 = one warp per centre, uncapped
 PRIOR_SIDE_CTAS = int(os.environ.get("HDP_PRIOR_SIDE_CTAS", "0"))
+_PRIOR_EARLY_ENV = os.environ.get("HDP_PRIOR_EARLY", "")
+PRIOR_SIDE = os.environ.get("HDP_PRIOR_SIDE", "1") != "0"  # diagnostics: 0 = priors inline on the level stream
+PRIOR_EARLY = _PRIOR_EARLY_ENV == "1"
 
 
 def prior_counts(lev: Level, stride=5, window=7, max_offset=1, cost: CostConsts = CostConsts(),
@@ -678,7 +681,7 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     with torch.cuda.stream(hi):
         outs = _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, delta0,
                                beta, cost, tree_kind, seed, teacher, keep, want_volume, timing,
-                               on_level, prior_stream=pri, st_k=st_k)
+                               on_level, prior_stream=pri if PRIOR_SIDE else None, st_k=st_k)
     caller.wait_stream(hi)
     for o in outs:
         o.disparity.record_stream(caller)
@@ -746,8 +749,15 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
         key = rt_keys(E, b, seed, top.img_l.device)
     else:
         key = level_keys(top.img_l, E, levels, block_size, key)
+    # every prior at once before the top level, unless the segment tree's
+    # window kernel (needs whole SMs) would be starved by a running prior grid
+    prior_first = (tree_kind != "st") if _PRIOR_EARLY_ENV == "" else PRIOR_EARLY
+    if prior_first:
+        for level in range(levels - 1, -1, -1):
+            launch_prior(level)
     in_tree, comp, _ = plain_tree(tree_kind, b, top.h, top.w, eu, ev, ew, key, st_k)
-    launch_prior(levels - 1)
+    if not prior_first:
+        launch_prior(levels - 1)
     f, disp, mc, _, vol = _forest_layer(top, eu, ev, ew, in_tree, comp, gamma, cost, None,
                                         want_volume=want_volume, clock=clock)
     o = finish(top, f, disp, mc, vol, clock)
@@ -778,7 +788,8 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
         in_tree, comp, tmasks, rounds = hdpf(b, lev.h * lev.w, E, eu, ev, key, rows,
                                              row_masks.contiguous(), beta, ew=ew,
                                              st_k=st_k if tree_kind == "st" else -1.0)
-        launch_prior(level - 1)
+        if not prior_first:
+            launch_prior(level - 1)
         fo = DeviceForest(b * lev.h * lev.w, eu, ev, ew, in_tree, comp, gamma)
         fo.set_lanes_nodes(tmasks.contiguous())
         disp, mc, _, vol = _aggregate_timed(fo, lev, cost, lclock, want_volume=want_volume)
@@ -865,7 +876,7 @@ def stage_pairs(lefts, rights):
     # both eyes are stacked in row blocks on the staging threads (left blocks
     # first); the left eye's copy starts as soon as its blocks are in
     pool = _stager()
-    parts = max(1, STAGE_THREADS) if pl.numel() >= (4 << 20) else 1
+    parts = max(1, STAGE_THREADS) if pl.numel() >= (8 << 20) else 1
     lj = _stack_into(lefts, pl.numpy(), pool, parts)
     rj = _stack_into(rights, pr.numpy(), pool, parts)
     for j in lj:

@@ -71,3 +71,12 @@ if os.environ.get("KPROF_TIMELINE"):
             print(f"  {(e.time_range.start - t0) / 1e3:9.3f} {(e.time_range.end - t0) / 1e3:9.3f} "
                   f"{(e.time_range.end - e.time_range.start) / 1e3:8.3f}  {e.name[:60]}")
     print(f"  last kernel end {(max(e.time_range.end for e in evs) - t0) / 1e3:.3f}")
+if os.environ.get("KPROF_LONG"):
+    thr = float(os.environ["KPROF_LONG"])
+    evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
+    t0 = min(e.time_range.start for e in evs)
+    print(f"kernels longer than {thr} ms:")
+    for e in sorted(evs, key=lambda e: e.time_range.start):
+        d = (e.time_range.end - e.time_range.start) / 1e3
+        if d >= thr:
+            print(f"  {(e.time_range.start - t0) / 1e3:9.3f} {d:8.3f}  {e.name[:70]}")
