@@ -1,7 +1,7 @@
 """Dense C2 pipeline time vs batch size (device events): how far the step is
 from linear in the work (latency / launch bound vs bandwidth bound)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 from paper_1509_08197_b200 import engine as E
 from paper_1509_08197_b200.synthetic import make_batch, CONFIGS

@@ -1,6 +1,6 @@
 """Run a pipeline R times on one config (for ncu launch lists / profiles)."""
 import argparse, os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 from paper_1509_08197_b200 import engine as E
 from paper_1509_08197_b200.hdp_model import GmmModel
