@@ -138,6 +138,18 @@ int hdp_check_exact_division(int64_t n, uint64_t seed, int64_t *mismatches, void
  * bitsets over the columns (pack of DisparityIntervalTable.masks()). */
 int hdp_predict_masks(const double *bayes, int64_t nrows, int ncols, double delta, uint32_t *masks, int nw,
                       void *stream);
+/* estimate_prior's histogram step (hdp_model.py:465-470) for B pairs:
+ * priors[b, :] = (counts[b, :] + 1) / sum, the sum in numpy's add.reduce
+ * order; kept[b] == 0 -> the uniform 1 / d1.  d1 <= 256. */
+int hdp_priors_from_counts(const int64_t *counts, const int64_t *kept, int batch, int d1, double *priors,
+                           void *stream);
+/* bayes_child_given_parent (hdp_model.py:334-363) for B priors:
+ * bayes[b, r, :] = cond[r, :] * priors[b, :] / row sum (numpy's add.reduce
+ * order), a row without mass -> all 1 / cols (n_dead[b] counts them when
+ * non-NULL; zero it first).  cond: (rows, cols) f64 (host-computed
+ * conditional_parent_given_child), cols <= 256. */
+int hdp_bayes(const double *cond, const double *priors, int batch, int rows, int cols, double *bayes,
+              int32_t *n_dead, void *stream);
 /* assign_pixel_intervals (hdp_forest.py:91-123): pixel_row[g] =
  * parent_disp[b, r/S, c/S]; DATA error if a parent disparity is outside
  * [0, n_rows). */

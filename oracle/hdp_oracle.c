@@ -25,12 +25,20 @@
 static double np_pairwise(const double *a, int64_t n);
 double or_np_sum(const double *a, int64_t n);
 
-/* numpy add.reduce / reduceat order over a strided run of n values. */
+/* np.add.reduceat segment order (pyramid.py:71, aggregation.py:172): the
+ * first value seeds the segment, the rest go through numpy's pairwise sum
+ * (pinned by the golden block means with s = 3: a0 + (a1 + a2)). */
+static double np_reduceat(const double *a, int64_t n) {
+    if (n == 0) return 0.0;
+    return a[0] + np_pairwise(a + 1, n - 1);
+}
+
+/* reduceat order over a strided run of n values (pyramid block sums). */
 static double np_sum_strided(const double *a, int64_t n, int64_t stride) {
     double buf[4096];
     double *b = n <= 4096 ? buf : (double *)malloc(sizeof(double) * (size_t)n);
     for (int64_t i = 0; i < n; i++) b[i] = a[i * stride];
-    double r = or_np_sum(b, n);
+    double r = np_reduceat(b, n);
     if (b != buf) free(b);
     return r;
 }
@@ -376,7 +384,7 @@ void or_aggregate_forest(int64_t n, int64_t m, const int64_t *parent, const int6
                 /* vals = sim * up, then np.add.reduceat over the sibling run */
                 for (int64_t c = 0; c < m; c++) {
                     for (int64_t q = i; q < j; q++) sum[q - i] = sim[order[q]] * up[order[q] * m + c];
-                    up[p * m + c] += or_np_sum(sum, j - i);
+                    up[p * m + c] += np_reduceat(sum, j - i);
                 }
                 i = j;
             }
@@ -399,9 +407,12 @@ void or_aggregate_forest(int64_t n, int64_t m, const int64_t *parent, const int6
 
 /* --------------------------------------------------------------- the prior */
 
-/* numpy's pairwise summation (add.reduce over a contiguous axis): the first
- * element seeds the accumulator, the rest go through pairwise_sum with eight
- * accumulators for blocks <= 128 (numpy loops_utils.h).  hdp_model.py:394. */
+/* numpy's pairwise summation (numpy loops_utils.h: eight accumulators for
+ * blocks <= 128, halves rounded to multiples of 8 above).  add.reduce over a
+ * contiguous axis (sum / mean, numpy 2.x) runs it over all n values from the
+ * identity 0 -- or_np_sum, checked against numpy itself for n = 49 and
+ * 81..241 (hdp_model.py:394, :353, :470); reduceat seeds with the first value
+ * and sums the rest pairwise -- np_reduceat. */
 static double np_pairwise(const double *a, int64_t n) {
     if (n < 8) {
         double r = 0.0;
@@ -424,8 +435,7 @@ static double np_pairwise(const double *a, int64_t n) {
 }
 
 double or_np_sum(const double *a, int64_t n) {
-    if (n == 0) return 0.0;
-    return a[0] + np_pairwise(a + 1, n - 1);
+    return np_pairwise(a, n);
 }
 
 /* hdp_model.py:377-422 _matched_window_cost + _windowed_wta.  sign=-1 matches
@@ -524,7 +534,7 @@ void or_layer_wta(int h, int w, int c, const double *lu, const double *lg, const
                     while (jn < lb[lev + 1] && pl[jn] == p) jn++;
                     for (int64_t j = 0; j < m; j++) {
                         for (int64_t q = i; q < jn; q++) sum[q - i] = sim[order[s + q]] * up[q * m + j];
-                        up[p * m + j] += or_np_sum(sum, jn - i);
+                        up[p * m + j] += np_reduceat(sum, jn - i);
                     }
                     i = jn;
                 }

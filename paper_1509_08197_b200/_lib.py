@@ -40,6 +40,8 @@ SIGNATURES = {
     "hdp_prepare_u8": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "hdp_grid_edges_u8": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "hdp_predict_masks": (_I, [_P, _I64, _I, _D, _P, _I, _P]),
+    "hdp_priors_from_counts": (_I, [_P, _P, _I, _I, _P, _P]),
+    "hdp_bayes": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "hdp_mst_grid": (_I, [_I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "hdp_prior_counts": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _D, _D, _D,
                               _P, _P, _I, _P]),

@@ -85,11 +85,12 @@ __device__ __forceinline__ double px_cost(const PriorArgs& a, const double* su, 
 __device__ double window_cost(const PriorArgs& a, const double* su, const double* sg,
                               const double* du, const double* dg, int64_t base, int cr, int cc,
                               int sign, int x) {
+    // numpy's mean over the window: pairwise_sum of all nwin values from the
+    // identity 0 (eight accumulators, nwin <= 121 <= 128), then / nwin
     int half = a.window / 2;
     int nwin = a.window * a.window;
-    int rest_n = nwin - 1;
-    int main_n = rest_n < 8 ? 0 : rest_n - (rest_n % 8);
-    double first = 0.0, res = 0.0;
+    int main_n = nwin < 8 ? 0 : nwin - (nwin % 8);
+    double res = 0.0;
     double acc[8];
     int q = 0;
     for (int dr = -half; dr <= half; dr++) {
@@ -105,32 +106,27 @@ __device__ double window_cost(const PriorArgs& a, const double* su, const double
             } else {
                 v = a.border;
             }
-            if (q == 0) {
-                first = v;
-            } else if (rest_n < 8) {
-                res = __dadd_rn(res, v);  // pairwise_sum below 8: 0 + a1 + a2 ...
+            if (nwin < 8) {
+                res = __dadd_rn(res, v);  // pairwise_sum below 8: 0 + a0 + a1 ...
+            } else if (q < 8) {
+                acc[q] = v;
+            } else if (q < main_n) {
+                acc[q & 7] = __dadd_rn(acc[q & 7], v);
             } else {
-                int i = q - 1;
-                if (i < 8) {
-                    acc[i] = v;
-                } else if (i < main_n) {
-                    acc[i & 7] = __dadd_rn(acc[i & 7], v);
-                } else {
-                    if (i == main_n) {
-                        res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
-                                        __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
-                    }
-                    res = __dadd_rn(res, v);
+                if (q == main_n) {
+                    res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
+                                    __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
                 }
+                res = __dadd_rn(res, v);
             }
             q++;
         }
     }
-    if (rest_n >= 8 && main_n == rest_n) {
+    if (nwin >= 8 && main_n == nwin) {
         res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
                         __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
     }
-    return div_rn_by(__dadd_rn(first, res), (double)nwin, a.inv_win);
+    return div_rn_by(res, (double)nwin, a.inv_win);
 }
 
 // warp-wide windowed WTA: first minimum over x = 0..d_max
@@ -186,10 +182,11 @@ __device__ __forceinline__ double4 ld_rec(const double2* plane01, int64_t plane,
 
 // The 7 x 7 window (the reference default): one warp per sample centre, one
 // disparity per lane (x = lane, lane + 32, ...).  A lane evaluates all 49
-// window elements of its disparity in numpy's order: element 0 is `first`,
-// element q >= 1 goes to accumulator (q - 1) & 7 (six sequential additions
-// each), then ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) and first + that, divided
-// by 49 -- np.add.reduce over the 49 values (verified bit-exact).  The
+// window elements of its disparity in numpy's order: element q < 48 goes to
+// accumulator q & 7 (six sequential additions each), then
+// ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)), then + element 48, divided by 49 --
+// numpy's mean: pairwise_sum of all 49 values from the identity (numpy 2.x;
+// oracle or_np_sum, pinned against numpy in test_oracle_golden).  The
 // window's source pixels are staged once per centre in shared memory (read
 // as broadcasts); the matched pixels of the 32 lanes are 32 consecutive
 // 32-byte records.  Fully unrolled: no shuffles, no divergent lanes, the
@@ -197,10 +194,11 @@ __device__ __forceinline__ double4 ld_rec(const double2* plane01, int64_t plane,
 constexpr int kPriorWarps = 8;
 
 // Window-mean cost of one lane's disparity (offset `off` = sign * x) over
-// the staged 7 x 7 window.  Element q >= 1 goes to accumulator (q - 1) & 7 =
-// (dc - dr - 1) mod 8: V[dc] names that accumulator in row dr when V is
-// rotated right by one register per row.  Accumulators start at +0 (0 + v == v
-// exactly).  FAST: every matched column is inside the image (no tests).
+// the staged 7 x 7 window.  Element q = 7 dr + dc < 48 goes to accumulator
+// q & 7 = (dc - dr) mod 8: V[dc] names that accumulator in row dr when V is
+// rotated right by one register per row; element 48 (dr = dc = 6) is added
+// after the tree.  Accumulators start at +0 (0 + v == v exactly).  FAST: every
+// matched column is inside the image (no tests).
 template <int C, bool FAST>
 __device__ __forceinline__ double window_at(const double4* win, const double2* db, int64_t plane, int ro0,
                                             const int* colv, int off, int cr, int h, int w, double tc, double tg,
@@ -214,9 +212,9 @@ __device__ __forceinline__ double window_at(const double4* win, const double2* d
     double V[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) V[j] = 0.0;
-    const double first = elem(0, ro0, 0);
 #pragma unroll
-    for (int dc = 1; dc < 7; dc++) V[dc] = elem(0, ro0, dc);
+    for (int dc = 0; dc < 7; dc++) V[dc] = elem(0, ro0, dc);
+    double last = 0.0;  // element 48
 #pragma unroll 1
     for (int dr = 1; dr < 7; dr++) {
         const int ro = min(max(cr + dr - 3, 0), h - 1) * w;
@@ -225,12 +223,15 @@ __device__ __forceinline__ double window_at(const double4* win, const double2* d
         for (int j = 7; j > 0; j--) V[j] = V[j - 1];
         V[0] = t;
 #pragma unroll
-        for (int dc = 0; dc < 7; dc++) V[dc] = __dadd_rn(V[dc], elem(dr, ro, dc));
+        for (int dc = 0; dc < 6; dc++) V[dc] = __dadd_rn(V[dc], elem(dr, ro, dc));
+        const double e6 = elem(dr, ro, 6);
+        if (dr < 6) V[6] = __dadd_rn(V[6], e6);
+        else last = e6;
     }
-    // after row 6, accumulator i is V[(i - 1) mod 8]
-    const double res = __dadd_rn(__dadd_rn(__dadd_rn(V[7], V[0]), __dadd_rn(V[1], V[2])),
-                                 __dadd_rn(__dadd_rn(V[3], V[4]), __dadd_rn(V[5], V[6])));
-    return div_rn_by(__dadd_rn(first, res), 49.0, inv_win);
+    // after row 6, accumulator i is V[(i + 6) mod 8]
+    const double res = __dadd_rn(__dadd_rn(__dadd_rn(V[6], V[7]), __dadd_rn(V[0], V[1])),
+                                 __dadd_rn(__dadd_rn(V[2], V[3]), __dadd_rn(V[4], V[5])));
+    return div_rn_by(__dadd_rn(res, last), 49.0, inv_win);
 }
 
 template <int C>
@@ -321,6 +322,116 @@ __global__ void __launch_bounds__(256, HDP_PRIOR_MINB) k_prior(PriorArgs a, int 
     for (int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wid < per * batch; wid += nwarp)
         prior_centre<W7>(a, per, wid, win[threadIdx.x >> 5]);
 }
+// numpy's pairwise_sum (eight accumulators for blocks <= 128, halves rounded
+// to multiples of 8 above; oracle/hdp_oracle.c np_pairwise): sequential
+// device code with exactly that association order.
+__device__ double np_pairwise_dev(const double* a, int n) {
+    // iterative form of the recursion: an explicit stack of (offset, count)
+    double part[16];
+    int off[16], cnt[16], state[16];
+    int sp = 0;
+    off[0] = 0;
+    cnt[0] = n;
+    state[0] = 0;
+    double ret = 0.0;
+    while (sp >= 0) {
+        const int o = off[sp], m = cnt[sp];
+        if (m <= 128) {
+            double r;
+            if (m < 8) {
+                r = 0.0;
+                for (int i = 0; i < m; i++) r += a[o + i];
+            } else {
+                double q[8];
+                for (int j = 0; j < 8; j++) q[j] = a[o + j];
+                int i;
+                for (i = 8; i < m - (m % 8); i += 8)
+                    for (int j = 0; j < 8; j++) q[j] += a[o + i + j];
+                r = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+                for (; i < m; i++) r += a[o + i];
+            }
+            ret = r;
+            sp--;
+            // hand the value to the parent frame
+            while (sp >= 0) {
+                if (state[sp] == 1) {  // left half done: remember it, do the right half
+                    part[sp] = ret;
+                    state[sp] = 2;
+                    int n2 = cnt[sp] / 2;
+                    n2 -= n2 % 8;
+                    off[sp + 1] = off[sp] + n2;
+                    cnt[sp + 1] = cnt[sp] - n2;
+                    state[sp + 1] = 0;
+                    sp++;
+                    break;
+                }
+                ret = part[sp] + ret;  // both halves done
+                sp--;
+            }
+        } else {
+            int n2 = m / 2;
+            n2 -= n2 % 8;
+            state[sp] = 1;
+            off[sp + 1] = o;
+            cnt[sp + 1] = n2;
+            state[sp + 1] = 0;
+            sp++;
+        }
+    }
+    return ret;
+}
+// add.reduce over a contiguous axis (sum / mean): pairwise over all n values
+// from the identity (numpy 2.x; oracle or_np_sum)
+__device__ __forceinline__ double np_sum_dev(const double* a, int n) { return np_pairwise_dev(a, n); }
+
+// priors from the cross-checked counts (hdp_model.py:465-470): hist = counts
+// + 1, hist / hist.sum(); no kept sample -> 1 / (d + 1).  One warp per pair,
+// hist staged in shared memory, lane 0 sums in numpy's order.
+constexpr int kBayesMaxCols = 256;
+__global__ void __launch_bounds__(256) k_priors(const long long* __restrict__ counts, const long long* __restrict__ kept,
+                                                int batch, int d1, double* __restrict__ out) {
+    __shared__ double hist[8][kBayesMaxCols];
+    __shared__ double tot[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int b = blockIdx.x * 8 + wib;
+    if (b >= batch) return;
+    const bool none = kept[b] == 0;
+    for (int i = lane; i < d1; i += 32) hist[wib][i] = (double)counts[(int64_t)b * d1 + i] + 1.0;
+    __syncwarp();
+    if (lane == 0) tot[wib] = np_sum_dev(hist[wib], d1);
+    __syncwarp();
+    const double uni = 1.0 / (double)d1;
+    for (int i = lane; i < d1; i += 32) out[(int64_t)b * d1 + i] = none ? uni : hist[wib][i] / tot[wib];
+}
+
+// bayes_child_given_parent (hdp_model.py:334-363) for every (pair, row):
+// joint = cond[r, :] * prior[b, :], row_sum in numpy's order, a row without
+// mass becomes all ones (so 1 / cols), out = joint / row_sum.  One warp per row.
+__global__ void __launch_bounds__(256) k_bayes(const double* __restrict__ cond, const double* __restrict__ priors,
+                                               int batch, int rows, int cols, double* __restrict__ out,
+                                               int* __restrict__ n_dead) {
+    __shared__ double joint[8][kBayesMaxCols];
+    __shared__ double tot[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * 8 + wib;
+    if (row >= (int64_t)batch * rows) return;
+    const int b = (int)(row / rows), r = (int)(row % rows);
+    for (int i = lane; i < cols; i += 32)
+        joint[wib][i] = __dmul_rn(cond[(int64_t)r * cols + i], priors[(int64_t)b * cols + i]);
+    __syncwarp();
+    if (lane == 0) {
+        double t = np_sum_dev(joint[wib], cols);
+        if (t <= 0.0) {
+            for (int i = 0; i < cols; i++) joint[wib][i] = 1.0;
+            t = np_sum_dev(joint[wib], cols);
+            if (n_dead) atomicAdd(n_dead + b, 1);
+        }
+        tot[wib] = t;
+    }
+    __syncwarp();
+    for (int i = lane; i < cols; i += 32) out[row * cols + i] = __ddiv_rn(joint[wib][i], tot[wib]);
+}
+
 __global__ void k_assign_rows(const int32_t* __restrict__ pd, int batch, int ph, int pw, int h,
                               int w, int s, int n_rows, int32_t* __restrict__ rows, int* bad) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -534,5 +645,28 @@ extern "C" int hdp_assign_rows(const int32_t* parent_disp, int batch, int ph, in
     HDP_CHECK_CUDA(cudaStreamSynchronize(st));
     HDP_REQUIRE(hb == 0, HDP_ERR_INTERNAL, "%d parent disparities outside the %d-row table", hb,
                 n_rows);
+    return HDP_OK;
+}
+
+extern "C" int hdp_priors_from_counts(const int64_t* counts, const int64_t* kept, int batch, int d1, double* priors,
+                                      void* stream) {
+    HDP_REQUIRE(batch >= 1 && d1 >= 1, HDP_ERR_CONFIG, "bad prior shape");
+    HDP_REQUIRE(d1 <= kBayesMaxCols, HDP_ERR_CONFIG, "disparity range above 255 not supported by hdp_priors_from_counts");
+    k_priors<<<(batch + 7) / 8, 256, 0, (cudaStream_t)stream>>>((const long long*)counts, (const long long*)kept,
+                                                               batch, d1, priors);
+    note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+extern "C" int hdp_bayes(const double* cond, const double* priors, int batch, int rows, int cols, double* bayes,
+                         int32_t* n_dead, void* stream) {
+    HDP_REQUIRE(batch >= 1 && rows >= 1 && cols >= 1, HDP_ERR_CONFIG, "bad Bayes shape");
+    HDP_REQUIRE(cols <= kBayesMaxCols, HDP_ERR_CONFIG, "disparity range above 255 not supported by hdp_bayes");
+    const int64_t nrows = (int64_t)batch * rows;
+    k_bayes<<<(unsigned)((nrows + 7) / 8), 256, 0, (cudaStream_t)stream>>>(cond, priors, batch, rows, cols, bayes,
+                                                                         n_dead);
+    note_launch();
+    HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

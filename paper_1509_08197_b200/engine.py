@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib as L
-from .errors import ConfigError, DataError
+from .errors import ConfigError, DataError, InternalError
 
 ALPHA, TAU_C, TAU_G = 0.9, 0.0275, 0.0078  # cost_volume.py:38-40
 TREE_KINDS = ("mst", "rt", "st")
@@ -346,14 +346,51 @@ def predict_masks(bayes, delta: float):
     return chosen
 
 
+_COND_CACHE: dict = {}
+
+
+def conditional_device(mix, d_child: int, d_parent: int, s: int, device):
+    """conditional_matrix on the host (numpy's exp and column sums), cached on
+    the device per (mixture, sizes): it depends only on the model."""
+    torch = _t()
+    key = (id(mix), d_child, d_parent, s, device.index if hasattr(device, "index") else device)
+    hit = _COND_CACHE.get(key)
+    if hit is not None and hit[0] is mix:
+        return hit[1]
+    cond = conditional_matrix(mix, d_child, d_parent, s)
+    t = torch.from_numpy(np.ascontiguousarray(cond, dtype=np.float64)).to(device)
+    _COND_CACHE[key] = (mix, t)
+    return t
+
+
+def bayes_device(counts, kept, cond_d):
+    """priors_from_counts + bayes_batched on the device (hdp_priors_from_counts,
+    hdp_bayes; numpy's summation order): no host round trip between the
+    prior's counts and the interval masks.  Returns (B, rows, cols) f64."""
+    torch = _t()
+    b, d1 = counts.shape
+    rows, cols = cond_d.shape
+    if cols != d1:
+        raise InternalError(f"conditional matrix has {cols} columns, prior has {d1}")
+    pri = torch.empty((b, d1), dtype=torch.float64, device=counts.device)
+    L.call("hdp_priors_from_counts", L.ptr(counts.contiguous()), L.ptr(kept.contiguous()), b, d1, L.ptr(pri),
+           L.stream())
+    bm = torch.empty((b, rows, cols), dtype=torch.float64, device=counts.device)
+    L.call("hdp_bayes", L.ptr(cond_d), L.ptr(pri), b, rows, cols, L.ptr(bm), None, L.stream())
+    return bm
+
+
 def predict_masks_device(bayes, delta: float, device):
     """predict_masks + pack_masks on the device (hdp_predict_masks): (B, rows,
-    cols) f64 host Bayes matrices -> (B, rows, nw) int32-viewed u32 bitsets on
-    `device`, bit-identical to the host functions."""
+    cols) f64 Bayes matrices (host numpy or a device tensor) -> (B, rows, nw)
+    int32-viewed u32 bitsets on `device`, bit-identical to the host functions."""
     torch = _t()
     b, rows, cols = bayes.shape
     nw = (cols + 31) // 32
-    bd = torch.from_numpy(np.ascontiguousarray(bayes, dtype=np.float64)).to(device, non_blocking=True)
+    if isinstance(bayes, np.ndarray):
+        bd = torch.from_numpy(np.ascontiguousarray(bayes, dtype=np.float64)).to(device, non_blocking=True)
+    else:
+        bd = bayes.contiguous()
     out = torch.empty((b, rows, nw), dtype=torch.int32, device=device)
     L.call("hdp_predict_masks", L.ptr(bd), b * rows, cols, float(delta), L.ptr(out), nw, L.stream())
     return out
@@ -772,12 +809,15 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
             torch.cuda.current_stream().wait_event(ev)
         else:
             counts, kept = prior_counts(lev, cost=cost)
-        counts_h, kept_h = counts.cpu().numpy(), kept.cpu().numpy()
-        priors = priors_from_counts(counts_h, kept_h)
-        cond = conditional_matrix(model.layers[level], lev.d_max, lv[level + 1].d_max, block_size)
-        bm, _ = bayes_batched(cond, priors)
+        # prior -> Bayes -> interval masks stay on the device (no host read)
+        cond_d = conditional_device(model.layers[level], lev.d_max, lv[level + 1].d_max, block_size,
+                                    lev.img_l.device)
+        bm = bayes_device(counts, kept, cond_d)
         row_masks = predict_masks_device(bm, delta0 * block_size**level, lev.img_l.device)
-        chosen = predict_masks(bm, delta0 * block_size**level) if keep else None
+        counts_h = kept_h = chosen = None
+        if keep:
+            counts_h, kept_h = counts.cpu().numpy(), kept.cpu().numpy()
+            chosen = predict_masks(bm.cpu().numpy(), delta0 * block_size**level)
         rows = assign_rows(parent.contiguous(), lev.h, lev.w, block_size, bm.shape[1])
         lclock.lap("predict")
         eu, ev, ew, key, E = grid_edges(lev.img_l)

@@ -3,6 +3,8 @@ and the CPU oracle.  Run on a B200: pytest -m gpu."""
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -245,3 +247,31 @@ def test_prior_division_is_ieee_exact():
     bad = ctypes.c_int64(-1)
     L.call("hdp_check_exact_division", 1 << 24, 12345, ctypes.byref(bad), L.stream())
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("d_child,d_parent", [(80, 40), (240, 120), (12, 6), (5, 2)])
+def test_device_bayes_matches_host(d_child, d_parent):
+    """hdp_priors_from_counts + hdp_bayes (the HDP level loop's device path)
+    == priors_from_counts + bayes_batched on the host, bit for bit, including
+    a pair without kept samples and rows without mass."""
+    import torch
+
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.hdp_model import GmmModel
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "default.gmm")) as fh:
+        model = GmmModel.parse(fh.read())
+    rng = np.random.default_rng(d_child)
+    b = 5
+    counts = rng.integers(0, 400, (b, d_child + 1)).astype(np.int64)
+    counts[:, rng.integers(0, d_child + 1, d_child // 3)] = 0
+    kept = counts.sum(axis=1).astype(np.int64)
+    counts[1] = 0
+    kept[1] = 0
+    cond = E.conditional_matrix(model.layers[0], d_child, d_parent, 2)
+    cond[cond.shape[0] // 2] = 0.0  # a parent row with no mass under any prior
+    pri = E.priors_from_counts(counts, kept)
+    bm, _ = E.bayes_batched(cond, pri)
+    cd = torch.from_numpy(np.ascontiguousarray(cond)).cuda()
+    got = E.bayes_device(torch.from_numpy(counts).cuda(), torch.from_numpy(kept).cuda(), cd)
+    np.testing.assert_array_equal(got.cpu().numpy(), bm)

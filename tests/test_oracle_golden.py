@@ -159,3 +159,19 @@ def test_evaluation_matches_reference():
             assert O.error_rate(g[p + "pred"], g[p + "pv"], g[p + "gl"], g[p + "vl"], None, t) == float(g[p + f"err{t}"])
             assert O.error_rate(g[p + "pred"], g[p + "pv"], g[p + "gl"], g[p + "vl"], occ, t) == float(
                 g[p + f"err{t}_occ"])
+
+
+def test_oracle_reduce_order_is_numpys():
+    """The oracle's add.reduce order (or_np_sum: the prior's 49-value window
+    mean, the prior histogram and Bayes row sums) against numpy itself."""
+    import ctypes as C
+
+    f = O.lib().or_np_sum
+    f.restype = C.c_double
+    f.argtypes = [C.c_void_p, C.c_int64]
+    rng = np.random.default_rng(5)
+    for n in (1, 3, 7, 8, 9, 49, 81, 121, 128, 129, 241, 300):
+        a = rng.uniform(-1, 1, (64, n)) * rng.uniform(0, 1e3, (64, 1))
+        want = a.sum(axis=-1)
+        got = np.array([f(np.ascontiguousarray(r).ctypes.data, n) for r in a])
+        np.testing.assert_array_equal(got, want, err_msg=f"n={n}")
