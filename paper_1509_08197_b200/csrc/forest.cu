@@ -1430,7 +1430,7 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
                              const int4* __restrict__ sinfo, const longlong2* __restrict__ srows,
                              const int32_t* __restrict__ lc_start, const int64_t* __restrict__ lc_rowoff,
                              const int64_t* __restrict__ auxd, const int64_t* __restrict__ W,
-                             ChunkDesc* desc, unsigned long long* max_words) {
+                             ChunkDesc* desc, unsigned long long* max_words, int uniform) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = c < cbase[nph];
     unsigned long long words = 0;
@@ -1452,8 +1452,13 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
         d.auxd0 = auxd[p0];
         d.naux_dn = (int)(auxd[p1] - d.auxd0);
         int mq = (f.z + 3) >> 2;
-        for (int p = p0 + 1; p < p1 && mq > 0; p++)
-            if (((sinfo[p].z + 3) >> 2) != mq) mq = 0;
+        // range lanes: every row has the same width; otherwise the uniform
+        // mapping only for chunks of few paths (a serial check per chunk)
+        if (!uniform) {
+            if (p1 - p0 > 64) mq = 0;
+            for (int p = p0 + 1; p < p1 && mq > 0; p++)
+                if (((sinfo[p].z + 3) >> 2) != mq) mq = 0;
+        }
         d.mqu = mq;
         d.inv = mq > 1 ? (unsigned)((0x100000000ull + mq - 1) / mq) : 0u;
         words = (unsigned long long)(W[p1] - W[p0]);
@@ -1546,7 +1551,8 @@ static int build_chunks(hdp_forest* f) {
     k_chunk_desc<<<grid_for(ncap, 256), 256, 0, st>>>(cbase.get(), nph, f->chunk_first.get(), f->short_info.get(),
                                                       f->short_rows.get(), f->lc_start.get(),
                                                       f->lc_rowoff.get(), f->auxd.get(), W.get(),
-                                                      f->chunk_desc.get(), mx.get()); note_launch();
+                                                      f->chunk_desc.get(), mx.get(), f->range_x0 >= 0 ? 1 : 0);
+    note_launch();
     HDP_CHECK_LAUNCH();
     // size classes (k_chunk_split): the chunk count is only known on the
     // device, so the class passes run over the bound ncap
