@@ -256,6 +256,10 @@ int hdp_forest_stage_ms(const hdp_forest *f, float *cost_ms, float *aggregate_ms
  * aggregation.py:418-426); host output arrays of length batch. */
 int hdp_forest_pair_stats(const hdp_forest *f, int batch, int64_t nodes_per_pair,
                           int64_t *n_trees, int64_t *stored, void *stream);
+/* The same into a device array out[2 * batch] = (tree counts, stored
+ * entries), stream-ordered, no host read. */
+int hdp_forest_pair_stats_device(const hdp_forest *f, int batch, int64_t nodes_per_pair, int64_t *out,
+                                 void *stream);
 
 void hdp_forest_destroy(hdp_forest *f);
 

@@ -59,6 +59,7 @@ SIGNATURES = {
     "hdp_forest_entries": (_I, [_P, C.POINTER(_I64), _P, _P]),
     "hdp_aggregate_wta": (_I, [_P, _P, _P, _I, _I, _I, _F, _F, _F, _P, _P, _P, _P, _P, _P]),
     "hdp_forest_pair_stats": (_I, [_P, _I, _I64, _P, _P, _P]),
+    "hdp_forest_pair_stats_device": (_I, [_P, _I, _I64, _P, _P]),
     "hdp_forest_set_timing": (_I, [_P, _I]),
     "hdp_forest_stage_ms": (_I, [_P, _P, _P]),
     "hdp_forest_destroy": (None, [_P]),

@@ -1860,6 +1860,18 @@ __global__ void k_pair_stats(int batch, int64_t npp, int64_t n, int64_t n_trees,
 }
 }  // namespace hdp
 
+extern "C" int hdp_forest_pair_stats_device(const hdp_forest* f, int batch, int64_t nodes_per_pair, int64_t* out,
+                                            void* stream) {
+    HDP_REQUIRE(f != nullptr && f->lanes_set, HDP_ERR_CONFIG, "forest lanes not set");
+    HDP_REQUIRE(batch >= 1 && (int64_t)batch * nodes_per_pair == f->n, HDP_ERR_CONFIG,
+                "batch x nodes_per_pair must equal the node count");
+    k_pair_stats<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(batch, nodes_per_pair, f->n, f->n_trees,
+                                                                        f->total_entries, f->tree_id.get(),
+                                                                        f->nodeoff.get(), out); note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
 extern "C" int hdp_forest_pair_stats(const hdp_forest* f, int batch, int64_t nodes_per_pair,
                                      int64_t* n_trees, int64_t* stored, void* stream) {
     HDP_REQUIRE(f != nullptr && f->lanes_set, HDP_ERR_CONFIG, "forest lanes not set");

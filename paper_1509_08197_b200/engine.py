@@ -467,6 +467,23 @@ def hdpf(batch, npp, epp, eu, ev, key, pixel_row, row_masks, beta: float, ew=Non
 
 
 # --------------------------------------------------------------- pipelines
+class _Lazy:
+    """A LevelOut statistic still on the device (hdp_forest_pair_stats_device):
+    read back on first access, so the level loop never waits for it."""
+
+    def __init__(self, dev, batch: int, npp: int, d_max: int, which: int):
+        self.dev, self.batch, self.npp, self.d_max, self.which = dev, batch, npp, d_max, which
+
+    def get(self):
+        h = self.dev.cpu().numpy()
+        nt, st = h[: self.batch].copy(), h[self.batch:].copy()
+        if self.which == 0:
+            return nt
+        if self.which == 1:
+            return st
+        return np.array([float(v) / self.npp / (self.d_max + 1) for v in st])
+
+
 @dataclass
 class LevelOut:
     level: int
@@ -481,6 +498,21 @@ class LevelOut:
     timings: dict = field(default_factory=dict)
     forest: object = None
     extra: dict = field(default_factory=dict)
+
+    def __getattribute__(self, name):
+        v = object.__getattribute__(self, name)
+        if isinstance(v, _Lazy):
+            v = v.get()
+            object.__setattr__(self, name, v)
+        return v
+
+
+def _per_pair_stats_lazy(f: DeviceForest, batch: int, npp: int, d_max: int):
+    """(n_trees, stored_entries, search_ratio) as _Lazy device-backed values."""
+    torch = _t()
+    dev = torch.empty(2 * batch, dtype=torch.int64, device=L.device())
+    L.call("hdp_forest_pair_stats_device", f._h, batch, npp, L.ptr(dev), L.stream())
+    return tuple(_Lazy(dev, batch, npp, d_max, k) for k in range(3))
 
 
 def _per_pair_stats(f: DeviceForest, batch: int, npp: int, d_max: int):
@@ -770,7 +802,7 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
             early[level] = (c_, k_, ev_)
 
     def finish(lev, f, disp, mc, vol, clk):
-        ntrees, stored, ratio = _per_pair_stats(f, b, lev.h * lev.w, lev.d_max)
+        ntrees, stored, ratio = _per_pair_stats_lazy(f, b, lev.h * lev.w, lev.d_max)
         o = LevelOut(lev.level, lev.h, lev.w, lev.d_max, disp.view(b, lev.h, lev.w),
                      mc.view(b, lev.h, lev.w), ntrees, stored, ratio, {},
                      f if keep else None)
