@@ -643,33 +643,37 @@ __global__ void k_path_fill(int64_t n, const int32_t* __restrict__ flag,
 }
 
 // light children of the node at layout position k, ascending id
-__global__ void k_lc_count(int64_t n, const int32_t* __restrict__ lnode,
+// One thread per node id (not per layout position): the adjacency, parent
+// and head reads of neighbouring threads are neighbouring (grid trees), only
+// the count / the CSR start is gathered through lpos.
+__global__ void k_lc_count(int64_t n, const int32_t* __restrict__ lpos,
                            const int32_t* __restrict__ adj_start, const int32_t* __restrict__ adst,
                            const int32_t* __restrict__ parent, const int32_t* __restrict__ head,
                            int32_t* cnt) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int32_t x = lnode[k];
+    int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
     int32_t c = 0;
     for (int32_t a = adj_start[x]; a < adj_start[x + 1]; a++) {
         int32_t y = adst[a];
         if (parent[y] == x && y != x && head[y] == y) c++;
     }
-    cnt[k] = c;
+    cnt[lpos[x]] = c;
 }
 
-__global__ void k_lc_fill(int64_t n, const int32_t* __restrict__ lnode,
+__global__ void k_lc_fill(int64_t n, const int32_t* __restrict__ lpos,
                           const int32_t* __restrict__ adj_start, const int32_t* __restrict__ adst,
                           const int32_t* __restrict__ parent, const int32_t* __restrict__ head,
-                          const int32_t* __restrict__ lpos, const int32_t* __restrict__ lc_start,
-                          int32_t* lc_list) {
-    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int32_t x = lnode[k];
-    int32_t o = lc_start[k];
-    for (int32_t a = adj_start[x]; a < adj_start[x + 1]; a++) {
+                          const int32_t* __restrict__ lc_start, int32_t* lc_list) {
+    int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= n) return;
+    const int32_t a0 = adj_start[x], a1 = adj_start[x + 1];
+    int32_t o = -1;
+    for (int32_t a = a0; a < a1; a++) {
         int32_t y = adst[a];
-        if (parent[y] == x && y != x && head[y] == y) lc_list[o++] = lpos[y];
+        if (parent[y] == x && y != x && head[y] == y) {
+            if (o < 0) o = lc_start[lpos[x]];
+            lc_list[o++] = lpos[y];
+        }
     }
 }
 
@@ -1270,13 +1274,13 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     HDP_TRY(lcc.alloc(n + 1, st));
     HDP_TRY(f->lc_start.alloc(n + 1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(lcc.get(), 0, (n + 1) * sizeof(int32_t), st));
-    k_lc_count<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
+    k_lc_count<<<grid_for(n, B), B, 0, st>>>(n, f->lpos.get(), adj_start.get(), adst.get(),
                                              f->parent.get(), head, lcc.get()); note_launch();
     HDP_TRY(exclusive_sum(lcc.get(), f->lc_start.get(), n + 1, st));
     HDP_TRY(f->lc_list.alloc(n + 1, st));  // light children <= n - 1
-    k_lc_fill<<<grid_for(n, B), B, 0, st>>>(n, f->lnode.get(), adj_start.get(), adst.get(),
-                                            f->parent.get(), head, f->lpos.get(),
-                                            f->lc_start.get(), f->lc_list.get()); note_launch();
+    k_lc_fill<<<grid_for(n, B), B, 0, st>>>(n, f->lpos.get(), adj_start.get(), adst.get(),
+                                            f->parent.get(), head, f->lc_start.get(), f->lc_list.get());
+    note_launch();
     HDP_CHECK_LAUNCH();
 
     tr.mark("9 light children");
