@@ -1704,31 +1704,6 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     HDP_REQUIRE(cost_rows || (int64_t)h * w < ((int64_t)1 << 31), HDP_ERR_CONFIG, "image too large");
     cudaStream_t st = (cudaStream_t)stream;
     if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[0], st));
-    // wide dense rows (a disparity range of >= HDP_WIDE_MIN lanes, no volume
-    // output): register-streaming kernels with the raw cost fused into the up
-    // pass (wide.cu)
-    if (!cost_rows && !volume && f->range_x0 >= 0 && wide_min_lanes() > 0 && f->max_m >= wide_min_lanes()) {
-        HDP_REQUIRE(f->n % w == 0, HDP_ERR_CONFIG, "node count is not a whole number of image rows");
-        if (f->geom_w != w || f->geom_np != h * w) {
-            k_fill_cols<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, f->lmeta.get(), h * w, w); note_launch();
-            f->geom_w = w;
-            f->geom_np = h * w;
-        }
-        DevBuf<unsigned long long> kb;
-        unsigned long long* kp = (unsigned long long*)keys;
-        if (!kp) {
-            HDP_TRY(kb.alloc(f->n, st));
-            kp = kb.get();
-        }
-        if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[1], st));  // the cost is fused: no stage of its own
-        HDP_TRY(wide_aggregate(f, packed_l, packed_r, c, alpha, tau_c, tau_g, kp, st));
-        if (disp || min_cost) {
-            k_keys_finish<<<grid_for(f->n, 256), 256, 0, st>>>(f->n, kp, disp, min_cost); note_launch();
-        }
-        if (f->timing) HDP_CHECK_CUDA(cudaEventRecord(f->tev[2], st));
-        HDP_CHECK_LAUNCH();
-        return HDP_OK;
-    }
     AggArgs a;
     a.lmeta = f->lmeta.get();
     a.lsimf = f->lsimf.get();

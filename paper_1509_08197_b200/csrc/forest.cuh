@@ -148,9 +148,4 @@ struct hdp_forest {
 };
 
 namespace hdp {
-// wide.cu: aggregation + first argmin for dense rows of >= wide_min_lanes()
-// lanes (keys: u64 first-argmin keys per node, written with atomicMin)
-int wide_min_lanes();
-int wide_aggregate(hdp_forest* f, const float* packed_l, const float* packed_r, int c, float alpha, float tau_c,
-                   float tau_g, unsigned long long* keys, cudaStream_t st);
 }  // namespace hdp

@@ -15,9 +15,7 @@
 // walked independently by one thread in Kruskal order against shared-memory
 // copies of its trees; merges are written back to the global union-find.
 // k_grp<true> adds the segment-tree criterion w <= min(Int(A) + k/|A|,
-// Int(B) + k/|B|) (hdp_segment_tree, tree kind "st").  k_dr, the earlier
-// deterministic-reservations kernel (an edge is decided once it holds the
-// reservation of both its roots), stays behind HDP_HDPF_DR=1 for diagnostics.
+// Int(B) + k/|B|) (hdp_segment_tree, tree kind "st").
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -86,12 +84,11 @@ __global__ void k_seg_bounds(int64_t ms, const uint64_t* __restrict__ skey, int 
 
 __global__ void k_uf_init(int64_t n, const int32_t* __restrict__ pixel_row,
                           const uint32_t* __restrict__ row_masks, int64_t npp, int n_rows, int nw,
-                          int32_t* uf, int32_t* usz, uint32_t* tm, unsigned long long* res) {
+                          int32_t* uf, int32_t* usz, uint32_t* tm) {
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     uf[v] = (int32_t)v;
     usz[v] = 1;
-    res[v] = 0ull;
     const uint32_t* pm = pix_mask(row_masks, pixel_row, (int32_t)v, npp, n_rows, nw);
     for (int i = 0; i < nw; i++) tm[v * nw + i] = pm[i];
 }
@@ -106,249 +103,7 @@ __device__ __forceinline__ int32_t uf_find(int32_t* uf, int32_t x) {
     }
 }
 
-constexpr int DR_THREADS = 1024;
-constexpr int DR_MAXS = 64;      // roots the multi-commit leader can absorb per round
-constexpr int DR_SCAN = 256;    // window edges the leader may inspect per round
-constexpr int DR_HASH = 256;     // shared-memory hash set of the leader's roots
 constexpr int DR_NW = 8;         // mask words per root staged in shared memory (d_max < 256)
-
-__device__ __forceinline__ unsigned dr_hash(int32_t x) {
-    return ((unsigned)x * 2654435761u) >> 24;  // top 8 bits
-}
-__device__ __forceinline__ void dr_hash_put(int32_t* h, int32_t x) {
-    unsigned i = dr_hash(x);
-    while (h[i] != -1 && h[i] != x) i = (i + 1) & (DR_HASH - 1);
-    h[i] = x;
-}
-__device__ __forceinline__ bool dr_hash_has(const int32_t* h, int32_t x) {
-    unsigned i = dr_hash(x);
-    while (true) {
-        int32_t v = h[i];
-        if (v == x) return true;
-        if (v == -1) return false;
-        i = (i + 1) & (DR_HASH - 1);
-    }
-}
-
-__device__ __forceinline__ unsigned long long dr_stamp(unsigned round, int pos) {
-    return ((unsigned long long)(round + 1) << 32) | (unsigned long long)(0xffffffffu - (unsigned)pos);
-}
-
-__device__ __forceinline__ bool dr_jaccard_ok(const uint32_t* tm, int32_t a, int32_t b, int nw,
-                                              double beta) {
-    int inter = 0, uni = 0;
-    for (int i = 0; i < nw; i++) {
-        uint32_t p = tm[(int64_t)a * nw + i], q = tm[(int64_t)b * nw + i];
-        inter += __popc(p & q);
-        uni += __popc(p | q);
-    }
-    // rule 2: IEEE double division, as hdp_forest.py:195
-    return !(__ddiv_rn((double)inter, (double)uni) < beta);
-}
-
-// merge roots a, b (union by size); returns the surviving root
-__device__ __forceinline__ int32_t dr_union(int32_t* uf, int32_t* usz, uint32_t* tm, int nw,
-                                            int32_t a, int32_t b) {
-    int32_t keep = a, gone = b;
-    if (usz[a] < usz[b]) { keep = b; gone = a; }
-    uf[gone] = keep;
-    usz[keep] += usz[gone];
-    for (int i = 0; i < nw; i++) tm[(int64_t)keep * nw + i] |= tm[(int64_t)gone * nw + i];
-    return keep;
-}
-
-// One CTA per stereo pair.  Per round: (A) every window edge finds its roots
-// and reserves both (atomicMax of a (round, -position) stamp); self-loops are
-// dropped.  (B) an edge holding both reservations has no earlier pending edge
-// touching either tree -> decided now.  (C) multi-commit: the leader of every
-// merge keeps scanning the window in order; the next edge touching its grown
-// component is decided too when its other root is reserved by that very edge
-// (no earlier pending edge touches it), otherwise the leader stops.
-// Compaction keeps the undecided edges, in order, for the next window.
-__global__ void __launch_bounds__(DR_THREADS) k_dr(const int32_t* __restrict__ seg,
-                                                   int32_t* __restrict__ order,
-                                                   const int32_t* __restrict__ eu,
-                                                   const int32_t* __restrict__ ev, int32_t* uf,
-                                                   int32_t* usz, uint32_t* tm,
-                                                   unsigned long long* res, int nw, double beta,
-                                                   uint8_t* in_tree, int* rounds_out) {
-    __shared__ int s_warp[DR_THREADS / 32];
-    __shared__ int s_total;
-    __shared__ int32_t s_ra[DR_THREADS], s_rb[DR_THREADS], s_e[DR_THREADS];
-    __shared__ uint8_t s_dec[DR_THREADS];
-    __shared__ int32_t s_hash[DR_HASH];
-    __shared__ unsigned long long s_best;
-    // per window edge: reservation stamps and masks of both (round-start)
-    // roots, staged for the multi-commit walk after the parallel commits
-    extern __shared__ unsigned long long s_dyn[];  // dynamic: DrStage
-    unsigned long long (*s_res)[DR_THREADS] = reinterpret_cast<unsigned long long (*)[DR_THREADS]>(s_dyn);
-    uint32_t (*s_msk)[DR_THREADS * DR_NW] =
-        reinterpret_cast<uint32_t (*)[DR_THREADS * DR_NW]>(s_dyn + 2 * DR_THREADS);
-    int b = blockIdx.x;
-    int tid = threadIdx.x;
-    int lane = tid & 31, wid = tid >> 5;
-    int32_t head = seg[b], end = seg[b + 1];
-    unsigned int round = 0;
-#ifdef HDP_DR_PROFILE
-    long long t_ph[6] = {0, 0, 0, 0, 0, 0};
-    long long t0 = clock64(), t1;
-#define DR_TICK(k) do { __syncthreads(); t1 = clock64(); t_ph[k] += t1 - t0; t0 = t1; } while (0)
-#else
-#define DR_TICK(k) __syncthreads()  // the round's phase barriers (timed in profile builds)
-#endif
-    while (head < end) {
-        int32_t win = min((int32_t)DR_THREADS, end - head);
-        bool pend = tid < win;
-        bool decided = false, leader = false;
-        int32_t e = 0, ra = 0, rb = 0, keep = 0;
-        unsigned long long stamp = dr_stamp(round, tid);
-        if (tid == 0) s_best = 0ull;
-        if (pend) {
-            e = order[head + tid];
-            ra = uf_find(uf, eu[e]);
-            rb = uf_find(uf, ev[e]);
-            if (ra == rb) {
-                decided = true;  // would close a cycle: skipped (hdp_forest.py:190-191)
-            } else {
-                atomicMax(&res[ra], stamp);
-                atomicMax(&res[rb], stamp);
-            }
-            s_ra[tid] = ra;
-            s_rb[tid] = rb;
-            s_e[tid] = e;
-        }
-        DR_TICK(0);
-        if (pend && !decided) {
-            unsigned long long xa = *((volatile unsigned long long*)&res[ra]);
-            unsigned long long xb = *((volatile unsigned long long*)&res[rb]);
-            if (xa == stamp && xb == stamp) {
-                decided = true;
-                if (dr_jaccard_ok(tm, ra, rb, nw, beta)) {
-                    keep = dr_union(uf, usz, tm, nw, ra, rb);
-                    in_tree[e] = 1;
-                    leader = true;
-                }
-            }
-        }
-        if (pend) s_dec[tid] = decided ? 1 : 0;
-        DR_TICK(1);
-        if (leader) atomicMax(&s_best, ((unsigned long long)usz[keep] << 32) | (unsigned)tid);
-        if (pend && !decided) {
-            // neither changes during the walk: only the giant's own mask
-            // (held in registers) and uf/usz are written there
-            s_res[0][tid] = *((volatile unsigned long long*)&res[ra]);
-            s_res[1][tid] = *((volatile unsigned long long*)&res[rb]);
-            for (int k = 0; k < nw; k++) {
-                s_msk[0][tid * DR_NW + k] = tm[(int64_t)ra * nw + k];
-                s_msk[1][tid * DR_NW + k] = tm[(int64_t)rb * nw + k];
-            }
-        }
-        DR_TICK(2);
-        // multi-commit for the largest merged tree of the round (the giant
-        // whose edges would otherwise be decided one per round), by warp 0
-        if (wid == 0 && s_best != 0ull) {
-            int lt = (int)(s_best & 0xffffffffu);
-            int32_t root = uf_find(uf, s_ra[lt]);  // the leader's surviving root
-            for (int i = lane; i < DR_HASH; i += 32) s_hash[i] = -1;
-            __syncwarp();
-            if (lane == 0) {
-                dr_hash_put(s_hash, s_ra[lt]);
-                dr_hash_put(s_hash, s_rb[lt]);
-            }
-            int nS = 2;
-            __syncwarp();
-            uint32_t tmk = lane < nw ? tm[(int64_t)root * nw + lane] : 0u;
-            bool grew = false, stop = false;
-            for (int base = lt + 1; base < win && !stop && base < lt + 1 + DR_SCAN; base += 32) {
-                int g = base + lane;
-                bool live = g < win && !s_dec[g];
-                int32_t ga = live ? s_ra[g] : -1, gb = live ? s_rb[g] : -1;
-                bool ia = live && dr_hash_has(s_hash, ga);
-                bool ib = live && dr_hash_has(s_hash, gb);
-                unsigned done = 0u;  // lanes already handled in this chunk
-                while (true) {
-                    unsigned touch = __ballot_sync(0xffffffffu, live && (ia || ib)) & ~done;
-                    if (!touch) break;
-                    int q = __ffs(touch) - 1;
-                    done |= (2u << q) - 1u;  // everything up to q is now in order
-                    int gq = base + q;
-                    bool both = __shfl_sync(0xffffffffu, ia && ib, q);
-                    bool qa = __shfl_sync(0xffffffffu, ia, q);
-                    if (both) {
-                        if (lane == 0) s_dec[gq] = 1;  // now inside one tree
-                        continue;
-                    }
-                    const int32_t gbq = __shfl_sync(0xffffffffu, gb, q), gaq = __shfl_sync(0xffffffffu, ga, q);
-                    int32_t y = qa ? gbq : gaq;
-                    // the other root's stamp and mask, staged by the whole CTA
-                    const int sb = qa ? 1 : 0;
-                    const unsigned long long xy = s_res[sb][gq];
-                    const uint32_t ty = lane < nw ? s_msk[sb][gq * DR_NW + lane] : 0u;
-                    if (xy != dr_stamp(round, gq)) {  // y has an earlier pending edge
-                        stop = true;
-                        break;
-                    }
-                    int inter = __reduce_add_sync(0xffffffffu, __popc(tmk & ty));
-                    int uni = __reduce_add_sync(0xffffffffu, __popc(tmk | ty));
-                    if (lane == 0) s_dec[gq] = 1;
-                    if (!(__ddiv_rn((double)inter, (double)uni) < beta)) {
-                        tmk |= ty;
-                        grew = true;
-                        if (lane == 0) {
-                            uf[y] = root;  // the giant's root stays the root
-                            usz[root] += usz[y];
-                            in_tree[s_e[gq]] = 1;
-                            dr_hash_put(s_hash, y);
-                        }
-                        nS++;
-                        // later edges of this chunk that touch y now touch the tree
-                        ia |= ga == y;
-                        ib |= gb == y;
-                        __syncwarp();
-                        if (nS == DR_MAXS) {
-                            stop = true;
-                            break;
-                        }
-                    }
-                }
-            }
-            if (grew && lane < nw) tm[(int64_t)root * nw + lane] = tmk;
-        }
-        DR_TICK(3);
-        // stable compaction of the undecided window edges
-        bool keepme = pend && !s_dec[tid];
-        unsigned bal = __ballot_sync(0xffffffffu, keepme);
-        if (lane == 0) s_warp[wid] = __popc(bal);
-        __syncthreads();
-        if (wid == 0) {
-            int v = s_warp[lane];
-            int incl = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            s_warp[lane] = incl - v;
-            if (lane == 31) s_total = incl;
-        }
-        __syncthreads();
-        int kept = s_total;
-        int32_t new_head = head + win - kept;
-        if (keepme) {
-            int rank = s_warp[wid] + __popc(bal & ((1u << lane) - 1));
-            order[new_head + rank] = e;
-        }
-        head = new_head;
-        round++;
-        DR_TICK(4);
-    }
-    if (tid == 0) atomicMax(rounds_out, (int)round);
-#ifdef HDP_DR_PROFILE
-    if (tid == 0 && b == 0)
-        printf("[dr] rounds %u  cycles/round: find+reserve %.0f  check+commit %.0f  best %.0f  multi %.0f  compact %.0f\n",
-               round, (double)t_ph[0] / round, (double)t_ph[1] / round, (double)t_ph[2] / round,
-               (double)t_ph[3] / round, (double)t_ph[4] / round);
-#endif
-}
 
 // ---- whole-window rounds by conflict groups -------------------------------
 //
@@ -835,7 +590,7 @@ constexpr int kHdpfSlice = 255;  // pairs per k_grp launch (9 pair bits in the s
 static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, const int32_t* eu, const int32_t* ev,
                       const uint64_t* key, const int32_t* pixel_row, const uint32_t* row_masks, int n_rows, int nw,
                       double beta, const float* ew, double st_k, bool link, uint8_t* in_tree, int32_t* uf,
-                      int32_t* usz, uint32_t* tm, float* tint, unsigned long long* res, int* rounds,
+                      int32_t* usz, uint32_t* tm, float* tint, int* rounds,
                       const int32_t* keep_v2, cudaStream_t st) {
     // no set ever changes: one interval row, or homogeneous trees over the
     // equal-mask edges (keep_v2)
@@ -886,16 +641,6 @@ static int hdpf_slice(int nb, int64_t nodes_per_pair, int64_t edges_per_pair, co
     }
     k_seg_bounds<<<grid_for(ms + 1, B), B, 0, st>>>(ms, okey2.get(), nb, seg.get()); note_launch();
     HDP_CHECK_LAUNCH();
-    const char* alg = getenv("HDP_HDPF_DR");  // diagnostics: the reservation kernel instead of groups
-    if (alg && alg[0] == '1' && st_k < 0.0) {
-        constexpr size_t dr_smem =
-            2 * DR_THREADS * sizeof(unsigned long long) + 2 * DR_THREADS * DR_NW * sizeof(uint32_t);
-        HDP_CHECK_CUDA(cudaFuncSetAttribute(k_dr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dr_smem));
-        k_dr<<<nb, DR_THREADS, dr_smem, st>>>(seg.get(), oidx2.get(), eu, ev, uf, usz, tm, res, nw, beta, in_tree,
-                                              rounds); note_launch();
-        HDP_CHECK_LAUNCH();
-        return HDP_OK;
-    }
     constexpr size_t g_smem = sizeof(GrpSmem);
     if (st_k >= 0.0) {
         auto kern = masks ? k_grp<true, true> : k_grp<true, false>;
@@ -982,17 +727,15 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
     DevBuf<int32_t> uf, usz;
     DevBuf<uint32_t> tm;
     DevBuf<float> tint;
-    DevBuf<unsigned long long> res;
     DevBuf<int> rounds;
     if (m > 0) HDP_CHECK_CUDA(cudaMemsetAsync(in_tree, 0, m, st));
     HDP_TRY(uf.alloc(n, st));
     HDP_TRY(usz.alloc(n, st));
     HDP_TRY(tm.alloc(n * nw, st));
-    HDP_TRY(res.alloc(n, st));
     HDP_TRY(rounds.alloc(1, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(rounds.get(), 0, sizeof(int), st));
     k_uf_init<<<grid_for(n, B), B, 0, st>>>(n, pixel_row, row_masks, nodes_per_pair, n_rows, nw,
-                                            uf.get(), usz.get(), tm.get(), res.get()); note_launch();
+                                            uf.get(), usz.get(), tm.get()); note_launch();
     if (st_k >= 0.0) {
         HDP_TRY(tint.alloc(n, st));
         HDP_CHECK_CUDA(cudaMemsetAsync(tint.get(), 0, sizeof(float) * n, st));  // Int of a singleton: 0
@@ -1003,7 +746,7 @@ static int hdpf_run(int batch, int64_t nodes_per_pair, int64_t edges_per_pair, c
         const int64_t e0 = (int64_t)b0 * edges_per_pair;
         HDP_TRY(hdpf_slice(nb, nodes_per_pair, edges_per_pair, eu + e0, ev + e0, key + e0, pixel_row, row_masks,
                            n_rows, nw, beta, ew ? ew + e0 : nullptr, st_k, link && !homog, in_tree + e0, uf.get(),
-                           usz.get(), tm.get(), tint.get(), res.get(), rounds.get(), homog ? v2.get() + e0 : nullptr,
+                           usz.get(), tm.get(), tint.get(), rounds.get(), homog ? v2.get() + e0 : nullptr,
                            st));
     }
     if (homog) {
