@@ -70,6 +70,8 @@ struct AggArgs {
     unsigned long long* aggp;   // per segment: local map product P / Q (epoch-tagged)
     unsigned long long* carry;  // per (segment, lane): (epoch << 32 | f32 bits), the
                                 // epoch tag doubles as the readiness flag
+    unsigned long long* segf;   // per (segment, column group): (local map, inclusive carry)
+                                // published hints, epoch << 32 (the words above stay authoritative)
     unsigned epoch_up, epoch_down;
     int* tickets;        // per (phase, pass, group)
     int groups;  // 32-lane groups per node when sub == 32
@@ -603,99 +605,110 @@ __device__ __forceinline__ bool try_carry1(const unsigned long long* p, unsigned
     return (unsigned)(w >> 32) == epoch;
 }
 
-// Carry-in of a segment by decoupled look-back over the segments at offsets
-// dir, 2 dir, ... (toward the tail on the way up, toward the head on the way
-// down): stop at the first published inclusive carry (or past the path's end,
-// where the carry is `edge`), then apply the published local maps in between
-// in the serial chain's order, X = x_loc(k) + P(k) * X.  The arithmetic is
-// exactly the serial chain's, so the result does not depend on timing.
-// Probes kLB segments per step (all their words loaded before any test), so a
-// walk of d segments costs ~d / kLB memory latencies.
-// (per kernel: kLB probes cost 18 kLB registers; the up pass, which also holds
-// light-child rows, probes 2, the down pass 4 -- both stay at 5 CTAs / SM)
-#ifndef HDP_KLB_UP
-#define HDP_KLB_UP 2
-#endif
-#ifndef HDP_KLB_DOWN
-#define HDP_KLB_DOWN 4
-#endif
-constexpr int kLBUp = HDP_KLB_UP, kLBDown = HDP_KLB_DOWN;
-
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
     unsigned long long w;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
     return w;
 }
 
-template <int kLB>
-__device__ __forceinline__ float4 seg_lookback(const AggArgs& a, int64_t gseg, int dir, int kmax,
-                                               unsigned epoch, int jq, bool act, float4 edge) {
+// Carry-in of a segment by decoupled look-back over the segments at offsets
+// dir, 2 dir, ... (toward the tail on the way up, toward the head on the way
+// down).  The warp probes the hint flags of 32 predecessor segments at once
+// (lane i: the segment i + 1 further away), takes the first whose inclusive
+// carry is published -- or the path's end, where the carry is `edge` --
+// provided every local map in between is published, then applies those maps
+// in the serial chain's order, X = x_loc(k) + P(k) * X, so the result does not
+// depend on timing.  The maps are read in batches of kApply with their own
+// epoch tags checked (a hint is not ordered with the data it announces: a
+// word not there yet is waited for).
+#ifndef HDP_APPLY
+#define HDP_APPLY 4
+#endif
+constexpr int kApply = HDP_APPLY;
+__device__ __forceinline__ void wait_word(const unsigned long long* p, unsigned long long& w, unsigned epoch) {
+    while ((unsigned)(w >> 32) != epoch) {
+        __nanosleep(20);
+        w = ld_relaxed(p);
+    }
+}
+__device__ __forceinline__ float4 seg_lookback_w(const AggArgs& a, int64_t gseg, int dir, int kmax, unsigned epoch,
+                                                 int jq, bool act, float4 edge, int g) {
     const size_t lw = (size_t)a.max_mp;
-    int k = 1;
-    float4 X = edge;
-    while (k <= kmax) {
-        const int nb = min(kLB, kmax - k + 1);
-        unsigned long long wi[kLB][4], wa[kLB][4], wp[kLB];
-#pragma unroll
-        for (int j = 0; j < kLB; j++) {
-            const int64_t gk = gseg + (int64_t)dir * (k + min(j, nb - 1));
-            const unsigned long long* pi = a.carry + gk * lw + 4 * jq;
-            const unsigned long long* pa = a.agg + gk * lw + 4 * jq;
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                wi[j][c] = act ? ld_relaxed(pi + c) : ((unsigned long long)epoch << 32);
-                wa[j][c] = act ? ld_relaxed(pa + c) : ((unsigned long long)epoch << 32);
-            }
-            wp[j] = ld_relaxed(a.aggp + gk);
+    const int lane = threadIdx.x & 31;
+    int base = 1, kstop = kmax + 1;
+    while (base <= kmax) {
+        const int k = base + lane;
+        bool inc = true, agg = false;  // past the path's end: the edge value
+        if (k <= kmax) {
+            const unsigned long long* fp = a.segf + 2 * ((gseg + (int64_t)dir * k) * a.qgroups + g);
+            agg = (unsigned)(ld_relaxed(fp) >> 32) == epoch;
+            inc = (unsigned)(ld_relaxed(fp + 1) >> 32) == epoch;
         }
-        int stop = -1;   // first probed segment with an inclusive carry
-        int ready = 0;   // probed segments whose local map is published, in order
-        bool gap = false;
-#pragma unroll
-        for (int j = 0; j < kLB; j++) {
-            if (j >= nb || stop >= 0 || gap) continue;
-            bool iok = true, aok = (unsigned)(wp[j] >> 32) == epoch;
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                iok = iok && (unsigned)(wi[j][c] >> 32) == epoch;
-                aok = aok && (unsigned)(wa[j][c] >> 32) == epoch;
+        const unsigned binc = __ballot_sync(0xffffffffu, inc), bagg = __ballot_sync(0xffffffffu, agg);
+        const int t = binc ? __ffs(binc) - 1 : 32;
+        const unsigned need = t >= 32 ? 0xffffffffu : ((1u << t) - 1u);
+        if ((bagg & need) == need) {
+            if (t < 32) {
+                kstop = base + t;
+                break;
             }
-            if (__all_sync(0xffffffffu, iok)) {
-                stop = j;
-                X = make_float4(__uint_as_float((unsigned)wi[j][0]), __uint_as_float((unsigned)wi[j][1]),
-                                __uint_as_float((unsigned)wi[j][2]), __uint_as_float((unsigned)wi[j][3]));
-            } else if (__all_sync(0xffffffffu, aok)) {
-                ready = j + 1;
-            } else {
-                gap = true;
-            }
-        }
-        if (stop >= 0) {
-            k += stop;
-            break;
-        }
-        if (ready > 0) {
-            k += ready;
+            base += 32;  // 32 maps published: the inclusive carry is further away
             continue;
         }
-        __nanosleep(20);
+        __nanosleep(32);
     }
-    // k: offset of the stop (an inclusive carry, or kmax + 1 past the end)
-    for (int kk = k - 1; kk >= 1; kk--) {
-        const int64_t gk = gseg + (int64_t)dir * kk;
-        float4 xl = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        if (act) {
+    float4 X = edge;
+    if (kstop <= kmax && act) {
+        const unsigned long long* pi = a.carry + (gseg + (int64_t)dir * kstop) * lw + 4 * jq;
+        unsigned long long w[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) w[c] = ld_relaxed(pi + c);
+#pragma unroll
+        for (int c = 0; c < 4; c++) wait_word(pi + c, w[c], epoch);
+        X = make_float4(__uint_as_float((unsigned)w[0]), __uint_as_float((unsigned)w[1]),
+                        __uint_as_float((unsigned)w[2]), __uint_as_float((unsigned)w[3]));
+    }
+    for (int kb = kstop - 1; kb >= 1; kb -= kApply) {
+        const int nb = min(kApply, kb);
+        unsigned long long wa[kApply][4], wp[kApply];
+#pragma unroll
+        for (int j = 0; j < kApply; j++) {
+            if (j >= nb) break;
+            const int64_t gk = gseg + (int64_t)dir * (kb - j);
             const unsigned long long* pa = a.agg + gk * lw + 4 * jq;
-            xl = make_float4(__uint_as_float((unsigned)__ldcg(pa)), __uint_as_float((unsigned)__ldcg(pa + 1)),
-                             __uint_as_float((unsigned)__ldcg(pa + 2)), __uint_as_float((unsigned)__ldcg(pa + 3)));
+#pragma unroll
+            for (int c = 0; c < 4; c++) wa[j][c] = act ? ld_relaxed(pa + c) : ((unsigned long long)epoch << 32);
+            wp[j] = ld_relaxed(a.aggp + gk);
         }
-        const float P = __uint_as_float((unsigned)__ldcg(a.aggp + gk));
-        X.x = xl.x + P * X.x;
-        X.y = xl.y + P * X.y;
-        X.z = xl.z + P * X.z;
-        X.w = xl.w + P * X.w;
+#pragma unroll
+        for (int j = 0; j < kApply; j++) {
+            if (j >= nb) break;
+            const int64_t gk = gseg + (int64_t)dir * (kb - j);
+            if (act) {
+                const unsigned long long* pa = a.agg + gk * lw + 4 * jq;
+#pragma unroll
+                for (int c = 0; c < 4; c++) wait_word(pa + c, wa[j][c], epoch);
+            }
+            wait_word(a.aggp + gk, wp[j], epoch);
+            const float P = __uint_as_float((unsigned)wp[j]);
+            X.x = __uint_as_float((unsigned)wa[j][0]) + P * X.x;
+            X.y = __uint_as_float((unsigned)wa[j][1]) + P * X.y;
+            X.z = __uint_as_float((unsigned)wa[j][2]) + P * X.z;
+            X.w = __uint_as_float((unsigned)wa[j][3]) + P * X.w;
+        }
     }
     return X;
+}
+
+// hint flags of this warp's (segment, column group): 0 = local map, 1 =
+// inclusive carry (after the warp's lanes stored their words)
+__device__ __forceinline__ void put_segf(const AggArgs& a, int64_t gseg, int g, int which, unsigned epoch) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long* fp = a.segf + 2 * (gseg * a.qgroups + g) + which;
+        const unsigned long long w = (unsigned long long)epoch << 32;
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(fp), "l"(w) : "memory");
+    }
 }
 
 // warp-uniform index i in [0, 32]: value of node a + i held in lane i of lo
@@ -879,18 +892,23 @@ __device__ __forceinline__ void seg_up_item(const AggArgs& a, const SegCtx& c, i
         }
         if (act) put_carry4(a.agg + c.gseg * a.max_mp + 4 * jq, a.epoch_up, x);
         if (lane == 0) put_carry(a.aggp + c.gseg, a.epoch_up, P);
+        put_segf(a, c.gseg, g, 0, a.epoch_up);
     }
     PROF_T(3);
     float4 Xb = z;
-    if (has_next) Xb = seg_lookback<kLBUp>(a, c.gseg, +1, c.nseg - 1 - c.s, a.epoch_up, jq, act, z);
+    if (has_next)
+        Xb = seg_lookback_w(a, c.gseg, +1, c.nseg - 1 - c.s, a.epoch_up, jq, act, z, g);
     PROF_T(4);
-    if (act && c.s > 0) {
-        float4 o;
-        o.x = x.x + P * Xb.x;
-        o.y = x.y + P * Xb.y;
-        o.z = x.z + P * Xb.z;
-        o.w = x.w + P * Xb.w;
-        put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_up, o);
+    if (c.s > 0) {
+        if (act) {
+            float4 o;
+            o.x = x.x + P * Xb.x;
+            o.y = x.y + P * Xb.y;
+            o.z = x.z + P * Xb.z;
+            o.w = x.w + P * Xb.w;
+            put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_up, o);
+        }
+        put_segf(a, c.gseg, g, 1, a.epoch_up);
     }
     // final pass: exact recurrence from the true X_b
     float4* rows = reinterpret_cast<float4*>(a.aup + c.rowa) + jq;
@@ -974,17 +992,21 @@ __device__ __forceinline__ void seg_down_item(const AggArgs& a, const SegCtx& c,
         }
         if (act) put_carry4(a.agg + c.gseg * a.max_mp + 4 * jq, a.epoch_down, yl);
         if (lane == 0) put_carry(a.aggp + c.gseg, a.epoch_down, Q);
+        put_segf(a, c.gseg, g, 0, a.epoch_down);
     }
     PROF_T(2);
-    const float4 Yin = c.s == 0 ? Ypar : seg_lookback<kLBDown>(a, c.gseg, -1, c.s, a.epoch_down, jq, act, Ypar);
+    const float4 Yin = c.s == 0 ? Ypar : seg_lookback_w(a, c.gseg, -1, c.s, a.epoch_down, jq, act, Ypar, g);
     PROF_T(3);
-    if (act && c.s + 1 < c.nseg) {
-        float4 o;
-        o.x = yl.x + Q * Yin.x;
-        o.y = yl.y + Q * Yin.y;
-        o.z = yl.z + Q * Yin.z;
-        o.w = yl.w + Q * Yin.w;
-        put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_down, o);
+    if (c.s + 1 < c.nseg) {
+        if (act) {
+            float4 o;
+            o.x = yl.x + Q * Yin.x;
+            o.y = yl.y + Q * Yin.y;
+            o.z = yl.z + Q * Yin.z;
+            o.w = yl.w + Q * Yin.w;
+            put_carry4(a.carry + c.gseg * a.max_mp + 4 * jq, a.epoch_down, o);
+        }
+        put_segf(a, c.gseg, g, 1, a.epoch_down);
     }
     float4* rows = reinterpret_cast<float4*>(a.aup + c.rowa) + jq;
     float4 y = Yin;
@@ -1736,6 +1758,9 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     a.max_m = f->max_m;
     a.max_mp = (f->max_m + 3) & ~3;
     a.qgroups = (a.max_mp / 4 + 31) / 32;
+    DevBuf<unsigned long long> segfb;
+    HDP_TRY(segfb.alloc(2 * f->n_segs * std::max(a.qgroups, 1) + 2, st));
+    a.segf = segfb.get();
     a.sub = f->max_m <= 16 ? std::max(4, pow2_at_least(f->max_m)) : 32;  // >= one padded row
     a.sub_shift = 0;
     while ((1 << a.sub_shift) < a.sub) a.sub_shift++;
