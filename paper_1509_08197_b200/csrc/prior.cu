@@ -32,6 +32,10 @@ struct PriorArgs {
     const double2* pl;  // left: (u0, u1) plane, then the (u2, grad) plane
     const double2* pr;
     int64_t plane;      // elements per plane
+    // filter-and-verify (7 x 7, d_max < 256): the same records rounded to f32
+    const float4* pl32;
+    const float4* pr32;
+    float eps32;        // f32 window means within eps32 of the f32 minimum are verified in f64
 };
 
 __global__ void k_pack_px(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
@@ -40,6 +44,15 @@ __global__ void k_pack_px(const double* __restrict__ u, const double* __restrict
     if (i >= n) return;
     out[i] = make_double2(u[i * c], c > 1 ? u[i * c + 1] : 0.0);
     out[n + i] = make_double2(c > 2 ? u[i * c + 2] : 0.0, g[i]);
+}
+
+// f32 copies of the records (u0, u1, u2, grad) for the filter pass
+__global__ void k_pack_px32(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
+                            float4* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = make_float4((float)u[i * c], c > 1 ? (float)u[i * c + 1] : 0.0f, c > 2 ? (float)u[i * c + 2] : 0.0f,
+                         (float)g[i]);
 }
 
 // 3 channels, two pixels per thread with 16-byte loads and stores (the planes
@@ -234,6 +247,123 @@ __device__ __forceinline__ double window_at(const double4* win, const double2* d
     return div_rn_by(__dadd_rn(res, last), 49.0, inv_win);
 }
 
+// Filter-and-verify WTA (exact): every disparity's 7 x 7 window mean is
+// first computed in f32 from f32-rounded records; the f64 argmin (first
+// minimum) is among the disparities whose f32 mean lies within eps32 of the
+// f32 minimum, because |mean32 - mean64| <= eps32 / 2 for every disparity
+// (inputs in [0, 1] / [-1, 1]: per element <= 4e-7 through the truncated
+// colour and gradient terms, <= 2e-5 over the 49-value sum, < 5e-7 on the
+// mean; eps32 = 1e-5 scaled by the border cost); only those candidates are
+// evaluated in f64 in numpy's order (window_at), and the first minimum among
+// them is the f64 first minimum over all disparities.
+template <int C>
+__device__ __forceinline__ float rec_cost32(const float4 L, const float4 R, float tc, float tg, float oma, float al) {
+    float acc = fabsf(L.x - R.x);
+    if (C > 1) acc += fabsf(L.y - R.y);
+    if (C > 2) acc += fabsf(L.z - R.z);
+    const float color = acc * (1.0f / (float)C);
+    return oma * fminf(color, tc) + al * fminf(fabsf(L.w - R.w), tg);
+}
+
+constexpr int kFiltMax = 256;  // disparities per warp in the filter's shared arrays
+
+template <int C>
+__device__ int warp_wta7_filter(const PriorArgs& a, const double2* src, const double2* dst, const float4* src32,
+                                const float4* dst32, int64_t base, int cr, int cc, int sign, double4* win,
+                                float4* win32, float* c32, int* cand) {
+    const int lane = threadIdx.x & 31;
+    int rowo[7], colv[7];
+#pragma unroll
+    for (int i = 0; i < 7; i++) {
+        rowo[i] = min(max(cr + i - 3, 0), a.h - 1) * a.w;
+        colv[i] = min(max(cc + i - 3, 0), a.w - 1);
+    }
+    for (int q = lane; q < 49; q += 32) {
+        const int dr = q / 7, dc = q - 7 * dr;
+        const int64_t px = base + (int64_t)rowo[dr] + colv[dc];
+        win[q] = ld_rec(src, a.plane, px);
+        win32[q] = __ldg(src32 + px);
+    }
+    __syncwarp();
+    const int w = a.w, h = a.h, d_max = a.d_max;
+    const float tc = (float)a.tc, tg = (float)a.tg, oma = (float)a.one_minus_alpha, al = (float)a.alpha;
+    const float border32 = (float)a.border;
+    const float4* db32 = dst32 + base;
+    // pass 1: f32 window means of every disparity
+    float mn = __int_as_float(0x7f800000);
+    for (int x0 = 0; x0 <= d_max; x0 += 32) {
+        const int x = x0 + lane;
+        const int off = sign * min(x, d_max);
+        float acc[7];  // one running sum per window column (independent chains)
+#pragma unroll
+        for (int dc = 0; dc < 7; dc++) acc[dc] = 0.0f;
+#pragma unroll 1
+        for (int dr = 0; dr < 7; dr++) {
+            const int ro = rowo[dr];
+#pragma unroll
+            for (int dc = 0; dc < 7; dc++) {
+                const int dcol = colv[dc] + off;
+                acc[dc] += (dcol >= 0 && dcol < w) ? rec_cost32<C>(win32[7 * dr + dc], __ldg(db32 + ro + dcol), tc,
+                                                                   tg, oma, al)
+                                                   : border32;
+            }
+        }
+        const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + acc[6]);
+        const float m = sum * (1.0f / 49.0f);
+        if (x <= d_max) {
+            c32[x] = m;
+            mn = fminf(mn, m);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    __syncwarp();
+    // pass 2: candidates, compacted in ascending disparity order
+    const float thr = mn + a.eps32;
+    int ncand = 0;
+    for (int x0 = 0; x0 <= d_max; x0 += 32) {
+        const int x = x0 + lane;
+        const bool is = x <= d_max && c32[x] <= thr;
+        const unsigned bal = __ballot_sync(0xffffffffu, is);
+        if (is) cand[ncand + __popc(bal & ((1u << lane) - 1u))] = x;
+        ncand += __popc(bal);
+    }
+    __syncwarp();
+    // pass 3: exact f64 means of the candidates, first minimum
+    const double2* db = dst + base;
+    const int64_t plane = a.plane;
+    const double dtc = a.tc, dtg = a.tg, doma = a.one_minus_alpha, dal = a.alpha, border = a.border;
+    const double inv_c = a.inv_c, inv_win = a.inv_win;
+    const int safe = sign < 0 ? colv[0] : a.w - 1 - colv[6];
+    double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    int bx = 0x7fffffff;
+    for (int i0 = 0; i0 < ncand; i0 += 32) {
+        const bool ok = i0 + lane < ncand;
+        const int x = cand[ok ? i0 + lane : i0];
+        const bool fast = __all_sync(0xffffffffu, x <= safe);
+        const int off = sign * x;
+        const double v = fast ? window_at<C, true>(win, db, plane, rowo[0], colv, off, cr, h, w, dtc, dtg, doma, dal,
+                                                   inv_c, inv_win, border)
+                              : window_at<C, false>(win, db, plane, rowo[0], colv, off, cr, h, w, dtc, dtg, doma,
+                                                    dal, inv_c, inv_win, border);
+        if (ok && (v < best || (v == best && x < bx))) {
+            best = v;
+            bx = x;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+        if (ob < best || (ob == best && ox < bx)) {
+            best = ob;
+            bx = ox;
+        }
+    }
+    __syncwarp();  // the shared arrays are rewritten by the next call
+    return bx;
+}
+
 template <int C>
 __device__ int warp_wta7(const PriorArgs& a, const double2* src, const double2* dst, int64_t base, int cr, int cc,
                          int sign, double4* win) {
@@ -285,8 +415,15 @@ __device__ int warp_wta7(const PriorArgs& a, const double2* src, const double2* 
     return bx;
 }
 
+struct FiltSmem {
+    float4 win32[49];
+    float c32[kFiltMax];
+    int cand[kFiltMax];
+};
+
 template <int W7>  // 0: any window; 1 / 3: 7 x 7 window, 1 / 3 channels
-__device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, int64_t wid, double4* win) {
+__device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, int64_t wid, double4* win,
+                                             FiltSmem* fs) {
     int b = (int)(wid / per);
     int k = (int)(wid % per);
     int i = k / a.ncc, j = k % a.ncc;
@@ -295,13 +432,23 @@ __device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, in
     int cc = (cs + min(cs + a.stride, a.w) - 1) / 2;
     int64_t base = (int64_t)b * a.h * a.w;
     int dl;
-    if constexpr (W7 > 0) dl = warp_wta7<W7>(a, a.pl, a.pr, base, cr, cc, -1, win);
-    else dl = warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
+    if constexpr (W7 > 0) {
+        dl = a.pl32 ? warp_wta7_filter<W7>(a, a.pl, a.pr, a.pl32, a.pr32, base, cr, cc, -1, win, fs->win32, fs->c32,
+                                           fs->cand)
+                    : warp_wta7<W7>(a, a.pl, a.pr, base, cr, cc, -1, win);
+    } else {
+        dl = warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
+    }
     int mc = cc - dl;
     if (mc < 0) return;  // infeasible (hdp_model.py:458-459)
     int dr;
-    if constexpr (W7 > 0) dr = warp_wta7<W7>(a, a.pr, a.pl, base, cr, mc, +1, win);
-    else dr = warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
+    if constexpr (W7 > 0) {
+        dr = a.pl32 ? warp_wta7_filter<W7>(a, a.pr, a.pl, a.pr32, a.pl32, base, cr, mc, +1, win, fs->win32, fs->c32,
+                                           fs->cand)
+                    : warp_wta7<W7>(a, a.pr, a.pl, base, cr, mc, +1, win);
+    } else {
+        dr = warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
+    }
     int diff = dl - dr;
     if (diff < 0) diff = -diff;
     if ((threadIdx.x & 31) == 0 && diff <= a.max_offset) {
@@ -318,9 +465,10 @@ __global__ void __launch_bounds__(256, HDP_PRIOR_MINB) k_prior(PriorArgs a, int 
     const int64_t per = (int64_t)a.nrc * a.ncc;
     const int64_t nwarp = (int64_t)gridDim.x * (blockDim.x >> 5);
     __shared__ double4 win[kPriorWarps][49];  // the 7 x 7 path's staged window, per warp
+    __shared__ FiltSmem fsm[W7 > 0 ? kPriorWarps : 1];  // the filter pass (7 x 7)
     // grid-stride over sample centres (a capped grid leaves SMs to other streams)
     for (int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wid < per * batch; wid += nwarp)
-        prior_centre<W7>(a, per, wid, win[threadIdx.x >> 5]);
+        prior_centre<W7>(a, per, wid, win[threadIdx.x >> 5], &fsm[W7 > 0 ? threadIdx.x >> 5 : 0]);
 }
 // numpy's pairwise_sum (eight accumulators for blocks <= 128, halves rounded
 // to multiples of 8 above; oracle/hdp_oracle.c np_pairwise): sequential
@@ -574,6 +722,24 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
         }
         a.pl = pk.get();
         a.pr = pk.get() + 2 * n;
+    }
+    DevBuf<float4> pk32;
+    a.pl32 = a.pr32 = nullptr;
+    a.eps32 = 0.0f;
+    {
+        const char* e = getenv("HDP_PRIOR_FILTER");  // diagnostics / tests: 0 = every disparity in f64
+        const bool filt = !(e && e[0] == '0');
+        // the f32 error bound assumes unit-scaled inputs (|u|, |grad| <= 1)
+        // and the default-sized truncations; eps32 scales with the border cost
+        if (filt && window == 7 && d_max < kFiltMax && a.border > 0.0 && a.border < 1.0) {
+            const int64_t n = a.plane;
+            HDP_TRY(pk32.alloc(2 * n, st));
+            k_pack_px32<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk32.get()); note_launch();
+            k_pack_px32<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk32.get() + n); note_launch();
+            a.pl32 = pk32.get();
+            a.pr32 = pk32.get() + n;
+            a.eps32 = (float)(1e-5 * std::max(1.0, a.border / 0.00977));
+        }
     }
     if (window == 7 && c == 3)
         k_prior<3><<<grid, 256, 0, st>>>(a, batch);

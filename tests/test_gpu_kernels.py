@@ -275,3 +275,27 @@ def test_device_bayes_matches_host(d_child, d_parent):
     cd = torch.from_numpy(np.ascontiguousarray(cond)).cuda()
     got = E.bayes_device(torch.from_numpy(counts).cuda(), torch.from_numpy(kept).cuda(), cd)
     np.testing.assert_array_equal(got.cpu().numpy(), bm)
+
+
+@pytest.mark.parametrize("cid,levels", [(2, 3), (4, 5)])
+def test_prior_filter_equals_full_f64(cid, levels, monkeypatch):
+    """The prior's f32 filter + f64 verification (default) gives the same
+    histograms as evaluating every disparity in f64 (HDP_PRIOR_FILTER=0), on
+    every pyramid level of a full-size pair of the configuration."""
+    import torch
+
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import CONFIGS, make_scene
+
+    spec = CONFIGS[cid]
+    sc = [make_scene(spec, i) for i in range(2)]
+    L = torch.from_numpy(np.stack([s.pair.left.data for s in sc])).cuda()
+    R = torch.from_numpy(np.stack([s.pair.right.data for s in sc])).cuda()
+    lv = E.build_levels(L, R, spec.d_max, levels, 2, True)
+    for lev in lv[:-1]:
+        monkeypatch.setenv("HDP_PRIOR_FILTER", "1")
+        c1, k1 = E.prior_counts(lev)
+        monkeypatch.setenv("HDP_PRIOR_FILTER", "0")
+        c0, k0 = E.prior_counts(lev)
+        np.testing.assert_array_equal(c1.cpu().numpy(), c0.cpu().numpy())
+        np.testing.assert_array_equal(k1.cpu().numpy(), k0.cpu().numpy())
