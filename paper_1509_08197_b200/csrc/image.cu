@@ -25,6 +25,12 @@ void keep_pool_memory() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // no hidden cross-stream waits: the pool may otherwise hand a block
+        // freed on one stream (the HDP prior's side stream, say) to another
+        // after inserting a wait on the first stream's pending work, which
+        // stalls the level loop behind a long kernel it never depends on
+        int no = 0;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     done_dev = dev;
 }
