@@ -354,6 +354,7 @@ class Runner:
         self.lib = _lib.load()
         self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
         self.args = args
+        self.cpu_todo = []
 
     def timed(self, fn, steps, warmup):
         """Device-timed steps (CUDA events on the current stream), L2 flushed
@@ -438,7 +439,8 @@ class Runner:
         pairs_done = B if slabs else self.world * B
         out = {
             "value": units * steps / t_dev / 1e9, "unit": "Gpd/s",
-            "ms_per_step": t_dev / steps * 1e3, "pairs_per_s": pairs_done * steps / t_dev,
+            "ms_per_step": t_dev / steps * 1e3, "ms_steps": [round(x, 3) for x in dev_ms],
+            "pairs_per_s": pairs_done * steps / t_dev,
             "scaling": "strong" if slabs else "weak",
             "config": config_dict(name, self.world, B),
             "e2e": {"value": units * steps / t_e2e / 1e9, "unit": "Gpd/s",
@@ -463,7 +465,7 @@ class Runner:
             "algorithmic_bytes_rule": "8 B per hypothesis (A-up written + read) + 30 B per pixel",
             "share_of_step": t_agg * 1e3 / (t_dev / steps * 1e3)}
         if with_cpu:
-            out["cpu_baseline"] = cpu_leg(name, Lh, Rh, spec)
+            self.cpu_todo.append((out, name, Lh, Rh, spec))
         return out
 
     # ---- HDP legs
@@ -515,7 +517,9 @@ class Runner:
         npx = spec.height * spec.width
         out = {
             "value": self.world * hyps * steps / t_dev / 1e9, "unit": "Gpd/s",
-            "ms_per_step": t_dev / steps * 1e3, "pairs_per_s": self.world * B * steps / t_dev,
+            "ms_per_step": t_dev / steps * 1e3, "ms_steps": [round(x, 3) for x in dev_ms],
+            "e2e_ms_steps": [round(x, 3) for x in e2e_ms],
+            "pairs_per_s": self.world * B * steps / t_dev,
             "dense_equivalent_gpd_s": self.world * B * npx * (spec.d_max + 1) * steps / t_dev / 1e9,
             "scaling": "weak", "config": config_dict(name, self.world, B),
             "hyps_per_step": hyps, "levels": wl["levels"],
@@ -538,8 +542,15 @@ class Runner:
             "accuracy": accuracy(scenes, info["final"]),
         }
         if with_cpu:
-            out["cpu_baseline"] = cpu_leg(name, Lh, Rh, spec)
+            self.cpu_todo.append((out, name, Lh, Rh, spec))
         return out
+
+    def run_cpu_legs(self):
+        """The CPU baselines run after every GPU leg has been timed, so that no
+        host thread pool is busy (or winding down) beside a timed GPU step."""
+        for out, name, Lh, Rh, spec in self.cpu_todo:
+            out["cpu_baseline"] = cpu_leg(name, Lh, Rh, spec)
+        self.cpu_todo = []
 
     def leg(self, name, steps, warmup, with_cpu):
         if WORKLOADS[name]["kind"] == "dense":
@@ -561,6 +572,7 @@ def run_ours(args):
         if r.dist:
             r.dist.destroy_process_group()
         return
+    r.run_cpu_legs()
     line = {
         "metric": METRIC, "value": head["value"], "unit": "Gpd/s", "n_gpus": r.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],

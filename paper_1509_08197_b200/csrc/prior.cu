@@ -36,6 +36,11 @@ struct PriorArgs {
     const float4* pl32;
     const float4* pr32;
     float eps32;        // f32 window means within eps32 of the f32 minimum are verified in f64
+    // u8 filter records (level 0: every unit value is k / 255): (packed channel bytes, f32 gradient);
+    // *nonint != 0 when some value is not a multiple of 1 / 255 (the kernel then filters from pl32)
+    const uint2* pl8;
+    const uint2* pr8;
+    const int* nonint;
 };
 
 __global__ void k_pack_px(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
@@ -53,6 +58,25 @@ __global__ void k_pack_px32(const double* __restrict__ u, const double* __restri
     if (i >= n) return;
     out[i] = make_float4((float)u[i * c], c > 1 ? (float)u[i * c + 1] : 0.0f, c > 2 ? (float)u[i * c + 2] : 0.0f,
                          (float)g[i]);
+}
+
+// The same records with the channels as bytes, for images whose unit values are
+// k / 255 (level 0 of a uint8 pair): RN(k / 255) * 255 is within an ulp of k,
+// so rint recovers k exactly; any other value raises *nonint.
+__global__ void k_pack_px8(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
+                           uint2* __restrict__ out, int* __restrict__ nonint) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned pk = 0;
+    bool bad = false;
+    for (int k = 0; k < c; k++) {
+        const double v = u[i * c + k] * 255.0;
+        const double r = rint(v);
+        bad = bad || !(fabs(v - r) <= 1e-9) || r < 0.0 || r > 255.0;
+        pk |= (unsigned)(bad ? 0 : (int)r) << (8 * k);
+    }
+    out[i] = make_uint2(pk, __float_as_uint((float)g[i]));
+    if (bad) *nonint = 1;
 }
 
 // 3 channels, two pixels per thread with 16-byte loads and stores (the planes
@@ -265,12 +289,51 @@ __device__ __forceinline__ float rec_cost32(const float4 L, const float4 R, floa
     return oma * fminf(color, tc) + al * fminf(fabsf(L.w - R.w), tg);
 }
 
+// u8 records: the channel sum of absolute differences is one VABSDIFF4 with
+// the accumulator preloaded with the bits of 2^23, so the result reads as the
+// float 2^23 + SAD (exact, SAD <= 765); tcs = tc * 255 C, omas = (1 - alpha) / (255 C)
+__device__ __forceinline__ float rec_cost8(const uint2 L, const uint2 R, float tcs, float tg, float omas, float al,
+                                           float acc) {
+    unsigned r;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(r) : "r"(L.x), "r"(R.x), "r"(0x4B000000u));
+    const float sad = __uint_as_float(r) - 8388608.0f;
+    const float g = fabsf(__uint_as_float(L.y) - __uint_as_float(R.y));
+    acc = fmaf(omas, fminf(sad, tcs), acc);
+    return fmaf(al, fminf(g, tg), acc);
+}
+
 constexpr int kFiltMax = 256;  // disparities per warp in the filter's shared arrays
+
+// One candidate's exact f64 window mean with the 49 elements spread over the
+// lanes: lane q holds element q (eA) and, for q <= 16, element 32 + q (eB).
+// numpy's order: accumulator k = ((((e_k + e_{k+8}) + e_{k+16}) + e_{k+24}) +
+// e_{k+32}) + e_{k+40}, then ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) (xor
+// shuffles: IEEE addition is commutative), + e_48, / 49.  Valid on every lane.
+__device__ __forceinline__ double window_mean_lanes(double eA, double eB, double inv_win) {
+    const unsigned full = 0xffffffffu;
+    const int k = threadIdx.x & 7;
+    double s = __shfl_sync(full, eA, k);
+    s = __dadd_rn(s, __shfl_sync(full, eA, k + 8));
+    s = __dadd_rn(s, __shfl_sync(full, eA, k + 16));
+    s = __dadd_rn(s, __shfl_sync(full, eA, k + 24));
+    s = __dadd_rn(s, __shfl_sync(full, eB, k));
+    s = __dadd_rn(s, __shfl_sync(full, eB, k + 8));
+    s = __dadd_rn(s, __shfl_xor_sync(full, s, 1));
+    s = __dadd_rn(s, __shfl_xor_sync(full, s, 2));
+    s = __dadd_rn(s, __shfl_xor_sync(full, s, 4));
+    const double last = __shfl_sync(full, eB, 16);
+    return div_rn_by(__dadd_rn(s, last), 49.0, inv_win);
+}
+
+// candidates above this count are verified one per lane (window_at), fewer with
+// the window's elements spread over the lanes (window_mean_lanes)
+constexpr int kLaneVerifyMax = 12;
 
 template <int C>
 __device__ int warp_wta7_filter(const PriorArgs& a, const double2* src, const double2* dst, const float4* src32,
-                                const float4* dst32, int64_t base, int cr, int cc, int sign, double4* win,
-                                float4* win32, float* c32, int* cand) {
+                                const float4* dst32, const uint2* src8, const uint2* dst8, bool use8,
+                                int64_t base, int cr, int cc, int sign, double4* win,
+                                float4* win32, uint2* win8, float* c32, int* cand) {
     const int lane = threadIdx.x & 31;
     int rowo[7], colv[7];
 #pragma unroll
@@ -282,37 +345,136 @@ __device__ int warp_wta7_filter(const PriorArgs& a, const double2* src, const do
         const int dr = q / 7, dc = q - 7 * dr;
         const int64_t px = base + (int64_t)rowo[dr] + colv[dc];
         win[q] = ld_rec(src, a.plane, px);
-        win32[q] = __ldg(src32 + px);
+        if (use8) win8[q] = __ldg(src8 + px);
+        else win32[q] = __ldg(src32 + px);
     }
     __syncwarp();
     const int w = a.w, h = a.h, d_max = a.d_max;
     const float tc = (float)a.tc, tg = (float)a.tg, oma = (float)a.one_minus_alpha, al = (float)a.alpha;
     const float border32 = (float)a.border;
-    const float4* db32 = dst32 + base;
+    // disparities whose matched columns are inside the image for every element
+    const int safe = sign < 0 ? colv[0] : a.w - 1 - colv[6];
     // pass 1: f32 window means of every disparity
     float mn = __int_as_float(0x7f800000);
-    for (int x0 = 0; x0 <= d_max; x0 += 32) {
-        const int x = x0 + lane;
-        const int off = sign * min(x, d_max);
-        float acc[7];  // one running sum per window column (independent chains)
+    if (use8) {
+        const float tcs = (float)(a.tc * 255.0 * C), omas = (float)(a.one_minus_alpha / (255.0 * C));
+        const uint2* db8 = dst8 + base;
+        const bool interior = cc - 3 >= 0 && cc + 3 <= w - 1;  // the window's columns are consecutive
+        // four 32-disparity blocks per round share the window's left records
+        for (int xg = 0; xg <= d_max; xg += 128) {
+            float acc[4];
+            int off[4];
 #pragma unroll
-        for (int dc = 0; dc < 7; dc++) acc[dc] = 0.0f;
+            for (int u = 0; u < 4; u++) {
+                acc[u] = 0.0f;
+                off[u] = sign * min(xg + 32 * u + lane, d_max);
+            }
+            // warp-uniform: every active block of the round stays inside the image
+            const bool fast = interior && min(xg + 127, d_max) <= safe;
+            if (fast && xg + 96 <= d_max) {
+                // four active blocks: software-pipelined, the next block's matched
+                // records are in flight while this block's costs are evaluated
+                uint2 Ra[7], Rb[7];
+                {
+                    const uint2* rp = db8 + min(max(cr - 3, 0), h - 1) * w + (cc - 3) + off[0];
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(rp + dc);
+                }
 #pragma unroll 1
-        for (int dr = 0; dr < 7; dr++) {
-            const int ro = rowo[dr];
+                for (int dr = 0; dr < 7; dr++) {
+                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w + (cc - 3);
+                    const int ron = min(max(cr + min(dr + 1, 6) - 3, 0), h - 1) * w + (cc - 3);
+                    uint2 Lr[7];
 #pragma unroll
-            for (int dc = 0; dc < 7; dc++) {
-                const int dcol = colv[dc] + off;
-                acc[dc] += (dcol >= 0 && dcol < w) ? rec_cost32<C>(win32[7 * dr + dc], __ldg(db32 + ro + dcol), tc,
-                                                                   tg, oma, al)
-                                                   : border32;
+                    for (int dc = 0; dc < 7; dc++) Lr[dc] = win8[7 * dr + dc];
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Rb[dc] = __ldg(db8 + ro + off[1] + dc);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[0] = rec_cost8(Lr[dc], Ra[dc], tcs, tg, omas, al, acc[0]);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(db8 + ro + off[2] + dc);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[1] = rec_cost8(Lr[dc], Rb[dc], tcs, tg, omas, al, acc[1]);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Rb[dc] = __ldg(db8 + ro + off[3] + dc);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[2] = rec_cost8(Lr[dc], Ra[dc], tcs, tg, omas, al, acc[2]);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(db8 + ron + off[0] + dc);  // row 6: reloaded, unused
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[3] = rec_cost8(Lr[dc], Rb[dc], tcs, tg, omas, al, acc[3]);
+                }
+            } else if (fast) {
+#pragma unroll 1
+                for (int dr = 0; dr < 7; dr++) {
+                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w + (cc - 3);
+                    uint2 Lr[7];
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Lr[dc] = win8[7 * dr + dc];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (xg + 32 * u <= d_max) {
+                            const uint2* rp = db8 + ro + off[u];
+#pragma unroll
+                            for (int dc = 0; dc < 7; dc++)
+                                acc[u] = rec_cost8(Lr[dc], __ldg(rp + dc), tcs, tg, omas, al, acc[u]);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int dr = 0; dr < 7; dr++) {
+                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w;
+#pragma unroll 1
+                    for (int dc = 0; dc < 7; dc++) {
+                        const uint2 Lq = win8[7 * dr + dc];
+                        const int col = min(max(cc + dc - 3, 0), w - 1);
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int dcol = col + off[u];
+                            if (dcol >= 0 && dcol < w)
+                                acc[u] = rec_cost8(Lq, __ldg(db8 + ro + dcol), tcs, tg, omas, al, acc[u]);
+                            else
+                                acc[u] += border32;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int x = xg + 32 * u + lane;
+                if (x <= d_max) {
+                    const float m = acc[u] * (1.0f / 49.0f);
+                    c32[x] = m;
+                    mn = fminf(mn, m);
+                }
             }
         }
-        const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + acc[6]);
-        const float m = sum * (1.0f / 49.0f);
-        if (x <= d_max) {
-            c32[x] = m;
-            mn = fminf(mn, m);
+    } else {
+        const float4* db32 = dst32 + base;
+        for (int x0 = 0; x0 <= d_max; x0 += 32) {
+            const int x = x0 + lane;
+            const int off = sign * min(x, d_max);
+            float acc[7];  // one running sum per window column (independent chains)
+#pragma unroll
+            for (int dc = 0; dc < 7; dc++) acc[dc] = 0.0f;
+#pragma unroll 1
+            for (int dr = 0; dr < 7; dr++) {
+                const int ro = rowo[dr];
+#pragma unroll
+                for (int dc = 0; dc < 7; dc++) {
+                    const int dcol = colv[dc] + off;
+                    acc[dc] += (dcol >= 0 && dcol < w) ? rec_cost32<C>(win32[7 * dr + dc], __ldg(db32 + ro + dcol), tc,
+                                                                       tg, oma, al)
+                                                       : border32;
+                }
+            }
+            const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + acc[6]);
+            const float m = sum * (1.0f / 49.0f);
+            if (x <= d_max) {
+                c32[x] = m;
+                mn = fminf(mn, m);
+            }
         }
     }
 #pragma unroll
@@ -334,9 +496,31 @@ __device__ int warp_wta7_filter(const PriorArgs& a, const double2* src, const do
     const int64_t plane = a.plane;
     const double dtc = a.tc, dtg = a.tg, doma = a.one_minus_alpha, dal = a.alpha, border = a.border;
     const double inv_c = a.inv_c, inv_win = a.inv_win;
-    const int safe = sign < 0 ? colv[0] : a.w - 1 - colv[6];
     double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     int bx = 0x7fffffff;
+    if (ncand <= kLaneVerifyMax) {
+        // few candidates (the usual case): one at a time, elements over the lanes
+        const int qB = min(32 + lane, 48);
+        const int drA = lane / 7, dcA = lane - 7 * drA, drB = qB / 7, dcB = qB - 7 * drB;
+        const int roA = min(max(cr + drA - 3, 0), h - 1) * w, roB = min(max(cr + drB - 3, 0), h - 1) * w;
+        const int colA = min(max(cc + dcA - 3, 0), w - 1), colB = min(max(cc + dcB - 3, 0), w - 1);
+        const double4 LA = win[lane], LB = win[qB];
+        for (int i = 0; i < ncand; i++) {
+            const int x = cand[i];
+            const int da = colA + sign * x, dbc = colB + sign * x;
+            double eA = border, eB = border;
+            if (da >= 0 && da < w) eA = rec_cost<C>(LA, ld_rec(db, plane, roA + da), dtc, dtg, doma, dal, inv_c);
+            if (lane <= 16 && dbc >= 0 && dbc < w)
+                eB = rec_cost<C>(LB, ld_rec(db, plane, roB + dbc), dtc, dtg, doma, dal, inv_c);
+            const double v = window_mean_lanes(eA, eB, inv_win);
+            if (v < best) {  // candidates ascend: strict < keeps the first minimum
+                best = v;
+                bx = x;
+            }
+        }
+        __syncwarp();  // the shared arrays are rewritten by the next call
+        return bx;
+    }
     for (int i0 = 0; i0 < ncand; i0 += 32) {
         const bool ok = i0 + lane < ncand;
         const int x = cand[ok ? i0 + lane : i0];
@@ -417,13 +601,14 @@ __device__ int warp_wta7(const PriorArgs& a, const double2* src, const double2* 
 
 struct FiltSmem {
     float4 win32[49];
+    uint2 win8[49];
     float c32[kFiltMax];
     int cand[kFiltMax];
 };
 
 template <int W7>  // 0: any window; 1 / 3: 7 x 7 window, 1 / 3 channels
 __device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, int64_t wid, double4* win,
-                                             FiltSmem* fs) {
+                                             FiltSmem* fs, bool use8) {
     int b = (int)(wid / per);
     int k = (int)(wid % per);
     int i = k / a.ncc, j = k % a.ncc;
@@ -433,8 +618,8 @@ __device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, in
     int64_t base = (int64_t)b * a.h * a.w;
     int dl;
     if constexpr (W7 > 0) {
-        dl = a.pl32 ? warp_wta7_filter<W7>(a, a.pl, a.pr, a.pl32, a.pr32, base, cr, cc, -1, win, fs->win32, fs->c32,
-                                           fs->cand)
+        dl = a.pl32 ? warp_wta7_filter<W7>(a, a.pl, a.pr, a.pl32, a.pr32, a.pl8, a.pr8, use8, base, cr, cc, -1, win,
+                                           fs->win32, fs->win8, fs->c32, fs->cand)
                     : warp_wta7<W7>(a, a.pl, a.pr, base, cr, cc, -1, win);
     } else {
         dl = warp_wta(a, a.ul, a.gl, a.ur, a.gr, base, cr, cc, -1);
@@ -443,8 +628,8 @@ __device__ __forceinline__ void prior_centre(const PriorArgs& a, int64_t per, in
     if (mc < 0) return;  // infeasible (hdp_model.py:458-459)
     int dr;
     if constexpr (W7 > 0) {
-        dr = a.pl32 ? warp_wta7_filter<W7>(a, a.pr, a.pl, a.pr32, a.pl32, base, cr, mc, +1, win, fs->win32, fs->c32,
-                                           fs->cand)
+        dr = a.pl32 ? warp_wta7_filter<W7>(a, a.pr, a.pl, a.pr32, a.pl32, a.pr8, a.pl8, use8, base, cr, mc, +1, win,
+                                           fs->win32, fs->win8, fs->c32, fs->cand)
                     : warp_wta7<W7>(a, a.pr, a.pl, base, cr, mc, +1, win);
     } else {
         dr = warp_wta(a, a.ur, a.gr, a.ul, a.gl, base, cr, mc, +1);
@@ -467,8 +652,9 @@ __global__ void __launch_bounds__(256, HDP_PRIOR_MINB) k_prior(PriorArgs a, int 
     __shared__ double4 win[kPriorWarps][49];  // the 7 x 7 path's staged window, per warp
     __shared__ FiltSmem fsm[W7 > 0 ? kPriorWarps : 1];  // the filter pass (7 x 7)
     // grid-stride over sample centres (a capped grid leaves SMs to other streams)
+    const bool use8 = W7 > 0 && a.pl8 != nullptr && __ldg(a.nonint) == 0;  // uniform over the grid
     for (int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wid < per * batch; wid += nwarp)
-        prior_centre<W7>(a, per, wid, win[threadIdx.x >> 5], &fsm[W7 > 0 ? threadIdx.x >> 5 : 0]);
+        prior_centre<W7>(a, per, wid, win[threadIdx.x >> 5], &fsm[W7 > 0 ? threadIdx.x >> 5 : 0], use8);
 }
 // numpy's pairwise_sum (eight accumulators for blocks <= 128, halves rounded
 // to multiples of 8 above; oracle/hdp_oracle.c np_pairwise): sequential
@@ -724,6 +910,10 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
         a.pr = pk.get() + 2 * n;
     }
     DevBuf<float4> pk32;
+    DevBuf<uint2> pk8;
+    DevBuf<int> nonint;
+    a.pl8 = a.pr8 = nullptr;
+    a.nonint = nullptr;
     a.pl32 = a.pr32 = nullptr;
     a.eps32 = 0.0f;
     {
@@ -739,6 +929,18 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
             a.pl32 = pk32.get();
             a.pr32 = pk32.get() + n;
             a.eps32 = (float)(1e-5 * std::max(1.0, a.border / 0.00977));
+            // level 0 of a uint8 pair: byte records for the filter (HDP_PRIOR_U8=0: diagnostics / tests)
+            const char* e8 = getenv("HDP_PRIOR_U8");
+            if (!(e8 && e8[0] == '0')) {
+                HDP_TRY(pk8.alloc(2 * n, st));
+                HDP_TRY(nonint.alloc(1, st));
+                HDP_CHECK_CUDA(cudaMemsetAsync(nonint.get(), 0, sizeof(int), st));
+                k_pack_px8<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk8.get(), nonint.get()); note_launch();
+                k_pack_px8<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk8.get() + n, nonint.get()); note_launch();
+                a.pl8 = pk8.get();
+                a.pr8 = pk8.get() + n;
+                a.nonint = nonint.get();
+            }
         }
     }
     if (window == 7 && c == 3)

@@ -410,6 +410,10 @@ def pack_masks(chosen) -> np.ndarray:
 # CTAs of the early (side-stream) prior launches; 0 = one warp per centre, uncapped
 PRIOR_SIDE_CTAS = int(os.environ.get("HDP_PRIOR_SIDE_CTAS", "0"))
 _PRIOR_EARLY_ENV = os.environ.get("HDP_PRIOR_EARLY", "")
+# diagnostics only (never set by bench.py or the tests): reuse the first step's prior counts, to
+# measure how much of an HDP step the sampled prior leaves exposed
+_DIAG_PRIOR_CACHE = os.environ.get("HDP_DIAG_PRIOR_CACHE", "0") == "1"
+_DIAG_PRIORS: dict = {}
 PRIOR_SIDE = os.environ.get("HDP_PRIOR_SIDE", "1") != "0"  # diagnostics: 0 = priors inline on the level stream
 PRIOR_EARLY = _PRIOR_EARLY_ENV == "1"
 
@@ -794,12 +798,20 @@ def _run_hdp_levels(left_u8, right_u8, d_max, model, levels, block_size, gamma, 
         # overlaps that level's tree build and aggregation
         if prior_stream is None or level < 0:
             return
+        if _DIAG_PRIOR_CACHE and (level, lv[level].h, lv[level].w, b) in _DIAG_PRIORS:
+            c_, k_ = _DIAG_PRIORS[(level, lv[level].h, lv[level].w, b)]
+            ev_ = torch.cuda.Event()
+            ev_.record(torch.cuda.current_stream())
+            early[level] = (c_, k_, ev_)
+            return
         prior_stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(prior_stream):
             c_, k_ = prior_counts(lv[level], cost=cost, max_ctas=PRIOR_SIDE_CTAS)
             ev_ = torch.cuda.Event()
             ev_.record(prior_stream)
             early[level] = (c_, k_, ev_)
+            if _DIAG_PRIOR_CACHE:
+                _DIAG_PRIORS[(level, lv[level].h, lv[level].w, b)] = (c_, k_)
 
     def finish(lev, f, disp, mc, vol, clk):
         ntrees, stored, ratio = _per_pair_stats_lazy(f, b, lev.h * lev.w, lev.d_max)
