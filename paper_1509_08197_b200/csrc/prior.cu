@@ -280,15 +280,6 @@ __device__ __forceinline__ double window_at(const double4* win, const double2* d
 // mean; eps32 = 1e-5 scaled by the border cost); only those candidates are
 // evaluated in f64 in numpy's order (window_at), and the first minimum among
 // them is the f64 first minimum over all disparities.
-template <int C>
-__device__ __forceinline__ float rec_cost32(const float4 L, const float4 R, float tc, float tg, float oma, float al) {
-    float acc = fabsf(L.x - R.x);
-    if (C > 1) acc += fabsf(L.y - R.y);
-    if (C > 2) acc += fabsf(L.z - R.z);
-    const float color = acc * (1.0f / (float)C);
-    return oma * fminf(color, tc) + al * fminf(fabsf(L.w - R.w), tg);
-}
-
 // u8 records: the channel sum of absolute differences is one VABSDIFF4 with
 // the accumulator preloaded with the bits of 2^23, so the result reads as the
 // float 2^23 + SAD (exact, SAD <= 765); tcs = tc * 255 C, omas = (1 - alpha) / (255 C)
@@ -325,6 +316,134 @@ __device__ __forceinline__ double window_mean_lanes(double eA, double eB, double
     return div_rn_by(__dadd_rn(s, last), 49.0, inv_win);
 }
 
+// Pass 1 of the filter: the f32 window mean of every disparity into c32,
+// returns this lane's minimum.  Rec = uint2 (byte records, level 0) or float4
+// (f32 records).  tcs / omas: the colour truncation and weight rescaled to
+// the record's channel sum (tc 255 C and (1 - alpha) / (255 C) for bytes, tc C
+// and (1 - alpha) / C for floats).
+template <int C>
+__device__ __forceinline__ float rec_acc(const float4 L, const float4 R, float tcs, float tg, float omas, float al,
+                                         float acc) {
+    float cs = fabsf(L.x - R.x);
+    if (C > 1) cs += fabsf(L.y - R.y);
+    if (C > 2) cs += fabsf(L.z - R.z);
+    acc = fmaf(omas, fminf(cs, tcs), acc);
+    return fmaf(al, fminf(fabsf(L.w - R.w), tg), acc);
+}
+template <int C>
+__device__ __forceinline__ float rec_acc(const uint2 L, const uint2 R, float tcs, float tg, float omas, float al,
+                                         float acc) {
+    return rec_cost8(L, R, tcs, tg, omas, al, acc);
+}
+
+template <int C, typename Rec>
+__device__ __forceinline__ float filter_means(const Rec* __restrict__ db, const Rec* wl, float tcs, float tg, float omas,
+                                              float al, float border32, int cr, int cc, int sign, int h, int w,
+                                              int d_max, const int* colv, int safe, int out, float* c32) {
+    const int lane = threadIdx.x & 31;
+    float mn = __int_as_float(0x7f800000);
+    const bool interior = cc - 3 >= 0 && cc + 3 <= w - 1;  // the window's columns are consecutive
+    // four 32-disparity blocks per round
+    for (int xg = 0; xg <= d_max; xg += 128) {
+        if constexpr (sizeof(Rec) == 8) {
+            // byte records, four active blocks inside the image: the blocks share
+            // the window's left records, and the next block's matched records are
+            // in flight while this block's costs are evaluated
+            if (interior && min(xg + 127, d_max) <= safe && xg + 96 <= d_max) {
+                float acc[4];
+                int off[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    acc[u] = 0.0f;
+                    off[u] = sign * min(xg + 32 * u + lane, d_max);
+                }
+                Rec Ra[7], Rb[7];
+                {
+                    const Rec* rp = db + min(max(cr - 3, 0), h - 1) * w + (cc - 3) + off[0];
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(rp + dc);
+                }
+#pragma unroll 1
+                for (int dr = 0; dr < 7; dr++) {
+                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w + (cc - 3);
+                    const int ron = min(max(cr + min(dr + 1, 6) - 3, 0), h - 1) * w + (cc - 3);
+                    Rec Lr[7];
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Lr[dc] = wl[7 * dr + dc];
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Rb[dc] = __ldg(db + ro + off[1] + dc);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[0] = rec_acc<C>(Lr[dc], Ra[dc], tcs, tg, omas, al, acc[0]);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(db + ro + off[2] + dc);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[1] = rec_acc<C>(Lr[dc], Rb[dc], tcs, tg, omas, al, acc[1]);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Rb[dc] = __ldg(db + ro + off[3] + dc);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[2] = rec_acc<C>(Lr[dc], Ra[dc], tcs, tg, omas, al, acc[2]);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(db + ron + off[0] + dc);  // row 6: reloaded, unused
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) acc[3] = rec_acc<C>(Lr[dc], Rb[dc], tcs, tg, omas, al, acc[3]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int x = xg + 32 * u + lane;
+                    if (x <= d_max) {
+                        const float m = acc[u] * (1.0f / 49.0f);
+                        c32[x] = m;
+                        mn = fminf(mn, m);
+                    }
+                }
+                continue;
+            }
+        }
+        // block by block: inside the image (no tests), entirely past the border
+        // (every element costs `border`), or mixed (per-element tests)
+#pragma unroll 1
+        for (int u = 0; u < 4; u++) {
+            const int xb = xg + 32 * u;
+            if (xb > d_max) break;
+            const int offu = sign * min(xb + lane, d_max);
+            float accu = 0.0f;
+            if (interior && min(xb + 31, d_max) <= safe) {
+#pragma unroll 1
+                for (int dr = 0; dr < 7; dr++) {
+                    const Rec* rp = db + min(max(cr + dr - 3, 0), h - 1) * w + (cc - 3) + offu;
+                    Rec Rr[7];
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) Rr[dc] = __ldg(rp + dc);
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) accu = rec_acc<C>(wl[7 * dr + dc], Rr[dc], tcs, tg, omas, al, accu);
+                }
+            } else if (xb > out) {
+                accu = 49.0f * border32;
+            } else {
+#pragma unroll 1
+                for (int dr = 0; dr < 7; dr++) {
+                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w;
+#pragma unroll
+                    for (int dc = 0; dc < 7; dc++) {
+                        const int dcol = colv[dc] + offu;
+                        if (dcol >= 0 && dcol < w)
+                            accu = rec_acc<C>(wl[7 * dr + dc], __ldg(db + ro + dcol), tcs, tg, omas, al, accu);
+                        else
+                            accu += border32;
+                    }
+                }
+            }
+            const int x = xb + lane;
+            if (x <= d_max) {
+                const float m = accu * (1.0f / 49.0f);
+                c32[x] = m;
+                mn = fminf(mn, m);
+            }
+        }
+    }
+    return mn;
+}
+
 // candidates above this count are verified one per lane (window_at), fewer with
 // the window's elements spread over the lanes (window_mean_lanes)
 constexpr int kLaneVerifyMax = 12;
@@ -350,133 +469,20 @@ __device__ int warp_wta7_filter(const PriorArgs& a, const double2* src, const do
     }
     __syncwarp();
     const int w = a.w, h = a.h, d_max = a.d_max;
-    const float tc = (float)a.tc, tg = (float)a.tg, oma = (float)a.one_minus_alpha, al = (float)a.alpha;
+    const float tg = (float)a.tg, al = (float)a.alpha;
     const float border32 = (float)a.border;
     // disparities whose matched columns are inside the image for every element
     const int safe = sign < 0 ? colv[0] : a.w - 1 - colv[6];
+    // disparities above `out` match every element outside the image
+    const int out = sign < 0 ? colv[6] : a.w - 1 - colv[0];
     // pass 1: f32 window means of every disparity
-    float mn = __int_as_float(0x7f800000);
-    if (use8) {
-        const float tcs = (float)(a.tc * 255.0 * C), omas = (float)(a.one_minus_alpha / (255.0 * C));
-        const uint2* db8 = dst8 + base;
-        const bool interior = cc - 3 >= 0 && cc + 3 <= w - 1;  // the window's columns are consecutive
-        // four 32-disparity blocks per round share the window's left records
-        for (int xg = 0; xg <= d_max; xg += 128) {
-            float acc[4];
-            int off[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                acc[u] = 0.0f;
-                off[u] = sign * min(xg + 32 * u + lane, d_max);
-            }
-            // warp-uniform: every active block of the round stays inside the image
-            const bool fast = interior && min(xg + 127, d_max) <= safe;
-            if (fast && xg + 96 <= d_max) {
-                // four active blocks: software-pipelined, the next block's matched
-                // records are in flight while this block's costs are evaluated
-                uint2 Ra[7], Rb[7];
-                {
-                    const uint2* rp = db8 + min(max(cr - 3, 0), h - 1) * w + (cc - 3) + off[0];
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(rp + dc);
-                }
-#pragma unroll 1
-                for (int dr = 0; dr < 7; dr++) {
-                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w + (cc - 3);
-                    const int ron = min(max(cr + min(dr + 1, 6) - 3, 0), h - 1) * w + (cc - 3);
-                    uint2 Lr[7];
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Lr[dc] = win8[7 * dr + dc];
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Rb[dc] = __ldg(db8 + ro + off[1] + dc);
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) acc[0] = rec_cost8(Lr[dc], Ra[dc], tcs, tg, omas, al, acc[0]);
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(db8 + ro + off[2] + dc);
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) acc[1] = rec_cost8(Lr[dc], Rb[dc], tcs, tg, omas, al, acc[1]);
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Rb[dc] = __ldg(db8 + ro + off[3] + dc);
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) acc[2] = rec_cost8(Lr[dc], Ra[dc], tcs, tg, omas, al, acc[2]);
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Ra[dc] = __ldg(db8 + ron + off[0] + dc);  // row 6: reloaded, unused
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) acc[3] = rec_cost8(Lr[dc], Rb[dc], tcs, tg, omas, al, acc[3]);
-                }
-            } else if (fast) {
-#pragma unroll 1
-                for (int dr = 0; dr < 7; dr++) {
-                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w + (cc - 3);
-                    uint2 Lr[7];
-#pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Lr[dc] = win8[7 * dr + dc];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        if (xg + 32 * u <= d_max) {
-                            const uint2* rp = db8 + ro + off[u];
-#pragma unroll
-                            for (int dc = 0; dc < 7; dc++)
-                                acc[u] = rec_cost8(Lr[dc], __ldg(rp + dc), tcs, tg, omas, al, acc[u]);
-                        }
-                    }
-                }
-            } else {
-#pragma unroll 1
-                for (int dr = 0; dr < 7; dr++) {
-                    const int ro = min(max(cr + dr - 3, 0), h - 1) * w;
-#pragma unroll 1
-                    for (int dc = 0; dc < 7; dc++) {
-                        const uint2 Lq = win8[7 * dr + dc];
-                        const int col = min(max(cc + dc - 3, 0), w - 1);
-#pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const int dcol = col + off[u];
-                            if (dcol >= 0 && dcol < w)
-                                acc[u] = rec_cost8(Lq, __ldg(db8 + ro + dcol), tcs, tg, omas, al, acc[u]);
-                            else
-                                acc[u] += border32;
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int x = xg + 32 * u + lane;
-                if (x <= d_max) {
-                    const float m = acc[u] * (1.0f / 49.0f);
-                    c32[x] = m;
-                    mn = fminf(mn, m);
-                }
-            }
-        }
-    } else {
-        const float4* db32 = dst32 + base;
-        for (int x0 = 0; x0 <= d_max; x0 += 32) {
-            const int x = x0 + lane;
-            const int off = sign * min(x, d_max);
-            float acc[7];  // one running sum per window column (independent chains)
-#pragma unroll
-            for (int dc = 0; dc < 7; dc++) acc[dc] = 0.0f;
-#pragma unroll 1
-            for (int dr = 0; dr < 7; dr++) {
-                const int ro = rowo[dr];
-#pragma unroll
-                for (int dc = 0; dc < 7; dc++) {
-                    const int dcol = colv[dc] + off;
-                    acc[dc] += (dcol >= 0 && dcol < w) ? rec_cost32<C>(win32[7 * dr + dc], __ldg(db32 + ro + dcol), tc,
-                                                                       tg, oma, al)
-                                                       : border32;
-                }
-            }
-            const float sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + acc[6]);
-            const float m = sum * (1.0f / 49.0f);
-            if (x <= d_max) {
-                c32[x] = m;
-                mn = fminf(mn, m);
-            }
-        }
-    }
+    float mn;
+    if (use8)
+        mn = filter_means<C>(dst8 + base, win8, (float)(a.tc * 255.0 * C), tg, (float)(a.one_minus_alpha / (255.0 * C)),
+                             al, border32, cr, cc, sign, h, w, d_max, colv, safe, out, c32);
+    else
+        mn = filter_means<C>(dst32 + base, win32, (float)(a.tc * C), tg, (float)(a.one_minus_alpha / C), al, border32, cr,
+                             cc, sign, h, w, d_max, colv, safe, out, c32);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
     __syncwarp();
