@@ -1610,8 +1610,11 @@ template <typename G>
 static int up_chunks(const AggArgs& sh, const hdp_forest* f, int64_t r, const G& cgrid, bool both, size_t ssmem,
                      size_t csmem, cudaStream_t s) {
     const int64_t c0 = f->chunk_off[r], nc = f->chunk_off[r + 1] - c0, nb = f->chunk_big[r], ns = nc - nb;
-    if (ns > 0) {
-        k_up_chunk<<<cgrid(ns, both), kChunkThreads, ssmem, s>>>(sh, f->chunk_desc.get(), c0, ns); note_launch();
+    // the small chunks that hold lone leaves only (the last chunk_lone[r] of
+    // them) have nothing to do on the way up: A_up = E is already in place
+    const int64_t nu = ns - (r < (int64_t)f->chunk_lone.size() ? f->chunk_lone[r] : 0);
+    if (nu > 0) {
+        k_up_chunk<<<cgrid(nu, both), kChunkThreads, ssmem, s>>>(sh, f->chunk_desc.get(), c0, nu); note_launch();
     }
     if (nb > 0) {
         k_up_chunk<<<cgrid(nb, both), kChunkThreads, csmem, s>>>(sh, f->chunk_desc.get(), c0 + ns, nb); note_launch();

@@ -591,7 +591,11 @@ __global__ void k_head_keys(int64_t n, const int32_t* __restrict__ hf, const int
     int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n || !hf[v]) return;
     const int32_t i = hpos[v];
-    hkey[i] = (uint8_t)((ld[v] << 1) | (plen[v] > kShortPath ? 1 : 0));
+    // class within the phase: short paths of two or more nodes, then the lone
+    // leaves (one-node paths: no work on the way up, so the up pass skips the
+    // chunks that hold nothing else), then the long paths
+    const int cls = plen[v] > kShortPath ? 2 : (plen[v] == 1 ? 1 : 0);
+    hkey[i] = (uint8_t)((ld[v] << 2) | cls);
     hval[i] = (int32_t)v;
 }
 
@@ -1474,20 +1478,36 @@ __global__ void k_chunk_desc(const int64_t* __restrict__ cbase, int nph, const i
     if ((threadIdx.x & 31) == 0 && words) atomicMax(max_words, words);
 }
 
-// chunk size classes: big[c] = the chunk needs more than kChunkSmallWords
-__global__ void k_chunk_big_flags(int64_t nc, const ChunkDesc* __restrict__ desc, int32_t* big) {
+// chunk classes: big[c] = the chunk needs more than kChunkSmallWords;
+// lone[c] = a small chunk of lone leaves only (one-node paths without light
+// children: nothing to do on the way up)
+__global__ void k_chunk_big_flags(int64_t nc, const ChunkDesc* __restrict__ desc, const int64_t* __restrict__ cbase,
+                                  int nph, int32_t* big, int32_t* lone) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < nc) big[c] = desc[c].pad0 + 64 > kChunkSmallWords ? 1 : 0;
+    if (c >= nc) return;
+    if (c >= cbase[nph]) {  // past the chunk count (nc is its bound): no descriptor was written
+        big[c] = 0;
+        lone[c] = 0;
+        return;
+    }
+    const ChunkDesc d = desc[c];
+    const int b = d.pad0 + 64 > kChunkSmallWords ? 1 : 0;
+    big[c] = b;
+    lone[c] = (!b && d.np > 0 && d.nl == 0 && d.nk == d.np) ? 1 : 0;
 }
 
-// stable partition of every phase's chunks: small ones first, then big ones
-// (bpos = exclusive scan of the big flags); nbig[r] = big chunks of phase r
+// stable partition of every phase's chunks: small ones with work on the way
+// up first, then the small lone-leaf chunks, then the big ones (bpos / lpos =
+// exclusive scans of the flags); nbig[r] / nlone[r] = those chunks of phase r
 __global__ void k_chunk_split(int64_t nc, int nph, const int64_t* __restrict__ cbase,
-                              const int32_t* __restrict__ bpos, const ChunkDesc* __restrict__ in, ChunkDesc* out,
-                              int64_t* nbig) {
+                              const int32_t* __restrict__ bpos, const int32_t* __restrict__ lpos,
+                              const ChunkDesc* __restrict__ in, ChunkDesc* out, int64_t* nbig, int64_t* nlone) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < nph) nbig[c] = bpos[cbase[c + 1]] - bpos[cbase[c]];
-    if (c >= nc) return;
+    if (c < nph) {
+        nbig[c] = bpos[cbase[c + 1]] - bpos[cbase[c]];
+        nlone[c] = lpos[cbase[c + 1]] - lpos[cbase[c]];
+    }
+    if (c >= nc || c >= cbase[nph]) return;
     int lo = 0, hi = nph - 1;  // phase r with cbase[r] <= c < cbase[r + 1]
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -1495,10 +1515,11 @@ __global__ void k_chunk_split(int64_t nc, int nph, const int64_t* __restrict__ c
         else hi = mid - 1;
     }
     const int64_t b0 = bpos[cbase[lo]], nb = bpos[cbase[lo + 1]] - b0;
-    const int64_t ns = cbase[lo + 1] - cbase[lo] - nb;
-    const int64_t lb = bpos[c] - b0, ls = (c - cbase[lo]) - lb;
-    const bool isbig = bpos[c + 1] != bpos[c];
-    out[cbase[lo] + (isbig ? ns + lb : ls)] = in[c];
+    const int64_t l0 = lpos[cbase[lo]], nl = lpos[cbase[lo + 1]] - l0;
+    const int64_t n0 = cbase[lo + 1] - cbase[lo] - nb - nl;  // small chunks with work on the way up
+    const int64_t lb = bpos[c] - b0, ll = lpos[c] - l0, ls = (c - cbase[lo]) - lb - ll;
+    const bool isbig = bpos[c + 1] != bpos[c], islone = lpos[c + 1] != lpos[c];
+    out[cbase[lo] + (isbig ? n0 + nl + lb : (islone ? n0 + ll : ls))] = in[c];
 }
 }  // namespace hdp
 
@@ -1560,26 +1581,34 @@ static int build_chunks(hdp_forest* f) {
     HDP_CHECK_LAUNCH();
     // size classes (k_chunk_split): the chunk count is only known on the
     // device, so the class passes run over the bound ncap
-    DevBuf<int32_t> bflag, bpos;
+    DevBuf<int32_t> bflag, bpos, lflag, lpos;
     DevBuf<ChunkDesc> split;
-    DevBuf<int64_t> nbig;
+    DevBuf<int64_t> nbig;  // nbig[0 .. nph), then nlone[0 .. nph)
     HDP_TRY(bflag.alloc(ncap + 1, st));
     HDP_TRY(bpos.alloc(ncap + 1, st));
+    HDP_TRY(lflag.alloc(ncap + 1, st));
+    HDP_TRY(lpos.alloc(ncap + 1, st));
     HDP_TRY(split.alloc(ncap + 1, st));
-    HDP_TRY(nbig.alloc(nph + 1, st));
+    HDP_TRY(nbig.alloc(2 * nph + 2, st));
     HDP_CHECK_CUDA(cudaMemsetAsync(bflag.get(), 0, sizeof(int32_t) * (ncap + 1), st));
-    k_chunk_big_flags<<<grid_for(ncap, 256), 256, 0, st>>>(ncap, f->chunk_desc.get(), bflag.get()); note_launch();
+    HDP_CHECK_CUDA(cudaMemsetAsync(lflag.get(), 0, sizeof(int32_t) * (ncap + 1), st));
+    k_chunk_big_flags<<<grid_for(ncap, 256), 256, 0, st>>>(ncap, f->chunk_desc.get(), cbase.get(), nph, bflag.get(),
+                                                           lflag.get());
+    note_launch();
     HDP_TRY(exclusive_sum(bflag.get(), bpos.get(), ncap + 1, st));
+    HDP_TRY(exclusive_sum(lflag.get(), lpos.get(), ncap + 1, st));
     k_chunk_split<<<grid_for(std::max<int64_t>(ncap, nph), 256), 256, 0, st>>>(
-        ncap, nph, cbase.get(), bpos.get(), f->chunk_desc.get(), split.get(), nbig.get()); note_launch();
+        ncap, nph, cbase.get(), bpos.get(), lpos.get(), f->chunk_desc.get(), split.get(), nbig.get(),
+        nbig.get() + nph); note_launch();
     HDP_CHECK_LAUNCH();
-    std::vector<int64_t> h(nph + 2), hb(nph + 1);
+    std::vector<int64_t> h(nph + 2), hb(2 * nph + 1);
     HDP_CHECK_CUDA(cudaMemcpyAsync(h.data(), cbase.get(), sizeof(int64_t) * (nph + 1), cudaMemcpyDeviceToHost, st));
     HDP_CHECK_CUDA(cudaMemcpyAsync(h.data() + nph + 1, mx.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    HDP_CHECK_CUDA(cudaMemcpyAsync(hb.data(), nbig.get(), sizeof(int64_t) * nph, cudaMemcpyDeviceToHost, st));
+    HDP_CHECK_CUDA(cudaMemcpyAsync(hb.data(), nbig.get(), sizeof(int64_t) * 2 * nph, cudaMemcpyDeviceToHost, st));
     HDP_CHECK_CUDA(cudaStreamSynchronize(st));
     f->chunk_desc = std::move(split);  // the partitioned table (chunks past the count are never read)
     f->chunk_big.assign(hb.begin(), hb.begin() + nph);
+    f->chunk_lone.assign(hb.begin() + nph, hb.begin() + 2 * nph);
     HDP_REQUIRE(h[nph] <= ncap, HDP_ERR_INTERNAL, "chunk count %lld above its bound %lld", (long long)h[nph],
                 (long long)ncap);
     f->chunk_off.assign(h.begin(), h.begin() + nph + 1);

@@ -134,6 +134,7 @@ struct hdp_forest {
     hdp::DevBuf<int64_t> auxd;       // per short path: prefix of m over paths with a parent (down pass)
     std::vector<int64_t> chunk_off;  // host: chunks of phase r = [chunk_off[r], chunk_off[r+1])
     std::vector<int64_t> chunk_big;  // host: of those, the last chunk_big[r] exceed kChunkSmallWords
+    std::vector<int64_t> chunk_lone; // host: the chunk_lone[r] small chunks before them hold lone leaves only
     int64_t chunk_words = 0;         // shared-memory words the largest chunk needs
     int chunks_ok = 0;               // chunks fit in shared memory
 
