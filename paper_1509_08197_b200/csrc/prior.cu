@@ -51,32 +51,29 @@ __global__ void k_pack_px(const double* __restrict__ u, const double* __restrict
     out[n + i] = make_double2(c > 2 ? u[i * c + 2] : 0.0, g[i]);
 }
 
-// f32 copies of the records (u0, u1, u2, grad) for the filter pass
-__global__ void k_pack_px32(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
-                            float4* __restrict__ out) {
+// All three record sets of one image in one pass over its planes (the
+// default 7 x 7 filter path): f64 planes, f32 records, byte records.
+__global__ void k_pack_all(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
+                           double2* __restrict__ out64, float4* __restrict__ out32, uint2* __restrict__ out8,
+                           int* __restrict__ nonint) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    out[i] = make_float4((float)u[i * c], c > 1 ? (float)u[i * c + 1] : 0.0f, c > 2 ? (float)u[i * c + 2] : 0.0f,
-                         (float)g[i]);
-}
-
-// The same records with the channels as bytes, for images whose unit values are
-// k / 255 (level 0 of a uint8 pair): RN(k / 255) * 255 is within an ulp of k,
-// so rint recovers k exactly; any other value raises *nonint.
-__global__ void k_pack_px8(const double* __restrict__ u, const double* __restrict__ g, int64_t n, int c,
-                           uint2* __restrict__ out, int* __restrict__ nonint) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    unsigned pk = 0;
-    bool bad = false;
-    for (int k = 0; k < c; k++) {
-        const double v = u[i * c + k] * 255.0;
-        const double r = rint(v);
-        bad = bad || !(fabs(v - r) <= 1e-9) || r < 0.0 || r > 255.0;
-        pk |= (unsigned)(bad ? 0 : (int)r) << (8 * k);
+    const double u0 = u[i * c], u1 = c > 1 ? u[i * c + 1] : 0.0, u2 = c > 2 ? u[i * c + 2] : 0.0, gg = g[i];
+    out64[i] = make_double2(u0, u1);
+    out64[n + i] = make_double2(u2, gg);
+    out32[i] = make_float4((float)u0, (float)u1, (float)u2, (float)gg);
+    if (out8) {
+        const double v[3] = {u0 * 255.0, u1 * 255.0, u2 * 255.0};
+        unsigned pk = 0;
+        bool bad = false;
+        for (int k = 0; k < c; k++) {
+            const double r = rint(v[k]);
+            bad = bad || !(fabs(v[k] - r) <= 1e-9) || r < 0.0 || r > 255.0;
+            pk |= (unsigned)(bad ? 0 : (int)r) << (8 * k);
+        }
+        out8[i] = make_uint2(pk, __float_as_uint((float)gg));
+        if (bad) *nonint = 1;
     }
-    out[i] = make_uint2(pk, __float_as_uint((float)g[i]));
-    if (bad) *nonint = 1;
 }
 
 // 3 channels, two pixels per thread with 16-byte loads and stores (the planes
@@ -408,14 +405,27 @@ __device__ __forceinline__ float filter_means(const Rec* __restrict__ db, const 
             const int offu = sign * min(xb + lane, d_max);
             float accu = 0.0f;
             if (interior && min(xb + 31, d_max) <= safe) {
+                // half rows software-pipelined: columns 4..6 of this row and 0..3 of
+                // the next are in flight while the other half is evaluated
+                Rec Ra[4], Rb[3];
+                {
+                    const Rec* rp = db + min(max(cr - 3, 0), h - 1) * w + (cc - 3) + offu;
+#pragma unroll
+                    for (int dc = 0; dc < 4; dc++) Ra[dc] = __ldg(rp + dc);
+                }
 #pragma unroll 1
                 for (int dr = 0; dr < 7; dr++) {
                     const Rec* rp = db + min(max(cr + dr - 3, 0), h - 1) * w + (cc - 3) + offu;
-                    Rec Rr[7];
+                    const Rec* rn = db + min(max(cr + min(dr + 1, 6) - 3, 0), h - 1) * w + (cc - 3) + offu;
 #pragma unroll
-                    for (int dc = 0; dc < 7; dc++) Rr[dc] = __ldg(rp + dc);
+                    for (int dc = 0; dc < 3; dc++) Rb[dc] = __ldg(rp + 4 + dc);
 #pragma unroll
-                    for (int dc = 0; dc < 7; dc++) accu = rec_acc<C>(wl[7 * dr + dc], Rr[dc], tcs, tg, omas, al, accu);
+                    for (int dc = 0; dc < 4; dc++) accu = rec_acc<C>(wl[7 * dr + dc], Ra[dc], tcs, tg, omas, al, accu);
+#pragma unroll
+                    for (int dc = 0; dc < 4; dc++) Ra[dc] = __ldg(rn + dc);  // row 6: reloaded, unused
+#pragma unroll
+                    for (int dc = 0; dc < 3; dc++)
+                        accu = rec_acc<C>(wl[7 * dr + 4 + dc], Rb[dc], tcs, tg, omas, al, accu);
                 }
             } else if (xb > out) {
                 accu = 49.0f * border32;
@@ -896,42 +906,26 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
     a.inv_c = 1.0 / (double)c;  // host IEEE: RN(1/c)
     a.inv_win = 1.0 / (double)(window * window);
     DevBuf<double2> pk;
-    a.pl = a.pr = nullptr;
-    a.plane = (int64_t)batch * h * w;
-    if (window == 7) {
-        const int64_t n = a.plane;
-        HDP_TRY(pk.alloc(4 * n, st));
-        const bool v2 = c == 3 && n % 2 == 0 && ((uintptr_t)unit_l | (uintptr_t)grad_l | (uintptr_t)unit_r |
-                                                 (uintptr_t)grad_r) % 16 == 0;
-        if (v2) {
-            k_pack_px3<<<grid_for(n / 2, 256), 256, 0, st>>>((const double2*)unit_l, (const double2*)grad_l, n / 2,
-                                                            pk.get(), n); note_launch();
-            k_pack_px3<<<grid_for(n / 2, 256), 256, 0, st>>>((const double2*)unit_r, (const double2*)grad_r, n / 2,
-                                                            pk.get() + 2 * n, n); note_launch();
-        } else {
-            k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk.get()); note_launch();
-            k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk.get() + 2 * n); note_launch();
-        }
-        a.pl = pk.get();
-        a.pr = pk.get() + 2 * n;
-    }
     DevBuf<float4> pk32;
     DevBuf<uint2> pk8;
     DevBuf<int> nonint;
+    a.pl = a.pr = nullptr;
     a.pl8 = a.pr8 = nullptr;
     a.nonint = nullptr;
     a.pl32 = a.pr32 = nullptr;
     a.eps32 = 0.0f;
-    {
+    a.plane = (int64_t)batch * h * w;
+    if (window == 7) {
+        const int64_t n = a.plane;
+        HDP_TRY(pk.alloc(4 * n, st));
+        a.pl = pk.get();
+        a.pr = pk.get() + 2 * n;
         const char* e = getenv("HDP_PRIOR_FILTER");  // diagnostics / tests: 0 = every disparity in f64
         const bool filt = !(e && e[0] == '0');
         // the f32 error bound assumes unit-scaled inputs (|u|, |grad| <= 1)
         // and the default-sized truncations; eps32 scales with the border cost
-        if (filt && window == 7 && d_max < kFiltMax && a.border > 0.0 && a.border < 1.0) {
-            const int64_t n = a.plane;
+        if (filt && d_max < kFiltMax && a.border > 0.0 && a.border < 1.0) {
             HDP_TRY(pk32.alloc(2 * n, st));
-            k_pack_px32<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk32.get()); note_launch();
-            k_pack_px32<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk32.get() + n); note_launch();
             a.pl32 = pk32.get();
             a.pr32 = pk32.get() + n;
             a.eps32 = (float)(1e-5 * std::max(1.0, a.border / 0.00977));
@@ -941,11 +935,26 @@ extern "C" int hdp_prior_counts(const double* unit_l, const double* grad_l, cons
                 HDP_TRY(pk8.alloc(2 * n, st));
                 HDP_TRY(nonint.alloc(1, st));
                 HDP_CHECK_CUDA(cudaMemsetAsync(nonint.get(), 0, sizeof(int), st));
-                k_pack_px8<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk8.get(), nonint.get()); note_launch();
-                k_pack_px8<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk8.get() + n, nonint.get()); note_launch();
                 a.pl8 = pk8.get();
                 a.pr8 = pk8.get() + n;
                 a.nonint = nonint.get();
+            }
+            // one pass per image writes all its record sets
+            k_pack_all<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk.get(), pk32.get(),
+                                                         a.pl8 ? pk8.get() : nullptr, nonint.get()); note_launch();
+            k_pack_all<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk.get() + 2 * n, pk32.get() + n,
+                                                         a.pl8 ? pk8.get() + n : nullptr, nonint.get()); note_launch();
+        } else {
+            const bool v2 = c == 3 && n % 2 == 0 && ((uintptr_t)unit_l | (uintptr_t)grad_l | (uintptr_t)unit_r |
+                                                     (uintptr_t)grad_r) % 16 == 0;
+            if (v2) {
+                k_pack_px3<<<grid_for(n / 2, 256), 256, 0, st>>>((const double2*)unit_l, (const double2*)grad_l, n / 2,
+                                                                pk.get(), n); note_launch();
+                k_pack_px3<<<grid_for(n / 2, 256), 256, 0, st>>>((const double2*)unit_r, (const double2*)grad_r, n / 2,
+                                                                pk.get() + 2 * n, n); note_launch();
+            } else {
+                k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_l, grad_l, n, c, pk.get()); note_launch();
+                k_pack_px<<<grid_for(n, 256), 256, 0, st>>>(unit_r, grad_r, n, c, pk.get() + 2 * n); note_launch();
             }
         }
     }
