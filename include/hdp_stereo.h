@@ -102,6 +102,19 @@ int hdp_grid_edge_weights64(const double *img, int batch, int h, int w, int c, d
  * median with reflected borders (scipy.ndimage mode "reflect"), uint8. */
 int hdp_median3x3(const uint8_t *src, uint8_t *dst, int batch, int h, int w, int c, void *stream);
 
+/* winner_takes_all_with_cost (aggregation.py:239-256) over an (n, m) float64
+ * matrix whose unused entries hold +inf: arg[r] = the first (lowest-column)
+ * minimum of row r, best[r] its value. */
+int hdp_rows_first_argmin(const double *rows, int64_t n, int m, int32_t *arg, double *best,
+                          void *stream);
+
+/* masked_cost_volume's per-tree blocks (cost_volume.py:225-231) from a dense
+ * (pixels, ncols) f32 cost grid: output row r = pixel node[r], columns
+ * cols[cstart[r] .. cstart[r] + cnt[r]), as float64 at out + off[r]. */
+int hdp_gather_ragged(const float *grid, int ncols, int64_t nrows, const int64_t *node,
+                      const int64_t *off, const int32_t *cstart, const int32_t *cnt,
+                      const int32_t *cols, double *out, void *stream);
+
 /* build_forest(edges, "mst") edge selection (spanning_forest.py:286-322) as
  * Boruvka on unique 64-bit keys (the MST under a total order is unique, so it
  * equals stable-sort Kruskal's).  Works on any edge list (not only grids).
@@ -294,6 +307,13 @@ int hdp_occlusion_from_gt(const int32_t *gt_left, const int32_t *gt_right, const
                           void *stream);
 
 /* --------------------------------------------------------- whole pipeline */
+/* hdp_dense_pipeline option: start the raw-cost pass on a side stream as soon
+ * as the tree's layout order is final, beside the rest of the build (dense
+ * range lanes have uniform rows, so a node's row is known from its layout
+ * position alone).  Returns the previous setting.  Off by default (measured
+ * +1.5 % at C5); HDP_EARLY_COST=1 sets the default. */
+int hdp_set_early_cost(int on);
+
 /* run_baseline_pipeline (aggregation.py:263-358) for a batch of pairs in one
  * call: u8 -> f64, prepare_layer, build_edge_list, MST, rooted forest, lanes
  * [x0, x0+nx), fused cost + aggregation + first argmin.  left/right (B,H,W,C)

@@ -169,9 +169,11 @@ def winner_takes_all_with_cost(volume: SparseCostVolume) -> tuple[DisparityMap, 
         pad[nodes, : blk.shape[1]] = blk
         cols[nodes, : blk.shape[1]] = volume.intervals[t]
     dp = torch.from_numpy(pad).to(L.device())
-    j = torch.argmin(dp, dim=1)  # first minimum
-    best = dp.gather(1, j[:, None])[:, 0].cpu().numpy()
-    jn = j.cpu().numpy()
+    j = torch.empty(n, dtype=torch.int32, device=dp.device)
+    bd = torch.empty(n, dtype=torch.float64, device=dp.device)
+    L.call("hdp_rows_first_argmin", L.ptr(dp), n, int(max_m), L.ptr(j), L.ptr(bd), L.stream())
+    best = bd.cpu().numpy()
+    jn = j.cpu().numpy().astype(np.int64)
     values = cols[np.arange(n), jn].astype(np.int32)
     disp = DisparityMap(values=values.reshape(volume.height, volume.width),
                         valid=np.ones((volume.height, volume.width), dtype=bool))

@@ -84,6 +84,7 @@ struct AggArgs {
     int max_mp;            // max_m rounded up to a multiple of 4 (carry stride)
     int qgroups;           // 32-float4 column groups of the widest row (segment kernels)
     int qsub, qsub_shift;  // chunk kernels: float4 lanes per path (power of 2 <= 32)
+    int uni_mp;            // rowoff == nullptr (early raw cost): row of layout position k = k * uni_mp
 };
 
 __device__ __forceinline__ int lane_disp(const AggArgs& a, int doff, int j) {
@@ -273,7 +274,8 @@ __global__ void __launch_bounds__(256) k_ecost_range_u(AggArgs a, const int32_t*
         win[i] = x >= 0 ? __ldg(a.pr + base + x) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     }
     for (int i = threadIdx.x; i < nt; i += 256) {
-        srow[i] = __ldg(a.rowoff + __ldg(lpos + base + c0 + i));
+        const int32_t k = __ldg(lpos + base + c0 + i);
+        srow[i] = a.rowoff ? __ldg(a.rowoff + k) : (long long)k * a.uni_mp;
         sL[i] = __ldg(a.pl + base + c0 + i);
     }
     __syncthreads();
@@ -1703,6 +1705,66 @@ struct PhaseClock {
     }
 };
 
+// Early raw cost of the dense pipeline (forest.cuh EarlyCost): called by
+// forest_build once the layout order is final.  Rows are uniform (range
+// lanes), so a node's row is its layout position times the padded width.
+int hdp::ecost_early(hdp_forest* f) {
+    EarlyCost& e = f->early;
+    cudaStream_t st = f->st;
+    const int m = e.nx, mp = (m + 3) & ~3, U = (mp + 31) / 32;
+    const size_t usmem = (size_t)(kETile + e.x0 + mp - 1) * sizeof(float4);
+    if (!(usmem <= 48 * 1024 && U <= 17) || e.w <= 0 || f->n % e.w != 0 || (int64_t)e.h * e.w >= ((int64_t)1 << 31)) {
+        e.want = 0;  // hdp_aggregate_wta runs its own pre-pass
+        return HDP_OK;
+    }
+    HDP_TRY(e.rows.alloc(f->n * (int64_t)mp + 32, st));
+    HDP_CHECK_CUDA(cudaEventRecord(e.layout_ev, st));
+    HDP_CHECK_CUDA(cudaStreamWaitEvent(e.side, e.layout_ev, 0));
+    AggArgs a = {};
+    a.pl = (const float4*)e.pl;
+    a.pr = (const float4*)e.pr;
+    a.npix = e.h * e.w;
+    a.w = e.w;
+    a.c = e.c;
+    a.range_x0 = e.x0;
+    a.alpha = e.alpha;
+    a.tc = e.tau_c;
+    a.tg = e.tau_g;
+    a.border = (1.0f - e.alpha) * e.tau_c + e.alpha * e.tau_g;
+    a.aup = e.rows.get();
+    a.rowoff = nullptr;
+    a.uni_mp = mp;
+    dim3 g((unsigned)(f->n / e.w), (unsigned)((e.w + kETile - 1) / kETile));
+    // shared-memory padding caps the grid's CTAs per SM (HDP_EARLY_SMEM_KB): the
+    // build's latency-bound kernels beside it suffer less from a DRAM queue
+    // that a full-occupancy write stream keeps saturated
+    static const int pad_kb = env_int("HDP_EARLY_SMEM_KB", 0);
+    const size_t esmem = std::max(usmem, (size_t)pad_kb * 1024);
+    if (esmem > 48 * 1024) {
+        switch (U) {
+#define HDP_ECU(n) case n: cudaFuncSetAttribute(k_ecost_range_u<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem); break;
+            HDP_ECU(1) HDP_ECU(2) HDP_ECU(3) HDP_ECU(4) HDP_ECU(5) HDP_ECU(6) HDP_ECU(7) HDP_ECU(8)
+            HDP_ECU(9) HDP_ECU(10) HDP_ECU(11) HDP_ECU(12) HDP_ECU(13) HDP_ECU(14) HDP_ECU(15)
+            HDP_ECU(16) HDP_ECU(17)
+#undef HDP_ECU
+            default: break;
+        }
+    }
+    switch (U) {
+#define HDP_ECU(n) case n: k_ecost_range_u<n><<<g, 256, esmem, e.side>>>(a, f->lpos.get(), m); break;
+        HDP_ECU(1) HDP_ECU(2) HDP_ECU(3) HDP_ECU(4) HDP_ECU(5) HDP_ECU(6) HDP_ECU(7) HDP_ECU(8)
+        HDP_ECU(9) HDP_ECU(10) HDP_ECU(11) HDP_ECU(12) HDP_ECU(13) HDP_ECU(14) HDP_ECU(15)
+        HDP_ECU(16) HDP_ECU(17)
+#undef HDP_ECU
+        default: break;
+    }
+    note_launch();
+    HDP_CHECK_LAUNCH();
+    HDP_CHECK_CUDA(cudaEventRecord(e.done_ev, e.side));
+    e.done = 1;
+    return HDP_OK;
+}
+
 #ifdef HDP_AGG_PROFILE
 // records of 8 words: kind << 56 | smid << 40 | aux, then globaltimer stamps;
 // returns the record count and resets it
@@ -1777,8 +1839,19 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     DevBuf<float> aup;
     DevBuf<unsigned long long> carry;
     DevBuf<int> tickets;
-    HDP_TRY(aup.alloc(f->total_rows + 32, st));
-    a.aup = aup.get();
+    // the dense pipeline's early raw cost (forest.cuh EarlyCost): the rows are
+    // already being filled on the side stream
+    const bool early = f->early.done && !cost_rows && !volume && packed_l == f->early.pl &&
+                       packed_r == f->early.pr && f->range_x0 == f->early.x0 && f->max_m == f->early.nx &&
+                       h == f->early.h && w == f->early.w && c == f->early.c && alpha == f->early.alpha &&
+                       tau_c == f->early.tau_c && tau_g == f->early.tau_g;
+    if (early) {
+        a.aup = f->early.rows.get();
+        HDP_CHECK_CUDA(cudaStreamWaitEvent(st, f->early.done_ev, 0));
+    } else {
+        HDP_TRY(aup.alloc(f->total_rows + 32, st));
+        a.aup = aup.get();
+    }
     const int64_t nseg = f->n_segs;
     HDP_TRY(carry.alloc(nseg * a.max_mp + 1, st));
     DevBuf<unsigned long long> aggb, aggpb;
@@ -1836,7 +1909,9 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     AggArgs sh = a;
     sh.pinfo = f->short_info.get();
     sh.prows = f->short_rows.get();
-    if (cost_rows) {
+    a.uni_mp = 0;
+    if (early) {
+    } else if (cost_rows) {
         k_ecompute<<<packed_grid(a, f->n, BU, 256), 256, 0, st>>>(a, 0, f->n); note_launch();
     } else {
         HDP_REQUIRE(f->n % a.w == 0, HDP_ERR_CONFIG, "node count is not a whole number of image rows");

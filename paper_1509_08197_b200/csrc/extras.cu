@@ -134,6 +134,52 @@ __global__ void k_occlusion(const int32_t* __restrict__ gl, const int32_t* __res
     occ[t] = (lv && !consistent) ? 1 : 0;
 }
 
+// first minimum of every row of an (n, m) float64 matrix (np.argmin: the
+// lowest index among equal minima); one warp per row
+__global__ void k_rows_argmin(const double* __restrict__ rows, int64_t n, int m, int32_t* __restrict__ arg,
+                              double* __restrict__ best) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= n) return;
+    double b = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    int bj = 0x7fffffff;
+    for (int j = lane; j < m; j += 32) {
+        const double v = rows[r * m + j];
+        if (v < b) {
+            b = v;
+            bj = j;
+        }
+    }
+    for (int o = 16; o >= 1; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ob < b || (ob == b && oj < bj)) {
+            b = ob;
+            bj = oj;
+        }
+    }
+    if (lane == 0) {
+        arg[r] = bj == 0x7fffffff ? 0 : bj;  // a row of +inf only: column 0, as np.argmin
+        best[r] = bj == 0x7fffffff ? rows[r * m] : b;
+    }
+}
+
+// ragged gather of a dense (pixels, ncols) f32 grid: output row r takes pixel
+// node[r] and the columns cols[cstart[r] .. cstart[r] + cnt[r]), written as
+// float64 at out + off[r]
+__global__ void k_gather_ragged(const float* __restrict__ grid, int ncols, int64_t nrows,
+                                const int64_t* __restrict__ node, const int64_t* __restrict__ off,
+                                const int32_t* __restrict__ cstart, const int32_t* __restrict__ cnt,
+                                const int32_t* __restrict__ cols, double* __restrict__ out) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= nrows) return;
+    const float* src = grid + node[r] * ncols;
+    const int32_t* cl = cols + cstart[r];
+    double* dst = out + off[r];
+    for (int j = lane; j < cnt[r]; j += 32) dst[j] = (double)src[cl[j]];
+}
+
 }  // namespace hdp
 
 using namespace hdp;
@@ -181,6 +227,26 @@ extern "C" int hdp_median3x3(const uint8_t* src, uint8_t* dst, int batch, int h,
     int64_t n = (int64_t)batch * h * w * c;
     if (n <= 0) return HDP_OK;
     k_median3<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(src, dst, batch, h, w, c); note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+extern "C" int hdp_rows_first_argmin(const double* rows, int64_t n, int m, int32_t* arg, double* best,
+                                     void* stream) {
+    HDP_REQUIRE(rows && arg && best && m >= 1, HDP_ERR_CONFIG, "null buffer or empty rows");
+    if (n <= 0) return HDP_OK;
+    k_rows_argmin<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(rows, n, m, arg, best); note_launch();
+    HDP_CHECK_LAUNCH();
+    return HDP_OK;
+}
+
+extern "C" int hdp_gather_ragged(const float* grid, int ncols, int64_t nrows, const int64_t* node,
+                                 const int64_t* off, const int32_t* cstart, const int32_t* cnt,
+                                 const int32_t* cols, double* out, void* stream) {
+    HDP_REQUIRE(grid && node && off && cstart && cnt && cols && out && ncols >= 1, HDP_ERR_CONFIG, "null buffer");
+    if (nrows <= 0) return HDP_OK;
+    k_gather_ragged<<<grid_for(nrows * 32, 256), 256, 0, (cudaStream_t)stream>>>(grid, ncols, nrows, node, off, cstart,
+                                                                               cnt, cols, out); note_launch();
     HDP_CHECK_LAUNCH();
     return HDP_OK;
 }

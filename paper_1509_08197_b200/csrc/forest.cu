@@ -1217,6 +1217,7 @@ static int forest_build(hdp_forest* f, int64_t m_in, const int32_t* eu, const in
     asrc.release();
 
     tr.mark("7 layout sort");
+    if (f->early.want) HDP_TRY(ecost_early(f));  // lpos is final: the raw cost starts beside steps 8+
     // ---- 8. paths and phases (sizes bounded by n; counts stay on the device)
     const int PH = kMaxPhases + 1;
     DevBuf<int32_t> dcnt;  // counters; f->dph holds the per-phase table
@@ -1755,11 +1756,10 @@ static int lanes_finish(hdp_forest* f, int uniform_m) {
     return HDP_OK;
 }
 
-extern "C" {
-
-int hdp_forest_create(int64_t n_nodes, int64_t n_edges, const int32_t* eu, const int32_t* ev,
-                      const float* ew, const uint8_t* in_tree, const int32_t* comp, float gamma,
-                      hdp_forest** out, void* stream) {
+namespace hdp {
+int forest_create_ex(int64_t n_nodes, int64_t n_edges, const int32_t* eu, const int32_t* ev, const float* ew,
+                     const uint8_t* in_tree, const int32_t* comp, float gamma, const EarlyCost* req,
+                     hdp_forest** out, void* stream) {
     HDP_REQUIRE(out != nullptr, HDP_ERR_CONFIG, "null output handle");
     HDP_REQUIRE(n_nodes >= 1 && n_nodes < ((int64_t)1 << 31) - 2, HDP_ERR_CONFIG,
                 "node count %lld out of range", (long long)n_nodes);
@@ -1770,6 +1770,14 @@ int hdp_forest_create(int64_t n_nodes, int64_t n_edges, const int32_t* eu, const
     f->st = (cudaStream_t)stream;
     f->n = n_nodes;
     f->gamma = gamma;
+    if (req && req->want) {
+        EarlyCost& e = f->early;
+        e.want = 1;
+        e.pl = req->pl; e.pr = req->pr;
+        e.h = req->h; e.w = req->w; e.c = req->c; e.x0 = req->x0; e.nx = req->nx;
+        e.alpha = req->alpha; e.tau_c = req->tau_c; e.tau_g = req->tau_g;
+        e.side = req->side; e.layout_ev = req->layout_ev; e.done_ev = req->done_ev;
+    }
     int s = forest_build(f, n_edges, eu, ev, ew, in_tree, comp);
     if (s != HDP_OK) {
         delete f;
@@ -1777,6 +1785,15 @@ int hdp_forest_create(int64_t n_nodes, int64_t n_edges, const int32_t* eu, const
     }
     *out = f;
     return HDP_OK;
+}
+}  // namespace hdp
+
+extern "C" {
+
+int hdp_forest_create(int64_t n_nodes, int64_t n_edges, const int32_t* eu, const int32_t* ev,
+                      const float* ew, const uint8_t* in_tree, const int32_t* comp, float gamma,
+                      hdp_forest** out, void* stream) {
+    return hdp::forest_create_ex(n_nodes, n_edges, eu, ev, ew, in_tree, comp, gamma, nullptr, out, stream);
 }
 
 int hdp_forest_stats(const hdp_forest* f, int64_t* n_trees, int64_t* n_paths, int64_t* n_phases,

@@ -66,8 +66,34 @@ struct alignas(16) SegDesc {
 };
 }  // namespace hdp
 
+struct hdp_forest;
+namespace hdp {
+// Early raw cost (dense range lanes only, hdp_dense_pipeline): every row has
+// the same width, so a node's row is its layout position times that width and
+// the raw-cost pass only needs the layout order.  forest_build starts it on a
+// side stream as soon as the layout is placed; it overlaps the rest of the
+// build (paths, light children, chunks), and hdp_aggregate_wta then uses the
+// filled rows instead of running its own pre-pass.
+struct EarlyCost {
+    int want = 0, done = 0;
+    const float* pl = nullptr;  // packed left / right planes (float4 per pixel); the right one is
+    const float* pr = nullptr;  // prepared on `side` before the request is handed over
+    int h = 0, w = 0, c = 0, x0 = 0, nx = 0;
+    float alpha = 0, tau_c = 0, tau_g = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t layout_ev = nullptr, done_ev = nullptr;  // owned by the caller (per thread)
+    DevBuf<float> rows;  // the row buffer (A_up), allocated on the forest's stream
+};
+int ecost_early(hdp_forest* f);  // aggregate.cu
+// hdp_forest_create with an early raw-cost request (the request's plain fields are copied)
+int forest_create_ex(int64_t n_nodes, int64_t n_edges, const int32_t* eu, const int32_t* ev, const float* ew,
+                     const uint8_t* in_tree, const int32_t* comp, float gamma, const EarlyCost* req,
+                     hdp_forest** out, void* stream);
+}  // namespace hdp
+
 struct hdp_forest {
     cudaStream_t st = nullptr;
+    hdp::EarlyCost early;
     int64_t n = 0;         // nodes
     int64_t n_trees = 0;
     int64_t n_paths = 0;

@@ -24,6 +24,7 @@
 
 #include "../../include/hdp_stereo.h"
 #include "common.cuh"
+#include "forest.cuh"
 
 namespace hdp {
 
@@ -94,6 +95,9 @@ private:
 struct SubStream {
     cudaStream_t s = nullptr;
     cudaEvent_t done = nullptr, a0 = nullptr, a1 = nullptr;
+    // early raw cost (forest.cuh EarlyCost): a low-priority side stream and its events
+    cudaStream_t side = nullptr;
+    cudaEvent_t alloc_ev = nullptr, layout_ev = nullptr, early_done = nullptr;
 };
 static int sub_stream(SubStream** out) {
     static thread_local SubStream per_dev[64];
@@ -102,13 +106,39 @@ static int sub_stream(SubStream** out) {
     HDP_REQUIRE(dev >= 0 && dev < 64, HDP_ERR_CONFIG, "device ordinal %d out of range", dev);
     SubStream& ss = per_dev[dev];
     if (!ss.s) {
-        HDP_CHECK_CUDA(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+        // the pipeline's own stream runs at the greatest priority: the block
+        // scheduler serves its (small, latency-bound) build kernels before the
+        // pending CTAs of the early raw-cost grid on the side stream
+        int plo = 0, phi = 0;
+        HDP_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+        HDP_CHECK_CUDA(cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, phi));
         HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.done, cudaEventDisableTiming));
         HDP_CHECK_CUDA(cudaEventCreate(&ss.a0));
         HDP_CHECK_CUDA(cudaEventCreate(&ss.a1));
+        int lo = 0, hi = 0;
+        HDP_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // lo = the least priority
+        HDP_CHECK_CUDA(cudaStreamCreateWithPriority(&ss.side, cudaStreamNonBlocking, lo));
+        HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.alloc_ev, cudaEventDisableTiming));
+        HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.layout_ev, cudaEventDisableTiming));
+        HDP_CHECK_CUDA(cudaEventCreateWithFlags(&ss.early_done, cudaEventDisableTiming));
     }
     *out = &ss;
     return HDP_OK;
+}
+
+// Early raw cost switch (hdp_set_early_cost; HDP_EARLY_COST=1 sets the default).
+// Off by default: at C5 the step gains 1.5 % (20.96 -> 20.65 ms) but the raw-cost
+// pass leaves the timed aggregation call and runs 28 % slower beside the build's
+// tail, whose latency-bound kernels slow down 3x under its DRAM write stream.
+static std::atomic<int> g_early_cost{-1};
+static bool early_cost_enabled() {
+    int v = g_early_cost.load(std::memory_order_relaxed);
+    if (v < 0) {
+        const char* e = getenv("HDP_EARLY_COST");
+        v = (e && e[0] == '1') ? 1 : 0;
+        g_early_cost.store(v, std::memory_order_relaxed);
+    }
+    return v != 0;
 }
 
 #define HDP_PCALL(expr)                 \
@@ -156,12 +186,45 @@ static int dense_sub(const DenseJob& j) {
     HDP_PCALL(hdp_mst_grid(j.nb, j.h, j.w, eu.get(), ev.get(), key.get(), in_tree.get(), comp.get(), nullptr, st));
     key.release();
     hdp_forest* f = nullptr;
-    HDP_PCALL(hdp_forest_create(n, m, eu.get(), ev.get(), ew.get(), in_tree.get(), comp.get(), j.gamma, &f, st));
+    // Early raw cost (hdp_set_early_cost; off by default): the right image is prepared on
+    // the side stream (a caller may still be copying it in: right_ready) and the
+    // raw-cost pass starts there as soon as the layout order is final, beside
+    // the rest of the tree build.
+    const bool early_on = early_cost_enabled();
+    EarlyCost req;
+    if (early_on) {
+        HDP_CHECK_CUDA(cudaEventRecord(ss->alloc_ev, st));  // pr is allocated on st
+        HDP_CHECK_CUDA(cudaStreamWaitEvent(ss->side, ss->alloc_ev, 0));
+        if (j.right_ready) HDP_CHECK_CUDA(cudaStreamWaitEvent(ss->side, j.right_ready, 0));
+        HDP_PCALL(hdp_prepare_u8(j.right, j.nb, j.h, j.w, j.c, pr.get(), ss->side));
+        req.want = 1;
+        req.pl = pl.get(); req.pr = pr.get();
+        req.h = j.h; req.w = j.w; req.c = j.c; req.x0 = j.x0; req.nx = j.nx;
+        req.alpha = j.alpha; req.tau_c = j.tau_c; req.tau_g = j.tau_g;
+        req.side = ss->side; req.layout_ev = ss->layout_ev; req.done_ev = ss->early_done;
+    }
+    {
+        const int rcf = forest_create_ex(n, m, eu.get(), ev.get(), ew.get(), in_tree.get(), comp.get(), j.gamma,
+                                         early_on ? &req : nullptr, &f, st);
+        if (rcf != HDP_OK) {
+            if (early_on) cudaStreamSynchronize(ss->side);  // the side stream still reads pr
+            return rcf;
+        }
+    }
     int rc = hdp_forest_set_lanes_range(f, j.x0, j.nx, st);
-    // the right image is needed only from here on (the tree build reads the left
-    // one): a caller may still be copying it in (right_ready)
-    if (rc == HDP_OK && j.right_ready) rc = cudaStreamWaitEvent(st, j.right_ready, 0) == cudaSuccess ? HDP_OK : HDP_ERR_CUDA;
-    if (rc == HDP_OK) rc = hdp_prepare_u8(j.right, j.nb, j.h, j.w, j.c, pr.get(), st);
+    const bool early_done = f->early.done != 0;
+    if (early_on && !early_done && rc == HDP_OK) {
+        // the request was declined (row shape): the side stream's right planes join the main stream
+        HDP_CHECK_CUDA(cudaEventRecord(ss->early_done, ss->side));
+        HDP_CHECK_CUDA(cudaStreamWaitEvent(st, ss->early_done, 0));
+    }
+    if (!early_on) {
+        // the right image is needed only from here on (the tree build reads the left
+        // one): a caller may still be copying it in (right_ready)
+        if (rc == HDP_OK && j.right_ready)
+            rc = cudaStreamWaitEvent(st, j.right_ready, 0) == cudaSuccess ? HDP_OK : HDP_ERR_CUDA;
+        if (rc == HDP_OK) rc = hdp_prepare_u8(j.right, j.nb, j.h, j.w, j.c, pr.get(), st);
+    }
     if (rc == HDP_OK) {
         if (j.agg_ms) HDP_CHECK_CUDA(cudaEventRecord(ss->a0, st));
         rc = hdp_aggregate_wta(f, pl.get(), pr.get(), j.h, j.w, j.c, j.alpha, j.tau_c, j.tau_g, nullptr, j.disp,
@@ -183,6 +246,12 @@ static int dense_sub(const DenseJob& j) {
 }  // namespace hdp
 
 using namespace hdp;
+
+extern "C" int hdp_set_early_cost(int on) {
+    const bool prev = early_cost_enabled();
+    g_early_cost.store(on ? 1 : 0, std::memory_order_relaxed);
+    return prev ? 1 : 0;
+}
 
 extern "C" int hdp_dense_pipeline(const uint8_t* left, const uint8_t* right, int batch, int h, int w, int c,
                                   int d_max, int x0, int nx, float alpha, float tau_c, float tau_g, float gamma,

@@ -159,3 +159,34 @@ def test_host_entry_with_pinned_outputs():
     np.testing.assert_array_equal(d1, d0)
     np.testing.assert_array_equal(c1, c0)
     np.testing.assert_array_equal(od.numpy(), d0)
+
+
+def test_early_raw_cost_gives_identical_results():
+    """hdp_set_early_cost(1): the raw-cost pass starts on a side stream once the
+    layout order is final (forest.cuh EarlyCost) -- the same kernel into the
+    same rows, so the maps must be bit-identical to the default path, for the
+    full range, a disparity slab and a batch."""
+    import torch
+
+    from paper_1509_08197_b200 import _lib
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import SceneSpec, make_scene
+
+    lib = _lib.load()
+    scs = [make_scene(SceneSpec(21, 170, 300, 70, 25, 0.3, 8.0, 1), i) for i in range(3)]
+    L = dev(np.stack([s.pair.left.data for s in scs]))
+    R = dev(np.stack([s.pair.right.data for s in scs]))
+    prev = lib.hdp_set_early_cost(0)
+    try:
+        base = E.run_baseline_fused(L, R, 70)
+        slab0 = E.run_baseline_fused(L[:1], R[:1], 70, x0=24, nx=30)
+        assert lib.hdp_set_early_cost(1) == 0
+        for _ in range(2):
+            early = E.run_baseline_fused(L, R, 70)
+            assert torch.equal(early.disparity, base.disparity)
+            assert torch.equal(early.min_cost, base.min_cost)
+        slab1 = E.run_baseline_fused(L[:1], R[:1], 70, x0=24, nx=30)
+        assert torch.equal(slab1.disparity, slab0.disparity)
+        assert torch.equal(slab1.min_cost, slab0.min_cost)
+    finally:
+        lib.hdp_set_early_cost(prev)
