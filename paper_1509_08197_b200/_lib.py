@@ -106,7 +106,22 @@ def check(status: int) -> None:
     raise _ERRORS.get(status, InternalError)(msg or f"hdp status {status}")
 
 
+# diagnostics: HDP_DIAG_SLOWCALL=<ms> reports every library call whose host time exceeds it
+_SLOW_MS = float(os.environ.get("HDP_DIAG_SLOWCALL", "0") or 0)
+
+
 def call(name: str, *args) -> None:
+    if _SLOW_MS > 0:
+        import sys
+        import time
+
+        t = time.perf_counter()
+        status = getattr(load(), name)(*args)
+        dt = 1e3 * (time.perf_counter() - t)
+        if dt > _SLOW_MS:
+            print(f"[hdp slow call] {name}: {dt:.0f} ms", file=sys.stderr, flush=True)
+        check(status)
+        return
     check(getattr(load(), name)(*args))
 
 
