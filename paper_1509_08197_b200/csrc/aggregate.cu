@@ -85,6 +85,9 @@ struct AggArgs {
     int qgroups;           // 32-float4 column groups of the widest row (segment kernels)
     int qsub, qsub_shift;  // chunk kernels: float4 lanes per path (power of 2 <= 32)
     int uni_mp;            // rowoff == nullptr (early raw cost): row of layout position k = k * uni_mp
+    const uint2* pl8;      // byte records of the two images (k_pack_rec8), or null
+    const uint2* pr8;
+    const int* nonint8;    // != 0: some plane value is not a byte's image; the f32 records are used
 };
 
 __device__ __forceinline__ int lane_disp(const AggArgs& a, int doff, int j) {
@@ -257,11 +260,59 @@ __global__ void __launch_bounds__(256) k_ecost_range(AggArgs a, const int32_t* _
 // compile-time offsets for the U lane blocks, border / padding by selects.
 // Roughly 15 instructions per hypothesis (was ~50: the k_ecost_range loop
 // was issue-bound at 92 % in ncu).
-template <int U>
-__global__ void __launch_bounds__(256) k_ecost_range_u(AggArgs a, const int32_t* __restrict__ lpos, int m) {
-    extern __shared__ float4 win[];
-    __shared__ long long srow[kETile];
-    __shared__ float4 sL[kETile];
+// Byte records (uint8 pairs at full resolution): (channel bytes, f32 gradient)
+// per pixel, 8 bytes instead of the 16-byte f32 record -- the pre-pass is
+// bound by the shared-memory wavefronts of its window reads (ncu: LSU 97 %),
+// which the narrower record halves.  The channel sum of absolute differences
+// is one VABSDIFF4 whose accumulator holds the bits of 2^23: the result reads
+// as the float 2^23 + SAD, exact.  k_pack_rec8 builds the records from the f32
+// planes and raises *nonint8 if any channel is not exactly f32(k / 255).
+struct CostK {
+    float wc, alpha, tc, tg;  // f32 records
+    float omas, tcs;          // byte records: (1 - alpha) / (255 C), tc * 255 C
+    int c;
+};
+__device__ __forceinline__ float rec_cost(const CostK& k, const float4& L, const float4& R) {
+    float color;
+    if (k.c == 3)
+        color = (fabsf(L.x - R.x) + fabsf(L.y - R.y) + fabsf(L.z - R.z)) * (1.0f / 3.0f);
+    else
+        color = fabsf(L.x - R.x);
+    return k.wc * fminf(k.tc, color) + k.alpha * fminf(k.tg, fabsf(L.w - R.w));
+}
+__device__ __forceinline__ float rec_cost(const CostK& k, const uint2& L, const uint2& R) {
+    unsigned r;
+    asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(r) : "r"(L.x), "r"(R.x), "r"(0x4B000000u));
+    const float sad = __uint_as_float(r) - 8388608.0f;
+    const float g = fabsf(__uint_as_float(L.y) - __uint_as_float(R.y));
+    return fmaf(k.alpha, fminf(g, k.tg), k.omas * fminf(sad, k.tcs));
+}
+__device__ __forceinline__ void rec_zero(float4& r) { r = make_float4(0.0f, 0.0f, 0.0f, 0.0f); }
+__device__ __forceinline__ void rec_zero(uint2& r) { r = make_uint2(0u, 0u); }
+
+__global__ void k_pack_rec8(const float4* __restrict__ planes, int64_t n, int c, uint2* __restrict__ out,
+                            int* __restrict__ nonint) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = __ldg(planes + i);
+    const float v[3] = {p.x, p.y, p.z};
+    unsigned pk = 0;
+    bool bad = false;
+    for (int k = 0; k < c; k++) {
+        const float r = rintf(v[k] * 255.0f);
+        // exactly the f32 image of a byte: the planes hold f32(u8 / 255) (image.cu k_prepare*)
+        const bool ok = r >= 0.0f && r <= 255.0f && (float)((double)r / 255.0) == v[k];
+        bad = bad || !ok;
+        pk |= (unsigned)(ok ? (int)r : 0) << (8 * k);
+    }
+    out[i] = make_uint2(pk, __float_as_uint(p.w));
+    if (bad) *nonint = 1;
+}
+
+template <int U, typename Rec>
+__device__ __forceinline__ void ecost_range_body(const AggArgs& a, const int32_t* __restrict__ lpos, int m,
+                                                 const Rec* __restrict__ pl, const Rec* __restrict__ pr, Rec* win,
+                                                 Rec* sL, long long* srow, const CostK& ck) {
     const int64_t base = (int64_t)blockIdx.x * a.w;  // node id of column 0 of this image row
     const int c0 = (int)blockIdx.y * kETile;
     const int mp = (m + 3) & ~3;
@@ -271,15 +322,17 @@ __global__ void __launch_bounds__(256) k_ecost_range_u(AggArgs a, const int32_t*
     const int nwin = hi - v0;
     for (int i = threadIdx.x; i < nwin; i += 256) {
         const int x = v0 + i;
-        win[i] = x >= 0 ? __ldg(a.pr + base + x) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        Rec r;
+        rec_zero(r);
+        if (x >= 0) r = __ldg(pr + base + x);
+        win[i] = r;
     }
     for (int i = threadIdx.x; i < nt; i += 256) {
         const int32_t k = __ldg(lpos + base + c0 + i);
         srow[i] = a.rowoff ? __ldg(a.rowoff + k) : (long long)k * a.uni_mp;
-        sL[i] = __ldg(a.pl + base + c0 + i);
+        sL[i] = __ldg(pl + base + c0 + i);
     }
     __syncthreads();
-    const float wc = 1.0f - a.alpha;
     const float border = a.border;
     const int lane = threadIdx.x & 31;
     // blocks 0 .. U-2 are full (32 (U-1) < mp) and hold no padding lanes
@@ -287,30 +340,50 @@ __global__ void __launch_bounds__(256) k_ecost_range_u(AggArgs a, const int32_t*
     // only the last block needs the row-end guard and the padding select
     const int jl = lane + 32 * (U - 1);
     for (int q = threadIdx.x >> 5; q < nt; q += 8) {
-        const float4 L = sL[q];
+        const Rec L = sL[q];
         float* out = a.aup + srow[q] + lane;
         const int xl = c0 + q - a.range_x0;  // lanes j > xl reach left of the image
-        const float4* wp = win + (q + mp - 1 - lane);
+        const Rec* wp = win + (q + mp - 1 - lane);
         if (xl >= mp - 1) {  // warp-uniform: no lane reaches the border
 #pragma unroll
-            for (int u = 0; u < U - 1; u++) out[32 * u] = pix_cost(a, wc, L, wp[-32 * u]);
+            for (int u = 0; u < U - 1; u++) out[32 * u] = rec_cost(ck, L, wp[-32 * u]);
             if (jl < mp) {
-                const float e = pix_cost(a, wc, L, wp[-32 * (U - 1)]);
+                const float e = rec_cost(ck, L, wp[-32 * (U - 1)]);
                 out[32 * (U - 1)] = jl >= m ? kPadCost : e;
             }
         } else {
 #pragma unroll
             for (int u = 0; u < U - 1; u++) {
-                const float e = pix_cost(a, wc, L, wp[-32 * u]);
+                const float e = rec_cost(ck, L, wp[-32 * u]);
                 out[32 * u] = lane + 32 * u > xl ? border : e;
             }
             if (jl < mp) {
-                float e = pix_cost(a, wc, L, wp[-32 * (U - 1)]);
+                float e = rec_cost(ck, L, wp[-32 * (U - 1)]);
                 e = jl > xl ? border : e;
                 out[32 * (U - 1)] = jl >= m ? kPadCost : e;
             }
         }
     }
+}
+
+template <int U>
+__global__ void __launch_bounds__(256) k_ecost_range_u(AggArgs a, const int32_t* __restrict__ lpos, int m) {
+    extern __shared__ float4 win[];
+    __shared__ long long srow[kETile];
+    __shared__ float4 sL[kETile];
+    CostK ck;
+    ck.wc = 1.0f - a.alpha;
+    ck.alpha = a.alpha;
+    ck.tc = a.tc;
+    ck.tg = a.tg;
+    ck.c = a.c;
+    ck.omas = (1.0f - a.alpha) / (255.0f * (float)a.c);
+    ck.tcs = a.tc * 255.0f * (float)a.c;
+    if (a.pl8 != nullptr && __ldg(a.nonint8) == 0)  // uniform over the grid
+        ecost_range_body<U, uint2>(a, lpos, m, a.pl8, a.pr8, reinterpret_cast<uint2*>(win),
+                                   reinterpret_cast<uint2*>(sL), srow, ck);
+    else
+        ecost_range_body<U, float4>(a, lpos, m, a.pl, a.pr, win, sL, srow, ck);
 }
 
 // RANGE: lane j is disparity range_x0 + j (dense / slab lanes); otherwise the
@@ -1705,6 +1778,26 @@ struct PhaseClock {
     }
 };
 
+constexpr int kByteRecMinRow = 128;  // padded row width (floats) from which byte records are used
+
+// Byte records for the range-lane raw cost (k_pack_rec8): both images' records in
+// `buf` (2 n uint2), the exactness flag in `flag`; fills a.pl8 / a.pr8 / a.nonint8.
+static int pack_byte_records(AggArgs& a, int64_t n, DevBuf<uint2>& buf, DevBuf<int>& flag, cudaStream_t st) {
+    static const bool on = env_int("HDP_COST_U8", 1) != 0;  // diagnostics: 0 = always the f32 records
+    a.pl8 = a.pr8 = nullptr;
+    a.nonint8 = nullptr;
+    if (!on) return HDP_OK;
+    HDP_TRY(buf.alloc(2 * n, st));
+    HDP_TRY(flag.alloc(1, st));
+    HDP_CHECK_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
+    k_pack_rec8<<<grid_for(n, 256), 256, 0, st>>>(a.pl, n, a.c, buf.get(), flag.get()); note_launch();
+    k_pack_rec8<<<grid_for(n, 256), 256, 0, st>>>(a.pr, n, a.c, buf.get() + n, flag.get()); note_launch();
+    a.pl8 = buf.get();
+    a.pr8 = buf.get() + n;
+    a.nonint8 = flag.get();
+    return HDP_OK;
+}
+
 // Early raw cost of the dense pipeline (forest.cuh EarlyCost): called by
 // forest_build once the layout order is final.  Rows are uniform (range
 // lanes), so a node's row is its layout position times the padded width.
@@ -1718,6 +1811,11 @@ int hdp::ecost_early(hdp_forest* f) {
         return HDP_OK;
     }
     HDP_TRY(e.rows.alloc(f->n * (int64_t)mp + 32, st));
+    if (env_int("HDP_COST_U8", 1) != 0 && mp >= kByteRecMinRow) {
+        HDP_TRY(e.rec8.alloc(2 * f->n, st));
+        HDP_TRY(e.flag8.alloc(1, st));
+        HDP_CHECK_CUDA(cudaMemsetAsync(e.flag8.get(), 0, sizeof(int), st));
+    }
     HDP_CHECK_CUDA(cudaEventRecord(e.layout_ev, st));
     HDP_CHECK_CUDA(cudaStreamWaitEvent(e.side, e.layout_ev, 0));
     AggArgs a = {};
@@ -1734,6 +1832,16 @@ int hdp::ecost_early(hdp_forest* f) {
     a.aup = e.rows.get();
     a.rowoff = nullptr;
     a.uni_mp = mp;
+    a.pl8 = a.pr8 = nullptr;
+    a.nonint8 = nullptr;
+    if (e.flag8.get()) {  // byte records (allocated above on the forest's stream), packed on the side stream
+        k_pack_rec8<<<grid_for(f->n, 256), 256, 0, e.side>>>(a.pl, f->n, a.c, e.rec8.get(), e.flag8.get()); note_launch();
+        k_pack_rec8<<<grid_for(f->n, 256), 256, 0, e.side>>>(a.pr, f->n, a.c, e.rec8.get() + f->n, e.flag8.get());
+        note_launch();
+        a.pl8 = e.rec8.get();
+        a.pr8 = e.rec8.get() + f->n;
+        a.nonint8 = e.flag8.get();
+    }
     dim3 g((unsigned)(f->n / e.w), (unsigned)((e.w + kETile - 1) / kETile));
     // shared-memory padding caps the grid's CTAs per SM (HDP_EARLY_SMEM_KB): the
     // build's latency-bound kernels beside it suffer less from a DRAM queue
@@ -1837,6 +1945,10 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
     }
     PhaseClock pc(st);  // HDP_AGG_TRACE=1: per-stage device times on stderr
     DevBuf<float> aup;
+    DevBuf<uint2> rec8;
+    DevBuf<int> flag8;
+    a.pl8 = a.pr8 = nullptr;
+    a.nonint8 = nullptr;
     DevBuf<unsigned long long> carry;
     DevBuf<int> tickets;
     // the dense pipeline's early raw cost (forest.cuh EarlyCost): the rows are
@@ -1928,6 +2040,9 @@ extern "C" int hdp_aggregate_wta(hdp_forest* f, const float* packed_l, const flo
             bool done = false;
             if (usmem <= 48 * 1024 && U <= 17) {
                 done = true;
+                // byte records pay for their pack pass when the rows are wide (C5:
+                // pre-pass 2.49 -> 2.18 ms + 0.07 ms of packing; C2's 84-lane rows: a loss)
+                if (mp >= kByteRecMinRow) HDP_TRY(pack_byte_records(a, f->n, rec8, flag8, st));
                 switch (U) {
 #define HDP_ECU(n) case n: k_ecost_range_u<n><<<g, 256, usmem, st>>>(a, f->lpos.get(), m); break;
                     HDP_ECU(1) HDP_ECU(2) HDP_ECU(3) HDP_ECU(4) HDP_ECU(5) HDP_ECU(6) HDP_ECU(7) HDP_ECU(8)

@@ -83,6 +83,8 @@ struct EarlyCost {
     cudaStream_t side = nullptr;
     cudaEvent_t layout_ev = nullptr, done_ev = nullptr;  // owned by the caller (per thread)
     DevBuf<float> rows;  // the row buffer (A_up), allocated on the forest's stream
+    DevBuf<uint2> rec8;  // byte records of the two images (aggregate.cu k_pack_rec8)
+    DevBuf<int> flag8;
 };
 int ecost_early(hdp_forest* f);  // aggregate.cu
 // hdp_forest_create with an early raw-cost request (the request's plain fields are copied)
