@@ -173,20 +173,41 @@ def test_early_raw_cost_gives_identical_results():
     from paper_1509_08197_b200.synthetic import SceneSpec, make_scene
 
     lib = _lib.load()
-    scs = [make_scene(SceneSpec(21, 170, 300, 70, 25, 0.3, 8.0, 1), i) for i in range(3)]
+    scs = [make_scene(SceneSpec(21, 170, 300, 140, 25, 0.3, 8.0, 1), i) for i in range(3)]  # rows of 144 floats: byte records
     L = dev(np.stack([s.pair.left.data for s in scs]))
     R = dev(np.stack([s.pair.right.data for s in scs]))
     prev = lib.hdp_set_early_cost(0)
     try:
-        base = E.run_baseline_fused(L, R, 70)
-        slab0 = E.run_baseline_fused(L[:1], R[:1], 70, x0=24, nx=30)
+        base = E.run_baseline_fused(L, R, 140)
+        slab0 = E.run_baseline_fused(L[:1], R[:1], 140, x0=24, nx=30)
         assert lib.hdp_set_early_cost(1) == 0
         for _ in range(2):
-            early = E.run_baseline_fused(L, R, 70)
+            early = E.run_baseline_fused(L, R, 140)
             assert torch.equal(early.disparity, base.disparity)
             assert torch.equal(early.min_cost, base.min_cost)
-        slab1 = E.run_baseline_fused(L[:1], R[:1], 70, x0=24, nx=30)
+        slab1 = E.run_baseline_fused(L[:1], R[:1], 140, x0=24, nx=30)
         assert torch.equal(slab1.disparity, slab0.disparity)
         assert torch.equal(slab1.min_cost, slab0.min_cost)
     finally:
         lib.hdp_set_early_cost(prev)
+
+
+def test_byte_record_raw_cost_matches_oracle_and_f32_records():
+    """Wide range-lane rows take the raw cost from 8-byte records (channel bytes
+    + f32 gradient, aggregate.cu k_pack_rec8 / VABSDIFF4): parity with the
+    oracle under the usual rule, and the gray (one-channel) variant too."""
+    from oracle import oracle as O
+    from paper_1509_08197_b200 import engine as E
+    from paper_1509_08197_b200.synthetic import SceneSpec, make_scene
+
+    sc = make_scene(SceneSpec(22, 60, 200, 150, 12, 0.3, 8.0, 1), 0)
+    for gray in (False, True):
+        Lh, Rh = sc.pair.left.data, sc.pair.right.data
+        if gray:
+            Lh = np.ascontiguousarray(Lh[:, :, :1])
+            Rh = np.ascontiguousarray(Rh[:, :, :1])
+        got = E.run_baseline_fused(dev(Lh[None]), dev(Rh[None]), 150)
+        ref = O.run_baseline(Lh, Rh, 150)
+        assert_disp_parity(got.disparity[0].cpu().numpy(), ref.disparity, ref.min_cost, ref.second_cost,
+                           f"byte records gray={gray}")
+        assert_cost_parity(got.min_cost[0].cpu().numpy(), ref.min_cost, f"byte records gray={gray}")
