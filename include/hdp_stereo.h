@@ -307,6 +307,12 @@ int hdp_occlusion_from_gt(const int32_t *gt_left, const int32_t *gt_right, const
                           void *stream);
 
 /* --------------------------------------------------------- whole pipeline */
+/* Grow the library's stream-ordered memory pool to `bytes` once (one block
+ * allocated and freed; the pool keeps its memory): later scratch allocations
+ * up to that size never wait for the driver to map new physical memory in the
+ * middle of a step.  Synchronises the stream. */
+int hdp_pool_reserve(int64_t bytes, void *stream);
+
 /* hdp_dense_pipeline option: start the raw-cost pass on a side stream as soon
  * as the tree's layout order is final, beside the rest of the build (dense
  * range lanes have uniform rows, so a node's row is known from its layout

@@ -70,6 +70,7 @@ SIGNATURES = {
     "hdp_rows_first_argmin": (_I, [_P, _I64, _I, _P, _P, _P]),
     "hdp_gather_ragged": (_I, [_P, _I, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "hdp_set_early_cost": (_I, [_I]),
+    "hdp_pool_reserve": (_I, [_I64, _P]),
     "hdp_dense_pipeline": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _F, _F, _F, _I, _P, _P, _P, _P, _P, _P]),
 }
 

@@ -35,6 +35,21 @@ void keep_pool_memory() {
     done_dev = dev;
 }
 
+}  // namespace hdp
+// Grow the stream-ordered pool once to `bytes` (allocate and free one block):
+// the pool keeps what it has (keep_pool_memory), so later allocations up to
+// that size are carved from memory the process already owns instead of going
+// to the driver for new physical memory in the middle of a step.
+extern "C" int hdp_pool_reserve(int64_t bytes, void* stream) {
+    hdp::keep_pool_memory();
+    if (bytes <= 0) return HDP_OK;
+    void* p = nullptr;
+    HDP_CHECK_CUDA(cudaMallocAsync(&p, (size_t)bytes, (cudaStream_t)stream));
+    HDP_CHECK_CUDA(cudaFreeAsync(p, (cudaStream_t)stream));
+    HDP_CHECK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return HDP_OK;
+}
+namespace hdp {
 static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }

@@ -606,6 +606,53 @@ def _aggregate_timed(f: DeviceForest, lev: Level, cost, clock=None, probe=None, 
     return out
 
 
+
+# ---- scratch pool sizing
+# The library's scratch comes from the stream-ordered CUDA pool.  A pool that
+# grows piecemeal goes back to the driver for physical memory in the middle of
+# steps whenever the streams' interleaving asks for a block it cannot carve from
+# what it holds (C4 at 64 pairs: one step in ten took 0.5-2 s instead of 0.35 s).
+# Sizing it once for the workload (one block allocated and freed,
+# hdp_pool_reserve; the pool keeps its memory) removes those stalls: every
+# later allocation is carved from memory the process already owns.
+# HDP_POOL_RESERVE=0 disables; HDP_POOL_RESERVE_GB=<n> fixes the size.
+_POOL_RESERVED: dict = {}
+_POOL_ON = os.environ.get("HDP_POOL_RESERVE", "1") != "0"
+_POOL_FIXED_GB = float(os.environ.get("HDP_POOL_RESERVE_GB", "0") or 0)
+
+
+def reserve_pool(nbytes: int) -> None:
+    """Grow the scratch pool of the current device to at least `nbytes` (once
+    per size: a later, smaller request is a no-op)."""
+    if not _POOL_ON:
+        return
+    torch = _t()
+    dev = torch.cuda.current_device()
+    if _POOL_FIXED_GB > 0:
+        nbytes = int(_POOL_FIXED_GB * 2**30)
+    have = _POOL_RESERVED.get(dev, 0)
+    if nbytes <= have:
+        return
+    free, _total = torch.cuda.mem_get_info(dev)
+    nbytes = int(min(nbytes, 0.6 * (free + have)))  # never more than 60 % of what is available
+    if nbytes <= have:
+        return
+    L.call("hdp_pool_reserve", int(nbytes), L.stream())
+    _POOL_RESERVED[dev] = nbytes
+
+
+def _dense_scratch_bytes(b, h, w, lanes):
+    """Upper estimate of the dense pipeline's scratch: the row buffer (4 bytes
+    per hypothesis, rows padded to 4 lanes), keys / records / planes and the
+    forest's tables (~450 bytes per pixel measured at C5 and C2)."""
+    return int(b * h * w * (4 * ((lanes + 3) & ~3) + 600))
+
+
+def _hdp_scratch_bytes(b, h, w):
+    """Upper estimate of the HDP level loop's scratch (measured: 197 bytes per
+    pixel at C4 with 64 pairs, the prior's record sets included) x 2."""
+    return int(b * h * w * 400)
+
 # sub-batches of the one-call dense pipeline (hdp_dense_pipeline): the tree
 # build of one overlaps the aggregation of another
 DENSE_SUB_BATCHES = int(os.environ.get("HDP_DENSE_SUB", "1"))
@@ -625,6 +672,7 @@ def run_baseline_fused(left_u8, right_u8, d_max: int, gamma: float = 0.1,
         raise ConfigError(f"d_max must be >= 1, got {d_max}")
     b, h, w, c = left_u8.shape
     nx = d_max + 1 if nx is None else nx
+    reserve_pool(_dense_scratch_bytes(b, h, w, nx))
     n_sub = DENSE_SUB_BATCHES if n_sub is None else n_sub
     n_sub = max(1, min(n_sub, b))
     dev = left_u8.device
@@ -701,6 +749,7 @@ def run_baseline_batch(left_u8, right_u8, d_max: int, gamma: float = 0.1,
         return run_baseline_fused(left_u8, right_u8, d_max, gamma, cost, x0, nx, timing=timing)
     clock = _Clock(timing)
     b, h, w, c = left_u8.shape
+    reserve_pool(_dense_scratch_bytes(b, h, w, d_max + 1 if nx is None else nx) + b * h * w * 200)
     il, ir = to_f64(left_u8), to_f64(right_u8)
     _, _, _, pl = prepare(il, False)
     _, _, _, pr = prepare(ir, False)
@@ -747,6 +796,7 @@ def run_hdp_batch(left_u8, right_u8, d_max: int, model, levels: int = 3, block_s
     # they run on a side stream from the start, beside the coarser levels'
     # tree builds (HDPF keeps one SM per pair busy), while the level loop
     # runs on a high-priority stream so the block scheduler serves it first.
+    reserve_pool(_hdp_scratch_bytes(left_u8.shape[0], left_u8.shape[1], left_u8.shape[2]))
     caller = torch.cuda.current_stream()
     pri, hi = _hdp_streams()
     pri.wait_stream(caller)

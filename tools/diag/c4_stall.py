@@ -16,6 +16,9 @@ L = torch.from_numpy(np.stack([s.pair.left.data for s in scenes])).cuda()
 R = torch.from_numpy(np.stack([s.pair.right.data for s in scenes])).cuda()
 model = GmmModel.parse(bench.load_model_text())
 pre = SIZE_CLASS_PRESETS[wl["size_class"]]
+if os.environ.get("C4_RESERVE_GB"):
+    from paper_1509_08197_b200 import _lib
+    _lib.call("hdp_pool_reserve", int(float(os.environ["C4_RESERVE_GB"]) * 2**30), _lib.stream())
 rows = []
 for r in range(reps):
     torch.cuda.synchronize()

@@ -23,6 +23,8 @@ def val(r, col):
 
 names = [r[h.index("Kernel Name")] for r in data]
 start = next(i for i, n in enumerate(names) if "k_ecost" in n)
+while start > 0 and "k_pack_rec8" in names[start - 1]:  # the byte-record pack passes belong to the call
+    start -= 1
 end = next(i for i in range(start, len(names)) if "k_keys_finish" in names[i])
 call = data[start:end + 1]
 tot_b = tot_t = 0.0

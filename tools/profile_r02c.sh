@@ -8,11 +8,11 @@ python bench.py --steps 2 --warmup 3 --legs none --no-cpu-baseline > gpurun_out/
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02c_launches_bench_c5.csv \
     python bench.py --steps 2 --warmup 3 --legs none --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 python tools/trace_full.py 5 2 > gpurun_out/plain_c5.log 2>&1 && \
-ncu --set full --clock-control none -k regex:'k_ecost|k_up_chunk|k_down_chunk|k_seg_up|k_seg_down|k_keys_finish' \
+ncu --set full --clock-control none -k regex:'k_pack_rec8|k_ecost|k_up_chunk|k_down_chunk|k_seg_up|k_seg_down|k_keys_finish' \
     -c 200 -o /tmp/agg_c5 -f python tools/trace_full.py 5 2 > gpurun_out/ncu_c5.log 2>&1
 ncu -i /tmp/agg_c5.ncu-rep --page raw --csv > gpurun_out/r02c_agg_c5_raw.csv 2>&1
 python tools/trace_full.py 2 2 > gpurun_out/plain_c2.log 2>&1 && \
-ncu --set full --clock-control none -k regex:'k_ecost|k_up_chunk|k_down_chunk|k_seg_up|k_seg_down|k_keys_finish' \
+ncu --set full --clock-control none -k regex:'k_pack_rec8|k_ecost|k_up_chunk|k_down_chunk|k_seg_up|k_seg_down|k_keys_finish' \
     -c 200 -o /tmp/agg_c2 -f python tools/trace_full.py 2 2 > gpurun_out/ncu_c2.log 2>&1
 ncu -i /tmp/agg_c2.ncu-rep --page raw --csv > gpurun_out/r02c_agg_c2_raw.csv 2>&1
 for lv in 0 1; do
